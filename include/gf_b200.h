@@ -1,0 +1,175 @@
+/*
+ * gf_b200.h -- C-ABI of the B200-native DEM step (libgf_b200.so).
+ *
+ * Plain pointers and sizes only; the caller owns every host buffer, the
+ * context owns every device buffer.  All array layouts are the reference's
+ * numpy layouts (row-major; int64 ids; float32 radii / quaternions / geometry
+ * parameters / contact history; float64 state), so a host that holds
+ * grainforge.StateStore arrays can pass them through unchanged.
+ *
+ * Return codes: 0 = ok, < 0 = CUDA/usage error (text via gf_last_error).
+ *
+ * Reference interfaces each entry point replaces (file:line under
+ * /root/reference/pkg/src/grainforge/):
+ *   gf_upload_owners / gf_download_owners  StateStore SoA (core.py:356-390)
+ *   gf_upload_geometry                     geometry slots (engine.py:444-458)
+ *   gf_upload_materials                    material_pair_stack (forces.py:443-460)
+ *   gf_upload_families                     family tables (engine.py:264-271, core.py:291-305)
+ *   gf_detect / gf_detect_snapshot         broadphase.detect_contacts (broadphase.py:202-288)
+ *   gf_bin_ranges                          _kernels.bin_ranges (_kernels.py:252-266)
+ *   gf_merge_history                       broadphase.merge_history (broadphase.py:110-135)
+ *   gf_adopt                               merge_history + _install_acs (broadphase.py:110-135,
+ *                                          engine.py:606-665)
+ *   gf_dt_step                             _step_once force/reduce/integrate chain
+ *                                          (engine.py:796-843; forces.py:553-591;
+ *                                          _kernels.py:516-545, 641-670)
+ *   gf_run                                 the kT/dT worker protocol of do_dynamics
+ *                                          (engine.py:512-526, 669-906)
+ */
+#ifndef GF_B200_H
+#define GF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gf_ctx gf_ctx;
+
+/* flags for gf_create */
+#define GF_STATE_F32 1u /* store owner velocities as float32 (throughput build) */
+
+gf_ctx *gf_create(int device, uint32_t flags);
+void gf_destroy(gf_ctx *ctx);
+/* copies the last error message into buf (always NUL-terminated) */
+int gf_last_error(gf_ctx *ctx, char *buf, size_t n);
+/* 1 when the library and a CUDA device are usable */
+int gf_device_count(void);
+
+/* ---- scene --------------------------------------------------------------- */
+int gf_set_domain(gf_ctx *ctx, const double *lo3, const double *hi3, double voxel_edge);
+
+/* n owners; sub is (n,3) uint16, quat (n,4) float32 (w,x,y,z), velocities
+ * (n,3) float64 (ang_vel in the owner frame), family (n) uint8, tpl (n)
+ * uint32 index into n_tpl mass-property rows: tpl_mass (n_tpl),
+ * tpl_moi (n_tpl,3). */
+int gf_upload_owners(gf_ctx *ctx, int64_t n, const uint64_t *voxel, const uint16_t *sub,
+                     const float *quat, const double *lin_vel, const double *ang_vel,
+                     const uint8_t *family, const uint32_t *tpl, int64_t n_tpl,
+                     const double *tpl_mass, const double *tpl_moi);
+/* any pointer may be NULL to skip that field */
+int gf_download_owners(gf_ctx *ctx, uint64_t *voxel, uint16_t *sub, float *quat,
+                       double *lin_vel, double *ang_vel, uint8_t *family);
+int gf_set_owner_families(gf_ctx *ctx, const uint8_t *family);
+/* external loads (n,3) float64 each; both NULL clears them */
+int gf_set_external_loads(gf_ctx *ctx, const double *force, const double *torque);
+/* per-owner contact force/torque of the last stepped step (n,3) each */
+int gf_download_accumulators(gf_ctx *ctx, double *acc_force, double *acc_torque);
+
+/* spheres: owner (n_s) int64, params (n_s,4) float32 = offset xyz + radius,
+ * material (n_s) uint8.  triangles: owner, local (n_t,9) float32, material.
+ * analytics: owner, kind (2 plane / 3 cylinder), local (n_a,8) float32,
+ * material.  Slots are the order given (ascending geometry id). */
+int gf_upload_geometry(gf_ctx *ctx, int64_t n_s, const int64_t *sph_owner,
+                       const float *sph_params, const uint8_t *sph_mat, int64_t n_t,
+                       const int64_t *tri_owner, const float *tri_local, const uint8_t *tri_mat,
+                       int64_t n_a, const int64_t *ana_owner, const uint8_t *ana_kind,
+                       const float *ana_local, const uint8_t *ana_mat);
+
+/* pair stack (n_rows, n_mat, n_mat) float64: E_cnt, G_cnt, CoR, mu, Crr; beta
+ * (n_mat, n_mat) restitution damping computed on the host (forces.py:41-44). */
+int gf_upload_materials(gf_ctx *ctx, int n_mat, int n_rows, const double *pair_stack,
+                        const double *beta);
+
+/* mask (256,256) uint8; flags (256) bit0 fixed, bit1 prescribed; lv_mask /
+ * av_mask (256) bit ax set when that component is prescribed; values (256,3). */
+int gf_upload_families(gf_ctx *ctx, const uint8_t *mask, const uint8_t *flags,
+                       const uint8_t *lv_mask, const uint8_t *av_mask, const double *lv_val,
+                       const double *av_val);
+
+/* world geometry derived from the current state; NULL skips a field */
+int gf_download_world(gf_ctx *ctx, double *sph_centers, double *tri_world, double *ana_world);
+
+/* ---- contact arrays ------------------------------------------------------- */
+/* install an ACS (canonical order) with its (n, W) float32 history */
+int gf_set_acs(gf_ctx *ctx, int64_t n, const uint8_t *kind, const int64_t *slot_a,
+               const int64_t *slot_b, const float *wild, int W);
+int64_t gf_acs_size(gf_ctx *ctx, int which /* 0 = active, 1 = last detected */);
+int gf_get_acs(gf_ctx *ctx, int which, uint8_t *kind, int64_t *slot_a, int64_t *slot_b,
+               float *wild);
+
+/* ---- kT ------------------------------------------------------------------- */
+/* detect on the current state into the "next" array; returns its size */
+int gf_detect(gf_ctx *ctx, double margin, int64_t *n_out);
+/* detect on an explicit snapshot (broadphase.DetectionSnapshot fields);
+ * grid_out = glo xyz + inv_bin, nb_out = bins per axis (may be NULL) */
+int gf_detect_snapshot(gf_ctx *ctx, int64_t m, const double *centers, const float *radii,
+                       const int64_t *sph_owner, const uint8_t *sph_family, int64_t n_t,
+                       const double *tri_world, const int64_t *tri_owner,
+                       const uint8_t *tri_family, int64_t n_a, const double *ana_world,
+                       const uint8_t *ana_kind, const int64_t *ana_owner,
+                       const uint8_t *ana_family, const uint8_t *mask, double margin,
+                       double bin_size /* <= 0: 2 (r_max + margin) */, double *grid_out,
+                       int64_t *nb_out, int64_t *n_out);
+/* per-sphere inclusive bin ranges (n_s,6) int64 of the last detection's grid */
+int gf_bin_ranges(gf_ctx *ctx, double margin, int64_t *out);
+/* history remap between two canonical arrays of (kind, geometry a, b) given as
+ * host buffers; out_wild (n_new, W) receives matched rows, zeros otherwise */
+int gf_merge_history(gf_ctx *ctx, int64_t n_old, const uint8_t *old_kind, const int64_t *old_a,
+                     const int64_t *old_b, const float *old_wild, int64_t n_new,
+                     const uint8_t *new_kind, const int64_t *new_a, const int64_t *new_b, int W,
+                     float *out_wild);
+/* adopt the last detection: history remap + incidence lists */
+int gf_adopt(gf_ctx *ctx);
+
+/* ---- dT ------------------------------------------------------------------- */
+typedef struct {
+  double h;
+  double g[3];
+  double v_err;
+  double sim_time;
+  int64_t step;
+  int32_t write_acc;
+  int32_t pad;
+} gf_step_params;
+
+/* one dT step (force -> reduce -> integrate -> refresh) on the active ACS;
+ * returns the touching count and the watchdog owners (-1 = ok) */
+int gf_dt_step(gf_ctx *ctx, const gf_step_params *p, int64_t *touching, int64_t *bad,
+               int64_t *oob);
+
+/* ---- the whole worker protocol -------------------------------------------- */
+typedef struct {
+  int64_t n_steps;
+  int64_t step0;        /* global step index of the first step */
+  double h;
+  double g[3];
+  double v_err;
+  double margin;        /* detection margin (engine._current_margin) */
+  int32_t period;       /* snapshot every `period` steps */
+  int32_t lag;          /* adopt `lag` steps after the snapshot (0 = sync) */
+  int32_t n_dyn;        /* dynamic prescription entries */
+  int32_t write_acc;    /* store accumulators on the final step */
+  const int32_t *dyn_spec;   /* (n_dyn, 3): family, table (0 lin / 1 ang), axis */
+  const double *dyn_vals;    /* (n_steps, n_dyn) values at each step's start time */
+} gf_run_params;
+
+typedef struct {
+  int64_t steps_done;
+  int64_t bad_owner, bad_step;
+  int64_t oob_owner, oob_step;
+  int64_t touching;     /* last step */
+  int64_t n_acs;
+  int64_t ca_updates;
+  double dt_ms, kt_ms;  /* device time of the dT and kT streams */
+  double wall_ms;
+} gf_run_result;
+
+int gf_run(gf_ctx *ctx, const gf_run_params *p, gf_run_result *r);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GF_B200_H */

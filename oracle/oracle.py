@@ -293,10 +293,12 @@ class OracleStepper:
       ext_force, ext_torque, geom_owner, geom_kind, geom_material,
       geom_params, lo, hi, edge, pair_stack, mask, fixed_flag,
       prescribed_flag, lv_mask, lv_val, av_mask, av_val, gravity, h, v_err.
-    Schedule: a snapshot is taken at the start of every step s with
-    s % period == 0 and the contact array built from it is adopted at the
-    start of step s + lag (lag=0, period=1 is the reference's sync mode,
-    engine.py:726-741).
+    Schedule (the B200 scheduler's, csrc/gf_context.cu gf_run): the first
+    detection is adopted immediately; afterwards, once no detection is in
+    flight and `period` steps passed since the last snapshot, a snapshot is
+    taken at the start of step s and adopted at the start of step s + lag
+    (adoption precedes the next snapshot check).  lag=0, period=1 is the
+    reference's sync mode (engine.py:726-741).
     """
 
     def __init__(self, scene: dict, margin: float, period: int = 1, lag: int = 0,
@@ -336,7 +338,9 @@ class OracleStepper:
         self.acs = dict(kind=np.zeros(0, np.uint8), geom_a=np.zeros(0, np.int64),
                         geom_b=np.zeros(0, np.int64))
         self.wild = np.zeros((0, 4), np.float32)
-        self.pending = []  # (adopt_step, acs)
+        self.pending = []  # (adopt_step, acs); at most one in flight
+        self.first = True
+        self.last_snap = 0
         self.dyn_prescriptions = []  # (family, table_name, axis, fn(t))
 
     def snapshot(self):
@@ -361,8 +365,14 @@ class OracleStepper:
 
     def step_once(self):
         s = self.s
-        if self.step % self.period == 0:
-            self.pending.append((self.step + self.lag, detect_contacts(self.snapshot(), self.margin)))
+        while self.pending and self.pending[0][0] <= self.step:
+            self.adopt(self.pending.pop(0)[1])
+        if self.first or (not self.pending and self.step - self.last_snap >= self.period):
+            # the first detection is waited for (engine.py:679-682)
+            adopt_at = self.step if self.first else self.step + self.lag
+            self.pending.append((adopt_at, detect_contacts(self.snapshot(), self.margin)))
+            self.last_snap = self.step
+            self.first = False
         while self.pending and self.pending[0][0] <= self.step:
             self.adopt(self.pending.pop(0)[1])
         acs = self.acs

@@ -1,0 +1,265 @@
+// gf_common.cuh -- device-side data model and exact-arithmetic helpers shared
+// by the kT (contact detection) and dT (force / reduce / integrate) kernels.
+//
+// Exactness: the kT translation unit and the fp64 "parity" dT unit are built
+// with -fmad=false, so every helper below rounds each fp64 operation
+// separately in the reference's statement order (numba fastmath=False,
+// /root/reference/pkg/src/grainforge/_kernels.py:17).  Only log() is avoided
+// on the device: restitution damping beta comes from a host table computed
+// with the same libm the reference uses (forces.py:41-44).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace gf {
+
+constexpr int kVoxBits = 21;                       // types.py:28
+constexpr int64_t kVoxPerAxis = int64_t(1) << kVoxBits;
+constexpr int kSubPerEdge = 65536;                 // types.py:31
+constexpr double kFlatRadius = 1.0e18;             // _kernels.py:25
+constexpr double kPi = 3.141592653589793;
+constexpr int kGeomPlane = 2;                      // core.py:46
+constexpr int kGeomCylinder = 3;
+constexpr uint32_t kKindShift = 30;                // ACS id word: kind in bits 30-31
+constexpr uint32_t kSlotMask = (1u << kKindShift) - 1u;
+constexpr int kMaxBins = 1 << 22;                  // broadphase.py:20
+constexpr int kFamilies = 256;
+
+// family flag bits (engine.py:264-271)
+constexpr uint8_t kFamFixed = 1;
+constexpr uint8_t kFamPrescribed = 2;
+
+// ---------------------------------------------------------------------------
+// device scene: plain pointers, passed by value to every kernel
+// ---------------------------------------------------------------------------
+struct Domain {
+  double lo[3], hi[3], edge;
+};
+
+struct Owners {
+  int64_t n;
+  uint64_t *voxel;     // packed 3 x 21-bit cells, x lowest (types.py:27-32)
+  ushort4 *sub;        // sub-voxel x, y, z (w unused)
+  float4 *quat;        // (w, x, y, z) float32 (types.py:15)
+  void *lin_vel;       // VelT[4] per owner (x, y, z, pad)
+  void *ang_vel;       // VelT[4] per owner, owner-local frame
+  uint32_t *meta;      // family (bits 24-31) | template id (bits 0-23)
+  double4 *tpl;        // per template: mass, moi x, y, z
+  double *acc;         // [n*6] force xyz, torque xyz (global frame), optional
+  double *ext;         // [n*6] external force/torque or nullptr
+};
+
+struct Spheres {
+  int64_t n;
+  uint32_t *owner;
+  float4 *offr;        // local offset xyz + radius (float32 geom params)
+  uint8_t *mat;
+};
+
+struct Tris {
+  int64_t n;
+  uint32_t *owner;
+  float *local;        // [n*9] owner-local vertices
+  uint8_t *mat;
+  double *world;       // [n*9]
+};
+
+struct Anas {
+  int64_t n;
+  uint32_t *owner;
+  uint8_t *kind;
+  float *local;        // [n*8]
+  uint8_t *mat;
+  double *world;       // [n*8]
+};
+
+struct Materials {
+  int n_mat;
+  const double *pair;  // [(2 + n_props) * M * M]: E_cnt, G_cnt, CoR, mu, Crr
+  const double *beta;  // [M * M] restitution damping, host-computed
+};
+
+struct Families {
+  const uint8_t *mask;        // [256*256]
+  const uint8_t *flags;       // [256] kFamFixed | kFamPrescribed
+  const uint8_t *lv_mask;     // [256] bit ax
+  const uint8_t *av_mask;     // [256]
+  const double *lv_val;       // [256*3]
+  const double *av_val;       // [256*3]
+};
+
+__host__ __device__ inline uint32_t meta_family(uint32_t m) { return m >> 24; }
+__host__ __device__ inline uint32_t meta_tpl(uint32_t m) { return m & 0xFFFFFFu; }
+
+// ---------------------------------------------------------------------------
+// exact fp64 helpers (explicit _rn intrinsics: no contraction possible)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub_(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+
+// compressed position -> fp64 (_kernels.py:55-67)
+__device__ __forceinline__ void decode_pos(const Domain &d, uint64_t v, ushort4 s,
+                                           double &x, double &y, double &z) {
+  const uint64_t m = uint64_t(kVoxPerAxis - 1);
+  double cx = double(v & m), cy = double((v >> kVoxBits) & m), cz = double((v >> (2 * kVoxBits)) & m);
+  x = add(d.lo[0], mul(add(cx, double(s.x) / double(kSubPerEdge)), d.edge));
+  y = add(d.lo[1], mul(add(cy, double(s.y) / double(kSubPerEdge)), d.edge));
+  z = add(d.lo[2], mul(add(cz, double(s.z) / double(kSubPerEdge)), d.edge));
+}
+
+// fp64 -> compressed position; false when outside the domain box
+// (_kernels.py:33-52)
+__device__ __forceinline__ bool encode_pos(const Domain &d, const double p[3], uint64_t &v,
+                                           ushort4 &s) {
+  v = 0;
+  unsigned short sv[3];
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    if (p[ax] < d.lo[ax] || p[ax] > d.hi[ax]) return false;
+    double t = sub_(p[ax], d.lo[ax]) / d.edge;
+    long long cell = (long long)t;
+    if (cell >= kVoxPerAxis) cell = kVoxPerAxis - 1;
+    long long q = (long long)mul(sub_(t, double(cell)), double(kSubPerEdge));
+    if (q >= kSubPerEdge) q = kSubPerEdge - 1;
+    v |= uint64_t(cell) << (kVoxBits * ax);
+    sv[ax] = (unsigned short)q;
+  }
+  s = make_ushort4(sv[0], sv[1], sv[2], 0);
+  return true;
+}
+
+// r = v + 2 u x (u x v + w v), term order of _kernels.py:75-83
+__device__ __forceinline__ void qrot(double qw, double qx, double qy, double qz, double vx,
+                                     double vy, double vz, double &rx, double &ry, double &rz) {
+  double tx = add(sub_(mul(qy, vz), mul(qz, vy)), mul(qw, vx));
+  double ty = add(sub_(mul(qz, vx), mul(qx, vz)), mul(qw, vy));
+  double tz = add(sub_(mul(qx, vy), mul(qy, vx)), mul(qw, vz));
+  rx = add(vx, mul(2.0, sub_(mul(qy, tz), mul(qz, ty))));
+  ry = add(vy, mul(2.0, sub_(mul(qz, tx), mul(qx, tz))));
+  rz = add(vz, mul(2.0, sub_(mul(qx, ty), mul(qy, tx))));
+}
+
+// sphere world centre: owner pos + q * offset (_kernels.py:91-106)
+__device__ __forceinline__ void sphere_center(const Domain &d, const Owners &o, const Spheres &s,
+                                              uint32_t k, double c[3], float &radius,
+                                              uint32_t &owner) {
+  owner = s.owner[k];
+  float4 orr = s.offr[k];
+  float4 q = o.quat[owner];
+  double px, py, pz;
+  decode_pos(d, o.voxel[owner], o.sub[owner], px, py, pz);
+  double rx, ry, rz;
+  qrot(double(q.x), double(q.y), double(q.z), double(q.w), double(orr.x), double(orr.y),
+       double(orr.z), rx, ry, rz);
+  c[0] = add(px, rx);
+  c[1] = add(py, ry);
+  c[2] = add(pz, rz);
+  radius = orr.w;
+}
+
+// Ericson RTCD 5.1.5, branch order of _kernels.py:159-194
+__device__ inline void closest_on_tri(double px, double py, double pz, const double *t,
+                                      double &qx, double &qy, double &qz) {
+  double ax = t[0], ay = t[1], az = t[2], bx = t[3], by = t[4], bz = t[5];
+  double cx = t[6], cy = t[7], cz = t[8];
+  double abx = sub_(bx, ax), aby = sub_(by, ay), abz = sub_(bz, az);
+  double acx = sub_(cx, ax), acy = sub_(cy, ay), acz = sub_(cz, az);
+  double apx = sub_(px, ax), apy = sub_(py, ay), apz = sub_(pz, az);
+  double d1 = add(add(mul(abx, apx), mul(aby, apy)), mul(abz, apz));
+  double d2 = add(add(mul(acx, apx), mul(acy, apy)), mul(acz, apz));
+  if (d1 <= 0.0 && d2 <= 0.0) { qx = ax; qy = ay; qz = az; return; }
+  double bpx = sub_(px, bx), bpy = sub_(py, by), bpz = sub_(pz, bz);
+  double d3 = add(add(mul(abx, bpx), mul(aby, bpy)), mul(abz, bpz));
+  double d4 = add(add(mul(acx, bpx), mul(acy, bpy)), mul(acz, bpz));
+  if (d3 >= 0.0 && d4 <= d3) { qx = bx; qy = by; qz = bz; return; }
+  double vc = sub_(mul(d1, d4), mul(d3, d2));
+  if (vc <= 0.0 && d1 >= 0.0 && d3 <= 0.0) {
+    double s = d1 / sub_(d1, d3);
+    qx = add(ax, mul(s, abx)); qy = add(ay, mul(s, aby)); qz = add(az, mul(s, abz));
+    return;
+  }
+  double cpx = sub_(px, cx), cpy = sub_(py, cy), cpz = sub_(pz, cz);
+  double d5 = add(add(mul(abx, cpx), mul(aby, cpy)), mul(abz, cpz));
+  double d6 = add(add(mul(acx, cpx), mul(acy, cpy)), mul(acz, cpz));
+  if (d6 >= 0.0 && d5 <= d6) { qx = cx; qy = cy; qz = cz; return; }
+  double vb = sub_(mul(d5, d2), mul(d1, d6));
+  if (vb <= 0.0 && d2 >= 0.0 && d6 <= 0.0) {
+    double s = d2 / sub_(d2, d6);
+    qx = add(ax, mul(s, acx)); qy = add(ay, mul(s, acy)); qz = add(az, mul(s, acz));
+    return;
+  }
+  double va = sub_(mul(d3, d6), mul(d5, d4));
+  if (va <= 0.0 && sub_(d4, d3) >= 0.0 && sub_(d5, d6) >= 0.0) {
+    double s = sub_(d4, d3) / add(sub_(d4, d3), sub_(d5, d6));
+    qx = add(bx, mul(s, sub_(cx, bx)));
+    qy = add(by, mul(s, sub_(cy, by)));
+    qz = add(bz, mul(s, sub_(cz, bz)));
+    return;
+  }
+  double denom = 1.0 / add(add(va, vb), vc);
+  double v = mul(vb, denom), w = mul(vc, denom);
+  qx = add(add(ax, mul(abx, v)), mul(acx, w));
+  qy = add(add(ay, mul(aby, v)), mul(acy, w));
+  qz = add(add(az, mul(abz, v)), mul(acz, w));
+}
+
+// plane / cylinder gap, push direction and signed curvature (_kernels.py:209-231)
+__device__ inline void analytic_gap(int kind, const double *prm, double cx, double cy, double cz,
+                                    double &gap, double &bx, double &by, double &bz, double &rb) {
+  if (kind == kGeomPlane) {
+    double nx = prm[3], ny = prm[4], nz = prm[5];
+    gap = add(add(mul(sub_(cx, prm[0]), nx), mul(sub_(cy, prm[1]), ny)), mul(sub_(cz, prm[2]), nz));
+    bx = nx; by = ny; bz = nz; rb = kFlatRadius;
+    return;
+  }
+  double ax = prm[3], ay = prm[4], az = prm[5];
+  double wx = sub_(cx, prm[0]), wy = sub_(cy, prm[1]), wz = sub_(cz, prm[2]);
+  double axial = add(add(mul(wx, ax), mul(wy, ay)), mul(wz, az));
+  double rx = sub_(wx, mul(axial, ax)), ry = sub_(wy, mul(axial, ay)), rz = sub_(wz, mul(axial, az));
+  double rho = sqrt(add(add(mul(rx, rx), mul(ry, ry)), mul(rz, rz)));
+  double radius = prm[6], facing = prm[7];
+  if (rho < 1e-300) { gap = radius; bx = 0.0; by = 0.0; bz = 0.0; rb = radius; return; }
+  double inv = 1.0 / rho;
+  if (facing > 0.0) {
+    gap = sub_(rho, radius); bx = mul(rx, inv); by = mul(ry, inv); bz = mul(rz, inv); rb = radius;
+  } else {
+    gap = sub_(radius, rho); bx = mul(-rx, inv); by = mul(-ry, inv); bz = mul(-rz, inv); rb = -radius;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// uniform grid (broadphase.py:160-186, _kernels.py:238-266)
+// ---------------------------------------------------------------------------
+struct Grid {
+  double glo[3];
+  double inv_bin;
+  long long nb[3];
+  int valid;
+};
+
+__device__ __forceinline__ long long axis_bin(double x, double glo, double inv_bin, long long nb) {
+  long long i = (long long)mul(sub_(x, glo), inv_bin);
+  if (i < 0) i = 0;
+  if (i >= nb) i = nb - 1;
+  return i;
+}
+
+// inclusive per-axis bin range of a margin-enlarged sphere (_kernels.py:253-266)
+__device__ __forceinline__ void sphere_range(const Grid &g, const double c[3], float radius,
+                                             double margin, long long lo[3], long long hi[3]) {
+  double r = add(double(radius), margin);
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    long long l = (long long)mul(sub_(sub_(c[ax], r), g.glo[ax]), g.inv_bin);
+    long long h = (long long)mul(sub_(add(c[ax], r), g.glo[ax]), g.inv_bin);
+    if (l < 0) l = 0;
+    if (h < 0) h = 0;
+    if (l >= g.nb[ax]) l = g.nb[ax] - 1;
+    if (h >= g.nb[ax]) h = g.nb[ax] - 1;
+    lo[ax] = l;
+    hi[ax] = h;
+  }
+}
+
+}  // namespace gf

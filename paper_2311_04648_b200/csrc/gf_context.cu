@@ -1,0 +1,681 @@
+// gf_context.cu -- C-ABI (include/gf_b200.h): context, scene upload/download,
+// per-kernel entry points and the kT/dT worker protocol (gf_run).
+//
+// Scheduler (replaces the reference's two threads + _Slot handoffs,
+// engine.py:90-115, 669-906): kT and dT are two CUDA streams of one device.
+// At a snapshot step the dT stream records the snapshot (sphere centres,
+// families, world geometry); the kT stream waits on that event and runs
+// detection into the second ACS buffer while the dT stream keeps stepping on
+// the active ACS.  `lag` steps later the dT stream waits on the kT completion
+// event, remaps the contact history onto the new array (merge_history) and
+// swaps the double buffer.  Adoption happens at a fixed step, so runs are
+// bitwise reproducible; period = 1, lag = 0 is the reference's sync mode.
+#include <chrono>
+#include <cstring>
+#include <vector>
+
+#include "../../include/gf_b200.h"
+#include "gf_context.h"
+
+struct gf_ctx {
+  gf::Ctx c;
+};
+
+namespace gf {
+
+void set_err(Ctx *c, const std::string &msg) { c->err = msg; }
+
+int ensure(Ctx *c, DBuf &b, size_t bytes, cudaStream_t s, bool keep) {
+  if (bytes == 0) bytes = 16;
+  if (b.bytes >= bytes) return 0;
+  size_t nb = bytes + bytes / 4 + 256;
+  void *p = nullptr;
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMalloc(&p, nb);
+  if (e != cudaSuccess) {
+    set_err(c, std::string("device allocation of ") + std::to_string(nb) + " bytes failed: " +
+                   cudaGetErrorString(e));
+    return -1;
+  }
+  if (keep && b.p && b.bytes) cudaMemcpy(p, b.p, b.bytes, cudaMemcpyDeviceToDevice);
+  if (b.p) cudaFree(b.p);
+  b.p = p;
+  b.bytes = nb;
+  (void)s;
+  return 0;
+}
+
+static void release(DBuf &b) {
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.bytes = 0;
+}
+
+Owners owners_view(Ctx *c) {
+  Owners o;
+  o.n = c->n_owner;
+  o.voxel = c->voxel.as<uint64_t>();
+  o.sub = c->sub.as<ushort4>();
+  o.quat = c->quat.as<float4>();
+  o.lin_vel = c->lin_vel.p;
+  o.ang_vel = c->ang_vel.p;
+  o.meta = c->meta.as<uint32_t>();
+  o.tpl = c->tpl.as<double4>();
+  o.acc = c->acc.as<double>();
+  o.ext = c->has_ext ? c->ext.as<double>() : nullptr;
+  return o;
+}
+Spheres spheres_view(Ctx *c) {
+  return Spheres{c->n_sph, c->sph_owner.as<uint32_t>(), c->sph_offr.as<float4>(), c->sph_mat.as<uint8_t>()};
+}
+Tris tris_view(Ctx *c) {
+  return Tris{c->n_tri, c->tri_owner.as<uint32_t>(), c->tri_local.as<float>(), c->tri_mat.as<uint8_t>(),
+              c->tri_world.as<double>()};
+}
+Anas anas_view(Ctx *c) {
+  return Anas{c->n_ana, c->ana_owner.as<uint32_t>(), c->ana_kind.as<uint8_t>(), c->ana_local.as<float>(),
+              c->ana_mat.as<uint8_t>(), c->ana_world.as<double>()};
+}
+Materials materials_view(Ctx *c) {
+  return Materials{c->n_mat, c->pair.as<double>(), c->beta.as<double>()};
+}
+Families families_view(Ctx *c) {
+  return Families{c->fam_mask.as<uint8_t>(), c->fam_flags.as<uint8_t>(), c->lv_mask.as<uint8_t>(),
+                  c->av_mask.as<uint8_t>(), c->lv_val.as<double>(), c->av_val.as<double>()};
+}
+
+static int dt_step(Ctx *c, const StepArgs &a) {
+  return c->f32_state ? dt_step_f32(c, a, c->s_dt) : dt_step_f64(c, a, c->s_dt);
+}
+
+static int reset_status(Ctx *c, cudaStream_t s) {
+  Status *st = c->status.as<Status>();
+  GF_CHECK(c, cudaMemsetAsync(st, 0xFF, 2 * sizeof(unsigned long long), s));
+  GF_CHECK(c, cudaMemsetAsync(&st->touching, 0, sizeof(unsigned long long), s));
+  GF_CHECK(c, cudaMemsetAsync(&st->err, 0, sizeof(int), s));
+  return 0;
+}
+
+static int read_status(Ctx *c, cudaStream_t s, Status *out) {
+  GF_CHECK(c, cudaMemcpyAsync(c->h_status, c->status.p, sizeof(Status), cudaMemcpyDeviceToHost, s));
+  GF_CHECK(c, cudaStreamSynchronize(s));
+  std::memcpy(out, c->h_status, sizeof(Status));
+  return 0;
+}
+
+static void decode_err(unsigned long long w, int64_t &owner, int64_t &step) {
+  if (w == ~0ull) { owner = -1; step = -1; return; }
+  owner = int64_t(w & ((1ull << 40) - 1));
+  step = int64_t(w >> 40);
+}
+
+static void world_moving_update(Ctx *c) {
+  // _refresh_moving_world (engine.py:552-568): skip while every mesh /
+  // analytic owner sits in a fixed family
+  c->world_moving = false;
+  std::vector<uint32_t> own;
+  auto scan = [&](const DBuf &b, int64_t n) {
+    if (!n) return;
+    std::vector<uint32_t> h(n);
+    cudaMemcpy(h.data(), b.p, 4 * n, cudaMemcpyDeviceToHost);
+    own.insert(own.end(), h.begin(), h.end());
+  };
+  scan(c->tri_owner, c->n_tri);
+  scan(c->ana_owner, c->n_ana);
+  if (own.empty() || !c->n_owner) return;
+  std::vector<uint32_t> meta(c->n_owner);
+  cudaMemcpy(meta.data(), c->meta.p, 4 * c->n_owner, cudaMemcpyDeviceToHost);
+  for (uint32_t o : own) {
+    uint32_t fam = meta_family(meta[o]);
+    if (!(c->h_fam_flags.size() == 256 && (c->h_fam_flags[fam] & kFamFixed))) {
+      c->world_moving = true;
+      return;
+    }
+  }
+}
+
+}  // namespace gf
+
+using namespace gf;
+
+#define CTX_CHECK(ctx)                 \
+  if (!(ctx)) return -1;               \
+  gf::Ctx *c = &(ctx)->c;              \
+  if (cudaSetDevice(c->device) != cudaSuccess) { c->err = "cudaSetDevice failed"; return -1; }
+
+extern "C" {
+
+int gf_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+gf_ctx *gf_create(int device, uint32_t flags) {
+  if (cudaSetDevice(device) != cudaSuccess) return nullptr;
+  gf_ctx *ctx = new gf_ctx();
+  Ctx *c = &ctx->c;
+  c->device = device;
+  c->flags = flags;
+  c->f32_state = (flags & GF_STATE_F32) != 0;
+  cudaStreamCreateWithFlags(&c->s_dt, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&c->s_kt, cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&c->ev_snap, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->ev_ca, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->ev_adopted, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->ev_count, cudaEventDisableTiming);
+  cudaEventCreate(&c->t0);
+  cudaEventCreate(&c->t1);
+  cudaEventRecord(c->ev_adopted, c->s_dt);
+  if (cudaMallocHost(&c->h_status, sizeof(Status)) != cudaSuccess) { delete ctx; return nullptr; }
+  if (ensure(c, c->status, sizeof(Status), c->s_dt) || ensure(c, c->heavy_count, 16, c->s_dt)) {
+    delete ctx;
+    return nullptr;
+  }
+  reset_status(c, c->s_dt);
+  cudaStreamSynchronize(c->s_dt);
+  return ctx;
+}
+
+void gf_destroy(gf_ctx *ctx) {
+  if (!ctx) return;
+  Ctx *c = &ctx->c;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  DBuf *bufs[] = {&c->voxel, &c->sub, &c->quat, &c->lin_vel, &c->ang_vel, &c->meta, &c->tpl, &c->acc,
+                  &c->ext, &c->sph_owner, &c->sph_offr, &c->sph_mat, &c->tri_owner, &c->tri_local,
+                  &c->tri_mat, &c->tri_world, &c->ana_owner, &c->ana_kind, &c->ana_local, &c->ana_mat,
+                  &c->ana_world, &c->pair, &c->beta, &c->fam_mask, &c->fam_flags, &c->lv_mask,
+                  &c->av_mask, &c->lv_val, &c->av_val, &c->acs.ids, &c->acs.wild, &c->acs_next.ids,
+                  &c->acs_next.wild, &c->out_c, &c->touch, &c->inc, &c->inc_alt, &c->inc_key,
+                  &c->inc_key_alt, &c->inc_start, &c->heavy, &c->heavy_count, &c->heavy_acc,
+                  &c->cub_tmp_dt, &c->status, &c->dyn_spec, &c->dyn_vals, &c->kt.centers, &c->kt.sfam,
+                  &c->kt.tri_world, &c->kt.ana_world, &c->kt.tfam, &c->kt.afam, &c->kt.grid,
+                  &c->kt.minmax, &c->kt.bin_key, &c->kt.bin_key_alt, &c->kt.sph_val, &c->kt.sph_val_alt,
+                  &c->kt.cell_start, &c->kt.cell_end, &c->kt.tri_ranges, &c->kt.tri_cnt,
+                  &c->kt.tri_start, &c->kt.tri_entries, &c->kt.counts, &c->kt.offsets, &c->kt.cub_tmp,
+                  &c->kt.total};
+  for (DBuf *b : bufs) release(*b);
+  if (c->h_status) cudaFreeHost(c->h_status);
+  cudaEvent_t evs[] = {c->ev_snap, c->ev_ca, c->ev_adopted, c->ev_count, c->t0, c->t1};
+  for (auto e : evs) cudaEventDestroy(e);
+  cudaStreamDestroy(c->s_dt);
+  cudaStreamDestroy(c->s_kt);
+  delete ctx;
+}
+
+int gf_last_error(gf_ctx *ctx, char *buf, size_t n) {
+  if (!ctx || !buf || !n) return -1;
+  std::strncpy(buf, ctx->c.err.c_str(), n - 1);
+  buf[n - 1] = 0;
+  return 0;
+}
+
+int gf_set_domain(gf_ctx *ctx, const double *lo3, const double *hi3, double edge) {
+  CTX_CHECK(ctx);
+  for (int a = 0; a < 3; ++a) { c->dom.lo[a] = lo3[a]; c->dom.hi[a] = hi3[a]; }
+  c->dom.edge = edge;
+  return 0;
+}
+
+int gf_upload_owners(gf_ctx *ctx, int64_t n, const uint64_t *voxel, const uint16_t *sub,
+                     const float *quat, const double *lin_vel, const double *ang_vel,
+                     const uint8_t *family, const uint32_t *tpl, int64_t n_tpl,
+                     const double *tpl_mass, const double *tpl_moi) {
+  CTX_CHECK(ctx);
+  if (n_tpl >= (1 << 24)) { c->err = "too many mass-property templates (max 2^24)"; return -1; }
+  c->n_owner = n;
+  c->n_tpl = n_tpl;
+  const size_t vb = c->f32_state ? sizeof(float) * 4 : sizeof(double) * 4;
+  if (ensure(c, c->voxel, 8 * n, c->s_dt) || ensure(c, c->sub, 8 * n, c->s_dt) ||
+      ensure(c, c->quat, 16 * n, c->s_dt) || ensure(c, c->lin_vel, vb * n, c->s_dt) ||
+      ensure(c, c->ang_vel, vb * n, c->s_dt) || ensure(c, c->meta, 4 * n, c->s_dt) ||
+      ensure(c, c->tpl, 32 * (n_tpl + 1), c->s_dt) || ensure(c, c->acc, 48 * n, c->s_dt) ||
+      ensure(c, c->heavy_acc, 48 * n, c->s_dt) || ensure(c, c->inc_start, 4 * (n + 2), c->s_dt) ||
+      ensure(c, c->heavy, 4 * (n + 1), c->s_dt))
+    return -1;
+  std::vector<uint16_t> s4(4 * n);
+  std::vector<uint32_t> meta(n);
+  for (int64_t i = 0; i < n; ++i) {
+    s4[4 * i] = sub[3 * i];
+    s4[4 * i + 1] = sub[3 * i + 1];
+    s4[4 * i + 2] = sub[3 * i + 2];
+    s4[4 * i + 3] = 0;
+    meta[i] = (uint32_t(family[i]) << 24) | (tpl[i] & 0xFFFFFFu);
+  }
+  GF_CHECK(c, cudaMemcpy(c->voxel.p, voxel, 8 * n, cudaMemcpyHostToDevice));
+  GF_CHECK(c, cudaMemcpy(c->sub.p, s4.data(), 8 * n, cudaMemcpyHostToDevice));
+  GF_CHECK(c, cudaMemcpy(c->quat.p, quat, 16 * n, cudaMemcpyHostToDevice));
+  GF_CHECK(c, cudaMemcpy(c->meta.p, meta.data(), 4 * n, cudaMemcpyHostToDevice));
+  for (int which = 0; which < 2; ++which) {
+    const double *src = which ? ang_vel : lin_vel;
+    DBuf &dst = which ? c->ang_vel : c->lin_vel;
+    if (c->f32_state) {
+      std::vector<float> v(4 * n, 0.f);
+      for (int64_t i = 0; i < n; ++i)
+        for (int a = 0; a < 3; ++a) v[4 * i + a] = float(src[3 * i + a]);
+      GF_CHECK(c, cudaMemcpy(dst.p, v.data(), 16 * n, cudaMemcpyHostToDevice));
+    } else {
+      std::vector<double> v(4 * n, 0.0);
+      for (int64_t i = 0; i < n; ++i)
+        for (int a = 0; a < 3; ++a) v[4 * i + a] = src[3 * i + a];
+      GF_CHECK(c, cudaMemcpy(dst.p, v.data(), 32 * n, cudaMemcpyHostToDevice));
+    }
+  }
+  std::vector<double> tp(4 * n_tpl);
+  for (int64_t t = 0; t < n_tpl; ++t) {
+    tp[4 * t] = tpl_mass[t];
+    tp[4 * t + 1] = tpl_moi[3 * t];
+    tp[4 * t + 2] = tpl_moi[3 * t + 1];
+    tp[4 * t + 3] = tpl_moi[3 * t + 2];
+  }
+  if (n_tpl) GF_CHECK(c, cudaMemcpy(c->tpl.p, tp.data(), 32 * n_tpl, cudaMemcpyHostToDevice));
+  GF_CHECK(c, cudaMemset(c->acc.p, 0, 48 * n));
+  if (c->has_ext) GF_CHECK(c, cudaMemset(c->ext.p, 0, 48 * n));
+  world_moving_update(c);
+  return 0;
+}
+
+int gf_download_owners(gf_ctx *ctx, uint64_t *voxel, uint16_t *sub, float *quat, double *lin_vel,
+                       double *ang_vel, uint8_t *family) {
+  CTX_CHECK(ctx);
+  const int64_t n = c->n_owner;
+  GF_CHECK(c, cudaDeviceSynchronize());
+  if (voxel) GF_CHECK(c, cudaMemcpy(voxel, c->voxel.p, 8 * n, cudaMemcpyDeviceToHost));
+  if (sub) {
+    std::vector<uint16_t> s4(4 * n);
+    GF_CHECK(c, cudaMemcpy(s4.data(), c->sub.p, 8 * n, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < n; ++i)
+      for (int a = 0; a < 3; ++a) sub[3 * i + a] = s4[4 * i + a];
+  }
+  if (quat) GF_CHECK(c, cudaMemcpy(quat, c->quat.p, 16 * n, cudaMemcpyDeviceToHost));
+  for (int which = 0; which < 2; ++which) {
+    double *dst = which ? ang_vel : lin_vel;
+    if (!dst) continue;
+    DBuf &src = which ? c->ang_vel : c->lin_vel;
+    if (c->f32_state) {
+      std::vector<float> v(4 * n);
+      GF_CHECK(c, cudaMemcpy(v.data(), src.p, 16 * n, cudaMemcpyDeviceToHost));
+      for (int64_t i = 0; i < n; ++i)
+        for (int a = 0; a < 3; ++a) dst[3 * i + a] = double(v[4 * i + a]);
+    } else {
+      std::vector<double> v(4 * n);
+      GF_CHECK(c, cudaMemcpy(v.data(), src.p, 32 * n, cudaMemcpyDeviceToHost));
+      for (int64_t i = 0; i < n; ++i)
+        for (int a = 0; a < 3; ++a) dst[3 * i + a] = v[4 * i + a];
+    }
+  }
+  if (family) {
+    std::vector<uint32_t> meta(n);
+    GF_CHECK(c, cudaMemcpy(meta.data(), c->meta.p, 4 * n, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < n; ++i) family[i] = uint8_t(meta_family(meta[i]));
+  }
+  return 0;
+}
+
+int gf_set_owner_families(gf_ctx *ctx, const uint8_t *family) {
+  CTX_CHECK(ctx);
+  const int64_t n = c->n_owner;
+  GF_CHECK(c, cudaDeviceSynchronize());
+  std::vector<uint32_t> meta(n);
+  GF_CHECK(c, cudaMemcpy(meta.data(), c->meta.p, 4 * n, cudaMemcpyDeviceToHost));
+  for (int64_t i = 0; i < n; ++i) meta[i] = (uint32_t(family[i]) << 24) | (meta[i] & 0xFFFFFFu);
+  GF_CHECK(c, cudaMemcpy(c->meta.p, meta.data(), 4 * n, cudaMemcpyHostToDevice));
+  world_moving_update(c);
+  return 0;
+}
+
+int gf_set_external_loads(gf_ctx *ctx, const double *force, const double *torque) {
+  CTX_CHECK(ctx);
+  const int64_t n = c->n_owner;
+  GF_CHECK(c, cudaDeviceSynchronize());
+  if (!force && !torque) { c->has_ext = false; return 0; }
+  if (ensure(c, c->ext, 48 * n, c->s_dt)) return -1;
+  std::vector<double> e(6 * n, 0.0);
+  for (int64_t i = 0; i < n; ++i)
+    for (int a = 0; a < 3; ++a) {
+      if (force) e[6 * i + a] = force[3 * i + a];
+      if (torque) e[6 * i + 3 + a] = torque[3 * i + a];
+    }
+  GF_CHECK(c, cudaMemcpy(c->ext.p, e.data(), 48 * n, cudaMemcpyHostToDevice));
+  c->has_ext = true;
+  return 0;
+}
+
+int gf_download_accumulators(gf_ctx *ctx, double *acc_force, double *acc_torque) {
+  CTX_CHECK(ctx);
+  const int64_t n = c->n_owner;
+  GF_CHECK(c, cudaDeviceSynchronize());
+  std::vector<double> a(6 * n);
+  GF_CHECK(c, cudaMemcpy(a.data(), c->acc.p, 48 * n, cudaMemcpyDeviceToHost));
+  for (int64_t i = 0; i < n; ++i)
+    for (int q = 0; q < 3; ++q) {
+      if (acc_force) acc_force[3 * i + q] = a[6 * i + q];
+      if (acc_torque) acc_torque[3 * i + q] = a[6 * i + 3 + q];
+    }
+  return 0;
+}
+
+static int upload_u32(Ctx *c, DBuf &b, const int64_t *src, int64_t n) {
+  std::vector<uint32_t> v(n);
+  for (int64_t i = 0; i < n; ++i) v[i] = uint32_t(src[i]);
+  if (ensure(c, b, 4 * (n + 1), c->s_dt)) return -1;
+  if (n) GF_CHECK(c, cudaMemcpy(b.p, v.data(), 4 * n, cudaMemcpyHostToDevice));
+  return 0;
+}
+
+static int upload_raw(Ctx *c, DBuf &b, const void *src, size_t bytes) {
+  if (ensure(c, b, bytes + 16, c->s_dt)) return -1;
+  if (bytes) GF_CHECK(c, cudaMemcpy(b.p, src, bytes, cudaMemcpyHostToDevice));
+  return 0;
+}
+
+int gf_upload_geometry(gf_ctx *ctx, int64_t n_s, const int64_t *sph_owner, const float *sph_params,
+                       const uint8_t *sph_mat, int64_t n_t, const int64_t *tri_owner,
+                       const float *tri_local, const uint8_t *tri_mat, int64_t n_a,
+                       const int64_t *ana_owner, const uint8_t *ana_kind, const float *ana_local,
+                       const uint8_t *ana_mat) {
+  CTX_CHECK(ctx);
+  GF_CHECK(c, cudaDeviceSynchronize());
+  if (n_s >= (int64_t(1) << 30) || n_t >= (int64_t(1) << 30)) { c->err = "too many geometries"; return -1; }
+  c->n_sph = n_s;
+  c->n_tri = n_t;
+  c->n_ana = n_a;
+  if (upload_u32(c, c->sph_owner, sph_owner, n_s) || upload_raw(c, c->sph_offr, sph_params, 16 * n_s) ||
+      upload_raw(c, c->sph_mat, sph_mat, n_s) || upload_u32(c, c->tri_owner, tri_owner, n_t) ||
+      upload_raw(c, c->tri_local, tri_local, 36 * n_t) || upload_raw(c, c->tri_mat, tri_mat, n_t) ||
+      upload_u32(c, c->ana_owner, ana_owner, n_a) || upload_raw(c, c->ana_kind, ana_kind, n_a) ||
+      upload_raw(c, c->ana_local, ana_local, 32 * n_a) || upload_raw(c, c->ana_mat, ana_mat, n_a) ||
+      ensure(c, c->tri_world, 72 * (n_t + 1), c->s_dt) || ensure(c, c->ana_world, 64 * (n_a + 1), c->s_dt))
+    return -1;
+  world_moving_update(c);
+  // world transforms of meshes / analytics for the current pose
+  if (refresh_world(c, c->s_dt)) return -1;
+  GF_CHECK(c, cudaStreamSynchronize(c->s_dt));
+  return 0;
+}
+
+int gf_upload_materials(gf_ctx *ctx, int n_mat, int n_rows, const double *pair_stack, const double *beta) {
+  CTX_CHECK(ctx);
+  GF_CHECK(c, cudaDeviceSynchronize());
+  if (n_rows < 5) { c->err = "pair stack needs rows E_cnt, G_cnt, CoR, mu, Crr"; return -1; }
+  c->n_mat = n_mat;
+  c->n_pair_rows = n_rows;
+  if (upload_raw(c, c->pair, pair_stack, sizeof(double) * n_rows * n_mat * n_mat) ||
+      upload_raw(c, c->beta, beta, sizeof(double) * n_mat * n_mat))
+    return -1;
+  return 0;
+}
+
+int gf_upload_families(gf_ctx *ctx, const uint8_t *mask, const uint8_t *flags, const uint8_t *lv_mask,
+                       const uint8_t *av_mask, const double *lv_val, const double *av_val) {
+  CTX_CHECK(ctx);
+  GF_CHECK(c, cudaDeviceSynchronize());
+  if (upload_raw(c, c->fam_mask, mask, 65536) || upload_raw(c, c->fam_flags, flags, 256) ||
+      upload_raw(c, c->lv_mask, lv_mask, 256) || upload_raw(c, c->av_mask, av_mask, 256) ||
+      upload_raw(c, c->lv_val, lv_val, sizeof(double) * 768) ||
+      upload_raw(c, c->av_val, av_val, sizeof(double) * 768))
+    return -1;
+  c->h_fam_flags.assign(flags, flags + 256);
+  world_moving_update(c);
+  return 0;
+}
+
+int gf_download_world(gf_ctx *ctx, double *sph_centers, double *tri_world, double *ana_world) {
+  CTX_CHECK(ctx);
+  GF_CHECK(c, cudaDeviceSynchronize());
+  if (sph_centers && c->n_sph) {
+    if (kt_snapshot(c, c->s_dt)) return -1;
+    GF_CHECK(c, cudaStreamSynchronize(c->s_dt));
+    GF_CHECK(c, cudaMemcpy(sph_centers, c->kt.centers.p, 24 * c->n_sph, cudaMemcpyDeviceToHost));
+  }
+  if (tri_world && c->n_tri) GF_CHECK(c, cudaMemcpy(tri_world, c->tri_world.p, 72 * c->n_tri, cudaMemcpyDeviceToHost));
+  if (ana_world && c->n_ana) GF_CHECK(c, cudaMemcpy(ana_world, c->ana_world.p, 64 * c->n_ana, cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int gf_set_acs(gf_ctx *ctx, int64_t n, const uint8_t *kind, const int64_t *slot_a, const int64_t *slot_b,
+               const float *wild, int W) {
+  CTX_CHECK(ctx);
+  GF_CHECK(c, cudaDeviceSynchronize());
+  if (W != 4) { c->err = "only 4 history wildcards are supported by this build"; return -1; }
+  c->wild_w = W;
+  int64_t cap = n + n / 2 + 1024;
+  if (ensure(c, c->acs.ids, 8 * cap, c->s_dt) || ensure(c, c->acs.wild, 4 * W * cap, c->s_dt)) return -1;
+  c->acs.cap = cap;
+  c->acs.n = n;
+  std::vector<uint32_t> ids(2 * n);
+  for (int64_t k = 0; k < n; ++k) {
+    ids[2 * k] = uint32_t(slot_a[k]);
+    ids[2 * k + 1] = uint32_t(slot_b[k]) | (uint32_t(kind[k]) << kKindShift);
+  }
+  if (n) {
+    GF_CHECK(c, cudaMemcpy(c->acs.ids.p, ids.data(), 8 * n, cudaMemcpyHostToDevice));
+    if (wild) GF_CHECK(c, cudaMemcpy(c->acs.wild.p, wild, 4 * W * n, cudaMemcpyHostToDevice));
+    else GF_CHECK(c, cudaMemset(c->acs.wild.p, 0, 4 * W * n));
+  }
+  if (build_incidence(c, c->s_dt)) return -1;
+  GF_CHECK(c, cudaStreamSynchronize(c->s_dt));
+  c->ca_updates = std::max<int64_t>(c->ca_updates, 1);
+  return 0;
+}
+
+int64_t gf_acs_size(gf_ctx *ctx, int which) {
+  if (!ctx) return -1;
+  return which ? ctx->c.acs_next.n : ctx->c.acs.n;
+}
+
+int gf_get_acs(gf_ctx *ctx, int which, uint8_t *kind, int64_t *slot_a, int64_t *slot_b, float *wild) {
+  CTX_CHECK(ctx);
+  GF_CHECK(c, cudaDeviceSynchronize());
+  Acs &a = which ? c->acs_next : c->acs;
+  const int64_t n = a.n;
+  if (!n) return 0;
+  std::vector<uint32_t> ids(2 * n);
+  GF_CHECK(c, cudaMemcpy(ids.data(), a.ids.p, 8 * n, cudaMemcpyDeviceToHost));
+  for (int64_t k = 0; k < n; ++k) {
+    if (slot_a) slot_a[k] = ids[2 * k];
+    if (slot_b) slot_b[k] = ids[2 * k + 1] & kSlotMask;
+    if (kind) kind[k] = uint8_t(ids[2 * k + 1] >> kKindShift);
+  }
+  if (wild && !which) GF_CHECK(c, cudaMemcpy(wild, a.wild.p, 4 * c->wild_w * n, cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+static int detect_now(Ctx *c, double margin, int64_t *n_out) {
+  c->kt_margin = margin;
+  if (kt_detect_count(c, margin, c->s_kt)) return -1;
+  GF_CHECK(c, cudaStreamSynchronize(c->s_kt));
+  c->acs_next.n = int64_t(reinterpret_cast<Status *>(c->h_status)->acs_total);
+  if (kt_detect_fill(c, c->acs_next, c->s_kt)) return -1;
+  GF_CHECK(c, cudaStreamSynchronize(c->s_kt));
+  if (n_out) *n_out = c->acs_next.n;
+  return 0;
+}
+
+int gf_detect(gf_ctx *ctx, double margin, int64_t *n_out) {
+  CTX_CHECK(ctx);
+  GF_CHECK(c, cudaDeviceSynchronize());
+  if (kt_snapshot(c, c->s_kt)) return -1;
+  return detect_now(c, margin, n_out);
+}
+
+int gf_detect_snapshot(gf_ctx *ctx, int64_t m, const double *centers, const float *radii,
+                       const int64_t *sph_owner, const uint8_t *sph_family, int64_t n_t,
+                       const double *tri_world, const int64_t *tri_owner, const uint8_t *tri_family,
+                       int64_t n_a, const double *ana_world, const uint8_t *ana_kind,
+                       const int64_t *ana_owner, const uint8_t *ana_family, const uint8_t *mask,
+                       double margin, double bin_size, double *grid_out, int64_t *nb_out,
+                       int64_t *n_out) {
+  CTX_CHECK(ctx);
+  c->kt_bin_size = bin_size;
+  GF_CHECK(c, cudaDeviceSynchronize());
+  c->n_sph = m;
+  c->n_tri = n_t;
+  c->n_ana = n_a;
+  std::vector<float> offr(4 * m);
+  for (int64_t i = 0; i < m; ++i) { offr[4 * i] = offr[4 * i + 1] = offr[4 * i + 2] = 0.f; offr[4 * i + 3] = radii[i]; }
+  KtScratch &k = c->kt;
+  if (upload_u32(c, c->sph_owner, sph_owner, m) || upload_raw(c, c->sph_offr, offr.data(), 16 * m) ||
+      upload_raw(c, k.centers, centers, 24 * m) || upload_raw(c, k.sfam, sph_family, m) ||
+      upload_u32(c, c->tri_owner, tri_owner, n_t) || upload_raw(c, k.tri_world, tri_world, 72 * n_t) ||
+      upload_raw(c, k.tfam, tri_family, n_t) || upload_u32(c, c->ana_owner, ana_owner, n_a) ||
+      upload_raw(c, c->ana_kind, ana_kind, n_a) || upload_raw(c, k.ana_world, ana_world, 64 * n_a) ||
+      upload_raw(c, k.afam, ana_family, n_a) || upload_raw(c, c->fam_mask, mask, 65536))
+    return -1;
+  int rc = detect_now(c, margin, n_out);
+  c->kt_bin_size = 0.0;
+  if (rc) return -1;
+  Grid g;
+  GF_CHECK(c, cudaMemcpy(&g, k.grid.p, sizeof(Grid), cudaMemcpyDeviceToHost));
+  if (grid_out) { grid_out[0] = g.glo[0]; grid_out[1] = g.glo[1]; grid_out[2] = g.glo[2]; grid_out[3] = g.inv_bin; }
+  if (nb_out) { nb_out[0] = g.nb[0]; nb_out[1] = g.nb[1]; nb_out[2] = g.nb[2]; }
+  return 0;
+}
+
+int gf_bin_ranges(gf_ctx *ctx, double margin, int64_t *out) {
+  CTX_CHECK(ctx);
+  static_assert(sizeof(long long) == sizeof(int64_t), "int64");
+  return kt_bin_ranges(c, margin, out);
+}
+
+static void pack_ids(int64_t n, const uint8_t *kind, const int64_t *a, const int64_t *b,
+                     std::vector<uint32_t> &ids) {
+  ids.resize(2 * n + 2);
+  for (int64_t k = 0; k < n; ++k) {
+    ids[2 * k] = uint32_t(a[k]);
+    ids[2 * k + 1] = uint32_t(b[k]) | (uint32_t(kind[k]) << kKindShift);
+  }
+}
+
+int gf_merge_history(gf_ctx *ctx, int64_t n_old, const uint8_t *old_kind, const int64_t *old_a,
+                     const int64_t *old_b, const float *old_wild, int64_t n_new,
+                     const uint8_t *new_kind, const int64_t *new_a, const int64_t *new_b, int W,
+                     float *out_wild) {
+  CTX_CHECK(ctx);
+  GF_CHECK(c, cudaDeviceSynchronize());
+  std::vector<uint32_t> oi, ni;
+  pack_ids(n_old, old_kind, old_a, old_b, oi);
+  pack_ids(n_new, new_kind, new_a, new_b, ni);
+  return merge_host(c, n_old, oi.data(), old_wild, n_new, ni.data(), W, out_wild);
+}
+
+int gf_adopt(gf_ctx *ctx) {
+  CTX_CHECK(ctx);
+  GF_CHECK(c, cudaDeviceSynchronize());
+  if (adopt_acs(c, c->s_dt)) return -1;
+  GF_CHECK(c, cudaStreamSynchronize(c->s_dt));
+  return 0;
+}
+
+int gf_dt_step(gf_ctx *ctx, const gf_step_params *p, int64_t *touching, int64_t *bad, int64_t *oob) {
+  CTX_CHECK(ctx);
+  if (reset_status(c, c->s_dt)) return -1;
+  c->n_dyn = 0;
+  StepArgs a{p->h, {p->g[0], p->g[1], p->g[2]}, p->v_err, p->sim_time, p->step, 0, p->write_acc};
+  if (dt_step(c, a)) return -1;
+  Status st;
+  if (read_status(c, c->s_dt, &st)) return -1;
+  int64_t bs, os;
+  if (touching) *touching = int64_t(st.touching);
+  if (bad) decode_err(st.bad, *bad, bs);
+  if (oob) decode_err(st.oob, *oob, os);
+  return 0;
+}
+
+int gf_run(gf_ctx *ctx, const gf_run_params *p, gf_run_result *r) {
+  CTX_CHECK(ctx);
+  auto w0 = std::chrono::steady_clock::now();
+  std::memset(r, 0, sizeof(*r));
+  const int64_t N = p->n_steps;
+  const int period = p->period < 1 ? 1 : p->period;
+  const int lag = p->lag < 0 ? 0 : p->lag;
+  c->kt_margin = p->margin;
+  c->n_dyn = p->n_dyn;
+  if (p->n_dyn > 0) {
+    if (upload_raw(c, c->dyn_spec, p->dyn_spec, sizeof(int32_t) * 3 * p->n_dyn) ||
+        upload_raw(c, c->dyn_vals, p->dyn_vals, sizeof(double) * p->n_dyn * (N > 0 ? N : 1)))
+      return -1;
+  }
+  if (reset_status(c, c->s_dt)) return -1;
+  GF_CHECK(c, cudaStreamSynchronize(c->s_dt));
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kt_ev;
+  GF_CHECK(c, cudaEventRecord(c->t0, c->s_dt));
+  auto do_fill = [&]() -> int {
+    GF_CHECK(c, cudaEventSynchronize(c->ev_count));
+    c->acs_next.n = int64_t(reinterpret_cast<Status *>(c->h_status)->acs_total);
+    if (kt_detect_fill(c, c->acs_next, c->s_kt)) return -1;
+    if (!kt_ev.empty()) GF_CHECK(c, cudaEventRecord(kt_ev.back().second, c->s_kt));
+    GF_CHECK(c, cudaEventRecord(c->ev_ca, c->s_kt));
+    c->fill_done = true;
+    return 0;
+  };
+  auto do_adopt = [&]() -> int {
+    if (!c->fill_done && do_fill()) return -1;
+    GF_CHECK(c, cudaStreamWaitEvent(c->s_dt, c->ev_ca, 0));
+    if (adopt_acs(c, c->s_dt)) return -1;
+    GF_CHECK(c, cudaEventRecord(c->ev_adopted, c->s_dt));
+    c->next_pending = false;
+    c->first_adopt = false;
+    return 0;
+  };
+  for (int64_t i = 0; i < N; ++i) {
+    const int64_t s = p->step0 + i;
+    // 1. a detection due at this step boundary is adopted first
+    if (c->next_pending && s >= c->adopt_at && do_adopt()) return -1;
+    // 2. work order: snapshot on the dT stream, detection on the kT stream
+    if (!c->next_pending && (c->first_adopt || s - c->last_snap >= period)) {
+      if (kt_snapshot(c, c->s_dt)) return -1;
+      GF_CHECK(c, cudaEventRecord(c->ev_snap, c->s_dt));
+      GF_CHECK(c, cudaStreamWaitEvent(c->s_kt, c->ev_snap, 0));
+      GF_CHECK(c, cudaStreamWaitEvent(c->s_kt, c->ev_adopted, 0));
+      cudaEvent_t e0, e1;
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      kt_ev.emplace_back(e0, e1);
+      GF_CHECK(c, cudaEventRecord(e0, c->s_kt));
+      if (kt_detect_count(c, p->margin, c->s_kt)) return -1;
+      GF_CHECK(c, cudaEventRecord(c->ev_count, c->s_kt));
+      c->next_pending = true;
+      c->fill_done = false;
+      c->last_snap = s;
+      // the very first detection is waited for (engine.py:679-682)
+      c->adopt_at = c->first_adopt ? s : s + lag;
+      if (c->adopt_at <= s && do_adopt()) return -1;
+    }
+    // 3. launch the fill as soon as the count is known (no dT stall)
+    if (c->next_pending && !c->fill_done && cudaEventQuery(c->ev_count) == cudaSuccess && do_fill())
+      return -1;
+    StepArgs a{p->h, {p->g[0], p->g[1], p->g[2]}, p->v_err, double(s) * p->h, s, i,
+               (i == N - 1) ? p->write_acc : 0};
+    if (dt_step(c, a)) return -1;
+  }
+  GF_CHECK(c, cudaEventRecord(c->t1, c->s_dt));
+  GF_CHECK(c, cudaStreamSynchronize(c->s_kt));
+  Status st;
+  if (read_status(c, c->s_dt, &st)) return -1;
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, c->t0, c->t1);
+  r->dt_ms = ms;
+  double kt_ms = 0.0;
+  for (auto &e : kt_ev) {
+    float m = 0.f;
+    if (cudaEventElapsedTime(&m, e.first, e.second) == cudaSuccess) kt_ms += m;
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  r->kt_ms = kt_ms;
+  decode_err(st.bad, r->bad_owner, r->bad_step);
+  decode_err(st.oob, r->oob_owner, r->oob_step);
+  int64_t err_step = -1;
+  if (r->bad_step >= 0) err_step = r->bad_step;
+  if (r->oob_step >= 0 && (err_step < 0 || r->oob_step < err_step)) err_step = r->oob_step;
+  r->steps_done = err_step >= 0 ? err_step - p->step0 : N;
+  r->touching = int64_t(st.touching);
+  r->n_acs = c->acs.n;
+  r->ca_updates = c->ca_updates;
+  r->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
+  return 0;
+}
+
+}  // extern "C"

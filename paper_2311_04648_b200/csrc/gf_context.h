@@ -1,0 +1,165 @@
+// gf_context.h -- host-side device context behind the C-ABI (include/gf_b200.h).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "gf_common.cuh"
+
+namespace gf {
+
+// A growable device buffer (stream-ordered allocator; no device-wide syncs).
+struct DBuf {
+  void *p = nullptr;
+  size_t bytes = 0;
+  template <class T> T *as() const { return reinterpret_cast<T *>(p); }
+};
+
+// Active contact set in device layout.  ids.x = sphere slot of A;
+// ids.y = slot of B within its kind | kind << 30.  Canonical order is
+// (kind, a, b), identical to the reference's (kind, geom_a, geom_b) order
+// because slots are monotone in geometry id within each kind
+// (engine.py:446-455).
+struct Acs {
+  int64_t n = 0, cap = 0;
+  DBuf ids;    // uint2[cap]
+  DBuf wild;   // float[cap * W]
+};
+
+struct KtScratch {
+  // snapshot (kT works on a frozen copy; engine.py:577-596)
+  DBuf centers;      // double[n_s*3]
+  DBuf sfam;         // uint8[n_s] sphere family
+  DBuf tri_world;    // double[n_t*9]
+  DBuf ana_world;    // double[n_a*8]
+  DBuf tfam, afam;   // uint8 families of tri / ana
+  DBuf grid;         // Grid
+  DBuf minmax;       // double[6]
+  // binning
+  DBuf bin_key, bin_key_alt, sph_val, sph_val_alt;  // uint32[n_s]
+  DBuf cell_start, cell_end;                         // uint32[nbins]
+  DBuf tri_ranges;                                   // int32[n_t*6]
+  DBuf tri_cnt, tri_start, tri_entries;              // tri CSR over bins
+  DBuf counts;       // uint32[3*n_s+1] per sphere SS / ST / SA counts
+  DBuf offsets;      // uint64? uint32[3*n_s+1] exclusive scan
+  DBuf cub_tmp;
+  DBuf total;        // device copy of totals
+  int64_t nbins_cap = 0;
+};
+
+struct Ctx {
+  int device = 0;
+  uint32_t flags = 0;
+  bool f32_state = false;
+  std::string err;
+  cudaStream_t s_dt = nullptr, s_kt = nullptr;
+  cudaEvent_t ev_snap = nullptr, ev_ca = nullptr, ev_adopted = nullptr, ev_count = nullptr;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+
+  Domain dom{};
+  // owners
+  int64_t n_owner = 0, n_tpl = 0;
+  DBuf voxel, sub, quat, lin_vel, ang_vel, meta, tpl, acc, ext;
+  bool has_ext = false;
+  // geometry
+  int64_t n_sph = 0, n_tri = 0, n_ana = 0;
+  DBuf sph_owner, sph_offr, sph_mat;
+  DBuf tri_owner, tri_local, tri_mat, tri_world;
+  DBuf ana_owner, ana_kind, ana_local, ana_mat, ana_world;
+  bool world_moving = true;  // any tri/ana owner not fixed
+  // tables
+  int n_mat = 0, n_pair_rows = 0;
+  DBuf pair, beta;
+  DBuf fam_mask, fam_flags, lv_mask, av_mask, lv_val, av_val;
+  std::vector<uint8_t> h_fam_flags;
+  // contact arrays
+  int wild_w = 4;
+  Acs acs, acs_next;
+  bool next_pending = false;
+  int64_t next_count = 0;
+  // per-contact outputs and incidence lists (sized with acs.cap)
+  DBuf out_c;      // double[cap*9]: F(3), F+tof(3), contact point(3)
+  DBuf touch;      // uint8[cap]
+  DBuf inc, inc_alt, inc_key, inc_key_alt;  // uint32[2*cap]
+  DBuf inc_start;  // uint32[n_owner+1]
+  DBuf heavy;      // uint32 list of heavy owners
+  DBuf heavy_count;  // unsigned long long
+  DBuf heavy_acc;  // double[n_owner*6]
+  DBuf cub_tmp_dt;
+  // flags / counters (device) and pinned host mirrors
+  DBuf status;     // Status struct
+  void *h_status = nullptr;  // pinned mirror
+  KtScratch kt;
+  // dynamic prescriptions
+  DBuf dyn_spec, dyn_vals;
+  int n_dyn = 0;
+  double kt_margin = 0.0;
+  double kt_bin_size = 0.0;  // > 0: explicit bin size (detect_contacts(bin_size=...))
+  // schedule state (kept across gf_run calls)
+  bool first_adopt = true;     // the first do_dynamics detects and waits (engine.py:679-682)
+  bool fill_done = false;
+  int64_t last_snap = 0;
+  int64_t adopt_at = 0;
+  int64_t step = 0;
+  int64_t ca_updates = 0;
+  double t_kt_ms = 0.0, t_dt_ms = 0.0;
+  int64_t last_touching = 0;
+};
+
+// device status block
+struct Status {
+  unsigned long long bad;    // (step << 40) | owner of first speeding owner, or ~0
+  unsigned long long oob;    // same for out-of-domain
+  unsigned long long touching;
+  unsigned long long acs_total;   // last detection's pair count
+  double oob_pos[3];
+  int err;                   // nonzero once a watchdog tripped (kernels stop)
+  int pad;
+};
+
+constexpr uint32_t kHeavyThreshold = 192;  // incidences above which an owner is block-reduced
+
+// helpers implemented in gf_context.cu
+int ensure(Ctx *c, DBuf &b, size_t bytes, cudaStream_t s, bool keep = false);
+void set_err(Ctx *c, const std::string &msg);
+#define GF_CHECK(c, call)                                                      \
+  do {                                                                         \
+    cudaError_t _e = (call);                                                   \
+    if (_e != cudaSuccess) {                                                   \
+      gf::set_err((c), std::string(#call) + ": " + cudaGetErrorString(_e));    \
+      return -1;                                                               \
+    }                                                                          \
+  } while (0)
+
+// views
+Owners owners_view(Ctx *c);
+Spheres spheres_view(Ctx *c);
+Tris tris_view(Ctx *c);
+Anas anas_view(Ctx *c);
+Materials materials_view(Ctx *c);
+Families families_view(Ctx *c);
+
+// kT (gf_kt.cu)
+int kt_snapshot(Ctx *c, cudaStream_t s);                 // centers/families -> kT scratch
+int kt_detect_count(Ctx *c, double margin, cudaStream_t s);
+int kt_detect_fill(Ctx *c, Acs &out, cudaStream_t s);
+int kt_bin_ranges(Ctx *c, double margin, int64_t *h_out);
+int adopt_acs(Ctx *c, cudaStream_t s);                   // merge history + incidence lists
+int build_incidence(Ctx *c, cudaStream_t s);
+int merge_host(Ctx *c, int64_t n_old, const uint32_t *old_ids, const float *old_wild, int64_t n_new,
+               const uint32_t *new_ids, int W, float *out_wild);
+int refresh_world(Ctx *c, cudaStream_t s);               // tri/ana world from owner pose
+
+// dT (gf_dt_f64.cu / gf_dt_f32.cu)
+struct StepArgs {
+  double h, g[3], v_err, sim_time;
+  int64_t step;          // global step index (for watchdog records)
+  int64_t dyn_row;       // row of the dynamic-prescription table for this step
+  int write_acc;         // store per-owner accumulators this step
+};
+int dt_step_f64(Ctx *c, const StepArgs &a, cudaStream_t s);
+int dt_step_f32(Ctx *c, const StepArgs &a, cudaStream_t s);
+
+}  // namespace gf

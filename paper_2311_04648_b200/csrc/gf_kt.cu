@@ -1,0 +1,733 @@
+// gf_kt.cu -- kinematics worker (kT): snapshot, uniform grid, binning,
+// sphere-sphere / sphere-triangle / sphere-analytic pair generation in
+// canonical order, and the kT -> dT handoff (history remap + incidence lists).
+//
+// Compiled with -fmad=false: pair predicates are evaluated with the exact
+// fp64 arithmetic of the reference so the produced pair lists are
+// bit-identical to broadphase.detect_contacts (broadphase.py:202-288).
+//
+// Binning scheme (B200-native, not the reference's): every sphere is
+// registered once, in the bin holding its centre (one radix-sort key per
+// sphere instead of the reference's up-to-8 registrations, _kernels.py:269);
+// candidates come from the 27-bin neighbourhood.  The reference reports a pair
+// iff it passes the distance test AND the bin of the min corner of the two
+// enlarged boxes' intersection lies in both spheres' registration ranges
+// (_kernels.py:317-321); that exact predicate is evaluated per candidate, so
+// the pair SET is the reference's.  A thread owns sphere i and emits the pairs
+// (i, j > i), sorted by j, at an exclusive-scan offset: the output is already
+// in canonical (kind, a, b) order and no global pair sort is needed.
+#include <cub/cub.cuh>
+
+#include "gf_context.h"
+
+namespace gf {
+
+namespace {
+
+constexpr int kBlock = 256;
+
+inline unsigned grid_for(int64_t n, int block = kBlock) {
+  int64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  return unsigned(g);
+}
+
+// order-preserving double <-> uint64 for exact atomic min/max
+__device__ __forceinline__ unsigned long long ord_key(double x) {
+  unsigned long long u = __double_as_longlong(x);
+  return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double ord_val(unsigned long long k) {
+  unsigned long long u = (k & 0x8000000000000000ull) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+  return __longlong_as_double(u);
+}
+
+struct KtView {
+  Domain dom;
+  Owners own;
+  Spheres sph;
+  int64_t n_tri, n_ana;
+  const uint32_t *tri_owner;
+  const uint32_t *ana_owner;
+  const uint8_t *ana_kind;
+  const double *centers;   // snapshot centres [n_s*3]
+  const uint8_t *sfam;
+  const double *tri_world;
+  const uint8_t *tfam;
+  const double *ana_world;
+  const uint8_t *afam;
+  const uint8_t *mask;
+  const uint32_t *bin_key;   // sorted centre-bin keys
+  const uint32_t *sph_sorted;
+  const uint32_t *cell_start, *cell_end;
+  const uint32_t *tri_start, *tri_entries;
+  const Grid *grid;
+  double margin;
+};
+
+// ---------------------------------------------------------------------------
+// snapshot
+// ---------------------------------------------------------------------------
+__global__ void k_snapshot(Domain dom, Owners own, Spheres sph, double *centers, uint8_t *sfam) {
+  int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (k >= sph.n) return;
+  double c[3];
+  float r;
+  uint32_t o;
+  sphere_center(dom, own, sph, uint32_t(k), c, r, o);
+  centers[3 * k] = c[0];
+  centers[3 * k + 1] = c[1];
+  centers[3 * k + 2] = c[2];
+  sfam[k] = uint8_t(meta_family(own.meta[o]));
+}
+
+__global__ void k_geom_family(int64_t n, const uint32_t *owner, const uint32_t *meta, uint8_t *fam) {
+  int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (k < n) fam[k] = uint8_t(meta_family(meta[owner[k]]));
+}
+
+// ---------------------------------------------------------------------------
+// grid (broadphase.py:160-186)
+// ---------------------------------------------------------------------------
+// mm[0..2] = min xyz, mm[3..5] = max xyz (ordered keys), mm[6] = max radius
+__global__ void k_minmax_init(unsigned long long *mm) {
+  if (threadIdx.x < 3) {
+    mm[threadIdx.x] = ord_key(__longlong_as_double(0x7FF0000000000000ll));        // +inf
+    mm[3 + threadIdx.x] = ord_key(__longlong_as_double(0xFFF0000000000000ull));   // -inf
+  }
+  if (threadIdx.x == 3) mm[6] = ord_key(0.0);
+}
+
+__global__ void k_minmax(int64_t n_pts, const double *pts, int64_t n_s, const float4 *offr,
+                         unsigned long long *mm) {
+  double lo[3] = {__longlong_as_double(0x7FF0000000000000ll), 0, 0};
+  lo[1] = lo[0]; lo[2] = lo[0];
+  double hi[3] = {-lo[0], -lo[0], -lo[0]};
+  double rmax = 0.0;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n_pts;
+       i += int64_t(gridDim.x) * blockDim.x) {
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      double v = pts[3 * i + ax];
+      lo[ax] = fmin(lo[ax], v);
+      hi[ax] = fmax(hi[ax], v);
+    }
+  }
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n_s;
+       i += int64_t(gridDim.x) * blockDim.x)
+    rmax = fmax(rmax, double(offr[i].w));
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      lo[ax] = fmin(lo[ax], __shfl_down_sync(0xffffffff, lo[ax], off));
+      hi[ax] = fmax(hi[ax], __shfl_down_sync(0xffffffff, hi[ax], off));
+    }
+    rmax = fmax(rmax, __shfl_down_sync(0xffffffff, rmax, off));
+  }
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      atomicMin(&mm[ax], ord_key(lo[ax]));
+      atomicMax(&mm[3 + ax], ord_key(hi[ax]));
+    }
+    atomicMax(&mm[6], ord_key(rmax));
+  }
+}
+
+// single thread: exact restatement of _grid_for's scalar arithmetic
+__global__ void k_grid(const unsigned long long *mm, int64_t n_pts, double margin, double bin_override,
+                       Grid *g) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  Grid out;
+  out.valid = n_pts > 0;
+  double r_max = ord_val(mm[6]);
+  double bin_size = bin_override > 0.0 ? bin_override : mul(2.0, add(r_max, margin));
+  if (bin_size <= 0.0) bin_size = 1.0;
+  double ext[3];
+  for (int ax = 0; ax < 3; ++ax) {
+    double mn = ord_val(mm[ax]), mx = ord_val(mm[3 + ax]);
+    out.glo[ax] = sub_(sub_(mn, add(r_max, margin)), 1e-9);
+    double ghi = add(add(mx, add(r_max, margin)), 1e-9);
+    ext[ax] = sub_(ghi, out.glo[ax]);
+  }
+  for (;;) {
+    for (int ax = 0; ax < 3; ++ax) {
+      double cc = ceil(ext[ax] / bin_size);
+      out.nb[ax] = cc < 1.0 ? 1 : (long long)cc;
+    }
+    if (out.nb[0] * out.nb[1] * out.nb[2] <= (long long)kMaxBins) break;
+    bin_size = mul(bin_size, 1.5);
+  }
+  out.inv_bin = 1.0 / bin_size;
+  if (!out.valid) { out.nb[0] = out.nb[1] = out.nb[2] = 1; }
+  *g = out;
+}
+
+// ---------------------------------------------------------------------------
+// binning
+// ---------------------------------------------------------------------------
+__global__ void k_bin_keys(int64_t n, const double *centers, const Grid *gp, uint32_t *key,
+                           uint32_t *val) {
+  int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  Grid g = *gp;
+  long long ix = axis_bin(centers[3 * i], g.glo[0], g.inv_bin, g.nb[0]);
+  long long iy = axis_bin(centers[3 * i + 1], g.glo[1], g.inv_bin, g.nb[1]);
+  long long iz = axis_bin(centers[3 * i + 2], g.glo[2], g.inv_bin, g.nb[2]);
+  key[i] = uint32_t((iz * g.nb[1] + iy) * g.nb[0] + ix);
+  val[i] = uint32_t(i);
+}
+
+__global__ void k_cell_bounds(int64_t n, const uint32_t *key, uint32_t *start, uint32_t *end) {
+  int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  uint32_t k = key[i];
+  if (i == 0 || key[i - 1] != k) start[k] = uint32_t(i);
+  if (i == n - 1 || key[i + 1] != k) end[k] = uint32_t(i + 1);
+}
+
+// triangle registration ranges (_kernels.py:333-351) and CSR over bins
+__global__ void k_tri_ranges(int64_t n_t, const double *tri, const Grid *gp, double margin,
+                             int *ranges, uint32_t *cnt) {
+  int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (t >= n_t) return;
+  Grid g = *gp;
+  int r[6];
+  for (int ax = 0; ax < 3; ++ax) {
+    double lo = tri[9 * t + ax], hi = tri[9 * t + ax];
+    for (int v = 1; v < 3; ++v) {
+      double x = tri[9 * t + 3 * v + ax];
+      if (x < lo) lo = x;
+      if (x > hi) hi = x;
+    }
+    long long l = (long long)mul(sub_(sub_(lo, margin), g.glo[ax]), g.inv_bin);
+    long long h = (long long)mul(sub_(add(hi, margin), g.glo[ax]), g.inv_bin);
+    if (l < 0) l = 0;
+    if (h < 0) h = 0;
+    if (l >= g.nb[ax]) l = g.nb[ax] - 1;
+    if (h >= g.nb[ax]) h = g.nb[ax] - 1;
+    r[2 * ax] = int(l);
+    r[2 * ax + 1] = int(h);
+  }
+  for (int q = 0; q < 6; ++q) ranges[6 * t + q] = r[q];
+  for (int iz = r[4]; iz <= r[5]; ++iz)
+    for (int iy = r[2]; iy <= r[3]; ++iy)
+      for (int ix = r[0]; ix <= r[1]; ++ix)
+        atomicAdd(&cnt[(int64_t(iz) * g.nb[1] + iy) * g.nb[0] + ix], 1u);
+}
+
+// fill: tris listed per bin in ascending order (one thread per bin walks the
+// triangle list; triangle counts are small, so a bin-parallel scan is fine)
+__global__ void k_tri_fill(int64_t n_t, const int *ranges, const Grid *gp, const uint32_t *start,
+                           uint32_t *fillc, uint32_t *entries) {
+  // serial-in-t per bin keeps ascending triangle order within each bin
+  int64_t b = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  Grid g = *gp;
+  int64_t nbins = g.nb[0] * g.nb[1] * g.nb[2];
+  if (b >= nbins) return;
+  uint32_t s0 = start[b], s1 = start[b + 1];
+  if (s0 == s1) return;
+  long long ix = b % g.nb[0], iy = (b / g.nb[0]) % g.nb[1], iz = b / (g.nb[0] * g.nb[1]);
+  uint32_t w = s0;
+  for (int64_t t = 0; t < n_t && w < s1; ++t) {
+    const int *r = ranges + 6 * t;
+    if (ix >= r[0] && ix <= r[1] && iy >= r[2] && iy <= r[3] && iz >= r[4] && iz <= r[5])
+      entries[w++] = uint32_t(t);
+  }
+  (void)fillc;
+}
+
+// ---------------------------------------------------------------------------
+// pair predicates (exact reference arithmetic)
+// ---------------------------------------------------------------------------
+
+// collect_sphere_pairs predicate for i < j (_kernels.py:305-321)
+__device__ __forceinline__ bool ss_pair(const KtView &v, const Grid &g, uint32_t i, uint32_t j,
+                                        const double ci[3], float ri_f, const long long lo_i[3],
+                                        const long long hi_i[3], uint32_t oi, uint8_t fi) {
+  uint32_t oj = v.sph.owner[j];
+  if (oi == oj) return false;
+  if (!v.mask[256 * fi + v.sfam[j]]) return false;
+  const double *cj = v.centers + 3 * size_t(j);
+  double dx = sub_(ci[0], cj[0]), dy = sub_(ci[1], cj[1]), dz = sub_(ci[2], cj[2]);
+  float rj_f = v.sph.offr[j].w;
+  double ri = add(double(ri_f), v.margin);
+  double rj = add(double(rj_f), v.margin);
+  double rr = sub_(add(ri, rj), v.margin);
+  if (add(add(mul(dx, dx), mul(dy, dy)), mul(dz, dz)) >= mul(rr, rr)) return false;
+  double cjv[3] = {cj[0], cj[1], cj[2]};
+  long long lo_j[3], hi_j[3];
+  sphere_range(g, cjv, rj_f, v.margin, lo_j, hi_j);
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    double m = fmax(sub_(ci[ax], ri), sub_(cj[ax], rj));
+    long long b = axis_bin(m, g.glo[ax], g.inv_bin, g.nb[ax]);
+    if (b < lo_i[ax] || b > hi_i[ax] || b < lo_j[ax] || b > hi_j[ax]) return false;
+  }
+  return true;
+}
+
+// collect_sphere_tri_pairs predicate evaluated in bin (bx, by, bz)
+// (_kernels.py:375-401)
+__device__ __forceinline__ bool st_pair(const KtView &v, const Grid &g, uint32_t t,
+                                        const double ci[3], float ri_f, uint32_t oi, uint8_t fi,
+                                        long long bx, long long by, long long bz) {
+  if (oi == v.tri_owner[t]) return false;
+  if (!v.mask[256 * fi + v.tfam[t]]) return false;
+  const double *T = v.tri_world + 9 * size_t(t);
+  double qx, qy, qz;
+  closest_on_tri(ci[0], ci[1], ci[2], T, qx, qy, qz);
+  double dx = sub_(ci[0], qx), dy = sub_(ci[1], qy), dz = sub_(ci[2], qz);
+  double rr = add(double(ri_f), v.margin);
+  if (add(add(mul(dx, dx), mul(dy, dy)), mul(dz, dz)) >= mul(rr, rr)) return false;
+  double mx = sub_(ci[0], rr), my = sub_(ci[1], rr), mz = sub_(ci[2], rr);
+  double tlx = sub_(fmin(fmin(T[0], T[3]), T[6]), v.margin);
+  double tly = sub_(fmin(fmin(T[1], T[4]), T[7]), v.margin);
+  double tlz = sub_(fmin(fmin(T[2], T[5]), T[8]), v.margin);
+  if (tlx > mx) mx = tlx;
+  if (tly > my) my = tly;
+  if (tlz > mz) mz = tlz;
+  return axis_bin(mx, g.glo[0], g.inv_bin, g.nb[0]) == bx &&
+         axis_bin(my, g.glo[1], g.inv_bin, g.nb[1]) == by &&
+         axis_bin(mz, g.glo[2], g.inv_bin, g.nb[2]) == bz;
+}
+
+// collect_sphere_analytic_pairs predicate (_kernels.py:418-428)
+__device__ __forceinline__ bool sa_pair(const KtView &v, uint32_t k, const double ci[3],
+                                        float ri_f, uint32_t oi, uint8_t fi) {
+  if (oi == v.ana_owner[k]) return false;
+  if (!v.mask[256 * fi + v.afam[k]]) return false;
+  double gap, bx, by, bz, rb;
+  analytic_gap(v.ana_kind[k], v.ana_world + 8 * size_t(k), ci[0], ci[1], ci[2], gap, bx, by, bz, rb);
+  return !(gap >= add(double(ri_f), v.margin));
+}
+
+// one thread per sphere i: count (FILL=false) or emit (FILL=true) its pairs
+template <bool FILL>
+__global__ void __launch_bounds__(128) k_pairs(KtView v, unsigned long long *counts,
+                                               const unsigned long long *offsets, uint2 *out) {
+  int64_t i64 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  int64_t n = v.sph.n;
+  if (i64 >= n) return;
+  const Grid g = *v.grid;
+  if (!g.valid) {
+    if (!FILL) { counts[i64] = 0; counts[n + i64] = 0; counts[2 * n + i64] = 0; }
+    return;
+  }
+  uint32_t i = uint32_t(i64);
+  double ci[3] = {v.centers[3 * i64], v.centers[3 * i64 + 1], v.centers[3 * i64 + 2]};
+  float ri_f = v.sph.offr[i].w;
+  uint32_t oi = v.sph.owner[i];
+  uint8_t fi = v.sfam[i];
+  long long lo_i[3], hi_i[3];
+  sphere_range(g, ci, ri_f, v.margin, lo_i, hi_i);
+  long long cb[3];
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) cb[ax] = axis_bin(ci[ax], g.glo[ax], g.inv_bin, g.nb[ax]);
+
+  // --- sphere-sphere ---
+  unsigned long long cnt = 0;
+  unsigned long long w = FILL ? offsets[i64] : 0;
+  for (long long z = cb[2] - 1; z <= cb[2] + 1; ++z) {
+    if (z < 0 || z >= g.nb[2]) continue;
+    for (long long y = cb[1] - 1; y <= cb[1] + 1; ++y) {
+      if (y < 0 || y >= g.nb[1]) continue;
+      for (long long x = cb[0] - 1; x <= cb[0] + 1; ++x) {
+        if (x < 0 || x >= g.nb[0]) continue;
+        uint32_t b = uint32_t((z * g.nb[1] + y) * g.nb[0] + x);
+        uint32_t s0 = v.cell_start[b];
+        if (s0 == 0xFFFFFFFFu) continue;
+        uint32_t s1 = v.cell_end[b];
+        for (uint32_t u = s0; u < s1; ++u) {
+          uint32_t j = v.sph_sorted[u];
+          if (j <= i) continue;
+          if (ss_pair(v, g, i, j, ci, ri_f, lo_i, hi_i, oi, fi)) {
+            if (FILL) out[w + cnt] = make_uint2(i, j);
+            ++cnt;
+          }
+        }
+      }
+    }
+  }
+  if (FILL && cnt > 1) {  // canonical order within the segment: ascending j
+    for (unsigned long long p = 1; p < cnt; ++p) {
+      uint2 e = out[w + p];
+      unsigned long long q = p;
+      while (q > 0 && out[w + q - 1].y > e.y) { out[w + q] = out[w + q - 1]; --q; }
+      out[w + q] = e;
+    }
+  }
+  if (!FILL) counts[i64] = cnt;
+
+  // --- sphere-triangle: iterate the sphere's own registration bins ---
+  unsigned long long cst = 0;
+  if (v.n_tri) {
+    unsigned long long wt = FILL ? offsets[n + i64] : 0;
+    for (long long z = lo_i[2]; z <= hi_i[2]; ++z)
+      for (long long y = lo_i[1]; y <= hi_i[1]; ++y)
+        for (long long x = lo_i[0]; x <= hi_i[0]; ++x) {
+          int64_t b = (z * g.nb[1] + y) * g.nb[0] + x;
+          for (uint32_t u = v.tri_start[b]; u < v.tri_start[b + 1]; ++u) {
+            uint32_t t = v.tri_entries[u];
+            if (st_pair(v, g, t, ci, ri_f, oi, fi, x, y, z)) {
+              if (FILL) out[wt + cst] = make_uint2(i, t | (1u << kKindShift));
+              ++cst;
+            }
+          }
+        }
+    if (FILL && cst > 1) {
+      for (unsigned long long p = 1; p < cst; ++p) {
+        uint2 e = out[wt + p];
+        unsigned long long q = p;
+        while (q > 0 && out[wt + q - 1].y > e.y) { out[wt + q] = out[wt + q - 1]; --q; }
+        out[wt + q] = e;
+      }
+    }
+  }
+  if (!FILL) counts[n + i64] = cst;
+
+  // --- sphere-analytic (brute force over the small analytic list) ---
+  unsigned long long csa = 0;
+  unsigned long long wa = FILL ? offsets[2 * n + i64] : 0;
+  for (int64_t k = 0; k < v.n_ana; ++k) {
+    if (sa_pair(v, uint32_t(k), ci, ri_f, oi, fi)) {
+      if (FILL) out[wa + csa] = make_uint2(i, uint32_t(k) | (2u << kKindShift));
+      ++csa;
+    }
+  }
+  if (!FILL) counts[2 * n + i64] = csa;
+}
+
+__global__ void k_bin_ranges(int64_t n, const double *centers, const float4 *offr, const Grid *gp,
+                             double margin, long long *out) {
+  int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  Grid g = *gp;
+  double c[3] = {centers[3 * i], centers[3 * i + 1], centers[3 * i + 2]};
+  long long lo[3], hi[3];
+  sphere_range(g, c, offr[i].w, margin, lo, hi);
+  for (int ax = 0; ax < 3; ++ax) {
+    out[6 * i + 2 * ax] = lo[ax];
+    out[6 * i + 2 * ax + 1] = hi[ax];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// handoff: history remap (broadphase.py:110-135) + incidence lists
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long acs_key(uint2 id) {
+  return (static_cast<unsigned long long>(id.y >> kKindShift) << 62) |
+         (static_cast<unsigned long long>(id.x) << 31) |
+         static_cast<unsigned long long>(id.y & kSlotMask);
+}
+
+__global__ void k_merge(int64_t n_new, const uint2 *new_ids, float *new_wild, int64_t n_old,
+                        const uint2 *old_ids, const float *old_wild, int W) {
+  int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (k >= n_new) return;
+  unsigned long long key = acs_key(new_ids[k]);
+  int64_t lo = 0, hi = n_old;  // lower_bound
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (acs_key(old_ids[mid]) < key) lo = mid + 1; else hi = mid;
+  }
+  bool hit = lo < n_old && acs_key(old_ids[lo]) == key;
+  for (int q = 0; q < W; ++q) new_wild[int64_t(W) * k + q] = hit ? old_wild[int64_t(W) * lo + q] : 0.0f;
+}
+
+__global__ void k_inc_keys(int64_t n, const uint2 *ids, const uint32_t *sph_owner,
+                           const uint32_t *tri_owner, const uint32_t *ana_owner, uint32_t *key,
+                           uint32_t *val) {
+  int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (k >= n) return;
+  uint2 id = ids[k];
+  uint32_t kind = id.y >> kKindShift, sb = id.y & kSlotMask;
+  uint32_t ob = kind == 0 ? sph_owner[sb] : (kind == 1 ? tri_owner[sb] : ana_owner[sb]);
+  key[2 * k] = sph_owner[id.x];
+  val[2 * k] = uint32_t(k) << 1;
+  key[2 * k + 1] = ob;
+  val[2 * k + 1] = (uint32_t(k) << 1) | 1u;
+}
+
+__global__ void k_inc_start(int64_t n_owner, int64_t n_inc, const uint32_t *sorted_key,
+                            uint32_t *start, uint32_t *heavy, unsigned long long *n_heavy,
+                            uint32_t heavy_threshold) {
+  int64_t o = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (o > n_owner) return;
+  int64_t lo = 0, hi = n_inc;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (sorted_key[mid] < uint32_t(o)) lo = mid + 1; else hi = mid;
+  }
+  start[o] = uint32_t(lo);
+  if (o < n_owner) {
+    int64_t lo2 = lo, hi2 = n_inc;
+    while (lo2 < hi2) {
+      int64_t mid = (lo2 + hi2) >> 1;
+      if (sorted_key[mid] <= uint32_t(o)) lo2 = mid + 1; else hi2 = mid;
+    }
+    if (uint32_t(lo2 - lo) > heavy_threshold) {
+      unsigned long long slot = atomicAdd(n_heavy, 1ull);
+      heavy[slot] = uint32_t(o);
+    }
+  }
+}
+
+}  // namespace
+
+// ===========================================================================
+// host entry points
+// ===========================================================================
+
+int kt_snapshot(Ctx *c, cudaStream_t s) {
+  KtScratch &k = c->kt;
+  if (ensure(c, k.centers, sizeof(double) * 3 * (c->n_sph + 1), s)) return -1;
+  if (ensure(c, k.sfam, c->n_sph + 1, s)) return -1;
+  if (ensure(c, k.tri_world, sizeof(double) * 9 * (c->n_tri + 1), s)) return -1;
+  if (ensure(c, k.ana_world, sizeof(double) * 8 * (c->n_ana + 1), s)) return -1;
+  if (ensure(c, k.tfam, c->n_tri + 1, s)) return -1;
+  if (ensure(c, k.afam, c->n_ana + 1, s)) return -1;
+  if (c->n_sph)
+    k_snapshot<<<grid_for(c->n_sph), kBlock, 0, s>>>(c->dom, owners_view(c), spheres_view(c),
+                                                   k.centers.as<double>(), k.sfam.as<uint8_t>());
+  if (c->n_tri) {
+    GF_CHECK(c, cudaMemcpyAsync(k.tri_world.p, c->tri_world.p, sizeof(double) * 9 * c->n_tri,
+                                cudaMemcpyDeviceToDevice, s));
+    k_geom_family<<<grid_for(c->n_tri), kBlock, 0, s>>>(c->n_tri, c->tri_owner.as<uint32_t>(),
+                                                       c->meta.as<uint32_t>(), k.tfam.as<uint8_t>());
+  }
+  if (c->n_ana) {
+    GF_CHECK(c, cudaMemcpyAsync(k.ana_world.p, c->ana_world.p, sizeof(double) * 8 * c->n_ana,
+                                cudaMemcpyDeviceToDevice, s));
+    k_geom_family<<<grid_for(c->n_ana), kBlock, 0, s>>>(c->n_ana, c->ana_owner.as<uint32_t>(),
+                                                       c->meta.as<uint32_t>(), k.afam.as<uint8_t>());
+  }
+  GF_CHECK(c, cudaGetLastError());
+  return 0;
+}
+
+static KtView kt_view(Ctx *c, double margin) {
+  KtScratch &k = c->kt;
+  KtView v;
+  v.dom = c->dom;
+  v.own = owners_view(c);
+  v.sph = spheres_view(c);
+  v.n_tri = c->n_tri;
+  v.n_ana = c->n_ana;
+  v.tri_owner = c->tri_owner.as<uint32_t>();
+  v.ana_owner = c->ana_owner.as<uint32_t>();
+  v.ana_kind = c->ana_kind.as<uint8_t>();
+  v.centers = k.centers.as<double>();
+  v.sfam = k.sfam.as<uint8_t>();
+  v.tri_world = k.tri_world.as<double>();
+  v.tfam = k.tfam.as<uint8_t>();
+  v.ana_world = k.ana_world.as<double>();
+  v.afam = k.afam.as<uint8_t>();
+  v.mask = c->fam_mask.as<uint8_t>();
+  v.bin_key = k.bin_key.as<uint32_t>();
+  v.sph_sorted = k.sph_val.as<uint32_t>();
+  v.cell_start = k.cell_start.as<uint32_t>();
+  v.cell_end = k.cell_end.as<uint32_t>();
+  v.tri_start = k.tri_start.as<uint32_t>();
+  v.tri_entries = k.tri_entries.as<uint32_t>();
+  v.grid = k.grid.as<Grid>();
+  v.margin = margin;
+  return v;
+}
+
+// grid + binning + per-sphere counts + scan; total -> status.acs_total
+int kt_detect_count(Ctx *c, double margin, cudaStream_t s) {
+  KtScratch &k = c->kt;
+  const int64_t n = c->n_sph, nt = c->n_tri;
+  const int64_t n_pts = n + 3 * nt;
+  if (ensure(c, k.grid, sizeof(Grid), s)) return -1;
+  if (ensure(c, k.minmax, sizeof(unsigned long long) * 8, s)) return -1;
+  if (ensure(c, k.bin_key, 4 * (n + 1), s) || ensure(c, k.bin_key_alt, 4 * (n + 1), s) ||
+      ensure(c, k.sph_val, 4 * (n + 1), s) || ensure(c, k.sph_val_alt, 4 * (n + 1), s))
+    return -1;
+  if (ensure(c, k.cell_start, sizeof(uint32_t) * kMaxBins, s) ||
+      ensure(c, k.cell_end, sizeof(uint32_t) * kMaxBins, s))
+    return -1;
+  if (ensure(c, k.counts, sizeof(unsigned long long) * (3 * n + 1), s) ||
+      ensure(c, k.offsets, sizeof(unsigned long long) * (3 * n + 1), s))
+    return -1;
+  // min/max over centres and triangle vertices (exact), r_max
+  unsigned long long *mm = k.minmax.as<unsigned long long>();
+  k_minmax_init<<<1, 32, 0, s>>>(mm);
+  if (n) k_minmax<<<std::min<int64_t>(grid_for(n), 1184), kBlock, 0, s>>>(n, k.centers.as<double>(), n, c->sph_offr.as<float4>(), mm);
+  if (nt) k_minmax<<<std::min<int64_t>(grid_for(3 * nt), 1184), kBlock, 0, s>>>(3 * nt, k.tri_world.as<double>(), 0, nullptr, mm);
+  k_grid<<<1, 1, 0, s>>>(mm, n_pts, margin, c->kt_bin_size, k.grid.as<Grid>());
+  if (n) {
+    k_bin_keys<<<grid_for(n), kBlock, 0, s>>>(n, k.centers.as<double>(), k.grid.as<Grid>(),
+                                             k.bin_key.as<uint32_t>(), k.sph_val.as<uint32_t>());
+    size_t tmp = 0;
+    cub::DoubleBuffer<uint32_t> dk(k.bin_key.as<uint32_t>(), k.bin_key_alt.as<uint32_t>());
+    cub::DoubleBuffer<uint32_t> dv(k.sph_val.as<uint32_t>(), k.sph_val_alt.as<uint32_t>());
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, int(n), 0, 22, s);
+    if (ensure(c, k.cub_tmp, tmp + 16, s)) return -1;
+    GF_CHECK(c, cub::DeviceRadixSort::SortPairs(k.cub_tmp.p, tmp, dk, dv, int(n), 0, 22, s));
+    if (dk.Current() != k.bin_key.as<uint32_t>()) {
+      std::swap(k.bin_key, k.bin_key_alt);
+      std::swap(k.sph_val, k.sph_val_alt);
+    }
+    GF_CHECK(c, cudaMemsetAsync(k.cell_start.p, 0xFF, sizeof(uint32_t) * kMaxBins, s));
+    k_cell_bounds<<<grid_for(n), kBlock, 0, s>>>(n, k.bin_key.as<uint32_t>(),
+                                                k.cell_start.as<uint32_t>(), k.cell_end.as<uint32_t>());
+  }
+  if (nt) {
+    if (ensure(c, k.tri_ranges, sizeof(int) * 6 * nt, s) ||
+        ensure(c, k.tri_cnt, sizeof(uint32_t) * (kMaxBins + 1), s) ||
+        ensure(c, k.tri_start, sizeof(uint32_t) * (kMaxBins + 1), s))
+      return -1;
+    GF_CHECK(c, cudaMemsetAsync(k.tri_cnt.p, 0, sizeof(uint32_t) * (kMaxBins + 1), s));
+    k_tri_ranges<<<grid_for(nt), kBlock, 0, s>>>(nt, k.tri_world.as<double>(), k.grid.as<Grid>(),
+                                                margin, k.tri_ranges.as<int>(), k.tri_cnt.as<uint32_t>());
+    size_t tmp = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp, k.tri_cnt.as<uint32_t>(), k.tri_start.as<uint32_t>(),
+                                  kMaxBins + 1, s);
+    if (ensure(c, k.cub_tmp, tmp + 16, s, false)) return -1;
+    GF_CHECK(c, cub::DeviceScan::ExclusiveSum(k.cub_tmp.p, tmp, k.tri_cnt.as<uint32_t>(),
+                                              k.tri_start.as<uint32_t>(), kMaxBins + 1, s));
+    // total registrations are bounded by n_t * (bins a triangle spans); size
+    // conservatively from the count array's last prefix after a small sync
+    uint32_t h_total = 0;
+    GF_CHECK(c, cudaMemcpyAsync(&h_total, k.tri_start.as<uint32_t>() + kMaxBins, 4,
+                                cudaMemcpyDeviceToHost, s));
+    GF_CHECK(c, cudaStreamSynchronize(s));
+    if (ensure(c, k.tri_entries, sizeof(uint32_t) * (h_total + 1), s)) return -1;
+    k_tri_fill<<<grid_for(kMaxBins), kBlock, 0, s>>>(nt, k.tri_ranges.as<int>(), k.grid.as<Grid>(),
+                                                    k.tri_start.as<uint32_t>(), nullptr,
+                                                    k.tri_entries.as<uint32_t>());
+  }
+  KtView v = kt_view(c, margin);
+  unsigned long long *cnt = k.counts.as<unsigned long long>();
+  if (n) k_pairs<false><<<grid_for(n, 128), 128, 0, s>>>(v, cnt, nullptr, nullptr);
+  GF_CHECK(c, cudaMemsetAsync(cnt + 3 * n, 0, sizeof(unsigned long long), s));
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, k.offsets.as<unsigned long long>(), int(3 * n + 1), s);
+  if (ensure(c, k.cub_tmp, tmp + 16, s, false)) return -1;
+  GF_CHECK(c, cub::DeviceScan::ExclusiveSum(k.cub_tmp.p, tmp, cnt, k.offsets.as<unsigned long long>(),
+                                            int(3 * n + 1), s));
+  // total -> status block -> pinned mirror
+  Status *st = c->status.as<Status>();
+  GF_CHECK(c, cudaMemcpyAsync(&st->acs_total, k.offsets.as<unsigned long long>() + 3 * n,
+                              sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
+  GF_CHECK(c, cudaMemcpyAsync(&reinterpret_cast<Status *>(c->h_status)->acs_total, &st->acs_total,
+                              sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  GF_CHECK(c, cudaGetLastError());
+  return 0;
+}
+
+int kt_detect_fill(Ctx *c, Acs &out, cudaStream_t s) {
+  KtScratch &k = c->kt;
+  const int64_t n = c->n_sph;
+  const int64_t total = out.n;
+  if (total > out.cap) {
+    int64_t cap = total + total / 2 + 1024;
+    if (ensure(c, out.ids, sizeof(uint2) * cap, s) ||
+        ensure(c, out.wild, sizeof(float) * c->wild_w * cap, s))
+      return -1;
+    out.cap = cap;
+  }
+  if (n && total) {
+    KtView v = kt_view(c, 0.0);
+    // margin is baked into the count pass only through the grid; re-read it
+    v.margin = c->kt_margin;
+    k_pairs<true><<<grid_for(n, 128), 128, 0, s>>>(v, nullptr, k.offsets.as<unsigned long long>(),
+                                                   out.ids.as<uint2>());
+  }
+  GF_CHECK(c, cudaGetLastError());
+  return 0;
+}
+
+int kt_bin_ranges(Ctx *c, double margin, int64_t *h_out) {
+  cudaStream_t s = c->s_kt;
+  const int64_t n = c->n_sph;
+  DBuf tmp;
+  if (ensure(c, tmp, sizeof(long long) * 6 * (n + 1), s)) return -1;
+  k_bin_ranges<<<grid_for(n), kBlock, 0, s>>>(n, c->kt.centers.as<double>(), c->sph_offr.as<float4>(),
+                                              c->kt.grid.as<Grid>(), margin, tmp.as<long long>());
+  GF_CHECK(c, cudaMemcpyAsync(h_out, tmp.p, sizeof(long long) * 6 * n, cudaMemcpyDeviceToHost, s));
+  GF_CHECK(c, cudaStreamSynchronize(s));
+  cudaFree(tmp.p);
+  return 0;
+}
+
+// adopt acs_next: remap history from acs, swap, rebuild incidence lists
+int adopt_acs(Ctx *c, cudaStream_t s) {
+  Acs &nw = c->acs_next;
+  Acs &old = c->acs;
+  if (nw.n)
+    k_merge<<<grid_for(nw.n), kBlock, 0, s>>>(nw.n, nw.ids.as<uint2>(), nw.wild.as<float>(), old.n,
+                                             old.ids.as<uint2>(), old.wild.as<float>(), c->wild_w);
+  std::swap(c->acs, c->acs_next);
+  c->ca_updates++;
+  GF_CHECK(c, cudaGetLastError());
+  return build_incidence(c, s);
+}
+
+// standalone history remap between two canonical arrays given as host
+// buffers (broadphase.merge_history); ids are (a, b | kind << 30)
+int merge_host(Ctx *c, int64_t n_old, const uint32_t *old_ids, const float *old_wild, int64_t n_new,
+               const uint32_t *new_ids, int W, float *out_wild) {
+  cudaStream_t s = c->s_dt;
+  DBuf a, b, wa, wb;
+  if (ensure(c, a, 8 * (n_old + 1), s) || ensure(c, b, 8 * (n_new + 1), s) ||
+      ensure(c, wa, 4 * W * (n_old + 1), s) || ensure(c, wb, 4 * W * (n_new + 1), s))
+    return -1;
+  if (n_old) {
+    GF_CHECK(c, cudaMemcpy(a.p, old_ids, 8 * n_old, cudaMemcpyHostToDevice));
+    GF_CHECK(c, cudaMemcpy(wa.p, old_wild, 4 * W * n_old, cudaMemcpyHostToDevice));
+  }
+  if (n_new) {
+    GF_CHECK(c, cudaMemcpy(b.p, new_ids, 8 * n_new, cudaMemcpyHostToDevice));
+    k_merge<<<grid_for(n_new), kBlock, 0, s>>>(n_new, b.as<uint2>(), wb.as<float>(), n_old, a.as<uint2>(),
+                                              wa.as<float>(), W);
+    GF_CHECK(c, cudaGetLastError());
+    GF_CHECK(c, cudaMemcpyAsync(out_wild, wb.p, 4 * W * n_new, cudaMemcpyDeviceToHost, s));
+    GF_CHECK(c, cudaStreamSynchronize(s));
+  }
+  cudaFree(a.p); cudaFree(b.p); cudaFree(wa.p); cudaFree(wb.p);
+  return 0;
+}
+
+int build_incidence(Ctx *c, cudaStream_t s) {
+  const int64_t n = c->acs.n;
+  const int64_t cap = std::max<int64_t>(c->acs.cap, 1);
+  if (ensure(c, c->out_c, sizeof(double) * 9 * cap, s) || ensure(c, c->touch, cap, s) ||
+      ensure(c, c->inc, sizeof(uint32_t) * 2 * cap, s) ||
+      ensure(c, c->inc_alt, sizeof(uint32_t) * 2 * cap, s) ||
+      ensure(c, c->inc_key, sizeof(uint32_t) * 2 * cap, s) ||
+      ensure(c, c->inc_key_alt, sizeof(uint32_t) * 2 * cap, s) ||
+      ensure(c, c->inc_start, sizeof(uint32_t) * (c->n_owner + 2), s) ||
+      ensure(c, c->heavy, sizeof(uint32_t) * (c->n_owner + 1), s))
+    return -1;
+  Status *st = c->status.as<Status>();
+  (void)st;
+  if (n) {
+    k_inc_keys<<<grid_for(n), kBlock, 0, s>>>(n, c->acs.ids.as<uint2>(), c->sph_owner.as<uint32_t>(),
+                                             c->tri_owner.as<uint32_t>(), c->ana_owner.as<uint32_t>(),
+                                             c->inc_key.as<uint32_t>(), c->inc.as<uint32_t>());
+    int bits = 1;
+    while ((int64_t(1) << bits) < c->n_owner + 1) ++bits;
+    size_t tmp = 0;
+    cub::DoubleBuffer<uint32_t> dk(c->inc_key.as<uint32_t>(), c->inc_key_alt.as<uint32_t>());
+    cub::DoubleBuffer<uint32_t> dv(c->inc.as<uint32_t>(), c->inc_alt.as<uint32_t>());
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, int(2 * n), 0, bits, s);
+    if (ensure(c, c->cub_tmp_dt, tmp + 16, s)) return -1;
+    GF_CHECK(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp_dt.p, tmp, dk, dv, int(2 * n), 0, bits, s));
+    if (dk.Current() != c->inc_key.as<uint32_t>()) {
+      std::swap(c->inc_key, c->inc_key_alt);
+      std::swap(c->inc, c->inc_alt);
+    }
+  }
+  GF_CHECK(c, cudaMemsetAsync(c->heavy_count.p, 0, sizeof(unsigned long long), s));
+  k_inc_start<<<grid_for(c->n_owner + 1), kBlock, 0, s>>>(
+      c->n_owner, 2 * n, c->inc_key.as<uint32_t>(), c->inc_start.as<uint32_t>(),
+      c->heavy.as<uint32_t>(), c->heavy_count.as<unsigned long long>(), kHeavyThreshold);
+  GF_CHECK(c, cudaGetLastError());
+  return 0;
+}
+
+}  // namespace gf
