@@ -1,0 +1,345 @@
+"""Benchmark: M sphere-steps/s of the B200 DEM step (BASELINE.json metric) on
+configs[1], the projectile-impact bed (1M polydisperse spheres).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+One JSON line on rank 0.  `value` = whole-job sphere-steps/s from CUDA events
+on the dT stream (t0 before the first timed step, t1 after the last step with
+the kT stream joined), max over ranks.  `e2e` = the same metric through the
+C-ABI with host buffers: every step uploads the owner state from pinned host
+memory, runs the step, downloads the state.  `--impl reference` times the
+reference algorithm on the host cores (the C restatement in oracle/, all
+threads) on the same scene.  Multi-GPU: independent replicas of the bed, one
+per rank (weak scaling, no data-path collective).
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "M element-steps/sec at 1/2/4/8 B200; % HBM roofline; CPU-ref x on host cores"
+UNIT = "M sphere-steps/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n-spheres", type=int, default=1_000_000)
+    ap.add_argument("--n-max", type=int, default=4)
+    ap.add_argument("--precision", default="f32", choices=["f32", "f64"])
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--cpu-steps", type=int, default=4)
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 5 + i and r[5 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def profiled_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu summary, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle restatement of the reference algorithm)
+# ---------------------------------------------------------------------------
+
+def cpu_run(scene, steps, warmup, period, lag, nthreads, margin):
+    from oracle import oracle as O
+    st = O.OracleStepper(scene, margin, period=period, lag=lag, nthreads=nthreads)
+    for _ in range(warmup):
+        st.step_once()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        st.step_once()
+    return time.perf_counter() - t0
+
+
+def build_scene(args, device):
+    from paper_2311_04648_b200 import scenes
+    return scenes.crater_bed(args.n_spheres, n_max=args.n_max, precision=args.precision, device=device)
+
+
+def schedule(sim):
+    period, lag = sim._schedule()
+    return period, lag, sim._current_margin()
+
+
+def reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2311_04648_b200 import scenes
+    sim = build_scene(args, 0)
+    scene = scenes.oracle_scene(sim)
+    period, lag, margin = schedule(sim)
+    n_s = int(np.sum(scene["geom_kind"] == 0))
+    threads = os.cpu_count() or 1
+    steps = max(1, min(args.steps, args.cpu_steps))
+    wall = cpu_run(scene, steps, max(1, min(args.warmup, 2)), period, lag, threads, margin)
+    value = n_s * steps / wall / 1e6
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": steps, "warmup": max(1, min(args.warmup, 2)), "ms_per_step": wall / steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"crater impact bed, {n_s} polydisperse spheres (configs[1])",
+                   "n_max": args.n_max, "h": scene["h"], "inputs_vs_l2": "larger than L2"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{steps} steps of the same bed (oracle/gf_oracle.c, OpenMP "
+                                   f"contact + integrate loops, serial detection)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def b200_arm(args):
+    rank, world, local = dist_env()
+    import torch
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    device = local
+    from paper_2311_04648_b200 import _lib, scenes
+    sim = build_scene(args, device)
+    scene0 = scenes.oracle_scene(sim) if (rank == 0 and not args.no_cpu) else None
+    sim.initialize()
+    n_s = int(sim._sph_geom.size)
+    n_o = int(sim.store.n_owners)
+    h = sim.h
+    # warm-up (untimed)
+    sim.do_dynamics(args.warmup * h)
+    ctx = sim._ctx
+    ctx.call("gf_set_profiling", C.c_int(1))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(device)
+
+    barrier()
+    with ClockSampler(device) as clocks:
+        sim.do_dynamics(args.steps * h)
+        barrier()
+    rr = sim.last_run
+    times = np.zeros(5)
+    ctx.call("gf_kernel_times", _lib.ptr(times))
+    ctx.call("gf_set_profiling", C.c_int(0))
+    dt_ms = float(rr.dt_ms)
+    if dist is not None:
+        t = torch.tensor([dt_ms], device=f"cuda:{device}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt_ms = float(t.item())
+    ms_per_step = dt_ms / args.steps
+    value = n_s * world * args.steps / (dt_ms * 1e-3) / 1e6
+    n_acs_avg = float(rr.sum_acs) / max(1, args.steps)
+    n_touch_avg = float(rr.sum_touch_pairs) / max(1, args.steps)
+    n_free = int(np.sum(~sim._fixed_flag[sim.store.owner_family[:n_o]]))
+
+    # --- roofline: dominant kernel (k_contacts) and the whole dT chain ---
+    hbm, hbm_kind = peaks()
+    steps_prof = max(1.0, times[4])
+    t_contacts = times[0] / steps_prof * 1e-3
+    t_chain = (times[0] + times[1] + times[2]) / steps_prof * 1e-3
+    vel_b = 12 if args.precision == "f32" else 24
+    per_owner = 58 + 54 + 48 + 2 * (vel_b - 12) * 2  # 160 B (fp32), 208 B (fp64)
+    bytes_contacts = 24.0 * n_acs_avg + 16.0 * n_touch_avg
+    bytes_chain = per_owner * n_free + 4.0 * n_s + bytes_contacts
+    ach_c = bytes_contacts / t_contacts / 1e9 if t_contacts > 0 else 0.0
+    ach_chain = bytes_chain / t_chain / 1e9 if t_chain > 0 else 0.0
+
+    # --- e2e: host-buffer round trip per step through the C-ABI ---
+    e2e = measure_e2e(sim, args.e2e_steps) if args.e2e_steps > 0 else None
+
+    line = None
+    if rank == 0:
+        cpu = None
+        if scene0 is not None:
+            period, lag, margin = schedule(sim)
+            csteps = max(1, args.cpu_steps)
+            wall = cpu_run(scene0, csteps, 1, period, lag, 1, margin)
+            cpu = {"value": n_s * csteps / wall / 1e6, "unit": UNIT, "cores": 1, "kind": "port",
+                   "sample": f"{csteps} steps (+1 warm-up) of the same bed from the same initial "
+                             f"state, serial C restatement (oracle/gf_oracle.c)"}
+        launches_per_step = 3 + (1 if sim._tri_geom.size or sim._ana_geom.size else 0)
+        period, lag, _ = schedule(sim)
+        kt_launches = 22
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64 contact math, " + ("f32" if args.precision == "f32" else "f64") + " velocities",
+            "data": "synthetic",
+            "config": {"workload": f"crater impact bed, {n_s} polydisperse spheres + projectile "
+                                   f"(configs[1])", "n_spheres": n_s, "n_owners": n_o,
+                       "n_max": args.n_max, "period": period, "lag": lag, "h": h,
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                       "inputs_vs_l2": "state + contact arrays larger than L2 (no flush)",
+                       "avg_acs": n_acs_avg, "avg_touching_pairs": n_touch_avg,
+                       "precision": args.precision},
+            "roofline": {"bound": "hbm", "kernel": "k_contacts", "achieved": ach_c, "peak": hbm,
+                         "unit": "GB/s", "frac": ach_c / hbm, "peak_kind": hbm_kind,
+                         "traffic": profiled_traffic("k_contacts"),
+                         "algorithmic_bytes_per_launch": bytes_contacts,
+                         "launch_ms": t_contacts * 1e3},
+            "roofline_dt_chain": {"bound": "hbm", "achieved": ach_chain, "peak": hbm, "unit": "GB/s",
+                                  "frac": ach_chain / hbm, "bytes_per_step": bytes_chain,
+                                  "ms": t_chain * 1e3,
+                                  "share_of_step": t_chain / (ms_per_step * 1e-3)},
+            "kernel_ms_per_step": {"k_contacts": times[0] / steps_prof, "k_heavy": times[1] / steps_prof,
+                                   "k_integrate": times[2] / steps_prof,
+                                   "kT_per_cycle": times[3] / max(1, args.steps // max(1, period))},
+            "clocks": clocks.summary(),
+            "e2e": e2e,
+            "gpu_launches": int(args.steps * launches_per_step + (args.steps // max(1, period)) * kt_launches),
+            "cpu_baseline": cpu,
+        }
+    sim.close()
+    if dist is not None:
+        dist.destroy_process_group()
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+def measure_e2e(sim, steps):
+    """Per step: pinned host state -> device (gf_upload_owners), one step
+    (gf_run), device -> pinned host state (gf_download_owners)."""
+    import torch
+    from paper_2311_04648_b200 import _lib
+    ctx = sim._ctx
+    n = sim.store.n_owners
+    P = _lib.ptr
+
+    def pinned(shape, dtype):
+        t = torch.empty(int(np.prod(shape)) * np.dtype(dtype).itemsize, dtype=torch.uint8).pin_memory()
+        return t.numpy().view(dtype).reshape(shape)
+
+    vox, sub = pinned((n,), np.uint64), pinned((n, 3), np.uint16)
+    quat, lv, av = pinned((n, 4), np.float32), pinned((n, 3), np.float64), pinned((n, 3), np.float64)
+    fam = pinned((n,), np.uint8)
+    ctx.call("gf_download_owners", P(vox), P(sub), P(quat), P(lv), P(av), P(fam))
+    tpl = _lib.carr(sim._tpl_id[sim._own_d2u], np.uint32)
+    rows = sim._tpl_rows
+    mass, moi = rows[:, 0].copy(), _lib.carr(rows[:, 1:], np.float64)
+    rp = _lib.RunParams()
+    rp.n_steps = 1
+    rp.h = sim.h
+    for a in range(3):
+        rp.g[a] = float(sim.gravity[a])
+    rp.v_err = sim.v_err
+    period, lag = sim._schedule()
+    rp.margin = sim._current_margin()
+    rp.period, rp.lag, rp.n_dyn, rp.write_acc = period, lag, 0, 0
+    rr = _lib.RunResult()
+    step0 = sim.scheduler.step_counter
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(steps):
+        ctx.call("gf_upload_owners", C.c_int64(n), P(vox), P(sub), P(quat), P(lv), P(av), P(fam),
+                 P(tpl), C.c_int64(rows.shape[0]), P(mass), P(moi))
+        rp.step0 = step0 + i
+        ctx.call("gf_run", C.byref(rp), C.byref(rr))
+        ctx.call("gf_download_owners", P(vox), P(sub), P(quat), P(lv), P(av), P(fam))
+    wall = time.perf_counter() - t0
+    sim.scheduler.step_counter = step0 + steps
+    n_s = int(sim._sph_geom.size)
+    per = n * (8 + 6 + 16 + 24 + 24 + 1)
+    return {"value": n_s * steps / wall / 1e6, "unit": UNIT, "h2d_bytes_per_step": per,
+            "d2h_bytes_per_step": per + 64, "steps": steps,
+            "path": "gf_upload_owners -> gf_run(1 step) -> gf_download_owners, pinned host buffers"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        b200_arm(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -163,11 +163,19 @@ typedef struct {
   int64_t touching;     /* last step */
   int64_t n_acs;
   int64_t ca_updates;
+  int64_t sum_acs;          /* active-contact entries summed over the run's steps */
+  int64_t sum_touch_pairs;  /* touching entries summed over the run's steps */
   double dt_ms, kt_ms;  /* device time of the dT and kT streams */
   double wall_ms;
 } gf_run_result;
 
 int gf_run(gf_ctx *ctx, const gf_run_params *p, gf_run_result *r);
+
+/* per-kernel device timing of subsequent gf_run calls (CUDA events on the dT
+ * stream); out5 = cumulative ms of {k_contacts, k_heavy, k_integrate, kT},
+ * then the number of profiled steps.  Enabling resets the counters. */
+int gf_set_profiling(gf_ctx *ctx, int on);
+int gf_kernel_times(gf_ctx *ctx, double *out5);
 
 #ifdef __cplusplus
 }

@@ -44,7 +44,8 @@ class RunParams(C.Structure):
 class RunResult(C.Structure):
     _fields_ = [("steps_done", _I64), ("bad_owner", _I64), ("bad_step", _I64),
                 ("oob_owner", _I64), ("oob_step", _I64), ("touching", _I64), ("n_acs", _I64),
-                ("ca_updates", _I64), ("dt_ms", _D), ("kt_ms", _D), ("wall_ms", _D)]
+                ("ca_updates", _I64), ("sum_acs", _I64), ("sum_touch_pairs", _I64), ("dt_ms", _D),
+                ("kt_ms", _D), ("wall_ms", _D)]
 
 
 # every symbol include/gf_b200.h declares
@@ -54,7 +55,7 @@ EXPORTS = (
     "gf_download_accumulators", "gf_upload_geometry", "gf_upload_materials",
     "gf_upload_families", "gf_download_world", "gf_set_acs", "gf_acs_size", "gf_get_acs",
     "gf_detect", "gf_detect_snapshot", "gf_bin_ranges", "gf_adopt", "gf_dt_step", "gf_run",
-    "gf_merge_history",
+    "gf_merge_history", "gf_set_profiling", "gf_kernel_times",
 )
 
 _lib = None

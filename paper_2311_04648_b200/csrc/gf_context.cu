@@ -84,6 +84,31 @@ Families families_view(Ctx *c) {
                   c->av_mask.as<uint8_t>(), c->lv_val.as<double>(), c->av_val.as<double>()};
 }
 
+cudaEvent_t *prof_events(Ctx *c) {
+  if (!c->prof) return nullptr;
+  if (c->prof_used + 4 > c->prof_ev.size()) {
+    for (int q = 0; q < 4; ++q) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      c->prof_ev.push_back(e);
+    }
+  }
+  cudaEvent_t *ev = &c->prof_ev[c->prof_used];
+  c->prof_used += 4;
+  return ev;
+}
+
+static void prof_collect(Ctx *c) {
+  for (size_t i = 0; i + 4 <= c->prof_used; i += 4) {
+    float m;
+    for (int q = 0; q < 3; ++q)
+      if (cudaEventElapsedTime(&m, c->prof_ev[i + q], c->prof_ev[i + q + 1]) == cudaSuccess)
+        c->prof_ms[q] += m;
+    c->prof_steps++;
+  }
+  c->prof_used = 0;
+}
+
 static int dt_step(Ctx *c, const StepArgs &a) {
   return c->f32_state ? dt_step_f32(c, a, c->s_dt) : dt_step_f64(c, a, c->s_dt);
 }
@@ -92,6 +117,7 @@ static int reset_status(Ctx *c, cudaStream_t s) {
   Status *st = c->status.as<Status>();
   GF_CHECK(c, cudaMemsetAsync(st, 0xFF, 2 * sizeof(unsigned long long), s));
   GF_CHECK(c, cudaMemsetAsync(&st->touching, 0, sizeof(unsigned long long), s));
+  GF_CHECK(c, cudaMemsetAsync(&st->touch_pairs, 0, sizeof(unsigned long long), s));
   GF_CHECK(c, cudaMemsetAsync(&st->err, 0, sizeof(int), s));
   return 0;
 }
@@ -548,6 +574,23 @@ static void pack_ids(int64_t n, const uint8_t *kind, const int64_t *a, const int
   }
 }
 
+int gf_set_profiling(gf_ctx *ctx, int on) {
+  CTX_CHECK(ctx);
+  GF_CHECK(c, cudaDeviceSynchronize());
+  c->prof = on != 0;
+  c->prof_used = 0;
+  for (int q = 0; q < 4; ++q) c->prof_ms[q] = 0.0;
+  c->prof_steps = 0;
+  return 0;
+}
+
+int gf_kernel_times(gf_ctx *ctx, double *out5) {
+  CTX_CHECK(ctx);
+  for (int q = 0; q < 4; ++q) out5[q] = c->prof_ms[q];
+  out5[4] = double(c->prof_steps);
+  return 0;
+}
+
 int gf_merge_history(gf_ctx *ctx, int64_t n_old, const uint8_t *old_kind, const int64_t *old_a,
                      const int64_t *old_b, const float *old_wild, int64_t n_new,
                      const uint8_t *new_kind, const int64_t *new_a, const int64_t *new_b, int W,
@@ -619,6 +662,7 @@ int gf_run(gf_ctx *ctx, const gf_run_params *p, gf_run_result *r) {
     c->first_adopt = false;
     return 0;
   };
+  int64_t sum_acs = 0;
   for (int64_t i = 0; i < N; ++i) {
     const int64_t s = p->step0 + i;
     // 1. a detection due at this step boundary is adopted first
@@ -646,10 +690,14 @@ int gf_run(gf_ctx *ctx, const gf_run_params *p, gf_run_result *r) {
     // 3. launch the fill as soon as the count is known (no dT stall)
     if (c->next_pending && !c->fill_done && cudaEventQuery(c->ev_count) == cudaSuccess && do_fill())
       return -1;
+    sum_acs += c->acs.n;
     StepArgs a{p->h, {p->g[0], p->g[1], p->g[2]}, p->v_err, double(s) * p->h, s, i,
                (i == N - 1) ? p->write_acc : 0};
     if (dt_step(c, a)) return -1;
   }
+  // join the kT stream so in-flight detection work counts in the timed window
+  GF_CHECK(c, cudaEventRecord(c->ev_snap, c->s_kt));
+  GF_CHECK(c, cudaStreamWaitEvent(c->s_dt, c->ev_snap, 0));
   GF_CHECK(c, cudaEventRecord(c->t1, c->s_dt));
   GF_CHECK(c, cudaStreamSynchronize(c->s_kt));
   Status st;
@@ -665,6 +713,10 @@ int gf_run(gf_ctx *ctx, const gf_run_params *p, gf_run_result *r) {
     cudaEventDestroy(e.second);
   }
   r->kt_ms = kt_ms;
+  if (c->prof) {
+    prof_collect(c);
+    c->prof_ms[3] += kt_ms;
+  }
   decode_err(st.bad, r->bad_owner, r->bad_step);
   decode_err(st.oob, r->oob_owner, r->oob_step);
   int64_t err_step = -1;
@@ -672,6 +724,8 @@ int gf_run(gf_ctx *ctx, const gf_run_params *p, gf_run_result *r) {
   if (r->oob_step >= 0 && (err_step < 0 || r->oob_step < err_step)) err_step = r->oob_step;
   r->steps_done = err_step >= 0 ? err_step - p->step0 : N;
   r->touching = int64_t(st.touching);
+  r->sum_touch_pairs = int64_t(st.touch_pairs);
+  r->sum_acs = sum_acs;
   r->n_acs = c->acs.n;
   r->ca_updates = c->ca_updates;
   r->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();

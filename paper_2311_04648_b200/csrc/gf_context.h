@@ -106,7 +106,16 @@ struct Ctx {
   int64_t ca_updates = 0;
   double t_kt_ms = 0.0, t_dt_ms = 0.0;
   int64_t last_touching = 0;
+  // per-kernel device timing (enabled by gf_set_profiling)
+  bool prof = false;
+  std::vector<cudaEvent_t> prof_ev;   // 4 per profiled step: start, contacts, heavy, integrate
+  size_t prof_used = 0;
+  double prof_ms[4] = {0, 0, 0, 0};   // contacts, heavy, integrate, kT
+  int64_t prof_steps = 0;
 };
+
+// take 4 timing events for one profiled dT step (nullptr when off)
+cudaEvent_t *prof_events(Ctx *c);
 
 // device status block
 struct Status {
@@ -114,6 +123,7 @@ struct Status {
   unsigned long long oob;    // same for out-of-domain
   unsigned long long touching;
   unsigned long long acs_total;   // last detection's pair count
+  unsigned long long touch_pairs;  // touching ACS entries summed over the run's steps
   double oob_pos[3];
   int err;                   // nonzero once a watchdog tripped (kernels stop)
   int pad;

@@ -169,7 +169,7 @@ __device__ __forceinline__ void owner_kin(const DtView &v, uint32_t o, double po
 template <typename VelT>
 __global__ void __launch_bounds__(128) k_contacts(DtView v, double ts) {
   int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  unsigned touching = 0;
+  unsigned touching = 0, pairs = 0;
   if (k < v.n_acs && !v.st->err) {
     uint2 id = v.ids[k];
     const uint32_t kind = id.y >> kKindShift, sb = id.y & kSlotMask;
@@ -251,12 +251,19 @@ __global__ void __launch_bounds__(128) k_contacts(DtView v, double ts) {
       oc[6] = px; oc[7] = py; oc[8] = pz;
       t = 1;
       touching = kind == 0 ? 2u : 1u;
+      pairs = 1;
     }
     v.touch[k] = t;
   }
   // block total of touching spheres (integer: order-independent)
-  for (int off = 16; off > 0; off >>= 1) touching += __shfl_down_sync(0xffffffff, touching, off);
-  if ((threadIdx.x & 31) == 0 && touching) atomicAdd(&v.st->touching, (unsigned long long)touching);
+  for (int off = 16; off > 0; off >>= 1) {
+    touching += __shfl_down_sync(0xffffffff, touching, off);
+    pairs += __shfl_down_sync(0xffffffff, pairs, off);
+  }
+  if ((threadIdx.x & 31) == 0 && touching) {
+    atomicAdd(&v.st->touching, (unsigned long long)touching);
+    atomicAdd(&v.st->touch_pairs, (unsigned long long)pairs);
+  }
 }
 
 // one owner's incidence contributions, in canonical order (_kernels.py:522-545)
@@ -488,11 +495,15 @@ int dt_step_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
   v.heavy_acc = c->heavy_acc.as<double>();
   v.st = c->status.as<Status>();
   GF_CHECK(c, cudaMemsetAsync(&v.st->touching, 0, sizeof(unsigned long long), s));
+  cudaEvent_t *ev = prof_events(c);
+  if (ev) cudaEventRecord(ev[0], s);
   if (v.n_acs) {
     unsigned g = unsigned((v.n_acs + 127) / 128);
     k_contacts<VelT><<<g, 128, 0, s>>>(v, a.h);
-    k_heavy<<<64, 256, 0, s>>>(v);
   }
+  if (ev) cudaEventRecord(ev[1], s);
+  if (v.n_acs) k_heavy<<<64, 256, 0, s>>>(v);
+  if (ev) cudaEventRecord(ev[2], s);
   if (c->n_dyn) {
     k_apply_dyn<<<(c->n_dyn + 127) / 128, 128, 0, s>>>(
         c->n_dyn, c->dyn_spec.as<int>(), c->dyn_vals.as<double>() + size_t(c->n_dyn) * a.dyn_row,
@@ -503,6 +514,7 @@ int dt_step_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
     k_integrate<VelT><<<g, 128, 0, s>>>(v, a.h, a.g[0], a.g[1], a.g[2], a.v_err,
                                        (unsigned long long)a.step, a.write_acc);
   }
+  if (ev) cudaEventRecord(ev[3], s);
   if ((c->n_tri || c->n_ana) && c->world_moving) {
     int64_t n = c->n_tri + c->n_ana;
     k_world<<<unsigned((n + 127) / 128), 128, 0, s>>>(c->dom, v.own, v.tri, v.ana);

@@ -178,7 +178,7 @@ class Simulator:
     default_sync = False
 
     def __init__(self, domain: Domain, force_model: str = "hertz_mindlin", *,
-                 device: int = 0, precision: str = "f64"):
+                 device: int = 0, precision: str = "f64", reorder=None):
         if precision not in ("f64", "f32"):
             raise ValidationError(f"precision must be 'f64' or 'f32', got {precision!r}")
         self.materials = MaterialTable()
@@ -194,6 +194,10 @@ class Simulator:
         self.active_box_policy = None
         self.device = int(device)
         self.precision = precision
+        # device memory order: Morton order of the initial positions so contact
+        # gathers hit nearby owners; the fp64 parity build keeps the reference's
+        # order (its per-owner summation order is then the reference's too)
+        self.reorder = (precision == "f32") if reorder is None else bool(reorder)
         self._initialized = False
         self._closed = False
         self._sph_geom = np.zeros(0, dtype=np.int64)
@@ -368,8 +372,9 @@ class Simulator:
             self._margin_cap_steps = max(4, int(r_min / (4.0 * self.v_err * self.h)))
         else:
             self._margin_cap_steps = None
-        # mass-property templates: unique (mass, moi) rows
         n = s.n_owners
+        self._build_permutation()
+        # mass-property templates: unique (mass, moi) rows
         mm = np.concatenate([s.mass[:n, None], s.moi[:n]], axis=1) if n else np.zeros((0, 4))
         tpl_rows, tpl_id = np.unique(mm, axis=0, return_inverse=True) if n else (np.zeros((0, 4)), np.zeros(0, int))
         self._tpl_rows = np.ascontiguousarray(tpl_rows, dtype=np.float64)
@@ -383,14 +388,16 @@ class Simulator:
         self._upload_tables()
         self._upload_owners()
         gp = s.geom_params[:n_g]
-        sph_params = _lib.carr(gp[self._sph_geom, :4], np.float32)
+        sph_dev = self._sph_geom[self._sph_d2u]  # user geometry id of each device sphere slot
+        sph_params = _lib.carr(gp[sph_dev, :4], np.float32)
         tri_local = _lib.carr(gp[self._tri_geom, :9], np.float32)
         ana_local = _lib.carr(gp[self._ana_geom, :8], np.float32)
         gm = s.geom_material[:n_g]
         go = s.geom_owner[:n_g]
-        keep = [_lib.carr(go[self._sph_geom], np.int64), sph_params, _lib.carr(gm[self._sph_geom], np.uint8),
-                _lib.carr(go[self._tri_geom], np.int64), tri_local, _lib.carr(gm[self._tri_geom], np.uint8),
-                _lib.carr(go[self._ana_geom], np.int64), _lib.carr(self._ana_kind_arr, np.uint8),
+        u2d = self._own_u2d
+        keep = [_lib.carr(u2d[go[sph_dev]], np.int64), sph_params, _lib.carr(gm[sph_dev], np.uint8),
+                _lib.carr(u2d[go[self._tri_geom]], np.int64), tri_local, _lib.carr(gm[self._tri_geom], np.uint8),
+                _lib.carr(u2d[go[self._ana_geom]], np.int64), _lib.carr(self._ana_kind_arr, np.uint8),
                 ana_local, _lib.carr(gm[self._ana_geom], np.uint8)]
         ctx.call("gf_upload_geometry", C.c_int64(self._sph_geom.size), P(keep[0]), P(keep[1]), P(keep[2]),
                  C.c_int64(self._tri_geom.size), P(keep[3]), P(keep[4]), P(keep[5]),
@@ -420,6 +427,31 @@ class Simulator:
         return False
 
     # -- host <-> device ----------------------------------------------------------
+    def _build_permutation(self):
+        s = self.store
+        n = s.n_owners
+        if self.reorder and n > 1:
+            pos = s.positions()
+            lo = pos.min(axis=0)
+            span = max(float((pos.max(axis=0) - lo).max()), 1e-300)
+            q = np.minimum((pos - lo) / span * 1023.0, 1023.0).astype(np.uint64)
+            code = np.zeros(n, np.uint64)
+            for bit in range(10):
+                for ax in range(3):
+                    code |= ((q[:, ax] >> np.uint64(bit)) & np.uint64(1)) << np.uint64(3 * bit + ax)
+            d2u = np.argsort(code, kind="stable").astype(np.int64)
+        else:
+            d2u = np.arange(n, dtype=np.int64)
+        u2d = np.empty(n, np.int64)
+        u2d[d2u] = np.arange(n, dtype=np.int64)
+        self._own_d2u, self._own_u2d = d2u, u2d
+        # device sphere slots: grouped by device owner, geometry order within
+        sph_owner_dev = u2d[s.geom_owner[self._sph_geom]] if self._sph_geom.size else np.zeros(0, np.int64)
+        sd2u = np.lexsort((np.arange(self._sph_geom.size), sph_owner_dev)).astype(np.int64)
+        su2d = np.empty(sd2u.size, np.int64)
+        su2d[sd2u] = np.arange(sd2u.size, dtype=np.int64)
+        self._sph_d2u, self._sph_u2d = sd2u, su2d
+
     def _upload_tables(self):
         ctx, P = self._ctx, _lib.ptr
         fam = self.store.families
@@ -439,15 +471,17 @@ class Simulator:
         s, ctx, P = self.store, self._ctx, _lib.ptr
         n = s.n_owners
         d = s.__dict__
-        keep = [_lib.carr(d["_voxel"][:n], np.uint64), _lib.carr(d["_subvoxel"][:n], np.uint16),
-                _lib.carr(d["_quat"][:n], np.float32), _lib.carr(d["_lin_vel"][:n], np.float64),
-                _lib.carr(d["_ang_vel"][:n], np.float64), _lib.carr(d["_owner_family"][:n], np.uint8),
-                self._tpl_id, self._tpl_rows[:, 0].copy(), _lib.carr(self._tpl_rows[:, 1:], np.float64)]
+        p = self._own_d2u
+        keep = [_lib.carr(d["_voxel"][:n][p], np.uint64), _lib.carr(d["_subvoxel"][:n][p], np.uint16),
+                _lib.carr(d["_quat"][:n][p], np.float32), _lib.carr(d["_lin_vel"][:n][p], np.float64),
+                _lib.carr(d["_ang_vel"][:n][p], np.float64), _lib.carr(d["_owner_family"][:n][p], np.uint8),
+                _lib.carr(self._tpl_id[p], np.uint32), self._tpl_rows[:, 0].copy(),
+                _lib.carr(self._tpl_rows[:, 1:], np.float64)]
         ctx.call("gf_upload_owners", C.c_int64(n), P(keep[0]), P(keep[1]), P(keep[2]), P(keep[3]),
                  P(keep[4]), P(keep[5]), P(keep[6]), C.c_int64(self._tpl_rows.shape[0]), P(keep[7]),
                  P(keep[8]))
-        ef = _lib.carr(d["_ext_force"][:n], np.float64)
-        et = _lib.carr(d["_ext_torque"][:n], np.float64)
+        ef = _lib.carr(d["_ext_force"][:n][p], np.float64)
+        et = _lib.carr(d["_ext_torque"][:n][p], np.float64)
         if np.any(ef != 0.0) or np.any(et != 0.0):
             ctx.call("gf_set_external_loads", P(ef), P(et))
         else:
@@ -470,14 +504,15 @@ class Simulator:
         af = np.zeros((n, 3))
         at = np.zeros((n, 3))
         self._ctx.call("gf_download_accumulators", P(af), P(at))
-        d["_voxel"][:n] = vox
-        d["_subvoxel"][:n] = sub
-        d["_quat"][:n] = quat
-        d["_lin_vel"][:n] = lv
-        d["_ang_vel"][:n] = av
-        d["_owner_family"][:n] = fam
-        d["_acc_force"][:n] = af
-        d["_acc_torque"][:n] = at
+        p = self._own_d2u
+        d["_voxel"][:n][p] = vox
+        d["_subvoxel"][:n][p] = sub
+        d["_quat"][:n][p] = quat
+        d["_lin_vel"][:n][p] = lv
+        d["_ang_vel"][:n][p] = av
+        d["_owner_family"][:n][p] = fam
+        d["_acc_force"][:n][p] = af
+        d["_acc_torque"][:n][p] = at
         self._host_stale = False
 
     def _sync_field(self, name):
@@ -502,10 +537,16 @@ class Simulator:
             wild[:, i] = ca.wildcards[name]
         P = _lib.ptr
         kind = _lib.carr(ca.kind, np.uint8)
-        sa = _lib.carr(self._geom_slot[ca.geom_a] if n else np.zeros(0), np.int64)
-        sb = _lib.carr(self._geom_slot[ca.geom_b] if n else np.zeros(0), np.int64)
-        self._ctx.call("gf_set_acs", C.c_int64(n), P(kind), P(sa), P(sb), P(wild),
-                       C.c_int(len(self.model.wildcards)))
+        sa = self._geom_slot[ca.geom_a] if n else np.zeros(0, np.int64)
+        sb = self._geom_slot[ca.geom_b] if n else np.zeros(0, np.int64)
+        if n:
+            sa = self._sph_u2d[sa]
+            sb = np.where(kind == 0, self._sph_u2d[np.where(kind == 0, sb, 0)], sb)
+            order = np.lexsort((sb, sa, kind))
+            kind, sa, sb, wild = kind[order], sa[order], sb[order], wild[order]
+        self._ctx.call("gf_set_acs", C.c_int64(n), P(_lib.carr(kind, np.uint8)),
+                       P(_lib.carr(sa, np.int64)), P(_lib.carr(sb, np.int64)),
+                       P(_lib.carr(wild, np.float32)), C.c_int(len(self.model.wildcards)))
 
     # -- host mirrors of engine internals (read by tests / IO) -------------------
     @property
@@ -517,7 +558,9 @@ class Simulator:
         out = np.zeros((self._sph_geom.shape[0], 3))
         if self._ctx is not None and out.shape[0]:
             self._push_host()
-            self._ctx.call("gf_download_world", _lib.ptr(out), None, None)
+            dev = np.zeros_like(out)
+            self._ctx.call("gf_download_world", _lib.ptr(dev), None, None)
+            out[self._sph_d2u] = dev
         return out
 
     @property
@@ -552,6 +595,9 @@ class Simulator:
         if self._ctx is None:
             return self._acs0
         kind, sa, sb, wild = self._acs_arrays()
+        if kind.size:
+            sa = self._sph_d2u[sa]
+            sb = np.where(kind == 0, self._sph_d2u[np.where(kind == 0, sb, 0)], sb)
         tabs = (self._sph_geom, self._tri_geom, self._ana_geom)
         ga = self._sph_geom[sa] if kind.size else np.zeros(0, np.int64)
         gb = np.zeros(kind.shape[0], np.int64)
@@ -562,7 +608,7 @@ class Simulator:
         ca = B.ContactArray(kind, ga, gb)
         for i, name in enumerate(self.model.wildcards):
             ca.wildcards[name] = wild[:, i].copy()
-        return ca
+        return ca.canonicalize() if self.reorder else ca
 
     @_acs.setter
     def _acs(self, value):
@@ -570,7 +616,10 @@ class Simulator:
 
     @property
     def _wild(self) -> np.ndarray:
-        return self._acs_arrays()[3]
+        ca = self._acs
+        if not ca.size:
+            return np.zeros((0, len(self.model.wildcards)), np.float32)
+        return np.stack([ca.wildcards[nm] for nm in self.model.wildcards], axis=1)
 
     def _refresh_world(self) -> None:
         """World geometry is derived on the device on demand."""

@@ -1,0 +1,139 @@
+"""Synthetic workloads of BASELINE.json's configs, built through the public
+Simulator API only (setup code; no compute here).
+
+crater_bed  configs[1]: projectile impact onto an n-sphere polydisperse bed.
+            Geometry and materials follow the reference's crater builders
+            (scenarios.py:229-307, _crater_sim / settle_crater_bed): bed
+            12 D x 12 D x 8 D, D = 2.54 cm, eleven grain diameters uniform over
+            the relative band [0.25, 0.35] scaled to the mean the bed volume
+            implies for n grains, rho_g = 2500, E = 5e6, nu = 0.3, CoR = 0.5,
+            mu = 0.3, Crr = 0.01, five fixed analytic walls, a 7.8 g/cc ball
+            released just above the bed at the free-fall speed of a 20 cm drop.
+            Deviations (stated in DESIGN.md): the grains start on an HCP
+            lattice of pitch d_max (the reference pours and settles first,
+            scenarios.py:286-291) and the step is h = 1e-5 s with v_err = 5 m/s
+            (the reference's 1e-4 s / 30 m/s give a 24 mm detection margin,
+            i.e. thousands of candidate pairs per grain).
+settling_box configs[0]: monodisperse r = 5 mm spheres in a walled box.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from .core import ClumpTemplate, Domain
+from .engine import Simulator, hcp_sample_box
+
+G = 9.81
+
+
+def crater_bed(n_spheres: int = 1_000_000, *, seed: int = 7, h: float = 1e-5, v_err: float = 5.0,
+               n_max: int = 4, precision: str = "f32", device: int = 0, ball: bool = True,
+               drop_height: float = 0.20, ball_density: float = 7800.0) -> Simulator:
+    rng = np.random.default_rng(seed)
+    D = 0.0254
+    bed_half = 12.0 * D / 2.0
+    depth = 8.0 * D
+    packing = 1460.0 / 2500.0
+    volume = (2 * bed_half) ** 2 * depth
+    d_mean = (6.0 * volume * packing / (math.pi * n_spheres)) ** (1.0 / 3.0)
+    dset = np.linspace(0.25, 0.35, 11) * (d_mean / 0.30)
+    radii = dset / 2.0
+    r_max = float(radii.max())
+    dom = Domain((-bed_half * 1.2, -bed_half * 1.2, -0.02), (bed_half * 1.2, bed_half * 1.2,
+                                                            depth * 3.0 + 0.3))
+    sim = Simulator(dom, precision=precision, device=device)
+    grain = sim.load_material({"E": 5e6, "nu": 0.3, "CoR": 0.5, "mu": 0.3, "Crr": 0.01})
+    wall = sim.load_material({"E": 5e6, "nu": 0.3, "CoR": 0.5, "mu": 0.3, "Crr": 0.01})
+    tpls = [sim.load_clump_template(ClumpTemplate.solid_sphere(
+        float(r), 2500.0 * 4.0 / 3.0 * math.pi * float(r) ** 3, grain)) for r in radii]
+    # lattice pitch d_max: the largest grains touch, nobody overlaps
+    pitch = 2.0 * r_max * 1.0005
+    half_xy = bed_half - r_max * 1.05
+    # enough layers for n grains (rows come out bottom layer first)
+    per_layer = (2 * half_xy) ** 2 / (math.sqrt(3.0) / 2.0 * pitch ** 2)
+    layer_dz = 2.0 * math.sqrt(6.0) / 3.0 * pitch / 2.0
+    n_layers = int(math.ceil(1.15 * n_spheres / max(per_layer, 1.0))) + 2
+    top = r_max * 1.05 + n_layers * layer_dz
+    pts = hcp_sample_box((0.0, 0.0, (top + r_max * 1.05) / 2.0), (half_xy, half_xy, (top - r_max * 1.05) / 2.0),
+                         pitch)
+    if pts.shape[0] < n_spheres:
+        raise RuntimeError(f"lattice holds {pts.shape[0]} < {n_spheres} grains")
+    pts = pts[:n_spheres]
+    kinds = rng.integers(0, 11, pts.shape[0])
+    for k, tpl in enumerate(tpls):
+        sel = pts[kinds == k]
+        if sel.shape[0]:
+            sim.add_clumps(tpl, sel)
+    walls = [("plane", (0, 0, 0), (0, 0, 1), wall),
+             ("plane", (-bed_half, 0, 0), (1, 0, 0), wall),
+             ("plane", (bed_half, 0, 0), (-1, 0, 0), wall),
+             ("plane", (0, -bed_half, 0), (0, 1, 0), wall),
+             ("plane", (0, bed_half, 0), (0, -1, 0), wall)]
+    sim.add_analytic(walls, family=255)
+    sim.set_family_fixed(255)
+    if ball:
+        R = D / 2.0
+        mass = ball_density * 4.0 / 3.0 * math.pi * R ** 3
+        btpl = sim.load_clump_template(ClumpTemplate.solid_sphere(R, mass, grain))
+        surface = float(pts[:, 2].max()) + r_max
+        b = sim.add_clumps(btpl, [[0.0, 0.0, surface + R + 2e-3]])[0]
+        sim.track(b).set_vel([0.0, 0.0, -math.sqrt(2.0 * G * drop_height)])
+    sim.set_gravity([0, 0, -G])
+    sim.set_init_time_step(h)
+    sim.set_error_out_velocity(v_err)
+    sim.set_fixed_lookahead(n_max)
+    return sim
+
+
+def settling_box(n_spheres: int = 10_000, *, h: float = 1e-5, v_err: float = 5.0, n_max: int = 4,
+                 precision: str = "f64", device: int = 0) -> Simulator:
+    """configs[0]: r = 5 mm, rho = 2600, {E 1e7, nu 0.3, CoR 0.6, mu 0.3}, floor
+    + 4 side walls fixed (test_engine.py:13-18 materials)."""
+    r = 0.005
+    side = (n_spheres * (2 * r * 1.02) ** 3 / 0.70) ** (1.0 / 3.0)
+    half = max(side / 2.0, 4 * r)
+    dom = Domain((-half - 0.05, -half - 0.05, -0.02), (half + 0.05, half + 0.05, 4 * half + 0.2))
+    sim = Simulator(dom, precision=precision, device=device)
+    mat = sim.load_material({"E": 1e7, "nu": 0.3, "CoR": 0.6, "mu": 0.3, "Crr": 0.0})
+    m = 2600.0 * 4.0 / 3.0 * math.pi * r ** 3
+    tpl = sim.load_clump_template(ClumpTemplate.solid_sphere(r, m, mat))
+    pts = hcp_sample_box((0, 0, 1.1 * half + 1.02 * r), (half - 1.5 * r, half - 1.5 * r, 1.1 * half),
+                         2 * r * 1.02)
+    if pts.shape[0] < n_spheres:
+        raise RuntimeError("box too small")
+    sim.add_clumps(tpl, pts[:n_spheres])
+    walls = [("plane", (0, 0, 0), (0, 0, 1), mat),
+             ("plane", (-half, 0, 0), (1, 0, 0), mat), ("plane", (half, 0, 0), (-1, 0, 0), mat),
+             ("plane", (0, -half, 0), (0, 1, 0), mat), ("plane", (0, half, 0), (0, -1, 0), mat)]
+    sim.add_analytic(walls, family=255)
+    sim.set_family_fixed(255)
+    sim.set_gravity([0, 0, -G])
+    sim.set_init_time_step(h)
+    sim.set_error_out_velocity(v_err)
+    sim.set_fixed_lookahead(n_max)
+    return sim
+
+
+def oracle_scene(sim: Simulator) -> dict:
+    """The simulator's setup state in the oracle's scene-dict layout (used by
+    the bench's CPU legs and tests; reads host mirrors only)."""
+    from .forces import material_pair_stack
+    s = sim.store
+    n, g = s.n_owners, s.n_geoms
+    return dict(
+        voxel=s.voxel[:n].copy(), subvoxel=s.subvoxel[:n].copy(), quat=s.quat[:n].copy(),
+        lin_vel=s.lin_vel[:n].copy(), ang_vel=s.ang_vel[:n].copy(), mass=s.mass[:n].copy(),
+        moi=s.moi[:n].copy(), owner_family=s.owner_family[:n].copy(),
+        ext_force=s.ext_force[:n].copy(), ext_torque=s.ext_torque[:n].copy(),
+        geom_owner=s.geom_owner[:g].copy(), geom_kind=s.geom_kind[:g].copy(),
+        geom_material=s.geom_material[:g].copy(), geom_params=s.geom_params[:g].copy(),
+        lo=s.domain.lo.copy(), hi=s.domain.hi.copy(), edge=float(s.domain.voxel_edge),
+        pair_stack=material_pair_stack(sim.materials, sim.model),
+        mask=s.families.mask.astype(np.uint8), fixed_flag=sim._fixed_flag.astype(np.uint8),
+        prescribed_flag=sim._prescribed_flag.astype(np.uint8),
+        lv_mask=sim._lv_mask.astype(np.uint8), lv_val=sim._lv_val.copy(),
+        av_mask=sim._av_mask.astype(np.uint8), av_val=sim._av_val.copy(),
+        gravity=sim.gravity.copy(), h=float(sim.h), v_err=float(sim.v_err))
