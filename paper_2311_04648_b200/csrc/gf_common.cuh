@@ -232,10 +232,17 @@ __device__ inline void analytic_gap(int kind, const double *prm, double cx, doub
 // uniform grid (broadphase.py:160-186, _kernels.py:238-266)
 // ---------------------------------------------------------------------------
 struct Grid {
+  // the reference's grid (bin = 2 (r_max + margin), _grid_for): used only
+  // to evaluate its exact pair predicate (the min-corner bin test)
   double glo[3];
   double inv_bin;
   long long nb[3];
   int valid;
+  // enumeration grid: cell = 2 (r_cut + margin) over the same origin; spheres
+  // with radius > r_cut ("big") are not registered and are paired by k_big
+  double inv_cell;
+  long long nc[3];
+  double r_cut;
 };
 
 __device__ __forceinline__ long long axis_bin(double x, double glo, double inv_bin, long long nb) {

@@ -10,6 +10,7 @@
 // event, remaps the contact history onto the new array (merge_history) and
 // swaps the double buffer.  Adoption happens at a fixed step, so runs are
 // bitwise reproducible; period = 1, lag = 0 is the reference's sync mode.
+#include <algorithm>
 #include <chrono>
 #include <cstring>
 #include <vector>
@@ -135,6 +136,30 @@ static void decode_err(unsigned long long w, int64_t &owner, int64_t &step) {
   step = int64_t(w >> 40);
 }
 
+// enumeration split (csrc/gf_kt.cu): r_cut = the largest radius not above
+// twice the median; spheres above it are "big" and paired by k_big
+static int set_split(Ctx *c, const float *radii, int64_t stride, int64_t n) {
+  std::vector<float> r(n);
+  for (int64_t i = 0; i < n; ++i) r[i] = radii[i * stride];
+  c->n_big = 0;
+  c->r_cut = 0.0;
+  if (!n) return 0;
+  std::vector<float> sorted(r);
+  std::nth_element(sorted.begin(), sorted.begin() + n / 2, sorted.end());
+  const double med = sorted[n / 2];
+  double rc = 0.0;
+  for (float x : r)
+    if (double(x) <= 2.0 * med && double(x) > rc) rc = double(x);
+  std::vector<uint32_t> big;
+  for (int64_t i = 0; i < n; ++i)
+    if (double(r[i]) > rc) big.push_back(uint32_t(i));
+  c->r_cut = rc;
+  c->n_big = int64_t(big.size());
+  if (ensure(c, c->big_slots, 4 * (big.size() + 1), c->s_dt)) return -1;
+  if (!big.empty()) GF_CHECK(c, cudaMemcpy(c->big_slots.p, big.data(), 4 * big.size(), cudaMemcpyHostToDevice));
+  return 0;
+}
+
 static void world_moving_update(Ctx *c) {
   // _refresh_moving_world (engine.py:552-568): skip while every mesh /
   // analytic owner sits in a fixed family
@@ -220,7 +245,7 @@ void gf_destroy(gf_ctx *ctx) {
                   &c->kt.minmax, &c->kt.bin_key, &c->kt.bin_key_alt, &c->kt.sph_val, &c->kt.sph_val_alt,
                   &c->kt.cell_start, &c->kt.cell_end, &c->kt.tri_ranges, &c->kt.tri_cnt,
                   &c->kt.tri_start, &c->kt.tri_entries, &c->kt.counts, &c->kt.offsets, &c->kt.cub_tmp,
-                  &c->kt.total};
+                  &c->kt.total, &c->kt.cursor, &c->kt.tri_cursor, &c->big_slots};
   for (DBuf *b : bufs) release(*b);
   if (c->h_status) cudaFreeHost(c->h_status);
   cudaEvent_t evs[] = {c->ev_snap, c->ev_ca, c->ev_adopted, c->ev_count, c->t0, c->t1};
@@ -414,6 +439,7 @@ int gf_upload_geometry(gf_ctx *ctx, int64_t n_s, const int64_t *sph_owner, const
       upload_raw(c, c->ana_local, ana_local, 32 * n_a) || upload_raw(c, c->ana_mat, ana_mat, n_a) ||
       ensure(c, c->tri_world, 72 * (n_t + 1), c->s_dt) || ensure(c, c->ana_world, 64 * (n_a + 1), c->s_dt))
     return -1;
+  if (set_split(c, sph_params + 3, 4, n_s)) return -1;
   world_moving_update(c);
   // world transforms of meshes / analytics for the current pose
   if (refresh_world(c, c->s_dt)) return -1;
@@ -549,6 +575,7 @@ int gf_detect_snapshot(gf_ctx *ctx, int64_t m, const double *centers, const floa
       upload_raw(c, c->ana_kind, ana_kind, n_a) || upload_raw(c, k.ana_world, ana_world, 64 * n_a) ||
       upload_raw(c, k.afam, ana_family, n_a) || upload_raw(c, c->fam_mask, mask, 65536))
     return -1;
+  if (set_split(c, radii, 1, m)) return -1;
   int rc = detect_now(c, margin, n_out);
   c->kt_bin_size = 0.0;
   if (rc) return -1;
@@ -688,13 +715,21 @@ int gf_run(gf_ctx *ctx, const gf_run_params *p, gf_run_result *r) {
       if (c->adopt_at <= s && do_adopt()) return -1;
     }
     // 3. launch the fill as soon as the count is known (no dT stall)
-    if (c->next_pending && !c->fill_done && cudaEventQuery(c->ev_count) == cudaSuccess && do_fill())
-      return -1;
+    if (c->next_pending && !c->fill_done) {
+      cudaError_t q = cudaEventQuery(c->ev_count);
+      if (q == cudaErrorNotReady) {
+        if (cudaPeekAtLastError() == cudaErrorNotReady) (void)cudaGetLastError();
+      } else if (do_fill()) {
+        return -1;
+      }
+    }
     sum_acs += c->acs.n;
     StepArgs a{p->h, {p->g[0], p->g[1], p->g[2]}, p->v_err, double(s) * p->h, s, i,
                (i == N - 1) ? p->write_acc : 0};
     if (dt_step(c, a)) return -1;
   }
+  // finish enqueuing an in-flight detection (its fill) inside this call
+  if (c->next_pending && !c->fill_done && do_fill()) return -1;
   // join the kT stream so in-flight detection work counts in the timed window
   GF_CHECK(c, cudaEventRecord(c->ev_snap, c->s_kt));
   GF_CHECK(c, cudaStreamWaitEvent(c->s_dt, c->ev_snap, 0));
@@ -712,6 +747,7 @@ int gf_run(gf_ctx *ctx, const gf_run_params *p, gf_run_result *r) {
     cudaEventDestroy(e.first);
     cudaEventDestroy(e.second);
   }
+  (void)cudaGetLastError();  // an unrecorded timing event is not an error
   r->kt_ms = kt_ms;
   if (c->prof) {
     prof_collect(c);

@@ -42,7 +42,9 @@ struct KtScratch {
   DBuf cell_start, cell_end;                         // uint32[nbins]
   DBuf tri_ranges;                                   // int32[n_t*6]
   DBuf tri_cnt, tri_start, tri_entries;              // tri CSR over bins
-  DBuf counts;       // uint32[3*n_s+1] per sphere SS / ST / SA counts
+  DBuf cursor;       // uint32[n_s] fill cursor of each sphere-sphere segment
+  DBuf tri_cursor;   // uint32 per cell
+  DBuf counts;       // uint64[3*n_s+1] per sphere SS / ST / SA counts
   DBuf offsets;      // uint64? uint32[3*n_s+1] exclusive scan
   DBuf cub_tmp;
   DBuf total;        // device copy of totals
@@ -69,6 +71,10 @@ struct Ctx {
   DBuf tri_owner, tri_local, tri_mat, tri_world;
   DBuf ana_owner, ana_kind, ana_local, ana_mat, ana_world;
   bool world_moving = true;  // any tri/ana owner not fixed
+  // enumeration split: spheres with radius > r_cut are paired by k_big
+  double r_cut = 0.0;
+  int64_t n_big = 0;
+  DBuf big_slots;
   // tables
   int n_mat = 0, n_pair_rows = 0;
   DBuf pair, beta;
@@ -129,7 +135,8 @@ struct Status {
   int pad;
 };
 
-constexpr uint32_t kHeavyThreshold = 192;  // incidences above which an owner is block-reduced
+constexpr uint32_t kHeavyThreshold = 192;
+constexpr int64_t kMaxCells = int64_t(1) << 25;  // enumeration-grid cell cap  // incidences above which an owner is block-reduced
 
 // helpers implemented in gf_context.cu
 int ensure(Ctx *c, DBuf &b, size_t bytes, cudaStream_t s, bool keep = false);

@@ -135,9 +135,10 @@ __global__ void k_minmax(int64_t n_pts, const double *pts, int64_t n_s, const fl
   }
 }
 
-// single thread: exact restatement of _grid_for's scalar arithmetic
+// single thread: exact restatement of _grid_for's scalar arithmetic, plus the
+// enumeration grid (cell = 2 (r_cut + margin), same growth rule, own cap)
 __global__ void k_grid(const unsigned long long *mm, int64_t n_pts, double margin, double bin_override,
-                       Grid *g) {
+                       double r_cut, long long max_cells, Grid *g) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   Grid out;
   out.valid = n_pts > 0;
@@ -160,89 +161,94 @@ __global__ void k_grid(const unsigned long long *mm, int64_t n_pts, double margi
     bin_size = mul(bin_size, 1.5);
   }
   out.inv_bin = 1.0 / bin_size;
-  if (!out.valid) { out.nb[0] = out.nb[1] = out.nb[2] = 1; }
+  // enumeration grid; r_cut <= 0 means "every sphere is small"
+  double rc = r_cut > 0.0 && r_cut < r_max ? r_cut : r_max;
+  out.r_cut = rc;
+  double cell = bin_override > 0.0 ? bin_size : 2.0 * (rc + margin);
+  if (cell <= 0.0) cell = 1.0;
+  for (;;) {
+    for (int ax = 0; ax < 3; ++ax) {
+      double cc = ceil(ext[ax] / cell);
+      out.nc[ax] = cc < 1.0 ? 1 : (long long)cc;
+    }
+    if (out.nc[0] * out.nc[1] * out.nc[2] <= max_cells) break;
+    cell *= 1.5;
+  }
+  out.inv_cell = 1.0 / cell;
+  if (!out.valid) {
+    out.nb[0] = out.nb[1] = out.nb[2] = 1;
+    out.nc[0] = out.nc[1] = out.nc[2] = 1;
+  }
   *g = out;
 }
 
 // ---------------------------------------------------------------------------
 // binning
 // ---------------------------------------------------------------------------
-__global__ void k_bin_keys(int64_t n, const double *centers, const Grid *gp, uint32_t *key,
-                           uint32_t *val) {
+// one key per sphere: its centre's enumeration cell; big spheres are kept out
+__global__ void k_bin_keys(int64_t n, const double *centers, const float4 *offr, const Grid *gp,
+                           uint32_t *key, uint32_t *val) {
   int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (i >= n) return;
   Grid g = *gp;
-  long long ix = axis_bin(centers[3 * i], g.glo[0], g.inv_bin, g.nb[0]);
-  long long iy = axis_bin(centers[3 * i + 1], g.glo[1], g.inv_bin, g.nb[1]);
-  long long iz = axis_bin(centers[3 * i + 2], g.glo[2], g.inv_bin, g.nb[2]);
-  key[i] = uint32_t((iz * g.nb[1] + iy) * g.nb[0] + ix);
   val[i] = uint32_t(i);
+  if (double(offr[i].w) > g.r_cut) { key[i] = 0xFFFFFFFFu; return; }
+  long long ix = axis_bin(centers[3 * i], g.glo[0], g.inv_cell, g.nc[0]);
+  long long iy = axis_bin(centers[3 * i + 1], g.glo[1], g.inv_cell, g.nc[1]);
+  long long iz = axis_bin(centers[3 * i + 2], g.glo[2], g.inv_cell, g.nc[2]);
+  key[i] = uint32_t((iz * g.nc[1] + iy) * g.nc[0] + ix);
 }
 
 __global__ void k_cell_bounds(int64_t n, const uint32_t *key, uint32_t *start, uint32_t *end) {
   int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (i >= n) return;
   uint32_t k = key[i];
+  if (k == 0xFFFFFFFFu) return;
   if (i == 0 || key[i - 1] != k) start[k] = uint32_t(i);
   if (i == n - 1 || key[i + 1] != k) end[k] = uint32_t(i + 1);
 }
 
-// triangle registration ranges (_kernels.py:333-351) and CSR over bins
-__global__ void k_tri_ranges(int64_t n_t, const double *tri, const Grid *gp, double margin,
-                             int *ranges, uint32_t *cnt) {
+// ---------------------------------------------------------------------------
+// enumeration-grid registration of triangles (fine cells overlapping the
+// triangle's margin-enlarged AABB; _kernels.py:333-351 on the fine grid)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void tri_cells(const Grid &g, const double *T, double margin, int r[6]) {
+  for (int ax = 0; ax < 3; ++ax) {
+    double lo = T[ax], hi = T[ax];
+    for (int v = 1; v < 3; ++v) {
+      double x = T[3 * v + ax];
+      if (x < lo) lo = x;
+      if (x > hi) hi = x;
+    }
+    r[2 * ax] = int(axis_bin(sub_(lo, margin), g.glo[ax], g.inv_cell, g.nc[ax]));
+    r[2 * ax + 1] = int(axis_bin(add(hi, margin), g.glo[ax], g.inv_cell, g.nc[ax]));
+  }
+}
+
+template <bool FILL>
+__global__ void k_tri_register(int64_t n_t, const double *tri, const Grid *gp, double margin,
+                               uint32_t *cnt, uint32_t *cursor, uint32_t *entries) {
   int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (t >= n_t) return;
   Grid g = *gp;
   int r[6];
-  for (int ax = 0; ax < 3; ++ax) {
-    double lo = tri[9 * t + ax], hi = tri[9 * t + ax];
-    for (int v = 1; v < 3; ++v) {
-      double x = tri[9 * t + 3 * v + ax];
-      if (x < lo) lo = x;
-      if (x > hi) hi = x;
-    }
-    long long l = (long long)mul(sub_(sub_(lo, margin), g.glo[ax]), g.inv_bin);
-    long long h = (long long)mul(sub_(add(hi, margin), g.glo[ax]), g.inv_bin);
-    if (l < 0) l = 0;
-    if (h < 0) h = 0;
-    if (l >= g.nb[ax]) l = g.nb[ax] - 1;
-    if (h >= g.nb[ax]) h = g.nb[ax] - 1;
-    r[2 * ax] = int(l);
-    r[2 * ax + 1] = int(h);
-  }
-  for (int q = 0; q < 6; ++q) ranges[6 * t + q] = r[q];
+  tri_cells(g, tri + 9 * t, margin, r);
   for (int iz = r[4]; iz <= r[5]; ++iz)
     for (int iy = r[2]; iy <= r[3]; ++iy)
-      for (int ix = r[0]; ix <= r[1]; ++ix)
-        atomicAdd(&cnt[(int64_t(iz) * g.nb[1] + iy) * g.nb[0] + ix], 1u);
-}
-
-// fill: tris listed per bin in ascending order (one thread per bin walks the
-// triangle list; triangle counts are small, so a bin-parallel scan is fine)
-__global__ void k_tri_fill(int64_t n_t, const int *ranges, const Grid *gp, const uint32_t *start,
-                           uint32_t *fillc, uint32_t *entries) {
-  // serial-in-t per bin keeps ascending triangle order within each bin
-  int64_t b = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  Grid g = *gp;
-  int64_t nbins = g.nb[0] * g.nb[1] * g.nb[2];
-  if (b >= nbins) return;
-  uint32_t s0 = start[b], s1 = start[b + 1];
-  if (s0 == s1) return;
-  long long ix = b % g.nb[0], iy = (b / g.nb[0]) % g.nb[1], iz = b / (g.nb[0] * g.nb[1]);
-  uint32_t w = s0;
-  for (int64_t t = 0; t < n_t && w < s1; ++t) {
-    const int *r = ranges + 6 * t;
-    if (ix >= r[0] && ix <= r[1] && iy >= r[2] && iy <= r[3] && iz >= r[4] && iz <= r[5])
-      entries[w++] = uint32_t(t);
-  }
-  (void)fillc;
+      for (int ix = r[0]; ix <= r[1]; ++ix) {
+        int64_t b = (int64_t(iz) * g.nc[1] + iy) * g.nc[0] + ix;
+        if (FILL) entries[atomicAdd(&cursor[b], 1u)] = uint32_t(t);
+        else atomicAdd(&cnt[b], 1u);
+      }
 }
 
 // ---------------------------------------------------------------------------
 // pair predicates (exact reference arithmetic)
 // ---------------------------------------------------------------------------
 
-// collect_sphere_pairs predicate for i < j (_kernels.py:305-321)
+// collect_sphere_pairs predicate (_kernels.py:305-321) for spheres i, j: the
+// distance test, then the reference's dedup bin (bin of the min corner of the
+// enlarged boxes' intersection) must lie in both registration ranges
 __device__ __forceinline__ bool ss_pair(const KtView &v, const Grid &g, uint32_t i, uint32_t j,
                                         const double ci[3], float ri_f, const long long lo_i[3],
                                         const long long hi_i[3], uint32_t oi, uint8_t fi) {
@@ -268,11 +274,14 @@ __device__ __forceinline__ bool ss_pair(const KtView &v, const Grid &g, uint32_t
   return true;
 }
 
-// collect_sphere_tri_pairs predicate evaluated in bin (bx, by, bz)
-// (_kernels.py:375-401)
+// collect_sphere_tri_pairs predicate (_kernels.py:375-401): distance test,
+// reported once -- in the enumeration cell (fx, fy, fz) holding the min
+// corner -- and only if the reference's dedup bin lies in both reference
+// registration ranges
 __device__ __forceinline__ bool st_pair(const KtView &v, const Grid &g, uint32_t t,
-                                        const double ci[3], float ri_f, uint32_t oi, uint8_t fi,
-                                        long long bx, long long by, long long bz) {
+                                        const double ci[3], float ri_f, const long long lo_i[3],
+                                        const long long hi_i[3], uint32_t oi, uint8_t fi,
+                                        long long fx, long long fy, long long fz) {
   if (oi == v.tri_owner[t]) return false;
   if (!v.mask[256 * fi + v.tfam[t]]) return false;
   const double *T = v.tri_world + 9 * size_t(t);
@@ -281,16 +290,30 @@ __device__ __forceinline__ bool st_pair(const KtView &v, const Grid &g, uint32_t
   double dx = sub_(ci[0], qx), dy = sub_(ci[1], qy), dz = sub_(ci[2], qz);
   double rr = add(double(ri_f), v.margin);
   if (add(add(mul(dx, dx), mul(dy, dy)), mul(dz, dz)) >= mul(rr, rr)) return false;
-  double mx = sub_(ci[0], rr), my = sub_(ci[1], rr), mz = sub_(ci[2], rr);
-  double tlx = sub_(fmin(fmin(T[0], T[3]), T[6]), v.margin);
-  double tly = sub_(fmin(fmin(T[1], T[4]), T[7]), v.margin);
-  double tlz = sub_(fmin(fmin(T[2], T[5]), T[8]), v.margin);
-  if (tlx > mx) mx = tlx;
-  if (tly > my) my = tly;
-  if (tlz > mz) mz = tlz;
-  return axis_bin(mx, g.glo[0], g.inv_bin, g.nb[0]) == bx &&
-         axis_bin(my, g.glo[1], g.inv_bin, g.nb[1]) == by &&
-         axis_bin(mz, g.glo[2], g.inv_bin, g.nb[2]) == bz;
+  double m[3] = {sub_(ci[0], rr), sub_(ci[1], rr), sub_(ci[2], rr)};
+  double tl[3] = {sub_(fmin(fmin(T[0], T[3]), T[6]), v.margin), sub_(fmin(fmin(T[1], T[4]), T[7]), v.margin),
+                  sub_(fmin(fmin(T[2], T[5]), T[8]), v.margin)};
+  long long f[3] = {fx, fy, fz};
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    if (tl[ax] > m[ax]) m[ax] = tl[ax];
+    if (axis_bin(m[ax], g.glo[ax], g.inv_cell, g.nc[ax]) != f[ax]) return false;
+  }
+  // reference registration range of the triangle on the reference grid
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    double lo = T[ax], hi = T[ax];
+    for (int q = 1; q < 3; ++q) {
+      double x = T[3 * q + ax];
+      if (x < lo) lo = x;
+      if (x > hi) hi = x;
+    }
+    long long tlo = axis_bin(sub_(lo, v.margin), g.glo[ax], g.inv_bin, g.nb[ax]);
+    long long thi = axis_bin(add(hi, v.margin), g.glo[ax], g.inv_bin, g.nb[ax]);
+    long long b = axis_bin(m[ax], g.glo[ax], g.inv_bin, g.nb[ax]);
+    if (b < lo_i[ax] || b > hi_i[ax] || b < tlo || b > thi) return false;
+  }
+  return true;
 }
 
 // collect_sphere_analytic_pairs predicate (_kernels.py:418-428)
@@ -303,10 +326,23 @@ __device__ __forceinline__ bool sa_pair(const KtView &v, uint32_t k, const doubl
   return !(gap >= add(double(ri_f), v.margin));
 }
 
-// one thread per sphere i: count (FILL=false) or emit (FILL=true) its pairs
+__device__ __forceinline__ void sort_segment_y(uint2 *out, unsigned long long w, unsigned long long cnt) {
+  for (unsigned long long p = 1; p < cnt; ++p) {
+    uint2 e = out[w + p];
+    unsigned long long q = p;
+    while (q > 0 && out[w + q - 1].y > e.y) { out[w + q] = out[w + q - 1]; --q; }
+    out[w + q] = e;
+  }
+}
+
+// One thread per sphere i.  Sphere-sphere pairs (i, j > i) between "small"
+// spheres from the 27-cell neighbourhood of the enumeration grid; sphere-
+// triangle pairs from the cells of i's enlarged box; sphere-analytic pairs by
+// brute force over the analytic list.  counts layout: [SS | ST | SA] x n.
 template <bool FILL>
 __global__ void __launch_bounds__(128) k_pairs(KtView v, unsigned long long *counts,
-                                               const unsigned long long *offsets, uint2 *out) {
+                                               const unsigned long long *offsets, uint2 *out,
+                                               unsigned *cursor) {
   int64_t i64 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   int64_t n = v.sph.n;
   if (i64 >= n) return;
@@ -322,23 +358,29 @@ __global__ void __launch_bounds__(128) k_pairs(KtView v, unsigned long long *cou
   uint8_t fi = v.sfam[i];
   long long lo_i[3], hi_i[3];
   sphere_range(g, ci, ri_f, v.margin, lo_i, hi_i);
-  long long cb[3];
-#pragma unroll
-  for (int ax = 0; ax < 3; ++ax) cb[ax] = axis_bin(ci[ax], g.glo[ax], g.inv_bin, g.nb[ax]);
 
-  // --- sphere-sphere ---
+  // --- sphere-sphere among small spheres ---
   unsigned long long cnt = 0;
-  unsigned long long w = FILL ? offsets[i64] : 0;
-  for (long long z = cb[2] - 1; z <= cb[2] + 1; ++z) {
-    if (z < 0 || z >= g.nb[2]) continue;
-    for (long long y = cb[1] - 1; y <= cb[1] + 1; ++y) {
-      if (y < 0 || y >= g.nb[1]) continue;
-      for (long long x = cb[0] - 1; x <= cb[0] + 1; ++x) {
-        if (x < 0 || x >= g.nb[0]) continue;
-        uint32_t b = uint32_t((z * g.nb[1] + y) * g.nb[0] + x);
-        uint32_t s0 = v.cell_start[b];
+  if (double(ri_f) <= g.r_cut) {
+    unsigned long long w = FILL ? offsets[i64] : 0;
+    long long cb[3];
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) cb[ax] = axis_bin(ci[ax], g.glo[ax], g.inv_cell, g.nc[ax]);
+    for (long long z = cb[2] - 1; z <= cb[2] + 1; ++z) {
+      if (z < 0 || z >= g.nc[2]) continue;
+      for (long long y = cb[1] - 1; y <= cb[1] + 1; ++y) {
+        if (y < 0 || y >= g.nc[1]) continue;
+        long long row = (z * g.nc[1] + y) * g.nc[0];
+        long long x0 = cb[0] > 0 ? cb[0] - 1 : 0, x1 = cb[0] + 1 < g.nc[0] ? cb[0] + 1 : g.nc[0] - 1;
+        // cells of one row are contiguous in the sorted order: one span
+        uint32_t s0 = 0xFFFFFFFFu, s1 = 0;
+        for (long long x = x0; x <= x1; ++x) {
+          uint32_t a = v.cell_start[row + x];
+          if (a == 0xFFFFFFFFu) continue;
+          if (s0 == 0xFFFFFFFFu) s0 = a;
+          s1 = v.cell_end[row + x];
+        }
         if (s0 == 0xFFFFFFFFu) continue;
-        uint32_t s1 = v.cell_end[b];
         for (uint32_t u = s0; u < s1; ++u) {
           uint32_t j = v.sph_sorted[u];
           if (j <= i) continue;
@@ -350,40 +392,33 @@ __global__ void __launch_bounds__(128) k_pairs(KtView v, unsigned long long *cou
       }
     }
   }
-  if (FILL && cnt > 1) {  // canonical order within the segment: ascending j
-    for (unsigned long long p = 1; p < cnt; ++p) {
-      uint2 e = out[w + p];
-      unsigned long long q = p;
-      while (q > 0 && out[w + q - 1].y > e.y) { out[w + q] = out[w + q - 1]; --q; }
-      out[w + q] = e;
-    }
-  }
-  if (!FILL) counts[i64] = cnt;
+  if (FILL) cursor[i64] = unsigned(cnt);
+  else counts[i64] = cnt;
 
-  // --- sphere-triangle: iterate the sphere's own registration bins ---
+  // --- sphere-triangle ---
   unsigned long long cst = 0;
   if (v.n_tri) {
     unsigned long long wt = FILL ? offsets[n + i64] : 0;
-    for (long long z = lo_i[2]; z <= hi_i[2]; ++z)
-      for (long long y = lo_i[1]; y <= hi_i[1]; ++y)
-        for (long long x = lo_i[0]; x <= hi_i[0]; ++x) {
-          int64_t b = (z * g.nb[1] + y) * g.nb[0] + x;
+    const double rr = add(double(ri_f), v.margin);
+    long long flo[3], fhi[3];
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      flo[ax] = axis_bin(sub_(ci[ax], rr), g.glo[ax], g.inv_cell, g.nc[ax]);
+      fhi[ax] = axis_bin(add(ci[ax], rr), g.glo[ax], g.inv_cell, g.nc[ax]);
+    }
+    for (long long z = flo[2]; z <= fhi[2]; ++z)
+      for (long long y = flo[1]; y <= fhi[1]; ++y)
+        for (long long x = flo[0]; x <= fhi[0]; ++x) {
+          int64_t b = (z * g.nc[1] + y) * g.nc[0] + x;
           for (uint32_t u = v.tri_start[b]; u < v.tri_start[b + 1]; ++u) {
             uint32_t t = v.tri_entries[u];
-            if (st_pair(v, g, t, ci, ri_f, oi, fi, x, y, z)) {
+            if (st_pair(v, g, t, ci, ri_f, lo_i, hi_i, oi, fi, x, y, z)) {
               if (FILL) out[wt + cst] = make_uint2(i, t | (1u << kKindShift));
               ++cst;
             }
           }
         }
-    if (FILL && cst > 1) {
-      for (unsigned long long p = 1; p < cst; ++p) {
-        uint2 e = out[wt + p];
-        unsigned long long q = p;
-        while (q > 0 && out[wt + q - 1].y > e.y) { out[wt + q] = out[wt + q - 1]; --q; }
-        out[wt + q] = e;
-      }
-    }
+    if (FILL && cst > 1) sort_segment_y(out, wt, cst);
   }
   if (!FILL) counts[n + i64] = cst;
 
@@ -397,6 +432,84 @@ __global__ void __launch_bounds__(128) k_pairs(KtView v, unsigned long long *cou
     }
   }
   if (!FILL) counts[2 * n + i64] = csa;
+}
+
+// One CTA per big sphere B (radius > r_cut): pairs with the small spheres of
+// the enumeration cells its reach covers, and with the bigs of higher slot.
+// Each pair is counted into / appended to the segment of its lower slot.
+template <bool FILL>
+__global__ void __launch_bounds__(128) k_big(KtView v, const uint32_t *bigs, int64_t n_big,
+                                             unsigned long long *counts,
+                                             const unsigned long long *offsets, uint2 *out,
+                                             unsigned *cursor) {
+  const Grid g = *v.grid;
+  if (!g.valid) return;
+  for (int64_t bi = blockIdx.x; bi < n_big; bi += gridDim.x) {
+    const uint32_t B = bigs[bi];
+    double cB[3] = {v.centers[3 * size_t(B)], v.centers[3 * size_t(B) + 1], v.centers[3 * size_t(B) + 2]};
+    const float rB = v.sph.offr[B].w;
+    const uint32_t oB = v.sph.owner[B];
+    const uint8_t fB = v.sfam[B];
+    long long loB[3], hiB[3];
+    sphere_range(g, cB, rB, v.margin, loB, hiB);
+    // reach: any partner j satisfies d < rB + r_cut + margin
+    const double reach = add(add(double(rB), g.r_cut), v.margin);
+    long long flo[3], fhi[3];
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      flo[ax] = axis_bin(sub_(cB[ax], reach), g.glo[ax], g.inv_cell, g.nc[ax]);
+      fhi[ax] = axis_bin(add(cB[ax], reach), g.glo[ax], g.inv_cell, g.nc[ax]);
+    }
+    const long long sx = fhi[0] - flo[0] + 1, sy = fhi[1] - flo[1] + 1, sz = fhi[2] - flo[2] + 1;
+    const long long ncell = sx * sy * sz;
+    for (long long q = threadIdx.x; q < ncell; q += blockDim.x) {
+      long long x = flo[0] + q % sx, y = flo[1] + (q / sx) % sy, z = flo[2] + q / (sx * sy);
+      long long b = (z * g.nc[1] + y) * g.nc[0] + x;
+      uint32_t s0 = v.cell_start[b];
+      if (s0 == 0xFFFFFFFFu) continue;
+      uint32_t s1 = v.cell_end[b];
+      for (uint32_t u = s0; u < s1; ++u) {
+        uint32_t j = v.sph_sorted[u];
+        // evaluate with the lower slot as `i` (the predicate is symmetric)
+        bool hit;
+        if (j < B) {
+          const double *cj = v.centers + 3 * size_t(j);
+          double cjv[3] = {cj[0], cj[1], cj[2]};
+          long long lo[3], hi[3];
+          sphere_range(g, cjv, v.sph.offr[j].w, v.margin, lo, hi);
+          hit = ss_pair(v, g, j, B, cjv, v.sph.offr[j].w, lo, hi, v.sph.owner[j], v.sfam[j]);
+        } else {
+          hit = ss_pair(v, g, B, j, cB, rB, loB, hiB, oB, fB);
+        }
+        if (!hit) continue;
+        uint32_t a = j < B ? j : B, c = j < B ? B : j;
+        if (FILL) out[offsets[a] + atomicAdd(&cursor[a], 1u)] = make_uint2(a, c);
+        else atomicAdd(&counts[a], 1ull);
+      }
+    }
+    for (int64_t q = threadIdx.x; q < n_big; q += blockDim.x) {
+      uint32_t j = bigs[q];
+      if (j <= B) continue;
+      if (!ss_pair(v, g, B, j, cB, rB, loB, hiB, oB, fB)) continue;
+      if (FILL) out[offsets[B] + atomicAdd(&cursor[B], 1u)] = make_uint2(B, j);
+      else atomicAdd(&counts[B], 1ull);
+    }
+  }
+}
+
+// canonical order inside every sphere-sphere segment (ascending b)
+__global__ void k_sort_ss(int64_t n, const unsigned long long *offsets, uint2 *out) {
+  int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  unsigned long long w = offsets[i], cnt = offsets[i + 1] - w;
+  if (cnt > 1) sort_segment_y(out, w, cnt);
+}
+
+__global__ void k_fill_u32(const Grid *gp, uint32_t *a, uint32_t value, int fine_plus_one) {
+  Grid g = *gp;
+  int64_t n = g.nc[0] * g.nc[1] * g.nc[2] + fine_plus_one;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    a[i] = value;
 }
 
 __global__ void k_bin_ranges(int64_t n, const double *centers, const float4 *offr, const Grid *gp,
@@ -541,13 +654,15 @@ int kt_detect_count(Ctx *c, double margin, cudaStream_t s) {
   KtScratch &k = c->kt;
   const int64_t n = c->n_sph, nt = c->n_tri;
   const int64_t n_pts = n + 3 * nt;
+  c->kt_margin = margin;
   if (ensure(c, k.grid, sizeof(Grid), s)) return -1;
   if (ensure(c, k.minmax, sizeof(unsigned long long) * 8, s)) return -1;
   if (ensure(c, k.bin_key, 4 * (n + 1), s) || ensure(c, k.bin_key_alt, 4 * (n + 1), s) ||
-      ensure(c, k.sph_val, 4 * (n + 1), s) || ensure(c, k.sph_val_alt, 4 * (n + 1), s))
+      ensure(c, k.sph_val, 4 * (n + 1), s) || ensure(c, k.sph_val_alt, 4 * (n + 1), s) ||
+      ensure(c, k.cursor, 4 * (n + 1), s))
     return -1;
-  if (ensure(c, k.cell_start, sizeof(uint32_t) * kMaxBins, s) ||
-      ensure(c, k.cell_end, sizeof(uint32_t) * kMaxBins, s))
+  if (ensure(c, k.cell_start, sizeof(uint32_t) * (kMaxCells + 1), s) ||
+      ensure(c, k.cell_end, sizeof(uint32_t) * (kMaxCells + 1), s))
     return -1;
   if (ensure(c, k.counts, sizeof(unsigned long long) * (3 * n + 1), s) ||
       ensure(c, k.offsets, sizeof(unsigned long long) * (3 * n + 1), s))
@@ -557,52 +672,57 @@ int kt_detect_count(Ctx *c, double margin, cudaStream_t s) {
   k_minmax_init<<<1, 32, 0, s>>>(mm);
   if (n) k_minmax<<<std::min<int64_t>(grid_for(n), 1184), kBlock, 0, s>>>(n, k.centers.as<double>(), n, c->sph_offr.as<float4>(), mm);
   if (nt) k_minmax<<<std::min<int64_t>(grid_for(3 * nt), 1184), kBlock, 0, s>>>(3 * nt, k.tri_world.as<double>(), 0, nullptr, mm);
-  k_grid<<<1, 1, 0, s>>>(mm, n_pts, margin, c->kt_bin_size, k.grid.as<Grid>());
+  k_grid<<<1, 1, 0, s>>>(mm, n_pts, margin, c->kt_bin_size, c->r_cut, (long long)kMaxCells,
+                         k.grid.as<Grid>());
+  const Grid *gp = k.grid.as<Grid>();
   if (n) {
-    k_bin_keys<<<grid_for(n), kBlock, 0, s>>>(n, k.centers.as<double>(), k.grid.as<Grid>(),
+    k_bin_keys<<<grid_for(n), kBlock, 0, s>>>(n, k.centers.as<double>(), c->sph_offr.as<float4>(), gp,
                                              k.bin_key.as<uint32_t>(), k.sph_val.as<uint32_t>());
     size_t tmp = 0;
     cub::DoubleBuffer<uint32_t> dk(k.bin_key.as<uint32_t>(), k.bin_key_alt.as<uint32_t>());
     cub::DoubleBuffer<uint32_t> dv(k.sph_val.as<uint32_t>(), k.sph_val_alt.as<uint32_t>());
-    cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, int(n), 0, 22, s);
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, int(n), 0, 32, s);
     if (ensure(c, k.cub_tmp, tmp + 16, s)) return -1;
-    GF_CHECK(c, cub::DeviceRadixSort::SortPairs(k.cub_tmp.p, tmp, dk, dv, int(n), 0, 22, s));
+    GF_CHECK(c, cub::DeviceRadixSort::SortPairs(k.cub_tmp.p, tmp, dk, dv, int(n), 0, 32, s));
     if (dk.Current() != k.bin_key.as<uint32_t>()) {
       std::swap(k.bin_key, k.bin_key_alt);
       std::swap(k.sph_val, k.sph_val_alt);
     }
-    GF_CHECK(c, cudaMemsetAsync(k.cell_start.p, 0xFF, sizeof(uint32_t) * kMaxBins, s));
+    k_fill_u32<<<592, 256, 0, s>>>(gp, k.cell_start.as<uint32_t>(), 0xFFFFFFFFu, 0);
     k_cell_bounds<<<grid_for(n), kBlock, 0, s>>>(n, k.bin_key.as<uint32_t>(),
                                                 k.cell_start.as<uint32_t>(), k.cell_end.as<uint32_t>());
   }
   if (nt) {
-    if (ensure(c, k.tri_ranges, sizeof(int) * 6 * nt, s) ||
-        ensure(c, k.tri_cnt, sizeof(uint32_t) * (kMaxBins + 1), s) ||
-        ensure(c, k.tri_start, sizeof(uint32_t) * (kMaxBins + 1), s))
+    if (ensure(c, k.tri_cnt, sizeof(uint32_t) * (kMaxCells + 1), s) ||
+        ensure(c, k.tri_start, sizeof(uint32_t) * (kMaxCells + 1), s) ||
+        ensure(c, k.tri_cursor, sizeof(uint32_t) * (kMaxCells + 1), s))
       return -1;
-    GF_CHECK(c, cudaMemsetAsync(k.tri_cnt.p, 0, sizeof(uint32_t) * (kMaxBins + 1), s));
-    k_tri_ranges<<<grid_for(nt), kBlock, 0, s>>>(nt, k.tri_world.as<double>(), k.grid.as<Grid>(),
-                                                margin, k.tri_ranges.as<int>(), k.tri_cnt.as<uint32_t>());
+    k_fill_u32<<<592, 256, 0, s>>>(gp, k.tri_cnt.as<uint32_t>(), 0u, 1);
+    k_tri_register<false><<<grid_for(nt), kBlock, 0, s>>>(nt, k.tri_world.as<double>(), gp, margin,
+                                                         k.tri_cnt.as<uint32_t>(), nullptr, nullptr);
     size_t tmp = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tmp, k.tri_cnt.as<uint32_t>(), k.tri_start.as<uint32_t>(),
-                                  kMaxBins + 1, s);
+                                  kMaxCells + 1, s);
     if (ensure(c, k.cub_tmp, tmp + 16, s, false)) return -1;
     GF_CHECK(c, cub::DeviceScan::ExclusiveSum(k.cub_tmp.p, tmp, k.tri_cnt.as<uint32_t>(),
-                                              k.tri_start.as<uint32_t>(), kMaxBins + 1, s));
-    // total registrations are bounded by n_t * (bins a triangle spans); size
-    // conservatively from the count array's last prefix after a small sync
+                                              k.tri_start.as<uint32_t>(), kMaxCells + 1, s));
     uint32_t h_total = 0;
-    GF_CHECK(c, cudaMemcpyAsync(&h_total, k.tri_start.as<uint32_t>() + kMaxBins, 4,
+    GF_CHECK(c, cudaMemcpyAsync(&h_total, k.tri_start.as<uint32_t>() + kMaxCells, 4,
                                 cudaMemcpyDeviceToHost, s));
     GF_CHECK(c, cudaStreamSynchronize(s));
     if (ensure(c, k.tri_entries, sizeof(uint32_t) * (h_total + 1), s)) return -1;
-    k_tri_fill<<<grid_for(kMaxBins), kBlock, 0, s>>>(nt, k.tri_ranges.as<int>(), k.grid.as<Grid>(),
-                                                    k.tri_start.as<uint32_t>(), nullptr,
-                                                    k.tri_entries.as<uint32_t>());
+    GF_CHECK(c, cudaMemcpyAsync(k.tri_cursor.p, k.tri_start.p, sizeof(uint32_t) * (kMaxCells + 1),
+                                cudaMemcpyDeviceToDevice, s));
+    k_tri_register<true><<<grid_for(nt), kBlock, 0, s>>>(nt, k.tri_world.as<double>(), gp, margin,
+                                                        nullptr, k.tri_cursor.as<uint32_t>(),
+                                                        k.tri_entries.as<uint32_t>());
   }
   KtView v = kt_view(c, margin);
   unsigned long long *cnt = k.counts.as<unsigned long long>();
-  if (n) k_pairs<false><<<grid_for(n, 128), 128, 0, s>>>(v, cnt, nullptr, nullptr);
+  if (n) k_pairs<false><<<grid_for(n, 128), 128, 0, s>>>(v, cnt, nullptr, nullptr, nullptr);
+  if (c->n_big)
+    k_big<false><<<unsigned(std::min<int64_t>(c->n_big, 4096)), 128, 0, s>>>(
+        v, c->big_slots.as<uint32_t>(), c->n_big, cnt, nullptr, nullptr, nullptr);
   GF_CHECK(c, cudaMemsetAsync(cnt + 3 * n, 0, sizeof(unsigned long long), s));
   size_t tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, k.offsets.as<unsigned long long>(), int(3 * n + 1), s);
@@ -631,11 +751,17 @@ int kt_detect_fill(Ctx *c, Acs &out, cudaStream_t s) {
     out.cap = cap;
   }
   if (n && total) {
-    KtView v = kt_view(c, 0.0);
-    // margin is baked into the count pass only through the grid; re-read it
-    v.margin = c->kt_margin;
-    k_pairs<true><<<grid_for(n, 128), 128, 0, s>>>(v, nullptr, k.offsets.as<unsigned long long>(),
-                                                   out.ids.as<uint2>());
+    KtView v = kt_view(c, c->kt_margin);
+    const unsigned long long *off = k.offsets.as<unsigned long long>();
+    unsigned *cur = k.cursor.as<unsigned>();
+    k_pairs<true><<<grid_for(n, 128), 128, 0, s>>>(v, nullptr, off, out.ids.as<uint2>(), cur);
+    if (c->n_big) {
+      k_big<true><<<unsigned(std::min<int64_t>(c->n_big, 4096)), 128, 0, s>>>(
+          v, c->big_slots.as<uint32_t>(), c->n_big, nullptr, off, out.ids.as<uint2>(), cur);
+      k_sort_ss<<<grid_for(n), kBlock, 0, s>>>(n, off, out.ids.as<uint2>());
+    } else {
+      k_sort_ss<<<grid_for(n), kBlock, 0, s>>>(n, off, out.ids.as<uint2>());
+    }
   }
   GF_CHECK(c, cudaGetLastError());
   return 0;

@@ -225,3 +225,31 @@ def test_async_schedule_matches_oracle_stepper():
     assert np.array_equal(out["lin_vel"], st.s["lin_vel"])
     assert rr.touching == st.last_touching
     ctx.close()
+
+
+def test_detect_polydisperse_with_big_spheres_vs_oracle():
+    """Spheres far above 2x the median radius take the k_big path; the pair
+    list must still equal the reference's (oracle) bit for bit."""
+    for seed in range(6):
+        rng = np.random.default_rng(100 + seed)
+        n = 3000
+        centers = rng.uniform(-0.3, 0.3, (n, 3))
+        radii = rng.uniform(0.008, 0.012, n)
+        big = rng.choice(n, 12, replace=False)
+        radii[big] = rng.uniform(0.03, 0.09, big.size)
+        radii = radii.astype(np.float32)
+        margin = float(rng.uniform(0.0, 0.004))
+        owners = np.arange(n)
+        owners[1::7] = owners[0::7][: owners[1::7].size]  # some clump-mates
+        tri = rng.uniform(-0.3, 0.3, (40, 9))
+        snap = dict(sph_center=centers, sph_radius=radii, sph_geom=np.arange(n), sph_owner=owners,
+                    sph_family=np.zeros(n, np.uint8), tri_world=tri, tri_geom=np.arange(n, n + 40),
+                    tri_owner=np.full(40, 10 ** 7), tri_family=np.zeros(40, np.uint8),
+                    ana_world=np.zeros((0, 8)), ana_kind=np.zeros(0, np.uint8),
+                    ana_geom=np.zeros(0, np.int64), ana_owner=np.zeros(0, np.int64),
+                    ana_family=np.zeros(0, np.uint8), mask=np.ones((256, 256), bool))
+        want = O.detect_contacts(snap, margin)
+        got = B.detect_contacts(B.DetectionSnapshot(**snap), margin)
+        assert np.array_equal(got.kind, want["kind"]), seed
+        assert np.array_equal(got.geom_a, want["geom_a"]), seed
+        assert np.array_equal(got.geom_b, want["geom_b"]), seed
