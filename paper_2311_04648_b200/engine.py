@@ -540,8 +540,9 @@ class Simulator:
         sa = self._geom_slot[ca.geom_a] if n else np.zeros(0, np.int64)
         sb = self._geom_slot[ca.geom_b] if n else np.zeros(0, np.int64)
         if n:
-            sa = self._sph_u2d[sa]
-            sb = np.where(kind == 0, self._sph_u2d[np.where(kind == 0, sb, 0)], sb)
+            sa, sb, wild = self._orient(kind, self._sph_u2d[sa],
+                                        np.where(kind == 0, self._sph_u2d[np.where(kind == 0, sb, 0)], sb),
+                                        wild)
             order = np.lexsort((sb, sa, kind))
             kind, sa, sb, wild = kind[order], sa[order], sb[order], wild[order]
         self._ctx.call("gf_set_acs", C.c_int64(n), P(_lib.carr(kind, np.uint8)),
@@ -596,8 +597,9 @@ class Simulator:
             return self._acs0
         kind, sa, sb, wild = self._acs_arrays()
         if kind.size:
-            sa = self._sph_d2u[sa]
-            sb = np.where(kind == 0, self._sph_d2u[np.where(kind == 0, sb, 0)], sb)
+            sa, sb, wild = self._orient(kind, self._sph_d2u[sa],
+                                        np.where(kind == 0, self._sph_d2u[np.where(kind == 0, sb, 0)], sb),
+                                        wild)
         tabs = (self._sph_geom, self._tri_geom, self._ana_geom)
         ga = self._sph_geom[sa] if kind.size else np.zeros(0, np.int64)
         gb = np.zeros(kind.shape[0], np.int64)
@@ -609,6 +611,19 @@ class Simulator:
         for i, name in enumerate(self.model.wildcards):
             ca.wildcards[name] = wild[:, i].copy()
         return ca.canonicalize() if self.reorder else ca
+
+    @staticmethod
+    def _orient(kind, sa, sb, wild):
+        """Sphere-sphere pairs are stored as (lower slot, higher slot); when a
+        slot permutation flips a pair, A and B swap roles and the tangential
+        history (displacement of A relative to B, forces.py:111-118) changes
+        sign.  delta_time is orientation-free."""
+        flip = (kind == 0) & (sa > sb)
+        if flip.any():
+            sa, sb = np.where(flip, sb, sa), np.where(flip, sa, sb)
+            wild = wild.copy()
+            wild[flip, :3] = -wild[flip, :3]
+        return sa, sb, wild
 
     @_acs.setter
     def _acs(self, value):
