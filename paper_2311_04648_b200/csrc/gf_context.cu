@@ -245,7 +245,8 @@ void gf_destroy(gf_ctx *ctx) {
                   &c->kt.minmax, &c->kt.bin_key, &c->kt.bin_key_alt, &c->kt.sph_val, &c->kt.sph_val_alt,
                   &c->kt.cell_start, &c->kt.cell_end, &c->kt.tri_ranges, &c->kt.tri_cnt,
                   &c->kt.tri_start, &c->kt.tri_entries, &c->kt.counts, &c->kt.offsets, &c->kt.cub_tmp,
-                  &c->kt.total, &c->kt.cursor, &c->kt.tri_cursor, &c->big_slots};
+                  &c->kt.total, &c->kt.cursor, &c->kt.tri_cursor, &c->big_slots, &c->kt.sc,
+                  &c->kt.sm, &c->kt.tmp, &c->kt.tmp_n, &c->acs.seg, &c->acs_next.seg};
   for (DBuf *b : bufs) release(*b);
   if (c->h_status) cudaFreeHost(c->h_status);
   cudaEvent_t evs[] = {c->ev_snap, c->ev_ca, c->ev_adopted, c->ev_count, c->t0, c->t1};
@@ -506,7 +507,7 @@ int gf_set_acs(gf_ctx *ctx, int64_t n, const uint8_t *kind, const int64_t *slot_
     if (wild) GF_CHECK(c, cudaMemcpy(c->acs.wild.p, wild, 4 * W * n, cudaMemcpyHostToDevice));
     else GF_CHECK(c, cudaMemset(c->acs.wild.p, 0, 4 * W * n));
   }
-  if (build_incidence(c, c->s_dt)) return -1;
+  if (build_segments(c, c->acs, c->s_dt) || build_incidence(c, c->s_dt)) return -1;
   GF_CHECK(c, cudaStreamSynchronize(c->s_dt));
   c->ca_updates = std::max<int64_t>(c->ca_updates, 1);
   return 0;

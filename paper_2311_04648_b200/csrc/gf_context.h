@@ -26,6 +26,7 @@ struct Acs {
   int64_t n = 0, cap = 0;
   DBuf ids;    // uint2[cap]
   DBuf wild;   // float[cap * W]
+  DBuf seg;    // uint64[3 n_sph + 1]: start of each (kind, sphere A) segment
 };
 
 struct KtScratch {
@@ -42,7 +43,10 @@ struct KtScratch {
   DBuf cell_start, cell_end;                         // uint32[nbins]
   DBuf tri_ranges;                                   // int32[n_t*6]
   DBuf tri_cnt, tri_start, tri_entries;              // tri CSR over bins
-  DBuf cursor;       // uint32[n_s] fill cursor of each sphere-sphere segment
+  DBuf cursor;       // uint32[3 n_s] fill cursor of each (kind, sphere) segment
+  DBuf sc, sm;       // cell-sorted copies: double4 (centre, radius), uint4 (slot, owner, family)
+  DBuf tmp, tmp_n;   // scratch pair list (uint2) and its append counter
+  int64_t tmp_cap = 0;
   DBuf tri_cursor;   // uint32 per cell
   DBuf counts;       // uint64[3*n_s+1] per sphere SS / ST / SA counts
   DBuf offsets;      // uint64? uint32[3*n_s+1] exclusive scan
@@ -165,6 +169,7 @@ int kt_detect_fill(Ctx *c, Acs &out, cudaStream_t s);
 int kt_bin_ranges(Ctx *c, double margin, int64_t *h_out);
 int adopt_acs(Ctx *c, cudaStream_t s);                   // merge history + incidence lists
 int build_incidence(Ctx *c, cudaStream_t s);
+int build_segments(Ctx *c, Acs &a, cudaStream_t s);
 int merge_host(Ctx *c, int64_t n_old, const uint32_t *old_ids, const float *old_wild, int64_t n_new,
                const uint32_t *new_ids, int W, float *out_wild);
 int refresh_world(Ctx *c, cudaStream_t s);               // tri/ana world from owner pose

@@ -335,70 +335,155 @@ __device__ __forceinline__ void sort_segment_y(uint2 *out, unsigned long long w,
   }
 }
 
-// One thread per sphere i.  Sphere-sphere pairs (i, j > i) between "small"
-// spheres from the 27-cell neighbourhood of the enumeration grid; sphere-
-// triangle pairs from the cells of i's enlarged box; sphere-analytic pairs by
-// brute force over the analytic list.  counts layout: [SS | ST | SA] x n.
-template <bool FILL>
-__global__ void __launch_bounds__(128) k_pairs(KtView v, unsigned long long *counts,
-                                               const unsigned long long *offsets, uint2 *out,
-                                               unsigned *cursor) {
-  int64_t i64 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  int64_t n = v.sph.n;
-  if (i64 >= n) return;
-  const Grid g = *v.grid;
-  if (!g.valid) {
-    if (!FILL) { counts[i64] = 0; counts[n + i64] = 0; counts[2 * n + i64] = 0; }
-    return;
+// warp-aggregated append of one pair per active lane (all 32 lanes call it)
+__device__ __forceinline__ void append_pair(bool hit, uint2 e, uint2 *tmp, unsigned long long *tmp_n,
+                                            unsigned long long cap) {
+  unsigned m = __ballot_sync(0xffffffffu, hit);
+  if (!m) return;
+  int lane = threadIdx.x & 31;
+  int leader = __ffs(m) - 1;
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(tmp_n, (unsigned long long)__popc(m));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (hit) {
+    unsigned long long pos = base + __popc(m & ((1u << lane) - 1u));
+    if (pos < cap) tmp[pos] = e;
   }
-  uint32_t i = uint32_t(i64);
-  double ci[3] = {v.centers[3 * i64], v.centers[3 * i64 + 1], v.centers[3 * i64 + 2]};
-  float ri_f = v.sph.offr[i].w;
-  uint32_t oi = v.sph.owner[i];
-  uint8_t fi = v.sfam[i];
-  long long lo_i[3], hi_i[3];
-  sphere_range(g, ci, ri_f, v.margin, lo_i, hi_i);
+}
 
-  // --- sphere-sphere among small spheres ---
-  unsigned long long cnt = 0;
-  if (double(ri_f) <= g.r_cut) {
-    unsigned long long w = FILL ? offsets[i64] : 0;
-    long long cb[3];
+// cell-sorted copies of the snapshot spheres: (centre, radius), (slot, owner, family)
+__global__ void k_gather_sorted(int64_t n, const uint32_t *sorted, const double *centers,
+                                const float4 *offr, const uint32_t *owner, const uint8_t *sfam,
+                                double4 *sc, uint4 *sm) {
+  int64_t u = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (u >= n) return;
+  uint32_t i = sorted[u];
+  sc[u] = make_double4(centers[3 * size_t(i)], centers[3 * size_t(i) + 1], centers[3 * size_t(i) + 2],
+                       double(offr[i].w));
+  sm[u] = make_uint4(i, owner[i], sfam[i], 0u);
+}
+
+// exact sphere-sphere predicate (_kernels.py:305-321) on cell-sorted copies;
+// (l, h) are the lower / higher slot, matching the reference's i < j order
+__device__ __forceinline__ bool ss_pair_sorted(const KtView &v, const Grid &g, const double4 &cl,
+                                               const uint4 &ml, const double4 &ch, const uint4 &mh) {
+  if (ml.y == mh.y) return false;
+  if (!v.mask[256 * ml.z + mh.z]) return false;
+  double dx = sub_(cl.x, ch.x), dy = sub_(cl.y, ch.y), dz = sub_(cl.z, ch.z);
+  double ri = add(cl.w, v.margin);
+  double rj = add(ch.w, v.margin);
+  double rr = sub_(add(ri, rj), v.margin);
+  if (add(add(mul(dx, dx), mul(dy, dy)), mul(dz, dz)) >= mul(rr, rr)) return false;
+  double ci[3] = {cl.x, cl.y, cl.z}, cj[3] = {ch.x, ch.y, ch.z};
+  long long lo_i[3], hi_i[3], lo_j[3], hi_j[3];
+  sphere_range(g, ci, float(cl.w), v.margin, lo_i, hi_i);
+  sphere_range(g, cj, float(ch.w), v.margin, lo_j, hi_j);
 #pragma unroll
-    for (int ax = 0; ax < 3; ++ax) cb[ax] = axis_bin(ci[ax], g.glo[ax], g.inv_cell, g.nc[ax]);
-    for (long long z = cb[2] - 1; z <= cb[2] + 1; ++z) {
-      if (z < 0 || z >= g.nc[2]) continue;
-      for (long long y = cb[1] - 1; y <= cb[1] + 1; ++y) {
-        if (y < 0 || y >= g.nc[1]) continue;
-        long long row = (z * g.nc[1] + y) * g.nc[0];
-        long long x0 = cb[0] > 0 ? cb[0] - 1 : 0, x1 = cb[0] + 1 < g.nc[0] ? cb[0] + 1 : g.nc[0] - 1;
-        // cells of one row are contiguous in the sorted order: one span
-        uint32_t s0 = 0xFFFFFFFFu, s1 = 0;
-        for (long long x = x0; x <= x1; ++x) {
-          uint32_t a = v.cell_start[row + x];
-          if (a == 0xFFFFFFFFu) continue;
-          if (s0 == 0xFFFFFFFFu) s0 = a;
-          s1 = v.cell_end[row + x];
-        }
-        if (s0 == 0xFFFFFFFFu) continue;
-        for (uint32_t u = s0; u < s1; ++u) {
-          uint32_t j = v.sph_sorted[u];
-          if (j <= i) continue;
-          if (ss_pair(v, g, i, j, ci, ri_f, lo_i, hi_i, oi, fi)) {
-            if (FILL) out[w + cnt] = make_uint2(i, j);
-            ++cnt;
+  for (int ax = 0; ax < 3; ++ax) {
+    double m = fmax(sub_(ci[ax], ri), sub_(cj[ax], rj));
+    long long b = axis_bin(m, g.glo[ax], g.inv_bin, g.nb[ax]);
+    if (b < lo_i[ax] || b > hi_i[ax] || b < lo_j[ax] || b > hi_j[ax]) return false;
+  }
+  return true;
+}
+
+// Sphere-sphere pairs among small spheres, one thread per cell-sorted sphere,
+// half stencil: the later spheres of its own cell plus the 13 forward
+// neighbour cells, so every unordered pair is evaluated exactly once.  Hits
+// are counted into the segment of the lower slot and appended to a scratch
+// list (placed into canonical segments by k_place / k_sort_seg).
+__global__ void __launch_bounds__(128) k_pairs_ss(KtView v, const double4 *sc, const uint4 *sm,
+                                                  unsigned long long *counts, uint2 *tmp,
+                                                  unsigned long long *tmp_n, unsigned long long cap) {
+  int64_t u64 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const Grid g = *v.grid;
+  bool active = u64 < v.sph.n && g.valid;
+  uint32_t key = active ? v.bin_key[u64] : 0xFFFFFFFFu;
+  active = active && key != 0xFFFFFFFFu;
+  double4 c0 = make_double4(0, 0, 0, 0);
+  uint4 m0 = make_uint4(0, 0, 0, 0);
+  long long cx = 0, cy = 0, cz = 0;
+  if (active) {
+    c0 = sc[u64];
+    m0 = sm[u64];
+    cx = key % g.nc[0];
+    cy = (key / g.nc[0]) % g.nc[1];
+    cz = key / (g.nc[0] * g.nc[1]);
+  }
+  // spans: own cell after u, then rows (dz, dy) = (0,0) x+1 only, (0,1), (1,-1), (1,0), (1,1)
+  for (int span = 0; span < 6; ++span) {
+    uint32_t s0 = 0, s1 = 0;
+    if (active) {
+      if (span == 0) {
+        s0 = uint32_t(u64) + 1;
+        s1 = v.cell_end[key];
+      } else {
+        long long dz = span >= 3 ? 1 : 0;
+        long long dy = span == 2 ? 1 : (span >= 3 ? span - 4 : 0);
+        long long x0 = span == 1 ? cx + 1 : cx - 1, x1 = cx + 1;
+        long long y = cy + dy, z = cz + dz;
+        if (x0 < 0) x0 = 0;
+        if (x1 >= g.nc[0]) x1 = g.nc[0] - 1;
+        if (y >= 0 && y < g.nc[1] && z < g.nc[2] && x0 <= x1) {
+          long long row = (z * g.nc[1] + y) * g.nc[0];
+          uint32_t a0 = 0xFFFFFFFFu;
+          for (long long x = x0; x <= x1; ++x) {
+            uint32_t st = v.cell_start[row + x];
+            if (st == 0xFFFFFFFFu) continue;
+            if (a0 == 0xFFFFFFFFu) a0 = st;
+            s1 = v.cell_end[row + x];
           }
+          s0 = a0 == 0xFFFFFFFFu ? 0 : a0;
+          if (a0 == 0xFFFFFFFFu) s1 = 0;
         }
       }
     }
+    // warp-uniform trip count keeps the ballot in append_pair convergent
+    uint32_t len = s1 > s0 ? s1 - s0 : 0;
+    uint32_t maxlen = len;
+    for (int off = 16; off > 0; off >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, off));
+    for (uint32_t t = 0; t < maxlen; ++t) {
+      bool hit = false;
+      uint2 e = make_uint2(0, 0);
+      if (t < len) {
+        uint32_t w = s0 + t;
+        double4 c1 = sc[w];
+        uint4 m1 = sm[w];
+        bool lower = m0.x < m1.x;
+        hit = lower ? ss_pair_sorted(v, g, c0, m0, c1, m1) : ss_pair_sorted(v, g, c1, m1, c0, m0);
+        if (hit) {
+          uint32_t a = lower ? m0.x : m1.x, b = lower ? m1.x : m0.x;
+          e = make_uint2(a, b);
+          atomicAdd(&counts[a], 1ull);
+        }
+      }
+      append_pair(hit, e, tmp, tmp_n, cap);
+    }
   }
-  if (FILL) cursor[i64] = unsigned(cnt);
-  else counts[i64] = cnt;
+}
 
-  // --- sphere-triangle ---
-  unsigned long long cst = 0;
-  if (v.n_tri) {
-    unsigned long long wt = FILL ? offsets[n + i64] : 0;
+// Sphere-triangle and sphere-analytic pairs, one thread per sphere slot.
+__global__ void __launch_bounds__(128) k_pairs_other(KtView v, unsigned long long *counts, uint2 *tmp,
+                                                     unsigned long long *tmp_n, unsigned long long cap) {
+  int64_t i64 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const int64_t n = v.sph.n;
+  const Grid g = *v.grid;
+  const bool active = i64 < n && g.valid;
+  uint32_t i = uint32_t(active ? i64 : 0);
+  double ci[3] = {0, 0, 0};
+  float ri_f = 0.f;
+  uint32_t oi = 0;
+  uint8_t fi = 0;
+  long long lo_i[3] = {0, 0, 0}, hi_i[3] = {0, 0, 0};
+  if (active) {
+    ci[0] = v.centers[3 * i64]; ci[1] = v.centers[3 * i64 + 1]; ci[2] = v.centers[3 * i64 + 2];
+    ri_f = v.sph.offr[i].w;
+    oi = v.sph.owner[i];
+    fi = v.sfam[i];
+    sphere_range(g, ci, ri_f, v.margin, lo_i, hi_i);
+  }
+  unsigned long long cst = 0, csa = 0;
+  if (v.n_tri && active) {
     const double rr = add(double(ri_f), v.margin);
     long long flo[3], fhi[3];
 #pragma unroll
@@ -413,52 +498,45 @@ __global__ void __launch_bounds__(128) k_pairs(KtView v, unsigned long long *cou
           for (uint32_t u = v.tri_start[b]; u < v.tri_start[b + 1]; ++u) {
             uint32_t t = v.tri_entries[u];
             if (st_pair(v, g, t, ci, ri_f, lo_i, hi_i, oi, fi, x, y, z)) {
-              if (FILL) out[wt + cst] = make_uint2(i, t | (1u << kKindShift));
+              unsigned long long pos = atomicAdd(tmp_n, 1ull);
+              if (pos < cap) tmp[pos] = make_uint2(i, t | (1u << kKindShift));
               ++cst;
             }
           }
         }
-    if (FILL && cst > 1) sort_segment_y(out, wt, cst);
   }
-  if (!FILL) counts[n + i64] = cst;
-
-  // --- sphere-analytic (brute force over the small analytic list) ---
-  unsigned long long csa = 0;
-  unsigned long long wa = FILL ? offsets[2 * n + i64] : 0;
+  // analytic list: warp-uniform loop
   for (int64_t k = 0; k < v.n_ana; ++k) {
-    if (sa_pair(v, uint32_t(k), ci, ri_f, oi, fi)) {
-      if (FILL) out[wa + csa] = make_uint2(i, uint32_t(k) | (2u << kKindShift));
-      ++csa;
-    }
+    bool hit = active && sa_pair(v, uint32_t(k), ci, ri_f, oi, fi);
+    if (hit) ++csa;
+    append_pair(hit, make_uint2(i, uint32_t(k) | (2u << kKindShift)), tmp, tmp_n, cap);
   }
-  if (!FILL) counts[2 * n + i64] = csa;
+  if (active) {
+    counts[n + i64] = cst;
+    counts[2 * n + i64] = csa;
+  }
 }
 
 // One CTA per big sphere B (radius > r_cut): pairs with the small spheres of
 // the enumeration cells its reach covers, and with the bigs of higher slot.
-// Each pair is counted into / appended to the segment of its lower slot.
-template <bool FILL>
 __global__ void __launch_bounds__(128) k_big(KtView v, const uint32_t *bigs, int64_t n_big,
-                                             unsigned long long *counts,
-                                             const unsigned long long *offsets, uint2 *out,
-                                             unsigned *cursor) {
+                                             const double4 *sc, const uint4 *sm,
+                                             unsigned long long *counts, uint2 *tmp,
+                                             unsigned long long *tmp_n, unsigned long long cap) {
   const Grid g = *v.grid;
   if (!g.valid) return;
   for (int64_t bi = blockIdx.x; bi < n_big; bi += gridDim.x) {
     const uint32_t B = bigs[bi];
-    double cB[3] = {v.centers[3 * size_t(B)], v.centers[3 * size_t(B) + 1], v.centers[3 * size_t(B) + 2]};
-    const float rB = v.sph.offr[B].w;
-    const uint32_t oB = v.sph.owner[B];
-    const uint8_t fB = v.sfam[B];
-    long long loB[3], hiB[3];
-    sphere_range(g, cB, rB, v.margin, loB, hiB);
-    // reach: any partner j satisfies d < rB + r_cut + margin
-    const double reach = add(add(double(rB), g.r_cut), v.margin);
+    const double4 cB = make_double4(v.centers[3 * size_t(B)], v.centers[3 * size_t(B) + 1],
+                                    v.centers[3 * size_t(B) + 2], double(v.sph.offr[B].w));
+    const uint4 mB = make_uint4(B, v.sph.owner[B], v.sfam[B], 0u);
+    const double reach = add(add(cB.w, g.r_cut), v.margin);
+    double cbv[3] = {cB.x, cB.y, cB.z};
     long long flo[3], fhi[3];
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
-      flo[ax] = axis_bin(sub_(cB[ax], reach), g.glo[ax], g.inv_cell, g.nc[ax]);
-      fhi[ax] = axis_bin(add(cB[ax], reach), g.glo[ax], g.inv_cell, g.nc[ax]);
+      flo[ax] = axis_bin(sub_(cbv[ax], reach), g.glo[ax], g.inv_cell, g.nc[ax]);
+      fhi[ax] = axis_bin(add(cbv[ax], reach), g.glo[ax], g.inv_cell, g.nc[ax]);
     }
     const long long sx = fhi[0] - flo[0] + 1, sy = fhi[1] - flo[1] + 1, sz = fhi[2] - flo[2] + 1;
     const long long ncell = sx * sy * sz;
@@ -468,39 +546,47 @@ __global__ void __launch_bounds__(128) k_big(KtView v, const uint32_t *bigs, int
       uint32_t s0 = v.cell_start[b];
       if (s0 == 0xFFFFFFFFu) continue;
       uint32_t s1 = v.cell_end[b];
-      for (uint32_t u = s0; u < s1; ++u) {
-        uint32_t j = v.sph_sorted[u];
-        // evaluate with the lower slot as `i` (the predicate is symmetric)
-        bool hit;
-        if (j < B) {
-          const double *cj = v.centers + 3 * size_t(j);
-          double cjv[3] = {cj[0], cj[1], cj[2]};
-          long long lo[3], hi[3];
-          sphere_range(g, cjv, v.sph.offr[j].w, v.margin, lo, hi);
-          hit = ss_pair(v, g, j, B, cjv, v.sph.offr[j].w, lo, hi, v.sph.owner[j], v.sfam[j]);
-        } else {
-          hit = ss_pair(v, g, B, j, cB, rB, loB, hiB, oB, fB);
-        }
-        if (!hit) continue;
-        uint32_t a = j < B ? j : B, c = j < B ? B : j;
-        if (FILL) out[offsets[a] + atomicAdd(&cursor[a], 1u)] = make_uint2(a, c);
-        else atomicAdd(&counts[a], 1ull);
+      for (uint32_t w = s0; w < s1; ++w) {
+        const double4 c1 = sc[w];
+        const uint4 m1 = sm[w];
+        const bool lower = m1.x < B;
+        if (!(lower ? ss_pair_sorted(v, g, c1, m1, cB, mB) : ss_pair_sorted(v, g, cB, mB, c1, m1))) continue;
+        uint32_t a = lower ? m1.x : B, c = lower ? B : m1.x;
+        atomicAdd(&counts[a], 1ull);
+        unsigned long long pos = atomicAdd(tmp_n, 1ull);
+        if (pos < cap) tmp[pos] = make_uint2(a, c);
       }
     }
     for (int64_t q = threadIdx.x; q < n_big; q += blockDim.x) {
-      uint32_t j = bigs[q];
+      const uint32_t j = bigs[q];
       if (j <= B) continue;
-      if (!ss_pair(v, g, B, j, cB, rB, loB, hiB, oB, fB)) continue;
-      if (FILL) out[offsets[B] + atomicAdd(&cursor[B], 1u)] = make_uint2(B, j);
-      else atomicAdd(&counts[B], 1ull);
+      const double4 cj = make_double4(v.centers[3 * size_t(j)], v.centers[3 * size_t(j) + 1],
+                                      v.centers[3 * size_t(j) + 2], double(v.sph.offr[j].w));
+      const uint4 mj = make_uint4(j, v.sph.owner[j], v.sfam[j], 0u);
+      if (!ss_pair_sorted(v, g, cB, mB, cj, mj)) continue;
+      atomicAdd(&counts[B], 1ull);
+      unsigned long long pos = atomicAdd(tmp_n, 1ull);
+      if (pos < cap) tmp[pos] = make_uint2(B, j);
     }
   }
 }
 
-// canonical order inside every sphere-sphere segment (ascending b)
-__global__ void k_sort_ss(int64_t n, const unsigned long long *offsets, uint2 *out) {
+// scatter the scratch list into per-(kind, sphere) segments
+__global__ void k_place(const unsigned long long *m_p, int64_t n, const uint2 *tmp,
+                        const unsigned long long *offsets, unsigned *cursor, uint2 *out) {
+  const unsigned long long m = *m_p;
+  for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < m;
+       e += (unsigned long long)gridDim.x * blockDim.x) {
+    uint2 p = tmp[e];
+    int64_t seg = int64_t(p.y >> kKindShift) * n + p.x;
+    out[offsets[seg] + atomicAdd(&cursor[seg], 1u)] = p;
+  }
+}
+
+// canonical order inside every (kind, sphere) segment: ascending b
+__global__ void k_sort_seg(int64_t nseg, const unsigned long long *offsets, uint2 *out) {
   int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (i >= n) return;
+  if (i >= nseg) return;
   unsigned long long w = offsets[i], cnt = offsets[i + 1] - w;
   if (cnt > 1) sort_segment_y(out, w, cnt);
 }
@@ -547,6 +633,37 @@ __global__ void k_merge(int64_t n_new, const uint2 *new_ids, float *new_wild, in
   }
   bool hit = lo < n_old && acs_key(old_ids[lo]) == key;
   for (int q = 0; q < W; ++q) new_wild[int64_t(W) * k + q] = hit ? old_wild[int64_t(W) * lo + q] : 0.0f;
+}
+
+// history remap using the old array's per-(kind, sphere) segments: the old
+// row of a new pair can only sit in the segment of the same (kind, a)
+__global__ void k_merge_seg(int64_t n_new, const uint2 *new_ids, float *new_wild, const uint2 *old_ids,
+                            const float *old_wild, const unsigned long long *old_seg, int64_t n_sph,
+                            int W) {
+  int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (k >= n_new) return;
+  const uint2 id = new_ids[k];
+  const int64_t seg = int64_t(id.y >> kKindShift) * n_sph + id.x;
+  const unsigned long long lo = old_seg[seg], hi = old_seg[seg + 1];
+  long long hit = -1;
+  for (unsigned long long q = lo; q < hi; ++q) {
+    uint32_t y = old_ids[q].y;
+    if (y == id.y) { hit = (long long)q; break; }
+    if (y > id.y) break;
+  }
+  if (W == 4) {
+    reinterpret_cast<float4 *>(new_wild)[k] =
+        hit >= 0 ? reinterpret_cast<const float4 *>(old_wild)[hit] : make_float4(0.f, 0.f, 0.f, 0.f);
+  } else {
+    for (int q = 0; q < W; ++q) new_wild[int64_t(W) * k + q] = hit >= 0 ? old_wild[int64_t(W) * hit + q] : 0.0f;
+  }
+}
+
+__global__ void k_seg_count(int64_t n, const uint2 *ids, int64_t n_sph, unsigned long long *cnt) {
+  int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (k >= n) return;
+  uint2 id = ids[k];
+  atomicAdd(&cnt[int64_t(id.y >> kKindShift) * n_sph + id.x], 1ull);
 }
 
 __global__ void k_inc_keys(int64_t n, const uint2 *ids, const uint32_t *sph_owner,
@@ -649,7 +766,29 @@ static KtView kt_view(Ctx *c, double margin) {
   return v;
 }
 
-// grid + binning + per-sphere counts + scan; total -> status.acs_total
+static int run_pair_kernels(Ctx *c, cudaStream_t s) {
+  KtScratch &k = c->kt;
+  const int64_t n = c->n_sph;
+  KtView v = kt_view(c, c->kt_margin);
+  unsigned long long *cnt = k.counts.as<unsigned long long>();
+  unsigned long long *tn = k.tmp_n.as<unsigned long long>();
+  GF_CHECK(c, cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * (3 * n + 1), s));
+  GF_CHECK(c, cudaMemsetAsync(tn, 0, sizeof(unsigned long long), s));
+  const unsigned long long cap = (unsigned long long)k.tmp_cap;
+  uint2 *tmp = k.tmp.as<uint2>();
+  if (n) {
+    k_pairs_ss<<<grid_for(n, 128), 128, 0, s>>>(v, k.sc.as<double4>(), k.sm.as<uint4>(), cnt, tmp, tn, cap);
+    k_pairs_other<<<grid_for(n, 128), 128, 0, s>>>(v, cnt, tmp, tn, cap);
+  }
+  if (c->n_big)
+    k_big<<<unsigned(std::min<int64_t>(c->n_big, 4096)), 128, 0, s>>>(
+        v, c->big_slots.as<uint32_t>(), c->n_big, k.sc.as<double4>(), k.sm.as<uint4>(), cnt, tmp, tn, cap);
+  GF_CHECK(c, cudaGetLastError());
+  return 0;
+}
+
+// grid + binning + one pair-enumeration pass (scratch list + per-segment
+// counts) + scan; the pair total goes to status.acs_total (pinned mirror)
 int kt_detect_count(Ctx *c, double margin, cudaStream_t s) {
   KtScratch &k = c->kt;
   const int64_t n = c->n_sph, nt = c->n_tri;
@@ -659,7 +798,8 @@ int kt_detect_count(Ctx *c, double margin, cudaStream_t s) {
   if (ensure(c, k.minmax, sizeof(unsigned long long) * 8, s)) return -1;
   if (ensure(c, k.bin_key, 4 * (n + 1), s) || ensure(c, k.bin_key_alt, 4 * (n + 1), s) ||
       ensure(c, k.sph_val, 4 * (n + 1), s) || ensure(c, k.sph_val_alt, 4 * (n + 1), s) ||
-      ensure(c, k.cursor, 4 * (n + 1), s))
+      ensure(c, k.cursor, 4 * (3 * n + 1), s) || ensure(c, k.sc, 32 * (n + 1), s) ||
+      ensure(c, k.sm, 16 * (n + 1), s) || ensure(c, k.tmp_n, 16, s))
     return -1;
   if (ensure(c, k.cell_start, sizeof(uint32_t) * (kMaxCells + 1), s) ||
       ensure(c, k.cell_end, sizeof(uint32_t) * (kMaxCells + 1), s))
@@ -667,6 +807,11 @@ int kt_detect_count(Ctx *c, double margin, cudaStream_t s) {
   if (ensure(c, k.counts, sizeof(unsigned long long) * (3 * n + 1), s) ||
       ensure(c, k.offsets, sizeof(unsigned long long) * (3 * n + 1), s))
     return -1;
+  if (k.tmp_cap == 0) {
+    int64_t cap = std::max<int64_t>(16 * n, 4096);
+    if (ensure(c, k.tmp, sizeof(uint2) * cap, s)) return -1;
+    k.tmp_cap = cap;
+  }
   // min/max over centres and triangle vertices (exact), r_max
   unsigned long long *mm = k.minmax.as<unsigned long long>();
   k_minmax_init<<<1, 32, 0, s>>>(mm);
@@ -691,6 +836,9 @@ int kt_detect_count(Ctx *c, double margin, cudaStream_t s) {
     k_fill_u32<<<592, 256, 0, s>>>(gp, k.cell_start.as<uint32_t>(), 0xFFFFFFFFu, 0);
     k_cell_bounds<<<grid_for(n), kBlock, 0, s>>>(n, k.bin_key.as<uint32_t>(),
                                                 k.cell_start.as<uint32_t>(), k.cell_end.as<uint32_t>());
+    k_gather_sorted<<<grid_for(n), kBlock, 0, s>>>(n, k.sph_val.as<uint32_t>(), k.centers.as<double>(),
+                                                  c->sph_offr.as<float4>(), c->sph_owner.as<uint32_t>(),
+                                                  k.sfam.as<uint8_t>(), k.sc.as<double4>(), k.sm.as<uint4>());
   }
   if (nt) {
     if (ensure(c, k.tri_cnt, sizeof(uint32_t) * (kMaxCells + 1), s) ||
@@ -717,13 +865,8 @@ int kt_detect_count(Ctx *c, double margin, cudaStream_t s) {
                                                         nullptr, k.tri_cursor.as<uint32_t>(),
                                                         k.tri_entries.as<uint32_t>());
   }
-  KtView v = kt_view(c, margin);
+  if (run_pair_kernels(c, s)) return -1;
   unsigned long long *cnt = k.counts.as<unsigned long long>();
-  if (n) k_pairs<false><<<grid_for(n, 128), 128, 0, s>>>(v, cnt, nullptr, nullptr, nullptr);
-  if (c->n_big)
-    k_big<false><<<unsigned(std::min<int64_t>(c->n_big, 4096)), 128, 0, s>>>(
-        v, c->big_slots.as<uint32_t>(), c->n_big, cnt, nullptr, nullptr, nullptr);
-  GF_CHECK(c, cudaMemsetAsync(cnt + 3 * n, 0, sizeof(unsigned long long), s));
   size_t tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, k.offsets.as<unsigned long long>(), int(3 * n + 1), s);
   if (ensure(c, k.cub_tmp, tmp + 16, s, false)) return -1;
@@ -739,10 +882,18 @@ int kt_detect_count(Ctx *c, double margin, cudaStream_t s) {
   return 0;
 }
 
+// canonical (kind, a, b) array from the scratch list; keeps the segment
+// offsets with the array for the next history remap
 int kt_detect_fill(Ctx *c, Acs &out, cudaStream_t s) {
   KtScratch &k = c->kt;
   const int64_t n = c->n_sph;
   const int64_t total = out.n;
+  if (total > k.tmp_cap) {  // scratch overflowed: grow and enumerate again
+    int64_t cap = total + total / 4 + 4096;
+    if (ensure(c, k.tmp, sizeof(uint2) * cap, s)) return -1;
+    k.tmp_cap = cap;
+    if (run_pair_kernels(c, s)) return -1;
+  }
   if (total > out.cap) {
     int64_t cap = total + total / 2 + 1024;
     if (ensure(c, out.ids, sizeof(uint2) * cap, s) ||
@@ -750,18 +901,16 @@ int kt_detect_fill(Ctx *c, Acs &out, cudaStream_t s) {
       return -1;
     out.cap = cap;
   }
+  if (ensure(c, out.seg, sizeof(unsigned long long) * (3 * n + 1), s)) return -1;
+  GF_CHECK(c, cudaMemcpyAsync(out.seg.p, k.offsets.p, sizeof(unsigned long long) * (3 * n + 1),
+                              cudaMemcpyDeviceToDevice, s));
   if (n && total) {
-    KtView v = kt_view(c, c->kt_margin);
-    const unsigned long long *off = k.offsets.as<unsigned long long>();
-    unsigned *cur = k.cursor.as<unsigned>();
-    k_pairs<true><<<grid_for(n, 128), 128, 0, s>>>(v, nullptr, off, out.ids.as<uint2>(), cur);
-    if (c->n_big) {
-      k_big<true><<<unsigned(std::min<int64_t>(c->n_big, 4096)), 128, 0, s>>>(
-          v, c->big_slots.as<uint32_t>(), c->n_big, nullptr, off, out.ids.as<uint2>(), cur);
-      k_sort_ss<<<grid_for(n), kBlock, 0, s>>>(n, off, out.ids.as<uint2>());
-    } else {
-      k_sort_ss<<<grid_for(n), kBlock, 0, s>>>(n, off, out.ids.as<uint2>());
-    }
+    GF_CHECK(c, cudaMemsetAsync(k.cursor.p, 0, sizeof(unsigned) * 3 * n, s));
+    k_place<<<1184, 256, 0, s>>>(k.tmp_n.as<unsigned long long>(), n, k.tmp.as<uint2>(),
+                                 k.offsets.as<unsigned long long>(), k.cursor.as<unsigned>(),
+                                 out.ids.as<uint2>());
+    k_sort_seg<<<grid_for(3 * n), kBlock, 0, s>>>(3 * n, k.offsets.as<unsigned long long>(),
+                                                  out.ids.as<uint2>());
   }
   GF_CHECK(c, cudaGetLastError());
   return 0;
@@ -784,9 +933,12 @@ int kt_bin_ranges(Ctx *c, double margin, int64_t *h_out) {
 int adopt_acs(Ctx *c, cudaStream_t s) {
   Acs &nw = c->acs_next;
   Acs &old = c->acs;
-  if (nw.n)
-    k_merge<<<grid_for(nw.n), kBlock, 0, s>>>(nw.n, nw.ids.as<uint2>(), nw.wild.as<float>(), old.n,
-                                             old.ids.as<uint2>(), old.wild.as<float>(), c->wild_w);
+  if (nw.n && old.n && old.seg.p)
+    k_merge_seg<<<grid_for(nw.n), kBlock, 0, s>>>(nw.n, nw.ids.as<uint2>(), nw.wild.as<float>(),
+                                                 old.ids.as<uint2>(), old.wild.as<float>(),
+                                                 old.seg.as<unsigned long long>(), c->n_sph, c->wild_w);
+  else if (nw.n)
+    GF_CHECK(c, cudaMemsetAsync(nw.wild.p, 0, sizeof(float) * c->wild_w * nw.n, s));
   std::swap(c->acs, c->acs_next);
   c->ca_updates++;
   GF_CHECK(c, cudaGetLastError());
@@ -815,6 +967,25 @@ int merge_host(Ctx *c, int64_t n_old, const uint32_t *old_ids, const float *old_
     GF_CHECK(c, cudaStreamSynchronize(s));
   }
   cudaFree(a.p); cudaFree(b.p); cudaFree(wa.p); cudaFree(wb.p);
+  return 0;
+}
+
+// per-(kind, sphere) segment offsets of an array installed from the host
+int build_segments(Ctx *c, Acs &a, cudaStream_t s) {
+  const int64_t n = c->n_sph;
+  KtScratch &k = c->kt;
+  if (ensure(c, a.seg, sizeof(unsigned long long) * (3 * n + 1), s) ||
+      ensure(c, k.counts, sizeof(unsigned long long) * (3 * n + 1), s))
+    return -1;
+  unsigned long long *cnt = k.counts.as<unsigned long long>();
+  GF_CHECK(c, cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * (3 * n + 1), s));
+  if (a.n) k_seg_count<<<grid_for(a.n), kBlock, 0, s>>>(a.n, a.ids.as<uint2>(), n, cnt);
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, a.seg.as<unsigned long long>(), int(3 * n + 1), s);
+  if (ensure(c, k.cub_tmp, tmp + 16, s, false)) return -1;
+  GF_CHECK(c, cub::DeviceScan::ExclusiveSum(k.cub_tmp.p, tmp, cnt, a.seg.as<unsigned long long>(),
+                                            int(3 * n + 1), s));
+  GF_CHECK(c, cudaGetLastError());
   return 0;
 }
 
