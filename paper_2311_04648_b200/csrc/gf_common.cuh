@@ -54,6 +54,8 @@ struct Spheres {
   uint32_t *owner;
   float4 *offr;        // local offset xyz + radius (float32 geom params)
   uint8_t *mat;
+  double4 *center;     // world centre + radius, refreshed by the integrator
+  uint32_t *first;     // [n_owner + 1] CSR: spheres of owner o are [first[o], first[o+1])
 };
 
 struct Tris {

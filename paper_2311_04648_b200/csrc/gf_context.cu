@@ -67,7 +67,8 @@ Owners owners_view(Ctx *c) {
   return o;
 }
 Spheres spheres_view(Ctx *c) {
-  return Spheres{c->n_sph, c->sph_owner.as<uint32_t>(), c->sph_offr.as<float4>(), c->sph_mat.as<uint8_t>()};
+  return Spheres{c->n_sph, c->sph_owner.as<uint32_t>(), c->sph_offr.as<float4>(), c->sph_mat.as<uint8_t>(),
+                 c->sph_center.as<double4>(), c->sph_first.as<uint32_t>()};
 }
 Tris tris_view(Ctx *c) {
   return Tris{c->n_tri, c->tri_owner.as<uint32_t>(), c->tri_local.as<float>(), c->tri_mat.as<uint8_t>(),
@@ -233,7 +234,7 @@ void gf_destroy(gf_ctx *ctx) {
   Ctx *c = &ctx->c;
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
-  DBuf *bufs[] = {&c->voxel, &c->sub, &c->quat, &c->lin_vel, &c->ang_vel, &c->meta, &c->tpl, &c->acc,
+  DBuf *bufs[] = {&c->sph_center, &c->sph_first, &c->voxel, &c->sub, &c->quat, &c->lin_vel, &c->ang_vel, &c->meta, &c->tpl, &c->acc,
                   &c->ext, &c->sph_owner, &c->sph_offr, &c->sph_mat, &c->tri_owner, &c->tri_local,
                   &c->tri_mat, &c->tri_world, &c->ana_owner, &c->ana_kind, &c->ana_local, &c->ana_mat,
                   &c->ana_world, &c->pair, &c->beta, &c->fam_mask, &c->fam_flags, &c->lv_mask,
@@ -246,7 +247,7 @@ void gf_destroy(gf_ctx *ctx) {
                   &c->kt.cell_start, &c->kt.cell_end, &c->kt.tri_ranges, &c->kt.tri_cnt,
                   &c->kt.tri_start, &c->kt.tri_entries, &c->kt.counts, &c->kt.offsets, &c->kt.cub_tmp,
                   &c->kt.total, &c->kt.cursor, &c->kt.tri_cursor, &c->big_slots, &c->kt.sc,
-                  &c->kt.sm, &c->kt.tmp, &c->kt.tmp_n, &c->acs.seg, &c->acs_next.seg};
+                  &c->kt.sm, &c->kt.sf, &c->kt.tmp, &c->kt.tmp_n, &c->acs.seg, &c->acs_next.seg};
   for (DBuf *b : bufs) release(*b);
   if (c->h_status) cudaFreeHost(c->h_status);
   cudaEvent_t evs[] = {c->ev_snap, c->ev_ca, c->ev_adopted, c->ev_count, c->t0, c->t1};
@@ -324,6 +325,10 @@ int gf_upload_owners(gf_ctx *ctx, int64_t n, const uint64_t *voxel, const uint16
   if (n_tpl) GF_CHECK(c, cudaMemcpy(c->tpl.p, tp.data(), 32 * n_tpl, cudaMemcpyHostToDevice));
   GF_CHECK(c, cudaMemset(c->acc.p, 0, 48 * n));
   if (c->has_ext) GF_CHECK(c, cudaMemset(c->ext.p, 0, 48 * n));
+  if (c->n_sph && c->sph_first.p && c->sph_center.bytes >= size_t(32 * c->n_sph)) {
+    if (refresh_centers(c, c->s_dt) || refresh_world(c, c->s_dt)) return -1;
+    GF_CHECK(c, cudaStreamSynchronize(c->s_dt));
+  }
   world_moving_update(c);
   return 0;
 }
@@ -441,6 +446,23 @@ int gf_upload_geometry(gf_ctx *ctx, int64_t n_s, const int64_t *sph_owner, const
       ensure(c, c->tri_world, 72 * (n_t + 1), c->s_dt) || ensure(c, c->ana_world, 64 * (n_a + 1), c->s_dt))
     return -1;
   if (set_split(c, sph_params + 3, 4, n_s)) return -1;
+  // spheres grouped by owner (ascending): CSR of each owner's sphere slots
+  {
+    std::vector<uint32_t> first(c->n_owner + 2, 0);
+    for (int64_t k = 0; k < n_s; ++k) {
+      if (k && sph_owner[k] < sph_owner[k - 1]) {
+        c->err = "sphere slots must be grouped by ascending owner";
+        return -1;
+      }
+      if (sph_owner[k] < 0 || sph_owner[k] >= c->n_owner) { c->err = "sphere owner out of range"; return -1; }
+      first[sph_owner[k] + 1]++;
+    }
+    for (int64_t o = 0; o < c->n_owner; ++o) first[o + 1] += first[o];
+    if (upload_raw(c, c->sph_first, first.data(), 4 * (c->n_owner + 1)) ||
+        ensure(c, c->sph_center, 32 * (n_s + 1), c->s_dt))
+      return -1;
+  }
+  if (refresh_centers(c, c->s_dt)) return -1;
   world_moving_update(c);
   // world transforms of meshes / analytics for the current pose
   if (refresh_world(c, c->s_dt)) return -1;

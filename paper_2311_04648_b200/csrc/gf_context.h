@@ -44,7 +44,8 @@ struct KtScratch {
   DBuf tri_ranges;                                   // int32[n_t*6]
   DBuf tri_cnt, tri_start, tri_entries;              // tri CSR over bins
   DBuf cursor;       // uint32[3 n_s] fill cursor of each (kind, sphere) segment
-  DBuf sc, sm;       // cell-sorted copies: double4 (centre, radius), uint4 (slot, owner, family)
+  DBuf sc, sm, sf;   // cell-sorted copies: double4 (centre, radius), uint4 (slot, owner, family),
+                     // float4 (centre - grid origin, radius) for the conservative fp32 prefilter
   DBuf tmp, tmp_n;   // scratch pair list (uint2) and its append counter
   int64_t tmp_cap = 0;
   DBuf tri_cursor;   // uint32 per cell
@@ -71,7 +72,7 @@ struct Ctx {
   bool has_ext = false;
   // geometry
   int64_t n_sph = 0, n_tri = 0, n_ana = 0;
-  DBuf sph_owner, sph_offr, sph_mat;
+  DBuf sph_owner, sph_offr, sph_mat, sph_center, sph_first;
   DBuf tri_owner, tri_local, tri_mat, tri_world;
   DBuf ana_owner, ana_kind, ana_local, ana_mat, ana_world;
   bool world_moving = true;  // any tri/ana owner not fixed
@@ -140,7 +141,7 @@ struct Status {
 };
 
 constexpr uint32_t kHeavyThreshold = 192;
-constexpr int64_t kMaxCells = int64_t(1) << 25;  // enumeration-grid cell cap  // incidences above which an owner is block-reduced
+constexpr int64_t kMaxCells = (int64_t(1) << 24) - 1;  // enumeration-grid cell cap; key 2^24-1 = unregistered  // incidences above which an owner is block-reduced
 
 // helpers implemented in gf_context.cu
 int ensure(Ctx *c, DBuf &b, size_t bytes, cudaStream_t s, bool keep = false);
@@ -173,6 +174,7 @@ int build_segments(Ctx *c, Acs &a, cudaStream_t s);
 int merge_host(Ctx *c, int64_t n_old, const uint32_t *old_ids, const float *old_wild, int64_t n_new,
                const uint32_t *new_ids, int W, float *out_wild);
 int refresh_world(Ctx *c, cudaStream_t s);               // tri/ana world from owner pose
+int refresh_centers(Ctx *c, cudaStream_t s);             // sphere world centres from owner pose
 
 // dT (gf_dt_f64.cu / gf_dt_f32.cu)
 struct StepArgs {

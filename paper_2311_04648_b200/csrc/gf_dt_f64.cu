@@ -6,6 +6,13 @@ int dt_step_f64(Ctx *c, const StepArgs &a, cudaStream_t s) { return dt_step_impl
 }  // namespace gf
 
 namespace gf {
+int refresh_centers(Ctx *c, cudaStream_t s) {
+  if (!c->n_sph) return 0;
+  k_centers<<<unsigned((c->n_sph + 127) / 128), 128, 0, s>>>(c->dom, owners_view(c), spheres_view(c));
+  GF_CHECK(c, cudaGetLastError());
+  return 0;
+}
+
 int refresh_world(Ctx *c, cudaStream_t s) {
   int64_t n = c->n_tri + c->n_ana;
   if (!n) return 0;

@@ -173,22 +173,19 @@ __global__ void __launch_bounds__(128) k_contacts(DtView v, double ts) {
   if (k < v.n_acs && !v.st->err) {
     uint2 id = v.ids[k];
     const uint32_t kind = id.y >> kKindShift, sb = id.y & kSlotMask;
-    double ca[3];
-    float ra_f;
-    uint32_t oa;
-    sphere_center(v.dom, v.own, v.sph, id.x, ca, ra_f, oa);
-    const double ra = double(ra_f);
+    const double4 cA = v.sph.center[id.x];
+    const double ca[3] = {cA.x, cA.y, cA.z};
+    const double ra = cA.w;
     double depth, bx, by, bz, rb;
     uint32_t ob;
     int mb;
     if (kind == 0) {
-      double cb[3];
-      float rb_f;
-      sphere_center(v.dom, v.own, v.sph, sb, cb, rb_f, ob);
-      mb = v.sph.mat[sb];
-      double dx = ca[0] - cb[0], dy = ca[1] - cb[1], dz = ca[2] - cb[2];
+      const double4 cB = v.sph.center[sb];
+      ob = sb;  // resolved to the owner below, only for touching pairs
+      mb = -1;
+      double dx = ca[0] - cB.x, dy = ca[1] - cB.y, dz = ca[2] - cB.z;
       double d = sqrt(dx * dx + dy * dy + dz * dz);
-      rb = double(rb_f);
+      rb = cB.w;
       if (d < 1e-300) {
         depth = ra + rb; bx = 0.0; by = 0.0; bz = 1.0;
       } else {
@@ -225,6 +222,11 @@ __global__ void __launch_bounds__(128) k_contacts(DtView v, double ts) {
     }
     uint8_t t = 0;
     if (depth > 0.0) {
+      const uint32_t oa = v.sph.owner[id.x];
+      if (kind == 0) {
+        ob = v.sph.owner[sb];
+        mb = v.sph.mat[sb];
+      }
       double half = ra - 0.5 * depth;
       double px = ca[0] - bx * half, py = ca[1] - by * half, pz = ca[2] - bz * half;
       double pa[3], va[3], wa[3], ma, pb[3], vb[3], wb[3], mbass;
@@ -425,6 +427,19 @@ __global__ void __launch_bounds__(128) k_integrate(DtView v, double h, double gx
   }
   v.own.voxel[o] = vox;
   v.own.sub[o] = s;
+  // refreshed sphere centres from the decoded position (_kernels.py:657-669)
+  const uint32_t s0 = v.sph.first[o], s1 = v.sph.first[o + 1];
+  if (s1 > s0) {
+    double pd[3];
+    decode_pos(v.dom, vox, s, pd[0], pd[1], pd[2]);
+    for (uint32_t k = s0; k < s1; ++k) {
+      const float4 orr = v.sph.offr[k];
+      double r[3];
+      qrot(double(q.x), double(q.y), double(q.z), double(q.w), double(orr.x), double(orr.y), double(orr.z),
+           r[0], r[1], r[2]);
+      v.sph.center[k] = make_double4(add(pd[0], r[0]), add(pd[1], r[1]), add(pd[2], r[2]), double(orr.w));
+    }
+  }
 }
 
 namespace {
@@ -434,6 +449,17 @@ __global__ void k_apply_dyn(int n_dyn, const int *spec, const double *vals, doub
   if (t >= n_dyn) return;
   int fam = spec[3 * t], table = spec[3 * t + 1], ax = spec[3 * t + 2];
   (table == 0 ? lv_val : av_val)[3 * fam + ax] = vals[t];
+}
+
+// sphere world centres from the owner pose (_kernels.py:91-106)
+__global__ void k_centers(Domain dom, Owners own, Spheres sph) {
+  int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (k >= sph.n) return;
+  double c[3];
+  float r;
+  uint32_t o;
+  sphere_center(dom, own, sph, uint32_t(k), c, r, o);
+  sph.center[k] = make_double4(c[0], c[1], c[2], double(r));
 }
 
 // triangle / analytic world transforms (_kernels.py:109-152)

@@ -25,6 +25,8 @@ namespace gf {
 namespace {
 
 constexpr int kBlock = 256;
+constexpr uint32_t kNoCell = uint32_t(kMaxCells);  // key of spheres kept out of the grid (24 bits)
+constexpr int kKeyBits = 24;
 
 inline unsigned grid_for(int64_t n, int block = kBlock) {
   int64_t g = (n + block - 1) / block;
@@ -68,17 +70,15 @@ struct KtView {
 // ---------------------------------------------------------------------------
 // snapshot
 // ---------------------------------------------------------------------------
+// frozen copy of the refreshed sphere centres and families (engine.py:577-596)
 __global__ void k_snapshot(Domain dom, Owners own, Spheres sph, double *centers, uint8_t *sfam) {
   int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (k >= sph.n) return;
-  double c[3];
-  float r;
-  uint32_t o;
-  sphere_center(dom, own, sph, uint32_t(k), c, r, o);
-  centers[3 * k] = c[0];
-  centers[3 * k + 1] = c[1];
-  centers[3 * k + 2] = c[2];
-  sfam[k] = uint8_t(meta_family(own.meta[o]));
+  const double4 c = sph.center[k];
+  centers[3 * k] = c.x;
+  centers[3 * k + 1] = c.y;
+  centers[3 * k + 2] = c.z;
+  sfam[k] = uint8_t(meta_family(own.meta[sph.owner[k]]));
 }
 
 __global__ void k_geom_family(int64_t n, const uint32_t *owner, const uint32_t *meta, uint8_t *fam) {
@@ -125,13 +125,19 @@ __global__ void k_minmax(int64_t n_pts, const double *pts, int64_t n_s, const fl
     }
     rmax = fmax(rmax, __shfl_down_sync(0xffffffff, rmax, off));
   }
+  __shared__ double sh[7][32];
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if ((threadIdx.x & 31) == 0) {
-#pragma unroll
-    for (int ax = 0; ax < 3; ++ax) {
-      atomicMin(&mm[ax], ord_key(lo[ax]));
-      atomicMax(&mm[3 + ax], ord_key(hi[ax]));
-    }
-    atomicMax(&mm[6], ord_key(rmax));
+    for (int ax = 0; ax < 3; ++ax) { sh[ax][warp] = lo[ax]; sh[3 + ax][warp] = hi[ax]; }
+    sh[6][warp] = rmax;
+  }
+  __syncthreads();
+  if (threadIdx.x < 7) {
+    const int q = threadIdx.x;
+    double acc = sh[q][0];
+    for (int w = 1; w < nw; ++w) acc = q < 3 ? fmin(acc, sh[q][w]) : fmax(acc, sh[q][w]);
+    if (q < 3) atomicMin(&mm[q], ord_key(acc));
+    else atomicMax(&mm[q], ord_key(acc));
   }
 }
 
@@ -192,7 +198,7 @@ __global__ void k_bin_keys(int64_t n, const double *centers, const float4 *offr,
   if (i >= n) return;
   Grid g = *gp;
   val[i] = uint32_t(i);
-  if (double(offr[i].w) > g.r_cut) { key[i] = 0xFFFFFFFFu; return; }
+  if (double(offr[i].w) > g.r_cut) { key[i] = kNoCell; return; }
   long long ix = axis_bin(centers[3 * i], g.glo[0], g.inv_cell, g.nc[0]);
   long long iy = axis_bin(centers[3 * i + 1], g.glo[1], g.inv_cell, g.nc[1]);
   long long iz = axis_bin(centers[3 * i + 2], g.glo[2], g.inv_cell, g.nc[2]);
@@ -203,7 +209,7 @@ __global__ void k_cell_bounds(int64_t n, const uint32_t *key, uint32_t *start, u
   int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (i >= n) return;
   uint32_t k = key[i];
-  if (k == 0xFFFFFFFFu) return;
+  if (k == kNoCell) return;
   if (i == 0 || key[i - 1] != k) start[k] = uint32_t(i);
   if (i == n - 1 || key[i + 1] != k) end[k] = uint32_t(i + 1);
 }
@@ -354,13 +360,15 @@ __device__ __forceinline__ void append_pair(bool hit, uint2 e, uint2 *tmp, unsig
 // cell-sorted copies of the snapshot spheres: (centre, radius), (slot, owner, family)
 __global__ void k_gather_sorted(int64_t n, const uint32_t *sorted, const double *centers,
                                 const float4 *offr, const uint32_t *owner, const uint8_t *sfam,
-                                double4 *sc, uint4 *sm) {
+                                const Grid *gp, double4 *sc, uint4 *sm, float4 *sf) {
   int64_t u = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (u >= n) return;
   uint32_t i = sorted[u];
-  sc[u] = make_double4(centers[3 * size_t(i)], centers[3 * size_t(i) + 1], centers[3 * size_t(i) + 2],
-                       double(offr[i].w));
+  const double x = centers[3 * size_t(i)], y = centers[3 * size_t(i) + 1], z = centers[3 * size_t(i) + 2];
+  sc[u] = make_double4(x, y, z, double(offr[i].w));
   sm[u] = make_uint4(i, owner[i], sfam[i], 0u);
+  const Grid g = *gp;
+  sf[u] = make_float4(float(x - g.glo[0]), float(y - g.glo[1]), float(z - g.glo[2]), offr[i].w);
 }
 
 // exact sphere-sphere predicate (_kernels.py:305-321) on cell-sorted copies;
@@ -393,7 +401,7 @@ __device__ __forceinline__ bool ss_pair_sorted(const KtView &v, const Grid &g, c
 // are counted into the segment of the lower slot and appended to a scratch
 // list (placed into canonical segments by k_place / k_sort_seg).
 __global__ void __launch_bounds__(128) k_pairs_ss(KtView v, const double4 *sc, const uint4 *sm,
-                                                  unsigned long long *counts, uint2 *tmp,
+                                                  const float4 *sf, unsigned long long *counts, uint2 *tmp,
                                                   unsigned long long *tmp_n, unsigned long long cap) {
   int64_t u64 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   const Grid g = *v.grid;
@@ -402,10 +410,17 @@ __global__ void __launch_bounds__(128) k_pairs_ss(KtView v, const double4 *sc, c
   active = active && key != 0xFFFFFFFFu;
   double4 c0 = make_double4(0, 0, 0, 0);
   uint4 m0 = make_uint4(0, 0, 0, 0);
+  float4 f0 = make_float4(0.f, 0.f, 0.f, 0.f);
   long long cx = 0, cy = 0, cz = 0;
+  // conservative fp32 prefilter: coordinates are rounded relative to the grid
+  // origin, so |d_f32 - d| <= ~4 * 2^-24 * extent; the slack below is > 10x that
+  const float ext = float(double(max(g.nc[0], max(g.nc[1], g.nc[2]))) / g.inv_cell);
+  const float slack = 1e-6f * ext + 1e-30f;
+  const float marg = float(v.margin);
   if (active) {
     c0 = sc[u64];
     m0 = sm[u64];
+    f0 = sf[u64];
     cx = key % g.nc[0];
     cy = (key / g.nc[0]) % g.nc[1];
     cz = key / (g.nc[0] * g.nc[1]);
@@ -447,14 +462,19 @@ __global__ void __launch_bounds__(128) k_pairs_ss(KtView v, const double4 *sc, c
       uint2 e = make_uint2(0, 0);
       if (t < len) {
         uint32_t w = s0 + t;
-        double4 c1 = sc[w];
-        uint4 m1 = sm[w];
-        bool lower = m0.x < m1.x;
-        hit = lower ? ss_pair_sorted(v, g, c0, m0, c1, m1) : ss_pair_sorted(v, g, c1, m1, c0, m0);
-        if (hit) {
-          uint32_t a = lower ? m0.x : m1.x, b = lower ? m1.x : m0.x;
-          e = make_uint2(a, b);
-          atomicAdd(&counts[a], 1ull);
+        const float4 f1 = sf[w];
+        const float dx = f0.x - f1.x, dy = f0.y - f1.y, dz = f0.z - f1.z;
+        const float rr = f0.w + f1.w + marg + slack;
+        if (dx * dx + dy * dy + dz * dz < rr * rr * 1.0001f) {
+          double4 c1 = sc[w];
+          uint4 m1 = sm[w];
+          bool lower = m0.x < m1.x;
+          hit = lower ? ss_pair_sorted(v, g, c0, m0, c1, m1) : ss_pair_sorted(v, g, c1, m1, c0, m0);
+          if (hit) {
+            uint32_t a = lower ? m0.x : m1.x, b = lower ? m1.x : m0.x;
+            e = make_uint2(a, b);
+            atomicAdd(&counts[a], 1ull);
+          }
         }
       }
       append_pair(hit, e, tmp, tmp_n, cap);
@@ -777,7 +797,7 @@ static int run_pair_kernels(Ctx *c, cudaStream_t s) {
   const unsigned long long cap = (unsigned long long)k.tmp_cap;
   uint2 *tmp = k.tmp.as<uint2>();
   if (n) {
-    k_pairs_ss<<<grid_for(n, 128), 128, 0, s>>>(v, k.sc.as<double4>(), k.sm.as<uint4>(), cnt, tmp, tn, cap);
+    k_pairs_ss<<<grid_for(n, 128), 128, 0, s>>>(v, k.sc.as<double4>(), k.sm.as<uint4>(), k.sf.as<float4>(), cnt, tmp, tn, cap);
     k_pairs_other<<<grid_for(n, 128), 128, 0, s>>>(v, cnt, tmp, tn, cap);
   }
   if (c->n_big)
@@ -799,7 +819,7 @@ int kt_detect_count(Ctx *c, double margin, cudaStream_t s) {
   if (ensure(c, k.bin_key, 4 * (n + 1), s) || ensure(c, k.bin_key_alt, 4 * (n + 1), s) ||
       ensure(c, k.sph_val, 4 * (n + 1), s) || ensure(c, k.sph_val_alt, 4 * (n + 1), s) ||
       ensure(c, k.cursor, 4 * (3 * n + 1), s) || ensure(c, k.sc, 32 * (n + 1), s) ||
-      ensure(c, k.sm, 16 * (n + 1), s) || ensure(c, k.tmp_n, 16, s))
+      ensure(c, k.sm, 16 * (n + 1), s) || ensure(c, k.sf, 16 * (n + 1), s) || ensure(c, k.tmp_n, 16, s))
     return -1;
   if (ensure(c, k.cell_start, sizeof(uint32_t) * (kMaxCells + 1), s) ||
       ensure(c, k.cell_end, sizeof(uint32_t) * (kMaxCells + 1), s))
@@ -826,9 +846,9 @@ int kt_detect_count(Ctx *c, double margin, cudaStream_t s) {
     size_t tmp = 0;
     cub::DoubleBuffer<uint32_t> dk(k.bin_key.as<uint32_t>(), k.bin_key_alt.as<uint32_t>());
     cub::DoubleBuffer<uint32_t> dv(k.sph_val.as<uint32_t>(), k.sph_val_alt.as<uint32_t>());
-    cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, int(n), 0, 32, s);
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, int(n), 0, kKeyBits, s);
     if (ensure(c, k.cub_tmp, tmp + 16, s)) return -1;
-    GF_CHECK(c, cub::DeviceRadixSort::SortPairs(k.cub_tmp.p, tmp, dk, dv, int(n), 0, 32, s));
+    GF_CHECK(c, cub::DeviceRadixSort::SortPairs(k.cub_tmp.p, tmp, dk, dv, int(n), 0, kKeyBits, s));
     if (dk.Current() != k.bin_key.as<uint32_t>()) {
       std::swap(k.bin_key, k.bin_key_alt);
       std::swap(k.sph_val, k.sph_val_alt);
@@ -838,7 +858,8 @@ int kt_detect_count(Ctx *c, double margin, cudaStream_t s) {
                                                 k.cell_start.as<uint32_t>(), k.cell_end.as<uint32_t>());
     k_gather_sorted<<<grid_for(n), kBlock, 0, s>>>(n, k.sph_val.as<uint32_t>(), k.centers.as<double>(),
                                                   c->sph_offr.as<float4>(), c->sph_owner.as<uint32_t>(),
-                                                  k.sfam.as<uint8_t>(), k.sc.as<double4>(), k.sm.as<uint4>());
+                                                  k.sfam.as<uint8_t>(), gp, k.sc.as<double4>(), k.sm.as<uint4>(),
+                                                  k.sf.as<float4>());
   }
   if (nt) {
     if (ensure(c, k.tri_cnt, sizeof(uint32_t) * (kMaxCells + 1), s) ||
