@@ -62,8 +62,10 @@ struct DtView {
   int W;
   double *out_c;        // [n_acs*9]
   uint8_t *touch;       // [n_acs]
-  const uint32_t *inc;  // sorted incidences (k << 1 | side)
-  const uint32_t *inc_start;
+  const uint32_t *inc;  // B-side incidences: contact indices sorted by (B owner, k)
+  const uint32_t *inc_start;  // per owner start in inc
+  const unsigned long long *seg;  // (kind, sphere A) segment starts of the active array
+  int64_t n_sph;
   const uint32_t *heavy;
   const unsigned long long *n_heavy;
   double *heavy_acc;    // [n_owner*6] (only heavy owners written)
@@ -268,27 +270,64 @@ __global__ void __launch_bounds__(128) k_contacts(DtView v, double ts) {
   }
 }
 
-// one owner's incidence contributions, in canonical order (_kernels.py:522-545)
-__device__ __forceinline__ void accumulate(const DtView &v, uint32_t lo, uint32_t hi, const double p[3],
+// one contact's contribution to owner position p (A side +, B side -)
+__device__ __forceinline__ void contribute(const DtView &v, uint32_t k, bool side_b, const double p[3],
                                            double af[3], double at[3]) {
-  for (uint32_t e = lo; e < hi; ++e) {
-    uint32_t w = v.inc[e];
-    uint32_t k = w >> 1;
-    if (!v.touch[k]) continue;  // exact: a false positive contributes +-0.0
-    const double *oc = v.out_c + 9 * size_t(k);
-    double fx = oc[0], fy = oc[1], fz = oc[2];
-    double tx = oc[3], ty = oc[4], tz = oc[5];
-    double rx = oc[6] - p[0], ry = oc[7] - p[1], rz = oc[8] - p[2];
-    if ((w & 1u) == 0) {
-      af[0] += fx; af[1] += fy; af[2] += fz;
-      at[0] += ry * tz - rz * ty;
-      at[1] += rz * tx - rx * tz;
-      at[2] += rx * ty - ry * tx;
+  if (!v.touch[k]) return;  // exact: a false positive contributes +-0.0
+  const double *oc = v.out_c + 9 * size_t(k);
+  double fx = oc[0], fy = oc[1], fz = oc[2];
+  double tx = oc[3], ty = oc[4], tz = oc[5];
+  double rx = oc[6] - p[0], ry = oc[7] - p[1], rz = oc[8] - p[2];
+  if (!side_b) {
+    af[0] += fx; af[1] += fy; af[2] += fz;
+    at[0] += ry * tz - rz * ty;
+    at[1] += rz * tx - rx * tz;
+    at[2] += rx * ty - ry * tx;
+  } else {
+    af[0] -= fx; af[1] -= fy; af[2] -= fz;
+    at[0] -= ry * tz - rz * ty;
+    at[1] -= rz * tx - rx * tz;
+    at[2] -= rx * ty - ry * tx;
+  }
+}
+
+// A-side contact ranges of owner o: its spheres' segments for kinds 0..2
+// (increasing contact index across kinds)
+__device__ __forceinline__ void a_ranges(const DtView &v, uint32_t o, unsigned long long lo[3],
+                                         unsigned long long hi[3]) {
+  const uint32_t f0 = v.sph.first[o], f1 = v.sph.first[o + 1];
+  for (int kind = 0; kind < 3; ++kind) {
+    lo[kind] = f1 > f0 ? v.seg[kind * v.n_sph + f0] : 0;
+    hi[kind] = f1 > f0 ? v.seg[kind * v.n_sph + f1] : 0;
+  }
+}
+
+// all contributions of owner o in canonical ACS order (the reference's
+// reduce_to_owners order, _kernels.py:522-545): merge of the A ranges and the
+// sorted B list by contact index
+__device__ __forceinline__ void accumulate(const DtView &v, uint32_t o, const double p[3], double af[3],
+                                           double at[3]) {
+  unsigned long long alo[3], ahi[3];
+  a_ranges(v, o, alo, ahi);
+  uint32_t b = v.inc_start[o];
+  const uint32_t be = v.inc_start[o + 1];
+  int kind = 0;
+  unsigned long long a = alo[0];
+  for (;;) {
+    while (kind < 3 && a >= ahi[kind]) {
+      ++kind;
+      if (kind < 3) a = alo[kind];
+    }
+    const bool have_a = kind < 3;
+    const bool have_b = b < be;
+    if (!have_a && !have_b) break;
+    uint32_t kb = have_b ? v.inc[b] : 0xFFFFFFFFu;
+    if (have_a && (!have_b || a < kb)) {
+      contribute(v, uint32_t(a), false, p, af, at);
+      ++a;
     } else {
-      af[0] -= fx; af[1] -= fy; af[2] -= fz;
-      at[0] -= ry * tz - rz * ty;
-      at[1] -= rz * tx - rx * tz;
-      at[2] -= rx * ty - ry * tx;
+      contribute(v, kb, true, p, af, at);
+      ++b;
     }
   }
 }
@@ -301,26 +340,33 @@ __global__ void __launch_bounds__(256) k_heavy(DtView v) {
   const unsigned long long nh = *v.n_heavy;
   for (unsigned long long hidx = blockIdx.x; hidx < nh; hidx += gridDim.x) {
     uint32_t o = v.heavy[hidx];
-    uint32_t lo = v.inc_start[o], hi = v.inc_start[o + 1];
     double p[3];
     decode_pos(v.dom, v.own.voxel[o], v.own.sub[o], p[0], p[1], p[2]);
+    unsigned long long alo[3], ahi[3];
+    a_ranges(v, o, alo, ahi);
+    const unsigned long long na0 = ahi[0] - alo[0], na1 = ahi[1] - alo[1], na2 = ahi[2] - alo[2];
+    const uint32_t b0 = v.inc_start[o], b1 = v.inc_start[o + 1];
+    const unsigned long long ntot = na0 + na1 + na2 + (b1 - b0);
     double af[3] = {0, 0, 0}, at[3] = {0, 0, 0};
-    uint32_t n = hi - lo;
-    uint32_t chunk = (n + blockDim.x - 1) / blockDim.x;
-    uint32_t b0 = lo + min(n, chunk * threadIdx.x), b1 = lo + min(n, chunk * (threadIdx.x + 1));
-    accumulate(v, b0, b1, p, af, at);
+    const unsigned long long chunk = (ntot + blockDim.x - 1) / blockDim.x;
+    const unsigned long long e0 = min(ntot, chunk * threadIdx.x), e1 = min(ntot, chunk * (threadIdx.x + 1));
+    for (unsigned long long e = e0; e < e1; ++e) {
+      if (e < na0) contribute(v, uint32_t(alo[0] + e), false, p, af, at);
+      else if (e < na0 + na1) contribute(v, uint32_t(alo[1] + e - na0), false, p, af, at);
+      else if (e < na0 + na1 + na2) contribute(v, uint32_t(alo[2] + e - na0 - na1), false, p, af, at);
+      else contribute(v, v.inc[b0 + (e - na0 - na1 - na2)], true, p, af, at);
+    }
     for (int q = 0; q < 3; ++q) { sh[q][threadIdx.x] = af[q]; sh[3 + q][threadIdx.x] = at[q]; }
     __syncthreads();
-    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-      if (threadIdx.x < s)
-        for (int q = 0; q < 6; ++q) sh[q][threadIdx.x] += sh[q][threadIdx.x + s];
+    for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+      if (threadIdx.x < st)
+        for (int q = 0; q < 6; ++q) sh[q][threadIdx.x] += sh[q][threadIdx.x + st];
       __syncthreads();
     }
     if (threadIdx.x < 6) v.heavy_acc[6 * size_t(o) + threadIdx.x] = sh[threadIdx.x][0];
     __syncthreads();
   }
 }
-
 }  // namespace
 
 template <typename VelT>
@@ -333,13 +379,18 @@ __global__ void __launch_bounds__(128) k_integrate(DtView v, double h, double gx
   decode_pos(v.dom, v.own.voxel[o], v.own.sub[o], p[0], p[1], p[2]);
   // --- reduction (reduce_to_owners order) ---
   double af[3] = {0, 0, 0}, at[3] = {0, 0, 0};
-  uint32_t lo = v.inc_start[o], hi = v.inc_start[o + 1];
-  if (hi - lo > kHeavyThreshold) {
-    const double *ha = v.heavy_acc + 6 * size_t(o);
-    af[0] = ha[0]; af[1] = ha[1]; af[2] = ha[2];
-    at[0] = ha[3]; at[1] = ha[4]; at[2] = ha[5];
-  } else if (hi > lo) {
-    accumulate(v, lo, hi, p, af, at);
+  {
+    unsigned long long alo[3], ahi[3];
+    a_ranges(v, o, alo, ahi);
+    const unsigned long long ninc = (ahi[0] - alo[0]) + (ahi[1] - alo[1]) + (ahi[2] - alo[2]) +
+                                    (v.inc_start[o + 1] - v.inc_start[o]);
+    if (ninc > kHeavyThreshold) {
+      const double *ha = v.heavy_acc + 6 * size_t(o);
+      af[0] = ha[0]; af[1] = ha[1]; af[2] = ha[2];
+      at[0] = ha[3]; at[1] = ha[4]; at[2] = ha[5];
+    } else if (ninc) {
+      accumulate(v, o, p, af, at);
+    }
   }
   if (write_acc && v.own.acc) {
     double *a = v.own.acc + 6 * size_t(o);
@@ -516,6 +567,8 @@ int dt_step_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
   v.touch = c->touch.as<uint8_t>();
   v.inc = c->inc.as<uint32_t>();
   v.inc_start = c->inc_start.as<uint32_t>();
+  v.seg = c->acs.seg.as<unsigned long long>();
+  v.n_sph = c->n_sph;
   v.heavy = c->heavy.as<uint32_t>();
   v.n_heavy = c->heavy_count.as<unsigned long long>();
   v.heavy_acc = c->heavy_acc.as<double>();

@@ -395,21 +395,46 @@ __device__ __forceinline__ bool ss_pair_sorted(const KtView &v, const Grid &g, c
   return true;
 }
 
+// exact test of one queued candidate (sorted indices u0, u1) and its output
+__device__ __forceinline__ void ss_resolve(const KtView &v, const Grid &g, const double4 *sc, const uint4 *sm,
+                                           bool valid, uint2 q, unsigned long long *counts, uint2 *tmp,
+                                           unsigned long long *tmp_n, unsigned long long cap) {
+  bool hit = false;
+  uint2 e = make_uint2(0, 0);
+  if (valid) {
+    const double4 c0 = sc[q.x], c1 = sc[q.y];
+    const uint4 m0 = sm[q.x], m1 = sm[q.y];
+    const bool lower = m0.x < m1.x;
+    hit = lower ? ss_pair_sorted(v, g, c0, m0, c1, m1) : ss_pair_sorted(v, g, c1, m1, c0, m0);
+    if (hit) {
+      const uint32_t a = lower ? m0.x : m1.x, b = lower ? m1.x : m0.x;
+      e = make_uint2(a, b);
+      atomicAdd(&counts[a], 1ull);
+    }
+  }
+  append_pair(hit, e, tmp, tmp_n, cap);
+}
+
 // Sphere-sphere pairs among small spheres, one thread per cell-sorted sphere,
 // half stencil: the later spheres of its own cell plus the 13 forward
-// neighbour cells, so every unordered pair is evaluated exactly once.  Hits
-// are counted into the segment of the lower slot and appended to a scratch
-// list (placed into canonical segments by k_place / k_sort_seg).
+// neighbour cells, so every unordered pair is evaluated exactly once.
+// A cheap conservative fp32 distance test runs per lane; survivors are
+// compacted (ballot) into a per-warp shared-memory queue and the exact fp64
+// reference predicate runs on full 32-lane batches.  Hits are counted into the
+// segment of the lower slot and appended to the scratch list (placed into
+// canonical segments by k_place / k_sort_seg).
 __global__ void __launch_bounds__(128) k_pairs_ss(KtView v, const double4 *sc, const uint4 *sm,
                                                   const float4 *sf, unsigned long long *counts, uint2 *tmp,
                                                   unsigned long long *tmp_n, unsigned long long cap) {
+  __shared__ uint2 queue[4][64];
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  uint2 *Q = queue[wq];
+  int qn = 0;  // warp-uniform queue length
   int64_t u64 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   const Grid g = *v.grid;
   bool active = u64 < v.sph.n && g.valid;
-  uint32_t key = active ? v.bin_key[u64] : 0xFFFFFFFFu;
-  active = active && key != 0xFFFFFFFFu;
-  double4 c0 = make_double4(0, 0, 0, 0);
-  uint4 m0 = make_uint4(0, 0, 0, 0);
+  uint32_t key = active ? v.bin_key[u64] : kNoCell;
+  active = active && key != kNoCell;
   float4 f0 = make_float4(0.f, 0.f, 0.f, 0.f);
   long long cx = 0, cy = 0, cz = 0;
   // conservative fp32 prefilter: coordinates are rounded relative to the grid
@@ -418,8 +443,6 @@ __global__ void __launch_bounds__(128) k_pairs_ss(KtView v, const double4 *sc, c
   const float slack = 1e-6f * ext + 1e-30f;
   const float marg = float(v.margin);
   if (active) {
-    c0 = sc[u64];
-    m0 = sm[u64];
     f0 = sf[u64];
     cx = key % g.nc[0];
     cy = (key / g.nc[0]) % g.nc[1];
@@ -453,32 +476,36 @@ __global__ void __launch_bounds__(128) k_pairs_ss(KtView v, const double4 *sc, c
         }
       }
     }
-    // warp-uniform trip count keeps the ballot in append_pair convergent
-    uint32_t len = s1 > s0 ? s1 - s0 : 0;
+    const uint32_t len = s1 > s0 ? s1 - s0 : 0;
     uint32_t maxlen = len;
     for (int off = 16; off > 0; off >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, off));
     for (uint32_t t = 0; t < maxlen; ++t) {
-      bool hit = false;
-      uint2 e = make_uint2(0, 0);
+      bool pass = false;
+      const uint32_t w = s0 + t;
       if (t < len) {
-        uint32_t w = s0 + t;
         const float4 f1 = sf[w];
         const float dx = f0.x - f1.x, dy = f0.y - f1.y, dz = f0.z - f1.z;
         const float rr = f0.w + f1.w + marg + slack;
-        if (dx * dx + dy * dy + dz * dz < rr * rr * 1.0001f) {
-          double4 c1 = sc[w];
-          uint4 m1 = sm[w];
-          bool lower = m0.x < m1.x;
-          hit = lower ? ss_pair_sorted(v, g, c0, m0, c1, m1) : ss_pair_sorted(v, g, c1, m1, c0, m0);
-          if (hit) {
-            uint32_t a = lower ? m0.x : m1.x, b = lower ? m1.x : m0.x;
-            e = make_uint2(a, b);
-            atomicAdd(&counts[a], 1ull);
-          }
-        }
+        pass = dx * dx + dy * dy + dz * dz < rr * rr * 1.0001f;
       }
-      append_pair(hit, e, tmp, tmp_n, cap);
+      const unsigned m = __ballot_sync(0xffffffffu, pass);
+      if (pass) Q[qn + __popc(m & ((1u << lane) - 1u))] = make_uint2(uint32_t(u64), w);
+      qn += __popc(m);
+      if (qn >= 32) {
+        __syncwarp();
+        const uint2 q = Q[lane];
+        __syncwarp();
+        if (lane < qn - 32) Q[lane] = Q[32 + lane];
+        qn -= 32;
+        __syncwarp();
+        ss_resolve(v, g, sc, sm, true, q, counts, tmp, tmp_n, cap);
+      }
     }
+  }
+  __syncwarp();
+  if (qn > 0) {
+    const uint2 q = Q[lane < qn ? lane : 0];
+    ss_resolve(v, g, sc, sm, lane < qn, q, counts, tmp, tmp_n, cap);
   }
 }
 
@@ -686,6 +713,8 @@ __global__ void k_seg_count(int64_t n, const uint2 *ids, int64_t n_sph, unsigned
   atomicAdd(&cnt[int64_t(id.y >> kKindShift) * n_sph + id.x], 1ull);
 }
 
+// B-side incidences only: the A side of every owner is the contiguous run of
+// its spheres' (kind, sphere) segments and needs no list
 __global__ void k_inc_keys(int64_t n, const uint2 *ids, const uint32_t *sph_owner,
                            const uint32_t *tri_owner, const uint32_t *ana_owner, uint32_t *key,
                            uint32_t *val) {
@@ -693,15 +722,15 @@ __global__ void k_inc_keys(int64_t n, const uint2 *ids, const uint32_t *sph_owne
   if (k >= n) return;
   uint2 id = ids[k];
   uint32_t kind = id.y >> kKindShift, sb = id.y & kSlotMask;
-  uint32_t ob = kind == 0 ? sph_owner[sb] : (kind == 1 ? tri_owner[sb] : ana_owner[sb]);
-  key[2 * k] = sph_owner[id.x];
-  val[2 * k] = uint32_t(k) << 1;
-  key[2 * k + 1] = ob;
-  val[2 * k + 1] = (uint32_t(k) << 1) | 1u;
+  key[k] = kind == 0 ? sph_owner[sb] : (kind == 1 ? tri_owner[sb] : ana_owner[sb]);
+  val[k] = uint32_t(k);
 }
 
+// per-owner start of its B list; heavy owners (A + B incidences above the
+// threshold) are collected for the block reduction
 __global__ void k_inc_start(int64_t n_owner, int64_t n_inc, const uint32_t *sorted_key,
-                            uint32_t *start, uint32_t *heavy, unsigned long long *n_heavy,
+                            uint32_t *start, const unsigned long long *seg, const uint32_t *first,
+                            int64_t n_sph, uint32_t *heavy, unsigned long long *n_heavy,
                             uint32_t heavy_threshold) {
   int64_t o = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (o > n_owner) return;
@@ -717,7 +746,11 @@ __global__ void k_inc_start(int64_t n_owner, int64_t n_inc, const uint32_t *sort
       int64_t mid = (lo2 + hi2) >> 1;
       if (sorted_key[mid] <= uint32_t(o)) lo2 = mid + 1; else hi2 = mid;
     }
-    if (uint32_t(lo2 - lo) > heavy_threshold) {
+    unsigned long long na = 0;
+    const uint32_t f0 = first[o], f1 = first[o + 1];
+    if (f1 > f0)
+      for (int kind = 0; kind < 3; ++kind) na += seg[kind * n_sph + f1] - seg[kind * n_sph + f0];
+    if ((unsigned long long)(lo2 - lo) + na > heavy_threshold) {
       unsigned long long slot = atomicAdd(n_heavy, 1ull);
       heavy[slot] = uint32_t(o);
     }
@@ -1014,15 +1047,13 @@ int build_incidence(Ctx *c, cudaStream_t s) {
   const int64_t n = c->acs.n;
   const int64_t cap = std::max<int64_t>(c->acs.cap, 1);
   if (ensure(c, c->out_c, sizeof(double) * 9 * cap, s) || ensure(c, c->touch, cap, s) ||
-      ensure(c, c->inc, sizeof(uint32_t) * 2 * cap, s) ||
-      ensure(c, c->inc_alt, sizeof(uint32_t) * 2 * cap, s) ||
-      ensure(c, c->inc_key, sizeof(uint32_t) * 2 * cap, s) ||
-      ensure(c, c->inc_key_alt, sizeof(uint32_t) * 2 * cap, s) ||
+      ensure(c, c->inc, sizeof(uint32_t) * cap, s) || ensure(c, c->inc_alt, sizeof(uint32_t) * cap, s) ||
+      ensure(c, c->inc_key, sizeof(uint32_t) * cap, s) ||
+      ensure(c, c->inc_key_alt, sizeof(uint32_t) * cap, s) ||
       ensure(c, c->inc_start, sizeof(uint32_t) * (c->n_owner + 2), s) ||
       ensure(c, c->heavy, sizeof(uint32_t) * (c->n_owner + 1), s))
     return -1;
-  Status *st = c->status.as<Status>();
-  (void)st;
+  if (!c->acs.seg.p && build_segments(c, c->acs, s)) return -1;
   if (n) {
     k_inc_keys<<<grid_for(n), kBlock, 0, s>>>(n, c->acs.ids.as<uint2>(), c->sph_owner.as<uint32_t>(),
                                              c->tri_owner.as<uint32_t>(), c->ana_owner.as<uint32_t>(),
@@ -1032,9 +1063,9 @@ int build_incidence(Ctx *c, cudaStream_t s) {
     size_t tmp = 0;
     cub::DoubleBuffer<uint32_t> dk(c->inc_key.as<uint32_t>(), c->inc_key_alt.as<uint32_t>());
     cub::DoubleBuffer<uint32_t> dv(c->inc.as<uint32_t>(), c->inc_alt.as<uint32_t>());
-    cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, int(2 * n), 0, bits, s);
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, int(n), 0, bits, s);
     if (ensure(c, c->cub_tmp_dt, tmp + 16, s)) return -1;
-    GF_CHECK(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp_dt.p, tmp, dk, dv, int(2 * n), 0, bits, s));
+    GF_CHECK(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp_dt.p, tmp, dk, dv, int(n), 0, bits, s));
     if (dk.Current() != c->inc_key.as<uint32_t>()) {
       std::swap(c->inc_key, c->inc_key_alt);
       std::swap(c->inc, c->inc_alt);
@@ -1042,7 +1073,8 @@ int build_incidence(Ctx *c, cudaStream_t s) {
   }
   GF_CHECK(c, cudaMemsetAsync(c->heavy_count.p, 0, sizeof(unsigned long long), s));
   k_inc_start<<<grid_for(c->n_owner + 1), kBlock, 0, s>>>(
-      c->n_owner, 2 * n, c->inc_key.as<uint32_t>(), c->inc_start.as<uint32_t>(),
+      c->n_owner, n, c->inc_key.as<uint32_t>(), c->inc_start.as<uint32_t>(),
+      c->acs.seg.as<unsigned long long>(), c->sph_first.as<uint32_t>(), c->n_sph,
       c->heavy.as<uint32_t>(), c->heavy_count.as<unsigned long long>(), kHeavyThreshold);
   GF_CHECK(c, cudaGetLastError());
   return 0;
