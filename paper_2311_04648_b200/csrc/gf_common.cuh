@@ -47,6 +47,8 @@ struct Owners {
   double4 *tpl;        // per template: mass, moi x, y, z
   double *acc;         // [n*6] force xyz, torque xyz (global frame), optional
   double *ext;         // [n*6] external force/torque or nullptr
+  long long *facc;     // [n*6] fixed-point accumulators (throughput build), zeroed by the integrator
+  double2 *tpl_scale;  // per template: fixed-point scale of force, torque
 };
 
 struct Spheres {

@@ -11,6 +11,7 @@
 // swaps the double buffer.  Adoption happens at a fixed step, so runs are
 // bitwise reproducible; period = 1, lag = 0 is the reference's sync mode.
 #include <algorithm>
+#include <cmath>
 #include <chrono>
 #include <cstring>
 #include <vector>
@@ -64,6 +65,8 @@ Owners owners_view(Ctx *c) {
   o.tpl = c->tpl.as<double4>();
   o.acc = c->acc.as<double>();
   o.ext = c->has_ext ? c->ext.as<double>() : nullptr;
+  o.facc = c->fixed_reduce ? c->facc.as<long long>() : nullptr;
+  o.tpl_scale = c->tpl_scale.as<double2>();
   return o;
 }
 Spheres spheres_view(Ctx *c) {
@@ -111,7 +114,38 @@ static void prof_collect(Ctx *c) {
   c->prof_used = 0;
 }
 
+// Fixed-point scales of the throughput build's owner accumulators.  A contact
+// force on owner o is bounded by F_o = 64 m_o max(v_err / h, |g|) (a larger
+// force trips the watchdog within a step); boundary owners (mass >= 1e13,
+// BOUNDARY_MASS in types.py:42) carry the sum over every clump instead.  The
+// scale leaves 12 bits of headroom for sums: resolution ~ 2^-50 F_o.
+static int update_fixed_scales(Ctx *c, double h, double v_err, const double *g) {
+  if (!c->fixed_reduce || (c->fx_h == h && c->fx_verr == v_err)) return 0;
+  double rate = v_err / h;
+  double gn = std::sqrt(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
+  if (gn > rate) rate = gn;
+  double m_clump_max = 0.0;
+  for (double m : c->h_tpl_mass)
+    if (m < 1e13 && m > m_clump_max) m_clump_max = m;
+  if (m_clump_max <= 0.0) m_clump_max = 1.0;
+  const double lever = c->lever_max > 0.0 ? c->lever_max : 1.0;
+  std::vector<double> sc(2 * (c->h_tpl_mass.size() + 1), 1.0);
+  for (size_t t = 0; t < c->h_tpl_mass.size(); ++t) {
+    double m = c->h_tpl_mass[t];
+    double fb = m < 1e13 ? 64.0 * m * rate : 64.0 * m_clump_max * rate * double(std::max<int64_t>(c->n_sph, 1));
+    double sf = std::ldexp(1.0, 50) / fb;
+    sc[2 * t] = sf;
+    sc[2 * t + 1] = sf / lever;
+  }
+  if (!c->h_tpl_mass.empty())
+    GF_CHECK(c, cudaMemcpy(c->tpl_scale.p, sc.data(), 16 * c->h_tpl_mass.size(), cudaMemcpyHostToDevice));
+  c->fx_h = h;
+  c->fx_verr = v_err;
+  return 0;
+}
+
 static int dt_step(Ctx *c, const StepArgs &a) {
+  if (update_fixed_scales(c, a.h, a.v_err, a.g)) return -1;
   return c->f32_state ? dt_step_f32(c, a, c->s_dt) : dt_step_f64(c, a, c->s_dt);
 }
 
@@ -210,6 +244,7 @@ gf_ctx *gf_create(int device, uint32_t flags) {
   c->device = device;
   c->flags = flags;
   c->f32_state = (flags & GF_STATE_F32) != 0;
+  c->fixed_reduce = c->f32_state;
   cudaStreamCreateWithFlags(&c->s_dt, cudaStreamNonBlocking);
   cudaStreamCreateWithFlags(&c->s_kt, cudaStreamNonBlocking);
   cudaEventCreateWithFlags(&c->ev_snap, cudaEventDisableTiming);
@@ -234,7 +269,7 @@ void gf_destroy(gf_ctx *ctx) {
   Ctx *c = &ctx->c;
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
-  DBuf *bufs[] = {&c->sph_center, &c->sph_first, &c->voxel, &c->sub, &c->quat, &c->lin_vel, &c->ang_vel, &c->meta, &c->tpl, &c->acc,
+  DBuf *bufs[] = {&c->facc, &c->tpl_scale, &c->sph_center, &c->sph_first, &c->voxel, &c->sub, &c->quat, &c->lin_vel, &c->ang_vel, &c->meta, &c->tpl, &c->acc,
                   &c->ext, &c->sph_owner, &c->sph_offr, &c->sph_mat, &c->tri_owner, &c->tri_local,
                   &c->tri_mat, &c->tri_world, &c->ana_owner, &c->ana_kind, &c->ana_local, &c->ana_mat,
                   &c->ana_world, &c->pair, &c->beta, &c->fam_mask, &c->fam_flags, &c->lv_mask,
@@ -285,6 +320,7 @@ int gf_upload_owners(gf_ctx *ctx, int64_t n, const uint64_t *voxel, const uint16
       ensure(c, c->ang_vel, vb * n, c->s_dt) || ensure(c, c->meta, 4 * n, c->s_dt) ||
       ensure(c, c->tpl, 32 * (n_tpl + 1), c->s_dt) || ensure(c, c->acc, 48 * n, c->s_dt) ||
       ensure(c, c->heavy_acc, 48 * n, c->s_dt) || ensure(c, c->inc_start, 4 * (n + 2), c->s_dt) ||
+      ensure(c, c->facc, 48 * n, c->s_dt) || ensure(c, c->tpl_scale, 16 * (n_tpl + 1), c->s_dt) ||
       ensure(c, c->heavy, 4 * (n + 1), c->s_dt))
     return -1;
   std::vector<uint16_t> s4(4 * n);
@@ -323,7 +359,10 @@ int gf_upload_owners(gf_ctx *ctx, int64_t n, const uint64_t *voxel, const uint16
     tp[4 * t + 3] = tpl_moi[3 * t + 2];
   }
   if (n_tpl) GF_CHECK(c, cudaMemcpy(c->tpl.p, tp.data(), 32 * n_tpl, cudaMemcpyHostToDevice));
+  c->h_tpl_mass.assign(tpl_mass, tpl_mass + n_tpl);
+  c->fx_h = -1.0;  // fixed-point scales recomputed at the next run
   GF_CHECK(c, cudaMemset(c->acc.p, 0, 48 * n));
+  GF_CHECK(c, cudaMemset(c->facc.p, 0, 48 * n));
   if (c->has_ext) GF_CHECK(c, cudaMemset(c->ext.p, 0, 48 * n));
   if (c->n_sph && c->sph_first.p && c->sph_center.bytes >= size_t(32 * c->n_sph)) {
     if (refresh_centers(c, c->s_dt) || refresh_world(c, c->s_dt)) return -1;
@@ -446,6 +485,19 @@ int gf_upload_geometry(gf_ctx *ctx, int64_t n_s, const int64_t *sph_owner, const
       ensure(c, c->tri_world, 72 * (n_t + 1), c->s_dt) || ensure(c, c->ana_world, 64 * (n_a + 1), c->s_dt))
     return -1;
   if (set_split(c, sph_params + 3, 4, n_s)) return -1;
+  c->lever_max = 0.0;
+  for (int64_t k = 0; k < n_s; ++k) {
+    const float *q = sph_params + 4 * k;
+    double l = std::sqrt(double(q[0]) * q[0] + double(q[1]) * q[1] + double(q[2]) * q[2]) + double(q[3]);
+    if (l > c->lever_max) c->lever_max = l;
+  }
+  for (int64_t k = 0; k < n_t; ++k)
+    for (int v = 0; v < 3; ++v) {
+      const float *q = tri_local + 9 * k + 3 * v;
+      double l = std::sqrt(double(q[0]) * q[0] + double(q[1]) * q[1] + double(q[2]) * q[2]);
+      if (l > c->lever_max) c->lever_max = l;
+    }
+  c->fx_h = -1.0;
   // spheres grouped by owner (ascending): CSR of each owner's sphere slots
   {
     std::vector<uint32_t> first(c->n_owner + 2, 0);

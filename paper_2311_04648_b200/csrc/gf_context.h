@@ -68,7 +68,10 @@ struct Ctx {
   Domain dom{};
   // owners
   int64_t n_owner = 0, n_tpl = 0;
-  DBuf voxel, sub, quat, lin_vel, ang_vel, meta, tpl, acc, ext;
+  DBuf voxel, sub, quat, lin_vel, ang_vel, meta, tpl, acc, ext, facc, tpl_scale;
+  bool fixed_reduce = false;  // throughput build: int64 fixed-point atomic owner reduction
+  std::vector<double> h_tpl_mass;
+  double lever_max = 0.0, fx_h = -1.0, fx_verr = -1.0;
   bool has_ext = false;
   // geometry
   int64_t n_sph = 0, n_tri = 0, n_ana = 0;

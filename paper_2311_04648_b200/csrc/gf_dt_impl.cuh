@@ -249,15 +249,33 @@ __global__ void __launch_bounds__(128) k_contacts(DtView v, double ts) {
       double out[6];
       hertz_mindlin(depth, ts, bx, by, bz, vx, vy, vz, rotbx - rotax, rotby - rotay, rotbz - rotaz,
                     mass_eff, ra, rb, v.sph.mat[id.x], mb, v.mat, v.wild + size_t(v.W) * k, out);
-      double *oc = v.out_c + 9 * size_t(k);
-      oc[0] = out[0]; oc[1] = out[1]; oc[2] = out[2];
-      oc[3] = out[0] + out[3]; oc[4] = out[1] + out[4]; oc[5] = out[2] + out[5];
-      oc[6] = px; oc[7] = py; oc[8] = pz;
+      const double tx = out[0] + out[3], ty = out[1] + out[4], tz = out[2] + out[5];
+      if (v.own.facc) {
+        // throughput build: +F / r_a x T on A, -F / -(r_b x T) on B, as int64
+        // fixed point (order-independent sums: bitwise reproducible runs)
+        const double2 sa = v.own.tpl_scale[meta_tpl(v.own.meta[oa])];
+        const double2 sbs = v.own.tpl_scale[meta_tpl(v.own.meta[ob])];
+        unsigned long long *fa = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(oa));
+        unsigned long long *fb = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(ob));
+        const double ta[3] = {ray * tz - raz * ty, raz * tx - rax * tz, rax * ty - ray * tx};
+        const double tb[3] = {rby * tz - rbz * ty, rbz * tx - rbx * tz, rbx * ty - rby * tx};
+        for (int q = 0; q < 3; ++q) {
+          atomicAdd(fa + q, (unsigned long long)__double2ll_rn(out[q] * sa.x));
+          atomicAdd(fa + 3 + q, (unsigned long long)__double2ll_rn(ta[q] * sa.y));
+          atomicAdd(fb + q, (unsigned long long)__double2ll_rn(-out[q] * sbs.x));
+          atomicAdd(fb + 3 + q, (unsigned long long)__double2ll_rn(-tb[q] * sbs.y));
+        }
+      } else {
+        double *oc = v.out_c + 9 * size_t(k);
+        oc[0] = out[0]; oc[1] = out[1]; oc[2] = out[2];
+        oc[3] = tx; oc[4] = ty; oc[5] = tz;
+        oc[6] = px; oc[7] = py; oc[8] = pz;
+      }
       t = 1;
       touching = kind == 0 ? 2u : 1u;
       pairs = 1;
     }
-    v.touch[k] = t;
+    if (!v.own.facc) v.touch[k] = t;
   }
   // block total of touching spheres (integer: order-independent)
   for (int off = 16; off > 0; off >>= 1) {
@@ -379,7 +397,15 @@ __global__ void __launch_bounds__(128) k_integrate(DtView v, double h, double gx
   decode_pos(v.dom, v.own.voxel[o], v.own.sub[o], p[0], p[1], p[2]);
   // --- reduction (reduce_to_owners order) ---
   double af[3] = {0, 0, 0}, at[3] = {0, 0, 0};
-  {
+  if (v.own.facc) {
+    longlong2 *fp = reinterpret_cast<longlong2 *>(v.own.facc + 6 * size_t(o));
+    const longlong2 a0 = fp[0], a1 = fp[1], a2 = fp[2];
+    const double2 sc = v.own.tpl_scale[meta_tpl(v.own.meta[o])];
+    af[0] = double(a0.x) / sc.x; af[1] = double(a0.y) / sc.x; af[2] = double(a1.x) / sc.x;
+    at[0] = double(a1.y) / sc.y; at[1] = double(a2.x) / sc.y; at[2] = double(a2.y) / sc.y;
+    const longlong2 z = make_longlong2(0, 0);
+    fp[0] = z; fp[1] = z; fp[2] = z;
+  } else {
     unsigned long long alo[3], ahi[3];
     a_ranges(v, o, alo, ahi);
     const unsigned long long ninc = (ahi[0] - alo[0]) + (ahi[1] - alo[1]) + (ahi[2] - alo[2]) +
@@ -581,7 +607,7 @@ int dt_step_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
     k_contacts<VelT><<<g, 128, 0, s>>>(v, a.h);
   }
   if (ev) cudaEventRecord(ev[1], s);
-  if (v.n_acs) k_heavy<<<64, 256, 0, s>>>(v);
+  if (v.n_acs && !c->fixed_reduce) k_heavy<<<64, 256, 0, s>>>(v);
   if (ev) cudaEventRecord(ev[2], s);
   if (c->n_dyn) {
     k_apply_dyn<<<(c->n_dyn + 127) / 128, 128, 0, s>>>(

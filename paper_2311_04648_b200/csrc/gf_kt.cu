@@ -1044,6 +1044,7 @@ int build_segments(Ctx *c, Acs &a, cudaStream_t s) {
 }
 
 int build_incidence(Ctx *c, cudaStream_t s) {
+  if (c->fixed_reduce) return 0;  // throughput build reduces with atomics
   const int64_t n = c->acs.n;
   const int64_t cap = std::max<int64_t>(c->acs.cap, 1);
   if (ensure(c, c->out_c, sizeof(double) * 9 * cap, s) || ensure(c, c->touch, cap, s) ||
