@@ -116,9 +116,10 @@ static void prof_collect(Ctx *c) {
 
 // Fixed-point scales of the throughput build's owner accumulators.  A contact
 // force on owner o is bounded by F_o = 64 m_o max(v_err / h, |g|) (a larger
-// force trips the watchdog within a step); boundary owners (mass >= 1e13,
-// BOUNDARY_MASS in types.py:42) carry the sum over every clump instead.  The
-// scale leaves 12 bits of headroom for sums: resolution ~ 2^-50 F_o.
+// force trips the watchdog within a step).  The scale leaves 13 bits of
+// headroom for sums: resolution ~ 2^-50 F_o.  Boundary owners (mass >= 1e13,
+// BOUNDARY_MASS in types.py:42) are fixed or prescribed, so their sums never
+// feed the dynamics; they accumulate with fp64 atomics (scale 0 marks them).
 static int update_fixed_scales(Ctx *c, double h, double v_err, const double *g) {
   if (!c->fixed_reduce || (c->fx_h == h && c->fx_verr == v_err)) return 0;
   double rate = v_err / h;
@@ -132,8 +133,12 @@ static int update_fixed_scales(Ctx *c, double h, double v_err, const double *g) 
   std::vector<double> sc(2 * (c->h_tpl_mass.size() + 1), 1.0);
   for (size_t t = 0; t < c->h_tpl_mass.size(); ++t) {
     double m = c->h_tpl_mass[t];
-    double fb = m < 1e13 ? 64.0 * m * rate : 64.0 * m_clump_max * rate * double(std::max<int64_t>(c->n_sph, 1));
-    double sf = std::ldexp(1.0, 50) / fb;
+    if (m >= 1e13) {  // boundary owner: fp64 atomics (its sums never feed the dynamics)
+      sc[2 * t] = 0.0;
+      sc[2 * t + 1] = 0.0;
+      continue;
+    }
+    double sf = std::ldexp(1.0, 50) / (64.0 * m * rate);
     sc[2 * t] = sf;
     sc[2 * t + 1] = sf / lever;
   }
@@ -269,7 +274,7 @@ void gf_destroy(gf_ctx *ctx) {
   Ctx *c = &ctx->c;
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
-  DBuf *bufs[] = {&c->facc, &c->tpl_scale, &c->sph_center, &c->sph_first, &c->voxel, &c->sub, &c->quat, &c->lin_vel, &c->ang_vel, &c->meta, &c->tpl, &c->acc,
+  DBuf *bufs[] = {&c->tlist, &c->tlist_n, &c->facc, &c->tpl_scale, &c->sph_center, &c->sph_first, &c->voxel, &c->sub, &c->quat, &c->lin_vel, &c->ang_vel, &c->meta, &c->tpl, &c->acc,
                   &c->ext, &c->sph_owner, &c->sph_offr, &c->sph_mat, &c->tri_owner, &c->tri_local,
                   &c->tri_mat, &c->tri_world, &c->ana_owner, &c->ana_kind, &c->ana_local, &c->ana_mat,
                   &c->ana_world, &c->pair, &c->beta, &c->fam_mask, &c->fam_flags, &c->lv_mask,

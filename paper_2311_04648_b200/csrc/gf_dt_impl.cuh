@@ -168,123 +168,160 @@ __device__ __forceinline__ void owner_kin(const DtView &v, uint32_t o, double po
   mass = v.own.tpl[meta_tpl(v.own.meta[o])].x;
 }
 
-template <typename VelT>
-__global__ void __launch_bounds__(128) k_contacts(DtView v, double ts) {
+// contact geometry of ACS entry `id` (_kernels.py:442-491): depth, B-to-A
+// unit vector, B-side curvature radius; A's centre and radius returned too
+__device__ __forceinline__ void contact_geometry(const DtView &v, uint2 id, double ca[3], double &ra,
+                                                 double &depth, double &bx, double &by, double &bz,
+                                                 double &rb) {
+  const uint32_t kind = id.y >> kKindShift, sb = id.y & kSlotMask;
+  const double4 cA = v.sph.center[id.x];
+  ca[0] = cA.x; ca[1] = cA.y; ca[2] = cA.z;
+  ra = cA.w;
+  if (kind == 0) {
+    const double4 cB = v.sph.center[sb];
+    double dx = ca[0] - cB.x, dy = ca[1] - cB.y, dz = ca[2] - cB.z;
+    double d = sqrt(dx * dx + dy * dy + dz * dz);
+    rb = cB.w;
+    if (d < 1e-300) {
+      depth = ra + rb; bx = 0.0; by = 0.0; bz = 1.0;
+    } else {
+      double inv = 1.0 / d;
+      bx = dx * inv; by = dy * inv; bz = dz * inv;
+      depth = ra + rb - d;
+    }
+  } else if (kind == 1) {
+    const double *T = v.tri.world + 9 * size_t(sb);
+    double qx, qy, qz;
+    closest_on_tri(ca[0], ca[1], ca[2], T, qx, qy, qz);
+    double dx = ca[0] - qx, dy = ca[1] - qy, dz = ca[2] - qz;
+    double d = sqrt(dx * dx + dy * dy + dz * dz);
+    if (d < 1e-300) {
+      double e1x = T[3] - T[0], e1y = T[4] - T[1], e1z = T[5] - T[2];
+      double e2x = T[6] - T[0], e2y = T[7] - T[1], e2z = T[8] - T[2];
+      double nx = e1y * e2z - e1z * e2y, ny = e1z * e2x - e1x * e2z, nz = e1x * e2y - e1y * e2x;
+      double nn = sqrt(nx * nx + ny * ny + nz * nz);
+      bx = nx / nn; by = ny / nn; bz = nz / nn;
+    } else {
+      double inv = 1.0 / d;
+      bx = dx * inv; by = dy * inv; bz = dz * inv;
+    }
+    depth = ra - d;
+    rb = kFlatRadius;
+  } else {
+    double gap;
+    analytic_gap(v.ana.kind[sb], v.ana.world + 8 * size_t(sb), ca[0], ca[1], ca[2], gap, bx, by, bz, rb);
+    depth = ra - gap;
+  }
+}
+
+namespace {
+// narrow phase of the step: one thread per ACS entry, geometry only.
+// Touching entries are compacted into tlist (warp-aggregated append); the
+// fp64 parity build also records a touch flag per entry for its reduction.
+// A false positive leaves its history untouched (forces.py:95-97).
+__global__ void __launch_bounds__(256, 4) k_touch(DtView v, uint32_t *tlist, unsigned long long *tlist_n) {
   int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  unsigned touching = 0, pairs = 0;
+  bool t = false;
+  unsigned kind = 0;
   if (k < v.n_acs && !v.st->err) {
-    uint2 id = v.ids[k];
+    const uint2 id = v.ids[k];
+    kind = id.y >> kKindShift;
+    double ca[3], ra, depth, bx, by, bz, rb;
+    contact_geometry(v, id, ca, ra, depth, bx, by, bz, rb);
+    t = depth > 0.0;
+    if (!v.own.facc) v.touch[k] = t ? 1 : 0;
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, t);
+  const int lane = threadIdx.x & 31;
+  unsigned long long base = 0;
+  if (m && lane == 0) base = atomicAdd(tlist_n, (unsigned long long)__popc(m));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (t) tlist[base + __popc(m & ((1u << lane) - 1u))] = uint32_t(k);
+  // touching counts (integers: order-independent)
+  unsigned touching = t ? (kind == 0 ? 2u : 1u) : 0u;
+  for (int off = 16; off > 0; off >>= 1) touching += __shfl_down_sync(0xffffffffu, touching, off);
+  if (lane == 0 && m) {
+    atomicAdd(&v.st->touching, (unsigned long long)touching);
+    atomicAdd(&v.st->touch_pairs, (unsigned long long)__popc(m));
+  }
+}
+
+}  // namespace
+
+// force phase: touching entries only.  Pair kinematics (forces.py:55-79), the
+// Hertz-Mindlin core, history update, then either the per-contact output of
+// the parity build (F, F + torque-only force, contact point) or the
+// fixed-point owner accumulation of the throughput build.
+template <typename VelT>
+__global__ void __launch_bounds__(128) k_forces(DtView v, double ts, const uint32_t *tlist,
+                                                const unsigned long long *tlist_n) {
+  const unsigned long long nt = *tlist_n;
+  if (v.st->err) return;
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < nt;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint32_t k = tlist[i];
+    const uint2 id = v.ids[k];
     const uint32_t kind = id.y >> kKindShift, sb = id.y & kSlotMask;
-    const double4 cA = v.sph.center[id.x];
-    const double ca[3] = {cA.x, cA.y, cA.z};
-    const double ra = cA.w;
-    double depth, bx, by, bz, rb;
+    double ca[3], ra, depth, bx, by, bz, rb;
+    contact_geometry(v, id, ca, ra, depth, bx, by, bz, rb);
+    const uint32_t oa = v.sph.owner[id.x];
     uint32_t ob;
     int mb;
-    if (kind == 0) {
-      const double4 cB = v.sph.center[sb];
-      ob = sb;  // resolved to the owner below, only for touching pairs
-      mb = -1;
-      double dx = ca[0] - cB.x, dy = ca[1] - cB.y, dz = ca[2] - cB.z;
-      double d = sqrt(dx * dx + dy * dy + dz * dz);
-      rb = cB.w;
-      if (d < 1e-300) {
-        depth = ra + rb; bx = 0.0; by = 0.0; bz = 1.0;
-      } else {
-        double inv = 1.0 / d;
-        bx = dx * inv; by = dy * inv; bz = dz * inv;
-        depth = ra + rb - d;
-      }
-    } else if (kind == 1) {
-      ob = v.tri.owner[sb];
-      mb = v.tri.mat[sb];
-      const double *T = v.tri.world + 9 * size_t(sb);
-      double qx, qy, qz;
-      closest_on_tri(ca[0], ca[1], ca[2], T, qx, qy, qz);
-      double dx = ca[0] - qx, dy = ca[1] - qy, dz = ca[2] - qz;
-      double d = sqrt(dx * dx + dy * dy + dz * dz);
-      if (d < 1e-300) {
-        double e1x = T[3] - T[0], e1y = T[4] - T[1], e1z = T[5] - T[2];
-        double e2x = T[6] - T[0], e2y = T[7] - T[1], e2z = T[8] - T[2];
-        double nx = e1y * e2z - e1z * e2y, ny = e1z * e2x - e1x * e2z, nz = e1x * e2y - e1y * e2x;
-        double nn = sqrt(nx * nx + ny * ny + nz * nz);
-        bx = nx / nn; by = ny / nn; bz = nz / nn;
-      } else {
-        double inv = 1.0 / d;
-        bx = dx * inv; by = dy * inv; bz = dz * inv;
-      }
-      depth = ra - d;
-      rb = kFlatRadius;
-    } else {
-      ob = v.ana.owner[sb];
-      mb = v.ana.mat[sb];
-      double gap;
-      analytic_gap(v.ana.kind[sb], v.ana.world + 8 * size_t(sb), ca[0], ca[1], ca[2], gap, bx, by, bz, rb);
-      depth = ra - gap;
-    }
-    uint8_t t = 0;
-    if (depth > 0.0) {
-      const uint32_t oa = v.sph.owner[id.x];
-      if (kind == 0) {
-        ob = v.sph.owner[sb];
-        mb = v.sph.mat[sb];
-      }
-      double half = ra - 0.5 * depth;
-      double px = ca[0] - bx * half, py = ca[1] - by * half, pz = ca[2] - bz * half;
-      double pa[3], va[3], wa[3], ma, pb[3], vb[3], wb[3], mbass;
-      owner_kin<VelT>(v, oa, pa, va, wa, ma);
-      owner_kin<VelT>(v, ob, pb, vb, wb, mbass);
-      double rax = px - pa[0], ray = py - pa[1], raz = pz - pa[2];
-      double rbx = px - pb[0], rby = py - pb[1], rbz = pz - pb[2];
-      double rotax = wa[1] * raz - wa[2] * ray;
-      double rotay = wa[2] * rax - wa[0] * raz;
-      double rotaz = wa[0] * ray - wa[1] * rax;
-      double rotbx = wb[1] * rbz - wb[2] * rby;
-      double rotby = wb[2] * rbx - wb[0] * rbz;
-      double rotbz = wb[0] * rby - wb[1] * rbx;
-      double vx = (va[0] + rotax) - (vb[0] + rotbx);
-      double vy = (va[1] + rotay) - (vb[1] + rotby);
-      double vz = (va[2] + rotaz) - (vb[2] + rotbz);
-      double mass_eff = (ma * mbass) / (ma + mbass);
-      double out[6];
-      hertz_mindlin(depth, ts, bx, by, bz, vx, vy, vz, rotbx - rotax, rotby - rotay, rotbz - rotaz,
-                    mass_eff, ra, rb, v.sph.mat[id.x], mb, v.mat, v.wild + size_t(v.W) * k, out);
-      const double tx = out[0] + out[3], ty = out[1] + out[4], tz = out[2] + out[5];
-      if (v.own.facc) {
-        // throughput build: +F / r_a x T on A, -F / -(r_b x T) on B, as int64
-        // fixed point (order-independent sums: bitwise reproducible runs)
-        const double2 sa = v.own.tpl_scale[meta_tpl(v.own.meta[oa])];
-        const double2 sbs = v.own.tpl_scale[meta_tpl(v.own.meta[ob])];
-        unsigned long long *fa = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(oa));
-        unsigned long long *fb = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(ob));
-        const double ta[3] = {ray * tz - raz * ty, raz * tx - rax * tz, rax * ty - ray * tx};
-        const double tb[3] = {rby * tz - rbz * ty, rbz * tx - rbx * tz, rbx * ty - rby * tx};
-        for (int q = 0; q < 3; ++q) {
+    if (kind == 0) { ob = v.sph.owner[sb]; mb = v.sph.mat[sb]; }
+    else if (kind == 1) { ob = v.tri.owner[sb]; mb = v.tri.mat[sb]; }
+    else { ob = v.ana.owner[sb]; mb = v.ana.mat[sb]; }
+    double half = ra - 0.5 * depth;
+    double px = ca[0] - bx * half, py = ca[1] - by * half, pz = ca[2] - bz * half;
+    double pa[3], va[3], wa[3], ma, pb[3], vb[3], wb[3], mbass;
+    owner_kin<VelT>(v, oa, pa, va, wa, ma);
+    owner_kin<VelT>(v, ob, pb, vb, wb, mbass);
+    double rax = px - pa[0], ray = py - pa[1], raz = pz - pa[2];
+    double rbx = px - pb[0], rby = py - pb[1], rbz = pz - pb[2];
+    double rotax = wa[1] * raz - wa[2] * ray;
+    double rotay = wa[2] * rax - wa[0] * raz;
+    double rotaz = wa[0] * ray - wa[1] * rax;
+    double rotbx = wb[1] * rbz - wb[2] * rby;
+    double rotby = wb[2] * rbx - wb[0] * rbz;
+    double rotbz = wb[0] * rby - wb[1] * rbx;
+    double vx = (va[0] + rotax) - (vb[0] + rotbx);
+    double vy = (va[1] + rotay) - (vb[1] + rotby);
+    double vz = (va[2] + rotaz) - (vb[2] + rotbz);
+    double mass_eff = (ma * mbass) / (ma + mbass);
+    double out[6];
+    hertz_mindlin(depth, ts, bx, by, bz, vx, vy, vz, rotbx - rotax, rotby - rotay, rotbz - rotaz,
+                  mass_eff, ra, rb, v.sph.mat[id.x], mb, v.mat, v.wild + size_t(v.W) * k, out);
+    const double tx = out[0] + out[3], ty = out[1] + out[4], tz = out[2] + out[5];
+    if (v.own.facc) {
+      // throughput build: +F / r_a x T on A, -F / -(r_b x T) on B, as int64
+      // fixed point (order-independent sums: bitwise reproducible runs)
+      const double2 sa = v.own.tpl_scale[meta_tpl(v.own.meta[oa])];
+      const double2 sbs = v.own.tpl_scale[meta_tpl(v.own.meta[ob])];
+      unsigned long long *fa = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(oa));
+      unsigned long long *fb = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(ob));
+      const double ta[3] = {ray * tz - raz * ty, raz * tx - rax * tz, rax * ty - ray * tx};
+      const double tb[3] = {rby * tz - rbz * ty, rbz * tx - rbx * tz, rbx * ty - rby * tx};
+      for (int q = 0; q < 3; ++q) {
+        if (sa.x > 0.0) {
           atomicAdd(fa + q, (unsigned long long)__double2ll_rn(out[q] * sa.x));
           atomicAdd(fa + 3 + q, (unsigned long long)__double2ll_rn(ta[q] * sa.y));
+        } else {
+          atomicAdd(reinterpret_cast<double *>(fa + q), out[q]);
+          atomicAdd(reinterpret_cast<double *>(fa + 3 + q), ta[q]);
+        }
+        if (sbs.x > 0.0) {
           atomicAdd(fb + q, (unsigned long long)__double2ll_rn(-out[q] * sbs.x));
           atomicAdd(fb + 3 + q, (unsigned long long)__double2ll_rn(-tb[q] * sbs.y));
+        } else {
+          atomicAdd(reinterpret_cast<double *>(fb + q), -out[q]);
+          atomicAdd(reinterpret_cast<double *>(fb + 3 + q), -tb[q]);
         }
-      } else {
-        double *oc = v.out_c + 9 * size_t(k);
-        oc[0] = out[0]; oc[1] = out[1]; oc[2] = out[2];
-        oc[3] = tx; oc[4] = ty; oc[5] = tz;
-        oc[6] = px; oc[7] = py; oc[8] = pz;
       }
-      t = 1;
-      touching = kind == 0 ? 2u : 1u;
-      pairs = 1;
+    } else {
+      double *oc = v.out_c + 9 * size_t(k);
+      oc[0] = out[0]; oc[1] = out[1]; oc[2] = out[2];
+      oc[3] = tx; oc[4] = ty; oc[5] = tz;
+      oc[6] = px; oc[7] = py; oc[8] = pz;
     }
-    if (!v.own.facc) v.touch[k] = t;
-  }
-  // block total of touching spheres (integer: order-independent)
-  for (int off = 16; off > 0; off >>= 1) {
-    touching += __shfl_down_sync(0xffffffff, touching, off);
-    pairs += __shfl_down_sync(0xffffffff, pairs, off);
-  }
-  if ((threadIdx.x & 31) == 0 && touching) {
-    atomicAdd(&v.st->touching, (unsigned long long)touching);
-    atomicAdd(&v.st->touch_pairs, (unsigned long long)pairs);
   }
 }
 
@@ -401,8 +438,14 @@ __global__ void __launch_bounds__(128) k_integrate(DtView v, double h, double gx
     longlong2 *fp = reinterpret_cast<longlong2 *>(v.own.facc + 6 * size_t(o));
     const longlong2 a0 = fp[0], a1 = fp[1], a2 = fp[2];
     const double2 sc = v.own.tpl_scale[meta_tpl(v.own.meta[o])];
-    af[0] = double(a0.x) / sc.x; af[1] = double(a0.y) / sc.x; af[2] = double(a1.x) / sc.x;
-    at[0] = double(a1.y) / sc.y; at[1] = double(a2.x) / sc.y; at[2] = double(a2.y) / sc.y;
+    if (sc.x > 0.0) {
+      af[0] = double(a0.x) / sc.x; af[1] = double(a0.y) / sc.x; af[2] = double(a1.x) / sc.x;
+      at[0] = double(a1.y) / sc.y; at[1] = double(a2.x) / sc.y; at[2] = double(a2.y) / sc.y;
+    } else {
+      af[0] = __longlong_as_double(a0.x); af[1] = __longlong_as_double(a0.y);
+      af[2] = __longlong_as_double(a1.x); at[0] = __longlong_as_double(a1.y);
+      at[1] = __longlong_as_double(a2.x); at[2] = __longlong_as_double(a2.y);
+    }
     const longlong2 z = make_longlong2(0, 0);
     fp[0] = z; fp[1] = z; fp[2] = z;
   } else {
@@ -603,8 +646,10 @@ int dt_step_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
   cudaEvent_t *ev = prof_events(c);
   if (ev) cudaEventRecord(ev[0], s);
   if (v.n_acs) {
-    unsigned g = unsigned((v.n_acs + 127) / 128);
-    k_contacts<VelT><<<g, 128, 0, s>>>(v, a.h);
+    unsigned long long *tn = c->tlist_n.as<unsigned long long>();
+    GF_CHECK(c, cudaMemsetAsync(tn, 0, sizeof(unsigned long long), s));
+    k_touch<<<unsigned((v.n_acs + 255) / 256), 256, 0, s>>>(v, c->tlist.as<uint32_t>(), tn);
+    k_forces<VelT><<<148 * 8, 128, 0, s>>>(v, a.h, c->tlist.as<uint32_t>(), tn);
   }
   if (ev) cudaEventRecord(ev[1], s);
   if (v.n_acs && !c->fixed_reduce) k_heavy<<<64, 256, 0, s>>>(v);

@@ -1044,9 +1044,12 @@ int build_segments(Ctx *c, Acs &a, cudaStream_t s) {
 }
 
 int build_incidence(Ctx *c, cudaStream_t s) {
-  if (c->fixed_reduce) return 0;  // throughput build reduces with atomics
   const int64_t n = c->acs.n;
   const int64_t cap = std::max<int64_t>(c->acs.cap, 1);
+  if (ensure(c, c->tlist, sizeof(uint32_t) * cap, s) || ensure(c, c->tlist_n, 16, s) ||
+      ensure(c, c->touch, cap, s))
+    return -1;
+  if (c->fixed_reduce) return 0;  // throughput build reduces with atomics
   if (ensure(c, c->out_c, sizeof(double) * 9 * cap, s) || ensure(c, c->touch, cap, s) ||
       ensure(c, c->inc, sizeof(uint32_t) * cap, s) || ensure(c, c->inc_alt, sizeof(uint32_t) * cap, s) ||
       ensure(c, c->inc_key, sizeof(uint32_t) * cap, s) ||
