@@ -287,7 +287,7 @@ void gf_destroy(gf_ctx *ctx) {
                   &c->kt.cell_start, &c->kt.cell_end, &c->kt.tri_ranges, &c->kt.tri_cnt,
                   &c->kt.tri_start, &c->kt.tri_entries, &c->kt.counts, &c->kt.offsets, &c->kt.cub_tmp,
                   &c->kt.total, &c->kt.cursor, &c->kt.tri_cursor, &c->big_slots, &c->kt.sc,
-                  &c->kt.sm, &c->kt.sf, &c->kt.tmp, &c->kt.tmp_n, &c->acs.seg, &c->acs_next.seg};
+                  &c->kt.sm, &c->kt.sf, &c->kt.cells, &c->kt.n_cells, &c->kt.tmp, &c->kt.tmp_n, &c->acs.seg, &c->acs_next.seg};
   for (DBuf *b : bufs) release(*b);
   if (c->h_status) cudaFreeHost(c->h_status);
   cudaEvent_t evs[] = {c->ev_snap, c->ev_ca, c->ev_adopted, c->ev_count, c->t0, c->t1};

@@ -47,6 +47,7 @@ struct KtScratch {
   DBuf sc, sm, sf;   // cell-sorted copies: double4 (centre, radius), uint4 (slot, owner, family),
                      // float4 (centre - grid origin, radius) for the conservative fp32 prefilter
   DBuf tmp, tmp_n;   // scratch pair list (uint2) and its append counter
+  DBuf cells, n_cells;  // non-empty enumeration cells
   int64_t tmp_cap = 0;
   DBuf tri_cursor;   // uint32 per cell
   DBuf counts;       // uint64[3*n_s+1] per sphere SS / ST / SA counts
