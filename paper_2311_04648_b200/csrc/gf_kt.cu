@@ -463,51 +463,50 @@ __global__ void __launch_bounds__(128) k_pairs_ss(KtView v, const double4 *sc, c
     for (uint32_t o0 = c0; o0 < c1; o0 += 32) {  // own spheres, 32 per round
       const uint32_t no = min(32u, c1 - o0);
       const float4 fo = sf[o0 + (lane < int(no) ? lane : 0)];
-      // pairs inside the cell: own i with every later sphere of the cell
-      for (uint32_t i = 0; i < no; ++i) {
-        const float4 fi = make_float4(__shfl_sync(0xffffffffu, fo.x, i), __shfl_sync(0xffffffffu, fo.y, i),
-                                      __shfl_sync(0xffffffffu, fo.z, i), __shfl_sync(0xffffffffu, fo.w, i));
-        for (uint32_t base = o0 + i + 1; base < c1; base += 32) {
-          const uint32_t w = base + lane;
-          bool pass = false;
-          if (w < c1) {
+      // spans: 0 = the own cell (pairs own i < sphere j), then forward rows
+      // (dz, dy) = (0,0) x+1, (0,1), (1,-1), (1,0), (1,1)
+      for (int span = 0; span < 6; ++span) {
+        uint32_t s0, s1;
+        if (span == 0) {
+          s0 = o0;
+          s1 = c1;
+        } else {
+          const long long dz = span >= 3 ? 1 : 0;
+          const long long dy = span == 2 ? 1 : (span >= 3 ? span - 4 : 0);
+          long long x0 = span == 1 ? cx + 1 : cx - 1, x1 = cx + 1;
+          const long long y = cy + dy, z = cz + dz;
+          if (x0 < 0) x0 = 0;
+          if (x1 >= g.nc[0]) x1 = g.nc[0] - 1;
+          if (y < 0 || y >= g.nc[1] || z >= g.nc[2] || x0 > x1) continue;
+          const long long row = (z * g.nc[1] + y) * g.nc[0];
+          s0 = 0xFFFFFFFFu;
+          s1 = 0;
+          for (long long x = x0; x <= x1; ++x) {
+            const uint32_t st = v.cell_start[row + x];
+            if (st == 0xFFFFFFFFu) continue;
+            if (s0 == 0xFFFFFFFFu) s0 = st;
+            s1 = v.cell_end[row + x];
+          }
+          if (s0 == 0xFFFFFFFFu) continue;
+        }
+        // every (own i, candidate j) combination, flattened across the lanes
+        const uint32_t ns = s1 - s0;
+        const uint32_t combos = no * ns;
+        for (uint32_t t = 0; t < combos; t += 32) {
+          const uint32_t cidx = t + lane;
+          const uint32_t i = cidx / ns, j = cidx - i * ns;
+          const int src = cidx < combos ? int(i) : 0;
+          const float fx = __shfl_sync(0xffffffffu, fo.x, src), fy = __shfl_sync(0xffffffffu, fo.y, src);
+          const float fz = __shfl_sync(0xffffffffu, fo.z, src), fw = __shfl_sync(0xffffffffu, fo.w, src);
+          const uint32_t w = s0 + j;
+          bool pass = cidx < combos && (span != 0 || w > o0 + i);
+          if (pass) {
             const float4 f1 = sf[w];
-            const float dx = fi.x - f1.x, dy = fi.y - f1.y, dz = fi.z - f1.z;
-            const float rr = fi.w + f1.w + marg + slack;
+            const float dx = fx - f1.x, dy = fy - f1.y, dz = fz - f1.z;
+            const float rr = fw + f1.w + marg + slack;
             pass = dx * dx + dy * dy + dz * dz < rr * rr * 1.0001f;
           }
           push(pass, o0 + i, w);
-        }
-      }
-      // forward neighbour rows: (dz, dy) = (0,0) x+1, (0,1), (1,-1), (1,0), (1,1)
-      for (int span = 1; span < 6; ++span) {
-        const long long dz = span >= 3 ? 1 : 0;
-        const long long dy = span == 2 ? 1 : (span >= 3 ? span - 4 : 0);
-        long long x0 = span == 1 ? cx + 1 : cx - 1, x1 = cx + 1;
-        const long long y = cy + dy, z = cz + dz;
-        if (x0 < 0) x0 = 0;
-        if (x1 >= g.nc[0]) x1 = g.nc[0] - 1;
-        if (y < 0 || y >= g.nc[1] || z >= g.nc[2] || x0 > x1) continue;
-        const long long row = (z * g.nc[1] + y) * g.nc[0];
-        uint32_t s0 = 0xFFFFFFFFu, s1 = 0;
-        for (long long x = x0; x <= x1; ++x) {
-          const uint32_t st = v.cell_start[row + x];
-          if (st == 0xFFFFFFFFu) continue;
-          if (s0 == 0xFFFFFFFFu) s0 = st;
-          s1 = v.cell_end[row + x];
-        }
-        if (s0 == 0xFFFFFFFFu) continue;
-        for (uint32_t base = s0; base < s1; base += 32) {
-          const uint32_t w = base + lane;
-          const bool have = w < s1;
-          const float4 f1 = sf[have ? w : s0];
-          for (uint32_t i = 0; i < no; ++i) {
-            const float fx = __shfl_sync(0xffffffffu, fo.x, i), fy = __shfl_sync(0xffffffffu, fo.y, i);
-            const float fz = __shfl_sync(0xffffffffu, fo.z, i), fw = __shfl_sync(0xffffffffu, fo.w, i);
-            const float dx = fx - f1.x, dy = fy - f1.y, dz = fz - f1.z;
-            const float rr = fw + f1.w + marg + slack;
-            push(have && dx * dx + dy * dy + dz * dz < rr * rr * 1.0001f, o0 + i, w);
-          }
         }
       }
     }
