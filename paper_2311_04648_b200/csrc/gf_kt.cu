@@ -415,99 +415,90 @@ __device__ __forceinline__ void ss_resolve(const KtView &v, const Grid &g, const
   append_pair(hit, e, tmp, tmp_n, cap);
 }
 
-// Sphere-sphere pairs among small spheres: one warp per non-empty cell.
-// Lanes hold the cell's own spheres; candidates of the 13 forward neighbour
-// cells (half stencil) are streamed 32 at a time, one per lane, and every
-// (own, candidate) combination goes through a conservative fp32 distance
-// test.  Survivors are compacted with a ballot into a per-warp shared-memory
-// queue and the exact fp64 reference predicate runs on full 32-lane batches.
-// Pairs inside the cell are tested once (own i < own j).  Hits are counted
-// into the segment of the lower slot and appended to the scratch list
-// (placed into canonical segments by k_place / k_sort_seg).
+// Sphere-sphere pairs among small spheres, one thread per cell-sorted sphere,
+// half stencil: the later spheres of its own cell plus the 13 forward
+// neighbour cells, so every unordered pair is evaluated exactly once.
+// A cheap conservative fp32 distance test runs per lane; survivors are
+// compacted (ballot) into a per-warp shared-memory queue and the exact fp64
+// reference predicate runs on full 32-lane batches.  Hits are counted into the
+// segment of the lower slot and appended to the scratch list (placed into
+// canonical segments by k_place / k_sort_seg).
 __global__ void __launch_bounds__(128) k_pairs_ss(KtView v, const double4 *sc, const uint4 *sm,
-                                                  const float4 *sf, const uint32_t *cells,
-                                                  const unsigned long long *n_cells,
-                                                  unsigned long long *counts, uint2 *tmp,
+                                                  const float4 *sf, unsigned long long *counts, uint2 *tmp,
                                                   unsigned long long *tmp_n, unsigned long long cap) {
   __shared__ uint2 queue[4][64];
   const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
   uint2 *Q = queue[wq];
   int qn = 0;  // warp-uniform queue length
+  int64_t u64 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   const Grid g = *v.grid;
-  if (!g.valid) return;
+  bool active = u64 < v.sph.n && g.valid;
+  uint32_t key = active ? v.bin_key[u64] : kNoCell;
+  active = active && key != kNoCell;
+  float4 f0 = make_float4(0.f, 0.f, 0.f, 0.f);
+  long long cx = 0, cy = 0, cz = 0;
+  // conservative fp32 prefilter: coordinates are rounded relative to the grid
+  // origin, so |d_f32 - d| <= ~4 * 2^-24 * extent; the slack below is > 10x that
   const float ext = float(double(max(g.nc[0], max(g.nc[1], g.nc[2]))) / g.inv_cell);
-  const float slack = 1e-6f * ext + 1e-30f;  // > 10x the fp32 rounding of |d|
+  const float slack = 1e-6f * ext + 1e-30f;
   const float marg = float(v.margin);
-  const unsigned long long ncell = *n_cells;
-  const unsigned lt = (1u << lane) - 1u;
-
-  auto push = [&](bool pass, uint32_t ua, uint32_t ub) {
-    const unsigned m = __ballot_sync(0xffffffffu, pass);
-    if (pass) Q[qn + __popc(m & lt)] = make_uint2(ua, ub);
-    qn += __popc(m);
-    if (qn >= 32) {
-      __syncwarp();
-      const uint2 q = Q[lane];
-      __syncwarp();
-      if (lane < qn - 32) Q[lane] = Q[32 + lane];
-      qn -= 32;
-      __syncwarp();
-      ss_resolve(v, g, sc, sm, true, q, counts, tmp, tmp_n, cap);
-    }
-  };
-
-  for (unsigned long long ci = blockIdx.x * 4ull + wq; ci < ncell; ci += gridDim.x * 4ull) {
-    const uint32_t key = cells[ci];
-    const uint32_t c0 = v.cell_start[key], c1 = v.cell_end[key];
-    const long long cx = key % g.nc[0], cy = (key / g.nc[0]) % g.nc[1], cz = key / (g.nc[0] * g.nc[1]);
-    for (uint32_t o0 = c0; o0 < c1; o0 += 32) {  // own spheres, 32 per round
-      const uint32_t no = min(32u, c1 - o0);
-      const float4 fo = sf[o0 + (lane < int(no) ? lane : 0)];
-      // spans: 0 = the own cell (pairs own i < sphere j), then forward rows
-      // (dz, dy) = (0,0) x+1, (0,1), (1,-1), (1,0), (1,1)
-      for (int span = 0; span < 6; ++span) {
-        uint32_t s0, s1;
-        if (span == 0) {
-          s0 = o0;
-          s1 = c1;
-        } else {
-          const long long dz = span >= 3 ? 1 : 0;
-          const long long dy = span == 2 ? 1 : (span >= 3 ? span - 4 : 0);
-          long long x0 = span == 1 ? cx + 1 : cx - 1, x1 = cx + 1;
-          const long long y = cy + dy, z = cz + dz;
-          if (x0 < 0) x0 = 0;
-          if (x1 >= g.nc[0]) x1 = g.nc[0] - 1;
-          if (y < 0 || y >= g.nc[1] || z >= g.nc[2] || x0 > x1) continue;
-          const long long row = (z * g.nc[1] + y) * g.nc[0];
-          s0 = 0xFFFFFFFFu;
-          s1 = 0;
+  if (active) {
+    f0 = sf[u64];
+    cx = key % g.nc[0];
+    cy = (key / g.nc[0]) % g.nc[1];
+    cz = key / (g.nc[0] * g.nc[1]);
+  }
+  // spans: own cell after u, then rows (dz, dy) = (0,0) x+1 only, (0,1), (1,-1), (1,0), (1,1)
+  for (int span = 0; span < 6; ++span) {
+    uint32_t s0 = 0, s1 = 0;
+    if (active) {
+      if (span == 0) {
+        s0 = uint32_t(u64) + 1;
+        s1 = v.cell_end[key];
+      } else {
+        long long dz = span >= 3 ? 1 : 0;
+        long long dy = span == 2 ? 1 : (span >= 3 ? span - 4 : 0);
+        long long x0 = span == 1 ? cx + 1 : cx - 1, x1 = cx + 1;
+        long long y = cy + dy, z = cz + dz;
+        if (x0 < 0) x0 = 0;
+        if (x1 >= g.nc[0]) x1 = g.nc[0] - 1;
+        if (y >= 0 && y < g.nc[1] && z < g.nc[2] && x0 <= x1) {
+          long long row = (z * g.nc[1] + y) * g.nc[0];
+          uint32_t a0 = 0xFFFFFFFFu;
           for (long long x = x0; x <= x1; ++x) {
-            const uint32_t st = v.cell_start[row + x];
+            uint32_t st = v.cell_start[row + x];
             if (st == 0xFFFFFFFFu) continue;
-            if (s0 == 0xFFFFFFFFu) s0 = st;
+            if (a0 == 0xFFFFFFFFu) a0 = st;
             s1 = v.cell_end[row + x];
           }
-          if (s0 == 0xFFFFFFFFu) continue;
+          s0 = a0 == 0xFFFFFFFFu ? 0 : a0;
+          if (a0 == 0xFFFFFFFFu) s1 = 0;
         }
-        // every (own i, candidate j) combination, flattened across the lanes
-        const uint32_t ns = s1 - s0;
-        const uint32_t combos = no * ns;
-        for (uint32_t t = 0; t < combos; t += 32) {
-          const uint32_t cidx = t + lane;
-          const uint32_t i = cidx / ns, j = cidx - i * ns;
-          const int src = cidx < combos ? int(i) : 0;
-          const float fx = __shfl_sync(0xffffffffu, fo.x, src), fy = __shfl_sync(0xffffffffu, fo.y, src);
-          const float fz = __shfl_sync(0xffffffffu, fo.z, src), fw = __shfl_sync(0xffffffffu, fo.w, src);
-          const uint32_t w = s0 + j;
-          bool pass = cidx < combos && (span != 0 || w > o0 + i);
-          if (pass) {
-            const float4 f1 = sf[w];
-            const float dx = fx - f1.x, dy = fy - f1.y, dz = fz - f1.z;
-            const float rr = fw + f1.w + marg + slack;
-            pass = dx * dx + dy * dy + dz * dz < rr * rr * 1.0001f;
-          }
-          push(pass, o0 + i, w);
-        }
+      }
+    }
+    const uint32_t len = s1 > s0 ? s1 - s0 : 0;
+    uint32_t maxlen = len;
+    for (int off = 16; off > 0; off >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, off));
+    for (uint32_t t = 0; t < maxlen; ++t) {
+      bool pass = false;
+      const uint32_t w = s0 + t;
+      if (t < len) {
+        const float4 f1 = sf[w];
+        const float dx = f0.x - f1.x, dy = f0.y - f1.y, dz = f0.z - f1.z;
+        const float rr = f0.w + f1.w + marg + slack;
+        pass = dx * dx + dy * dy + dz * dz < rr * rr * 1.0001f;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, pass);
+      if (pass) Q[qn + __popc(m & ((1u << lane) - 1u))] = make_uint2(uint32_t(u64), w);
+      qn += __popc(m);
+      if (qn >= 32) {
+        __syncwarp();
+        const uint2 q = Q[lane];
+        __syncwarp();
+        if (lane < qn - 32) Q[lane] = Q[32 + lane];
+        qn -= 32;
+        __syncwarp();
+        ss_resolve(v, g, sc, sm, true, q, counts, tmp, tmp_n, cap);
       }
     }
   }
@@ -856,8 +847,7 @@ static int run_pair_kernels(Ctx *c, cudaStream_t s) {
   const unsigned long long cap = (unsigned long long)k.tmp_cap;
   uint2 *tmp = k.tmp.as<uint2>();
   if (n) {
-    k_pairs_ss<<<148 * 16, 128, 0, s>>>(v, k.sc.as<double4>(), k.sm.as<uint4>(), k.sf.as<float4>(),
-                                        k.cells.as<uint32_t>(), k.n_cells.as<unsigned long long>(), cnt, tmp, tn, cap);
+    k_pairs_ss<<<grid_for(n, 128), 128, 0, s>>>(v, k.sc.as<double4>(), k.sm.as<uint4>(), k.sf.as<float4>(), cnt, tmp, tn, cap);
     k_pairs_other<<<grid_for(n, 128), 128, 0, s>>>(v, cnt, tmp, tn, cap);
   }
   if (c->n_big)
