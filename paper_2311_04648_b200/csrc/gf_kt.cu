@@ -509,23 +509,6 @@ __global__ void __launch_bounds__(128) k_pairs_ss(KtView v, const double4 *sc, c
   }
 }
 
-// compact list of non-empty enumeration cells (order irrelevant)
-__global__ void k_cell_list(int64_t n, const uint32_t *key, uint32_t *cells, unsigned long long *n_cells) {
-  int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  bool first = false;
-  uint32_t k = kNoCell;
-  if (i < n) {
-    k = key[i];
-    first = k != kNoCell && (i == 0 || key[i - 1] != k);
-  }
-  const unsigned m = __ballot_sync(0xffffffffu, first);
-  const int lane = threadIdx.x & 31;
-  unsigned long long base = 0;
-  if (m && lane == 0) base = atomicAdd(n_cells, (unsigned long long)__popc(m));
-  base = __shfl_sync(0xffffffffu, base, 0);
-  if (first) cells[base + __popc(m & ((1u << lane) - 1u))] = k;
-}
-
 // Sphere-triangle and sphere-analytic pairs, one thread per sphere slot.
 __global__ void __launch_bounds__(128) k_pairs_other(KtView v, unsigned long long *counts, uint2 *tmp,
                                                      unsigned long long *tmp_n, unsigned long long cap) {
@@ -907,9 +890,7 @@ int kt_detect_count(Ctx *c, double margin, cudaStream_t s) {
     k_fill_u32<<<592, 256, 0, s>>>(gp, k.cell_start.as<uint32_t>(), 0xFFFFFFFFu, 0);
     k_cell_bounds<<<grid_for(n), kBlock, 0, s>>>(n, k.bin_key.as<uint32_t>(),
                                                 k.cell_start.as<uint32_t>(), k.cell_end.as<uint32_t>());
-    GF_CHECK(c, cudaMemsetAsync(k.n_cells.p, 0, sizeof(unsigned long long), s));
-    k_cell_list<<<grid_for(n), kBlock, 0, s>>>(n, k.bin_key.as<uint32_t>(), k.cells.as<uint32_t>(),
-                                              k.n_cells.as<unsigned long long>());
+
     k_gather_sorted<<<grid_for(n), kBlock, 0, s>>>(n, k.sph_val.as<uint32_t>(), k.centers.as<double>(),
                                                   c->sph_offr.as<float4>(), c->sph_owner.as<uint32_t>(),
                                                   k.sfam.as<uint8_t>(), gp, k.sc.as<double4>(), k.sm.as<uint4>(),
