@@ -23,6 +23,8 @@
  *   gf_dt_step                             _step_once force/reduce/integrate chain
  *                                          (engine.py:796-843; forces.py:553-591;
  *                                          _kernels.py:516-545, 641-670)
+ *   gf_set_force_model                     ForceModel registry + numba specialisation
+ *                                          (forces.py:360-440, engine.py:222-232)
  *   gf_run                                 the kT/dT worker protocol of do_dynamics
  *                                          (engine.py:512-526, 669-906)
  */
@@ -139,6 +141,21 @@ typedef struct {
  * returns the touching count and the watchdog owners (-1 = ok) */
 int gf_dt_step(gf_ctx *ctx, const gf_step_params *p, int64_t *touching, int64_t *bad,
                int64_t *oob);
+
+/* ---- user force models (NVRTC) ------------------------------------------- */
+/* Compile a user contact model from CUDA source (forces.py:82-87 contract):
+ *   __device__ void user_core(double overlap, double ts, double sim_time,
+ *       double b2ax, double b2ay, double b2az, double vx, double vy, double vz,
+ *       double wrx, double wry, double wrz, double mass_eff, double ra, double rb,
+ *       int mat_a, int mat_b, const double *pair, int n_mat, float *wild, double *out);
+ * pair(row, a, b) = pair[(row * n_mat + a) * n_mat + b]; rows E_cnt, G_cnt,
+ * then the model's pair properties.  W = wildcards per contact.  NULL source
+ * restores the built-in Hertz-Mindlin model.  include_dir = the directory of
+ * gf_device.cuh.  The compiler log is copied to log. */
+int gf_set_force_model(gf_ctx *ctx, const char *cuda_src, const char *include_dir, int W, char *log,
+                       size_t log_n);
+/* NVRTC compile of a user model without a device (validation only) */
+int gf_nvrtc_compile(const char *cuda_src, const char *include_dir, char *log, size_t log_n);
 
 /* ---- the whole worker protocol -------------------------------------------- */
 typedef struct {

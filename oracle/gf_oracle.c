@@ -685,7 +685,7 @@ int64_t orc_contact_forces(int64_t n, const uint8_t *kind, const int64_t *slot_a
                            const double *pair, int64_t n_mat, int64_t wstride,
                            float *wild, double ts, double sim_time,
                            double *out_ft, double *depth, double *cp,
-                           int nthreads) {
+                           int nthreads, int model) {
   int64_t touching = 0;
 #ifdef _OPENMP
   if (nthreads < 1) nthreads = 1;
@@ -717,10 +717,18 @@ int64_t orc_contact_forces(int64_t n, const uint8_t *kind, const int64_t *slot_a
     double vz = (va[2] + rotaz) - (vb[2] + rotbz);
     double ma = mass[oa], mb = mass[ob];
     double mass_eff = (ma * mb) / (ma + mb);
+    double *o6 = out_ft + 6 * k;
+    double ra_k = (double)sph_radii[slot_a[k]];
     orc_hertz_mindlin_core(dep, ts, sim_time, bx, by, bz, vx, vy, vz,
                            rotbx - rotax, rotby - rotay, rotbz - rotaz, mass_eff,
-                           (double)sph_radii[slot_a[k]], rb, mat_a[k], mat_b[k],
-                           pair, n_mat, wild + wstride * k, out_ft + 6 * k);
+                           ra_k, rb, mat_a[k], mat_b[k], pair, n_mat, wild + wstride * k, o6);
+    if (model == 1 && dep > 0.0) {
+      /* models.py hertz_mindlin_cohesive: F_c = coh * pi * R_eff * overlap along -B2A */
+      double coh = pair[(5 * n_mat + mat_a[k]) * n_mat + mat_b[k]];
+      double r_eff = ra_k * rb / (ra_k + rb);
+      double f = coh * 3.141592653589793 * r_eff * dep;
+      o6[0] -= f * bx; o6[1] -= f * by; o6[2] -= f * bz;
+    }
     if (dep > 0.0) touching += kind[k] == 0 ? 2 : 1;
   }
   return touching;

@@ -214,7 +214,7 @@ def merge_history(old_keys, old_wild, new_keys):
 def contact_forces(kind, slot_a, slot_b, owner_a, owner_b, mat_a, mat_b,
                    sph_centers, sph_radii, tri_world, ana_world, ana_kind,
                    owner_pos, lin_vel, ang_vel_global, mass, pair_stack, wild,
-                   ts, sim_time, nthreads=1):
+                   ts, sim_time, nthreads=1, model=0):
     """make_contact_kernel(hertz_mindlin_core_jit) (forces.py:547-593).
     wild (n, W) f32 is updated in place.  Returns (touching, out_ft, depth, cp)."""
     n = int(np.asarray(kind).shape[0])
@@ -233,7 +233,7 @@ def contact_forces(kind, slot_a, slot_b, owner_a, owner_b, mat_a, mat_b,
         _p(_c(lin_vel, np.float64)), _p(_c(ang_vel_global, np.float64)),
         _p(_c(mass, np.float64)), _p(pair_stack), _I64(pair_stack.shape[1]),
         _I64(wild.shape[1] if n else 4), _p(wild), _D(ts), _D(sim_time),
-        _p(out_ft), _p(depth), _p(cp), C.c_int(nthreads))
+        _p(out_ft), _p(depth), _p(cp), C.c_int(nthreads), C.c_int(model))
     return int(touching), out_ft, depth, cp
 
 
@@ -302,7 +302,7 @@ class OracleStepper:
     """
 
     def __init__(self, scene: dict, margin: float, period: int = 1, lag: int = 0,
-                 nthreads: int = 1):
+                 nthreads: int = 1, model: int = 0):
         s = {k: (np.array(v, copy=True) if isinstance(v, np.ndarray) else v)
              for k, v in scene.items()}
         self.s = s
@@ -310,6 +310,7 @@ class OracleStepper:
         self.period = int(period)
         self.lag = int(lag)
         self.nthreads = int(nthreads)
+        self.model = int(model)  # 0 Hertz-Mindlin, 1 models.py hertz_mindlin_cohesive
         kinds = s["geom_kind"]
         self.sph_geom = np.nonzero(kinds == GEOM_SPHERE)[0].astype(np.int64)
         self.tri_geom = np.nonzero(kinds == GEOM_TRIANGLE)[0].astype(np.int64)
@@ -385,7 +386,7 @@ class OracleStepper:
                 s["geom_material"][ga].astype(np.int64), s["geom_material"][gb].astype(np.int64),
                 self.centers, self.sph_radius, self.tri_world, self.ana_world,
                 self.ana_kind, self.pos, s["lin_vel"], wang, s["mass"],
-                s["pair_stack"], self.wild, s["h"], self.sim_time, self.nthreads)
+                s["pair_stack"], self.wild, s["h"], self.sim_time, self.nthreads, self.model)
         else:
             self.last_touching = 0
             out_ft = np.zeros((0, 6)); cp = np.zeros((0, 3))

@@ -16,6 +16,7 @@ import numpy as np
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG_DIR, "libgf_b200.so")
+CSRC_DIR = os.path.join(PKG_DIR, "csrc")  # gf_device.cuh for NVRTC user models
 
 GF_STATE_F32 = 1
 
@@ -55,7 +56,8 @@ EXPORTS = (
     "gf_download_accumulators", "gf_upload_geometry", "gf_upload_materials",
     "gf_upload_families", "gf_download_world", "gf_set_acs", "gf_acs_size", "gf_get_acs",
     "gf_detect", "gf_detect_snapshot", "gf_bin_ranges", "gf_adopt", "gf_dt_step", "gf_run",
-    "gf_merge_history", "gf_set_profiling", "gf_kernel_times",
+    "gf_merge_history", "gf_set_profiling", "gf_kernel_times", "gf_set_force_model",
+    "gf_nvrtc_compile",
 )
 
 _lib = None

@@ -8,8 +8,17 @@
 // on the device: restitution damping beta comes from a host table computed
 // with the same libm the reference uses (forces.py:41-44).
 #pragma once
+#ifdef __CUDACC_RTC__
+// NVRTC (user force models): no host headers; fixed-width types by hand
+typedef unsigned long long uint64_t;
+typedef long long int64_t;
+typedef unsigned int uint32_t;
+typedef unsigned short uint16_t;
+typedef unsigned char uint8_t;
+#else
 #include <cstdint>
 #include <cuda_runtime.h>
+#endif
 
 namespace gf {
 
@@ -90,6 +99,18 @@ struct Families {
   const uint8_t *av_mask;     // [256]
   const double *lv_val;       // [256*3]
   const double *av_val;       // [256*3]
+};
+
+// device status block (watchdog records, counters)
+struct Status {
+  unsigned long long bad;    // (step << 40) | owner of first speeding owner, or ~0
+  unsigned long long oob;    // same for out-of-domain
+  unsigned long long touching;
+  unsigned long long acs_total;   // last detection's pair count
+  unsigned long long touch_pairs;  // touching ACS entries summed over the run's steps
+  double oob_pos[3];
+  int err;                   // nonzero once a watchdog tripped (kernels stop)
+  int pad;
 };
 
 __host__ __device__ inline uint32_t meta_family(uint32_t m) { return m >> 24; }

@@ -236,6 +236,16 @@ using namespace gf;
 
 extern "C" {
 
+int gf_nvrtc_compile(const char *cuda_src, const char *include_dir, char *log, size_t log_n) {
+  std::string lg;
+  int rc = nvrtc_compile_check(cuda_src, include_dir, lg);
+  if (log && log_n) {
+    std::strncpy(log, lg.c_str(), log_n - 1);
+    log[log_n - 1] = 0;
+  }
+  return rc;
+}
+
 int gf_device_count(void) {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
@@ -570,8 +580,7 @@ int gf_set_acs(gf_ctx *ctx, int64_t n, const uint8_t *kind, const int64_t *slot_
                const float *wild, int W) {
   CTX_CHECK(ctx);
   GF_CHECK(c, cudaDeviceSynchronize());
-  if (W != 4) { c->err = "only 4 history wildcards are supported by this build"; return -1; }
-  c->wild_w = W;
+  if (W != c->wild_w) { c->err = "wildcard count differs from the active force model's"; return -1; }
   int64_t cap = n + n / 2 + 1024;
   if (ensure(c, c->acs.ids, 8 * cap, c->s_dt) || ensure(c, c->acs.wild, 4 * W * cap, c->s_dt)) return -1;
   c->acs.cap = cap;
@@ -679,6 +688,22 @@ static void pack_ids(int64_t n, const uint8_t *kind, const int64_t *a, const int
     ids[2 * k] = uint32_t(a[k]);
     ids[2 * k + 1] = uint32_t(b[k]) | (uint32_t(kind[k]) << kKindShift);
   }
+}
+
+int gf_set_force_model(gf_ctx *ctx, const char *cuda_src, const char *include_dir, int W, char *log,
+                       size_t log_n) {
+  CTX_CHECK(ctx);
+  GF_CHECK(c, cudaDeviceSynchronize());
+  if (W < 1 || W > 64) { c->err = "wildcard count must be in [1, 64]"; return -1; }
+  std::string lg;
+  int rc = set_user_model(c, cuda_src, include_dir ? include_dir : ".", lg);
+  if (log && log_n) {
+    std::strncpy(log, lg.c_str(), log_n - 1);
+    log[log_n - 1] = 0;
+  }
+  if (rc) return -1;
+  c->wild_w = cuda_src ? W : 4;
+  return 0;
 }
 
 int gf_set_profiling(gf_ctx *ctx, int on) {

@@ -122,6 +122,9 @@ struct Ctx {
   int64_t ca_updates = 0;
   double t_kt_ms = 0.0, t_dt_ms = 0.0;
   int64_t last_touching = 0;
+  // NVRTC user force model (gf_nvrtc.cu)
+  bool user_model = false;
+  void *user_fn_f64 = nullptr, *user_fn_f32 = nullptr;
   // per-kernel device timing (enabled by gf_set_profiling)
   bool prof = false;
   std::vector<cudaEvent_t> prof_ev;   // 4 per profiled step: start, contacts, heavy, integrate
@@ -132,18 +135,6 @@ struct Ctx {
 
 // take 4 timing events for one profiled dT step (nullptr when off)
 cudaEvent_t *prof_events(Ctx *c);
-
-// device status block
-struct Status {
-  unsigned long long bad;    // (step << 40) | owner of first speeding owner, or ~0
-  unsigned long long oob;    // same for out-of-domain
-  unsigned long long touching;
-  unsigned long long acs_total;   // last detection's pair count
-  unsigned long long touch_pairs;  // touching ACS entries summed over the run's steps
-  double oob_pos[3];
-  int err;                   // nonzero once a watchdog tripped (kernels stop)
-  int pad;
-};
 
 constexpr uint32_t kHeavyThreshold = 192;
 constexpr int64_t kMaxCells = (int64_t(1) << 24) - 1;  // enumeration-grid cell cap; key 2^24-1 = unregistered  // incidences above which an owner is block-reduced
@@ -180,6 +171,12 @@ int merge_host(Ctx *c, int64_t n_old, const uint32_t *old_ids, const float *old_
                const uint32_t *new_ids, int W, float *out_wild);
 int refresh_world(Ctx *c, cudaStream_t s);               // tri/ana world from owner pose
 int refresh_centers(Ctx *c, cudaStream_t s);             // sphere world centres from owner pose
+
+// NVRTC user force models (gf_nvrtc.cu)
+struct DtView;
+int set_user_model(Ctx *c, const char *src, const char *include_dir, std::string &log);
+int launch_user_forces(Ctx *c, const DtView &v, double ts, double sim_time, cudaStream_t s);
+int nvrtc_compile_check(const char *src, const char *include_dir, std::string &log);
 
 // dT (gf_dt_f64.cu / gf_dt_f32.cu)
 struct StepArgs {

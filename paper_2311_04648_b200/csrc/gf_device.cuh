@@ -1,0 +1,356 @@
+// gf_device.cuh -- device-only dT step code: owner/contact views, contact
+// geometry, pair kinematics and the force loop, templated on the contact
+// model ("core").  Compiled both ahead of time into libgf_b200.so and at run
+// time by NVRTC for user force models (the paper's JIT-compiled models,
+// PAPER.md:149-158; the reference's ForceModel plugin, forces.py:360-440), so
+// it must not include host headers.
+#pragma once
+#include "gf_common.cuh"
+
+namespace gf {
+
+template <typename VelT> struct Vel;
+template <> struct Vel<double> {
+  static __device__ __forceinline__ void load(const void *p, int64_t i, double v[3]) {
+    const double2 *q = reinterpret_cast<const double2 *>(p) + 2 * i;
+    double2 a = q[0], b = q[1];
+    v[0] = a.x; v[1] = a.y; v[2] = b.x;
+  }
+  static __device__ __forceinline__ void store(void *p, int64_t i, const double v[3]) {
+    double2 *q = reinterpret_cast<double2 *>(p) + 2 * i;
+    q[0] = make_double2(v[0], v[1]);
+    q[1] = make_double2(v[2], 0.0);
+  }
+};
+template <> struct Vel<float> {
+  static __device__ __forceinline__ void load(const void *p, int64_t i, double v[3]) {
+    float4 a = reinterpret_cast<const float4 *>(p)[i];
+    v[0] = a.x; v[1] = a.y; v[2] = a.z;
+  }
+  static __device__ __forceinline__ void store(void *p, int64_t i, const double v[3]) {
+    reinterpret_cast<float4 *>(p)[i] = make_float4(float(v[0]), float(v[1]), float(v[2]), 0.f);
+  }
+};
+
+struct DtView {
+  Domain dom;
+  Owners own;
+  Spheres sph;
+  Tris tri;
+  Anas ana;
+  Materials mat;
+  Families fam;
+  int64_t n_acs;
+  const uint2 *ids;
+  float *wild;
+  int W;
+  double *out_c;        // [n_acs*9]
+  uint8_t *touch;       // [n_acs]
+  const uint32_t *inc;  // B-side incidences: contact indices sorted by (B owner, k)
+  const uint32_t *inc_start;  // per owner start in inc
+  const unsigned long long *seg;  // (kind, sphere A) segment starts of the active array
+  int64_t n_sph;
+  const uint32_t *heavy;
+  const unsigned long long *n_heavy;
+  double *heavy_acc;    // [n_owner*6] (only heavy owners written)
+  Status *st;
+};
+
+template <typename VelT>
+__device__ __forceinline__ void owner_kin(const DtView &v, uint32_t o, double pos[3], double vel[3],
+                                          double wg[3], double &mass) {
+  decode_pos(v.dom, v.own.voxel[o], v.own.sub[o], pos[0], pos[1], pos[2]);
+  Vel<VelT>::load(v.own.lin_vel, o, vel);
+  double wl[3];
+  Vel<VelT>::load(v.own.ang_vel, o, wl);
+  float4 q = v.own.quat[o];
+  qrot(double(q.x), double(q.y), double(q.z), double(q.w), wl[0], wl[1], wl[2], wg[0], wg[1], wg[2]);
+  mass = v.own.tpl[meta_tpl(v.own.meta[o])].x;
+}
+
+// contact geometry of ACS entry `id` (_kernels.py:442-491): depth, B-to-A
+// unit vector, B-side curvature radius; A's centre and radius returned too
+__device__ __forceinline__ void contact_geometry(const DtView &v, uint2 id, double ca[3], double &ra,
+                                                 double &depth, double &bx, double &by, double &bz,
+                                                 double &rb) {
+  const uint32_t kind = id.y >> kKindShift, sb = id.y & kSlotMask;
+  const double4 cA = v.sph.center[id.x];
+  ca[0] = cA.x; ca[1] = cA.y; ca[2] = cA.z;
+  ra = cA.w;
+  if (kind == 0) {
+    const double4 cB = v.sph.center[sb];
+    double dx = ca[0] - cB.x, dy = ca[1] - cB.y, dz = ca[2] - cB.z;
+    double d = sqrt(dx * dx + dy * dy + dz * dz);
+    rb = cB.w;
+    if (d < 1e-300) {
+      depth = ra + rb; bx = 0.0; by = 0.0; bz = 1.0;
+    } else {
+      double inv = 1.0 / d;
+      bx = dx * inv; by = dy * inv; bz = dz * inv;
+      depth = ra + rb - d;
+    }
+  } else if (kind == 1) {
+    const double *T = v.tri.world + 9 * size_t(sb);
+    double qx, qy, qz;
+    closest_on_tri(ca[0], ca[1], ca[2], T, qx, qy, qz);
+    double dx = ca[0] - qx, dy = ca[1] - qy, dz = ca[2] - qz;
+    double d = sqrt(dx * dx + dy * dy + dz * dz);
+    if (d < 1e-300) {
+      double e1x = T[3] - T[0], e1y = T[4] - T[1], e1z = T[5] - T[2];
+      double e2x = T[6] - T[0], e2y = T[7] - T[1], e2z = T[8] - T[2];
+      double nx = e1y * e2z - e1z * e2y, ny = e1z * e2x - e1x * e2z, nz = e1x * e2y - e1y * e2x;
+      double nn = sqrt(nx * nx + ny * ny + nz * nz);
+      bx = nx / nn; by = ny / nn; bz = nz / nn;
+    } else {
+      double inv = 1.0 / d;
+      bx = dx * inv; by = dy * inv; bz = dz * inv;
+    }
+    depth = ra - d;
+    rb = kFlatRadius;
+  } else {
+    double gap;
+    analytic_gap(v.ana.kind[sb], v.ana.world + 8 * size_t(sb), ca[0], ca[1], ca[2], gap, bx, by, bz, rb);
+    depth = ra - gap;
+  }
+}
+
+// Hertz-Mindlin core (forces.py:82-182) for a touching contact; material
+// pair values passed in (beta = restitution damping, forces.py:41-44)
+__device__ __forceinline__ void hertz_mindlin_core(double overlap, double ts, double b2ax, double b2ay,
+                                                   double b2az, double vx, double vy, double vz,
+                                                   double wrx, double wry, double wrz, double mass_eff,
+                                                   double ra, double rb, double e_cnt, double g_cnt,
+                                                   double mu, double crr, double beta, float *wild,
+                                                   double out[6]) {
+  for (int q = 0; q < 6; ++q) out[q] = 0.0;
+  double projection = vx * b2ax + vy * b2ay + vz * b2az;
+  double vtx = vx - projection * b2ax;
+  double vty = vy - projection * b2ay;
+  double vtz = vz - projection * b2az;
+  double dtx = double(wild[0]) + ts * vtx;
+  double dty = double(wild[1]) + ts * vty;
+  double dtz = double(wild[2]) + ts * vtz;
+  double disp_proj = dtx * b2ax + dty * b2ay + dtz * b2az;
+  dtx -= disp_proj * b2ax;
+  dty -= disp_proj * b2ay;
+  dtz -= disp_proj * b2az;
+  double delta_time = double(wild[3]) + ts;
+
+  double sqrt_rd = sqrt(overlap * (ra * rb) / (ra + rb));
+  double sn = 2.0 * e_cnt * sqrt_rd;
+  double k_n = 2.0 / 3.0 * sn;
+  double gamma_n = 2.0 * sqrt(5.0 / 6.0) * beta * sqrt(sn * mass_eff);
+  double fn = k_n * overlap + gamma_n * projection;
+  out[0] = fn * b2ax;
+  out[1] = fn * b2ay;
+  out[2] = fn * b2az;
+
+  if (crr > 0.0) {
+    bool add_rolling = true;
+    double r_eff = sqrt((ra * rb) / (ra + rb));
+    double kn_simple = 4.0 / 3.0 * e_cnt * sqrt(r_eff);
+    double gn_simple = -2.0 * sqrt(5.0 / 3.0 * mass_eff * e_cnt) * beta * pow(r_eff, 0.25);
+    double d_coeff = gn_simple / (2.0 * sqrt(kn_simple * mass_eff));
+    if (d_coeff < 1.0) {
+      double t_collision = kPi * sqrt(mass_eff / (kn_simple * (1.0 - d_coeff * d_coeff)));
+      if (delta_time <= t_collision) add_rolling = false;
+    }
+    if (add_rolling) {
+      double v_rot_mag = sqrt(wrx * wrx + wry * wry + wrz * wrz);
+      if (v_rot_mag > 1e-12) {
+        double fmag = sqrt(out[0] * out[0] + out[1] * out[1] + out[2] * out[2]);
+        double scale = crr * fmag / v_rot_mag;
+        out[3] = wrx * scale;
+        out[4] = wry * scale;
+        out[5] = wrz * scale;
+      }
+    }
+  }
+  if (mu > 0.0) {
+    double kt = 8.0 * g_cnt * sqrt_rd;
+    double gt = -2.0 * sqrt(5.0 / 6.0) * beta * sqrt(mass_eff * kt);
+    double tfx = -kt * dtx - gt * vtx;
+    double tfy = -kt * dty - gt * vty;
+    double tfz = -kt * dtz - gt * vtz;
+    double ft = sqrt(tfx * tfx + tfy * tfy + tfz * tfz);
+    if (ft > 1e-12) {
+      double fmag = sqrt(out[0] * out[0] + out[1] * out[1] + out[2] * out[2]);
+      double ft_max = fmag * mu;
+      if (ft > ft_max) {
+        double scale = ft_max / ft;
+        tfx *= scale; tfy *= scale; tfz *= scale;
+        dtx = (tfx + gt * vtx) / (-kt);
+        dty = (tfy + gt * vty) / (-kt);
+        dtz = (tfz + gt * vtz) / (-kt);
+      }
+    } else {
+      tfx = 0.0; tfy = 0.0; tfz = 0.0;
+    }
+    out[0] += tfx;
+    out[1] += tfy;
+    out[2] += tfz;
+  }
+  wild[0] = float(dtx);
+  wild[1] = float(dty);
+  wild[2] = float(dtz);
+  wild[3] = float(delta_time);
+}
+
+// built-in model: pair values and beta from the uploaded tables
+__device__ __forceinline__ void hertz_mindlin(double overlap, double ts, double b2ax, double b2ay,
+                                              double b2az, double vx, double vy, double vz,
+                                              double wrx, double wry, double wrz, double mass_eff,
+                                              double ra, double rb, int ma, int mb,
+                                              const Materials &M, float *wild, double out[6]) {
+  const int mm = M.n_mat * M.n_mat, ab = ma * M.n_mat + mb;
+  hertz_mindlin_core(overlap, ts, b2ax, b2ay, b2az, vx, vy, vz, wrx, wry, wrz, mass_eff, ra, rb,
+                     M.pair[ab], M.pair[mm + ab], M.pair[3 * mm + ab], M.pair[4 * mm + ab], M.beta[ab],
+                     wild, out);
+}
+
+// For user models (NVRTC): the default Hertz-Mindlin law with the reference
+// core's argument list, beta computed on the device from the CoR row.  Acts
+// only for overlap > 0 and leaves history untouched otherwise (forces.py:95-97).
+__device__ __forceinline__ void hm_default_core(double overlap, double ts, double sim_time, double b2ax,
+                                                double b2ay, double b2az, double vx, double vy, double vz,
+                                                double wrx, double wry, double wrz, double mass_eff,
+                                                double ra, double rb, int mat_a, int mat_b,
+                                                const double *pair, int n_mat, float *wild, double *out) {
+  (void)sim_time;
+  if (overlap <= 0.0) return;
+  const int mm = n_mat * n_mat, ab = mat_a * n_mat + mat_b;
+  const double cor = pair[2 * mm + ab];
+  const double loge = cor < 1e-12 ? log(1e-12) : log(cor);
+  const double beta = loge / sqrt(loge * loge + kPi * kPi);
+  hertz_mindlin_core(overlap, ts, b2ax, b2ay, b2az, vx, vy, vz, wrx, wry, wrz, mass_eff, ra, rb, pair[ab],
+                     pair[mm + ab], pair[3 * mm + ab], pair[4 * mm + ab], beta, wild, out);
+}
+
+
+// The core contract of the reference (forces.py:82-87): per contact,
+// overlap (may be <= 0 for a margin false positive), step size, time, B-to-A
+// normal, relative velocity at the contact point, rolling direction,
+// effective mass, radii (B = 1e18 for flat, negative for concave), material
+// ids, the material pair stack (rows E_cnt, G_cnt, then the model's pair
+// properties; pair(row, a, b) = pair[(row * n_mat + a) * n_mat + b]), the
+// contact's wildcard (history) row and out[6] = force on A, torque-only
+// force.  out arrives zeroed.
+struct CoreArgs {
+  double overlap, ts, sim_time;
+  double b2ax, b2ay, b2az, vx, vy, vz, wrx, wry, wrz;
+  double mass_eff, ra, rb;
+  int mat_a, mat_b;
+  const double *pair;
+  int n_mat;
+  float *wild;
+  const Materials *M;
+};
+
+// built-in model: history-based Hertz-Mindlin (skips false positives)
+struct HmCore {
+  static constexpr bool kAllEntries = false;
+  __device__ static __forceinline__ void eval(const CoreArgs &a, double out[6]) {
+    if (a.overlap <= 0.0) return;
+    hertz_mindlin(a.overlap, a.ts, a.b2ax, a.b2ay, a.b2az, a.vx, a.vy, a.vz, a.wrx, a.wry, a.wrz, a.mass_eff,
+                  a.ra, a.rb, a.mat_a, a.mat_b, *a.M, a.wild, out);
+  }
+};
+
+// Force of one ACS entry with core `Core`; returns false when it produced no
+// force (nothing to reduce).  Parity build: writes the per-contact output and
+// touch flag; throughput build: fixed-point owner accumulation.
+template <typename VelT, typename Core>
+__device__ __forceinline__ void force_entry(const DtView &v, uint32_t k, double ts, double sim_time) {
+  const uint2 id = v.ids[k];
+  const uint32_t kind = id.y >> kKindShift, sb = id.y & kSlotMask;
+  double ca[3], ra, depth, bx, by, bz, rb;
+  contact_geometry(v, id, ca, ra, depth, bx, by, bz, rb);
+  if (!Core::kAllEntries && depth <= 0.0) return;
+  const uint32_t oa = v.sph.owner[id.x];
+  uint32_t ob;
+  int mb;
+  if (kind == 0) { ob = v.sph.owner[sb]; mb = v.sph.mat[sb]; }
+  else if (kind == 1) { ob = v.tri.owner[sb]; mb = v.tri.mat[sb]; }
+  else { ob = v.ana.owner[sb]; mb = v.ana.mat[sb]; }
+  double half = ra - 0.5 * depth;
+  double px = ca[0] - bx * half, py = ca[1] - by * half, pz = ca[2] - bz * half;
+  double pa[3], va[3], wa[3], ma, pb[3], vb[3], wb[3], mbass;
+  owner_kin<VelT>(v, oa, pa, va, wa, ma);
+  owner_kin<VelT>(v, ob, pb, vb, wb, mbass);
+  double rax = px - pa[0], ray = py - pa[1], raz = pz - pa[2];
+  double rbx = px - pb[0], rby = py - pb[1], rbz = pz - pb[2];
+  double rotax = wa[1] * raz - wa[2] * ray;
+  double rotay = wa[2] * rax - wa[0] * raz;
+  double rotaz = wa[0] * ray - wa[1] * rax;
+  double rotbx = wb[1] * rbz - wb[2] * rby;
+  double rotby = wb[2] * rbx - wb[0] * rbz;
+  double rotbz = wb[0] * rby - wb[1] * rbx;
+  CoreArgs arg;
+  arg.overlap = depth; arg.ts = ts; arg.sim_time = sim_time;
+  arg.b2ax = bx; arg.b2ay = by; arg.b2az = bz;
+  arg.vx = (va[0] + rotax) - (vb[0] + rotbx);
+  arg.vy = (va[1] + rotay) - (vb[1] + rotby);
+  arg.vz = (va[2] + rotaz) - (vb[2] + rotbz);
+  arg.wrx = rotbx - rotax; arg.wry = rotby - rotay; arg.wrz = rotbz - rotaz;
+  arg.mass_eff = (ma * mbass) / (ma + mbass);
+  arg.ra = ra; arg.rb = rb;
+  arg.mat_a = v.sph.mat[id.x]; arg.mat_b = mb;
+  arg.pair = v.mat.pair; arg.n_mat = v.mat.n_mat;
+  arg.wild = v.wild + size_t(v.W) * k;
+  arg.M = &v.mat;
+  double out[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  Core::eval(arg, out);
+  if (Core::kAllEntries && out[0] == 0.0 && out[1] == 0.0 && out[2] == 0.0 && out[3] == 0.0 &&
+      out[4] == 0.0 && out[5] == 0.0) {
+    if (!v.own.facc) v.touch[k] = 0;
+    return;
+  }
+  const double tx = out[0] + out[3], ty = out[1] + out[4], tz = out[2] + out[5];
+  if (v.own.facc) {
+    // throughput build: +F / r_a x T on A, -F / -(r_b x T) on B, as int64
+    // fixed point (order-independent sums: bitwise reproducible runs)
+    const double2 sa = v.own.tpl_scale[meta_tpl(v.own.meta[oa])];
+    const double2 sbs = v.own.tpl_scale[meta_tpl(v.own.meta[ob])];
+    unsigned long long *fa = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(oa));
+    unsigned long long *fb = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(ob));
+    const double ta[3] = {ray * tz - raz * ty, raz * tx - rax * tz, rax * ty - ray * tx};
+    const double tb[3] = {rby * tz - rbz * ty, rbz * tx - rbx * tz, rbx * ty - rby * tx};
+    for (int q = 0; q < 3; ++q) {
+      if (sa.x > 0.0) {
+        atomicAdd(fa + q, (unsigned long long)__double2ll_rn(out[q] * sa.x));
+        atomicAdd(fa + 3 + q, (unsigned long long)__double2ll_rn(ta[q] * sa.y));
+      } else {
+        atomicAdd(reinterpret_cast<double *>(fa + q), out[q]);
+        atomicAdd(reinterpret_cast<double *>(fa + 3 + q), ta[q]);
+      }
+      if (sbs.x > 0.0) {
+        atomicAdd(fb + q, (unsigned long long)__double2ll_rn(-out[q] * sbs.x));
+        atomicAdd(fb + 3 + q, (unsigned long long)__double2ll_rn(-tb[q] * sbs.y));
+      } else {
+        atomicAdd(reinterpret_cast<double *>(fb + q), -out[q]);
+        atomicAdd(reinterpret_cast<double *>(fb + 3 + q), -tb[q]);
+      }
+    }
+  } else {
+    double *oc = v.out_c + 9 * size_t(k);
+    oc[0] = out[0]; oc[1] = out[1]; oc[2] = out[2];
+    oc[3] = tx; oc[4] = ty; oc[5] = tz;
+    oc[6] = px; oc[7] = py; oc[8] = pz;
+    v.touch[k] = 1;
+  }
+}
+
+// The force loop: entries listed in `list` (touching entries of the built-in
+// model) or, for cores that act on every entry (user models may act at
+// negative overlap), all entries.
+template <typename VelT, typename Core>
+__device__ __forceinline__ void forces_loop(const DtView &v, double ts, double sim_time, const uint32_t *list,
+                                            const unsigned long long *list_n) {
+  if (v.st->err) return;
+  const unsigned long long n = Core::kAllEntries ? (unsigned long long)v.n_acs : *list_n;
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x)
+    force_entry<VelT, Core>(v, Core::kAllEntries ? uint32_t(i) : list[i], ts, sim_time);
+}
+
+}  // namespace gf

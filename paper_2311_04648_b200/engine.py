@@ -385,6 +385,10 @@ class Simulator:
         dom = s.domain
         ctx.call("gf_set_domain", P(_lib.carr(dom.lo, np.float64)), P(_lib.carr(dom.hi, np.float64)),
                  C.c_double(dom.voxel_edge))
+        if self.model.cuda_src is not None:  # NVRTC user model (the paper's JIT)
+            log = C.create_string_buffer(1 << 16)
+            ctx.call("gf_set_force_model", self.model.cuda_src.encode(), _lib.CSRC_DIR.encode(),
+                     C.c_int(len(self.model.wildcards)), log, C.c_size_t(1 << 16))
         self._upload_tables()
         self._upload_owners()
         gp = s.geom_params[:n_g]
@@ -612,17 +616,17 @@ class Simulator:
             ca.wildcards[name] = wild[:, i].copy()
         return ca.canonicalize() if self.reorder else ca
 
-    @staticmethod
-    def _orient(kind, sa, sb, wild):
+    def _orient(self, kind, sa, sb, wild):
         """Sphere-sphere pairs are stored as (lower slot, higher slot); when a
-        slot permutation flips a pair, A and B swap roles and the tangential
-        history (displacement of A relative to B, forces.py:111-118) changes
-        sign.  delta_time is orientation-free."""
+        slot permutation flips a pair, A and B swap roles and the model's
+        orientation-dependent history (e.g. the tangential displacement of A
+        relative to B, forces.py:111-118) changes sign."""
         flip = (kind == 0) & (sa > sb)
         if flip.any():
             sa, sb = np.where(flip, sb, sa), np.where(flip, sa, sb)
             wild = wild.copy()
-            wild[flip, :3] = -wild[flip, :3]
+            for col in self.model.flip_on_swap:
+                wild[flip, col] = -wild[flip, col]
         return sa, sb, wild
 
     @_acs.setter

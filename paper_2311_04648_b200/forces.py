@@ -38,13 +38,24 @@ def restitution_damping(cor: float) -> float:
 
 @dataclass(frozen=True)
 class ForceModel:
-    """A contact force model.
+    """A contact force model (forces.py:360-405).
 
     ``wildcards`` are the ordered per-contact history names; ``pair_props``
-    the material properties stacked after E_cnt / G_cnt.  ``device_kernel``
-    names the compiled device implementation.  ``core`` / ``jit_core`` keep
-    the reference's field names for source compatibility; the device path
-    does not call them.
+    the material properties stacked after E_cnt / G_cnt.
+
+    ``cuda_src`` is the device implementation of a user model: CUDA source
+    defining ``__device__ void user_core(...)`` with the reference core's
+    argument list (forces.py:82-87; see include/gf_b200.h,
+    gf_set_force_model).  It is compiled for sm_100a with NVRTC when a
+    Simulator using the model initialises -- the paper's JIT-compiled force
+    models.  ``gf::hm_default_core`` (same arguments) is available to build
+    on the default law.  Without ``cuda_src`` the model is the built-in
+    compiled Hertz-Mindlin kernel.
+
+    ``flip_on_swap`` lists the wildcards that change sign when a contact's A
+    and B sides swap (tangential displacement for Hertz-Mindlin).
+    ``core`` / ``jit_core`` keep the reference's field names for source
+    compatibility; the device path does not call them.
     """
 
     name: str
@@ -53,6 +64,8 @@ class ForceModel:
     device_kernel: str = "hertz_mindlin"
     core: Optional[Callable] = None
     jit_core: Optional[Callable] = None
+    cuda_src: Optional[str] = None
+    flip_on_swap: tuple = ()
 
 
 _REGISTRY: dict = {}
@@ -61,7 +74,7 @@ _REGISTRY: dict = {}
 def register_force_model(model: ForceModel) -> ForceModel:
     if model.name in _REGISTRY:
         raise ConfigurationError(f"force model {model.name!r} already registered")
-    if model.device_kernel != "hertz_mindlin":
+    if model.cuda_src is None and model.device_kernel != "hertz_mindlin":
         raise ConfigurationError(
             f"force model {model.name!r}: no compiled device kernel {model.device_kernel!r}")
     _REGISTRY[model.name] = model
@@ -79,7 +92,24 @@ DEFAULT_MODEL = register_force_model(ForceModel(
     name="hertz_mindlin",
     wildcards=("delta_tan_x", "delta_tan_y", "delta_tan_z", "delta_time"),
     pair_props=("CoR", "mu", "Crr"),
+    flip_on_swap=(0, 1, 2),
 ))
+
+
+def compile_check(model: ForceModel) -> str:
+    """NVRTC-compile a user model's source without a device; returns the
+    compiler log, raises ConfigurationError on failure."""
+    import ctypes as C
+    from . import _lib
+    if model.cuda_src is None:
+        return ""
+    L = _lib.load_library()
+    log = C.create_string_buffer(1 << 16)
+    rc = L.gf_nvrtc_compile(model.cuda_src.encode(), _lib.CSRC_DIR.encode(), log, C.c_size_t(1 << 16))
+    text = log.value.decode(errors="replace")
+    if rc != 0:
+        raise ConfigurationError(f"force model {model.name!r} does not compile:\n{text}")
+    return text
 
 
 def material_pair_stack(materials: MaterialTable, model: ForceModel) -> np.ndarray:

@@ -253,3 +253,122 @@ def test_detect_polydisperse_with_big_spheres_vs_oracle():
         assert np.array_equal(got.kind, want["kind"]), seed
         assert np.array_equal(got.geom_a, want["geom_a"]), seed
         assert np.array_equal(got.geom_b, want["geom_b"]), seed
+
+
+# ---------------------------------------------------------------------------
+# NVRTC user force models (forces.py:360-440 plugin contract)
+# ---------------------------------------------------------------------------
+
+def _with_coh(scene, coh=2.0e3):
+    s = dict(scene)
+    ps = s["pair_stack"]
+    s["pair_stack"] = np.concatenate([ps, np.full((1,) + ps.shape[1:], coh)], axis=0)
+    return s
+
+
+def _set_model(ctx, src, W=4):
+    import ctypes as C
+    from paper_2311_04648_b200 import _lib
+    log = C.create_string_buffer(1 << 16)
+    ctx.call("gf_set_force_model", src.encode(), _lib.CSRC_DIR.encode(), C.c_int(W), log,
+             C.c_size_t(1 << 16))
+
+
+HM_AS_USER = r"""
+__device__ void user_core(double overlap, double ts, double sim_time, double b2ax, double b2ay,
+                          double b2az, double vx, double vy, double vz, double wrx, double wry,
+                          double wrz, double mass_eff, double ra, double rb, int mat_a, int mat_b,
+                          const double *pair, int n_mat, float *wild, double *out) {
+  gf::hm_default_core(overlap, ts, sim_time, b2ax, b2ay, b2az, vx, vy, vz, wrx, wry, wrz, mass_eff,
+                      ra, rb, mat_a, mat_b, pair, n_mat, wild, out);
+}
+"""
+
+
+@pytest.mark.parametrize("name", ["dyn_box", "dyn_clumps"])
+def test_user_model_equal_to_builtin(name):
+    """A user model that is the default law, compiled by NVRTC, reproduces the
+    built-in kernel (beta from the device log instead of the host table)."""
+    g = load(name)
+    scene = scene_of(g)
+    outs = []
+    for user in (False, True):
+        ctx = S.upload_scene(scene)
+        if user:
+            _set_model(ctx, HM_AS_USER)
+        S.set_acs(ctx, g["acs_kind"], g["acs_slot_a"], g["acs_slot_b"], g["wild_in"])
+        touching, bad, oob = S.dt_step(ctx, scene, float(g["sim_time"]))
+        st = S.download_state(ctx, g["voxel"].shape[0])
+        outs.append((touching, st, S.get_acs(ctx)[3]))
+        ctx.close()
+    assert outs[0][0] == outs[1][0]
+    for key in ("acc_f", "acc_t", "lin_vel", "ang_vel"):
+        np.testing.assert_allclose(outs[1][1][key], outs[0][1][key], rtol=1e-12, atol=1e-18)
+    np.testing.assert_allclose(outs[1][2], outs[0][2], rtol=1e-6, atol=1e-12)
+
+
+@pytest.mark.parametrize("f32", [False, True])
+def test_cohesive_user_model_vs_oracle(f32):
+    """configs[3]'s cohesive contact model: NVRTC-compiled CUDA source vs the
+    oracle twin (oracle/gf_oracle.c model 1) on the same state."""
+    from paper_2311_04648_b200 import models
+    g = load("dyn_box")
+    scene = _with_coh(scene_of(g))
+    if f32:
+        scene["lin_vel"] = scene["lin_vel"].astype(np.float32).astype(np.float64)
+        scene["ang_vel"] = scene["ang_vel"].astype(np.float32).astype(np.float64)
+    ctx = S.upload_scene(scene, f32_state=f32)
+    _set_model(ctx, models.COHESIVE_SRC)
+    S.set_acs(ctx, g["acs_kind"], g["acs_slot_a"], g["acs_slot_b"], g["wild_in"])
+    touching, bad, oob = S.dt_step(ctx, scene, float(g["sim_time"]))
+    st = S.download_state(ctx, g["voxel"].shape[0])
+    ctx.close()
+    wang = O.angular_velocity_global(scene["quat"], scene["ang_vel"])
+    wild = g["wild_in"].copy()
+    tch, out_ft, depth, cp = O.contact_forces(
+        g["acs_kind"], g["acs_slot_a"], g["acs_slot_b"], g["acs_owner_a"], g["acs_owner_b"],
+        g["acs_mat_a"], g["acs_mat_b"], g["sph_centers"], g["sph_radius"], g["tri_world"],
+        g["ana_world"], g["ana_kind"], g["owner_pos"], scene["lin_vel"], wang, scene["mass"],
+        scene["pair_stack"], wild, float(scene["h"]), float(g["sim_time"]), model=1)
+    acc_f, acc_t = O.reduce_to_owners(g["acs_owner_a"], g["acs_owner_b"], out_ft, cp, g["owner_pos"])
+    assert touching == tch
+    fscale = np.median(np.linalg.norm(out_ft[depth > 0, :3], axis=1))
+    tol = 1e-5 if f32 else 1e-10
+    assert np.max(np.abs(st["acc_f"] - acc_f)) <= tol * fscale
+    # the cohesive pull is really there: compare with plain Hertz-Mindlin
+    wild2 = g["wild_in"].copy()
+    _, out_hm, _, _ = O.contact_forces(
+        g["acs_kind"], g["acs_slot_a"], g["acs_slot_b"], g["acs_owner_a"], g["acs_owner_b"],
+        g["acs_mat_a"], g["acs_mat_b"], g["sph_centers"], g["sph_radius"], g["tri_world"],
+        g["ana_world"], g["ana_kind"], g["owner_pos"], scene["lin_vel"], wang, scene["mass"],
+        scene["pair_stack"], wild2, float(scene["h"]), float(g["sim_time"]), model=0)
+    assert np.max(np.abs(out_ft[:, :3] - out_hm[:, :3])) > 1e3 * tol * fscale
+
+
+def test_cohesive_model_through_simulator():
+    """Simulator(force_model=...) compiles the user model at initialize and
+    runs a sync-mode trajectory that matches the oracle driver."""
+    import paper_2311_04648_b200 as gf
+    from paper_2311_04648_b200 import models, scenes
+    models.cohesive_model()
+    sim = gf.Simulator(gf.Domain.cube(1.0), force_model="hertz_mindlin_cohesive")
+    mat = sim.load_material({"E": 1e7, "nu": 0.3, "CoR": 0.5, "mu": 0.3, "Crr": 0.0, "coh": 5e3})
+    tpl = sim.load_clump_template(gf.ClumpTemplate.solid_sphere(0.01, 0.0109, mat))
+    sim.add_clumps(tpl, gf.hcp_sample_box((0, 0, 0.06), (0.05, 0.05, 0.05), 0.0199))
+    sim.add_analytic([("plane", (0, 0, 0), (0, 0, 1), mat)], family=255)
+    sim.set_family_fixed(255)
+    sim.set_gravity([0, 0, -9.81])
+    sim.set_init_time_step(2e-5)
+    sim.set_error_out_velocity(5.0)
+    sim.set_sync_mode(True)
+    scene = scenes.oracle_scene(sim)
+    sim.initialize()
+    with sim:
+        sim.do_dynamics(100 * sim.h)
+        pos = sim._pos.copy()
+        v = sim.store.lin_vel[: sim.store.n_owners].copy()
+    st = O.OracleStepper(scene, sim._current_margin(), period=1, lag=0, model=1)
+    for _ in range(100):
+        st.step_once()
+    np.testing.assert_allclose(pos, st.pos, atol=1e-12)
+    np.testing.assert_allclose(v, st.s["lin_vel"], rtol=1e-8, atol=1e-12)
