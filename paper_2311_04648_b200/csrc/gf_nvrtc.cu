@@ -67,9 +67,10 @@ int set_user_model(Ctx *c, const char *src, const char *include_dir, std::string
       return -1;
     }
     std::string inc = std::string("--include-path=") + include_dir;
+    // --fmad=false: user cores round like the reference's numba cores (fastmath=False)
     const char *opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "--device-as-default-execution-space",
-                          inc.c_str(), "-lineinfo"};
-    nvrtcResult rc = nvrtcCompileProgram(prog, 5, opts);
+                          inc.c_str(), "-lineinfo", "--fmad=false"};
+    nvrtcResult rc = nvrtcCompileProgram(prog, 6, opts);
     size_t ln = 0;
     nvrtcGetProgramLogSize(prog, &ln);
     std::string plog(ln, '\0');

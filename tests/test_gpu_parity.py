@@ -303,7 +303,8 @@ def test_user_model_equal_to_builtin(name):
         ctx.close()
     assert outs[0][0] == outs[1][0]
     for key in ("acc_f", "acc_t", "lin_vel", "ang_vel"):
-        np.testing.assert_allclose(outs[1][1][key], outs[0][1][key], rtol=1e-12, atol=1e-18)
+        ref = outs[0][1][key]
+        np.testing.assert_allclose(outs[1][1][key], ref, rtol=1e-12, atol=1e-12 * np.max(np.abs(ref)))
     np.testing.assert_allclose(outs[1][2], outs[0][2], rtol=1e-6, atol=1e-12)
 
 
