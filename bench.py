@@ -260,6 +260,7 @@ def b200_arm(args):
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
                        "inputs_vs_l2": "state + contact arrays larger than L2 (no flush)",
                        "avg_acs": n_acs_avg, "avg_touching_pairs": n_touch_avg,
+                       "kt_candidate_rebuilds": int(rr.kt_rebuilds),
                        "precision": args.precision},
             "roofline": {"bound": "hbm", "kernel": "k_contacts", "achieved": ach_c, "peak": hbm,
                          "unit": "GB/s", "frac": ach_c / hbm, "peak_kind": hbm_kind,

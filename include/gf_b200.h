@@ -184,6 +184,7 @@ typedef struct {
   int64_t sum_touch_pairs;  /* touching entries summed over the run's steps */
   double dt_ms, kt_ms;  /* device time of the dT and kT streams */
   double wall_ms;
+  int64_t kt_rebuilds;  /* candidate-list rebuilds so far (Verlet skin exceeded) */
 } gf_run_result;
 
 int gf_run(gf_ctx *ctx, const gf_run_params *p, gf_run_result *r);

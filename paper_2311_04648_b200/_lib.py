@@ -46,7 +46,7 @@ class RunResult(C.Structure):
     _fields_ = [("steps_done", _I64), ("bad_owner", _I64), ("bad_step", _I64),
                 ("oob_owner", _I64), ("oob_step", _I64), ("touching", _I64), ("n_acs", _I64),
                 ("ca_updates", _I64), ("sum_acs", _I64), ("sum_touch_pairs", _I64), ("dt_ms", _D),
-                ("kt_ms", _D), ("wall_ms", _D)]
+                ("kt_ms", _D), ("wall_ms", _D), ("kt_rebuilds", _I64)]
 
 
 # every symbol include/gf_b200.h declares

@@ -108,9 +108,11 @@ struct Status {
   unsigned long long touching;
   unsigned long long acs_total;   // last detection's pair count
   unsigned long long touch_pairs;  // touching ACS entries summed over the run's steps
+  unsigned long long cand_total;   // candidate pairs of the last rebuild
+  unsigned long long other_total;  // sphere-triangle / sphere-analytic pairs of the last detection
   double oob_pos[3];
   int err;                   // nonzero once a watchdog tripped (kernels stop)
-  int pad;
+  int rebuild;               // detection phase A: candidate lists must be rebuilt
 };
 
 __host__ __device__ inline uint32_t meta_family(uint32_t m) { return m >> 24; }

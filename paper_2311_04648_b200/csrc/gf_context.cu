@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cmath>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -266,6 +267,8 @@ gf_ctx *gf_create(int device, uint32_t flags) {
   cudaEventCreateWithFlags(&c->ev_ca, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->ev_adopted, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->ev_count, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->ev_disp, cudaEventDisableTiming);
+  if (const char *sf = std::getenv("GF_SKIN_FACTOR")) c->skin_factor = std::atof(sf);
   cudaEventCreate(&c->t0);
   cudaEventCreate(&c->t1);
   cudaEventRecord(c->ev_adopted, c->s_dt);
@@ -297,10 +300,11 @@ void gf_destroy(gf_ctx *ctx) {
                   &c->kt.cell_start, &c->kt.cell_end, &c->kt.tri_ranges, &c->kt.tri_cnt,
                   &c->kt.tri_start, &c->kt.tri_entries, &c->kt.counts, &c->kt.offsets, &c->kt.cub_tmp,
                   &c->kt.total, &c->kt.cursor, &c->kt.tri_cursor, &c->big_slots, &c->kt.sc,
-                  &c->kt.sm, &c->kt.sf, &c->kt.cells, &c->kt.n_cells, &c->kt.tmp, &c->kt.tmp_n, &c->acs.seg, &c->acs_next.seg};
+                  &c->kt.sm, &c->kt.sf, &c->kt.cells, &c->kt.n_cells, &c->kt.cand, &c->kt.cand_tmp, &c->kt.cand_n,
+                  &c->kt.cand_cnt, &c->kt.cand_seg, &c->kt.ref, &c->kt.flag, &c->kt.tmp, &c->kt.tmp_n, &c->acs.seg, &c->acs_next.seg};
   for (DBuf *b : bufs) release(*b);
   if (c->h_status) cudaFreeHost(c->h_status);
-  cudaEvent_t evs[] = {c->ev_snap, c->ev_ca, c->ev_adopted, c->ev_count, c->t0, c->t1};
+  cudaEvent_t evs[] = {c->ev_snap, c->ev_ca, c->ev_adopted, c->ev_count, c->ev_disp, c->t0, c->t1};
   for (auto e : evs) cudaEventDestroy(e);
   cudaStreamDestroy(c->s_dt);
   cudaStreamDestroy(c->s_kt);
@@ -500,6 +504,7 @@ int gf_upload_geometry(gf_ctx *ctx, int64_t n_s, const int64_t *sph_owner, const
       ensure(c, c->tri_world, 72 * (n_t + 1), c->s_dt) || ensure(c, c->ana_world, 64 * (n_a + 1), c->s_dt))
     return -1;
   if (set_split(c, sph_params + 3, 4, n_s)) return -1;
+  c->kt.cand_valid = false;
   c->lever_max = 0.0;
   for (int64_t k = 0; k < n_s; ++k) {
     const float *q = sph_params + 4 * k;
@@ -625,7 +630,9 @@ int gf_get_acs(gf_ctx *ctx, int which, uint8_t *kind, int64_t *slot_a, int64_t *
 
 static int detect_now(Ctx *c, double margin, int64_t *n_out) {
   c->kt_margin = margin;
-  if (kt_detect_count(c, margin, c->s_kt)) return -1;
+  if (kt_begin(c, margin, c->s_kt)) return -1;
+  GF_CHECK(c, cudaStreamSynchronize(c->s_kt));
+  if (kt_count(c, c->s_kt)) return -1;
   GF_CHECK(c, cudaStreamSynchronize(c->s_kt));
   c->acs_next.n = int64_t(reinterpret_cast<Status *>(c->h_status)->acs_total);
   if (kt_detect_fill(c, c->acs_next, c->s_kt)) return -1;
@@ -665,6 +672,7 @@ int gf_detect_snapshot(gf_ctx *ctx, int64_t m, const double *centers, const floa
       upload_raw(c, k.afam, ana_family, n_a) || upload_raw(c, c->fam_mask, mask, 65536))
     return -1;
   if (set_split(c, radii, 1, m)) return -1;
+  c->kt.cand_valid = false;
   int rc = detect_now(c, margin, n_out);
   c->kt_bin_size = 0.0;
   if (rc) return -1;
@@ -776,7 +784,17 @@ int gf_run(gf_ctx *ctx, const gf_run_params *p, gf_run_result *r) {
   GF_CHECK(c, cudaStreamSynchronize(c->s_dt));
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kt_ev;
   GF_CHECK(c, cudaEventRecord(c->t0, c->s_dt));
+  // kT phases: begun (grid + displacement check queued) -> counted (candidate
+  // filter + counts queued) -> filled (canonical array queued)
+  auto do_count = [&]() -> int {
+    GF_CHECK(c, cudaEventSynchronize(c->ev_disp));
+    if (kt_count(c, c->s_kt)) return -1;
+    GF_CHECK(c, cudaEventRecord(c->ev_count, c->s_kt));
+    c->kt_phase = 2;
+    return 0;
+  };
   auto do_fill = [&]() -> int {
+    if (c->kt_phase == 1 && do_count()) return -1;
     GF_CHECK(c, cudaEventSynchronize(c->ev_count));
     c->acs_next.n = int64_t(reinterpret_cast<Status *>(c->h_status)->acs_total);
     if (kt_detect_fill(c, c->acs_next, c->s_kt)) return -1;
@@ -810,8 +828,9 @@ int gf_run(gf_ctx *ctx, const gf_run_params *p, gf_run_result *r) {
       cudaEventCreate(&e1);
       kt_ev.emplace_back(e0, e1);
       GF_CHECK(c, cudaEventRecord(e0, c->s_kt));
-      if (kt_detect_count(c, p->margin, c->s_kt)) return -1;
-      GF_CHECK(c, cudaEventRecord(c->ev_count, c->s_kt));
+      if (kt_begin(c, p->margin, c->s_kt)) return -1;
+      GF_CHECK(c, cudaEventRecord(c->ev_disp, c->s_kt));
+      c->kt_phase = 1;
       c->next_pending = true;
       c->fill_done = false;
       c->last_snap = s;
@@ -820,7 +839,7 @@ int gf_run(gf_ctx *ctx, const gf_run_params *p, gf_run_result *r) {
       if (c->adopt_at <= s && do_adopt()) return -1;
     }
     // 3. launch the fill as soon as the count is known (no dT stall)
-    if (c->next_pending && !c->fill_done) {
+    if (c->next_pending && !c->fill_done && c->kt_phase == 2) {
       cudaError_t q = cudaEventQuery(c->ev_count);
       if (q == cudaErrorNotReady) {
         if (cudaPeekAtLastError() == cudaErrorNotReady) (void)cudaGetLastError();
@@ -832,6 +851,8 @@ int gf_run(gf_ctx *ctx, const gf_run_params *p, gf_run_result *r) {
     StepArgs a{p->h, {p->g[0], p->g[1], p->g[2]}, p->v_err, double(s) * p->h, s, i,
                (i == N - 1) ? p->write_acc : 0};
     if (dt_step(c, a)) return -1;
+    // the detection's candidate filter is queued once the dT step is in flight
+    if (c->next_pending && c->kt_phase == 1 && do_count()) return -1;
   }
   // finish enqueuing an in-flight detection (its fill) inside this call
   if (c->next_pending && !c->fill_done && do_fill()) return -1;
@@ -870,6 +891,7 @@ int gf_run(gf_ctx *ctx, const gf_run_params *p, gf_run_result *r) {
   r->n_acs = c->acs.n;
   r->ca_updates = c->ca_updates;
   r->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
+  r->kt_rebuilds = c->kt.rebuilds;
   return 0;
 }
 

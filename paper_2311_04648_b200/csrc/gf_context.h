@@ -48,6 +48,11 @@ struct KtScratch {
                      // float4 (centre - grid origin, radius) for the conservative fp32 prefilter
   DBuf tmp, tmp_n;   // scratch pair list (uint2) and its append counter
   DBuf cells, n_cells;  // non-empty enumeration cells
+  // Verlet candidate lists (rebuilt when a sphere moved > skin / 2)
+  DBuf cand, cand_tmp, cand_n, cand_cnt, cand_seg, ref, flag;
+  int64_t cand_cap = 0, rebuilds = 0;
+  bool cand_valid = false;
+  double cand_skin = -1.0;
   int64_t tmp_cap = 0;
   DBuf tri_cursor;   // uint32 per cell
   DBuf counts;       // uint64[3*n_s+1] per sphere SS / ST / SA counts
@@ -63,7 +68,8 @@ struct Ctx {
   bool f32_state = false;
   std::string err;
   cudaStream_t s_dt = nullptr, s_kt = nullptr;
-  cudaEvent_t ev_snap = nullptr, ev_ca = nullptr, ev_adopted = nullptr, ev_count = nullptr;
+  cudaEvent_t ev_snap = nullptr, ev_ca = nullptr, ev_adopted = nullptr, ev_count = nullptr, ev_disp = nullptr;
+  int kt_phase = 0;  // in-flight detection: 1 begun, 2 counted
   cudaEvent_t t0 = nullptr, t1 = nullptr;
 
   Domain dom{};
@@ -113,6 +119,7 @@ struct Ctx {
   int n_dyn = 0;
   double kt_margin = 0.0;
   double kt_bin_size = 0.0;  // > 0: explicit bin size (detect_contacts(bin_size=...))
+  double skin_factor = 1.0;  // Verlet skin = skin_factor * margin
   // schedule state (kept across gf_run calls)
   bool first_adopt = true;     // the first do_dynamics detects and waits (engine.py:679-682)
   bool fill_done = false;
@@ -161,7 +168,8 @@ Families families_view(Ctx *c);
 
 // kT (gf_kt.cu)
 int kt_snapshot(Ctx *c, cudaStream_t s);                 // centers/families -> kT scratch
-int kt_detect_count(Ctx *c, double margin, cudaStream_t s);
+int kt_begin(Ctx *c, double margin, cudaStream_t s);               // grid + displacement check
+int kt_count(Ctx *c, cudaStream_t s, bool force_rebuild = false);   // candidates -> counts
 int kt_detect_fill(Ctx *c, Acs &out, cudaStream_t s);
 int kt_bin_ranges(Ctx *c, double margin, int64_t *h_out);
 int adopt_acs(Ctx *c, cudaStream_t s);                   // merge history + incidence lists

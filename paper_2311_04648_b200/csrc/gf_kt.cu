@@ -144,7 +144,7 @@ __global__ void k_minmax(int64_t n_pts, const double *pts, int64_t n_s, const fl
 // single thread: exact restatement of _grid_for's scalar arithmetic, plus the
 // enumeration grid (cell = 2 (r_cut + margin), same growth rule, own cap)
 __global__ void k_grid(const unsigned long long *mm, int64_t n_pts, double margin, double bin_override,
-                       double r_cut, long long max_cells, Grid *g) {
+                       double r_cut, long long max_cells, double enum_margin, Grid *g) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   Grid out;
   out.valid = n_pts > 0;
@@ -170,7 +170,7 @@ __global__ void k_grid(const unsigned long long *mm, int64_t n_pts, double margi
   // enumeration grid; r_cut <= 0 means "every sphere is small"
   double rc = r_cut > 0.0 && r_cut < r_max ? r_cut : r_max;
   out.r_cut = rc;
-  double cell = bin_override > 0.0 ? bin_size : 2.0 * (rc + margin);
+  double cell = bin_override > 0.0 ? bin_size : 2.0 * (rc + enum_margin);
   if (cell <= 0.0) cell = 1.0;
   for (;;) {
     for (int ax = 0; ax < 3; ++ax) {
@@ -638,6 +638,206 @@ __global__ void k_sort_seg(int64_t nseg, const unsigned long long *offsets, uint
   if (cnt > 1) sort_segment_y(out, w, cnt);
 }
 
+// ---------------------------------------------------------------------------
+// Verlet candidate lists.  A rebuild enumerates every sphere-sphere pair
+// within margin + skin (fp32 test with conservative slack, different owners;
+// families / masks are NOT applied -- they may change between detections)
+// into per-sphere candidate segments sorted by the partner slot.  Each
+// detection then evaluates the exact reference predicate on the candidates
+// only.  Exactness: a pair within the margin at a detection was within
+// margin + skin at the rebuild if neither sphere moved more than skin / 2
+// since, which k_disp checks before every detection.
+// ---------------------------------------------------------------------------
+
+// any sphere displaced more than skin / 2 since the rebuild -> flag
+__global__ void k_disp(int64_t n, const double *c, const double *ref, double lim2, int *flag) {
+  int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  bool far = false;
+  if (i < n) {
+    double dx = c[3 * i] - ref[3 * i], dy = c[3 * i + 1] - ref[3 * i + 1], dz = c[3 * i + 2] - ref[3 * i + 2];
+    far = dx * dx + dy * dy + dz * dz > lim2;
+  }
+  if (__any_sync(0xffffffffu, far) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+// candidate pairs among small spheres: half stencil on the enumeration grid
+// (cell = 2 (r_cut + margin + skin)); hits counted per lower slot and
+// appended to a scratch list
+__global__ void __launch_bounds__(128) k_cand_ss(KtView v, const uint4 *sm, const float4 *sf, double reach_m,
+                                                 unsigned long long *counts, uint2 *tmp,
+                                                 unsigned long long *tmp_n, unsigned long long cap) {
+  int64_t u64 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const Grid g = *v.grid;
+  bool active = u64 < v.sph.n && g.valid;
+  uint32_t key = active ? v.bin_key[u64] : kNoCell;
+  active = active && key != kNoCell;
+  const float ext = float(double(max(g.nc[0], max(g.nc[1], g.nc[2]))) / g.inv_cell);
+  const float slack = 1e-6f * ext + 1e-30f;
+  const float marg = float(reach_m);
+  float4 f0 = make_float4(0.f, 0.f, 0.f, 0.f);
+  uint4 m0 = make_uint4(0, 0, 0, 0);
+  long long cx = 0, cy = 0, cz = 0;
+  if (active) {
+    f0 = sf[u64];
+    m0 = sm[u64];
+    cx = key % g.nc[0];
+    cy = (key / g.nc[0]) % g.nc[1];
+    cz = key / (g.nc[0] * g.nc[1]);
+  }
+  for (int span = 0; span < 6; ++span) {
+    uint32_t s0 = 0, s1 = 0;
+    if (active) {
+      if (span == 0) {
+        s0 = uint32_t(u64) + 1;
+        s1 = v.cell_end[key];
+      } else {
+        long long dz = span >= 3 ? 1 : 0;
+        long long dy = span == 2 ? 1 : (span >= 3 ? span - 4 : 0);
+        long long x0 = span == 1 ? cx + 1 : cx - 1, x1 = cx + 1;
+        long long y = cy + dy, z = cz + dz;
+        if (x0 < 0) x0 = 0;
+        if (x1 >= g.nc[0]) x1 = g.nc[0] - 1;
+        if (y >= 0 && y < g.nc[1] && z < g.nc[2] && x0 <= x1) {
+          long long row = (z * g.nc[1] + y) * g.nc[0];
+          uint32_t a0 = 0xFFFFFFFFu;
+          for (long long x = x0; x <= x1; ++x) {
+            uint32_t st = v.cell_start[row + x];
+            if (st == 0xFFFFFFFFu) continue;
+            if (a0 == 0xFFFFFFFFu) a0 = st;
+            s1 = v.cell_end[row + x];
+          }
+          s0 = a0 == 0xFFFFFFFFu ? 0 : a0;
+          if (a0 == 0xFFFFFFFFu) s1 = 0;
+        }
+      }
+    }
+    const uint32_t len = s1 > s0 ? s1 - s0 : 0;
+    uint32_t maxlen = len;
+    for (int off = 16; off > 0; off >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, off));
+    for (uint32_t t = 0; t < maxlen; ++t) {
+      bool hit = false;
+      uint2 e = make_uint2(0, 0);
+      if (t < len) {
+        const uint32_t w = s0 + t;
+        const float4 f1 = sf[w];
+        const float dx = f0.x - f1.x, dy = f0.y - f1.y, dz = f0.z - f1.z;
+        const float rr = f0.w + f1.w + marg + slack;
+        if (dx * dx + dy * dy + dz * dz < rr * rr * 1.0001f) {
+          const uint4 m1 = sm[w];
+          if (m1.y != m0.y) {
+            hit = true;
+            const uint32_t a = min(m0.x, m1.x), b = max(m0.x, m1.x);
+            e = make_uint2(a, b);
+            atomicAdd(&counts[a], 1ull);
+          }
+        }
+      }
+      append_pair(hit, e, tmp, tmp_n, cap);
+    }
+  }
+}
+
+// candidate pairs involving big spheres (fp64 distance < r_i + r_j + M)
+__global__ void __launch_bounds__(128) k_cand_big(KtView v, const uint32_t *bigs, int64_t n_big,
+                                                  const double4 *sc, const uint4 *sm, double reach_m,
+                                                  unsigned long long *counts, uint2 *tmp,
+                                                  unsigned long long *tmp_n, unsigned long long cap) {
+  const Grid g = *v.grid;
+  if (!g.valid) return;
+  for (int64_t bi = blockIdx.x; bi < n_big; bi += gridDim.x) {
+    const uint32_t B = bigs[bi];
+    const double bx = v.centers[3 * size_t(B)], by = v.centers[3 * size_t(B) + 1], bz = v.centers[3 * size_t(B) + 2];
+    const double rB = double(v.sph.offr[B].w);
+    const uint32_t oB = v.sph.owner[B];
+    const double reach = rB + g.r_cut + reach_m;
+    const double cbv[3] = {bx, by, bz};
+    long long flo[3], fhi[3];
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      flo[ax] = axis_bin(cbv[ax] - reach, g.glo[ax], g.inv_cell, g.nc[ax]);
+      fhi[ax] = axis_bin(cbv[ax] + reach, g.glo[ax], g.inv_cell, g.nc[ax]);
+    }
+    const long long sx = fhi[0] - flo[0] + 1, sy = fhi[1] - flo[1] + 1, sz = fhi[2] - flo[2] + 1;
+    const long long ncell = sx * sy * sz;
+    for (long long q = threadIdx.x; q < ncell; q += blockDim.x) {
+      long long x = flo[0] + q % sx, y = flo[1] + (q / sx) % sy, z = flo[2] + q / (sx * sy);
+      long long b = (z * g.nc[1] + y) * g.nc[0] + x;
+      uint32_t s0 = v.cell_start[b];
+      if (s0 == 0xFFFFFFFFu) continue;
+      uint32_t s1 = v.cell_end[b];
+      for (uint32_t w = s0; w < s1; ++w) {
+        const double4 c1 = sc[w];
+        const uint4 m1 = sm[w];
+        if (m1.y == oB) continue;
+        const double dx = bx - c1.x, dy = by - c1.y, dz = bz - c1.z;
+        const double rr = rB + c1.w + reach_m;
+        if (dx * dx + dy * dy + dz * dz >= rr * rr * (1.0 + 1e-9)) continue;
+        const uint32_t a = min(m1.x, B), c = max(m1.x, B);
+        atomicAdd(&counts[a], 1ull);
+        unsigned long long pos = atomicAdd(tmp_n, 1ull);
+        if (pos < cap) tmp[pos] = make_uint2(a, c);
+      }
+    }
+    for (int64_t q = threadIdx.x; q < n_big; q += blockDim.x) {
+      const uint32_t j = bigs[q];
+      if (j <= B || v.sph.owner[j] == oB) continue;
+      const double dx = bx - v.centers[3 * size_t(j)], dy = by - v.centers[3 * size_t(j) + 1],
+                   dz = bz - v.centers[3 * size_t(j) + 2];
+      const double rr = rB + double(v.sph.offr[j].w) + reach_m;
+      if (dx * dx + dy * dy + dz * dz >= rr * rr * (1.0 + 1e-9)) continue;
+      atomicAdd(&counts[B], 1ull);
+      unsigned long long pos = atomicAdd(tmp_n, 1ull);
+      if (pos < cap) tmp[pos] = make_uint2(B, j);
+    }
+  }
+}
+
+// scatter candidates into per-sphere segments (k_sort_seg then orders them)
+__global__ void k_place_cand(const unsigned long long *m_p, const uint2 *tmp, const unsigned long long *seg,
+                             unsigned *cursor, uint2 *cand, unsigned long long cap) {
+  const unsigned long long m = min(*m_p, cap);
+  for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < m;
+       e += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint2 p = tmp[e];
+    cand[seg[p.x] + atomicAdd(&cursor[p.x], 1u)] = p;
+  }
+}
+
+// exact reference predicate on the candidates of sphere i; the output keeps
+// the candidate order (ascending partner slot), i.e. canonical order
+template <bool FILL>
+__global__ void __launch_bounds__(128) k_filter(KtView v, const uint2 *cand, const unsigned long long *cseg,
+                                                unsigned long long *counts, const unsigned long long *offsets,
+                                                uint2 *out) {
+  int64_t i64 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i64 >= v.sph.n) return;
+  const Grid g = *v.grid;
+  const uint32_t i = uint32_t(i64);
+  const unsigned long long e0 = cseg[i64], e1 = cseg[i64 + 1];
+  unsigned long long cnt = 0, w = FILL ? offsets[i64] : 0;
+  if (e1 > e0 && g.valid) {
+    double ci[3] = {v.centers[3 * i64], v.centers[3 * i64 + 1], v.centers[3 * i64 + 2]};
+    const float ri_f = v.sph.offr[i].w;
+    const uint32_t oi = v.sph.owner[i];
+    const uint8_t fi = v.sfam[i];
+    long long lo_i[3], hi_i[3];
+    sphere_range(g, ci, ri_f, v.margin, lo_i, hi_i);
+    for (unsigned long long e = e0; e < e1; ++e) {
+      const uint32_t j = cand[e].y;
+      if (ss_pair(v, g, i, j, ci, ri_f, lo_i, hi_i, oi, fi)) {
+        if (FILL) out[w + cnt] = make_uint2(i, j);
+        ++cnt;
+      }
+    }
+  }
+  if (!FILL) counts[i64] = cnt;
+}
+
+__global__ void k_copy_ref(int64_t n3, const double *c, double *ref) {
+  int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < n3) ref[i] = c[i];
+}
+
 __global__ void k_fill_u32(const Grid *gp, uint32_t *a, uint32_t value, int fine_plus_one) {
   Grid g = *gp;
   int64_t n = g.nc[0] * g.nc[1] * g.nc[2] + fine_plus_one;
@@ -819,83 +1019,37 @@ static KtView kt_view(Ctx *c, double margin) {
   return v;
 }
 
-static int run_pair_kernels(Ctx *c, cudaStream_t s) {
-  KtScratch &k = c->kt;
-  const int64_t n = c->n_sph;
-  KtView v = kt_view(c, c->kt_margin);
-  unsigned long long *cnt = k.counts.as<unsigned long long>();
-  unsigned long long *tn = k.tmp_n.as<unsigned long long>();
-  GF_CHECK(c, cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * (3 * n + 1), s));
-  GF_CHECK(c, cudaMemsetAsync(tn, 0, sizeof(unsigned long long), s));
-  const unsigned long long cap = (unsigned long long)k.tmp_cap;
-  uint2 *tmp = k.tmp.as<uint2>();
-  if (n) {
-    k_pairs_ss<<<grid_for(n, 128), 128, 0, s>>>(v, k.sc.as<double4>(), k.sm.as<uint4>(), k.sf.as<float4>(), cnt, tmp, tn, cap);
-    k_pairs_other<<<grid_for(n, 128), 128, 0, s>>>(v, cnt, tmp, tn, cap);
-  }
-  if (c->n_big)
-    k_big<<<unsigned(std::min<int64_t>(c->n_big, 4096)), 128, 0, s>>>(
-        v, c->big_slots.as<uint32_t>(), c->n_big, k.sc.as<double4>(), k.sm.as<uint4>(), cnt, tmp, tn, cap);
-  GF_CHECK(c, cudaGetLastError());
-  return 0;
-}
+__global__ void k_set_int(int *p, int v) { *p = v; }
 
-// grid + binning + one pair-enumeration pass (scratch list + per-segment
-// counts) + scan; the pair total goes to status.acs_total (pinned mirror)
-int kt_detect_count(Ctx *c, double margin, cudaStream_t s) {
+// phase A of a detection: grid, triangle registration, and the displacement
+// check that decides whether the candidate lists must be rebuilt (flag copied
+// to the pinned status mirror; the host reads it before kt_count)
+int kt_begin(Ctx *c, double margin, cudaStream_t s) {
   KtScratch &k = c->kt;
   const int64_t n = c->n_sph, nt = c->n_tri;
   const int64_t n_pts = n + 3 * nt;
   c->kt_margin = margin;
-  if (ensure(c, k.grid, sizeof(Grid), s)) return -1;
-  if (ensure(c, k.minmax, sizeof(unsigned long long) * 8, s)) return -1;
-  if (ensure(c, k.bin_key, 4 * (n + 1), s) || ensure(c, k.bin_key_alt, 4 * (n + 1), s) ||
-      ensure(c, k.sph_val, 4 * (n + 1), s) || ensure(c, k.sph_val_alt, 4 * (n + 1), s) ||
-      ensure(c, k.cursor, 4 * (3 * n + 1), s) || ensure(c, k.sc, 32 * (n + 1), s) ||
-      ensure(c, k.sm, 16 * (n + 1), s) || ensure(c, k.sf, 16 * (n + 1), s) || ensure(c, k.tmp_n, 16, s) ||
-      ensure(c, k.cells, 4 * (n + 1), s) || ensure(c, k.n_cells, 16, s))
+  const double skin = c->skin_factor * margin;
+  if (k.cand_valid && skin != k.cand_skin) k.cand_valid = false;
+  if (ensure(c, k.grid, sizeof(Grid), s) || ensure(c, k.minmax, sizeof(unsigned long long) * 8, s) ||
+      ensure(c, k.flag, 16, s))
     return -1;
-  if (ensure(c, k.cell_start, sizeof(uint32_t) * (kMaxCells + 1), s) ||
-      ensure(c, k.cell_end, sizeof(uint32_t) * (kMaxCells + 1), s))
-    return -1;
-  if (ensure(c, k.counts, sizeof(unsigned long long) * (3 * n + 1), s) ||
-      ensure(c, k.offsets, sizeof(unsigned long long) * (3 * n + 1), s))
-    return -1;
-  if (k.tmp_cap == 0) {
-    int64_t cap = std::max<int64_t>(16 * n, 4096);
-    if (ensure(c, k.tmp, sizeof(uint2) * cap, s)) return -1;
-    k.tmp_cap = cap;
-  }
-  // min/max over centres and triangle vertices (exact), r_max
   unsigned long long *mm = k.minmax.as<unsigned long long>();
   k_minmax_init<<<1, 32, 0, s>>>(mm);
   if (n) k_minmax<<<std::min<int64_t>(grid_for(n), 1184), kBlock, 0, s>>>(n, k.centers.as<double>(), n, c->sph_offr.as<float4>(), mm);
   if (nt) k_minmax<<<std::min<int64_t>(grid_for(3 * nt), 1184), kBlock, 0, s>>>(3 * nt, k.tri_world.as<double>(), 0, nullptr, mm);
-  k_grid<<<1, 1, 0, s>>>(mm, n_pts, margin, c->kt_bin_size, c->r_cut, (long long)kMaxCells,
+  k_grid<<<1, 1, 0, s>>>(mm, n_pts, margin, c->kt_bin_size, c->r_cut, (long long)kMaxCells, margin + skin,
                          k.grid.as<Grid>());
   const Grid *gp = k.grid.as<Grid>();
-  if (n) {
-    k_bin_keys<<<grid_for(n), kBlock, 0, s>>>(n, k.centers.as<double>(), c->sph_offr.as<float4>(), gp,
-                                             k.bin_key.as<uint32_t>(), k.sph_val.as<uint32_t>());
-    size_t tmp = 0;
-    cub::DoubleBuffer<uint32_t> dk(k.bin_key.as<uint32_t>(), k.bin_key_alt.as<uint32_t>());
-    cub::DoubleBuffer<uint32_t> dv(k.sph_val.as<uint32_t>(), k.sph_val_alt.as<uint32_t>());
-    cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, int(n), 0, kKeyBits, s);
-    if (ensure(c, k.cub_tmp, tmp + 16, s)) return -1;
-    GF_CHECK(c, cub::DeviceRadixSort::SortPairs(k.cub_tmp.p, tmp, dk, dv, int(n), 0, kKeyBits, s));
-    if (dk.Current() != k.bin_key.as<uint32_t>()) {
-      std::swap(k.bin_key, k.bin_key_alt);
-      std::swap(k.sph_val, k.sph_val_alt);
-    }
-    k_fill_u32<<<592, 256, 0, s>>>(gp, k.cell_start.as<uint32_t>(), 0xFFFFFFFFu, 0);
-    k_cell_bounds<<<grid_for(n), kBlock, 0, s>>>(n, k.bin_key.as<uint32_t>(),
-                                                k.cell_start.as<uint32_t>(), k.cell_end.as<uint32_t>());
-
-    k_gather_sorted<<<grid_for(n), kBlock, 0, s>>>(n, k.sph_val.as<uint32_t>(), k.centers.as<double>(),
-                                                  c->sph_offr.as<float4>(), c->sph_owner.as<uint32_t>(),
-                                                  k.sfam.as<uint8_t>(), gp, k.sc.as<double4>(), k.sm.as<uint4>(),
-                                                  k.sf.as<float4>());
+  int *flag = k.flag.as<int>();
+  if (k.cand_valid && n) {
+    GF_CHECK(c, cudaMemsetAsync(flag, 0, sizeof(int), s));
+    k_disp<<<grid_for(n), kBlock, 0, s>>>(n, k.centers.as<double>(), k.ref.as<double>(), 0.25 * skin * skin, flag);
+  } else {
+    k_set_int<<<1, 1, 0, s>>>(flag, 1);
   }
+  GF_CHECK(c, cudaMemcpyAsync(&reinterpret_cast<Status *>(c->h_status)->rebuild, flag, sizeof(int),
+                              cudaMemcpyDeviceToHost, s));
   if (nt) {
     if (ensure(c, k.tri_cnt, sizeof(uint32_t) * (kMaxCells + 1), s) ||
         ensure(c, k.tri_start, sizeof(uint32_t) * (kMaxCells + 1), s) ||
@@ -921,39 +1075,156 @@ int kt_detect_count(Ctx *c, double margin, cudaStream_t s) {
                                                         nullptr, k.tri_cursor.as<uint32_t>(),
                                                         k.tri_entries.as<uint32_t>());
   }
-  if (run_pair_kernels(c, s)) return -1;
+  GF_CHECK(c, cudaGetLastError());
+  return 0;
+}
+
+// rebuild the candidate lists from the current snapshot (enumeration grid
+// with reach margin + skin)
+static int rebuild_candidates(Ctx *c, cudaStream_t s) {
+  KtScratch &k = c->kt;
+  const int64_t n = c->n_sph;
+  const double reach = c->kt_margin + c->skin_factor * c->kt_margin;
+  if (ensure(c, k.bin_key, 4 * (n + 1), s) || ensure(c, k.bin_key_alt, 4 * (n + 1), s) ||
+      ensure(c, k.sph_val, 4 * (n + 1), s) || ensure(c, k.sph_val_alt, 4 * (n + 1), s) ||
+      ensure(c, k.cursor, 4 * (3 * n + 1), s) || ensure(c, k.sc, 32 * (n + 1), s) ||
+      ensure(c, k.sm, 16 * (n + 1), s) || ensure(c, k.sf, 16 * (n + 1), s) ||
+      ensure(c, k.cand_n, 16, s) || ensure(c, k.cand_cnt, 8 * (n + 1), s) ||
+      ensure(c, k.cand_seg, 8 * (n + 1), s) || ensure(c, k.ref, 24 * (n + 1), s) ||
+      ensure(c, k.cell_start, sizeof(uint32_t) * (kMaxCells + 1), s) ||
+      ensure(c, k.cell_end, sizeof(uint32_t) * (kMaxCells + 1), s))
+    return -1;
+  if (k.cand_cap == 0) {
+    int64_t cap = std::max<int64_t>(16 * n, 4096);
+    if (ensure(c, k.cand_tmp, sizeof(uint2) * cap, s) || ensure(c, k.cand, sizeof(uint2) * cap, s)) return -1;
+    k.cand_cap = cap;
+  }
+  const Grid *gp = k.grid.as<Grid>();
+  KtView v = kt_view(c, c->kt_margin);
+  unsigned long long *cc = k.cand_cnt.as<unsigned long long>();
+  unsigned long long *cn = k.cand_n.as<unsigned long long>();
+  GF_CHECK(c, cudaMemsetAsync(cc, 0, 8 * (n + 1), s));
+  GF_CHECK(c, cudaMemsetAsync(cn, 0, 8, s));
+  if (n) {
+    k_bin_keys<<<grid_for(n), kBlock, 0, s>>>(n, k.centers.as<double>(), c->sph_offr.as<float4>(), gp,
+                                             k.bin_key.as<uint32_t>(), k.sph_val.as<uint32_t>());
+    size_t tmp = 0;
+    cub::DoubleBuffer<uint32_t> dk(k.bin_key.as<uint32_t>(), k.bin_key_alt.as<uint32_t>());
+    cub::DoubleBuffer<uint32_t> dv(k.sph_val.as<uint32_t>(), k.sph_val_alt.as<uint32_t>());
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, int(n), 0, kKeyBits, s);
+    if (ensure(c, k.cub_tmp, tmp + 16, s, false)) return -1;
+    GF_CHECK(c, cub::DeviceRadixSort::SortPairs(k.cub_tmp.p, tmp, dk, dv, int(n), 0, kKeyBits, s));
+    if (dk.Current() != k.bin_key.as<uint32_t>()) {
+      std::swap(k.bin_key, k.bin_key_alt);
+      std::swap(k.sph_val, k.sph_val_alt);
+    }
+    v = kt_view(c, c->kt_margin);
+    k_fill_u32<<<592, 256, 0, s>>>(gp, k.cell_start.as<uint32_t>(), 0xFFFFFFFFu, 0);
+    k_cell_bounds<<<grid_for(n), kBlock, 0, s>>>(n, k.bin_key.as<uint32_t>(), k.cell_start.as<uint32_t>(),
+                                                k.cell_end.as<uint32_t>());
+    k_gather_sorted<<<grid_for(n), kBlock, 0, s>>>(n, k.sph_val.as<uint32_t>(), k.centers.as<double>(),
+                                                  c->sph_offr.as<float4>(), c->sph_owner.as<uint32_t>(),
+                                                  k.sfam.as<uint8_t>(), gp, k.sc.as<double4>(),
+                                                  k.sm.as<uint4>(), k.sf.as<float4>());
+    k_cand_ss<<<grid_for(n, 128), 128, 0, s>>>(v, k.sm.as<uint4>(), k.sf.as<float4>(), reach, cc,
+                                               k.cand_tmp.as<uint2>(), cn, (unsigned long long)k.cand_cap);
+    if (c->n_big)
+      k_cand_big<<<unsigned(std::min<int64_t>(c->n_big, 4096)), 128, 0, s>>>(
+          v, c->big_slots.as<uint32_t>(), c->n_big, k.sc.as<double4>(), k.sm.as<uint4>(), reach, cc,
+          k.cand_tmp.as<uint2>(), cn, (unsigned long long)k.cand_cap);
+  }
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, cc, k.cand_seg.as<unsigned long long>(), int(n + 1), s);
+  if (ensure(c, k.cub_tmp, tmp + 16, s, false)) return -1;
+  GF_CHECK(c, cub::DeviceScan::ExclusiveSum(k.cub_tmp.p, tmp, cc, k.cand_seg.as<unsigned long long>(),
+                                            int(n + 1), s));
+  if (n) {
+    GF_CHECK(c, cudaMemsetAsync(k.cursor.p, 0, 4 * n, s));
+    k_place_cand<<<1184, 256, 0, s>>>(cn, k.cand_tmp.as<uint2>(), k.cand_seg.as<unsigned long long>(),
+                                      k.cursor.as<unsigned>(), k.cand.as<uint2>(),
+                                      (unsigned long long)k.cand_cap);
+    k_sort_seg<<<grid_for(n), kBlock, 0, s>>>(n, k.cand_seg.as<unsigned long long>(), k.cand.as<uint2>());
+    k_copy_ref<<<grid_for(3 * n), kBlock, 0, s>>>(3 * n, k.centers.as<double>(), k.ref.as<double>());
+  }
+  GF_CHECK(c, cudaMemcpyAsync(&reinterpret_cast<Status *>(c->h_status)->cand_total, cn, 8,
+                              cudaMemcpyDeviceToHost, s));
+  k.cand_valid = true;
+  k.cand_skin = c->skin_factor * c->kt_margin;
+  k.rebuilds++;
+  GF_CHECK(c, cudaGetLastError());
+  return 0;
+}
+
+// phase B (after the host read the phase-A flag): optional rebuild, exact
+// filter of the candidates, sphere-triangle / sphere-analytic pairs, counts,
+// scan; the pair total goes to the pinned status mirror
+int kt_count(Ctx *c, cudaStream_t s, bool force_rebuild) {
+  KtScratch &k = c->kt;
+  const int64_t n = c->n_sph;
+  Status *hs = reinterpret_cast<Status *>(c->h_status);
+  if (force_rebuild || !k.cand_valid || hs->rebuild) {
+    hs->cand_total = 0;
+    if (rebuild_candidates(c, s)) return -1;
+  }
+  if (ensure(c, k.counts, sizeof(unsigned long long) * (3 * n + 1), s) ||
+      ensure(c, k.offsets, sizeof(unsigned long long) * (3 * n + 1), s) || ensure(c, k.tmp_n, 16, s))
+    return -1;
+  if (k.tmp_cap == 0) {
+    int64_t cap = std::max<int64_t>(n, 4096);
+    if (ensure(c, k.tmp, sizeof(uint2) * cap, s)) return -1;
+    k.tmp_cap = cap;
+  }
+  KtView v = kt_view(c, c->kt_margin);
   unsigned long long *cnt = k.counts.as<unsigned long long>();
+  unsigned long long *tn = k.tmp_n.as<unsigned long long>();
+  GF_CHECK(c, cudaMemsetAsync(cnt + 3 * n, 0, sizeof(unsigned long long), s));
+  GF_CHECK(c, cudaMemsetAsync(tn, 0, sizeof(unsigned long long), s));
+  if (n) {
+    k_filter<false><<<grid_for(n, 128), 128, 0, s>>>(v, k.cand.as<uint2>(), k.cand_seg.as<unsigned long long>(),
+                                                      cnt, nullptr, nullptr);
+    k_pairs_other<<<grid_for(n, 128), 128, 0, s>>>(v, cnt, k.tmp.as<uint2>(), tn, (unsigned long long)k.tmp_cap);
+  }
   size_t tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, k.offsets.as<unsigned long long>(), int(3 * n + 1), s);
   if (ensure(c, k.cub_tmp, tmp + 16, s, false)) return -1;
   GF_CHECK(c, cub::DeviceScan::ExclusiveSum(k.cub_tmp.p, tmp, cnt, k.offsets.as<unsigned long long>(),
                                             int(3 * n + 1), s));
-  // total -> status block -> pinned mirror
   Status *st = c->status.as<Status>();
   GF_CHECK(c, cudaMemcpyAsync(&st->acs_total, k.offsets.as<unsigned long long>() + 3 * n,
                               sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
-  GF_CHECK(c, cudaMemcpyAsync(&reinterpret_cast<Status *>(c->h_status)->acs_total, &st->acs_total,
-                              sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  GF_CHECK(c, cudaMemcpyAsync(&hs->acs_total, &st->acs_total, sizeof(unsigned long long),
+                              cudaMemcpyDeviceToHost, s));
+  GF_CHECK(c, cudaMemcpyAsync(&hs->other_total, tn, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   GF_CHECK(c, cudaGetLastError());
   return 0;
 }
 
-// canonical (kind, a, b) array from the scratch list; keeps the segment
-// offsets with the array for the next history remap
+// canonical (kind, a, b) array; keeps the segment offsets with the array for
+// the next history remap.  Host has synced on the count phase.
 int kt_detect_fill(Ctx *c, Acs &out, cudaStream_t s) {
   KtScratch &k = c->kt;
   const int64_t n = c->n_sph;
-  const int64_t total = out.n;
-  if (total > k.tmp_cap) {  // scratch overflowed: grow and enumerate again
-    int64_t cap = total + total / 4 + 4096;
-    if (ensure(c, k.tmp, sizeof(uint2) * cap, s)) return -1;
-    k.tmp_cap = cap;
-    if (run_pair_kernels(c, s)) return -1;
+  Status *hs = reinterpret_cast<Status *>(c->h_status);
+  if ((int64_t)hs->cand_total > k.cand_cap || (int64_t)hs->other_total > k.tmp_cap) {
+    // a scratch list overflowed: grow and redo the detection synchronously
+    if ((int64_t)hs->cand_total > k.cand_cap) {
+      int64_t cap = int64_t(hs->cand_total) + int64_t(hs->cand_total) / 4 + 4096;
+      if (ensure(c, k.cand_tmp, sizeof(uint2) * cap, s) || ensure(c, k.cand, sizeof(uint2) * cap, s)) return -1;
+      k.cand_cap = cap;
+    }
+    if ((int64_t)hs->other_total > k.tmp_cap) {
+      int64_t cap = int64_t(hs->other_total) + int64_t(hs->other_total) / 4 + 4096;
+      if (ensure(c, k.tmp, sizeof(uint2) * cap, s)) return -1;
+      k.tmp_cap = cap;
+    }
+    if (kt_count(c, s, true)) return -1;
+    GF_CHECK(c, cudaStreamSynchronize(s));
+    out.n = int64_t(hs->acs_total);
   }
+  const int64_t total = out.n;
   if (total > out.cap) {
     int64_t cap = total + total / 2 + 1024;
-    if (ensure(c, out.ids, sizeof(uint2) * cap, s) ||
-        ensure(c, out.wild, sizeof(float) * c->wild_w * cap, s))
+    if (ensure(c, out.ids, sizeof(uint2) * cap, s) || ensure(c, out.wild, sizeof(float) * c->wild_w * cap, s))
       return -1;
     out.cap = cap;
   }
@@ -961,12 +1232,14 @@ int kt_detect_fill(Ctx *c, Acs &out, cudaStream_t s) {
   GF_CHECK(c, cudaMemcpyAsync(out.seg.p, k.offsets.p, sizeof(unsigned long long) * (3 * n + 1),
                               cudaMemcpyDeviceToDevice, s));
   if (n && total) {
+    KtView v = kt_view(c, c->kt_margin);
+    const unsigned long long *off = k.offsets.as<unsigned long long>();
+    k_filter<true><<<grid_for(n, 128), 128, 0, s>>>(v, k.cand.as<uint2>(), k.cand_seg.as<unsigned long long>(),
+                                                     nullptr, off, out.ids.as<uint2>());
     GF_CHECK(c, cudaMemsetAsync(k.cursor.p, 0, sizeof(unsigned) * 3 * n, s));
-    k_place<<<1184, 256, 0, s>>>(k.tmp_n.as<unsigned long long>(), n, k.tmp.as<uint2>(),
-                                 k.offsets.as<unsigned long long>(), k.cursor.as<unsigned>(),
-                                 out.ids.as<uint2>());
-    k_sort_seg<<<grid_for(3 * n), kBlock, 0, s>>>(3 * n, k.offsets.as<unsigned long long>(),
-                                                  out.ids.as<uint2>());
+    k_place<<<1184, 256, 0, s>>>(k.tmp_n.as<unsigned long long>(), n, k.tmp.as<uint2>(), off,
+                                 k.cursor.as<unsigned>(), out.ids.as<uint2>());
+    k_sort_seg<<<grid_for(2 * n), kBlock, 0, s>>>(2 * n, off + n, out.ids.as<uint2>());
   }
   GF_CHECK(c, cudaGetLastError());
   return 0;
