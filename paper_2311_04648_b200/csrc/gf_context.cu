@@ -301,7 +301,7 @@ void gf_destroy(gf_ctx *ctx) {
                   &c->kt.tri_start, &c->kt.tri_entries, &c->kt.counts, &c->kt.offsets, &c->kt.cub_tmp,
                   &c->kt.total, &c->kt.cursor, &c->kt.tri_cursor, &c->big_slots, &c->kt.sc,
                   &c->kt.sm, &c->kt.sf, &c->kt.cells, &c->kt.n_cells, &c->kt.cand, &c->kt.cand_tmp, &c->kt.cand_n,
-                  &c->kt.cand_cnt, &c->kt.cand_seg, &c->kt.ref, &c->kt.flag, &c->kt.tmp, &c->kt.tmp_n, &c->acs.seg, &c->acs_next.seg};
+                  &c->kt.cand_cnt, &c->kt.cand_seg, &c->kt.ref, &c->kt.flag, &c->kt.cflags, &c->kt.sel_n, &c->kt.tmp, &c->kt.tmp_n, &c->acs.seg, &c->acs_next.seg};
   for (DBuf *b : bufs) release(*b);
   if (c->h_status) cudaFreeHost(c->h_status);
   cudaEvent_t evs[] = {c->ev_snap, c->ev_ca, c->ev_adopted, c->ev_count, c->ev_disp, c->t0, c->t1};

@@ -49,8 +49,8 @@ struct KtScratch {
   DBuf tmp, tmp_n;   // scratch pair list (uint2) and its append counter
   DBuf cells, n_cells;  // non-empty enumeration cells
   // Verlet candidate lists (rebuilt when a sphere moved > skin / 2)
-  DBuf cand, cand_tmp, cand_n, cand_cnt, cand_seg, ref, flag;
-  int64_t cand_cap = 0, rebuilds = 0;
+  DBuf cand, cand_tmp, cand_n, cand_cnt, cand_seg, ref, flag, cflags, sel_n;
+  int64_t cand_cap = 0, n_cand = 0, rebuilds = 0;
   bool cand_valid = false;
   double cand_skin = -1.0;
   int64_t tmp_cap = 0;

@@ -803,34 +803,24 @@ __global__ void k_place_cand(const unsigned long long *m_p, const uint2 *tmp, co
   }
 }
 
-// exact reference predicate on the candidates of sphere i; the output keeps
-// the candidate order (ascending partner slot), i.e. canonical order
-template <bool FILL>
-__global__ void __launch_bounds__(128) k_filter(KtView v, const uint2 *cand, const unsigned long long *cseg,
-                                                unsigned long long *counts, const unsigned long long *offsets,
-                                                uint2 *out) {
-  int64_t i64 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (i64 >= v.sph.n) return;
+// exact reference predicate on every candidate (one thread each, coalesced
+// over the candidate array, which is globally sorted by (a, b)): a flag per
+// candidate plus the per-sphere count; an order-preserving compaction of the
+// flagged candidates is then the canonical sphere-sphere block
+__global__ void __launch_bounds__(256) k_filter_flags(KtView v, const uint2 *cand, int64_t n_cand,
+                                                      uint8_t *flags, unsigned long long *counts) {
+  int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (e >= n_cand) return;
   const Grid g = *v.grid;
-  const uint32_t i = uint32_t(i64);
-  const unsigned long long e0 = cseg[i64], e1 = cseg[i64 + 1];
-  unsigned long long cnt = 0, w = FILL ? offsets[i64] : 0;
-  if (e1 > e0 && g.valid) {
-    double ci[3] = {v.centers[3 * i64], v.centers[3 * i64 + 1], v.centers[3 * i64 + 2]};
-    const float ri_f = v.sph.offr[i].w;
-    const uint32_t oi = v.sph.owner[i];
-    const uint8_t fi = v.sfam[i];
-    long long lo_i[3], hi_i[3];
-    sphere_range(g, ci, ri_f, v.margin, lo_i, hi_i);
-    for (unsigned long long e = e0; e < e1; ++e) {
-      const uint32_t j = cand[e].y;
-      if (ss_pair(v, g, i, j, ci, ri_f, lo_i, hi_i, oi, fi)) {
-        if (FILL) out[w + cnt] = make_uint2(i, j);
-        ++cnt;
-      }
-    }
-  }
-  if (!FILL) counts[i64] = cnt;
+  const uint2 p = cand[e];
+  const uint32_t i = p.x, j = p.y;
+  double ci[3] = {v.centers[3 * size_t(i)], v.centers[3 * size_t(i) + 1], v.centers[3 * size_t(i) + 2]};
+  const float ri_f = v.sph.offr[i].w;
+  long long lo_i[3], hi_i[3];
+  sphere_range(g, ci, ri_f, v.margin, lo_i, hi_i);
+  const bool hit = g.valid && ss_pair(v, g, i, j, ci, ri_f, lo_i, hi_i, v.sph.owner[i], v.sfam[i]);
+  flags[e] = hit ? 1 : 0;
+  if (hit) atomicAdd(&counts[i], 1ull);
 }
 
 __global__ void k_copy_ref(int64_t n3, const double *c, double *ref) {
@@ -1138,6 +1128,19 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
   if (ensure(c, k.cub_tmp, tmp + 16, s, false)) return -1;
   GF_CHECK(c, cub::DeviceScan::ExclusiveSum(k.cub_tmp.p, tmp, cc, k.cand_seg.as<unsigned long long>(),
                                             int(n + 1), s));
+  // a rebuild is rare: check the candidate total right away and grow on overflow
+  GF_CHECK(c, cudaMemcpyAsync(&reinterpret_cast<Status *>(c->h_status)->cand_total, cn, 8,
+                              cudaMemcpyDeviceToHost, s));
+  GF_CHECK(c, cudaStreamSynchronize(s));
+  const int64_t total = int64_t(reinterpret_cast<Status *>(c->h_status)->cand_total);
+  if (total > k.cand_cap) {
+    int64_t cap = total + total / 4 + 4096;
+    if (ensure(c, k.cand_tmp, sizeof(uint2) * cap, s) || ensure(c, k.cand, sizeof(uint2) * cap, s)) return -1;
+    k.cand_cap = cap;
+    return rebuild_candidates(c, s);
+  }
+  k.n_cand = total;
+  if (ensure(c, k.cflags, total + 16, s)) return -1;
   if (n) {
     GF_CHECK(c, cudaMemsetAsync(k.cursor.p, 0, 4 * n, s));
     k_place_cand<<<1184, 256, 0, s>>>(cn, k.cand_tmp.as<uint2>(), k.cand_seg.as<unsigned long long>(),
@@ -1146,8 +1149,6 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
     k_sort_seg<<<grid_for(n), kBlock, 0, s>>>(n, k.cand_seg.as<unsigned long long>(), k.cand.as<uint2>());
     k_copy_ref<<<grid_for(3 * n), kBlock, 0, s>>>(3 * n, k.centers.as<double>(), k.ref.as<double>());
   }
-  GF_CHECK(c, cudaMemcpyAsync(&reinterpret_cast<Status *>(c->h_status)->cand_total, cn, 8,
-                              cudaMemcpyDeviceToHost, s));
   k.cand_valid = true;
   k.cand_skin = c->skin_factor * c->kt_margin;
   k.rebuilds++;
@@ -1167,7 +1168,8 @@ int kt_count(Ctx *c, cudaStream_t s, bool force_rebuild) {
     if (rebuild_candidates(c, s)) return -1;
   }
   if (ensure(c, k.counts, sizeof(unsigned long long) * (3 * n + 1), s) ||
-      ensure(c, k.offsets, sizeof(unsigned long long) * (3 * n + 1), s) || ensure(c, k.tmp_n, 16, s))
+      ensure(c, k.offsets, sizeof(unsigned long long) * (3 * n + 1), s) || ensure(c, k.tmp_n, 16, s) ||
+      ensure(c, k.sel_n, 16, s))
     return -1;
   if (k.tmp_cap == 0) {
     int64_t cap = std::max<int64_t>(n, 4096);
@@ -1179,9 +1181,10 @@ int kt_count(Ctx *c, cudaStream_t s, bool force_rebuild) {
   unsigned long long *tn = k.tmp_n.as<unsigned long long>();
   GF_CHECK(c, cudaMemsetAsync(cnt + 3 * n, 0, sizeof(unsigned long long), s));
   GF_CHECK(c, cudaMemsetAsync(tn, 0, sizeof(unsigned long long), s));
+  GF_CHECK(c, cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * n, s));
+  if (k.n_cand)
+    k_filter_flags<<<grid_for(k.n_cand), 256, 0, s>>>(v, k.cand.as<uint2>(), k.n_cand, k.cflags.as<uint8_t>(), cnt);
   if (n) {
-    k_filter<false><<<grid_for(n, 128), 128, 0, s>>>(v, k.cand.as<uint2>(), k.cand_seg.as<unsigned long long>(),
-                                                      cnt, nullptr, nullptr);
     k_pairs_other<<<grid_for(n, 128), 128, 0, s>>>(v, cnt, k.tmp.as<uint2>(), tn, (unsigned long long)k.tmp_cap);
   }
   size_t tmp = 0;
@@ -1205,19 +1208,14 @@ int kt_detect_fill(Ctx *c, Acs &out, cudaStream_t s) {
   KtScratch &k = c->kt;
   const int64_t n = c->n_sph;
   Status *hs = reinterpret_cast<Status *>(c->h_status);
-  if ((int64_t)hs->cand_total > k.cand_cap || (int64_t)hs->other_total > k.tmp_cap) {
-    // a scratch list overflowed: grow and redo the detection synchronously
-    if ((int64_t)hs->cand_total > k.cand_cap) {
-      int64_t cap = int64_t(hs->cand_total) + int64_t(hs->cand_total) / 4 + 4096;
-      if (ensure(c, k.cand_tmp, sizeof(uint2) * cap, s) || ensure(c, k.cand, sizeof(uint2) * cap, s)) return -1;
-      k.cand_cap = cap;
-    }
-    if ((int64_t)hs->other_total > k.tmp_cap) {
+  if ((int64_t)hs->other_total > k.tmp_cap) {
+    // the sphere-triangle / sphere-analytic scratch list overflowed: grow, redo
+    {
       int64_t cap = int64_t(hs->other_total) + int64_t(hs->other_total) / 4 + 4096;
       if (ensure(c, k.tmp, sizeof(uint2) * cap, s)) return -1;
       k.tmp_cap = cap;
     }
-    if (kt_count(c, s, true)) return -1;
+    if (kt_count(c, s)) return -1;
     GF_CHECK(c, cudaStreamSynchronize(s));
     out.n = int64_t(hs->acs_total);
   }
@@ -1234,8 +1232,15 @@ int kt_detect_fill(Ctx *c, Acs &out, cudaStream_t s) {
   if (n && total) {
     KtView v = kt_view(c, c->kt_margin);
     const unsigned long long *off = k.offsets.as<unsigned long long>();
-    k_filter<true><<<grid_for(n, 128), 128, 0, s>>>(v, k.cand.as<uint2>(), k.cand_seg.as<unsigned long long>(),
-                                                     nullptr, off, out.ids.as<uint2>());
+    if (k.n_cand) {
+      size_t tmpb = 0;
+      cub::DeviceSelect::Flagged(nullptr, tmpb, k.cand.as<uint2>(), k.cflags.as<uint8_t>(), out.ids.as<uint2>(),
+                                 k.sel_n.as<unsigned long long>(), k.n_cand, s);
+      if (ensure(c, k.cub_tmp, tmpb + 16, s, false)) return -1;
+      GF_CHECK(c, cub::DeviceSelect::Flagged(k.cub_tmp.p, tmpb, k.cand.as<uint2>(), k.cflags.as<uint8_t>(),
+                                             out.ids.as<uint2>(), k.sel_n.as<unsigned long long>(), k.n_cand,
+                                             s));
+    }
     GF_CHECK(c, cudaMemsetAsync(k.cursor.p, 0, sizeof(unsigned) * 3 * n, s));
     k_place<<<1184, 256, 0, s>>>(k.tmp_n.as<unsigned long long>(), n, k.tmp.as<uint2>(), off,
                                  k.cursor.as<unsigned>(), out.ids.as<uint2>());
