@@ -294,7 +294,7 @@ void gf_destroy(gf_ctx *ctx) {
                   &c->av_mask, &c->lv_val, &c->av_val, &c->acs.ids, &c->acs.wild, &c->acs_next.ids,
                   &c->acs_next.wild, &c->out_c, &c->touch, &c->inc, &c->inc_alt, &c->inc_key,
                   &c->inc_key_alt, &c->inc_start, &c->heavy, &c->heavy_count, &c->heavy_acc,
-                  &c->cub_tmp_dt, &c->status, &c->dyn_spec, &c->dyn_vals, &c->kt.centers, &c->kt.sfam,
+                  &c->cub_tmp_dt, &c->status, &c->dyn_spec, &c->dyn_vals, &c->kt.centers, &c->kt.c4, &c->kt.sfam,
                   &c->kt.tri_world, &c->kt.ana_world, &c->kt.tfam, &c->kt.afam, &c->kt.grid,
                   &c->kt.minmax, &c->kt.bin_key, &c->kt.bin_key_alt, &c->kt.sph_val, &c->kt.sph_val_alt,
                   &c->kt.cell_start, &c->kt.cell_end, &c->kt.tri_ranges, &c->kt.tri_cnt,
@@ -563,6 +563,9 @@ int gf_upload_families(gf_ctx *ctx, const uint8_t *mask, const uint8_t *flags, c
       upload_raw(c, c->lv_val, lv_val, sizeof(double) * 768) ||
       upload_raw(c, c->av_val, av_val, sizeof(double) * 768))
     return -1;
+  c->mask_trivial = true;
+  for (int q = 0; q < 65536; ++q)
+    if (!mask[q]) { c->mask_trivial = false; break; }
   c->h_fam_flags.assign(flags, flags + 256);
   world_moving_update(c);
   return 0;
@@ -671,6 +674,17 @@ int gf_detect_snapshot(gf_ctx *ctx, int64_t m, const double *centers, const floa
       upload_raw(c, c->ana_kind, ana_kind, n_a) || upload_raw(c, k.ana_world, ana_world, 64 * n_a) ||
       upload_raw(c, k.afam, ana_family, n_a) || upload_raw(c, c->fam_mask, mask, 65536))
     return -1;
+  {
+    std::vector<double> c4(4 * m);
+    for (int64_t i = 0; i < m; ++i) {
+      c4[4 * i] = centers[3 * i]; c4[4 * i + 1] = centers[3 * i + 1]; c4[4 * i + 2] = centers[3 * i + 2];
+      c4[4 * i + 3] = double(radii[i]);
+    }
+    if (upload_raw(c, k.c4, c4.data(), 32 * m)) return -1;
+  }
+  c->mask_trivial = true;
+  for (int q = 0; q < 65536; ++q)
+    if (!mask[q]) { c->mask_trivial = false; break; }
   if (set_split(c, radii, 1, m)) return -1;
   c->kt.cand_valid = false;
   int rc = detect_now(c, margin, n_out);

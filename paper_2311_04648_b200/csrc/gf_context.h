@@ -32,6 +32,7 @@ struct Acs {
 struct KtScratch {
   // snapshot (kT works on a frozen copy; engine.py:577-596)
   DBuf centers;      // double[n_s*3]
+  DBuf c4;           // double4[n_s] (centre, radius)
   DBuf sfam;         // uint8[n_s] sphere family
   DBuf tri_world;    // double[n_t*9]
   DBuf ana_world;    // double[n_a*8]
@@ -95,6 +96,7 @@ struct Ctx {
   DBuf pair, beta;
   DBuf fam_mask, fam_flags, lv_mask, av_mask, lv_val, av_val;
   std::vector<uint8_t> h_fam_flags;
+  bool mask_trivial = true;  // every family pair may contact
   // contact arrays
   int wild_w = 4;
   Acs acs, acs_next;

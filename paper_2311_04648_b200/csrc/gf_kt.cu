@@ -65,19 +65,22 @@ struct KtView {
   const uint32_t *tri_start, *tri_entries;
   const Grid *grid;
   double margin;
+  const double4 *c4;   // snapshot (centre, radius) records
+  int mask_trivial;    // the family mask allows every pair
 };
 
 // ---------------------------------------------------------------------------
 // snapshot
 // ---------------------------------------------------------------------------
 // frozen copy of the refreshed sphere centres and families (engine.py:577-596)
-__global__ void k_snapshot(Domain dom, Owners own, Spheres sph, double *centers, uint8_t *sfam) {
+__global__ void k_snapshot(Domain dom, Owners own, Spheres sph, double *centers, double4 *c4, uint8_t *sfam) {
   int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (k >= sph.n) return;
   const double4 c = sph.center[k];
   centers[3 * k] = c.x;
   centers[3 * k + 1] = c.y;
   centers[3 * k + 2] = c.z;
+  c4[k] = c;
   sfam[k] = uint8_t(meta_family(own.meta[sph.owner[k]]));
 }
 
@@ -413,6 +416,28 @@ __device__ __forceinline__ void ss_resolve(const KtView &v, const Grid &g, const
     }
   }
   append_pair(hit, e, tmp, tmp_n, cap);
+}
+
+// the exact predicate without the owner / family checks (done elsewhere)
+__device__ __forceinline__ bool ss_pair_sorted_nomask(const KtView &v, const Grid &g, const double4 &cl,
+                                                      const uint4 &ml, const double4 &ch, const uint4 &mh) {
+  (void)ml; (void)mh;
+  double dx = sub_(cl.x, ch.x), dy = sub_(cl.y, ch.y), dz = sub_(cl.z, ch.z);
+  double ri = add(cl.w, v.margin);
+  double rj = add(ch.w, v.margin);
+  double rr = sub_(add(ri, rj), v.margin);
+  if (add(add(mul(dx, dx), mul(dy, dy)), mul(dz, dz)) >= mul(rr, rr)) return false;
+  double ci[3] = {cl.x, cl.y, cl.z}, cj[3] = {ch.x, ch.y, ch.z};
+  long long lo_i[3], hi_i[3], lo_j[3], hi_j[3];
+  sphere_range(g, ci, float(cl.w), v.margin, lo_i, hi_i);
+  sphere_range(g, cj, float(ch.w), v.margin, lo_j, hi_j);
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    double m = fmax(sub_(ci[ax], ri), sub_(cj[ax], rj));
+    long long b = axis_bin(m, g.glo[ax], g.inv_bin, g.nb[ax]);
+    if (b < lo_i[ax] || b > hi_i[ax] || b < lo_j[ax] || b > hi_j[ax]) return false;
+  }
+  return true;
 }
 
 // Sphere-sphere pairs among small spheres, one thread per cell-sorted sphere,
@@ -814,11 +839,19 @@ __global__ void __launch_bounds__(256) k_filter_flags(KtView v, const uint2 *can
   const Grid g = *v.grid;
   const uint2 p = cand[e];
   const uint32_t i = p.x, j = p.y;
-  double ci[3] = {v.centers[3 * size_t(i)], v.centers[3 * size_t(i) + 1], v.centers[3 * size_t(i) + 2]};
-  const float ri_f = v.sph.offr[i].w;
-  long long lo_i[3], hi_i[3];
-  sphere_range(g, ci, ri_f, v.margin, lo_i, hi_i);
-  const bool hit = g.valid && ss_pair(v, g, i, j, ci, ri_f, lo_i, hi_i, v.sph.owner[i], v.sfam[i]);
+  // candidates never pair clump-mates (excluded at the rebuild); the family
+  // mask is looked up only when it is not all-allow
+  const double4 ci4 = v.c4[i], cj4 = v.c4[j];
+  bool hit = g.valid;
+  if (hit && !v.mask_trivial) hit = v.mask[256 * v.sfam[i] + v.sfam[j]] != 0;
+  if (hit) {
+    const uint4 mi = make_uint4(i, 0u, 0u, 0u), mj = make_uint4(j, 1u, 0u, 0u);
+    const double4 cl = make_double4(ci4.x, ci4.y, ci4.z, double(float(ci4.w)));
+    const double4 ch = make_double4(cj4.x, cj4.y, cj4.z, double(float(cj4.w)));
+    KtView vv = v;
+    vv.mask_trivial = 1;
+    hit = ss_pair_sorted_nomask(vv, g, cl, mi, ch, mj);
+  }
   flags[e] = hit ? 1 : 0;
   if (hit) atomicAdd(&counts[i], 1ull);
 }
@@ -955,7 +988,9 @@ __global__ void k_inc_start(int64_t n_owner, int64_t n_inc, const uint32_t *sort
 
 int kt_snapshot(Ctx *c, cudaStream_t s) {
   KtScratch &k = c->kt;
-  if (ensure(c, k.centers, sizeof(double) * 3 * (c->n_sph + 1), s)) return -1;
+  if (ensure(c, k.centers, sizeof(double) * 3 * (c->n_sph + 1), s) ||
+      ensure(c, k.c4, sizeof(double4) * (c->n_sph + 1), s))
+    return -1;
   if (ensure(c, k.sfam, c->n_sph + 1, s)) return -1;
   if (ensure(c, k.tri_world, sizeof(double) * 9 * (c->n_tri + 1), s)) return -1;
   if (ensure(c, k.ana_world, sizeof(double) * 8 * (c->n_ana + 1), s)) return -1;
@@ -963,7 +998,8 @@ int kt_snapshot(Ctx *c, cudaStream_t s) {
   if (ensure(c, k.afam, c->n_ana + 1, s)) return -1;
   if (c->n_sph)
     k_snapshot<<<grid_for(c->n_sph), kBlock, 0, s>>>(c->dom, owners_view(c), spheres_view(c),
-                                                   k.centers.as<double>(), k.sfam.as<uint8_t>());
+                                                   k.centers.as<double>(), k.c4.as<double4>(),
+                                                   k.sfam.as<uint8_t>());
   if (c->n_tri) {
     GF_CHECK(c, cudaMemcpyAsync(k.tri_world.p, c->tri_world.p, sizeof(double) * 9 * c->n_tri,
                                 cudaMemcpyDeviceToDevice, s));
@@ -1006,6 +1042,8 @@ static KtView kt_view(Ctx *c, double margin) {
   v.tri_entries = k.tri_entries.as<uint32_t>();
   v.grid = k.grid.as<Grid>();
   v.margin = margin;
+  v.c4 = k.c4.as<double4>();
+  v.mask_trivial = c->mask_trivial ? 1 : 0;
   return v;
 }
 
