@@ -255,6 +255,35 @@ __global__ void k_tri_register(int64_t n_t, const double *tri, const Grid *gp, d
 // pair predicates (exact reference arithmetic)
 // ---------------------------------------------------------------------------
 
+// The reference reports a sphere pair that passed the distance test only if
+// the bin of the min corner mx of the two enlarged boxes' intersection lies in
+// both spheres' registration ranges (_kernels.py:317-321).  The lower ends
+// always hold (mx >= fl(c - r) and the bin map fl(fl(x - glo) * inv) with
+// truncation and clamping is monotone).  If the boxes overlap in the same
+// fp64 arithmetic, i.e. fl(c_j - r_j) <= fl(c_i + r_i) and
+// fl(c_i - r_i) <= fl(c_j + r_j) on every axis, then mx <= both upper box
+// ends and, by the same monotonicity, the upper ends hold too.  Only pairs
+// whose boxes do not overlap in fp64 (possible only for ties at zero margin)
+// need the full range evaluation.
+__device__ __forceinline__ bool bstar_in_ranges(const Grid &g, const double ci[3], double ri, float ri_f,
+                                                const double cj[3], double rj, float rj_f, double margin) {
+  bool overlap = true;
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax)
+    overlap = overlap && sub_(cj[ax], rj) <= add(ci[ax], ri) && sub_(ci[ax], ri) <= add(cj[ax], rj);
+  if (overlap) return true;
+  long long lo_i[3], hi_i[3], lo_j[3], hi_j[3];
+  sphere_range(g, ci, ri_f, margin, lo_i, hi_i);
+  sphere_range(g, cj, rj_f, margin, lo_j, hi_j);
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    double m = fmax(sub_(ci[ax], ri), sub_(cj[ax], rj));
+    long long b = axis_bin(m, g.glo[ax], g.inv_bin, g.nb[ax]);
+    if (b < lo_i[ax] || b > hi_i[ax] || b < lo_j[ax] || b > hi_j[ax]) return false;
+  }
+  return true;
+}
+
 // collect_sphere_pairs predicate (_kernels.py:305-321) for spheres i, j: the
 // distance test, then the reference's dedup bin (bin of the min corner of the
 // enlarged boxes' intersection) must lie in both registration ranges
@@ -271,16 +300,9 @@ __device__ __forceinline__ bool ss_pair(const KtView &v, const Grid &g, uint32_t
   double rj = add(double(rj_f), v.margin);
   double rr = sub_(add(ri, rj), v.margin);
   if (add(add(mul(dx, dx), mul(dy, dy)), mul(dz, dz)) >= mul(rr, rr)) return false;
+  (void)lo_i; (void)hi_i;
   double cjv[3] = {cj[0], cj[1], cj[2]};
-  long long lo_j[3], hi_j[3];
-  sphere_range(g, cjv, rj_f, v.margin, lo_j, hi_j);
-#pragma unroll
-  for (int ax = 0; ax < 3; ++ax) {
-    double m = fmax(sub_(ci[ax], ri), sub_(cj[ax], rj));
-    long long b = axis_bin(m, g.glo[ax], g.inv_bin, g.nb[ax]);
-    if (b < lo_i[ax] || b > hi_i[ax] || b < lo_j[ax] || b > hi_j[ax]) return false;
-  }
-  return true;
+  return bstar_in_ranges(g, ci, ri, ri_f, cjv, rj, rj_f, v.margin);
 }
 
 // collect_sphere_tri_pairs predicate (_kernels.py:375-401): distance test,
@@ -386,16 +408,7 @@ __device__ __forceinline__ bool ss_pair_sorted(const KtView &v, const Grid &g, c
   double rr = sub_(add(ri, rj), v.margin);
   if (add(add(mul(dx, dx), mul(dy, dy)), mul(dz, dz)) >= mul(rr, rr)) return false;
   double ci[3] = {cl.x, cl.y, cl.z}, cj[3] = {ch.x, ch.y, ch.z};
-  long long lo_i[3], hi_i[3], lo_j[3], hi_j[3];
-  sphere_range(g, ci, float(cl.w), v.margin, lo_i, hi_i);
-  sphere_range(g, cj, float(ch.w), v.margin, lo_j, hi_j);
-#pragma unroll
-  for (int ax = 0; ax < 3; ++ax) {
-    double m = fmax(sub_(ci[ax], ri), sub_(cj[ax], rj));
-    long long b = axis_bin(m, g.glo[ax], g.inv_bin, g.nb[ax]);
-    if (b < lo_i[ax] || b > hi_i[ax] || b < lo_j[ax] || b > hi_j[ax]) return false;
-  }
-  return true;
+  return bstar_in_ranges(g, ci, ri, float(cl.w), cj, rj, float(ch.w), v.margin);
 }
 
 // exact test of one queued candidate (sorted indices u0, u1) and its output
@@ -428,16 +441,7 @@ __device__ __forceinline__ bool ss_pair_sorted_nomask(const KtView &v, const Gri
   double rr = sub_(add(ri, rj), v.margin);
   if (add(add(mul(dx, dx), mul(dy, dy)), mul(dz, dz)) >= mul(rr, rr)) return false;
   double ci[3] = {cl.x, cl.y, cl.z}, cj[3] = {ch.x, ch.y, ch.z};
-  long long lo_i[3], hi_i[3], lo_j[3], hi_j[3];
-  sphere_range(g, ci, float(cl.w), v.margin, lo_i, hi_i);
-  sphere_range(g, cj, float(ch.w), v.margin, lo_j, hi_j);
-#pragma unroll
-  for (int ax = 0; ax < 3; ++ax) {
-    double m = fmax(sub_(ci[ax], ri), sub_(cj[ax], rj));
-    long long b = axis_bin(m, g.glo[ax], g.inv_bin, g.nb[ax]);
-    if (b < lo_i[ax] || b > hi_i[ax] || b < lo_j[ax] || b > hi_j[ax]) return false;
-  }
-  return true;
+  return bstar_in_ranges(g, ci, ri, float(cl.w), cj, rj, float(ch.w), v.margin);
 }
 
 // Sphere-sphere pairs among small spheres, one thread per cell-sorted sphere,
