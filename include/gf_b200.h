@@ -27,6 +27,10 @@
  *                                          (forces.py:360-440, engine.py:222-232)
  *   gf_run                                 the kT/dT worker protocol of do_dynamics
  *                                          (engine.py:512-526, 669-906)
+ *   gf_run_begin / gf_step_forces /        the same protocol one step at a time, split
+ *   gf_step_integrate / gf_run_end         between force and integration (engine.py:796-843)
+ *   gf_set_decomposition, gf_pack_*,       spatial slab decomposition (no reference
+ *   gf_unpack_state, gf_add_forces         counterpart: SURVEY.md 8(e))
  */
 #ifndef GF_B200_H
 #define GF_B200_H
@@ -185,9 +189,60 @@ typedef struct {
   double dt_ms, kt_ms;  /* device time of the dT and kT streams */
   double wall_ms;
   int64_t kt_rebuilds;  /* candidate-list rebuilds so far (Verlet skin exceeded) */
+  int64_t dd_trip_step; /* decomposition: first step a local owner moved more than `travel`
+                           along the slab axis (the run stops after it), or -1 */
 } gf_run_result;
 
 int gf_run(gf_ctx *ctx, const gf_run_params *p, gf_run_result *r);
+
+/* gf_run one step at a time: gf_run_begin, then for i in [0, n_steps)
+ * gf_step_forces(i) (kT schedule + contact forces) and gf_step_integrate(i)
+ * (prescriptions + integration), then gf_run_end.  gf_run is exactly this
+ * loop; the split lets a decomposed run exchange ghost forces between the
+ * halves and ghost state after the second.  Everything is queued on the dT
+ * stream (gf_stream) -- no host synchronisation between the calls. */
+int gf_run_begin(gf_ctx *ctx, const gf_run_params *p);
+int gf_step_forces(gf_ctx *ctx, int64_t i);
+int gf_step_integrate(gf_ctx *ctx, int64_t i);
+int gf_run_end(gf_ctx *ctx, gf_run_result *r);
+
+/* ---- spatial decomposition (needs GF_STATE_F32) -------------
+ * dd[o] = class | global_owner_id << 2 for every owner of this context:
+ * class 0 local (integrated here), 1 ghost (copy of another rank's owner,
+ * not integrated), 2 shared boundary owner replicated on every rank, 3 the
+ * same on the one rank that also computes shared-shared contacts.  A
+ * local-ghost contact is computed only by the rank owning the lower global
+ * id, so every physical contact is computed exactly once across ranks.
+ * lever_max = the global fixed-point torque lever (max sphere offset+radius
+ * / triangle vertex distance over ALL ranks' geometry), so every rank's
+ * fixed-point units agree.  axis / travel: the static ghost layer is valid
+ * while every local owner stays within `travel` of its current coordinate
+ * along `axis`; the first step that breaks it is reported in
+ * gf_run_result.dd_trip_step and the run stops after that (complete) step, so
+ * the host can repartition.  dd = NULL switches the decomposition off. */
+int gf_set_decomposition(gf_ctx *ctx, const uint32_t *dd, double lever_max, int axis, double travel);
+/* bytes of one packed owner-state record (64 for GF_STATE_F32) */
+int gf_halo_record_bytes(gf_ctx *ctx);
+/* the dT stream (a cudaStream_t) the halo calls are queued on, for a
+ * transport (NCCL) to order itself against */
+void *gf_stream(gf_ctx *ctx);
+/* DEVICE arrays: idx = uint32 owner indices of this context; out / in =
+ * n records.  pack_state gathers owner state (voxel, sub-voxel, quaternion,
+ * velocities) bit for bit; unpack_state scatters it into ghosts and refreshes
+ * their sphere centres; pack_forces gathers the 48-byte fixed-point force /
+ * torque accumulators of ghosts and clears them; add_forces adds returned
+ * accumulators into local owners (exact integer addition). */
+int gf_pack_state(gf_ctx *ctx, const uint32_t *idx, int64_t n, void *out);
+int gf_unpack_state(gf_ctx *ctx, const uint32_t *idx, int64_t n, const void *in);
+int gf_pack_forces(gf_ctx *ctx, const uint32_t *idx, int64_t n, void *out);
+int gf_add_forces(gf_ctx *ctx, const uint32_t *idx, int64_t n, const void *in);
+/* the guard's trip step and a DEVICE int64 word (INT64_MAX = none): mode 0
+ * writes this context's trip step into *word, mode 1 lowers it to *word.
+ * A transport min-reduces the word across ranks between the two (every rank
+ * then skips the same steps). */
+int gf_trip_word(gf_ctx *ctx, void *word, int mode);
+/* block until the context's dT stream is idle */
+int gf_sync(gf_ctx *ctx);
 
 /* per-kernel device timing of subsequent gf_run calls (CUDA events on the dT
  * stream); out5 = cumulative ms of {k_contacts, k_heavy, k_integrate, kT},

@@ -46,7 +46,7 @@ class RunResult(C.Structure):
     _fields_ = [("steps_done", _I64), ("bad_owner", _I64), ("bad_step", _I64),
                 ("oob_owner", _I64), ("oob_step", _I64), ("touching", _I64), ("n_acs", _I64),
                 ("ca_updates", _I64), ("sum_acs", _I64), ("sum_touch_pairs", _I64), ("dt_ms", _D),
-                ("kt_ms", _D), ("wall_ms", _D), ("kt_rebuilds", _I64)]
+                ("kt_ms", _D), ("wall_ms", _D), ("kt_rebuilds", _I64), ("dd_trip_step", _I64)]
 
 
 # every symbol include/gf_b200.h declares
@@ -57,7 +57,9 @@ EXPORTS = (
     "gf_upload_families", "gf_download_world", "gf_set_acs", "gf_acs_size", "gf_get_acs",
     "gf_detect", "gf_detect_snapshot", "gf_bin_ranges", "gf_adopt", "gf_dt_step", "gf_run",
     "gf_merge_history", "gf_set_profiling", "gf_kernel_times", "gf_set_force_model",
-    "gf_nvrtc_compile",
+    "gf_nvrtc_compile", "gf_run_begin", "gf_step_forces", "gf_step_integrate", "gf_run_end",
+    "gf_set_decomposition", "gf_halo_record_bytes", "gf_stream", "gf_pack_state", "gf_unpack_state",
+    "gf_pack_forces", "gf_add_forces", "gf_trip_word", "gf_sync",
 )
 
 _lib = None
@@ -84,9 +86,17 @@ def load_library():
     L.gf_destroy.argtypes = [_P]
     L.gf_acs_size.restype = _I64
     L.gf_acs_size.argtypes = [_P, C.c_int]
+    L.gf_stream.restype = _P
+    L.gf_stream.argtypes = [_P]
+    L.gf_step_forces.argtypes = [_P, _I64]
+    L.gf_step_integrate.argtypes = [_P, _I64]
+    L.gf_set_decomposition.argtypes = [_P, _P, _D, C.c_int, _D]
+    L.gf_trip_word.argtypes = [_P, _P, C.c_int]
+    for name in ("gf_pack_state", "gf_unpack_state", "gf_pack_forces", "gf_add_forces"):
+        getattr(L, name).argtypes = [_P, _P, _I64, _P]
     for name in EXPORTS:
         fn = getattr(L, name)
-        if name not in ("gf_create", "gf_destroy", "gf_acs_size"):
+        if name not in ("gf_create", "gf_destroy", "gf_acs_size", "gf_stream"):
             fn.restype = C.c_int
     _lib = L
     return L

@@ -58,7 +58,36 @@ struct Owners {
   double *ext;         // [n*6] external force/torque or nullptr
   long long *facc;     // [n*6] fixed-point accumulators (throughput build), zeroed by the integrator
   double2 *tpl_scale;  // per template: fixed-point scale of force, torque
+  const uint32_t *dd;  // spatial decomposition: class (bits 0-1) | global owner id << 2, or nullptr
+  const double *dd_x0; // partition-time coordinate of each owner along the slab axis
+  double dd_travel;    // allowed displacement along the axis before a repartition
+  int dd_axis;
 };
+
+// Spatial decomposition (slab partition across ranks).  Every owner of a
+// rank-local context is one of
+//   kDdLocal   integrated here; its state is the truth
+//   kDdGhost   a copy of an owner integrated on another rank (halo)
+//   kDdShared  a boundary owner (mesh / analytic) replicated on every rank
+//   kDdPrimary the same, on the one rank that also computes shared-shared pairs
+// Each physical contact is computed on exactly one rank: ghost-ghost and
+// ghost-shared pairs never (the ghost's home rank has them), local-ghost
+// pairs only on the rank owning the lower global owner id.  Integer
+// (fixed-point) force contributions of ghosts are returned to their home rank,
+// so a decomposed run sums exactly the terms a single context sums.
+enum : uint32_t { kDdLocal = 0, kDdGhost = 1, kDdShared = 2, kDdPrimary = 3 };
+
+__host__ __device__ inline bool dd_keep(const uint32_t *dd, uint32_t oa, uint32_t ob) {
+  if (!dd) return true;
+  const uint32_t a = dd[oa], b = dd[ob], ca = a & 3u, cb = b & 3u;
+  if (ca == kDdGhost || cb == kDdGhost) {
+    if (ca == kDdLocal) return (a >> 2) < (b >> 2);
+    if (cb == kDdLocal) return (b >> 2) < (a >> 2);
+    return false;
+  }
+  if (ca == kDdLocal || cb == kDdLocal) return true;
+  return ca == kDdPrimary && cb == kDdPrimary;
+}
 
 struct Spheres {
   int64_t n;
@@ -113,6 +142,8 @@ struct Status {
   double oob_pos[3];
   int err;                   // nonzero once a watchdog tripped (kernels stop)
   int rebuild;               // detection phase A: candidate lists must be rebuilt
+  unsigned long long dd_trip;  // first step a local owner exceeded the decomposition travel, or ~0;
+                               // later steps are skipped (that step itself completes)
 };
 
 __host__ __device__ inline uint32_t meta_family(uint32_t m) { return m >> 24; }

@@ -68,6 +68,10 @@ Owners owners_view(Ctx *c) {
   o.ext = c->has_ext ? c->ext.as<double>() : nullptr;
   o.facc = c->fixed_reduce ? c->facc.as<long long>() : nullptr;
   o.tpl_scale = c->tpl_scale.as<double2>();
+  o.dd = c->dd_on ? c->dd.as<uint32_t>() : nullptr;
+  o.dd_x0 = c->dd_x0.as<double>();
+  o.dd_travel = c->dd_travel;
+  o.dd_axis = c->dd_axis;
   return o;
 }
 Spheres spheres_view(Ctx *c) {
@@ -88,6 +92,11 @@ Materials materials_view(Ctx *c) {
 Families families_view(Ctx *c) {
   return Families{c->fam_mask.as<uint8_t>(), c->fam_flags.as<uint8_t>(), c->lv_mask.as<uint8_t>(),
                   c->av_mask.as<uint8_t>(), c->lv_val.as<double>(), c->av_val.as<double>()};
+}
+
+cudaEvent_t *prof_current(Ctx *c) {
+  if (!c->prof || c->prof_used < 4) return nullptr;
+  return &c->prof_ev[c->prof_used - 4];
 }
 
 cudaEvent_t *prof_events(Ctx *c) {
@@ -130,7 +139,7 @@ static int update_fixed_scales(Ctx *c, double h, double v_err, const double *g) 
   for (double m : c->h_tpl_mass)
     if (m < 1e13 && m > m_clump_max) m_clump_max = m;
   if (m_clump_max <= 0.0) m_clump_max = 1.0;
-  const double lever = c->lever_max > 0.0 ? c->lever_max : 1.0;
+  const double lever = c->lever_override > 0.0 ? c->lever_override : (c->lever_max > 0.0 ? c->lever_max : 1.0);
   std::vector<double> sc(2 * (c->h_tpl_mass.size() + 1), 1.0);
   for (size_t t = 0; t < c->h_tpl_mass.size(); ++t) {
     double m = c->h_tpl_mass[t];
@@ -155,12 +164,75 @@ static int dt_step(Ctx *c, const StepArgs &a) {
   return c->f32_state ? dt_step_f32(c, a, c->s_dt) : dt_step_f64(c, a, c->s_dt);
 }
 
+// state of one gf_run call (gf_run_begin .. gf_run_end)
+struct RunState {
+  gf_run_params p{};
+  int period = 1, lag = 0;
+  int64_t sum_acs = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kt_ev;   // per-detection kT timing
+  std::chrono::steady_clock::time_point w0;
+};
+
+static void free_run(Ctx *c) {
+  if (!c->run) return;
+  for (auto &e : c->run->kt_ev) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  delete c->run;
+  c->run = nullptr;
+}
+
+static int fail_run(Ctx *c) {
+  free_run(c);
+  return -1;
+}
+
+static StepArgs step_args(const RunState *R, int64_t i) {
+  const gf_run_params *p = &R->p;
+  const int64_t s = p->step0 + i;
+  return StepArgs{p->h, {p->g[0], p->g[1], p->g[2]}, p->v_err, double(s) * p->h, s, i,
+                  (i == p->n_steps - 1) ? p->write_acc : 0};
+}
+
+// kT phases: begun (grid + displacement check queued) -> counted (candidate
+// filter + counts queued) -> filled (canonical array queued)
+static int run_count(Ctx *c) {
+  GF_CHECK(c, cudaEventSynchronize(c->ev_disp));
+  if (kt_count(c, c->s_kt)) return -1;
+  GF_CHECK(c, cudaEventRecord(c->ev_count, c->s_kt));
+  c->kt_phase = 2;
+  return 0;
+}
+
+static int run_fill(Ctx *c) {
+  if (c->kt_phase == 1 && run_count(c)) return -1;
+  GF_CHECK(c, cudaEventSynchronize(c->ev_count));
+  c->acs_next.n = int64_t(reinterpret_cast<Status *>(c->h_status)->acs_total);
+  if (kt_detect_fill(c, c->acs_next, c->s_kt)) return -1;
+  if (c->run && !c->run->kt_ev.empty()) GF_CHECK(c, cudaEventRecord(c->run->kt_ev.back().second, c->s_kt));
+  GF_CHECK(c, cudaEventRecord(c->ev_ca, c->s_kt));
+  c->fill_done = true;
+  return 0;
+}
+
+static int run_adopt(Ctx *c) {
+  if (!c->fill_done && run_fill(c)) return -1;
+  GF_CHECK(c, cudaStreamWaitEvent(c->s_dt, c->ev_ca, 0));
+  if (adopt_acs(c, c->s_dt)) return -1;
+  GF_CHECK(c, cudaEventRecord(c->ev_adopted, c->s_dt));
+  c->next_pending = false;
+  c->first_adopt = false;
+  return 0;
+}
+
 static int reset_status(Ctx *c, cudaStream_t s) {
   Status *st = c->status.as<Status>();
   GF_CHECK(c, cudaMemsetAsync(st, 0xFF, 2 * sizeof(unsigned long long), s));
   GF_CHECK(c, cudaMemsetAsync(&st->touching, 0, sizeof(unsigned long long), s));
   GF_CHECK(c, cudaMemsetAsync(&st->touch_pairs, 0, sizeof(unsigned long long), s));
   GF_CHECK(c, cudaMemsetAsync(&st->err, 0, sizeof(int), s));
+  GF_CHECK(c, cudaMemsetAsync(&st->dd_trip, 0xFF, sizeof(unsigned long long), s));
   return 0;
 }
 
@@ -301,8 +373,9 @@ void gf_destroy(gf_ctx *ctx) {
                   &c->kt.tri_start, &c->kt.tri_entries, &c->kt.counts, &c->kt.offsets, &c->kt.cub_tmp,
                   &c->kt.total, &c->kt.cursor, &c->kt.tri_cursor, &c->big_slots, &c->kt.sc,
                   &c->kt.sm, &c->kt.sf, &c->kt.cells, &c->kt.n_cells, &c->kt.cand, &c->kt.cand_tmp, &c->kt.cand_n,
-                  &c->kt.cand_cnt, &c->kt.cand_seg, &c->kt.ref, &c->kt.flag, &c->kt.cflags, &c->kt.sel_n, &c->kt.tmp, &c->kt.tmp_n, &c->acs.seg, &c->acs_next.seg};
+                  &c->kt.cand_cnt, &c->kt.cand_seg, &c->kt.ref, &c->kt.flag, &c->kt.cflags, &c->kt.sel_n, &c->kt.tmp, &c->kt.tmp_n, &c->acs.seg, &c->acs_next.seg, &c->dd, &c->dd_x0, &c->halo_scratch};
   for (DBuf *b : bufs) release(*b);
+  free_run(c);
   if (c->h_status) cudaFreeHost(c->h_status);
   cudaEvent_t evs[] = {c->ev_snap, c->ev_ca, c->ev_adopted, c->ev_count, c->ev_disp, c->t0, c->t1};
   for (auto e : evs) cudaEventDestroy(e);
@@ -780,112 +853,115 @@ int gf_dt_step(gf_ctx *ctx, const gf_step_params *p, int64_t *touching, int64_t 
   return 0;
 }
 
-int gf_run(gf_ctx *ctx, const gf_run_params *p, gf_run_result *r) {
+// One gf_run call: the deterministic kT/dT schedule over n_steps.  Split into
+// begin / per-step forces / per-step integrate / end so a decomposed run can
+// exchange ghost forces and ghost state between the halves (gf_run is the
+// plain loop over them).
+int gf_run_begin(gf_ctx *ctx, const gf_run_params *p) {
   CTX_CHECK(ctx);
-  auto w0 = std::chrono::steady_clock::now();
-  std::memset(r, 0, sizeof(*r));
+  if (c->run) { c->err = "a run is already in progress (gf_run_end missing)"; return -1; }
+  RunState *R = new RunState();
+  R->w0 = std::chrono::steady_clock::now();
+  R->p = *p;
+  R->period = p->period < 1 ? 1 : p->period;
+  R->lag = p->lag < 0 ? 0 : p->lag;
+  c->run = R;
   const int64_t N = p->n_steps;
-  const int period = p->period < 1 ? 1 : p->period;
-  const int lag = p->lag < 0 ? 0 : p->lag;
   c->kt_margin = p->margin;
   c->n_dyn = p->n_dyn;
   if (p->n_dyn > 0) {
     if (upload_raw(c, c->dyn_spec, p->dyn_spec, sizeof(int32_t) * 3 * p->n_dyn) ||
         upload_raw(c, c->dyn_vals, p->dyn_vals, sizeof(double) * p->n_dyn * (N > 0 ? N : 1)))
+      return fail_run(c);
+  }
+  if (reset_status(c, c->s_dt)) return fail_run(c);
+  if (cudaStreamSynchronize(c->s_dt) != cudaSuccess || cudaEventRecord(c->t0, c->s_dt) != cudaSuccess) {
+    c->err = cudaGetErrorString(cudaGetLastError());
+    return fail_run(c);
+  }
+  return 0;
+}
+
+int gf_step_forces(gf_ctx *ctx, int64_t i) {
+  CTX_CHECK(ctx);
+  RunState *R = c->run;
+  if (!R) { c->err = "gf_step_forces outside gf_run_begin / gf_run_end"; return -1; }
+  const gf_run_params *p = &R->p;
+  const int64_t s = p->step0 + i;
+  // 1. a detection due at this step boundary is adopted first
+  if (c->next_pending && s >= c->adopt_at && run_adopt(c)) return -1;
+  // 2. work order: snapshot on the dT stream, detection on the kT stream
+  if (!c->next_pending && (c->first_adopt || s - c->last_snap >= R->period)) {
+    if (kt_snapshot(c, c->s_dt)) return -1;
+    GF_CHECK(c, cudaEventRecord(c->ev_snap, c->s_dt));
+    GF_CHECK(c, cudaStreamWaitEvent(c->s_kt, c->ev_snap, 0));
+    GF_CHECK(c, cudaStreamWaitEvent(c->s_kt, c->ev_adopted, 0));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    R->kt_ev.emplace_back(e0, e1);
+    GF_CHECK(c, cudaEventRecord(e0, c->s_kt));
+    if (kt_begin(c, p->margin, c->s_kt)) return -1;
+    GF_CHECK(c, cudaEventRecord(c->ev_disp, c->s_kt));
+    c->kt_phase = 1;
+    c->next_pending = true;
+    c->fill_done = false;
+    c->last_snap = s;
+    // the very first detection is waited for (engine.py:679-682)
+    c->adopt_at = c->first_adopt ? s : s + R->lag;
+    if (c->adopt_at <= s && run_adopt(c)) return -1;
+  }
+  // 3. launch the fill as soon as the count is known (no dT stall)
+  if (c->next_pending && !c->fill_done && c->kt_phase == 2) {
+    cudaError_t q = cudaEventQuery(c->ev_count);
+    if (q == cudaErrorNotReady) {
+      if (cudaPeekAtLastError() == cudaErrorNotReady) (void)cudaGetLastError();
+    } else if (run_fill(c)) {
       return -1;
-  }
-  if (reset_status(c, c->s_dt)) return -1;
-  GF_CHECK(c, cudaStreamSynchronize(c->s_dt));
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kt_ev;
-  GF_CHECK(c, cudaEventRecord(c->t0, c->s_dt));
-  // kT phases: begun (grid + displacement check queued) -> counted (candidate
-  // filter + counts queued) -> filled (canonical array queued)
-  auto do_count = [&]() -> int {
-    GF_CHECK(c, cudaEventSynchronize(c->ev_disp));
-    if (kt_count(c, c->s_kt)) return -1;
-    GF_CHECK(c, cudaEventRecord(c->ev_count, c->s_kt));
-    c->kt_phase = 2;
-    return 0;
-  };
-  auto do_fill = [&]() -> int {
-    if (c->kt_phase == 1 && do_count()) return -1;
-    GF_CHECK(c, cudaEventSynchronize(c->ev_count));
-    c->acs_next.n = int64_t(reinterpret_cast<Status *>(c->h_status)->acs_total);
-    if (kt_detect_fill(c, c->acs_next, c->s_kt)) return -1;
-    if (!kt_ev.empty()) GF_CHECK(c, cudaEventRecord(kt_ev.back().second, c->s_kt));
-    GF_CHECK(c, cudaEventRecord(c->ev_ca, c->s_kt));
-    c->fill_done = true;
-    return 0;
-  };
-  auto do_adopt = [&]() -> int {
-    if (!c->fill_done && do_fill()) return -1;
-    GF_CHECK(c, cudaStreamWaitEvent(c->s_dt, c->ev_ca, 0));
-    if (adopt_acs(c, c->s_dt)) return -1;
-    GF_CHECK(c, cudaEventRecord(c->ev_adopted, c->s_dt));
-    c->next_pending = false;
-    c->first_adopt = false;
-    return 0;
-  };
-  int64_t sum_acs = 0;
-  for (int64_t i = 0; i < N; ++i) {
-    const int64_t s = p->step0 + i;
-    // 1. a detection due at this step boundary is adopted first
-    if (c->next_pending && s >= c->adopt_at && do_adopt()) return -1;
-    // 2. work order: snapshot on the dT stream, detection on the kT stream
-    if (!c->next_pending && (c->first_adopt || s - c->last_snap >= period)) {
-      if (kt_snapshot(c, c->s_dt)) return -1;
-      GF_CHECK(c, cudaEventRecord(c->ev_snap, c->s_dt));
-      GF_CHECK(c, cudaStreamWaitEvent(c->s_kt, c->ev_snap, 0));
-      GF_CHECK(c, cudaStreamWaitEvent(c->s_kt, c->ev_adopted, 0));
-      cudaEvent_t e0, e1;
-      cudaEventCreate(&e0);
-      cudaEventCreate(&e1);
-      kt_ev.emplace_back(e0, e1);
-      GF_CHECK(c, cudaEventRecord(e0, c->s_kt));
-      if (kt_begin(c, p->margin, c->s_kt)) return -1;
-      GF_CHECK(c, cudaEventRecord(c->ev_disp, c->s_kt));
-      c->kt_phase = 1;
-      c->next_pending = true;
-      c->fill_done = false;
-      c->last_snap = s;
-      // the very first detection is waited for (engine.py:679-682)
-      c->adopt_at = c->first_adopt ? s : s + lag;
-      if (c->adopt_at <= s && do_adopt()) return -1;
     }
-    // 3. launch the fill as soon as the count is known (no dT stall)
-    if (c->next_pending && !c->fill_done && c->kt_phase == 2) {
-      cudaError_t q = cudaEventQuery(c->ev_count);
-      if (q == cudaErrorNotReady) {
-        if (cudaPeekAtLastError() == cudaErrorNotReady) (void)cudaGetLastError();
-      } else if (do_fill()) {
-        return -1;
-      }
-    }
-    sum_acs += c->acs.n;
-    StepArgs a{p->h, {p->g[0], p->g[1], p->g[2]}, p->v_err, double(s) * p->h, s, i,
-               (i == N - 1) ? p->write_acc : 0};
-    if (dt_step(c, a)) return -1;
-    // the detection's candidate filter is queued once the dT step is in flight
-    if (c->next_pending && c->kt_phase == 1 && do_count()) return -1;
   }
+  R->sum_acs += c->acs.n;
+  const StepArgs a = step_args(R, i);
+  if (update_fixed_scales(c, a.h, a.v_err, a.g)) return -1;
+  return c->f32_state ? dt_forces_f32(c, a, c->s_dt) : dt_forces_f64(c, a, c->s_dt);
+}
+
+int gf_step_integrate(gf_ctx *ctx, int64_t i) {
+  CTX_CHECK(ctx);
+  RunState *R = c->run;
+  if (!R) { c->err = "gf_step_integrate outside gf_run_begin / gf_run_end"; return -1; }
+  const StepArgs a = step_args(R, i);
+  if (c->f32_state ? dt_integrate_f32(c, a, c->s_dt) : dt_integrate_f64(c, a, c->s_dt)) return -1;
+  // the detection's candidate filter is queued once the dT step is in flight
+  if (c->next_pending && c->kt_phase == 1 && run_count(c)) return -1;
+  return 0;
+}
+
+int gf_run_end(gf_ctx *ctx, gf_run_result *r) {
+  CTX_CHECK(ctx);
+  RunState *R = c->run;
+  if (!R) { c->err = "gf_run_end without gf_run_begin"; return -1; }
+  std::memset(r, 0, sizeof(*r));
+  const gf_run_params *p = &R->p;
+  const int64_t N = p->n_steps;
   // finish enqueuing an in-flight detection (its fill) inside this call
-  if (c->next_pending && !c->fill_done && do_fill()) return -1;
+  if (c->next_pending && !c->fill_done && run_fill(c)) return fail_run(c);
   // join the kT stream so in-flight detection work counts in the timed window
-  GF_CHECK(c, cudaEventRecord(c->ev_snap, c->s_kt));
-  GF_CHECK(c, cudaStreamWaitEvent(c->s_dt, c->ev_snap, 0));
-  GF_CHECK(c, cudaEventRecord(c->t1, c->s_dt));
-  GF_CHECK(c, cudaStreamSynchronize(c->s_kt));
+  if (cudaEventRecord(c->ev_snap, c->s_kt) != cudaSuccess ||
+      cudaStreamWaitEvent(c->s_dt, c->ev_snap, 0) != cudaSuccess ||
+      cudaEventRecord(c->t1, c->s_dt) != cudaSuccess || cudaStreamSynchronize(c->s_kt) != cudaSuccess) {
+    c->err = cudaGetErrorString(cudaGetLastError());
+    return fail_run(c);
+  }
   Status st;
-  if (read_status(c, c->s_dt, &st)) return -1;
+  if (read_status(c, c->s_dt, &st)) return fail_run(c);
   float ms = 0.f;
   cudaEventElapsedTime(&ms, c->t0, c->t1);
   r->dt_ms = ms;
   double kt_ms = 0.0;
-  for (auto &e : kt_ev) {
+  for (auto &e : R->kt_ev) {
     float m = 0.f;
     if (cudaEventElapsedTime(&m, e.first, e.second) == cudaSuccess) kt_ms += m;
-    cudaEventDestroy(e.first);
-    cudaEventDestroy(e.second);
   }
   (void)cudaGetLastError();  // an unrecorded timing event is not an error
   r->kt_ms = kt_ms;
@@ -899,13 +975,97 @@ int gf_run(gf_ctx *ctx, const gf_run_params *p, gf_run_result *r) {
   if (r->bad_step >= 0) err_step = r->bad_step;
   if (r->oob_step >= 0 && (err_step < 0 || r->oob_step < err_step)) err_step = r->oob_step;
   r->steps_done = err_step >= 0 ? err_step - p->step0 : N;
+  r->dd_trip_step = st.dd_trip == ~0ull ? -1 : int64_t(st.dd_trip);
+  if (r->dd_trip_step >= 0 && r->dd_trip_step + 1 - p->step0 < r->steps_done)
+    r->steps_done = r->dd_trip_step + 1 - p->step0;
   r->touching = int64_t(st.touching);
   r->sum_touch_pairs = int64_t(st.touch_pairs);
-  r->sum_acs = sum_acs;
+  r->sum_acs = R->sum_acs;
   r->n_acs = c->acs.n;
   r->ca_updates = c->ca_updates;
-  r->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
+  r->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - R->w0).count();
   r->kt_rebuilds = c->kt.rebuilds;
+  free_run(c);
+  return 0;
+}
+
+int gf_run(gf_ctx *ctx, const gf_run_params *p, gf_run_result *r) {
+  if (gf_run_begin(ctx, p)) return -1;
+  for (int64_t i = 0; i < p->n_steps; ++i)
+    if (gf_step_forces(ctx, i) || gf_step_integrate(ctx, i)) {
+      free_run(&ctx->c);
+      return -1;
+    }
+  return gf_run_end(ctx, r);
+}
+
+// ---------------------------------------------------------------------------
+// spatial decomposition (gf_halo.cu)
+// ---------------------------------------------------------------------------
+int gf_set_decomposition(gf_ctx *ctx, const uint32_t *dd, double lever_max, int axis, double travel) {
+  CTX_CHECK(ctx);
+  if (!dd) {
+    c->dd_on = false;
+    c->lever_override = 0.0;
+  } else {
+    if (!c->fixed_reduce) {
+      c->err = "spatial decomposition needs the fixed-point owner reduction (GF_STATE_F32)";
+      return -1;
+    }
+    if (ensure(c, c->dd, 4 * (c->n_owner + 1), c->s_dt)) return -1;
+    if (axis < 0 || axis > 2) { c->err = "decomposition axis must be 0, 1 or 2"; return -1; }
+    GF_CHECK(c, cudaMemcpy(c->dd.p, dd, 4 * c->n_owner, cudaMemcpyHostToDevice));
+    // partition-time axis coordinate of every owner (device-side decode)
+    if (ensure(c, c->dd_x0, 8 * (c->n_owner + 1), c->s_dt)) return -1;
+    if (halo_axis_coords(c, axis, c->dd_x0.as<double>(), c->s_dt)) return -1;
+    GF_CHECK(c, cudaStreamSynchronize(c->s_dt));
+    c->dd_axis = axis;
+    c->dd_travel = travel;
+    c->dd_on = true;
+    c->lever_override = lever_max;
+  }
+  c->fx_h = -1.0;              // fixed-point scales follow the (global) lever arm
+  c->kt.cand_valid = false;    // candidate lists were filtered with the old classes
+  return 0;
+}
+
+int gf_halo_record_bytes(gf_ctx *ctx) {
+  if (!ctx) return -1;
+  return halo_record_bytes(&ctx->c);
+}
+
+void *gf_stream(gf_ctx *ctx) { return ctx ? reinterpret_cast<void *>(ctx->c.s_dt) : nullptr; }
+
+int gf_pack_state(gf_ctx *ctx, const uint32_t *idx, int64_t n, void *out) {
+  CTX_CHECK(ctx);
+  return halo_pack_state(c, idx, n, out, c->s_dt);
+}
+
+int gf_unpack_state(gf_ctx *ctx, const uint32_t *idx, int64_t n, const void *in) {
+  CTX_CHECK(ctx);
+  return halo_unpack_state(c, idx, n, in, c->s_dt);
+}
+
+int gf_pack_forces(gf_ctx *ctx, const uint32_t *idx, int64_t n, void *out) {
+  CTX_CHECK(ctx);
+  if (!c->fixed_reduce) { c->err = "gf_pack_forces needs the fixed-point owner reduction"; return -1; }
+  return halo_pack_forces(c, idx, n, out, c->s_dt);
+}
+
+int gf_add_forces(gf_ctx *ctx, const uint32_t *idx, int64_t n, const void *in) {
+  CTX_CHECK(ctx);
+  if (!c->fixed_reduce) { c->err = "gf_add_forces needs the fixed-point owner reduction"; return -1; }
+  return halo_add_forces(c, idx, n, in, c->s_dt);
+}
+
+int gf_trip_word(gf_ctx *ctx, void *word, int mode) {
+  CTX_CHECK(ctx);
+  return halo_trip_word(c, word, mode, c->s_dt);
+}
+
+int gf_sync(gf_ctx *ctx) {
+  CTX_CHECK(ctx);
+  GF_CHECK(c, cudaStreamSynchronize(c->s_dt));
   return 0;
 }
 

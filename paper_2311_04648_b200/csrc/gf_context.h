@@ -140,10 +140,21 @@ struct Ctx {
   size_t prof_used = 0;
   double prof_ms[4] = {0, 0, 0, 0};   // contacts, heavy, integrate, kT
   int64_t prof_steps = 0;
+  // spatial decomposition (gf_set_decomposition): per-owner class | gid << 2
+  DBuf dd, dd_x0;
+  bool dd_on = false;
+  int dd_axis = 0;
+  double dd_travel = 0.0;
+  double lever_override = 0.0;   // global lever arm so fixed-point scales agree across ranks
+  DBuf halo_scratch;             // uint32 index staging for host-index halo calls
+  // split-step run in progress (gf_run_begin ... gf_run_end)
+  struct RunState *run = nullptr;
 };
 
 // take 4 timing events for one profiled dT step (nullptr when off)
 cudaEvent_t *prof_events(Ctx *c);
+// the set the current step's force phase opened (nullptr when off)
+cudaEvent_t *prof_current(Ctx *c);
 
 constexpr uint32_t kHeavyThreshold = 192;
 constexpr int64_t kMaxCells = (int64_t(1) << 24) - 1;  // enumeration-grid cell cap; key 2^24-1 = unregistered  // incidences above which an owner is block-reduced
@@ -196,6 +207,18 @@ struct StepArgs {
   int write_acc;         // store per-owner accumulators this step
 };
 int dt_step_f64(Ctx *c, const StepArgs &a, cudaStream_t s);
+// halo exchange of the spatial decomposition (gf_halo.cu)
+int halo_record_bytes(const Ctx *c);
+int halo_axis_coords(Ctx *c, int axis, double *out, cudaStream_t s);
+int halo_trip_word(Ctx *c, void *word, int mode, cudaStream_t s);
+int halo_pack_state(Ctx *c, const uint32_t *idx, int64_t n, void *out, cudaStream_t s);
+int halo_unpack_state(Ctx *c, const uint32_t *idx, int64_t n, const void *in, cudaStream_t s);
+int halo_pack_forces(Ctx *c, const uint32_t *idx, int64_t n, void *out, cudaStream_t s);
+int halo_add_forces(Ctx *c, const uint32_t *idx, int64_t n, const void *in, cudaStream_t s);
+int dt_forces_f32(Ctx *c, const StepArgs &a, cudaStream_t s);
+int dt_integrate_f32(Ctx *c, const StepArgs &a, cudaStream_t s);
+int dt_forces_f64(Ctx *c, const StepArgs &a, cudaStream_t s);
+int dt_integrate_f64(Ctx *c, const StepArgs &a, cudaStream_t s);
 int dt_step_f32(Ctx *c, const StepArgs &a, cudaStream_t s);
 
 }  // namespace gf

@@ -3,6 +3,8 @@
 #include "gf_dt_impl.cuh"
 namespace gf {
 int dt_step_f64(Ctx *c, const StepArgs &a, cudaStream_t s) { return dt_step_impl<double>(c, a, s); }
+int dt_forces_f64(Ctx *c, const StepArgs &a, cudaStream_t s) { return dt_forces_impl<double>(c, a, s); }
+int dt_integrate_f64(Ctx *c, const StepArgs &a, cudaStream_t s) { return dt_integrate_impl<double>(c, a, s); }
 }  // namespace gf
 
 namespace gf {

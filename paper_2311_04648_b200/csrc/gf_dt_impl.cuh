@@ -31,11 +31,12 @@ namespace {
 // Touching entries are compacted into tlist (warp-aggregated append); the
 // fp64 parity build also records a touch flag per entry for its reduction.
 // A false positive leaves its history untouched (forces.py:95-97).
-__global__ void __launch_bounds__(256, 4) k_touch(DtView v, uint32_t *tlist, unsigned long long *tlist_n) {
+__global__ void __launch_bounds__(256, 4) k_touch(DtView v, uint32_t *tlist, unsigned long long *tlist_n,
+                                                  unsigned long long step) {
   int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   bool t = false;
   unsigned kind = 0;
-  if (k < v.n_acs && !v.st->err) {
+  if (k < v.n_acs && !v.st->err && v.st->dd_trip >= step) {
     const uint2 id = v.ids[k];
     kind = id.y >> kKindShift;
     double ca[3], ra, depth, bx, by, bz, rb;
@@ -170,8 +171,10 @@ template <typename VelT>
 __global__ void __launch_bounds__(128) k_integrate(DtView v, double h, double gx, double gy, double gz,
                                                    double v_err, unsigned long long step, int write_acc) {
   int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (i >= v.own.n || v.st->err) return;
+  if (i >= v.own.n || v.st->err || v.st->dd_trip < step) return;
   const uint32_t o = uint32_t(i);
+  // a ghost is integrated on its home rank; its state arrives by halo exchange
+  if (v.own.dd && (v.own.dd[o] & 3u) == kDdGhost) return;
   double p[3];
   decode_pos(v.dom, v.own.voxel[o], v.own.sub[o], p[0], p[1], p[2]);
   // --- reduction (reduce_to_owners order) ---
@@ -289,6 +292,10 @@ __global__ void __launch_bounds__(128) k_integrate(DtView v, double h, double gx
   }
   v.own.voxel[o] = vox;
   v.own.sub[o] = s;
+  // decomposition guard: the static ghost layer covers displacements up to
+  // dd_travel along the slab axis
+  if (v.own.dd && (v.own.dd[o] & 3u) == kDdLocal && fabs(p[v.own.dd_axis] - v.own.dd_x0[o]) > v.own.dd_travel)
+    atomicMin(&v.st->dd_trip, step);
   // refreshed sphere centres from the decoded position (_kernels.py:657-669)
   const uint32_t s0 = v.sph.first[o], s1 = v.sph.first[o + 1];
   if (s1 > s0) {
@@ -361,7 +368,7 @@ __global__ void k_world(Domain dom, Owners own, Tris tri, Anas ana) {
 }  // namespace
 
 template <typename VelT>
-int dt_step_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
+static DtView dt_view(Ctx *c) {
   DtView v;
   v.dom = c->dom;
   v.own = owners_view(c);
@@ -384,13 +391,23 @@ int dt_step_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
   v.n_heavy = c->heavy_count.as<unsigned long long>();
   v.heavy_acc = c->heavy_acc.as<double>();
   v.st = c->status.as<Status>();
+  return v;
+}
+
+// first half of a step: narrow phase + contact forces (+ the heavy-owner
+// pre-reduction of the parity build).  Split from the integration so a
+// decomposed run can return ghost force contributions in between.
+template <typename VelT>
+int dt_forces_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
+  DtView v = dt_view<VelT>(c);
   GF_CHECK(c, cudaMemsetAsync(&v.st->touching, 0, sizeof(unsigned long long), s));
   cudaEvent_t *ev = prof_events(c);
   if (ev) cudaEventRecord(ev[0], s);
   if (v.n_acs) {
     unsigned long long *tn = c->tlist_n.as<unsigned long long>();
     GF_CHECK(c, cudaMemsetAsync(tn, 0, sizeof(unsigned long long), s));
-    k_touch<<<unsigned((v.n_acs + 255) / 256), 256, 0, s>>>(v, c->tlist.as<uint32_t>(), tn);
+    k_touch<<<unsigned((v.n_acs + 255) / 256), 256, 0, s>>>(v, c->tlist.as<uint32_t>(), tn,
+                                                             (unsigned long long)a.step);
     if (c->user_model) {
       if (launch_user_forces(c, v, a.h, a.sim_time, s)) return -1;
     } else {
@@ -400,6 +417,15 @@ int dt_step_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
   if (ev) cudaEventRecord(ev[1], s);
   if (v.n_acs && !c->fixed_reduce) k_heavy<<<64, 256, 0, s>>>(v);
   if (ev) cudaEventRecord(ev[2], s);
+  GF_CHECK(c, cudaGetLastError());
+  return 0;
+}
+
+// second half: prescriptions, integration, world transforms
+template <typename VelT>
+int dt_integrate_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
+  DtView v = dt_view<VelT>(c);
+  cudaEvent_t *ev = prof_current(c);  // the set the force phase opened
   if (c->n_dyn) {
     k_apply_dyn<<<(c->n_dyn + 127) / 128, 128, 0, s>>>(
         c->n_dyn, c->dyn_spec.as<int>(), c->dyn_vals.as<double>() + size_t(c->n_dyn) * a.dyn_row,
@@ -417,6 +443,12 @@ int dt_step_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
   }
   GF_CHECK(c, cudaGetLastError());
   return 0;
+}
+
+template <typename VelT>
+int dt_step_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
+  if (dt_forces_impl<VelT>(c, a, s)) return -1;
+  return dt_integrate_impl<VelT>(c, a, s);
 }
 
 }  // namespace gf

@@ -291,7 +291,7 @@ __device__ __forceinline__ bool ss_pair(const KtView &v, const Grid &g, uint32_t
                                         const double ci[3], float ri_f, const long long lo_i[3],
                                         const long long hi_i[3], uint32_t oi, uint8_t fi) {
   uint32_t oj = v.sph.owner[j];
-  if (oi == oj) return false;
+  if (oi == oj || !dd_keep(v.own.dd, oi, oj)) return false;
   if (!v.mask[256 * fi + v.sfam[j]]) return false;
   const double *cj = v.centers + 3 * size_t(j);
   double dx = sub_(ci[0], cj[0]), dy = sub_(ci[1], cj[1]), dz = sub_(ci[2], cj[2]);
@@ -313,7 +313,7 @@ __device__ __forceinline__ bool st_pair(const KtView &v, const Grid &g, uint32_t
                                         const double ci[3], float ri_f, const long long lo_i[3],
                                         const long long hi_i[3], uint32_t oi, uint8_t fi,
                                         long long fx, long long fy, long long fz) {
-  if (oi == v.tri_owner[t]) return false;
+  if (oi == v.tri_owner[t] || !dd_keep(v.own.dd, oi, v.tri_owner[t])) return false;
   if (!v.mask[256 * fi + v.tfam[t]]) return false;
   const double *T = v.tri_world + 9 * size_t(t);
   double qx, qy, qz;
@@ -350,7 +350,7 @@ __device__ __forceinline__ bool st_pair(const KtView &v, const Grid &g, uint32_t
 // collect_sphere_analytic_pairs predicate (_kernels.py:418-428)
 __device__ __forceinline__ bool sa_pair(const KtView &v, uint32_t k, const double ci[3],
                                         float ri_f, uint32_t oi, uint8_t fi) {
-  if (oi == v.ana_owner[k]) return false;
+  if (oi == v.ana_owner[k] || !dd_keep(v.own.dd, oi, v.ana_owner[k])) return false;
   if (!v.mask[256 * fi + v.afam[k]]) return false;
   double gap, bx, by, bz, rb;
   analytic_gap(v.ana_kind[k], v.ana_world + 8 * size_t(k), ci[0], ci[1], ci[2], gap, bx, by, bz, rb);
@@ -400,7 +400,7 @@ __global__ void k_gather_sorted(int64_t n, const uint32_t *sorted, const double 
 // (l, h) are the lower / higher slot, matching the reference's i < j order
 __device__ __forceinline__ bool ss_pair_sorted(const KtView &v, const Grid &g, const double4 &cl,
                                                const uint4 &ml, const double4 &ch, const uint4 &mh) {
-  if (ml.y == mh.y) return false;
+  if (ml.y == mh.y || !dd_keep(v.own.dd, ml.y, mh.y)) return false;
   if (!v.mask[256 * ml.z + mh.z]) return false;
   double dx = sub_(cl.x, ch.x), dy = sub_(cl.y, ch.y), dz = sub_(cl.z, ch.z);
   double ri = add(cl.w, v.margin);
@@ -753,7 +753,7 @@ __global__ void __launch_bounds__(128) k_cand_ss(KtView v, const uint4 *sm, cons
         const float rr = f0.w + f1.w + marg + slack;
         if (dx * dx + dy * dy + dz * dz < rr * rr * 1.0001f) {
           const uint4 m1 = sm[w];
-          if (m1.y != m0.y) {
+          if (m1.y != m0.y && dd_keep(v.own.dd, m0.y, m1.y)) {
             hit = true;
             const uint32_t a = min(m0.x, m1.x), b = max(m0.x, m1.x);
             e = make_uint2(a, b);
@@ -797,7 +797,7 @@ __global__ void __launch_bounds__(128) k_cand_big(KtView v, const uint32_t *bigs
       for (uint32_t w = s0; w < s1; ++w) {
         const double4 c1 = sc[w];
         const uint4 m1 = sm[w];
-        if (m1.y == oB) continue;
+        if (m1.y == oB || !dd_keep(v.own.dd, m1.y, oB)) continue;
         const double dx = bx - c1.x, dy = by - c1.y, dz = bz - c1.z;
         const double rr = rB + c1.w + reach_m;
         if (dx * dx + dy * dy + dz * dz >= rr * rr * (1.0 + 1e-9)) continue;
@@ -809,7 +809,7 @@ __global__ void __launch_bounds__(128) k_cand_big(KtView v, const uint32_t *bigs
     }
     for (int64_t q = threadIdx.x; q < n_big; q += blockDim.x) {
       const uint32_t j = bigs[q];
-      if (j <= B || v.sph.owner[j] == oB) continue;
+      if (j <= B || v.sph.owner[j] == oB || !dd_keep(v.own.dd, v.sph.owner[j], oB)) continue;
       const double dx = bx - v.centers[3 * size_t(j)], dy = by - v.centers[3 * size_t(j) + 1],
                    dz = bz - v.centers[3 * size_t(j) + 2];
       const double rr = rB + double(v.sph.offr[j].w) + reach_m;

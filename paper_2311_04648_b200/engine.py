@@ -178,7 +178,7 @@ class Simulator:
     default_sync = False
 
     def __init__(self, domain: Domain, force_model: str = "hertz_mindlin", *,
-                 device: int = 0, precision: str = "f64", reorder=None):
+                 device: int = 0, precision: str = "f64", reorder=None, decomposition=None):
         if precision not in ("f64", "f32"):
             raise ValidationError(f"precision must be 'f64' or 'f32', got {precision!r}")
         self.materials = MaterialTable()
@@ -222,6 +222,11 @@ class Simulator:
         self._kin_delay = None     # accepted for API compatibility (engine.py:285-287)
         self._dyn_delay = None
         self.last_run = None
+        # spatial slab decomposition across ranks (decomp.SlabDecomposition);
+        # None = the whole scene on this device
+        self.decomposition = decomposition
+        if decomposition is not None and precision != "f32":
+            raise ConfigurationError("a decomposed simulator needs precision='f32' (fixed-point reduction)")
 
     # -- scene construction ---------------------------------------------------
     def load_material(self, props: dict) -> int:
@@ -351,6 +356,9 @@ class Simulator:
             raise ConfigurationError("already initialized")
         if len(self.materials) == 0:
             raise ConfigurationError("no materials loaded")
+        if self.decomposition is not None:
+            from . import decomp
+            decomp.prepare(self)   # self.store becomes this rank's piece of the scene
         s = self.store
         self.pair_stack = F.material_pair_stack(self.materials, self.model)
         self._beta = F.beta_table(self.pair_stack)
@@ -408,6 +416,8 @@ class Simulator:
                  C.c_int64(self._ana_geom.size), P(keep[6]), P(keep[7]), P(keep[8]), P(keep[9]))
         self._install_acs(self._acs0.canonicalize())
         s._sync_hook = self._sync_field
+        if self.decomposition is not None:
+            decomp.attach(self)
         self._initialized = True
 
     def close(self) -> None:
@@ -742,68 +752,85 @@ class Simulator:
             s.ang_vel[:n][frozen_now] = 0.0
 
     def _run(self, steps: int) -> None:
-        sch = self.scheduler
+        if self.decomposition is not None:
+            from . import decomp
+            decomp.run_member(self, steps)
+            return
         with self._lock:
             self._push_host()
-            period, lag = self._schedule()
-            margin = self._current_margin()
-            step0 = sch.step_counter
-            dyn = self._dynamic_prescriptions
-            spec = np.zeros((max(1, len(dyn)), 3), np.int32)
-            vals = np.zeros((steps, max(1, len(dyn))), np.float64)
-            if dyn:
-                ns = dict(_SAFE_EVAL_NS)
-                for j, (famid, table, ax, _) in enumerate(dyn):
-                    spec[j] = (famid, table, ax)
-                for i in range(steps):
-                    ns["t"] = (step0 + i) * self.h
-                    for j, (_, _, _, code) in enumerate(dyn):
-                        vals[i, j] = float(eval(code, {"__builtins__": {}}, ns))
-            rp = _lib.RunParams()
-            rp.n_steps = steps
-            rp.step0 = step0
-            rp.h = self.h
-            for a in range(3):
-                rp.g[a] = float(self.gravity[a])
-            rp.v_err = self.v_err
-            rp.margin = margin
-            rp.period = period
-            rp.lag = lag
-            rp.n_dyn = len(dyn)
-            rp.write_acc = 1
-            rp.dyn_spec = spec.ctypes.data_as(C.c_void_p)
-            rp.dyn_vals = vals.ctypes.data_as(C.c_void_p)
+            rp, keep = self._run_params(steps)
             rr = _lib.RunResult()
             t0 = _time.perf_counter()
             self._ctx.call("gf_run", C.byref(rp), C.byref(rr))
-            wall = _time.perf_counter() - t0
-            self.last_run = rr
-            self._host_stale = True
-            done = int(rr.steps_done)
-            sch.step_counter = step0 + done
-            self.sim_time = sch.step_counter * self.h
-            sch.ca_updates = int(rr.ca_updates)
-            sch.timing["dyn_force"] += rr.dt_ms * 1e-3
-            sch.timing["kin_detect"] += rr.kt_ms * 1e-3
-            sch.timing["dyn_transfer"] += max(0.0, wall - rr.dt_ms * 1e-3)
-            sch.last_wo_stamp = step0 + done
-            self._last_touching = int(rr.touching)
-            if done > 0:
-                sch.step_time_ema = rr.dt_ms * 1e-3 / done
-            n_cd = max(1, done // max(1, period))
-            sch.last_cd_seconds = rr.kt_ms * 1e-3 / n_cd
-            if rr.oob_owner >= 0 or rr.bad_owner >= 0:
-                self._raise_watchdog(rr)
+            self._finish_run(rr, _time.perf_counter() - t0)
+
+    def _run_params(self, steps: int):
+        """gf_run_params of the next `steps` steps (+ the arrays it points to)."""
+        sch = self.scheduler
+        period, lag = self._schedule()
+        margin = self._current_margin()
+        step0 = sch.step_counter
+        dyn = self._dynamic_prescriptions
+        spec = np.zeros((max(1, len(dyn)), 3), np.int32)
+        vals = np.zeros((steps, max(1, len(dyn))), np.float64)
+        if dyn:
+            ns = dict(_SAFE_EVAL_NS)
+            for j, (famid, table, ax, _) in enumerate(dyn):
+                spec[j] = (famid, table, ax)
+            for i in range(steps):
+                ns["t"] = (step0 + i) * self.h
+                for j, (_, _, _, code) in enumerate(dyn):
+                    vals[i, j] = float(eval(code, {"__builtins__": {}}, ns))
+        rp = _lib.RunParams()
+        rp.n_steps = steps
+        rp.step0 = step0
+        rp.h = self.h
+        for a in range(3):
+            rp.g[a] = float(self.gravity[a])
+        rp.v_err = self.v_err
+        rp.margin = margin
+        rp.period = period
+        rp.lag = lag
+        rp.n_dyn = len(dyn)
+        rp.write_acc = 1
+        rp.dyn_spec = spec.ctypes.data_as(C.c_void_p)
+        rp.dyn_vals = vals.ctypes.data_as(C.c_void_p)
+        return rp, (spec, vals)
+
+    def _finish_run(self, rr, wall: float, adapt: bool = True) -> None:
+        """Scheduler / timing bookkeeping after a gf_run; raises on a watchdog."""
+        sch = self.scheduler
+        period, _ = self._schedule()
+        step0 = sch.step_counter
+        self.last_run = rr
+        self._host_stale = True
+        done = int(rr.steps_done)
+        sch.step_counter = step0 + done
+        self.sim_time = sch.step_counter * self.h
+        sch.ca_updates = int(rr.ca_updates)
+        sch.timing["dyn_force"] += rr.dt_ms * 1e-3
+        sch.timing["kin_detect"] += rr.kt_ms * 1e-3
+        sch.timing["dyn_transfer"] += max(0.0, wall - rr.dt_ms * 1e-3)
+        sch.last_wo_stamp = step0 + done
+        self._last_touching = int(rr.touching)
+        if done > 0:
+            sch.step_time_ema = rr.dt_ms * 1e-3 / done
+        n_cd = max(1, done // max(1, period))
+        sch.last_cd_seconds = rr.kt_ms * 1e-3 / n_cd
+        if rr.oob_owner >= 0 or rr.bad_owner >= 0:
+            self._raise_watchdog(rr)
+        if adapt:
             self._adapt_n_max(waited_event=False)
 
     def _raise_watchdog(self, rr) -> None:
         oob_first = rr.oob_owner >= 0 and (rr.bad_owner < 0 or rr.oob_step <= rr.bad_step)
+        d2u = self._own_d2u
         if oob_first:
-            o = int(rr.oob_owner)
+            o = int(d2u[int(rr.oob_owner)])
             msg = (f"owner {o} left the domain at t={self.sim_time:.6g} "
                    f"(position {self._pos[o].tolist()})")
         else:
-            o = int(rr.bad_owner)
+            o = int(d2u[int(rr.bad_owner)])
             v = self.store.lin_vel[o]
             msg = (f"owner {o} exceeded error-out velocity {self.v_err} m/s "
                    f"(speed {float(np.linalg.norm(v)):.3g}) at t={self.sim_time:.6g}")

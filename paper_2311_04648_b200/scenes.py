@@ -31,7 +31,7 @@ G = 9.81
 
 def crater_bed(n_spheres: int = 1_000_000, *, seed: int = 7, h: float = 1e-5, v_err: float = 5.0,
                n_max: int = 4, precision: str = "f32", device: int = 0, ball: bool = True,
-               drop_height: float = 0.20, ball_density: float = 7800.0) -> Simulator:
+               drop_height: float = 0.20, ball_density: float = 7800.0, decomposition=None) -> Simulator:
     rng = np.random.default_rng(seed)
     D = 0.0254
     bed_half = 12.0 * D / 2.0
@@ -44,7 +44,7 @@ def crater_bed(n_spheres: int = 1_000_000, *, seed: int = 7, h: float = 1e-5, v_
     r_max = float(radii.max())
     dom = Domain((-bed_half * 1.2, -bed_half * 1.2, -0.02), (bed_half * 1.2, bed_half * 1.2,
                                                             depth * 3.0 + 0.3))
-    sim = Simulator(dom, precision=precision, device=device)
+    sim = Simulator(dom, precision=precision, device=device, decomposition=decomposition)
     grain = sim.load_material({"E": 5e6, "nu": 0.3, "CoR": 0.5, "mu": 0.3, "Crr": 0.01})
     wall = sim.load_material({"E": 5e6, "nu": 0.3, "CoR": 0.5, "mu": 0.3, "Crr": 0.01})
     tpls = [sim.load_clump_template(ClumpTemplate.solid_sphere(
