@@ -9,8 +9,13 @@ the kT stream joined), max over ranks.  `e2e` = the same metric through the
 C-ABI with host buffers: every step uploads the owner state from pinned host
 memory, runs the step, downloads the state.  `--impl reference` times the
 reference algorithm on the host cores (the C restatement in oracle/, all
-threads) on the same scene.  Multi-GPU: independent replicas of the bed, one
-per rank (weak scaling, no data-path collective).
+threads) on the same scene.
+
+Multi-GPU (torchrun, one process per GPU): the spatial slab decomposition
+(paper_2311_04648_b200/decomp.py) of N beds laid side by side -- each rank
+owns one 1M-sphere bed plus its projectile and exchanges ghost state and
+ghost forces with its neighbours over NCCL every step (weak scaling).
+`--mode replicas` runs N independent beds instead.
 """
 
 from __future__ import annotations
@@ -47,6 +52,10 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-steps", type=int, default=4)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--mode", default="auto", choices=["auto", "single", "replicas", "decomp"],
+                    help="auto: single on 1 GPU, decomp (slab decomposition) on N > 1")
+    ap.add_argument("--travel", type=float, default=5e-3,
+                    help="decomposition: displacement allowed before a repartition (m)")
     return ap.parse_args()
 
 
@@ -137,9 +146,10 @@ def cpu_run(scene, steps, warmup, period, lag, nthreads, margin):
     return time.perf_counter() - t0
 
 
-def build_scene(args, device):
+def build_scene(args, device, tiles=1, decomposition=None):
     from paper_2311_04648_b200 import scenes
-    return scenes.crater_bed(args.n_spheres, n_max=args.n_max, precision=args.precision, device=device)
+    return scenes.crater_bed(args.n_spheres, n_max=args.n_max, precision=args.precision, device=device,
+                             tiles=tiles, decomposition=decomposition)
 
 
 def schedule(sim):
@@ -178,17 +188,35 @@ def reference_arm(args):
 def b200_arm(args):
     rank, world, local = dist_env()
     import torch
+    mode = args.mode if args.mode != "auto" else ("decomp" if world > 1 else "single")
+    if mode == "single" and world > 1:
+        mode = "replicas"
     dist = None
-    if world > 1:
+    if world > 1 or mode == "decomp":
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29511")
+        dist.init_process_group("nccl", rank=rank, world_size=world)
     device = local
-    from paper_2311_04648_b200 import _lib, scenes
-    sim = build_scene(args, device)
-    scene0 = scenes.oracle_scene(sim) if (rank == 0 and not args.no_cpu) else None
+    from paper_2311_04648_b200 import _lib, decomp, scenes
+    dec = decomp.SlabDecomposition(travel=args.travel) if mode == "decomp" else None
+    sim = build_scene(args, device, tiles=world if mode == "decomp" else 1, decomposition=dec)
+    scene0 = scenes.oracle_scene(sim) if (rank == 0 and world == 1 and not args.no_cpu) else None
     sim.initialize()
-    n_s = int(sim._sph_geom.size)
+    if mode == "decomp":
+        cls = sim._dd.dd & 3
+        n_s = int(np.sum(cls[sim._sph_owner] == decomp.DD_LOCAL))   # spheres this rank integrates
+        n_ghost_owners = int(np.sum(cls == decomp.DD_GHOST))
+        n_sph_total = n_s
+        if dist is not None:
+            t = torch.tensor([n_s], device=f"cuda:{device}", dtype=torch.int64)
+            dist.all_reduce(t)
+            n_sph_total = int(t.item())
+    else:
+        n_s = int(sim._sph_geom.size)
+        n_ghost_owners = 0
+        n_sph_total = n_s * world
     n_o = int(sim.store.n_owners)
     h = sim.h
     # warm-up (untimed)
@@ -202,20 +230,26 @@ def b200_arm(args):
         torch.cuda.synchronize(device)
 
     barrier()
+    reps0 = getattr(sim.scheduler, "repartitions", 0)
+    dev0 = sim.scheduler.timing["dyn_force"]
     with ClockSampler(device) as clocks:
         sim.do_dynamics(args.steps * h)
         barrier()
     rr = sim.last_run
+    ctx = sim._ctx   # a repartition rebuilds the context
     times = np.zeros(5)
     ctx.call("gf_kernel_times", _lib.ptr(times))
     ctx.call("gf_set_profiling", C.c_int(0))
-    dt_ms = float(rr.dt_ms)
+    # device time of the timed steps: CUDA events on the dT stream around
+    # every gf_run segment (one segment unless a repartition split the call)
+    dt_ms = (sim.scheduler.timing["dyn_force"] - dev0) * 1e3
+    repartitions = getattr(sim.scheduler, "repartitions", 0) - reps0
     if dist is not None:
         t = torch.tensor([dt_ms], device=f"cuda:{device}", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dt_ms = float(t.item())
     ms_per_step = dt_ms / args.steps
-    value = n_s * world * args.steps / (dt_ms * 1e-3) / 1e6
+    value = n_sph_total * args.steps / (dt_ms * 1e-3) / 1e6
     n_acs_avg = float(rr.sum_acs) / max(1, args.steps)
     n_touch_avg = float(rr.sum_touch_pairs) / max(1, args.steps)
     n_free = int(np.sum(~sim._fixed_flag[sim.store.owner_family[:n_o]]))
@@ -233,7 +267,16 @@ def b200_arm(args):
     ach_chain = bytes_chain / t_chain / 1e9 if t_chain > 0 else 0.0
 
     # --- e2e: host-buffer round trip per step through the C-ABI ---
-    e2e = measure_e2e(sim, args.e2e_steps) if args.e2e_steps > 0 else None
+    e2e = None
+    if args.e2e_steps > 0:
+        e2e = measure_e2e_decomp(sim, args.e2e_steps, dist) if mode == "decomp" else \
+            measure_e2e(sim, args.e2e_steps)
+        if e2e is not None and dist is not None:
+            t = torch.tensor([e2e.pop("wall")], device=f"cuda:{device}", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e["value"] = (n_sph_total if mode == "decomp" else n_s * world) * e2e["steps"] / float(t.item()) / 1e6
+        elif e2e is not None:
+            e2e.pop("wall")
 
     line = None
     if rank == 0:
@@ -246,6 +289,8 @@ def b200_arm(args):
                    "sample": f"{csteps} steps (+1 warm-up) of the same bed from the same initial "
                              f"state, serial C restatement (oracle/gf_oracle.c)"}
         launches_per_step = 3 + (1 if sim._tri_geom.size or sim._ana_geom.size else 0)
+        if mode == "decomp":   # halo: pack/add forces, pack/unpack(+centres) state per peer; guard word x2
+            launches_per_step += 2 + 5 * len(sim._dd.peers)
         period, lag, _ = schedule(sim)
         kt_launches = 22
         line = {
@@ -255,13 +300,18 @@ def b200_arm(args):
             "dtype": "f64 contact math, " + ("f32" if args.precision == "f32" else "f64") + " velocities",
             "data": "synthetic",
             "config": {"workload": f"crater impact bed, {n_s} polydisperse spheres + projectile "
-                                   f"(configs[1])", "n_spheres": n_s, "n_owners": n_o,
+                                   f"(configs[1])" + (f" per GPU, {world} beds side by side" if world > 1 else ""),
+                       "n_spheres": n_s, "n_owners": n_o,
                        "n_max": args.n_max, "period": period, "lag": lag, "h": h,
-                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                       "parallelism": ({"decomp": f"slab decomposition x{world} (NCCL halo + force return)",
+                                        "replicas": f"replicas x{world}"}.get(mode, "single GPU")),
+                       "n_spheres_total": n_sph_total,
                        "inputs_vs_l2": "state + contact arrays larger than L2 (no flush)",
                        "avg_acs": n_acs_avg, "avg_touching_pairs": n_touch_avg,
                        "kt_candidate_rebuilds": int(rr.kt_rebuilds),
-                       "precision": args.precision},
+                       "precision": args.precision,
+                       **({"ghost_owners_rank0": n_ghost_owners, "travel_m": args.travel,
+                           "repartitions_in_timed_steps": repartitions} if mode == "decomp" else {})},
             "roofline": {"bound": "hbm", "kernel": "k_contacts", "achieved": ach_c, "peak": hbm,
                          "unit": "GB/s", "frac": ach_c / hbm, "peak_kind": hbm_kind,
                          "traffic": profiled_traffic("k_contacts"),
@@ -330,8 +380,49 @@ def measure_e2e(sim, steps):
     n_s = int(sim._sph_geom.size)
     per = n * (8 + 6 + 16 + 24 + 24 + 1)
     return {"value": n_s * steps / wall / 1e6, "unit": UNIT, "h2d_bytes_per_step": per,
-            "d2h_bytes_per_step": per + 64, "steps": steps,
+            "d2h_bytes_per_step": per + 64, "steps": steps, "wall": wall,
             "path": "gf_upload_owners -> gf_run(1 step) -> gf_download_owners, pinned host buffers"}
+
+
+def measure_e2e_decomp(sim, steps, dist):
+    """The decomposed step end to end: per step the rank's owner state from
+    pinned host memory (gf_upload_owners), one step through the public API
+    (Simulator.do_dynamics: forces, NCCL ghost-force return, integration,
+    NCCL ghost state), the state back to pinned host memory."""
+    import torch
+    from paper_2311_04648_b200 import _lib
+    ctx = sim._ctx
+    n = sim.store.n_owners
+    P = _lib.ptr
+
+    def pinned(shape, dtype):
+        t = torch.empty(int(np.prod(shape)) * np.dtype(dtype).itemsize, dtype=torch.uint8).pin_memory()
+        return t.numpy().view(dtype).reshape(shape)
+
+    vox, sub = pinned((n,), np.uint64), pinned((n, 3), np.uint16)
+    quat, lv, av = pinned((n, 4), np.float32), pinned((n, 3), np.float64), pinned((n, 3), np.float64)
+    fam = pinned((n,), np.uint8)
+    ctx.call("gf_download_owners", P(vox), P(sub), P(quat), P(lv), P(av), P(fam))
+    tpl = _lib.carr(sim._tpl_id[sim._own_d2u], np.uint32)
+    rows = sim._tpl_rows
+    mass, moi = rows[:, 0].copy(), _lib.carr(rows[:, 1:], np.float64)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(steps):
+        ctx = sim._ctx
+        ctx.call("gf_upload_owners", C.c_int64(n), P(vox), P(sub), P(quat), P(lv), P(av), P(fam),
+                 P(tpl), C.c_int64(rows.shape[0]), P(mass), P(moi))
+        sim._host_stale = False
+        sim.do_dynamics(sim.h)
+        sim._ctx.call("gf_download_owners", P(vox), P(sub), P(quat), P(lv), P(av), P(fam))
+    wall = time.perf_counter() - t0
+    per = n * (8 + 6 + 16 + 24 + 24 + 1)
+    return {"value": 0.0, "unit": UNIT, "h2d_bytes_per_step": per, "d2h_bytes_per_step": per + 64,
+            "steps": steps, "wall": wall,
+            "path": "gf_upload_owners -> Simulator.do_dynamics(1 step; NCCL halo) -> gf_download_owners, "
+                    "pinned host buffers, per rank"}
 
 
 def main():

@@ -121,10 +121,20 @@ class SlabPlan:
     n_ranks: int
     axis: int
     cuts: np.ndarray      # (n_ranks - 1,) slab boundaries along axis
-    width: float          # ghost layer width
+    pad: float            # margin + 2 travel + the largest reach of a non-big owner
     travel: float         # guard: allowed displacement before a repartition
     home: np.ndarray      # (n_owners,) home rank, -1 = shared boundary owner
     x: np.ndarray         # (n_owners,) partition-time coordinate along axis
+    reach: np.ndarray     # (n_owners,) owner reach (owner_reach)
+    big: np.ndarray       # indices of big owners (reach > 2 x median): own halo
+    margin: float = 0.0
+
+    @property
+    def width(self) -> float:
+        """Ghost layer width for the largest non-big owner."""
+        r = self.reach[self.home >= 0]
+        small = r[~np.isin(np.nonzero(self.home >= 0)[0], self.big)] if r.size else r
+        return self.pad + (float(small.max()) if small.size else 0.0)
 
     def bounds(self, r: int):
         lo = -math.inf if r == 0 else float(self.cuts[r - 1])
@@ -132,9 +142,19 @@ class SlabPlan:
         return lo, hi
 
     def ghost_on(self, r: int) -> np.ndarray:
-        """Owners homed elsewhere whose coordinate lies within width of slab r."""
+        """Owners homed elsewhere that can touch one of rank r's owners while
+        every owner stays within `travel` of its partition coordinate:
+        within reach_b + pad of slab r, or within reach_a + reach_b + margin
+        + 2 travel of a big owner a of rank r."""
         lo, hi = self.bounds(r)
-        return (self.home >= 0) & (self.home != r) & (self.x >= lo - self.width) & (self.x <= hi + self.width)
+        other = (self.home >= 0) & (self.home != r)
+        dist = np.maximum(np.maximum(lo - self.x, self.x - hi), 0.0)
+        g = other & (dist <= self.reach + self.pad)
+        for a in self.big:
+            if self.home[a] == r:
+                g |= other & (np.abs(self.x - self.x[a]) <=
+                              self.reach + self.reach[a] + self.margin + 2.0 * self.travel)
+        return g
 
     def classes(self, r: int) -> np.ndarray:
         """Per owner: DD class on rank r, or -1 when the owner is absent there."""
@@ -167,9 +187,12 @@ def plan_slabs(pos: np.ndarray, eligible: np.ndarray, reach: np.ndarray, n_ranks
     the longest extent)."""
     pos = np.asarray(pos, dtype=np.float64)
     eligible = np.asarray(eligible, dtype=bool)
+    reach = np.asarray(reach, dtype=np.float64)
     n = pos.shape[0]
     if n_ranks < 1:
         raise ConfigurationError("n_ranks must be >= 1")
+    if (1 << 30) <= n:
+        raise ConfigurationError("decomposition supports < 2^30 owners")
     pts = pos[eligible]
     if axis is None:
         axis = int(np.argmax(pts.max(axis=0) - pts.min(axis=0))) if pts.shape[0] else 0
@@ -184,11 +207,15 @@ def plan_slabs(pos: np.ndarray, eligible: np.ndarray, reach: np.ndarray, n_ranks
     x = pos[:, axis].copy()
     home = np.full(n, -1, np.int64)
     home[eligible] = np.searchsorted(cuts, x[eligible], side="right")
-    r_max = float(reach[eligible].max()) if eligible.any() else 0.0
-    width = 2.0 * r_max + margin + 2.0 * travel
-    if (1 << 30) <= n:
-        raise ConfigurationError("decomposition supports < 2^30 owners")
-    return SlabPlan(n_ranks, int(axis), cuts, width, float(travel), home, x)
+    er = reach[eligible]
+    if er.size:
+        big_cut = 2.0 * float(np.median(er))
+        big = np.nonzero(eligible & (reach > big_cut))[0].astype(np.int64)
+        small_max = float(er[er <= big_cut].max())
+    else:
+        big, small_max = np.zeros(0, np.int64), 0.0
+    pad = small_max + margin + 2.0 * travel
+    return SlabPlan(n_ranks, int(axis), cuts, pad, float(travel), home, x, reach, big, float(margin))
 
 
 # ----------------------------------------------------------------------------
@@ -201,8 +228,9 @@ class SlabDecomposition:
 
     n_ranks / rank default to torch.distributed's world size / rank (one
     process per GPU, NCCL); with ``group`` (a LoopbackGroup) the ranks are
-    contexts of this process.  ``travel`` (default: one largest clump
-    diameter) trades ghost-layer width against repartition frequency."""
+    contexts of this process.  ``travel`` (default: the diameter of the
+    largest ordinary owner; big owners such as projectiles get their own
+    halo) trades ghost-layer width against repartition frequency."""
     n_ranks: Optional[int] = None
     rank: Optional[int] = None
     axis: Optional[int] = None
@@ -304,7 +332,9 @@ def prepare(sim) -> None:
     if dec.travel is not None:
         travel = float(dec.travel)
     else:
-        travel = 2.0 * float(reach[eligible].max()) if eligible.any() else 0.0
+        # one diameter of the largest ordinary (non-big) owner
+        er = reach[eligible]
+        travel = 2.0 * float(er[er <= 2.0 * np.median(er)].max()) if er.size else 0.0
     axis = dec.axis if dec.axis is not None else (prev.plan.axis if prev is not None else None)
     plan = plan_slabs(pos, eligible, reach, n_ranks, margin, travel, axis)
     cls = plan.classes(rank)

@@ -31,7 +31,8 @@ G = 9.81
 
 def crater_bed(n_spheres: int = 1_000_000, *, seed: int = 7, h: float = 1e-5, v_err: float = 5.0,
                n_max: int = 4, precision: str = "f32", device: int = 0, ball: bool = True,
-               drop_height: float = 0.20, ball_density: float = 7800.0, decomposition=None) -> Simulator:
+               drop_height: float = 0.20, ball_density: float = 7800.0, decomposition=None,
+               tiles: int = 1) -> Simulator:
     rng = np.random.default_rng(seed)
     D = 0.0254
     bed_half = 12.0 * D / 2.0
@@ -39,11 +40,15 @@ def crater_bed(n_spheres: int = 1_000_000, *, seed: int = 7, h: float = 1e-5, v_
     packing = 1460.0 / 2500.0
     volume = (2 * bed_half) ** 2 * depth
     d_mean = (6.0 * volume * packing / (math.pi * n_spheres)) ** (1.0 / 3.0)
+    # `tiles` beds side by side along x (weak-scaling scene: one bed and one
+    # projectile per rank); tiles = 1 is configs[1] itself
+    tiles = max(1, int(tiles))
+    half_x = bed_half * tiles
     dset = np.linspace(0.25, 0.35, 11) * (d_mean / 0.30)
     radii = dset / 2.0
     r_max = float(radii.max())
-    dom = Domain((-bed_half * 1.2, -bed_half * 1.2, -0.02), (bed_half * 1.2, bed_half * 1.2,
-                                                            depth * 3.0 + 0.3))
+    dom = Domain((-half_x - 0.2 * bed_half, -bed_half * 1.2, -0.02),
+                 (half_x + 0.2 * bed_half, bed_half * 1.2, depth * 3.0 + 0.3))
     sim = Simulator(dom, precision=precision, device=device, decomposition=decomposition)
     grain = sim.load_material({"E": 5e6, "nu": 0.3, "CoR": 0.5, "mu": 0.3, "Crr": 0.01})
     wall = sim.load_material({"E": 5e6, "nu": 0.3, "CoR": 0.5, "mu": 0.3, "Crr": 0.01})
@@ -62,14 +67,16 @@ def crater_bed(n_spheres: int = 1_000_000, *, seed: int = 7, h: float = 1e-5, v_
     if pts.shape[0] < n_spheres:
         raise RuntimeError(f"lattice holds {pts.shape[0]} < {n_spheres} grains")
     pts = pts[:n_spheres]
-    kinds = rng.integers(0, 11, pts.shape[0])
-    for k, tpl in enumerate(tpls):
-        sel = pts[kinds == k]
-        if sel.shape[0]:
-            sim.add_clumps(tpl, sel)
+    offsets = [-half_x + (2 * t + 1) * bed_half for t in range(tiles)]
+    for x_off in offsets:
+        kinds = rng.integers(0, 11, pts.shape[0])
+        for k, tpl in enumerate(tpls):
+            sel = pts[kinds == k]
+            if sel.shape[0]:
+                sim.add_clumps(tpl, sel + np.array([x_off, 0.0, 0.0]))
     walls = [("plane", (0, 0, 0), (0, 0, 1), wall),
-             ("plane", (-bed_half, 0, 0), (1, 0, 0), wall),
-             ("plane", (bed_half, 0, 0), (-1, 0, 0), wall),
+             ("plane", (-half_x, 0, 0), (1, 0, 0), wall),
+             ("plane", (half_x, 0, 0), (-1, 0, 0), wall),
              ("plane", (0, -bed_half, 0), (0, 1, 0), wall),
              ("plane", (0, bed_half, 0), (0, -1, 0), wall)]
     sim.add_analytic(walls, family=255)
@@ -79,8 +86,9 @@ def crater_bed(n_spheres: int = 1_000_000, *, seed: int = 7, h: float = 1e-5, v_
         mass = ball_density * 4.0 / 3.0 * math.pi * R ** 3
         btpl = sim.load_clump_template(ClumpTemplate.solid_sphere(R, mass, grain))
         surface = float(pts[:, 2].max()) + r_max
-        b = sim.add_clumps(btpl, [[0.0, 0.0, surface + R + 2e-3]])[0]
-        sim.track(b).set_vel([0.0, 0.0, -math.sqrt(2.0 * G * drop_height)])
+        for x_off in offsets:
+            b = sim.add_clumps(btpl, [[x_off, 0.0, surface + R + 2e-3]])[0]
+            sim.track(b).set_vel([0.0, 0.0, -math.sqrt(2.0 * G * drop_height)])
     sim.set_gravity([0, 0, -G])
     sim.set_init_time_step(h)
     sim.set_error_out_velocity(v_err)

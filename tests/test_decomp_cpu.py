@@ -36,6 +36,8 @@ def scene(n=3000, seed=1):
     eligible = np.ones(n, bool)
     eligible[-2:] = False                      # two boundary owners (walls)
     reach = np.where(eligible, rng.uniform(0.002, 0.004, n), np.inf)
+    reach[:3] = (0.02, 0.013, 0.03)            # big owners (projectiles) with their own halo
+    pos[0, 0], pos[1, 0] = 0.0, -0.1          # ... near the slab cuts
     return pos, eligible, reach
 
 
@@ -69,11 +71,11 @@ def test_every_contact_is_computed_exactly_once(n_ranks):
         c = plan.classes(r)
         dd = np.where(c >= 0, c, 0).astype(np.int64) | (np.arange(n, dtype=np.int64) << 2)
         dds.append((c, dd))
-    rmax = reach[el].max()
+    assert plan.big.tolist() == [0, 1, 2]
     idx = np.nonzero(el)[0]
     for i in idx[:400]:
         # worst case: both move `travel` towards each other along the axis
-        near = idx[np.abs(pos[idx, plan.axis] - pos[i, plan.axis]) < 2 * rmax + 2 * travel]
+        near = idx[np.abs(pos[idx, plan.axis] - pos[i, plan.axis]) < reach[i] + reach[idx] + 1e-3 + 2 * travel]
         for j in near:
             if j == i:
                 continue
