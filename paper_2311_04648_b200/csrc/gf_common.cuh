@@ -132,18 +132,25 @@ struct Families {
 
 // device status block (watchdog records, counters)
 struct Status {
+  // line 0: watchdog words and stop flags -- read by every dT thread, written
+  // only when something trips, so it stays clean in every L1
   unsigned long long bad;    // (step << 40) | owner of first speeding owner, or ~0
   unsigned long long oob;    // same for out-of-domain
-  unsigned long long touching;
-  unsigned long long acs_total;   // last detection's pair count
-  unsigned long long touch_pairs;  // touching ACS entries summed over the run's steps
-  unsigned long long cand_total;   // candidate pairs of the last rebuild
-  unsigned long long other_total;  // sphere-triangle / sphere-analytic pairs of the last detection
+  unsigned long long dd_trip;  // first step a local owner exceeded the decomposition travel, or ~0;
+                               // later steps are skipped (that step itself completes)
   double oob_pos[3];
   int err;                   // nonzero once a watchdog tripped (kernels stop)
   int rebuild;               // detection phase A: candidate lists must be rebuilt
-  unsigned long long dd_trip;  // first step a local owner exceeded the decomposition travel, or ~0;
-                               // later steps are skipped (that step itself completes)
+  unsigned long long pad0[9];
+  // line 1: kT counters (atomics on the kT stream)
+  unsigned long long acs_total;   // last detection's pair count
+  unsigned long long cand_total;   // candidate pairs of the last rebuild
+  unsigned long long other_total;  // sphere-triangle / sphere-analytic pairs of the last detection
+  unsigned long long pad1[13];
+  // line 2: dT counters (one atomic per k_touch block)
+  unsigned long long touching;
+  unsigned long long touch_pairs;  // touching ACS entries summed over the run's steps
+  unsigned long long pad2[14];
 };
 
 __host__ __device__ inline uint32_t meta_family(uint32_t m) { return m >> 24; }

@@ -105,7 +105,8 @@ struct Ctx {
   // per-contact outputs and incidence lists (sized with acs.cap)
   DBuf out_c;      // double[cap*9]: F(3), F+tof(3), contact point(3)
   DBuf touch;      // uint8[cap]
-  DBuf tlist, tlist_n;  // compacted touching entries of the current step
+  DBuf tlist, tlist_n;  // compacted touching entries of the current step (two lists, two counters)
+  int64_t tlist_cap = 0;
   DBuf inc, inc_alt, inc_key, inc_key_alt;  // uint32[2*cap]
   DBuf inc_start;  // uint32[n_owner+1]
   DBuf heavy;      // uint32 list of heavy owners

@@ -196,6 +196,86 @@ __device__ __forceinline__ void hertz_mindlin_core(double overlap, double ts, do
   wild[3] = float(delta_time);
 }
 
+// The same law in fp32 for the throughput build's sphere-sphere fast path
+// (k_forces_f32): DEM-Engine evaluates its contact models in float once the
+// overlap is known.  Same expression order as above.
+__device__ __forceinline__ void hertz_mindlin_core_f32(float overlap, float ts, float b2ax, float b2ay,
+                                                       float b2az, float vx, float vy, float vz, float wrx,
+                                                       float wry, float wrz, float mass_eff, float ra, float rb,
+                                                       float e_cnt, float g_cnt, float mu, float crr, float beta,
+                                                       float *wild, float out[6]) {
+  for (int q = 0; q < 6; ++q) out[q] = 0.f;
+  const float4 w4 = *reinterpret_cast<const float4 *>(wild);
+  float projection = vx * b2ax + vy * b2ay + vz * b2az;
+  float vtx = vx - projection * b2ax;
+  float vty = vy - projection * b2ay;
+  float vtz = vz - projection * b2az;
+  float dtx = w4.x + ts * vtx;
+  float dty = w4.y + ts * vty;
+  float dtz = w4.z + ts * vtz;
+  float disp_proj = dtx * b2ax + dty * b2ay + dtz * b2az;
+  dtx -= disp_proj * b2ax;
+  dty -= disp_proj * b2ay;
+  dtz -= disp_proj * b2az;
+  float delta_time = w4.w + ts;
+
+  const float rr = (ra * rb) / (ra + rb);
+  float sqrt_rd = sqrtf(overlap * rr);
+  float sn = 2.f * e_cnt * sqrt_rd;
+  float k_n = (2.f / 3.f) * sn;
+  float gamma_n = 2.f * 0.91287092917527685f * beta * sqrtf(sn * mass_eff);
+  float fn = k_n * overlap + gamma_n * projection;
+  out[0] = fn * b2ax;
+  out[1] = fn * b2ay;
+  out[2] = fn * b2az;
+  const float fmag = fabsf(fn);
+  if (crr > 0.f) {
+    bool add_rolling = true;
+    float r_eff = sqrtf(rr);
+    float kn_simple = (4.f / 3.f) * e_cnt * sqrtf(r_eff);
+    float gn_simple = -2.f * sqrtf((5.f / 3.f) * mass_eff * e_cnt) * beta * sqrtf(sqrtf(r_eff));
+    float d_coeff = gn_simple / (2.f * sqrtf(kn_simple * mass_eff));
+    if (d_coeff < 1.f) {
+      float t_collision = float(kPi) * sqrtf(mass_eff / (kn_simple * (1.f - d_coeff * d_coeff)));
+      if (delta_time <= t_collision) add_rolling = false;
+    }
+    if (add_rolling) {
+      float v_rot_mag = sqrtf(wrx * wrx + wry * wry + wrz * wrz);
+      if (v_rot_mag > 1e-12f) {
+        float scale = crr * fmag / v_rot_mag;
+        out[3] = wrx * scale;
+        out[4] = wry * scale;
+        out[5] = wrz * scale;
+      }
+    }
+  }
+  if (mu > 0.f) {
+    float kt = 8.f * g_cnt * sqrt_rd;
+    float gt = -2.f * 0.91287092917527685f * beta * sqrtf(mass_eff * kt);
+    float tfx = -kt * dtx - gt * vtx;
+    float tfy = -kt * dty - gt * vty;
+    float tfz = -kt * dtz - gt * vtz;
+    float ft = sqrtf(tfx * tfx + tfy * tfy + tfz * tfz);
+    if (ft > 1e-12f) {
+      float ft_max = fmag * mu;
+      if (ft > ft_max) {
+        float scale = ft_max / ft;
+        tfx *= scale; tfy *= scale; tfz *= scale;
+        const float ik = -1.f / kt;
+        dtx = (tfx + gt * vtx) * ik;
+        dty = (tfy + gt * vty) * ik;
+        dtz = (tfz + gt * vtz) * ik;
+      }
+    } else {
+      tfx = 0.f; tfy = 0.f; tfz = 0.f;
+    }
+    out[0] += tfx;
+    out[1] += tfy;
+    out[2] += tfz;
+  }
+  *reinterpret_cast<float4 *>(wild) = make_float4(dtx, dty, dtz, delta_time);
+}
+
 // built-in model: pair values and beta from the uploaded tables
 __device__ __forceinline__ void hertz_mindlin(double overlap, double ts, double b2ax, double b2ay,
                                               double b2az, double vx, double vy, double vz,

@@ -19,6 +19,7 @@
 //                prescriptions, quaternion renormalisation, re-encode /
 //                decode and the watchdog (_kernels.py:548-670) -- fused.
 #pragma once
+#include <type_traits>
 #include "gf_context.h"
 #include "gf_device.cuh"
 
@@ -31,12 +32,18 @@ namespace {
 // Touching entries are compacted into tlist (warp-aggregated append); the
 // fp64 parity build also records a touch flag per entry for its reduction.
 // A false positive leaves its history untouched (forces.py:95-97).
-__global__ void __launch_bounds__(256, 4) k_touch(DtView v, uint32_t *tlist, unsigned long long *tlist_n,
-                                                  unsigned long long step) {
-  int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+__global__ void __launch_bounds__(256, 4) k_touch(DtView v, uint32_t *tlist, uint32_t *tlist_other,
+                                                  unsigned long long *tlist_n, unsigned long long step) {
+  __shared__ int s_live;
+  __shared__ unsigned s_cnt[2][8], s_tch[8], s_off[2][8];
+  __shared__ unsigned long long s_base[2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_live = !v.st->err && v.st->dd_trip >= step;
+  __syncthreads();
+  const int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   bool t = false;
   unsigned kind = 0;
-  if (k < v.n_acs && !v.st->err && v.st->dd_trip >= step) {
+  if (k < v.n_acs && s_live) {
     const uint2 id = v.ids[k];
     kind = id.y >> kKindShift;
     double ca[3], ra, depth, bx, by, bz, rb;
@@ -44,28 +51,152 @@ __global__ void __launch_bounds__(256, 4) k_touch(DtView v, uint32_t *tlist, uns
     t = depth > 0.0;
     if (!v.own.facc) v.touch[k] = t ? 1 : 0;
   }
-  const unsigned m = __ballot_sync(0xffffffffu, t);
-  const int lane = threadIdx.x & 31;
-  unsigned long long base = 0;
-  if (m && lane == 0) base = atomicAdd(tlist_n, (unsigned long long)__popc(m));
-  base = __shfl_sync(0xffffffffu, base, 0);
-  if (t) tlist[base + __popc(m & ((1u << lane) - 1u))] = uint32_t(k);
-  // touching counts (integers: order-independent)
+  // block-aggregated appends (ascending k within the block): sphere-sphere
+  // entries to tlist, the other kinds to tlist_other; one atomic per block
+  // on each shared counter
+  const unsigned m0 = __ballot_sync(0xffffffffu, t && kind == 0);
+  const unsigned m1 = __ballot_sync(0xffffffffu, t && kind != 0);
   unsigned touching = t ? (kind == 0 ? 2u : 1u) : 0u;
   for (int off = 16; off > 0; off >>= 1) touching += __shfl_down_sync(0xffffffffu, touching, off);
-  if (lane == 0 && m) {
-    atomicAdd(&v.st->touching, (unsigned long long)touching);
-    atomicAdd(&v.st->touch_pairs, (unsigned long long)__popc(m));
+  if (lane == 0) {
+    s_cnt[0][warp] = __popc(m0);
+    s_cnt[1][warp] = __popc(m1);
+    s_tch[warp] = touching;
   }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned tot[2] = {0, 0}, tch = 0;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) {
+      for (int l = 0; l < 2; ++l) {
+        s_off[l][w] = tot[l];
+        tot[l] += s_cnt[l][w];
+      }
+      tch += s_tch[w];
+    }
+    for (int l = 0; l < 2; ++l) s_base[l] = tot[l] ? atomicAdd(tlist_n + l, (unsigned long long)tot[l]) : 0ull;
+    if (tot[0] + tot[1]) {
+      atomicAdd(&v.st->touching, (unsigned long long)tch);
+      atomicAdd(&v.st->touch_pairs, (unsigned long long)(tot[0] + tot[1]));
+    }
+  }
+  __syncthreads();
+  const unsigned lt = (1u << lane) - 1u;
+  if (t && kind == 0) tlist[s_base[0] + s_off[0][warp] + __popc(m0 & lt)] = uint32_t(k);
+  if (t && kind != 0) tlist_other[s_base[1] + s_off[1][warp] + __popc(m1 & lt)] = uint32_t(k);
 }
 
 }  // namespace
 
 // force phase of the built-in Hertz-Mindlin model: touching entries only
+// (list0 = sphere-sphere entries unless skip0, then list1 = other kinds)
 template <typename VelT>
-__global__ void __launch_bounds__(128) k_forces(DtView v, double ts, double sim_time, const uint32_t *tlist,
-                                                const unsigned long long *tlist_n) {
-  forces_loop<VelT, HmCore>(v, ts, sim_time, tlist, tlist_n);
+__global__ void __launch_bounds__(128) k_forces(DtView v, double ts, double sim_time, const uint32_t *list0,
+                                                const uint32_t *list1, const unsigned long long *counts,
+                                                int skip0) {
+  if (v.st->err) return;
+  const unsigned long long n0 = skip0 ? 0ull : counts[0], n = n0 + counts[1];
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x)
+    force_entry<VelT, HmCore>(v, i < n0 ? list0[i] : list1[i - n0], ts, sim_time);
+}
+
+// fp32 rotation by q = (w, x, y, z) (lever arms and angular velocities of
+// the fp32 fast path; same formula as qrot)
+__device__ __forceinline__ void qrotf(const float4 q, float x, float y, float z, float &rx, float &ry, float &rz) {
+  const float tx = (q.z * z - q.w * y) + q.x * x;
+  const float ty = (q.w * x - q.y * z) + q.x * y;
+  const float tz = (q.y * y - q.z * x) + q.x * z;
+  rx = x + 2.f * (q.z * tz - q.w * ty);
+  ry = y + 2.f * (q.w * tx - q.y * tz);
+  rz = z + 2.f * (q.y * ty - q.z * tx);
+}
+
+// Throughput build, built-in Hertz-Mindlin: sphere-sphere contacts with the
+// centre difference and the overlap numerator R^2 - d^2 in fp64, everything
+// after in fp32 (normal, lever arms from the fp32-rotated clump offsets,
+// velocities, the contact law).  The other kinds (walls) take k_forces.
+// Contributions go to the int64 fixed-point owner accumulators as before.
+static __global__ void __launch_bounds__(256, 3) k_forces_f32(DtView v, double ts_d, double sim_time,
+                                                    const uint32_t *tlist, const unsigned long long *tlist_n) {
+  if (v.st->err) return;
+  const unsigned long long n = *tlist_n;
+  const float ts = float(ts_d);
+  const int nm = v.mat.n_mat, mm = nm * nm;
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint32_t k = tlist[i];
+    const uint2 id = v.ids[k];
+    const uint32_t a = id.x, b = id.y & kSlotMask;
+    const double4 cA = v.sph.center[a], cB = v.sph.center[b];
+    const double dx = cA.x - cB.x, dy = cA.y - cB.y, dz = cA.z - cB.z;
+    const double d2 = dx * dx + dy * dy + dz * dz;
+    const double R = cA.w + cB.w;
+    const float num = float(R * R - d2);
+    if (!(num > 0.f)) continue;
+    const float fdx = float(dx), fdy = float(dy), fdz = float(dz);
+    const float d = sqrtf(float(d2));
+    const float depth = num / (float(R) + d);
+    float bx = 0.f, by = 0.f, bz = 1.f;
+    if (d > 1e-30f) {
+      const float inv = 1.f / d;
+      bx = fdx * inv; by = fdy * inv; bz = fdz * inv;
+    }
+    const uint32_t oa = v.sph.owner[a], ob = v.sph.owner[b];
+    const float4 offA = v.sph.offr[a], offB = v.sph.offr[b];
+    const float4 qa = v.own.quat[oa], qb = v.own.quat[ob];
+    // contact point p = cA - b (ra - depth / 2); lever arms p - pos_a, p - pos_b
+    const float ha = offA.w - 0.5f * depth;
+    float rax, ray, raz, rbx, rby, rbz;
+    qrotf(qa, offA.x, offA.y, offA.z, rax, ray, raz);
+    qrotf(qb, offB.x, offB.y, offB.z, rbx, rby, rbz);
+    rbx += fdx - bx * ha; rby += fdy - by * ha; rbz += fdz - bz * ha;
+    rax -= bx * ha; ray -= by * ha; raz -= bz * ha;
+    const float4 va = reinterpret_cast<const float4 *>(v.own.lin_vel)[oa];
+    const float4 vb = reinterpret_cast<const float4 *>(v.own.lin_vel)[ob];
+    const float4 wla = reinterpret_cast<const float4 *>(v.own.ang_vel)[oa];
+    const float4 wlb = reinterpret_cast<const float4 *>(v.own.ang_vel)[ob];
+    float wax, way, waz, wbx, wby, wbz;
+    qrotf(qa, wla.x, wla.y, wla.z, wax, way, waz);
+    qrotf(qb, wlb.x, wlb.y, wlb.z, wbx, wby, wbz);
+    const float rotax = way * raz - waz * ray, rotay = waz * rax - wax * raz, rotaz = wax * ray - way * rax;
+    const float rotbx = wby * rbz - wbz * rby, rotby = wbz * rbx - wbx * rbz, rotbz = wbx * rby - wby * rbx;
+    const float vx = (va.x + rotax) - (vb.x + rotbx);
+    const float vy = (va.y + rotay) - (vb.y + rotby);
+    const float vz = (va.z + rotaz) - (vb.z + rotbz);
+    const uint32_t ma_meta = v.own.meta[oa], mb_meta = v.own.meta[ob];
+    const double ma = v.own.tpl[meta_tpl(ma_meta)].x, mb = v.own.tpl[meta_tpl(mb_meta)].x;
+    const float mass_eff = float((ma * mb) / (ma + mb));
+    const int ab = v.sph.mat[a] * nm + v.sph.mat[b];
+    float out[6];
+    hertz_mindlin_core_f32(depth, ts, bx, by, bz, vx, vy, vz, rotbx - rotax, rotby - rotay, rotbz - rotaz,
+                           mass_eff, offA.w, offB.w, float(v.mat.pair[ab]), float(v.mat.pair[mm + ab]),
+                           float(v.mat.pair[3 * mm + ab]), float(v.mat.pair[4 * mm + ab]), float(v.mat.beta[ab]),
+                           v.wild + 4 * size_t(k), out);
+    const float tx = out[0] + out[3], ty = out[1] + out[4], tz = out[2] + out[5];
+    const float ta[3] = {ray * tz - raz * ty, raz * tx - rax * tz, rax * ty - ray * tx};
+    const float tb[3] = {rby * tz - rbz * ty, rbz * tx - rbx * tz, rbx * ty - rby * tx};
+    const double2 sa = v.own.tpl_scale[meta_tpl(ma_meta)];
+    const double2 sbs = v.own.tpl_scale[meta_tpl(mb_meta)];
+    unsigned long long *fa = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(oa));
+    unsigned long long *fb = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(ob));
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      if (sa.x > 0.0) {
+        atomicAdd(fa + q, (unsigned long long)__double2ll_rn(double(out[q]) * sa.x));
+        atomicAdd(fa + 3 + q, (unsigned long long)__double2ll_rn(double(ta[q]) * sa.y));
+      } else {
+        atomicAdd(reinterpret_cast<double *>(fa + q), double(out[q]));
+        atomicAdd(reinterpret_cast<double *>(fa + 3 + q), double(ta[q]));
+      }
+      if (sbs.x > 0.0) {
+        atomicAdd(fb + q, (unsigned long long)__double2ll_rn(-double(out[q]) * sbs.x));
+        atomicAdd(fb + 3 + q, (unsigned long long)__double2ll_rn(-double(tb[q]) * sbs.y));
+      } else {
+        atomicAdd(reinterpret_cast<double *>(fb + q), -double(out[q]));
+        atomicAdd(reinterpret_cast<double *>(fb + 3 + q), -double(tb[q]));
+      }
+    }
+  }
 }
 
 // one contact's contribution to owner position p (A side +, B side -)
@@ -405,13 +536,15 @@ int dt_forces_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
   if (ev) cudaEventRecord(ev[0], s);
   if (v.n_acs) {
     unsigned long long *tn = c->tlist_n.as<unsigned long long>();
-    GF_CHECK(c, cudaMemsetAsync(tn, 0, sizeof(unsigned long long), s));
-    k_touch<<<unsigned((v.n_acs + 255) / 256), 256, 0, s>>>(v, c->tlist.as<uint32_t>(), tn,
-                                                             (unsigned long long)a.step);
+    uint32_t *list0 = c->tlist.as<uint32_t>(), *list1 = list0 + c->tlist_cap;
+    GF_CHECK(c, cudaMemsetAsync(tn, 0, 2 * sizeof(unsigned long long), s));
+    k_touch<<<unsigned((v.n_acs + 255) / 256), 256, 0, s>>>(v, list0, list1, tn, (unsigned long long)a.step);
     if (c->user_model) {
       if (launch_user_forces(c, v, a.h, a.sim_time, s)) return -1;
     } else {
-      k_forces<VelT><<<148 * 8, 128, 0, s>>>(v, a.h, a.sim_time, c->tlist.as<uint32_t>(), tn);
+      const bool fast = std::is_same<VelT, float>::value && c->wild_w == 4;
+      if (fast) k_forces_f32<<<148 * 8, 256, 0, s>>>(v, a.h, a.sim_time, list0, tn);
+      k_forces<VelT><<<fast ? 148 : 148 * 8, 128, 0, s>>>(v, a.h, a.sim_time, list0, list1, tn, fast ? 1 : 0);
     }
   }
   if (ev) cudaEventRecord(ev[1], s);

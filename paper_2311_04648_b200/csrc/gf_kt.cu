@@ -1368,9 +1368,12 @@ int build_segments(Ctx *c, Acs &a, cudaStream_t s) {
 int build_incidence(Ctx *c, cudaStream_t s) {
   const int64_t n = c->acs.n;
   const int64_t cap = std::max<int64_t>(c->acs.cap, 1);
-  if (ensure(c, c->tlist, sizeof(uint32_t) * cap, s) || ensure(c, c->tlist_n, 16, s) ||
+  // two compacted lists of touching entries: sphere-sphere at [0, cap), the
+  // other kinds at [cap, 2 cap)
+  if (ensure(c, c->tlist, 2 * sizeof(uint32_t) * cap, s) || ensure(c, c->tlist_n, 16, s) ||
       ensure(c, c->touch, cap, s))
     return -1;
+  c->tlist_cap = cap;
   if (c->fixed_reduce) return 0;  // throughput build reduces with atomics
   if (ensure(c, c->out_c, sizeof(double) * 9 * cap, s) || ensure(c, c->touch, cap, s) ||
       ensure(c, c->inc, sizeof(uint32_t) * cap, s) || ensure(c, c->inc_alt, sizeof(uint32_t) * cap, s) ||

@@ -304,6 +304,7 @@ class _RankState:
         self.global_store = global_store
         self.peers: dict = {}
         self.word = None
+        self.order = None         # global device order (Morton order of the first partition)
 
 
 def prepare(sim) -> None:
@@ -338,11 +339,15 @@ def prepare(sim) -> None:
     axis = dec.axis if dec.axis is not None else (prev.plan.axis if prev is not None else None)
     plan = plan_slabs(pos, eligible, reach, n_ranks, margin, travel, axis)
     cls = plan.classes(rank)
-    order = morton_order(pos)        # the single-context device order
+    # device order: the Morton order of the scene at the FIRST partition,
+    # kept for the scene's life (as a single context keeps its order), so
+    # every contact keeps its A/B orientation across repartitions
+    order = prev.order if prev is not None else morton_order(pos)
     ids = order[cls[order] >= 0]
     sub, geoms = g.subset(ids)
     dd = (cls[ids].astype(np.uint64) | (ids.astype(np.uint64) << np.uint64(2))).astype(np.uint32)
     st = _RankState(plan, rank, ids, geoms, dd, lever_max(g), g)
+    st.order = order
     # contact history handed over by a repartition: keep the pairs this piece holds
     acs = sim._acs0
     if acs.size:
@@ -701,7 +706,19 @@ def gather_state(sims, xport) -> dict:
     return state
 
 
-def repartition(sims, xport) -> None:
+def update_global(sim_or_group, edit) -> None:
+    """Host edit of a decomposed scene: gather the global state, apply
+    ``edit(global_store)`` on every member's copy of the scene, repartition.
+    Every rank calls it with the same edit (one process per GPU), or a
+    LoopbackGroup is passed."""
+    if isinstance(sim_or_group, LoopbackGroup):
+        sims, xport = sim_or_group.sims, _LoopbackTransport(sim_or_group.sims)
+    else:
+        sims, xport = [sim_or_group], _NcclTransport(sim_or_group)
+    repartition(sims, xport, edit)
+
+
+def repartition(sims, xport, edit=None) -> None:
     """Migration: gather every rank's owners and contact history, cut new
     slabs from the current positions and rebuild each rank's context (the
     history is carried over, so contacts keep their tangential state)."""
@@ -715,6 +732,8 @@ def repartition(sims, xport) -> None:
         for name in ("voxel", "subvoxel", "quat", "lin_vel", "ang_vel", "owner_family", "acc_force",
                      "acc_torque", "ext_force", "ext_torque"):
             d["_" + name][:n] = state[name]
+        if edit is not None:
+            edit(g)
     for s in sims:
         s._ctx.close()
         s._ctx = None
@@ -725,5 +744,6 @@ def repartition(sims, xport) -> None:
         s._host_stale = False
         s._host_dirty = False
         s.initialize()
-    for s in sims:
-        s.scheduler.repartitions = getattr(s.scheduler, "repartitions", 0) + 1
+    if edit is None:
+        for s in sims:
+            s.scheduler.repartitions = getattr(s.scheduler, "repartitions", 0) + 1

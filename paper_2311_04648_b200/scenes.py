@@ -32,7 +32,7 @@ G = 9.81
 def crater_bed(n_spheres: int = 1_000_000, *, seed: int = 7, h: float = 1e-5, v_err: float = 5.0,
                n_max: int = 4, precision: str = "f32", device: int = 0, ball: bool = True,
                drop_height: float = 0.20, ball_density: float = 7800.0, decomposition=None,
-               tiles: int = 1) -> Simulator:
+               tiles: int = 1, hold_ball: bool = False) -> Simulator:
     rng = np.random.default_rng(seed)
     D = 0.0254
     bed_half = 12.0 * D / 2.0
@@ -88,12 +88,64 @@ def crater_bed(n_spheres: int = 1_000_000, *, seed: int = 7, h: float = 1e-5, v_
         surface = float(pts[:, 2].max()) + r_max
         for x_off in offsets:
             b = sim.add_clumps(btpl, [[x_off, 0.0, surface + R + 2e-3]])[0]
-            sim.track(b).set_vel([0.0, 0.0, -math.sqrt(2.0 * G * drop_height)])
+            if hold_ball:   # parked (family 1, fixed) while the bed settles; see release_balls
+                sim.store.owner_family[b] = 1
+            else:
+                sim.track(b).set_vel([0.0, 0.0, -math.sqrt(2.0 * G * drop_height)])
+        if hold_ball:
+            sim.set_family_fixed(1)
     sim.set_gravity([0, 0, -G])
     sim.set_init_time_step(h)
     sim.set_error_out_velocity(v_err)
     sim.set_fixed_lookahead(n_max)
     return sim
+
+
+def release_balls(sim: Simulator, drop_height: float = 0.20) -> list:
+    """After the bed settled (crater_bed(hold_ball=True)): every parked
+    projectile (family 1) moves to 2 mm above the highest grain under its
+    footprint with the
+    free-fall speed of a `drop_height` drop, and becomes free (family 0) --
+    the reference's settle-then-drop order (scenarios.py:255-307).  Works on
+    a decomposed simulator too (a global edit, decomp.update_global)."""
+    from .core import GEOM_SPHERE, OWNER_CLUMP, decode_position
+
+    def edit(store):
+        n = store.n_owners
+        d = store.__dict__
+        pos = decode_position(d["_voxel"][:n], d["_subvoxel"][:n], store.domain)
+        fam = d["_owner_family"][:n]
+        kind = d["_owner_kind"][:n]
+        ng = store.n_geoms
+        go = d["_geom_owner"][:ng]
+        sph = d["_geom_kind"][:ng] == GEOM_SPHERE
+        rad = np.zeros(n)
+        np.maximum.at(rad, go[sph], d["_geom_params"][:ng][sph, 3].astype(np.float64))
+        balls = np.nonzero((fam == 1) & (kind == OWNER_CLUMP))[0]
+        grains = (fam == 0) & (kind == OWNER_CLUMP)
+        v = -math.sqrt(2.0 * G * drop_height)
+        for b in balls:
+            # clear the highest grain under the ball's footprint
+            rho = np.hypot(pos[:, 0] - pos[b, 0], pos[:, 1] - pos[b, 1])
+            near = grains & (rho < rad[b] + rad + 1e-3)
+            top = float(np.max(pos[near, 2] + rad[near]))
+            xyz = np.array([pos[b, 0], pos[b, 1], top + rad[b] + 2e-3])
+            store.set_position(int(b), xyz)
+            d["_lin_vel"][b] = (0.0, 0.0, v)
+            d["_ang_vel"][b] = 0.0
+            d["_owner_family"][b] = 0
+        return balls.tolist()
+
+    if sim.decomposition is not None:
+        from . import decomp
+        target = sim.decomposition.group if sim.decomposition.group is not None else sim
+        decomp.update_global(target, edit)
+        return []
+    s = sim.store
+    s.voxel  # sync the host mirror
+    out = edit(s)
+    sim._host_dirty = True
+    return out
 
 
 def settling_box(n_spheres: int = 10_000, *, h: float = 1e-5, v_err: float = 5.0, n_max: int = 4,
