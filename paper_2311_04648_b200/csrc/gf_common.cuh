@@ -89,6 +89,16 @@ __host__ __device__ inline bool dd_keep(const uint32_t *dd, uint32_t oa, uint32_
   return ca == kDdPrimary && cb == kDdPrimary;
 }
 
+// Per-sphere kinematics record of the throughput build, written wherever the
+// sphere centres are (integrator, refresh, halo unpack) so the contact kernel
+// reaches everything it needs one load after the contact list:
+// v = owner linear velocity, w = owner angular velocity (global frame),
+// r = centre minus owner position, id = (owner, material, -, -).
+struct SphKin {
+  float4 v, w, r;
+  uint4 id;
+};
+
 struct Spheres {
   int64_t n;
   uint32_t *owner;
@@ -96,6 +106,7 @@ struct Spheres {
   uint8_t *mat;
   double4 *center;     // world centre + radius, refreshed by the integrator
   uint32_t *first;     // [n_owner + 1] CSR: spheres of owner o are [first[o], first[o+1])
+  SphKin *kin;         // throughput build only (fp32 velocities), else nullptr
 };
 
 struct Tris {
@@ -203,6 +214,29 @@ __device__ __forceinline__ void qrot(double qw, double qx, double qy, double qz,
   rx = add(vx, mul(2.0, sub_(mul(qy, tz), mul(qz, ty))));
   ry = add(vy, mul(2.0, sub_(mul(qz, tx), mul(qx, tz))));
   rz = add(vz, mul(2.0, sub_(mul(qx, ty), mul(qy, tx))));
+}
+
+// kinematics record from the STORED owner state (quaternion, float32
+// velocities), identical wherever it is computed
+__device__ __forceinline__ void write_kin(const Spheres &sph, uint32_t k, uint32_t o, const float4 q,
+                                          const float4 lv, const float4 av) {
+  const float4 orr = sph.offr[k];
+  double r[3], w[3];
+  qrot(double(q.x), double(q.y), double(q.z), double(q.w), double(orr.x), double(orr.y), double(orr.z), r[0], r[1],
+       r[2]);
+  qrot(double(q.x), double(q.y), double(q.z), double(q.w), double(av.x), double(av.y), double(av.z), w[0], w[1],
+       w[2]);
+  SphKin kr;
+  kr.v = make_float4(lv.x, lv.y, lv.z, 0.f);
+  kr.w = make_float4(float(w[0]), float(w[1]), float(w[2]), 0.f);
+  kr.r = make_float4(float(r[0]), float(r[1]), float(r[2]), 0.f);
+  kr.id = make_uint4(o, sph.mat[k], 0u, 0u);
+  sph.kin[k] = kr;
+}
+
+__device__ __forceinline__ void write_kin_from_state(const Owners &own, const Spheres &sph, uint32_t k, uint32_t o) {
+  write_kin(sph, k, o, own.quat[o], reinterpret_cast<const float4 *>(own.lin_vel)[o],
+            reinterpret_cast<const float4 *>(own.ang_vel)[o]);
 }
 
 // sphere world centre: owner pos + q * offset (_kernels.py:91-106)

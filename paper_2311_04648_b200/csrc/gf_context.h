@@ -84,6 +84,7 @@ struct Ctx {
   // geometry
   int64_t n_sph = 0, n_tri = 0, n_ana = 0;
   DBuf sph_owner, sph_offr, sph_mat, sph_center, sph_first;
+  DBuf sph_kin;  // SphKin per sphere (fp32-velocity build)
   DBuf tri_owner, tri_local, tri_mat, tri_world;
   DBuf ana_owner, ana_kind, ana_local, ana_mat, ana_world;
   bool world_moving = true;  // any tri/ana owner not fixed

@@ -54,7 +54,17 @@ struct DtView {
   const unsigned long long *n_heavy;
   double *heavy_acc;    // [n_owner*6] (only heavy owners written)
   Status *st;
+  int acc_all;          // throughput build: also accumulate onto passive owners (write_acc step)
 };
+
+// An owner whose accumulated force never feeds its motion: fixed, or every
+// velocity component prescribed (walls).  The throughput build accumulates
+// onto it only on the step whose accumulators are reported (write_acc);
+// thousands of wall contacts would otherwise serialise on its six words.
+__device__ __forceinline__ bool passive_owner(const DtView &v, uint32_t o) {
+  const uint32_t f = meta_family(v.own.meta[o]);
+  return (v.fam.flags[f] & kFamFixed) || (v.fam.lv_mask[f] == 7 && v.fam.av_mask[f] == 7);
+}
 
 template <typename VelT>
 __device__ __forceinline__ void owner_kin(const DtView &v, uint32_t o, double pos[3], double vel[3],
@@ -395,15 +405,19 @@ __device__ __forceinline__ void force_entry(const DtView &v, uint32_t k, double 
     unsigned long long *fb = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(ob));
     const double ta[3] = {ray * tz - raz * ty, raz * tx - rax * tz, rax * ty - ray * tx};
     const double tb[3] = {rby * tz - rbz * ty, rbz * tx - rbx * tz, rbx * ty - rby * tx};
+    const bool skip_a = !v.acc_all && passive_owner(v, oa);
+    const bool skip_b = !v.acc_all && passive_owner(v, ob);
     for (int q = 0; q < 3; ++q) {
-      if (sa.x > 0.0) {
+      if (skip_a) {
+      } else if (sa.x > 0.0) {
         atomicAdd(fa + q, (unsigned long long)__double2ll_rn(out[q] * sa.x));
         atomicAdd(fa + 3 + q, (unsigned long long)__double2ll_rn(ta[q] * sa.y));
       } else {
         atomicAdd(reinterpret_cast<double *>(fa + q), out[q]);
         atomicAdd(reinterpret_cast<double *>(fa + 3 + q), ta[q]);
       }
-      if (sbs.x > 0.0) {
+      if (skip_b) {
+      } else if (sbs.x > 0.0) {
         atomicAdd(fb + q, (unsigned long long)__double2ll_rn(-out[q] * sbs.x));
         atomicAdd(fb + 3 + q, (unsigned long long)__double2ll_rn(-tb[q] * sbs.y));
       } else {

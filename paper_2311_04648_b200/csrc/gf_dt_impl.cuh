@@ -33,7 +33,8 @@ namespace {
 // fp64 parity build also records a touch flag per entry for its reduction.
 // A false positive leaves its history untouched (forces.py:95-97).
 __global__ void __launch_bounds__(256, 4) k_touch(DtView v, uint32_t *tlist, uint32_t *tlist_other,
-                                                  unsigned long long *tlist_n, unsigned long long step) {
+                                                  unsigned long long *tlist_n, unsigned long long step,
+                                                  int records) {
   __shared__ int s_live;
   __shared__ unsigned s_cnt[2][8], s_tch[8], s_off[2][8];
   __shared__ unsigned long long s_base[2];
@@ -43,13 +44,21 @@ __global__ void __launch_bounds__(256, 4) k_touch(DtView v, uint32_t *tlist, uin
   const int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   bool t = false;
   unsigned kind = 0;
+  uint2 id = make_uint2(0, 0);
   if (k < v.n_acs && s_live) {
-    const uint2 id = v.ids[k];
+    id = v.ids[k];
     kind = id.y >> kKindShift;
-    double ca[3], ra, depth, bx, by, bz, rb;
-    contact_geometry(v, id, ca, ra, depth, bx, by, bz, rb);
-    t = depth > 0.0;
-    if (!v.own.facc) v.touch[k] = t ? 1 : 0;
+    if (v.own.facc && kind == 0) {
+      // throughput build: d^2 < (ra + rb)^2, the predicate k_forces_f32 uses
+      const double4 cA = v.sph.center[id.x], cB = v.sph.center[id.y & kSlotMask];
+      const double dx = cA.x - cB.x, dy = cA.y - cB.y, dz = cA.z - cB.z, R = cA.w + cB.w;
+      t = float(R * R - (dx * dx + dy * dy + dz * dz)) > 0.f;
+    } else {
+      double ca[3], ra, depth, bx, by, bz, rb;
+      contact_geometry(v, id, ca, ra, depth, bx, by, bz, rb);
+      t = depth > 0.0;
+      if (!v.own.facc) v.touch[k] = t ? 1 : 0;
+    }
   }
   // block-aggregated appends (ascending k within the block): sphere-sphere
   // entries to tlist, the other kinds to tlist_other; one atomic per block
@@ -81,7 +90,13 @@ __global__ void __launch_bounds__(256, 4) k_touch(DtView v, uint32_t *tlist, uin
   }
   __syncthreads();
   const unsigned lt = (1u << lane) - 1u;
-  if (t && kind == 0) tlist[s_base[0] + s_off[0][warp] + __popc(m0 & lt)] = uint32_t(k);
+  if (t && kind == 0) {
+    const unsigned long long pos = s_base[0] + s_off[0][warp] + __popc(m0 & lt);
+    if (records)   // (a, b, k) for k_forces_f32: no dependent load of ids[k]
+      reinterpret_cast<uint4 *>(tlist)[pos] = make_uint4(id.x, id.y & kSlotMask, uint32_t(k), 0u);
+    else
+      tlist[pos] = uint32_t(k);
+  }
   if (t && kind != 0) tlist_other[s_base[1] + s_off[1][warp] + __popc(m1 & lt)] = uint32_t(k);
 }
 
@@ -116,84 +131,123 @@ __device__ __forceinline__ void qrotf(const float4 q, float x, float y, float z,
 // after in fp32 (normal, lever arms from the fp32-rotated clump offsets,
 // velocities, the contact law).  The other kinds (walls) take k_forces.
 // Contributions go to the int64 fixed-point owner accumulators as before.
+// Sum of v over this lane's run [lane, run_end] of equal keys, left in the
+// run's head lane (segmented reduction; all 32 lanes take part).
+__device__ __forceinline__ long long run_sum(long long v, int lane, int run_end) {
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const long long o = __shfl_down_sync(0xffffffffu, v, off);
+    if (lane + off <= run_end) v += o;
+  }
+  return v;
+}
+
 static __global__ void __launch_bounds__(256, 3) k_forces_f32(DtView v, double ts_d, double sim_time,
-                                                    const uint32_t *tlist, const unsigned long long *tlist_n) {
+                                                               const uint4 *rec, const unsigned long long *tlist_n) {
+  (void)sim_time;
   if (v.st->err) return;
   const unsigned long long n = *tlist_n;
   const float ts = float(ts_d);
   const int nm = v.mat.n_mat, mm = nm * nm;
-  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
-       i += (unsigned long long)gridDim.x * blockDim.x) {
-    const uint32_t k = tlist[i];
-    const uint2 id = v.ids[k];
-    const uint32_t a = id.x, b = id.y & kSlotMask;
-    const double4 cA = v.sph.center[a], cB = v.sph.center[b];
-    const double dx = cA.x - cB.x, dy = cA.y - cB.y, dz = cA.z - cB.z;
-    const double d2 = dx * dx + dy * dy + dz * dz;
-    const double R = cA.w + cB.w;
-    const float num = float(R * R - d2);
-    if (!(num > 0.f)) continue;
-    const float fdx = float(dx), fdy = float(dy), fdz = float(dz);
-    const float d = sqrtf(float(d2));
-    const float depth = num / (float(R) + d);
-    float bx = 0.f, by = 0.f, bz = 1.f;
-    if (d > 1e-30f) {
-      const float inv = 1.f / d;
-      bx = fdx * inv; by = fdy * inv; bz = fdz * inv;
-    }
-    const uint32_t oa = v.sph.owner[a], ob = v.sph.owner[b];
-    const float4 offA = v.sph.offr[a], offB = v.sph.offr[b];
-    const float4 qa = v.own.quat[oa], qb = v.own.quat[ob];
-    // contact point p = cA - b (ra - depth / 2); lever arms p - pos_a, p - pos_b
-    const float ha = offA.w - 0.5f * depth;
-    float rax, ray, raz, rbx, rby, rbz;
-    qrotf(qa, offA.x, offA.y, offA.z, rax, ray, raz);
-    qrotf(qb, offB.x, offB.y, offB.z, rbx, rby, rbz);
-    rbx += fdx - bx * ha; rby += fdy - by * ha; rbz += fdz - bz * ha;
-    rax -= bx * ha; ray -= by * ha; raz -= bz * ha;
-    const float4 va = reinterpret_cast<const float4 *>(v.own.lin_vel)[oa];
-    const float4 vb = reinterpret_cast<const float4 *>(v.own.lin_vel)[ob];
-    const float4 wla = reinterpret_cast<const float4 *>(v.own.ang_vel)[oa];
-    const float4 wlb = reinterpret_cast<const float4 *>(v.own.ang_vel)[ob];
-    float wax, way, waz, wbx, wby, wbz;
-    qrotf(qa, wla.x, wla.y, wla.z, wax, way, waz);
-    qrotf(qb, wlb.x, wlb.y, wlb.z, wbx, wby, wbz);
-    const float rotax = way * raz - waz * ray, rotay = waz * rax - wax * raz, rotaz = wax * ray - way * rax;
-    const float rotbx = wby * rbz - wbz * rby, rotby = wbz * rbx - wbx * rbz, rotbz = wbx * rby - wby * rbx;
-    const float vx = (va.x + rotax) - (vb.x + rotbx);
-    const float vy = (va.y + rotay) - (vb.y + rotby);
-    const float vz = (va.z + rotaz) - (vb.z + rotbz);
-    const uint32_t ma_meta = v.own.meta[oa], mb_meta = v.own.meta[ob];
-    const double ma = v.own.tpl[meta_tpl(ma_meta)].x, mb = v.own.tpl[meta_tpl(mb_meta)].x;
-    const float mass_eff = float((ma * mb) / (ma + mb));
-    const int ab = v.sph.mat[a] * nm + v.sph.mat[b];
-    float out[6];
-    hertz_mindlin_core_f32(depth, ts, bx, by, bz, vx, vy, vz, rotbx - rotax, rotby - rotay, rotbz - rotaz,
-                           mass_eff, offA.w, offB.w, float(v.mat.pair[ab]), float(v.mat.pair[mm + ab]),
-                           float(v.mat.pair[3 * mm + ab]), float(v.mat.pair[4 * mm + ab]), float(v.mat.beta[ab]),
-                           v.wild + 4 * size_t(k), out);
-    const float tx = out[0] + out[3], ty = out[1] + out[4], tz = out[2] + out[5];
-    const float ta[3] = {ray * tz - raz * ty, raz * tx - rax * tz, rax * ty - ray * tx};
-    const float tb[3] = {rby * tz - rbz * ty, rbz * tx - rbx * tz, rbx * ty - rby * tx};
-    const double2 sa = v.own.tpl_scale[meta_tpl(ma_meta)];
-    const double2 sbs = v.own.tpl_scale[meta_tpl(mb_meta)];
-    unsigned long long *fa = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(oa));
-    unsigned long long *fb = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(ob));
+  const int lane = threadIdx.x & 31;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  // whole warps iterate together (the A-side reduction needs every lane)
+  for (unsigned long long base = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) & ~31ull; base < n;
+       base += stride) {
+    const unsigned long long i = base + lane;
+    float out[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    float ta[3] = {0.f, 0.f, 0.f};
+    uint32_t oa = 0xFFFFFFFFu, ma_meta = 0;
+    bool live = false;
+    if (i < n) {
+      const uint4 t = rec[i];   // sphere A, sphere B, contact index
+      const uint32_t a = t.x, b = t.y, k = t.z;
+      const double4 cA = v.sph.center[a], cB = v.sph.center[b];
+      const SphKin ka = v.sph.kin[a], kb = v.sph.kin[b];
+      const double dx = cA.x - cB.x, dy = cA.y - cB.y, dz = cA.z - cB.z;
+      const double d2 = dx * dx + dy * dy + dz * dz;
+      const double R = cA.w + cB.w;
+      const float num = float(R * R - d2);
+      if (num > 0.f) {
+        live = true;
+        const float fdx = float(dx), fdy = float(dy), fdz = float(dz);
+        const float d = sqrtf(float(d2));
+        const float depth = num / (float(R) + d);
+        float bx = 0.f, by = 0.f, bz = 1.f;
+        if (d > 1e-30f) {
+          const float inv = 1.f / d;
+          bx = fdx * inv; by = fdy * inv; bz = fdz * inv;
+        }
+        oa = ka.id.x;
+        const uint32_t ob = kb.id.x;
+        ma_meta = v.own.meta[oa];
+        const uint32_t mb_meta = v.own.meta[ob];
+        // contact point p = cA - b (ra - depth / 2); lever arms p - pos_a, p - pos_b
+        const float ha = float(cA.w) - 0.5f * depth;
+        const float rax = ka.r.x - bx * ha, ray = ka.r.y - by * ha, raz = ka.r.z - bz * ha;
+        const float rbx = kb.r.x + fdx - bx * ha, rby = kb.r.y + fdy - by * ha, rbz = kb.r.z + fdz - bz * ha;
+        const float rotax = ka.w.y * raz - ka.w.z * ray, rotay = ka.w.z * rax - ka.w.x * raz,
+                    rotaz = ka.w.x * ray - ka.w.y * rax;
+        const float rotbx = kb.w.y * rbz - kb.w.z * rby, rotby = kb.w.z * rbx - kb.w.x * rbz,
+                    rotbz = kb.w.x * rby - kb.w.y * rbx;
+        const float vx = (ka.v.x + rotax) - (kb.v.x + rotbx);
+        const float vy = (ka.v.y + rotay) - (kb.v.y + rotby);
+        const float vz = (ka.v.z + rotaz) - (kb.v.z + rotbz);
+        const double ma = v.own.tpl[meta_tpl(ma_meta)].x, mb = v.own.tpl[meta_tpl(mb_meta)].x;
+        const float mass_eff = float((ma * mb) / (ma + mb));
+        const int ab = int(ka.id.y) * nm + int(kb.id.y);
+        hertz_mindlin_core_f32(depth, ts, bx, by, bz, vx, vy, vz, rotbx - rotax, rotby - rotay, rotbz - rotaz,
+                               mass_eff, float(cA.w), float(cB.w), float(v.mat.pair[ab]),
+                               float(v.mat.pair[mm + ab]), float(v.mat.pair[3 * mm + ab]),
+                               float(v.mat.pair[4 * mm + ab]), float(v.mat.beta[ab]), v.wild + 4 * size_t(k), out);
+        const float tx = out[0] + out[3], ty = out[1] + out[4], tz = out[2] + out[5];
+        ta[0] = ray * tz - raz * ty; ta[1] = raz * tx - rax * tz; ta[2] = rax * ty - ray * tx;
+        const float tb[3] = {rby * tz - rbz * ty, rbz * tx - rbx * tz, rbx * ty - rby * tx};
+        // B side: one atomic per word (B owners are scattered)
+        if (v.acc_all || !passive_owner(v, ob)) {
+          const double2 sbs = v.own.tpl_scale[meta_tpl(mb_meta)];
+          unsigned long long *fb = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(ob));
 #pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      if (sa.x > 0.0) {
-        atomicAdd(fa + q, (unsigned long long)__double2ll_rn(double(out[q]) * sa.x));
-        atomicAdd(fa + 3 + q, (unsigned long long)__double2ll_rn(double(ta[q]) * sa.y));
-      } else {
+          for (int q = 0; q < 3; ++q) {
+            if (sbs.x > 0.0) {
+              atomicAdd(fb + q, (unsigned long long)__double2ll_rn(-double(out[q]) * sbs.x));
+              atomicAdd(fb + 3 + q, (unsigned long long)__double2ll_rn(-double(tb[q]) * sbs.y));
+            } else {
+              atomicAdd(reinterpret_cast<double *>(fb + q), -double(out[q]));
+              atomicAdd(reinterpret_cast<double *>(fb + 3 + q), -double(tb[q]));
+            }
+          }
+        }
+      }
+    }
+    // A side: entries are in A-sorted contact order, so equal A owners sit in
+    // consecutive lanes -- sum each run's int64 words in registers (exact)
+    // and let the run's head lane add them
+    double2 sa = make_double2(0.0, 0.0);
+    bool use_a = live && (v.acc_all || !passive_owner(v, oa));
+    if (use_a) sa = v.own.tpl_scale[meta_tpl(ma_meta)];
+    const bool fixed_a = use_a && sa.x > 0.0;
+    if (use_a && !fixed_a) {   // boundary owner: fp64 atomics, not aggregated
+      unsigned long long *fa = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(oa));
+      for (int q = 0; q < 3; ++q) {
         atomicAdd(reinterpret_cast<double *>(fa + q), double(out[q]));
         atomicAdd(reinterpret_cast<double *>(fa + 3 + q), double(ta[q]));
       }
-      if (sbs.x > 0.0) {
-        atomicAdd(fb + q, (unsigned long long)__double2ll_rn(-double(out[q]) * sbs.x));
-        atomicAdd(fb + 3 + q, (unsigned long long)__double2ll_rn(-double(tb[q]) * sbs.y));
-      } else {
-        atomicAdd(reinterpret_cast<double *>(fb + q), -double(out[q]));
-        atomicAdd(reinterpret_cast<double *>(fb + 3 + q), -double(tb[q]));
+    }
+    const uint32_t key = fixed_a ? oa : 0xFFFFFFFFu;
+    const uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
+    const bool head = lane == 0 || prev != key;
+    const unsigned heads = __ballot_sync(0xffffffffu, head);
+    const unsigned later = heads & ~((2u << lane) - 1u);   // heads after this lane
+    const int run_end = later ? __ffs(later) - 2 : 31;
+    unsigned long long *fa = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(fixed_a ? oa : 0));
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const long long f = run_sum(fixed_a ? __double2ll_rn(double(out[q]) * sa.x) : 0ll, lane, run_end);
+      const long long t = run_sum(fixed_a ? __double2ll_rn(double(ta[q]) * sa.y) : 0ll, lane, run_end);
+      if (head && fixed_a) {
+        atomicAdd(fa + q, (unsigned long long)f);
+        atomicAdd(fa + 3 + q, (unsigned long long)t);
       }
     }
   }
@@ -438,6 +492,7 @@ __global__ void __launch_bounds__(128) k_integrate(DtView v, double h, double gx
       qrot(double(q.x), double(q.y), double(q.z), double(q.w), double(orr.x), double(orr.y), double(orr.z),
            r[0], r[1], r[2]);
       v.sph.center[k] = make_double4(add(pd[0], r[0]), add(pd[1], r[1]), add(pd[2], r[2]), double(orr.w));
+      if (v.sph.kin) write_kin_from_state(v.own, v.sph, k, o);
     }
   }
 }
@@ -460,6 +515,7 @@ __global__ void k_centers(Domain dom, Owners own, Spheres sph) {
   uint32_t o;
   sphere_center(dom, own, sph, uint32_t(k), c, r, o);
   sph.center[k] = make_double4(c[0], c[1], c[2], double(r));
+  if (sph.kin) write_kin_from_state(own, sph, uint32_t(k), o);
 }
 
 // triangle / analytic world transforms (_kernels.py:109-152)
@@ -522,6 +578,7 @@ static DtView dt_view(Ctx *c) {
   v.n_heavy = c->heavy_count.as<unsigned long long>();
   v.heavy_acc = c->heavy_acc.as<double>();
   v.st = c->status.as<Status>();
+  v.acc_all = 1;
   return v;
 }
 
@@ -531,20 +588,26 @@ static DtView dt_view(Ctx *c) {
 template <typename VelT>
 int dt_forces_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
   DtView v = dt_view<VelT>(c);
+  v.acc_all = a.write_acc;
   GF_CHECK(c, cudaMemsetAsync(&v.st->touching, 0, sizeof(unsigned long long), s));
   cudaEvent_t *ev = prof_events(c);
   if (ev) cudaEventRecord(ev[0], s);
   if (v.n_acs) {
     unsigned long long *tn = c->tlist_n.as<unsigned long long>();
-    uint32_t *list0 = c->tlist.as<uint32_t>(), *list1 = list0 + c->tlist_cap;
+    // list0: sphere-sphere entries (uint4 records in the fused build), list1: the other kinds
+    uint32_t *list0 = c->tlist.as<uint32_t>(), *list1 = list0 + 4 * c->tlist_cap;
     GF_CHECK(c, cudaMemsetAsync(tn, 0, 2 * sizeof(unsigned long long), s));
-    k_touch<<<unsigned((v.n_acs + 255) / 256), 256, 0, s>>>(v, list0, list1, tn, (unsigned long long)a.step);
+    // throughput build + built-in model: sphere-sphere contacts take the fp32
+    // path (k_forces_f32), the wall kinds the generic k_forces
+    const bool fused = std::is_same<VelT, float>::value && c->wild_w == 4 && !c->user_model && v.sph.kin;
+    k_touch<<<unsigned((v.n_acs + 255) / 256), 256, 0, s>>>(v, list0, list1, tn, (unsigned long long)a.step,
+                                                             fused ? 1 : 0);
+    if (fused)
+      k_forces_f32<<<148 * 8, 256, 0, s>>>(v, a.h, a.sim_time, reinterpret_cast<const uint4 *>(list0), tn);
     if (c->user_model) {
       if (launch_user_forces(c, v, a.h, a.sim_time, s)) return -1;
     } else {
-      const bool fast = std::is_same<VelT, float>::value && c->wild_w == 4;
-      if (fast) k_forces_f32<<<148 * 8, 256, 0, s>>>(v, a.h, a.sim_time, list0, tn);
-      k_forces<VelT><<<fast ? 148 : 148 * 8, 128, 0, s>>>(v, a.h, a.sim_time, list0, list1, tn, fast ? 1 : 0);
+      k_forces<VelT><<<fused ? 148 : 148 * 8, 128, 0, s>>>(v, a.h, a.sim_time, list0, list1, tn, fused ? 1 : 0);
     }
   }
   if (ev) cudaEventRecord(ev[1], s);

@@ -78,6 +78,7 @@ __global__ void k_owner_centers(Domain dom, Owners own, Spheres sph, const uint3
     uint32_t ow;
     sphere_center(dom, own, sph, k, c, rad, ow);
     sph.center[k] = make_double4(c[0], c[1], c[2], double(rad));
+    if (sph.kin) write_kin_from_state(own, sph, k, o);
   }
 }
 

@@ -1368,9 +1368,9 @@ int build_segments(Ctx *c, Acs &a, cudaStream_t s) {
 int build_incidence(Ctx *c, cudaStream_t s) {
   const int64_t n = c->acs.n;
   const int64_t cap = std::max<int64_t>(c->acs.cap, 1);
-  // two compacted lists of touching entries: sphere-sphere at [0, cap), the
-  // other kinds at [cap, 2 cap)
-  if (ensure(c, c->tlist, 2 * sizeof(uint32_t) * cap, s) || ensure(c, c->tlist_n, 16, s) ||
+  // two compacted lists of touching entries: sphere-sphere (uint4 records)
+  // at [0, 4 cap) words, the other kinds at [4 cap, 5 cap)
+  if (ensure(c, c->tlist, 5 * sizeof(uint32_t) * cap, s) || ensure(c, c->tlist_n, 16, s) ||
       ensure(c, c->touch, cap, s))
     return -1;
   c->tlist_cap = cap;
