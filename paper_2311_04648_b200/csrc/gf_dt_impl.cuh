@@ -19,6 +19,7 @@
 //                prescriptions, quaternion renormalisation, re-encode /
 //                decode and the watchdog (_kernels.py:548-670) -- fused.
 #pragma once
+#include <algorithm>
 #include <type_traits>
 #include "gf_context.h"
 #include "gf_device.cuh"
@@ -32,72 +33,120 @@ namespace {
 // Touching entries are compacted into tlist (warp-aggregated append); the
 // fp64 parity build also records a touch flag per entry for its reduction.
 // A false positive leaves its history untouched (forces.py:95-97).
-__global__ void __launch_bounds__(256, 4) k_touch(DtView v, uint32_t *tlist, uint32_t *tlist_other,
-                                                  unsigned long long *tlist_n, unsigned long long step,
-                                                  int records) {
-  __shared__ int s_live;
+// Block-aggregated append of per-thread counts: returns this thread's first
+// output slot in each list; one atomic per block per counter.
+__device__ __forceinline__ void block_append(unsigned c0, unsigned c1, unsigned tch, unsigned long long *tlist_n,
+                                             Status *st, unsigned long long &w0, unsigned long long &w1) {
   __shared__ unsigned s_cnt[2][8], s_tch[8], s_off[2][8];
   __shared__ unsigned long long s_base[2];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_live = !v.st->err && v.st->dd_trip >= step;
-  __syncthreads();
-  const int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  bool t = false;
-  unsigned kind = 0;
-  uint2 id = make_uint2(0, 0);
-  if (k < v.n_acs && s_live) {
-    id = v.ids[k];
-    kind = id.y >> kKindShift;
-    if (v.own.facc && kind == 0) {
-      // throughput build: d^2 < (ra + rb)^2, the predicate k_forces_f32 uses
-      const double4 cA = v.sph.center[id.x], cB = v.sph.center[id.y & kSlotMask];
-      const double dx = cA.x - cB.x, dy = cA.y - cB.y, dz = cA.z - cB.z, R = cA.w + cB.w;
-      t = float(R * R - (dx * dx + dy * dy + dz * dz)) > 0.f;
-    } else {
-      double ca[3], ra, depth, bx, by, bz, rb;
-      contact_geometry(v, id, ca, ra, depth, bx, by, bz, rb);
-      t = depth > 0.0;
-      if (!v.own.facc) v.touch[k] = t ? 1 : 0;
-    }
+  unsigned p0 = c0, p1 = c1;   // inclusive warp scans
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned u0 = __shfl_up_sync(0xffffffffu, p0, off), u1 = __shfl_up_sync(0xffffffffu, p1, off);
+    if (lane >= off) { p0 += u0; p1 += u1; }
   }
-  // block-aggregated appends (ascending k within the block): sphere-sphere
-  // entries to tlist, the other kinds to tlist_other; one atomic per block
-  // on each shared counter
-  const unsigned m0 = __ballot_sync(0xffffffffu, t && kind == 0);
-  const unsigned m1 = __ballot_sync(0xffffffffu, t && kind != 0);
-  unsigned touching = t ? (kind == 0 ? 2u : 1u) : 0u;
-  for (int off = 16; off > 0; off >>= 1) touching += __shfl_down_sync(0xffffffffu, touching, off);
-  if (lane == 0) {
-    s_cnt[0][warp] = __popc(m0);
-    s_cnt[1][warp] = __popc(m1);
-    s_tch[warp] = touching;
+  for (int off = 16; off > 0; off >>= 1) tch += __shfl_down_sync(0xffffffffu, tch, off);
+  if (lane == 31) {
+    s_cnt[0][warp] = p0;
+    s_cnt[1][warp] = p1;
   }
+  if (lane == 0) s_tch[warp] = tch;
   __syncthreads();
   if (threadIdx.x == 0) {
-    unsigned tot[2] = {0, 0}, tch = 0;
+    unsigned tot[2] = {0, 0}, tt = 0;
     for (int w = 0; w < int(blockDim.x >> 5); ++w) {
       for (int l = 0; l < 2; ++l) {
         s_off[l][w] = tot[l];
         tot[l] += s_cnt[l][w];
       }
-      tch += s_tch[w];
+      tt += s_tch[w];
     }
     for (int l = 0; l < 2; ++l) s_base[l] = tot[l] ? atomicAdd(tlist_n + l, (unsigned long long)tot[l]) : 0ull;
     if (tot[0] + tot[1]) {
-      atomicAdd(&v.st->touching, (unsigned long long)tch);
-      atomicAdd(&v.st->touch_pairs, (unsigned long long)(tot[0] + tot[1]));
+      atomicAdd(&st->touching, (unsigned long long)tt);
+      atomicAdd(&st->touch_pairs, (unsigned long long)(tot[0] + tot[1]));
     }
   }
   __syncthreads();
-  const unsigned lt = (1u << lane) - 1u;
-  if (t && kind == 0) {
-    const unsigned long long pos = s_base[0] + s_off[0][warp] + __popc(m0 & lt);
-    if (records)   // (a, b, k) for k_forces_f32: no dependent load of ids[k]
-      reinterpret_cast<uint4 *>(tlist)[pos] = make_uint4(id.x, id.y & kSlotMask, uint32_t(k), 0u);
-    else
-      tlist[pos] = uint32_t(k);
+  w0 = s_base[0] + s_off[0][warp] + (p0 - c0);
+  w1 = s_base[1] + s_off[1][warp] + (p1 - c1);
+}
+
+// Generic narrow phase over entries [*k0p, n_acs) (from 0 if k0p is null):
+// all kinds (parity build / user models) or -- in the throughput build, where
+// k_touch_ss takes the sphere-sphere block -- only the wall kinds.  Block-
+// uniform grid-stride loop (the tail's length is known only on the device).
+__global__ void __launch_bounds__(256, 4) k_touch(DtView v, uint32_t *tlist, uint32_t *tlist_other,
+                                                  unsigned long long *tlist_n, unsigned long long step,
+                                                  const unsigned long long *k0p) {
+  __shared__ int s_live;
+  if (threadIdx.x == 0) s_live = !v.st->err && v.st->dd_trip >= step;
+  __syncthreads();
+  if (!s_live) return;
+  const int64_t start = k0p ? int64_t(*k0p) : 0;
+  for (int64_t base = start + blockIdx.x * int64_t(blockDim.x); base < v.n_acs;
+       base += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t k = base + threadIdx.x;
+    bool t = false;
+    unsigned kind = 0;
+    if (k < v.n_acs) {
+      const uint2 id = v.ids[k];
+      kind = id.y >> kKindShift;
+      double ca[3], ra, depth, bx, by, bz, rb;
+      contact_geometry(v, id, ca, ra, depth, bx, by, bz, rb);
+      t = depth > 0.0;
+      if (!v.own.facc) v.touch[k] = t ? 1 : 0;
+    }
+    unsigned long long w0, w1;
+    block_append((t && kind == 0) ? 1u : 0u, (t && kind != 0) ? 1u : 0u, t ? (kind == 0 ? 2u : 1u) : 0u,
+                 tlist_n, v.st, w0, w1);
+    if (t && kind == 0) tlist[w0] = uint32_t(k);
+    if (t && kind != 0) tlist_other[w1] = uint32_t(k);
+    __syncthreads();   // block_append's shared words are reused next round
   }
-  if (t && kind != 0) tlist_other[s_base[1] + s_off[1][warp] + __popc(m1 & lt)] = uint32_t(k);
+}
+
+// Throughput build, sphere-sphere block [0, seg[n_sph]) of the contact
+// array: d^2 < (ra + rb)^2 (the predicate k_forces_f32 uses), E entries per
+// thread so their centre gathers are in flight together; touching entries
+// leave as (a, b, k) records, ascending within the block.
+constexpr int kTouchPerThread = 2;
+__global__ void __launch_bounds__(256, 4) k_touch_ss(DtView v, uint4 *rec, unsigned long long *tlist_n,
+                                                     unsigned long long step) {
+  constexpr int E = kTouchPerThread;
+  __shared__ int s_live;
+  if (threadIdx.x == 0) s_live = !v.st->err && v.st->dd_trip >= step;
+  __syncthreads();
+  const int64_t n_ss = int64_t(v.seg[v.n_sph]);
+  const int64_t k0 = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) * E;
+  uint2 id[E];
+#pragma unroll
+  for (int j = 0; j < E; ++j) id[j] = (s_live && k0 + j < n_ss) ? v.ids[k0 + j] : make_uint2(0u, 0u);
+  unsigned m = 0;
+  {
+    double4 ca[E], cb[E];
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      if (s_live && k0 + j < n_ss) {
+        ca[j] = v.sph.center[id[j].x];
+        cb[j] = v.sph.center[id[j].y & kSlotMask];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      if (s_live && k0 + j < n_ss) {
+        const double dx = ca[j].x - cb[j].x, dy = ca[j].y - cb[j].y, dz = ca[j].z - cb[j].z;
+        const double R = ca[j].w + cb[j].w;
+        if (float(R * R - (dx * dx + dy * dy + dz * dz)) > 0.f) m |= 1u << j;
+      }
+    }
+  }
+  unsigned long long w0, w1;
+  block_append(__popc(m), 0u, 2u * __popc(m), tlist_n, v.st, w0, w1);
+#pragma unroll
+  for (int j = 0; j < E; ++j)
+    if (m & (1u << j)) rec[w0++] = make_uint4(id[j].x, id[j].y & kSlotMask, uint32_t(k0 + j), 0u);
 }
 
 }  // namespace
@@ -142,7 +191,7 @@ __device__ __forceinline__ long long run_sum(long long v, int lane, int run_end)
   return v;
 }
 
-static __global__ void __launch_bounds__(256, 3) k_forces_f32(DtView v, double ts_d, double sim_time,
+static __global__ void __launch_bounds__(256, 4) k_forces_f32(DtView v, double ts_d, double sim_time,
                                                                const uint4 *rec, const unsigned long long *tlist_n) {
   (void)sim_time;
   if (v.st->err) return;
@@ -600,14 +649,21 @@ int dt_forces_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
     // throughput build + built-in model: sphere-sphere contacts take the fp32
     // path (k_forces_f32), the wall kinds the generic k_forces
     const bool fused = std::is_same<VelT, float>::value && c->wild_w == 4 && !c->user_model && v.sph.kin;
-    k_touch<<<unsigned((v.n_acs + 255) / 256), 256, 0, s>>>(v, list0, list1, tn, (unsigned long long)a.step,
-                                                             fused ? 1 : 0);
-    if (fused)
+    if (fused) {
+      const int64_t per_block = 256 * kTouchPerThread;
+      k_touch_ss<<<unsigned((v.n_acs + per_block - 1) / per_block), 256, 0, s>>>(
+          v, reinterpret_cast<uint4 *>(list0), tn, (unsigned long long)a.step);
+      // the wall kinds: from the start of the (kind 1, sphere 0) segment
+      k_touch<<<148 * 4, 256, 0, s>>>(v, list0, list1, tn, (unsigned long long)a.step, v.seg + c->n_sph);
       k_forces_f32<<<148 * 8, 256, 0, s>>>(v, a.h, a.sim_time, reinterpret_cast<const uint4 *>(list0), tn);
+    } else {
+      k_touch<<<unsigned(std::min<int64_t>((v.n_acs + 255) / 256, 148 * 16)), 256, 0, s>>>(
+          v, list0, list1, tn, (unsigned long long)a.step, nullptr);
+    }
     if (c->user_model) {
       if (launch_user_forces(c, v, a.h, a.sim_time, s)) return -1;
     } else {
-      k_forces<VelT><<<fused ? 148 : 148 * 8, 128, 0, s>>>(v, a.h, a.sim_time, list0, list1, tn, fused ? 1 : 0);
+      k_forces<VelT><<<148 * 8, 128, 0, s>>>(v, a.h, a.sim_time, list0, list1, tn, fused ? 1 : 0);
     }
   }
   if (ev) cudaEventRecord(ev[1], s);
