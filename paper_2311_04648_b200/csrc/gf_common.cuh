@@ -62,6 +62,7 @@ struct Owners {
   const double *dd_x0; // partition-time coordinate of each owner along the slab axis
   double dd_travel;    // allowed displacement along the axis before a repartition
   int dd_axis;
+  const uint8_t *passive;  // [256] per family: fixed or fully prescribed (its accumulators never feed it)
 };
 
 // Spatial decomposition (slab partition across ranks).  Every owner of a
@@ -91,9 +92,16 @@ __host__ __device__ inline bool dd_keep(const uint32_t *dd, uint32_t oa, uint32_
 
 // Per-sphere kinematics record of the throughput build, written wherever the
 // sphere centres are (integrator, refresh, halo unpack) so the contact kernel
-// reaches everything it needs one load after the contact list:
-// v = owner linear velocity, w = owner angular velocity (global frame),
-// r = centre minus owner position, id = (owner, material, -, -).
+// reaches everything it needs one load after the contact list, with no
+// further dependent loads:
+//   v  = owner linear velocity,                  v.w = owner mass (float)
+//   w  = owner angular velocity (global frame),  w.w = fixed-point force scale
+//   r  = centre minus owner position,            r.w = fixed-point torque scale
+//   id = (owner, material, flags, -); flags bit 0 = passive owner.
+// The scales are the owner template's tpl_scale (float-exact by
+// construction, gf_context.cu update_fixed_scales); 0 = boundary owner,
+// summed with fp64 atomics.
+constexpr uint32_t kKinPassive = 1u;
 struct SphKin {
   float4 v, w, r;
   uint4 id;
@@ -219,7 +227,8 @@ __device__ __forceinline__ void qrot(double qw, double qx, double qy, double qz,
 // kinematics record from the STORED owner state (quaternion, float32
 // velocities), identical wherever it is computed
 __device__ __forceinline__ void write_kin(const Spheres &sph, uint32_t k, uint32_t o, const float4 q,
-                                          const float4 lv, const float4 av) {
+                                          const float4 lv, const float4 av, float mass, double2 scale,
+                                          uint32_t flags) {
   const float4 orr = sph.offr[k];
   double r[3], w[3];
   qrot(double(q.x), double(q.y), double(q.z), double(q.w), double(orr.x), double(orr.y), double(orr.z), r[0], r[1],
@@ -227,16 +236,18 @@ __device__ __forceinline__ void write_kin(const Spheres &sph, uint32_t k, uint32
   qrot(double(q.x), double(q.y), double(q.z), double(q.w), double(av.x), double(av.y), double(av.z), w[0], w[1],
        w[2]);
   SphKin kr;
-  kr.v = make_float4(lv.x, lv.y, lv.z, 0.f);
-  kr.w = make_float4(float(w[0]), float(w[1]), float(w[2]), 0.f);
-  kr.r = make_float4(float(r[0]), float(r[1]), float(r[2]), 0.f);
-  kr.id = make_uint4(o, sph.mat[k], 0u, 0u);
+  kr.v = make_float4(lv.x, lv.y, lv.z, mass);
+  kr.w = make_float4(float(w[0]), float(w[1]), float(w[2]), float(scale.x));
+  kr.r = make_float4(float(r[0]), float(r[1]), float(r[2]), float(scale.y));
+  kr.id = make_uint4(o, sph.mat[k], flags, 0u);
   sph.kin[k] = kr;
 }
 
 __device__ __forceinline__ void write_kin_from_state(const Owners &own, const Spheres &sph, uint32_t k, uint32_t o) {
+  const uint32_t meta = own.meta[o], t = meta_tpl(meta);
+  const uint32_t flags = (own.passive && own.passive[meta_family(meta)]) ? kKinPassive : 0u;
   write_kin(sph, k, o, own.quat[o], reinterpret_cast<const float4 *>(own.lin_vel)[o],
-            reinterpret_cast<const float4 *>(own.ang_vel)[o]);
+            reinterpret_cast<const float4 *>(own.ang_vel)[o], float(own.tpl[t].x), own.tpl_scale[t], flags);
 }
 
 // sphere world centre: owner pos + q * offset (_kernels.py:91-106)

@@ -72,6 +72,7 @@ Owners owners_view(Ctx *c) {
   o.dd_x0 = c->dd_x0.as<double>();
   o.dd_travel = c->dd_travel;
   o.dd_axis = c->dd_axis;
+  o.passive = c->fam_passive.p ? c->fam_passive.as<uint8_t>() : nullptr;
   return o;
 }
 Spheres spheres_view(Ctx *c) {
@@ -149,14 +150,17 @@ static int update_fixed_scales(Ctx *c, double h, double v_err, const double *g) 
       sc[2 * t + 1] = 0.0;
       continue;
     }
-    double sf = std::ldexp(1.0, 50) / (64.0 * m * rate);
+    // float-exact: the contact kernel reads them from the fp32 kinematics record
+    double sf = double(float(std::ldexp(1.0, 50) / (64.0 * m * rate)));
     sc[2 * t] = sf;
-    sc[2 * t + 1] = sf / lever;
+    sc[2 * t + 1] = double(float(sf / lever));
   }
   if (!c->h_tpl_mass.empty())
     GF_CHECK(c, cudaMemcpy(c->tpl_scale.p, sc.data(), 16 * c->h_tpl_mass.size(), cudaMemcpyHostToDevice));
   c->fx_h = h;
   c->fx_verr = v_err;
+  // the kinematics records carry the scales
+  if (c->f32_state && c->n_sph && c->sph_first.p && refresh_centers(c, c->s_dt)) return -1;
   return 0;
 }
 
@@ -342,6 +346,7 @@ gf_ctx *gf_create(int device, uint32_t flags) {
   cudaEventCreateWithFlags(&c->ev_count, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->ev_disp, cudaEventDisableTiming);
   if (const char *sf = std::getenv("GF_SKIN_FACTOR")) c->skin_factor = std::atof(sf);
+  if (const char *sp = std::getenv("GF_SS_SPLIT")) c->ss_split = std::atoi(sp);
   cudaEventCreate(&c->t0);
   cudaEventCreate(&c->t1);
   cudaEventRecord(c->ev_adopted, c->s_dt);
@@ -364,7 +369,7 @@ void gf_destroy(gf_ctx *ctx) {
                   &c->ext, &c->sph_owner, &c->sph_offr, &c->sph_mat, &c->tri_owner, &c->tri_local,
                   &c->tri_mat, &c->tri_world, &c->ana_owner, &c->ana_kind, &c->ana_local, &c->ana_mat,
                   &c->ana_world, &c->pair, &c->beta, &c->fam_mask, &c->fam_flags, &c->lv_mask,
-                  &c->av_mask, &c->lv_val, &c->av_val, &c->acs.ids, &c->acs.wild, &c->acs_next.ids,
+                  &c->av_mask, &c->lv_val, &c->av_val, &c->fam_passive, &c->acs.ids, &c->acs.wild, &c->acs_next.ids,
                   &c->acs_next.wild, &c->out_c, &c->touch, &c->inc, &c->inc_alt, &c->inc_key,
                   &c->inc_key_alt, &c->inc_start, &c->heavy, &c->heavy_count, &c->heavy_acc,
                   &c->cub_tmp_dt, &c->status, &c->dyn_spec, &c->dyn_vals, &c->kt.centers, &c->kt.c4, &c->kt.sfam,
@@ -642,7 +647,16 @@ int gf_upload_families(gf_ctx *ctx, const uint8_t *mask, const uint8_t *flags, c
   for (int q = 0; q < 65536; ++q)
     if (!mask[q]) { c->mask_trivial = false; break; }
   c->h_fam_flags.assign(flags, flags + 256);
+  uint8_t passive[256];
+  for (int f = 0; f < 256; ++f)
+    passive[f] = ((flags[f] & kFamFixed) || (lv_mask[f] == 7 && av_mask[f] == 7)) ? 1 : 0;
+  if (upload_raw(c, c->fam_passive, passive, 256)) return -1;
   world_moving_update(c);
+  // the kinematics records carry the passive flag
+  if (c->f32_state && c->n_sph && c->sph_first.p && c->sph_center.bytes >= size_t(32 * c->n_sph)) {
+    if (refresh_centers(c, c->s_dt)) return -1;
+    GF_CHECK(c, cudaStreamSynchronize(c->s_dt));
+  }
   return 0;
 }
 

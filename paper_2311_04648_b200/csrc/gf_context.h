@@ -95,7 +95,7 @@ struct Ctx {
   // tables
   int n_mat = 0, n_pair_rows = 0;
   DBuf pair, beta;
-  DBuf fam_mask, fam_flags, lv_mask, av_mask, lv_val, av_val;
+  DBuf fam_mask, fam_flags, lv_mask, av_mask, lv_val, av_val, fam_passive;
   std::vector<uint8_t> h_fam_flags;
   bool mask_trivial = true;  // every family pair may contact
   // contact arrays
@@ -124,6 +124,7 @@ struct Ctx {
   double kt_margin = 0.0;
   double kt_bin_size = 0.0;  // > 0: explicit bin size (detect_contacts(bin_size=...))
   double skin_factor = 1.0;  // Verlet skin = skin_factor * margin
+  int ss_split = 0;          // throughput build: split narrow/force sphere-sphere kernels (GF_SS_SPLIT=1)
   // schedule state (kept across gf_run calls)
   bool first_adopt = true;     // the first do_dynamics detects and waits (engine.py:679-682)
   bool fill_done = false;

@@ -213,9 +213,8 @@ __device__ __forceinline__ void hertz_mindlin_core_f32(float overlap, float ts, 
                                                        float b2az, float vx, float vy, float vz, float wrx,
                                                        float wry, float wrz, float mass_eff, float ra, float rb,
                                                        float e_cnt, float g_cnt, float mu, float crr, float beta,
-                                                       float *wild, float out[6]) {
+                                                       const float4 w4, float4 &w_new, float out[6]) {
   for (int q = 0; q < 6; ++q) out[q] = 0.f;
-  const float4 w4 = *reinterpret_cast<const float4 *>(wild);
   float projection = vx * b2ax + vy * b2ay + vz * b2az;
   float vtx = vx - projection * b2ax;
   float vty = vy - projection * b2ay;
@@ -283,7 +282,7 @@ __device__ __forceinline__ void hertz_mindlin_core_f32(float overlap, float ts, 
     out[1] += tfy;
     out[2] += tfz;
   }
-  *reinterpret_cast<float4 *>(wild) = make_float4(dtx, dty, dtz, delta_time);
+  w_new = make_float4(dtx, dty, dtz, delta_time);
 }
 
 // built-in model: pair values and beta from the uploaded tables

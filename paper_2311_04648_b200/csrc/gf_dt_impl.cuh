@@ -191,114 +191,264 @@ __device__ __forceinline__ long long run_sum(long long v, int lane, int run_end)
   return v;
 }
 
+constexpr int kSmemMat = 256;   // material pairs staged in shared memory (n_mat <= 16)
+
+// pair table rows E_cnt, G_cnt, mu, C_rr, beta as float (forces.py:443-460),
+// staged in shared memory when n_mat <= 16
+__device__ __forceinline__ bool stage_materials(const DtView &v, float (*s_mat)[kSmemMat]) {
+  const int nm = v.mat.n_mat, mm = nm * nm;
+  if (mm > kSmemMat) return false;
+  for (int q = threadIdx.x; q < mm; q += blockDim.x) {
+    s_mat[0][q] = float(v.mat.pair[q]);
+    s_mat[1][q] = float(v.mat.pair[mm + q]);
+    s_mat[2][q] = float(v.mat.pair[3 * mm + q]);
+    s_mat[3][q] = float(v.mat.pair[4 * mm + q]);
+    s_mat[4][q] = float(v.mat.beta[q]);
+  }
+  return true;
+}
+
+// Geometry of a touching sphere-sphere entry, as the narrow phase leaves it:
+// centre difference A - B (fp64, rounded to fp32), its length, the overlap
+// numerator R^2 - d^2 (fp64, rounded) and the radii.
+struct SsGeom {
+  float dx, dy, dz, d, num, ra, rb;
+};
+
+__device__ __forceinline__ bool ss_geom(const DtView &v, uint32_t a, uint32_t b, SsGeom &g) {
+  const double4 cA = v.sph.center[a], cB = v.sph.center[b];
+  const double dx = cA.x - cB.x, dy = cA.y - cB.y, dz = cA.z - cB.z;
+  const double d2 = dx * dx + dy * dy + dz * dz;
+  const double R = cA.w + cB.w;
+  g.num = float(R * R - d2);
+  g.dx = float(dx); g.dy = float(dy); g.dz = float(dz);
+  g.d = sqrtf(float(d2));
+  g.ra = float(cA.w); g.rb = float(cB.w);
+  return g.num > 0.f;
+}
+
+// Warp-collective force phase of the fp32 sphere-sphere path: lanes with
+// `live` evaluate contact (a, b, k) -- kinematics records, Hertz-Mindlin,
+// history in place -- and add their contributions to the int64 fixed-point
+// owner accumulators: B side one atomic per word, A side summed over runs of
+// equal A owners in consecutive lanes (entries arrive in A-sorted order).
+// Every lane of the warp must call it.
+__device__ __forceinline__ void ss_force_warp(const DtView &v, bool live, uint32_t a, uint32_t b, uint32_t k,
+                                              const SsGeom &g, float ts, const float (*s_mat)[kSmemMat],
+                                              bool smem, int lane) {
+  float out[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  float ta[3] = {0.f, 0.f, 0.f};
+  uint32_t oa = 0xFFFFFFFFu;
+  float sa_f = 0.f, sa_t = 0.f;
+  bool use_a = false;
+  if (live) {
+    // one load round: kinematics records (mass, scales, flags included) and
+    // the history row
+    const SphKin ka = v.sph.kin[a], kb = v.sph.kin[b];
+    float4 *wp = reinterpret_cast<float4 *>(v.wild) + k;
+    const float4 w4 = *wp;
+    const int nm = v.mat.n_mat, mm = nm * nm;
+    const float depth = g.num / ((g.ra + g.rb) + g.d);
+    float bx = 0.f, by = 0.f, bz = 1.f;
+    if (g.d > 1e-30f) {
+      const float inv = 1.f / g.d;
+      bx = g.dx * inv; by = g.dy * inv; bz = g.dz * inv;
+    }
+    oa = ka.id.x;
+    const uint32_t ob = kb.id.x;
+    // contact point p = cA - b (ra - depth / 2); lever arms p - pos_a, p - pos_b
+    const float ha = g.ra - 0.5f * depth;
+    const float rax = ka.r.x - bx * ha, ray = ka.r.y - by * ha, raz = ka.r.z - bz * ha;
+    const float rbx = kb.r.x + g.dx - bx * ha, rby = kb.r.y + g.dy - by * ha, rbz = kb.r.z + g.dz - bz * ha;
+    const float rotax = ka.w.y * raz - ka.w.z * ray, rotay = ka.w.z * rax - ka.w.x * raz,
+                rotaz = ka.w.x * ray - ka.w.y * rax;
+    const float rotbx = kb.w.y * rbz - kb.w.z * rby, rotby = kb.w.z * rbx - kb.w.x * rbz,
+                rotbz = kb.w.x * rby - kb.w.y * rbx;
+    const float vx = (ka.v.x + rotax) - (kb.v.x + rotbx);
+    const float vy = (ka.v.y + rotay) - (kb.v.y + rotby);
+    const float vz = (ka.v.z + rotaz) - (kb.v.z + rotbz);
+    const double ma = ka.v.w, mb = kb.v.w;
+    const float mass_eff = float((ma * mb) / (ma + mb));
+    const int ab = int(ka.id.y) * nm + int(kb.id.y);
+    float e_cnt, g_cnt, mu, crr, beta;
+    if (smem) {
+      e_cnt = s_mat[0][ab]; g_cnt = s_mat[1][ab]; mu = s_mat[2][ab]; crr = s_mat[3][ab]; beta = s_mat[4][ab];
+    } else {
+      e_cnt = float(v.mat.pair[ab]); g_cnt = float(v.mat.pair[mm + ab]); mu = float(v.mat.pair[3 * mm + ab]);
+      crr = float(v.mat.pair[4 * mm + ab]); beta = float(v.mat.beta[ab]);
+    }
+    float4 w_new;
+    hertz_mindlin_core_f32(depth, ts, bx, by, bz, vx, vy, vz, rotbx - rotax, rotby - rotay, rotbz - rotaz, mass_eff,
+                           g.ra, g.rb, e_cnt, g_cnt, mu, crr, beta, w4, w_new, out);
+    *wp = w_new;
+    const float tx = out[0] + out[3], ty = out[1] + out[4], tz = out[2] + out[5];
+    ta[0] = ray * tz - raz * ty; ta[1] = raz * tx - rax * tz; ta[2] = rax * ty - ray * tx;
+    const float tb[3] = {rby * tz - rbz * ty, rbz * tx - rbx * tz, rbx * ty - rby * tx};
+    // B side: one atomic per word (B owners are scattered)
+    if (v.acc_all || !(kb.id.z & kKinPassive)) {
+      const double sbf = kb.w.w, sbt = kb.r.w;
+      unsigned long long *fb = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(ob));
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        if (sbf > 0.0) {
+          atomicAdd(fb + q, (unsigned long long)__double2ll_rn(-double(out[q]) * sbf));
+          atomicAdd(fb + 3 + q, (unsigned long long)__double2ll_rn(-double(tb[q]) * sbt));
+        } else {
+          atomicAdd(reinterpret_cast<double *>(fb + q), -double(out[q]));
+          atomicAdd(reinterpret_cast<double *>(fb + 3 + q), -double(tb[q]));
+        }
+      }
+    }
+    use_a = v.acc_all || !(ka.id.z & kKinPassive);
+    sa_f = ka.w.w;
+    sa_t = ka.r.w;
+  }
+  // A side: sum each run of equal A owners' int64 words in registers (exact)
+  // and let the run's head lane add them
+  const bool fixed_a = use_a && sa_f > 0.f;
+  if (use_a && !fixed_a) {   // boundary owner: fp64 atomics, not aggregated
+    unsigned long long *fa = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(oa));
+    for (int q = 0; q < 3; ++q) {
+      atomicAdd(reinterpret_cast<double *>(fa + q), double(out[q]));
+      atomicAdd(reinterpret_cast<double *>(fa + 3 + q), double(ta[q]));
+    }
+  }
+  const uint32_t key = fixed_a ? oa : 0xFFFFFFFFu;
+  const uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
+  const bool head = lane == 0 || prev != key;
+  const unsigned heads = __ballot_sync(0xffffffffu, head);
+  const unsigned later = heads & ~((2u << lane) - 1u);   // heads after this lane
+  const int run_end = later ? __ffs(later) - 2 : 31;
+  unsigned long long *fa = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(fixed_a ? oa : 0));
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const long long f = run_sum(fixed_a ? __double2ll_rn(double(out[q]) * double(sa_f)) : 0ll, lane, run_end);
+    const long long t = run_sum(fixed_a ? __double2ll_rn(double(ta[q]) * double(sa_t)) : 0ll, lane, run_end);
+    if (head && fixed_a) {
+      atomicAdd(fa + q, (unsigned long long)f);
+      atomicAdd(fa + 3 + q, (unsigned long long)t);
+    }
+  }
+}
+
+// Throughput build, built-in Hertz-Mindlin, split form: force phase over the
+// (a, b, k) records k_touch_ss compacted.  Centre difference and the overlap
+// numerator R^2 - d^2 in fp64, everything after in fp32 (normal, lever arms
+// from the fp32-rotated clump offsets, velocities, the contact law).  The
+// other kinds (walls) take k_forces.
 static __global__ void __launch_bounds__(256, 4) k_forces_f32(DtView v, double ts_d, double sim_time,
                                                                const uint4 *rec, const unsigned long long *tlist_n) {
   (void)sim_time;
+  __shared__ float s_mat[5][kSmemMat];
   if (v.st->err) return;
   const unsigned long long n = *tlist_n;
-  const float ts = float(ts_d);
-  const int nm = v.mat.n_mat, mm = nm * nm;
+  const bool smem = stage_materials(v, s_mat);
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
   // whole warps iterate together (the A-side reduction needs every lane)
   for (unsigned long long base = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) & ~31ull; base < n;
        base += stride) {
     const unsigned long long i = base + lane;
-    float out[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    float ta[3] = {0.f, 0.f, 0.f};
-    uint32_t oa = 0xFFFFFFFFu, ma_meta = 0;
+    uint4 t = make_uint4(0u, 0u, 0u, 0u);
+    SsGeom g;
     bool live = false;
     if (i < n) {
-      const uint4 t = rec[i];   // sphere A, sphere B, contact index
-      const uint32_t a = t.x, b = t.y, k = t.z;
-      const double4 cA = v.sph.center[a], cB = v.sph.center[b];
-      const SphKin ka = v.sph.kin[a], kb = v.sph.kin[b];
-      const double dx = cA.x - cB.x, dy = cA.y - cB.y, dz = cA.z - cB.z;
-      const double d2 = dx * dx + dy * dy + dz * dz;
-      const double R = cA.w + cB.w;
-      const float num = float(R * R - d2);
-      if (num > 0.f) {
-        live = true;
-        const float fdx = float(dx), fdy = float(dy), fdz = float(dz);
-        const float d = sqrtf(float(d2));
-        const float depth = num / (float(R) + d);
-        float bx = 0.f, by = 0.f, bz = 1.f;
-        if (d > 1e-30f) {
-          const float inv = 1.f / d;
-          bx = fdx * inv; by = fdy * inv; bz = fdz * inv;
-        }
-        oa = ka.id.x;
-        const uint32_t ob = kb.id.x;
-        ma_meta = v.own.meta[oa];
-        const uint32_t mb_meta = v.own.meta[ob];
-        // contact point p = cA - b (ra - depth / 2); lever arms p - pos_a, p - pos_b
-        const float ha = float(cA.w) - 0.5f * depth;
-        const float rax = ka.r.x - bx * ha, ray = ka.r.y - by * ha, raz = ka.r.z - bz * ha;
-        const float rbx = kb.r.x + fdx - bx * ha, rby = kb.r.y + fdy - by * ha, rbz = kb.r.z + fdz - bz * ha;
-        const float rotax = ka.w.y * raz - ka.w.z * ray, rotay = ka.w.z * rax - ka.w.x * raz,
-                    rotaz = ka.w.x * ray - ka.w.y * rax;
-        const float rotbx = kb.w.y * rbz - kb.w.z * rby, rotby = kb.w.z * rbx - kb.w.x * rbz,
-                    rotbz = kb.w.x * rby - kb.w.y * rbx;
-        const float vx = (ka.v.x + rotax) - (kb.v.x + rotbx);
-        const float vy = (ka.v.y + rotay) - (kb.v.y + rotby);
-        const float vz = (ka.v.z + rotaz) - (kb.v.z + rotbz);
-        const double ma = v.own.tpl[meta_tpl(ma_meta)].x, mb = v.own.tpl[meta_tpl(mb_meta)].x;
-        const float mass_eff = float((ma * mb) / (ma + mb));
-        const int ab = int(ka.id.y) * nm + int(kb.id.y);
-        hertz_mindlin_core_f32(depth, ts, bx, by, bz, vx, vy, vz, rotbx - rotax, rotby - rotay, rotbz - rotaz,
-                               mass_eff, float(cA.w), float(cB.w), float(v.mat.pair[ab]),
-                               float(v.mat.pair[mm + ab]), float(v.mat.pair[3 * mm + ab]),
-                               float(v.mat.pair[4 * mm + ab]), float(v.mat.beta[ab]), v.wild + 4 * size_t(k), out);
-        const float tx = out[0] + out[3], ty = out[1] + out[4], tz = out[2] + out[5];
-        ta[0] = ray * tz - raz * ty; ta[1] = raz * tx - rax * tz; ta[2] = rax * ty - ray * tx;
-        const float tb[3] = {rby * tz - rbz * ty, rbz * tx - rbx * tz, rbx * ty - rby * tx};
-        // B side: one atomic per word (B owners are scattered)
-        if (v.acc_all || !passive_owner(v, ob)) {
-          const double2 sbs = v.own.tpl_scale[meta_tpl(mb_meta)];
-          unsigned long long *fb = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(ob));
+      t = rec[i];   // sphere A, sphere B, contact index
+      live = ss_geom(v, t.x, t.y, g);
+    }
+    ss_force_warp(v, live, t.x, t.y, t.z, g, float(ts_d), s_mat, smem, lane);
+  }
+}
+
+// Throughput build, fused form: narrow phase and force phase in one pass over
+// the sphere-sphere block [0, seg[n_sph]).  Each warp tests kSsPerLane x 32
+// consecutive entries, appends the touching ones -- in contact order -- to
+// its shared-memory queue, and runs the force phase on full batches of 32
+// queued contacts, so force lanes are never idle on false positives and the
+// touching list never goes through HBM.
+constexpr int kSsWarps = 8;
+
+template <int kSsPerLane, int kMinBlocks>
+static __global__ void __launch_bounds__(256, kMinBlocks) k_contacts_ss(DtView v, double ts_d, unsigned long long step) {
+  constexpr int kSsQueue = 32 * (kSsPerLane + 1);
+  __shared__ float s_mat[5][kSmemMat];
+  __shared__ uint32_t q_a[kSsWarps][kSsQueue], q_b[kSsWarps][kSsQueue], q_k[kSsWarps][kSsQueue];
+  __shared__ float q_g[7][kSsWarps][kSsQueue];
+  __shared__ int s_live;
+  if (threadIdx.x == 0) s_live = !v.st->err && v.st->dd_trip >= step;
+  const bool smem = stage_materials(v, s_mat);
+  __syncthreads();
+  if (!s_live) return;
+  const float ts = float(ts_d);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned long long n_ss = v.seg[v.n_sph];
+  const unsigned long long wstride = (unsigned long long)gridDim.x * kSsWarps * 32 * kSsPerLane;
+  const unsigned long long w0 = (blockIdx.x * (unsigned long long)kSsWarps + warp) * 32 * kSsPerLane;
+  uint32_t *qa = q_a[warp], *qb = q_b[warp], *qk = q_k[warp];
+  int qn = 0;
+  unsigned long long touched = 0;
+  auto run_batch = [&](int take) {
+    const bool live = lane < take;
+    SsGeom g;
+    uint32_t a = 0, b = 0, k = 0;
+    if (live) {
+      a = qa[lane]; b = qb[lane]; k = qk[lane];
+      g.dx = q_g[0][warp][lane]; g.dy = q_g[1][warp][lane]; g.dz = q_g[2][warp][lane];
+      g.d = q_g[3][warp][lane]; g.num = q_g[4][warp][lane]; g.ra = q_g[5][warp][lane]; g.rb = q_g[6][warp][lane];
+    }
+    ss_force_warp(v, live, a, b, k, g, ts, s_mat, smem, lane);
+    __syncwarp();
+    // shift the rest of the queue down
+    const int rest = qn - take;
+    for (int j = lane; j < rest; j += 32) {
+      const int src = take + j;
+      const uint32_t xa = qa[src], xb = qb[src], xk = qk[src];
+      float xg[7];
 #pragma unroll
-          for (int q = 0; q < 3; ++q) {
-            if (sbs.x > 0.0) {
-              atomicAdd(fb + q, (unsigned long long)__double2ll_rn(-double(out[q]) * sbs.x));
-              atomicAdd(fb + 3 + q, (unsigned long long)__double2ll_rn(-double(tb[q]) * sbs.y));
-            } else {
-              atomicAdd(reinterpret_cast<double *>(fb + q), -double(out[q]));
-              atomicAdd(reinterpret_cast<double *>(fb + 3 + q), -double(tb[q]));
-            }
-          }
-        }
-      }
-    }
-    // A side: entries are in A-sorted contact order, so equal A owners sit in
-    // consecutive lanes -- sum each run's int64 words in registers (exact)
-    // and let the run's head lane add them
-    double2 sa = make_double2(0.0, 0.0);
-    bool use_a = live && (v.acc_all || !passive_owner(v, oa));
-    if (use_a) sa = v.own.tpl_scale[meta_tpl(ma_meta)];
-    const bool fixed_a = use_a && sa.x > 0.0;
-    if (use_a && !fixed_a) {   // boundary owner: fp64 atomics, not aggregated
-      unsigned long long *fa = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(oa));
-      for (int q = 0; q < 3; ++q) {
-        atomicAdd(reinterpret_cast<double *>(fa + q), double(out[q]));
-        atomicAdd(reinterpret_cast<double *>(fa + 3 + q), double(ta[q]));
-      }
-    }
-    const uint32_t key = fixed_a ? oa : 0xFFFFFFFFu;
-    const uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
-    const bool head = lane == 0 || prev != key;
-    const unsigned heads = __ballot_sync(0xffffffffu, head);
-    const unsigned later = heads & ~((2u << lane) - 1u);   // heads after this lane
-    const int run_end = later ? __ffs(later) - 2 : 31;
-    unsigned long long *fa = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(fixed_a ? oa : 0));
+      for (int f = 0; f < 7; ++f) xg[f] = q_g[f][warp][src];
+      __syncwarp(__activemask());
+      qa[j] = xa; qb[j] = xb; qk[j] = xk;
 #pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      const long long f = run_sum(fixed_a ? __double2ll_rn(double(out[q]) * sa.x) : 0ll, lane, run_end);
-      const long long t = run_sum(fixed_a ? __double2ll_rn(double(ta[q]) * sa.y) : 0ll, lane, run_end);
-      if (head && fixed_a) {
-        atomicAdd(fa + q, (unsigned long long)f);
-        atomicAdd(fa + 3 + q, (unsigned long long)t);
-      }
+      for (int f = 0; f < 7; ++f) q_g[f][warp][j] = xg[f];
     }
+    __syncwarp();
+    qn = rest;
+  };
+  for (unsigned long long base = w0; base < n_ss; base += wstride) {
+    uint2 id[kSsPerLane];
+#pragma unroll
+    for (int j = 0; j < kSsPerLane; ++j) {
+      const unsigned long long e = base + 32 * j + lane;
+      id[j] = e < n_ss ? v.ids[e] : make_uint2(0u, 0u);
+    }
+    SsGeom g[kSsPerLane];
+    bool t[kSsPerLane];
+#pragma unroll
+    for (int j = 0; j < kSsPerLane; ++j) {
+      const unsigned long long e = base + 32 * j + lane;
+      t[j] = e < n_ss && ss_geom(v, id[j].x, id[j].y & kSlotMask, g[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < kSsPerLane; ++j) {
+      const unsigned m = __ballot_sync(0xffffffffu, t[j]);
+      if (t[j]) {
+        const int pos = qn + __popc(m & ((1u << lane) - 1u));
+        qa[pos] = id[j].x; qb[pos] = id[j].y & kSlotMask; qk[pos] = uint32_t(base + 32 * j + lane);
+        q_g[0][warp][pos] = g[j].dx; q_g[1][warp][pos] = g[j].dy; q_g[2][warp][pos] = g[j].dz;
+        q_g[3][warp][pos] = g[j].d; q_g[4][warp][pos] = g[j].num; q_g[5][warp][pos] = g[j].ra;
+        q_g[6][warp][pos] = g[j].rb;
+      }
+      qn += __popc(m);
+      touched += __popc(m);
+    }
+    __syncwarp();
+    while (qn >= 32) run_batch(32);
+  }
+  if (qn > 0) run_batch(qn);
+  if (lane == 0 && touched) {
+    atomicAdd(&v.st->touching, 2ull * touched);
+    atomicAdd(&v.st->touch_pairs, touched);
   }
 }
 
@@ -649,13 +799,23 @@ int dt_forces_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
     // throughput build + built-in model: sphere-sphere contacts take the fp32
     // path (k_forces_f32), the wall kinds the generic k_forces
     const bool fused = std::is_same<VelT, float>::value && c->wild_w == 4 && !c->user_model && v.sph.kin;
-    if (fused) {
+    if (fused && c->ss_split == 1) {
       const int64_t per_block = 256 * kTouchPerThread;
       k_touch_ss<<<unsigned((v.n_acs + per_block - 1) / per_block), 256, 0, s>>>(
           v, reinterpret_cast<uint4 *>(list0), tn, (unsigned long long)a.step);
       // the wall kinds: from the start of the (kind 1, sphere 0) segment
       k_touch<<<148 * 4, 256, 0, s>>>(v, list0, list1, tn, (unsigned long long)a.step, v.seg + c->n_sph);
       k_forces_f32<<<148 * 8, 256, 0, s>>>(v, a.h, a.sim_time, reinterpret_cast<const uint4 *>(list0), tn);
+    } else if (fused) {
+      // the wall kinds' narrow phase (feeds k_forces below), then the
+      // sphere-sphere block in one fused pass
+      k_touch<<<148 * 4, 256, 0, s>>>(v, list0, list1, tn, (unsigned long long)a.step, v.seg + c->n_sph);
+      if (c->ss_split == 2)
+        k_contacts_ss<1, 4><<<148 * 4, 256, 0, s>>>(v, a.h, (unsigned long long)a.step);
+      else if (c->ss_split == 3)
+        k_contacts_ss<2, 4><<<148 * 4, 256, 0, s>>>(v, a.h, (unsigned long long)a.step);
+      else
+        k_contacts_ss<2, 3><<<148 * 3, 256, 0, s>>>(v, a.h, (unsigned long long)a.step);
     } else {
       k_touch<<<unsigned(std::min<int64_t>((v.n_acs + 255) / 256, 148 * 16)), 256, 0, s>>>(
           v, list0, list1, tn, (unsigned long long)a.step, nullptr);
