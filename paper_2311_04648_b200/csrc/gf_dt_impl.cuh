@@ -551,25 +551,39 @@ __global__ void __launch_bounds__(256) k_heavy(DtView v) {
 }
 }  // namespace
 
-template <typename VelT>
-__global__ void __launch_bounds__(128) k_integrate(DtView v, double h, double gx, double gy, double gz,
+template <typename VelT, int kMinBlocks = 1>
+__global__ void __launch_bounds__(128, kMinBlocks) k_integrate(DtView v, double h, double gx, double gy, double gz,
                                                    double v_err, unsigned long long step, int write_acc) {
   int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (i >= v.own.n || v.st->err || v.st->dd_trip < step) return;
   const uint32_t o = uint32_t(i);
   // a ghost is integrated on its home rank; its state arrives by halo exchange
   if (v.own.dd && (v.own.dd[o] & 3u) == kDdGhost) return;
+  // independent loads first (one latency round)
+  const uint32_t meta = v.own.meta[o];
+  const uint64_t vox0 = v.own.voxel[o];
+  const ushort4 sub0 = v.own.sub[o];
+  float4 q = v.own.quat[o];
+  const uint32_t s0 = v.sph.first[o], s1 = v.sph.first[o + 1];
+  const uint32_t fam = meta_family(meta);
+  const uint8_t fl = v.fam.flags[fam];
+  const double4 tp = v.own.tpl[meta_tpl(meta)];
   double p[3];
-  decode_pos(v.dom, v.own.voxel[o], v.own.sub[o], p[0], p[1], p[2]);
+  decode_pos(v.dom, vox0, sub0, p[0], p[1], p[2]);
   // --- reduction (reduce_to_owners order) ---
   double af[3] = {0, 0, 0}, at[3] = {0, 0, 0};
-  if (v.own.facc) {
+  double2 sc = make_double2(0.0, 0.0);
+  // the fp32-velocity build always reduces into the fixed-point accumulators
+  // (Ctx::fixed_reduce == f32_state); the fp64 build always by incidence lists
+  if (std::is_same<VelT, float>::value) {
     longlong2 *fp = reinterpret_cast<longlong2 *>(v.own.facc + 6 * size_t(o));
     const longlong2 a0 = fp[0], a1 = fp[1], a2 = fp[2];
-    const double2 sc = v.own.tpl_scale[meta_tpl(v.own.meta[o])];
+    sc = v.own.tpl_scale[meta_tpl(meta)];
     if (sc.x > 0.0) {
-      af[0] = double(a0.x) / sc.x; af[1] = double(a0.y) / sc.x; af[2] = double(a1.x) / sc.x;
-      at[0] = double(a1.y) / sc.y; at[1] = double(a2.x) / sc.y; at[2] = double(a2.y) / sc.y;
+      // scales are powers of two: multiplying by the reciprocal is exact
+      const double isf = 1.0 / sc.x, ist = 1.0 / sc.y;
+      af[0] = double(a0.x) * isf; af[1] = double(a0.y) * isf; af[2] = double(a1.x) * isf;
+      at[0] = double(a1.y) * ist; at[1] = double(a2.x) * ist; at[2] = double(a2.y) * ist;
     } else {
       af[0] = __longlong_as_double(a0.x); af[1] = __longlong_as_double(a0.y);
       af[2] = __longlong_as_double(a1.x); at[0] = __longlong_as_double(a1.y);
@@ -595,11 +609,7 @@ __global__ void __launch_bounds__(128) k_integrate(DtView v, double h, double gx
     a[0] = af[0]; a[1] = af[1]; a[2] = af[2]; a[3] = at[0]; a[4] = at[1]; a[5] = at[2];
   }
   // --- integrate_step (_kernels.py:564-636) ---
-  const uint32_t meta = v.own.meta[o];
-  const uint32_t fam = meta_family(meta);
-  const uint8_t fl = v.fam.flags[fam];
-  float4 q = v.own.quat[o];
-  double vel[3], w[3];
+  double vel[3] = {0.0, 0.0, 0.0}, w[3] = {0.0, 0.0, 0.0};
   bool moved = false;
   if (fl & kFamFixed) {
     double z[3] = {0.0, 0.0, 0.0};
@@ -625,7 +635,6 @@ __global__ void __launch_bounds__(128) k_integrate(DtView v, double h, double gx
         qrot(qw, -qx, -qy, -qz, pw[0], pw[1], pw[2], w[0], w[1], w[2]);
       }
     } else {
-      const double4 tp = v.own.tpl[meta_tpl(meta)];
       const double m = tp.x;
       double ef[6] = {0, 0, 0, 0, 0, 0};
       if (v.own.ext) {
@@ -678,11 +687,14 @@ __global__ void __launch_bounds__(128) k_integrate(DtView v, double h, double gx
   v.own.sub[o] = s;
   // decomposition guard: the static ghost layer covers displacements up to
   // dd_travel along the slab axis
-  if (v.own.dd && (v.own.dd[o] & 3u) == kDdLocal && fabs(p[v.own.dd_axis] - v.own.dd_x0[o]) > v.own.dd_travel)
+  if (v.own.dd && (v.own.dd[o] & 3u) == kDdLocal && fabs((v.own.dd_axis == 0 ? p[0] : (v.own.dd_axis == 1 ? p[1] : p[2])) - v.own.dd_x0[o]) > v.own.dd_travel)
     atomicMin(&v.st->dd_trip, step);
   // refreshed sphere centres from the decoded position (_kernels.py:657-669)
-  const uint32_t s0 = v.sph.first[o], s1 = v.sph.first[o + 1];
   if (s1 > s0) {
+    // the stored (float32) velocities, for the kinematics records
+    const float4 lv4 = make_float4(float(vel[0]), float(vel[1]), float(vel[2]), 0.f);
+    const float4 av4 = make_float4(float(w[0]), float(w[1]), float(w[2]), 0.f);
+    const uint32_t kflags = (v.own.passive && v.own.passive[fam]) ? kKinPassive : 0u;
     double pd[3];
     decode_pos(v.dom, vox, s, pd[0], pd[1], pd[2]);
     for (uint32_t k = s0; k < s1; ++k) {
@@ -691,7 +703,7 @@ __global__ void __launch_bounds__(128) k_integrate(DtView v, double h, double gx
       qrot(double(q.x), double(q.y), double(q.z), double(q.w), double(orr.x), double(orr.y), double(orr.z),
            r[0], r[1], r[2]);
       v.sph.center[k] = make_double4(add(pd[0], r[0]), add(pd[1], r[1]), add(pd[2], r[2]), double(orr.w));
-      if (v.sph.kin) write_kin_from_state(v.own, v.sph, k, o);
+      if (v.sph.kin) write_kin(v.sph, k, o, q, lv4, av4, float(tp.x), sc, kflags);
     }
   }
 }
@@ -845,8 +857,9 @@ int dt_integrate_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
   }
   if (c->n_owner) {
     unsigned g = unsigned((c->n_owner + 127) / 128);
-    k_integrate<VelT><<<g, 128, 0, s>>>(v, a.h, a.g[0], a.g[1], a.g[2], a.v_err,
-                                       (unsigned long long)a.step, a.write_acc);
+    // 8 CTAs / SM (64 registers, a few spills) beats 6 at 91 registers
+    k_integrate<VelT, 8><<<g, 128, 0, s>>>(v, a.h, a.g[0], a.g[1], a.g[2], a.v_err,
+                                          (unsigned long long)a.step, a.write_acc);
   }
   if (ev) cudaEventRecord(ev[3], s);
   if ((c->n_tri || c->n_ana) && c->world_moving) {
