@@ -381,7 +381,7 @@ void gf_destroy(gf_ctx *ctx) {
                   &c->kt.tri_start, &c->kt.tri_entries, &c->kt.counts, &c->kt.offsets, &c->kt.cub_tmp,
                   &c->kt.total, &c->kt.cursor, &c->kt.tri_cursor, &c->big_slots, &c->kt.sc,
                   &c->kt.sm, &c->kt.sf, &c->kt.cells, &c->kt.n_cells, &c->kt.cand, &c->kt.cand_tmp, &c->kt.cand_n,
-                  &c->kt.cand_cnt, &c->kt.cand_seg, &c->kt.ref, &c->kt.flag, &c->kt.cflags, &c->kt.sel_n, &c->kt.tmp, &c->kt.tmp_n, &c->acs.seg, &c->acs_next.seg, &c->dd, &c->dd_x0, &c->halo_scratch};
+                  &c->kt.cand_cnt, &c->kt.cand_seg, &c->kt.ref, &c->kt.flag, &c->kt.cflags, &c->kt.sel_n, &c->kt.tmp, &c->kt.tmp_n, &c->acs.seg, &c->acs_next.seg, &c->acs.old_pos, &c->acs_next.old_pos, &c->kt.fbits[0], &c->kt.fbits[1], &c->kt.fpre[0], &c->kt.fpre[1], &c->kt.fcnt, &c->dd, &c->dd_x0, &c->halo_scratch};
   for (DBuf *b : bufs) release(*b);
   free_run(c);
   if (c->h_status) cudaFreeHost(c->h_status);
@@ -684,6 +684,8 @@ int gf_set_acs(gf_ctx *ctx, int64_t n, const uint8_t *kind, const int64_t *slot_
   if (ensure(c, c->acs.ids, 8 * cap, c->s_dt) || ensure(c, c->acs.wild, 4 * W * cap, c->s_dt)) return -1;
   c->acs.cap = cap;
   c->acs.n = n;
+  c->acs.det_id = 0;   // installed: no candidate rows refer to it
+  c->acs.pos_valid = false;
   std::vector<uint32_t> ids(2 * n);
   for (int64_t k = 0; k < n; ++k) {
     ids[2 * k] = uint32_t(slot_a[k]);

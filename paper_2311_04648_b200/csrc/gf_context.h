@@ -27,6 +27,13 @@ struct Acs {
   DBuf ids;    // uint2[cap]
   DBuf wild;   // float[cap * W]
   DBuf seg;    // uint64[3 n_sph + 1]: start of each (kind, sphere A) segment
+  // history remap by candidate slot (gf_kt.cu k_filter_compact): for each
+  // sphere-sphere entry, its row in the array of detection prev_det (~0u:
+  // not there); valid only while the candidate list is unchanged
+  DBuf old_pos;              // uint32[cap]
+  uint64_t det_id = 0;       // detection serial that produced this array (0: installed)
+  uint64_t prev_det = 0;     // detection whose rows old_pos refers to
+  bool pos_valid = false;
 };
 
 struct KtScratch {
@@ -52,6 +59,15 @@ struct KtScratch {
   // Verlet candidate lists (rebuilt when a sphere moved > skin / 2)
   DBuf cand, cand_tmp, cand_n, cand_cnt, cand_seg, ref, flag, cflags, sel_n;
   int64_t cand_cap = 0, n_cand = 0, rebuilds = 0;
+  // hit bitmask and scanned per-block hit counts of the last two filtered
+  // arrays (double-buffered), with the detection serial / candidate
+  // generation they belong to
+  DBuf fbits[2], fpre[2], fcnt;
+  int cslot_cur = 0;
+  uint64_t cslot_det[2] = {0, 0};
+  int64_t cslot_gen[2] = {-1, -1};
+  int64_t cand_gen = 0;
+  uint64_t det_serial = 0;
   bool cand_valid = false;
   double cand_skin = -1.0;
   int64_t tmp_cap = 0;

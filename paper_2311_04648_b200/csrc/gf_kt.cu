@@ -556,7 +556,7 @@ __global__ void __launch_bounds__(128) k_pairs_other(KtView v, unsigned long lon
     ri_f = v.sph.offr[i].w;
     oi = v.sph.owner[i];
     fi = v.sfam[i];
-    sphere_range(g, ci, ri_f, v.margin, lo_i, hi_i);
+    if (v.n_tri) sphere_range(g, ci, ri_f, v.margin, lo_i, hi_i);   // only the triangle predicate needs it
   }
   unsigned long long cst = 0, csa = 0;
   if (v.n_tri && active) {
@@ -832,32 +832,126 @@ __global__ void k_place_cand(const unsigned long long *m_p, const uint2 *tmp, co
   }
 }
 
-// exact reference predicate on every candidate (one thread each, coalesced
-// over the candidate array, which is globally sorted by (a, b)): a flag per
-// candidate plus the per-sphere count; an order-preserving compaction of the
-// flagged candidates is then the canonical sphere-sphere block
-__global__ void __launch_bounds__(256) k_filter_flags(KtView v, const uint2 *cand, int64_t n_cand,
-                                                      uint8_t *flags, unsigned long long *counts) {
-  int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (e >= n_cand) return;
+// Sphere-sphere block of a detection in two coalesced passes over the
+// candidate list (sorted by (a, b)):
+//   k_filter_bits  the exact reference predicate per candidate; hits as a
+//                  bitmask (one word per warp) plus a count per 256-candidate
+//                  block (then scanned);
+//   k_compact      the hits' rows from the scanned counts and the bitmask:
+//                  writes the canonical sphere-sphere block, its per-sphere
+//                  segment starts (the spheres in (previous candidate's
+//                  sphere, this candidate's sphere] start at this row) and --
+//                  when the previous filtered array came from the same
+//                  candidate list -- each hit's row in that array (old_pos,
+//                  from that array's bitmask and counts), which makes the
+//                  history remap at adoption a plain gather.
+constexpr int kFcBlock = 256;
+
+// kFcPer candidates per thread (item q of lane l in warp w is candidate
+// block_base + w * 32 * kFcPer + q * 32 + l: one bitmask word per (warp, q))
+// so their record gathers are in flight together
+constexpr int kFcPer = 2;
+constexpr int kFcSpan = kFcBlock * kFcPer;   // candidates per filter block
+
+__global__ void __launch_bounds__(kFcBlock) k_filter_bits(KtView v, const uint2 *cand, int64_t n_cand,
+                                                          uint32_t *bits, uint32_t *blk_cnt) {
+  __shared__ uint32_t s_cnt[kFcBlock / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t e0 = blockIdx.x * int64_t(kFcSpan) + warp * 32 * kFcPer + lane;
   const Grid g = *v.grid;
-  const uint2 p = cand[e];
-  const uint32_t i = p.x, j = p.y;
-  // candidates never pair clump-mates (excluded at the rebuild); the family
-  // mask is looked up only when it is not all-allow
-  const double4 ci4 = v.c4[i], cj4 = v.c4[j];
-  bool hit = g.valid;
-  if (hit && !v.mask_trivial) hit = v.mask[256 * v.sfam[i] + v.sfam[j]] != 0;
-  if (hit) {
-    const uint4 mi = make_uint4(i, 0u, 0u, 0u), mj = make_uint4(j, 1u, 0u, 0u);
-    const double4 cl = make_double4(ci4.x, ci4.y, ci4.z, double(float(ci4.w)));
-    const double4 ch = make_double4(cj4.x, cj4.y, cj4.z, double(float(cj4.w)));
-    KtView vv = v;
-    vv.mask_trivial = 1;
-    hit = ss_pair_sorted_nomask(vv, g, cl, mi, ch, mj);
+  uint2 p[kFcPer];
+  double4 ci4[kFcPer], cj4[kFcPer];
+#pragma unroll
+  for (int q = 0; q < kFcPer; ++q) p[q] = e0 + 32 * q < n_cand ? cand[e0 + 32 * q] : make_uint2(0u, 0u);
+#pragma unroll
+  for (int q = 0; q < kFcPer; ++q) {
+    if (e0 + 32 * q < n_cand) {
+      ci4[q] = v.c4[p[q].x];
+      cj4[q] = v.c4[p[q].y];
+    }
   }
-  flags[e] = hit ? 1 : 0;
-  if (hit) atomicAdd(&counts[i], 1ull);
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int q = 0; q < kFcPer; ++q) {
+    const int64_t e = e0 + 32 * q;
+    bool hit = false;
+    if (e < n_cand && g.valid) {
+      hit = v.mask_trivial || v.mask[256 * v.sfam[p[q].x] + v.sfam[p[q].y]] != 0;
+      if (hit) {
+        const uint4 mi = make_uint4(p[q].x, 0u, 0u, 0u), mj = make_uint4(p[q].y, 1u, 0u, 0u);
+        const double4 cl = make_double4(ci4[q].x, ci4[q].y, ci4[q].z, double(float(ci4[q].w)));
+        const double4 ch = make_double4(cj4[q].x, cj4[q].y, cj4[q].z, double(float(cj4[q].w)));
+        hit = ss_pair_sorted_nomask(v, g, cl, mi, ch, mj);
+      }
+    }
+    const uint32_t word = __ballot_sync(0xffffffffu, hit);
+    if (lane == 0 && e < n_cand) bits[e >> 5] = word;
+    cnt += __popc(word);
+  }
+  if (lane == 0) s_cnt[warp] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+#pragma unroll
+    for (int w = 0; w < kFcBlock / 32; ++w) t += s_cnt[w];
+    blk_cnt[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(kFcBlock) k_compact(KtView v, const uint2 *cand, int64_t n_cand,
+                                                      const uint32_t *bits, const unsigned long long *blk_pre,
+                                                      const uint32_t *obits, const unsigned long long *oblk_pre,
+                                                      uint2 *out_ids, unsigned long long *seg, uint32_t *old_pos) {
+  // the filter block's kFcSpan candidates: kFcSpan / 32 bitmask words
+  constexpr int kW = kFcSpan / 32;
+  __shared__ uint32_t s_w[kW], s_ow[kW];
+  const int64_t w_base = blockIdx.x * int64_t(kW);
+  const int64_t n_words = (n_cand + 31) / 32;
+  if (threadIdx.x < kW) {
+    const int64_t w = w_base + threadIdx.x;
+    s_w[threadIdx.x] = w < n_words ? __popc(bits[w]) : 0u;
+    s_ow[threadIdx.x] = (obits && w < n_words) ? __popc(obits[w]) : 0u;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {   // exclusive scan of the word counts (kW <= 32)
+    const int l = threadIdx.x;
+    const uint32_t x0 = l < kW ? s_w[l] : 0u, y0 = l < kW ? s_ow[l] : 0u;
+    uint32_t x = x0, y = y0;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t xo = __shfl_up_sync(0xffffffffu, x, off), yo = __shfl_up_sync(0xffffffffu, y, off);
+      if (l >= off) { x += xo; y += yo; }
+    }
+    __syncwarp();
+    if (l < kW) { s_w[l] = x - x0; s_ow[l] = y - y0; }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const uint32_t below = (1u << lane) - 1u;
+#pragma unroll
+  for (int q = 0; q < kFcPer; ++q) {
+    const int wl = (threadIdx.x >> 5) + q * (kFcBlock / 32);   // word within the block
+    const int64_t e = (w_base + wl) * 32 + lane;
+    if (e >= n_cand) continue;
+    const uint32_t word = bits[w_base + wl];
+    unsigned long long p = blk_pre[blockIdx.x] + s_w[wl] + __popc(word & below);
+    const uint2 it = cand[e];
+    const long long a = (long long)it.x;
+    const long long ap = e > 0 ? (long long)cand[e - 1].x : -1;
+    for (long long sp = ap + 1; sp <= a; ++sp) seg[sp] = p;
+    const bool hit = (word >> lane) & 1u;
+    if (hit) {
+      out_ids[p] = it;
+      if (obits) {
+        const uint32_t oword = obits[w_base + wl];
+        old_pos[p] = ((oword >> lane) & 1u)
+                         ? uint32_t(oblk_pre[blockIdx.x] + s_ow[wl] + __popc(oword & below))
+                         : 0xFFFFFFFFu;
+      }
+    }
+    if (e == n_cand - 1)   // the last candidate closes the block
+      for (long long sp = a + 1; sp <= v.sph.n; ++sp) seg[sp] = p + (hit ? 1 : 0);
+  }
 }
 
 __global__ void k_copy_ref(int64_t n3, const double *c, double *ref) {
@@ -924,6 +1018,36 @@ __global__ void k_merge_seg(int64_t n_new, const uint2 *new_ids, float *new_wild
     uint32_t y = old_ids[q].y;
     if (y == id.y) { hit = (long long)q; break; }
     if (y > id.y) break;
+  }
+  if (W == 4) {
+    reinterpret_cast<float4 *>(new_wild)[k] =
+        hit >= 0 ? reinterpret_cast<const float4 *>(old_wild)[hit] : make_float4(0.f, 0.f, 0.f, 0.f);
+  } else {
+    for (int q = 0; q < W; ++q) new_wild[int64_t(W) * k + q] = hit >= 0 ? old_wild[int64_t(W) * hit + q] : 0.0f;
+  }
+}
+
+// history remap at adoption when both arrays were filtered from the same
+// candidate list: sphere-sphere rows gather their old row directly (old_pos),
+// the wall kinds search their old (kind, a) segment like k_merge_seg
+__global__ void k_adopt_hist(int64_t n_new, const uint2 *new_ids, const uint32_t *old_pos,
+                             const unsigned long long *new_seg, float *new_wild, const uint2 *old_ids,
+                             const float *old_wild, const unsigned long long *old_seg, int64_t n_sph, int W) {
+  int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (k >= n_new) return;
+  long long hit = -1;
+  if ((unsigned long long)k < new_seg[n_sph]) {
+    const uint32_t q = old_pos[k];
+    if (q != 0xFFFFFFFFu) hit = (long long)q;
+  } else {
+    const uint2 id = new_ids[k];
+    const int64_t sg = int64_t(id.y >> kKindShift) * n_sph + id.x;
+    const unsigned long long lo = old_seg[sg], hi = old_seg[sg + 1];
+    for (unsigned long long q = lo; q < hi; ++q) {
+      uint32_t y = old_ids[q].y;
+      if (y == id.y) { hit = (long long)q; break; }
+      if (y > id.y) break;
+    }
   }
   if (W == 4) {
     reinterpret_cast<float4 *>(new_wild)[k] =
@@ -1182,7 +1306,6 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
     return rebuild_candidates(c, s);
   }
   k.n_cand = total;
-  if (ensure(c, k.cflags, total + 16, s)) return -1;
   if (n) {
     GF_CHECK(c, cudaMemsetAsync(k.cursor.p, 0, 4 * n, s));
     k_place_cand<<<1184, 256, 0, s>>>(cn, k.cand_tmp.as<uint2>(), k.cand_seg.as<unsigned long long>(),
@@ -1194,6 +1317,7 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
   k.cand_valid = true;
   k.cand_skin = c->skin_factor * c->kt_margin;
   k.rebuilds++;
+  k.cand_gen++;   // candidate rows of earlier arrays no longer apply
   GF_CHECK(c, cudaGetLastError());
   return 0;
 }
@@ -1209,34 +1333,79 @@ int kt_count(Ctx *c, cudaStream_t s, bool force_rebuild) {
     hs->cand_total = 0;
     if (rebuild_candidates(c, s)) return -1;
   }
-  if (ensure(c, k.counts, sizeof(unsigned long long) * (3 * n + 1), s) ||
-      ensure(c, k.offsets, sizeof(unsigned long long) * (3 * n + 1), s) || ensure(c, k.tmp_n, 16, s) ||
-      ensure(c, k.sel_n, 16, s))
+  if (ensure(c, k.counts, sizeof(unsigned long long) * (3 * n + 1), s) || ensure(c, k.tmp_n, 16, s))
     return -1;
   if (k.tmp_cap == 0) {
     int64_t cap = std::max<int64_t>(n, 4096);
     if (ensure(c, k.tmp, sizeof(uint2) * cap, s)) return -1;
     k.tmp_cap = cap;
   }
+  // the sphere-sphere block is compacted straight into the next array: size it
+  // for every candidate plus the wall-pair scratch capacity
+  Acs &out = c->acs_next;
+  const int64_t need = k.n_cand + k.tmp_cap + 1;
+  if (need > out.cap) {
+    int64_t cap = need + need / 4 + 1024;
+    if (ensure(c, out.ids, sizeof(uint2) * cap, s) || ensure(c, out.wild, sizeof(float) * c->wild_w * cap, s) ||
+        ensure(c, out.old_pos, sizeof(uint32_t) * cap, s))
+      return -1;
+    out.cap = cap;
+  }
+  if (ensure(c, out.seg, sizeof(unsigned long long) * (3 * n + 1), s)) return -1;
   KtView v = kt_view(c, c->kt_margin);
   unsigned long long *cnt = k.counts.as<unsigned long long>();
   unsigned long long *tn = k.tmp_n.as<unsigned long long>();
+  unsigned long long *oseg = out.seg.as<unsigned long long>();
   GF_CHECK(c, cudaMemsetAsync(cnt + 3 * n, 0, sizeof(unsigned long long), s));
   GF_CHECK(c, cudaMemsetAsync(tn, 0, sizeof(unsigned long long), s));
-  GF_CHECK(c, cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * n, s));
-  if (k.n_cand)
-    k_filter_flags<<<grid_for(k.n_cand), 256, 0, s>>>(v, k.cand.as<uint2>(), k.n_cand, k.cflags.as<uint8_t>(), cnt);
+  // exact filter of the sphere-sphere candidates, then their compaction
+  const int prev = k.cslot_cur ^ 1;   // bitmask + counts of the last filtered array
+  const bool rows_ok = k.cslot_gen[prev] == k.cand_gen && k.cslot_det[prev] != 0;
+  const uint64_t det = ++k.det_serial;
+  const int cur = k.cslot_cur;
+  const int64_t nblk = (k.n_cand + kFcSpan - 1) / kFcSpan;
+  if (ensure(c, k.fbits[cur], 4 * ((k.n_cand + 31) / 32 + 1), s) ||
+      ensure(c, k.fcnt, 4 * (nblk + 1), s) || ensure(c, k.fpre[cur], 8 * (nblk + 1), s))
+    return -1;
+  unsigned long long *ss_tot = k.fpre[cur].as<unsigned long long>() + nblk;   // the block's size
+  if (k.n_cand) {
+    k_filter_bits<<<unsigned(nblk), kFcBlock, 0, s>>>(v, k.cand.as<uint2>(), k.n_cand, k.fbits[cur].as<uint32_t>(),
+                                                      k.fcnt.as<uint32_t>());
+    GF_CHECK(c, cudaMemsetAsync(k.fcnt.as<uint32_t>() + nblk, 0, 4, s));
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, k.fcnt.as<uint32_t>(), k.fpre[cur].as<unsigned long long>(),
+                                  int(nblk + 1), s);
+    if (ensure(c, k.cub_tmp, tb + 16, s, false)) return -1;
+    GF_CHECK(c, cub::DeviceScan::ExclusiveSum(k.cub_tmp.p, tb, k.fcnt.as<uint32_t>(),
+                                              k.fpre[cur].as<unsigned long long>(), int(nblk + 1), s));
+    k_compact<<<unsigned(nblk), kFcBlock, 0, s>>>(
+        v, k.cand.as<uint2>(), k.n_cand, k.fbits[cur].as<uint32_t>(), k.fpre[cur].as<unsigned long long>(),
+        rows_ok ? k.fbits[prev].as<uint32_t>() : nullptr, rows_ok ? k.fpre[prev].as<unsigned long long>() : nullptr,
+        out.ids.as<uint2>(), oseg, out.old_pos.as<uint32_t>());
+  } else {
+    GF_CHECK(c, cudaMemsetAsync(oseg, 0, sizeof(unsigned long long) * (n + 1), s));
+    GF_CHECK(c, cudaMemsetAsync(k.fpre[cur].p, 0, sizeof(unsigned long long), s));
+  }
+  out.det_id = det;
+  out.prev_det = rows_ok ? k.cslot_det[prev] : 0;
+  out.pos_valid = rows_ok && k.n_cand > 0;
+  k.cslot_det[cur] = det;
+  k.cslot_gen[cur] = k.cand_gen;
+  k.cslot_cur ^= 1;
+  // sphere-triangle / sphere-analytic pairs: per-sphere counts of kinds 1, 2
   if (n) {
     k_pairs_other<<<grid_for(n, 128), 128, 0, s>>>(v, cnt, k.tmp.as<uint2>(), tn, (unsigned long long)k.tmp_cap);
   }
+  // their segment starts follow the sphere-sphere block: exclusive scan of
+  // counts[n, 3n] seeded with the block's size
   size_t tmp = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, k.offsets.as<unsigned long long>(), int(3 * n + 1), s);
+  auto init = cub::FutureValue<unsigned long long>(ss_tot);
+  cub::DeviceScan::ExclusiveScan(nullptr, tmp, cnt + n, oseg + n, cub::Sum(), init, int(2 * n + 1), s);
   if (ensure(c, k.cub_tmp, tmp + 16, s, false)) return -1;
-  GF_CHECK(c, cub::DeviceScan::ExclusiveSum(k.cub_tmp.p, tmp, cnt, k.offsets.as<unsigned long long>(),
-                                            int(3 * n + 1), s));
+  GF_CHECK(c, cub::DeviceScan::ExclusiveScan(k.cub_tmp.p, tmp, cnt + n, oseg + n, cub::Sum(), init, int(2 * n + 1),
+                                             s));
   Status *st = c->status.as<Status>();
-  GF_CHECK(c, cudaMemcpyAsync(&st->acs_total, k.offsets.as<unsigned long long>() + 3 * n,
-                              sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
+  GF_CHECK(c, cudaMemcpyAsync(&st->acs_total, oseg + 3 * n, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
   GF_CHECK(c, cudaMemcpyAsync(&hs->acs_total, &st->acs_total, sizeof(unsigned long long),
                               cudaMemcpyDeviceToHost, s));
   GF_CHECK(c, cudaMemcpyAsync(&hs->other_total, tn, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
@@ -1257,32 +1426,16 @@ int kt_detect_fill(Ctx *c, Acs &out, cudaStream_t s) {
       if (ensure(c, k.tmp, sizeof(uint2) * cap, s)) return -1;
       k.tmp_cap = cap;
     }
+    k.cslot_cur ^= 1;   // the redo rewrites the same detection's rows
+    --k.det_serial;
     if (kt_count(c, s)) return -1;
     GF_CHECK(c, cudaStreamSynchronize(s));
     out.n = int64_t(hs->acs_total);
   }
-  const int64_t total = out.n;
-  if (total > out.cap) {
-    int64_t cap = total + total / 2 + 1024;
-    if (ensure(c, out.ids, sizeof(uint2) * cap, s) || ensure(c, out.wild, sizeof(float) * c->wild_w * cap, s))
-      return -1;
-    out.cap = cap;
-  }
-  if (ensure(c, out.seg, sizeof(unsigned long long) * (3 * n + 1), s)) return -1;
-  GF_CHECK(c, cudaMemcpyAsync(out.seg.p, k.offsets.p, sizeof(unsigned long long) * (3 * n + 1),
-                              cudaMemcpyDeviceToDevice, s));
-  if (n && total) {
-    KtView v = kt_view(c, c->kt_margin);
-    const unsigned long long *off = k.offsets.as<unsigned long long>();
-    if (k.n_cand) {
-      size_t tmpb = 0;
-      cub::DeviceSelect::Flagged(nullptr, tmpb, k.cand.as<uint2>(), k.cflags.as<uint8_t>(), out.ids.as<uint2>(),
-                                 k.sel_n.as<unsigned long long>(), k.n_cand, s);
-      if (ensure(c, k.cub_tmp, tmpb + 16, s, false)) return -1;
-      GF_CHECK(c, cub::DeviceSelect::Flagged(k.cub_tmp.p, tmpb, k.cand.as<uint2>(), k.cflags.as<uint8_t>(),
-                                             out.ids.as<uint2>(), k.sel_n.as<unsigned long long>(), k.n_cand,
-                                             s));
-    }
+  // kt_count sized the array for every candidate plus the scratch capacity
+  if (out.n > out.cap) { c->err = "contact array overflow"; return -1; }
+  if (n && out.n) {
+    const unsigned long long *off = out.seg.as<unsigned long long>();
     GF_CHECK(c, cudaMemsetAsync(k.cursor.p, 0, sizeof(unsigned) * 3 * n, s));
     k_place<<<1184, 256, 0, s>>>(k.tmp_n.as<unsigned long long>(), n, k.tmp.as<uint2>(), off,
                                  k.cursor.as<unsigned>(), out.ids.as<uint2>());
@@ -1309,7 +1462,12 @@ int kt_bin_ranges(Ctx *c, double margin, int64_t *h_out) {
 int adopt_acs(Ctx *c, cudaStream_t s) {
   Acs &nw = c->acs_next;
   Acs &old = c->acs;
-  if (nw.n && old.n && old.seg.p)
+  if (nw.n && old.n && old.seg.p && nw.pos_valid && old.det_id != 0 && old.det_id == nw.prev_det)
+    k_adopt_hist<<<grid_for(nw.n), kBlock, 0, s>>>(nw.n, nw.ids.as<uint2>(), nw.old_pos.as<uint32_t>(),
+                                                  nw.seg.as<unsigned long long>(), nw.wild.as<float>(),
+                                                  old.ids.as<uint2>(), old.wild.as<float>(),
+                                                  old.seg.as<unsigned long long>(), c->n_sph, c->wild_w);
+  else if (nw.n && old.n && old.seg.p)
     k_merge_seg<<<grid_for(nw.n), kBlock, 0, s>>>(nw.n, nw.ids.as<uint2>(), nw.wild.as<float>(),
                                                  old.ids.as<uint2>(), old.wild.as<float>(),
                                                  old.seg.as<unsigned long long>(), c->n_sph, c->wild_w);
