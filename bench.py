@@ -245,6 +245,7 @@ def b200_arm(args):
         torch.cuda.synchronize(device)
 
     barrier()
+    rebuilds0 = int(sim.last_run.kt_rebuilds) if sim.last_run is not None else 0
     reps0 = getattr(sim.scheduler, "repartitions", 0)
     dev0 = sim.scheduler.timing["dyn_force"]
     prof_range = bool(os.environ.get("GF_PROFILE_TIMED"))   # ncu --profile-from-start off
@@ -257,7 +258,7 @@ def b200_arm(args):
             torch.cuda.profiler.stop()
     rr = sim.last_run
     ctx = sim._ctx   # a repartition rebuilds the context
-    times = np.zeros(5)
+    times = np.zeros(6)
     ctx.call("gf_kernel_times", _lib.ptr(times))
     ctx.call("gf_set_profiling", C.c_int(0))
     # device time of the timed steps: CUDA events on the dT stream around
@@ -274,16 +275,19 @@ def b200_arm(args):
     n_touch_avg = float(rr.sum_touch_pairs) / max(1, args.steps)
     n_free = int(np.sum(~sim._fixed_flag[sim.store.owner_family[:n_o]]))
 
-    # --- roofline: dominant kernel (k_contacts) and the whole dT chain ---
+    # --- roofline: dominant kernel (k_contacts_ss) and the whole dT chain ---
     hbm, hbm_kind = peaks()
     steps_prof = max(1.0, times[4])
-    t_contacts = times[0] / steps_prof * 1e-3
+    t_contacts = times[0] / steps_prof * 1e-3      # contact phase: k_contacts_ss + wall kinds
+    t_ss = times[5] / steps_prof * 1e-3            # the fused sphere-sphere kernel alone
     t_chain = (times[0] + times[1] + times[2]) / steps_prof * 1e-3
     vel_b = 12 if args.precision == "f32" else 24
     per_owner = 58 + 54 + 48 + 2 * (vel_b - 12) * 2  # 160 B (fp32), 208 B (fp64)
+    # 24 B per ACS entry (ids + history read), 16 B per touching
+    # entry (history write); all kinds counted (the wall kinds are ~1% here)
     bytes_contacts = 24.0 * n_acs_avg + 16.0 * n_touch_avg
     bytes_chain = per_owner * n_free + 4.0 * n_s + bytes_contacts
-    ach_c = bytes_contacts / t_contacts / 1e9 if t_contacts > 0 else 0.0
+    ach_c = bytes_contacts / t_ss / 1e9 if t_ss > 0 else 0.0
     ach_chain = bytes_chain / t_chain / 1e9 if t_chain > 0 else 0.0
 
     # --- e2e: host-buffer round trip per step through the C-ABI ---
@@ -328,23 +332,25 @@ def b200_arm(args):
                        "n_spheres_total": n_sph_total,
                        "inputs_vs_l2": "state + contact arrays larger than L2 (no flush)",
                        "avg_acs": n_acs_avg, "avg_touching_pairs": n_touch_avg,
-                       "kt_candidate_rebuilds": int(rr.kt_rebuilds),
+                       "kt_candidate_rebuilds_in_timed_steps": int(rr.kt_rebuilds) - rebuilds0,
                        "precision": args.precision,
                        "bed": (f"settled: {args.settle_steps} untimed steps from the HCP lattice, then the "
                                f"projectile released 2 mm above the surface at the 20 cm-drop speed "
                                f"({settle_s:.1f} s setup)") if args.settle_steps > 0 else "raw HCP lattice",
                        **({"ghost_owners_rank0": n_ghost_owners, "travel_m": args.travel,
                            "repartitions_in_timed_steps": repartitions} if mode == "decomp" else {})},
-            "roofline": {"bound": "hbm", "kernel": "k_contacts", "achieved": ach_c, "peak": hbm,
+            "roofline": {"bound": "hbm", "kernel": "k_contacts_ss", "achieved": ach_c, "peak": hbm,
                          "unit": "GB/s", "frac": ach_c / hbm, "peak_kind": hbm_kind,
-                         "traffic": profiled_traffic("k_contacts"),
+                         "traffic": profiled_traffic("k_contacts_ss"),
+                         "traffic_note": "ncu dram bytes per launch, cold cache (profiles/ncu_traffic.json)",
                          "algorithmic_bytes_per_launch": bytes_contacts,
-                         "launch_ms": t_contacts * 1e3},
+                         "launch_ms": t_ss * 1e3},
             "roofline_dt_chain": {"bound": "hbm", "achieved": ach_chain, "peak": hbm, "unit": "GB/s",
                                   "frac": ach_chain / hbm, "bytes_per_step": bytes_chain,
                                   "ms": t_chain * 1e3,
                                   "share_of_step": t_chain / (ms_per_step * 1e-3)},
-            "kernel_ms_per_step": {"k_contacts": times[0] / steps_prof, "k_heavy": times[1] / steps_prof,
+            "kernel_ms_per_step": {"contact_phase": times[0] / steps_prof, "k_contacts_ss": times[5] / steps_prof,
+                                   "k_heavy": times[1] / steps_prof,
                                    "k_integrate": times[2] / steps_prof,
                                    "kT_per_cycle": times[3] / max(1, args.steps // max(1, period))},
             "clocks": clocks.summary(),

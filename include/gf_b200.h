@@ -245,10 +245,11 @@ int gf_trip_word(gf_ctx *ctx, void *word, int mode);
 int gf_sync(gf_ctx *ctx);
 
 /* per-kernel device timing of subsequent gf_run calls (CUDA events on the dT
- * stream); out5 = cumulative ms of {k_contacts, k_heavy, k_integrate, kT},
- * then the number of profiled steps.  Enabling resets the counters. */
+ * stream); out6 = cumulative ms of {contact phase, k_heavy, k_integrate, kT},
+ * the number of profiled steps, then the ms of the fused sphere-sphere kernel
+ * (k_contacts_ss) inside the contact phase.  Enabling resets the counters. */
 int gf_set_profiling(gf_ctx *ctx, int on);
-int gf_kernel_times(gf_ctx *ctx, double *out5);
+int gf_kernel_times(gf_ctx *ctx, double *out6);
 
 #ifdef __cplusplus
 }

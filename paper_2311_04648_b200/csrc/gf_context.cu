@@ -97,30 +97,31 @@ Families families_view(Ctx *c) {
 }
 
 cudaEvent_t *prof_current(Ctx *c) {
-  if (!c->prof || c->prof_used < 4) return nullptr;
-  return &c->prof_ev[c->prof_used - 4];
+  if (!c->prof || c->prof_used < kProfEv) return nullptr;
+  return &c->prof_ev[c->prof_used - kProfEv];
 }
 
 cudaEvent_t *prof_events(Ctx *c) {
   if (!c->prof) return nullptr;
-  if (c->prof_used + 4 > c->prof_ev.size()) {
-    for (int q = 0; q < 4; ++q) {
+  if (c->prof_used + kProfEv > c->prof_ev.size()) {
+    for (int q = 0; q < kProfEv; ++q) {
       cudaEvent_t e;
       cudaEventCreate(&e);
       c->prof_ev.push_back(e);
     }
   }
   cudaEvent_t *ev = &c->prof_ev[c->prof_used];
-  c->prof_used += 4;
+  c->prof_used += kProfEv;
   return ev;
 }
 
 static void prof_collect(Ctx *c) {
-  for (size_t i = 0; i + 4 <= c->prof_used; i += 4) {
+  for (size_t i = 0; i + kProfEv <= c->prof_used; i += kProfEv) {
     float m;
     for (int q = 0; q < 3; ++q)
       if (cudaEventElapsedTime(&m, c->prof_ev[i + q], c->prof_ev[i + q + 1]) == cudaSuccess)
         c->prof_ms[q] += m;
+    if (cudaEventElapsedTime(&m, c->prof_ev[i], c->prof_ev[i + 4]) == cudaSuccess) c->prof_ms[4] += m;
     c->prof_steps++;
   }
   c->prof_used = 0;
@@ -381,7 +382,7 @@ void gf_destroy(gf_ctx *ctx) {
                   &c->kt.tri_start, &c->kt.tri_entries, &c->kt.counts, &c->kt.offsets, &c->kt.cub_tmp,
                   &c->kt.total, &c->kt.cursor, &c->kt.tri_cursor, &c->big_slots, &c->kt.sc,
                   &c->kt.sm, &c->kt.sf, &c->kt.cells, &c->kt.n_cells, &c->kt.cand, &c->kt.cand_tmp, &c->kt.cand_n,
-                  &c->kt.cand_cnt, &c->kt.cand_seg, &c->kt.ref, &c->kt.flag, &c->kt.cflags, &c->kt.sel_n, &c->kt.tmp, &c->kt.tmp_n, &c->acs.seg, &c->acs_next.seg, &c->acs.old_pos, &c->acs_next.old_pos, &c->kt.fbits[0], &c->kt.fbits[1], &c->kt.fpre[0], &c->kt.fpre[1], &c->kt.fcnt, &c->dd, &c->dd_x0, &c->halo_scratch};
+                  &c->kt.cand_cnt, &c->kt.cand_seg, &c->kt.ref, &c->kt.flag, &c->kt.cflags, &c->kt.sel_n, &c->kt.tmp, &c->kt.tmp_n, &c->acs.seg, &c->acs_next.seg, &c->acs.old_pos, &c->acs_next.old_pos, &c->kt.fbits[0], &c->kt.fbits[1], &c->kt.fpre[0], &c->kt.fpre[1], &c->kt.fcnt, &c->dd, &c->dd_x0, &c->halo_scratch, &c->owner_stage};
   for (DBuf *b : bufs) release(*b);
   free_run(c);
   if (c->h_status) cudaFreeHost(c->h_status);
@@ -406,69 +407,144 @@ int gf_set_domain(gf_ctx *ctx, const double *lo3, const double *hi3, double edge
   return 0;
 }
 
+// Owner state in the reference's host layouts (StateStore arrays, core.py:356-390)
+// <-> the device layouts.  The host arrays are copied as they are into a
+// device staging buffer (stream-ordered; full PCIe rate from pinned memory)
+// and converted on the device, so a per-step host round trip costs the
+// transfers, not host-side repacking.
+namespace {
+__global__ void k_owners_in(int64_t n, const uint16_t *sub3, const double *lv3, const double *av3,
+                            const uint8_t *family, const uint32_t *tpl, ushort4 *sub, void *lin_vel,
+                            void *ang_vel, uint32_t *meta, int f32) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  sub[i] = make_ushort4(sub3[3 * i], sub3[3 * i + 1], sub3[3 * i + 2], 0);
+  meta[i] = (uint32_t(family[i]) << 24) | (tpl[i] & 0xFFFFFFu);
+  if (f32) {
+    reinterpret_cast<float4 *>(lin_vel)[i] = make_float4(float(lv3[3 * i]), float(lv3[3 * i + 1]), float(lv3[3 * i + 2]), 0.f);
+    reinterpret_cast<float4 *>(ang_vel)[i] = make_float4(float(av3[3 * i]), float(av3[3 * i + 1]), float(av3[3 * i + 2]), 0.f);
+  } else {
+    double2 *l = reinterpret_cast<double2 *>(lin_vel) + 2 * i, *w = reinterpret_cast<double2 *>(ang_vel) + 2 * i;
+    l[0] = make_double2(lv3[3 * i], lv3[3 * i + 1]);
+    l[1] = make_double2(lv3[3 * i + 2], 0.0);
+    w[0] = make_double2(av3[3 * i], av3[3 * i + 1]);
+    w[1] = make_double2(av3[3 * i + 2], 0.0);
+  }
+}
+
+__global__ void k_owners_out(int64_t n, const ushort4 *sub, const void *lin_vel, const void *ang_vel,
+                             const uint32_t *meta, uint16_t *sub3, double *lv3, double *av3, uint8_t *family,
+                             int f32) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const ushort4 s = sub[i];
+  sub3[3 * i] = s.x; sub3[3 * i + 1] = s.y; sub3[3 * i + 2] = s.z;
+  family[i] = uint8_t(meta_family(meta[i]));
+  if (f32) {
+    const float4 l = reinterpret_cast<const float4 *>(lin_vel)[i], w = reinterpret_cast<const float4 *>(ang_vel)[i];
+    lv3[3 * i] = l.x; lv3[3 * i + 1] = l.y; lv3[3 * i + 2] = l.z;
+    av3[3 * i] = w.x; av3[3 * i + 1] = w.y; av3[3 * i + 2] = w.z;
+  } else {
+    const double2 *l = reinterpret_cast<const double2 *>(lin_vel) + 2 * i,
+                  *w = reinterpret_cast<const double2 *>(ang_vel) + 2 * i;
+    const double2 l0 = l[0], l1 = l[1], w0 = w[0], w1 = w[1];
+    lv3[3 * i] = l0.x; lv3[3 * i + 1] = l0.y; lv3[3 * i + 2] = l1.x;
+    av3[3 * i] = w0.x; av3[3 * i + 1] = w0.y; av3[3 * i + 2] = w1.x;
+  }
+}
+
+// staging layout for n owners: sub3 u16[3n] | lv f64[3n] | av f64[3n] | tpl u32[n] | family u8[n]
+struct Stage {
+  uint16_t *sub3;
+  double *lv, *av;
+  uint32_t *tpl;
+  uint8_t *fam;
+};
+Stage stage_of(DBuf &b, int64_t n) {
+  char *p = static_cast<char *>(b.p);
+  Stage st;
+  st.lv = reinterpret_cast<double *>(p);
+  st.av = st.lv + 3 * n;
+  st.tpl = reinterpret_cast<uint32_t *>(st.av + 3 * n);
+  st.sub3 = reinterpret_cast<uint16_t *>(st.tpl + n);
+  st.fam = reinterpret_cast<uint8_t *>(st.sub3 + 3 * n);
+  return st;
+}
+constexpr size_t kStageBytesPerOwner = 24 + 24 + 4 + 6 + 1;
+}  // namespace
+
+// world_moving from the host family array and the cached mesh / analytic
+// owners (no device read-back)
+static void world_moving_from_host(Ctx *c, const uint8_t *family) {
+  c->world_moving = false;
+  for (const auto *v : {&c->h_tri_owner, &c->h_ana_owner})
+    for (uint32_t o : *v)
+      if (!(c->h_fam_flags.size() == 256 && (c->h_fam_flags[family[o]] & kFamFixed))) {
+        c->world_moving = true;
+        return;
+      }
+}
+
 int gf_upload_owners(gf_ctx *ctx, int64_t n, const uint64_t *voxel, const uint16_t *sub,
                      const float *quat, const double *lin_vel, const double *ang_vel,
                      const uint8_t *family, const uint32_t *tpl, int64_t n_tpl,
                      const double *tpl_mass, const double *tpl_moi) {
   CTX_CHECK(ctx);
   if (n_tpl >= (1 << 24)) { c->err = "too many mass-property templates (max 2^24)"; return -1; }
+  const bool resized = n != c->n_owner;
   c->n_owner = n;
   c->n_tpl = n_tpl;
+  cudaStream_t s = c->s_dt;
   const size_t vb = c->f32_state ? sizeof(float) * 4 : sizeof(double) * 4;
-  if (ensure(c, c->voxel, 8 * n, c->s_dt) || ensure(c, c->sub, 8 * n, c->s_dt) ||
-      ensure(c, c->quat, 16 * n, c->s_dt) || ensure(c, c->lin_vel, vb * n, c->s_dt) ||
-      ensure(c, c->ang_vel, vb * n, c->s_dt) || ensure(c, c->meta, 4 * n, c->s_dt) ||
-      ensure(c, c->tpl, 32 * (n_tpl + 1), c->s_dt) || ensure(c, c->acc, 48 * n, c->s_dt) ||
-      ensure(c, c->heavy_acc, 48 * n, c->s_dt) || ensure(c, c->inc_start, 4 * (n + 2), c->s_dt) ||
-      ensure(c, c->facc, 48 * n, c->s_dt) || ensure(c, c->tpl_scale, 16 * (n_tpl + 1), c->s_dt) ||
-      ensure(c, c->heavy, 4 * (n + 1), c->s_dt))
+  if (ensure(c, c->voxel, 8 * n, s) || ensure(c, c->sub, 8 * n, s) ||
+      ensure(c, c->quat, 16 * n, s) || ensure(c, c->lin_vel, vb * n, s) ||
+      ensure(c, c->ang_vel, vb * n, s) || ensure(c, c->meta, 4 * n, s) ||
+      ensure(c, c->tpl, 32 * (n_tpl + 1), s) || ensure(c, c->acc, 48 * n, s) ||
+      ensure(c, c->heavy_acc, 48 * n, s) || ensure(c, c->inc_start, 4 * (n + 2), s) ||
+      ensure(c, c->facc, 48 * n, s) || ensure(c, c->tpl_scale, 16 * (n_tpl + 1), s) ||
+      ensure(c, c->heavy, 4 * (n + 1), s) || ensure(c, c->owner_stage, kStageBytesPerOwner * (n + 1), s))
     return -1;
-  std::vector<uint16_t> s4(4 * n);
-  std::vector<uint32_t> meta(n);
-  for (int64_t i = 0; i < n; ++i) {
-    s4[4 * i] = sub[3 * i];
-    s4[4 * i + 1] = sub[3 * i + 1];
-    s4[4 * i + 2] = sub[3 * i + 2];
-    s4[4 * i + 3] = 0;
-    meta[i] = (uint32_t(family[i]) << 24) | (tpl[i] & 0xFFFFFFu);
+  const Stage st = stage_of(c->owner_stage, n);
+  if (n) {
+    GF_CHECK(c, cudaMemcpyAsync(c->voxel.p, voxel, 8 * n, cudaMemcpyHostToDevice, s));
+    GF_CHECK(c, cudaMemcpyAsync(c->quat.p, quat, 16 * n, cudaMemcpyHostToDevice, s));
+    GF_CHECK(c, cudaMemcpyAsync(st.sub3, sub, 6 * n, cudaMemcpyHostToDevice, s));
+    GF_CHECK(c, cudaMemcpyAsync(st.lv, lin_vel, 24 * n, cudaMemcpyHostToDevice, s));
+    GF_CHECK(c, cudaMemcpyAsync(st.av, ang_vel, 24 * n, cudaMemcpyHostToDevice, s));
+    GF_CHECK(c, cudaMemcpyAsync(st.fam, family, n, cudaMemcpyHostToDevice, s));
+    GF_CHECK(c, cudaMemcpyAsync(st.tpl, tpl, 4 * n, cudaMemcpyHostToDevice, s));
+    k_owners_in<<<unsigned((n + 255) / 256), 256, 0, s>>>(n, st.sub3, st.lv, st.av, st.fam, st.tpl,
+                                                        c->sub.as<ushort4>(), c->lin_vel.p, c->ang_vel.p,
+                                                        c->meta.as<uint32_t>(), c->f32_state ? 1 : 0);
   }
-  GF_CHECK(c, cudaMemcpy(c->voxel.p, voxel, 8 * n, cudaMemcpyHostToDevice));
-  GF_CHECK(c, cudaMemcpy(c->sub.p, s4.data(), 8 * n, cudaMemcpyHostToDevice));
-  GF_CHECK(c, cudaMemcpy(c->quat.p, quat, 16 * n, cudaMemcpyHostToDevice));
-  GF_CHECK(c, cudaMemcpy(c->meta.p, meta.data(), 4 * n, cudaMemcpyHostToDevice));
-  for (int which = 0; which < 2; ++which) {
-    const double *src = which ? ang_vel : lin_vel;
-    DBuf &dst = which ? c->ang_vel : c->lin_vel;
-    if (c->f32_state) {
-      std::vector<float> v(4 * n, 0.f);
-      for (int64_t i = 0; i < n; ++i)
-        for (int a = 0; a < 3; ++a) v[4 * i + a] = float(src[3 * i + a]);
-      GF_CHECK(c, cudaMemcpy(dst.p, v.data(), 16 * n, cudaMemcpyHostToDevice));
-    } else {
-      std::vector<double> v(4 * n, 0.0);
-      for (int64_t i = 0; i < n; ++i)
-        for (int a = 0; a < 3; ++a) v[4 * i + a] = src[3 * i + a];
-      GF_CHECK(c, cudaMemcpy(dst.p, v.data(), 32 * n, cudaMemcpyHostToDevice));
+  // mass-property templates: the fixed-point scales (and the kinematics
+  // records carrying them) are recomputed only when the masses change
+  const bool tpl_changed = resized || c->h_tpl_mass.size() != size_t(n_tpl) ||
+                           !std::equal(tpl_mass, tpl_mass + n_tpl, c->h_tpl_mass.begin()) ||
+                           c->h_tpl_moi.size() != size_t(3 * n_tpl) ||
+                           !std::equal(tpl_moi, tpl_moi + 3 * n_tpl, c->h_tpl_moi.begin());
+  if (tpl_changed) {
+    std::vector<double> tp(4 * n_tpl);
+    for (int64_t t = 0; t < n_tpl; ++t) {
+      tp[4 * t] = tpl_mass[t];
+      tp[4 * t + 1] = tpl_moi[3 * t];
+      tp[4 * t + 2] = tpl_moi[3 * t + 1];
+      tp[4 * t + 3] = tpl_moi[3 * t + 2];
     }
+    if (n_tpl) GF_CHECK(c, cudaMemcpyAsync(c->tpl.p, tp.data(), 32 * n_tpl, cudaMemcpyHostToDevice, s));
+    GF_CHECK(c, cudaStreamSynchronize(s));   // tp is a host temporary
+    c->h_tpl_mass.assign(tpl_mass, tpl_mass + n_tpl);
+    c->h_tpl_moi.assign(tpl_moi, tpl_moi + 3 * n_tpl);
+    c->fx_h = -1.0;  // fixed-point scales recomputed at the next run
   }
-  std::vector<double> tp(4 * n_tpl);
-  for (int64_t t = 0; t < n_tpl; ++t) {
-    tp[4 * t] = tpl_mass[t];
-    tp[4 * t + 1] = tpl_moi[3 * t];
-    tp[4 * t + 2] = tpl_moi[3 * t + 1];
-    tp[4 * t + 3] = tpl_moi[3 * t + 2];
-  }
-  if (n_tpl) GF_CHECK(c, cudaMemcpy(c->tpl.p, tp.data(), 32 * n_tpl, cudaMemcpyHostToDevice));
-  c->h_tpl_mass.assign(tpl_mass, tpl_mass + n_tpl);
-  c->fx_h = -1.0;  // fixed-point scales recomputed at the next run
-  GF_CHECK(c, cudaMemset(c->acc.p, 0, 48 * n));
-  GF_CHECK(c, cudaMemset(c->facc.p, 0, 48 * n));
-  if (c->has_ext) GF_CHECK(c, cudaMemset(c->ext.p, 0, 48 * n));
+  GF_CHECK(c, cudaMemsetAsync(c->acc.p, 0, 48 * n, s));
+  GF_CHECK(c, cudaMemsetAsync(c->facc.p, 0, 48 * n, s));
+  if (c->has_ext) GF_CHECK(c, cudaMemsetAsync(c->ext.p, 0, 48 * n, s));
   if (c->n_sph && c->sph_first.p && c->sph_center.bytes >= size_t(32 * c->n_sph)) {
-    if (refresh_centers(c, c->s_dt) || refresh_world(c, c->s_dt)) return -1;
-    GF_CHECK(c, cudaStreamSynchronize(c->s_dt));
+    if (refresh_centers(c, s) || refresh_world(c, s)) return -1;
   }
-  world_moving_update(c);
+  GF_CHECK(c, cudaStreamSynchronize(s));
+  world_moving_from_host(c, family);
   return 0;
 }
 
@@ -476,36 +552,21 @@ int gf_download_owners(gf_ctx *ctx, uint64_t *voxel, uint16_t *sub, float *quat,
                        double *ang_vel, uint8_t *family) {
   CTX_CHECK(ctx);
   const int64_t n = c->n_owner;
-  GF_CHECK(c, cudaDeviceSynchronize());
-  if (voxel) GF_CHECK(c, cudaMemcpy(voxel, c->voxel.p, 8 * n, cudaMemcpyDeviceToHost));
-  if (sub) {
-    std::vector<uint16_t> s4(4 * n);
-    GF_CHECK(c, cudaMemcpy(s4.data(), c->sub.p, 8 * n, cudaMemcpyDeviceToHost));
-    for (int64_t i = 0; i < n; ++i)
-      for (int a = 0; a < 3; ++a) sub[3 * i + a] = s4[4 * i + a];
-  }
-  if (quat) GF_CHECK(c, cudaMemcpy(quat, c->quat.p, 16 * n, cudaMemcpyDeviceToHost));
-  for (int which = 0; which < 2; ++which) {
-    double *dst = which ? ang_vel : lin_vel;
-    if (!dst) continue;
-    DBuf &src = which ? c->ang_vel : c->lin_vel;
-    if (c->f32_state) {
-      std::vector<float> v(4 * n);
-      GF_CHECK(c, cudaMemcpy(v.data(), src.p, 16 * n, cudaMemcpyDeviceToHost));
-      for (int64_t i = 0; i < n; ++i)
-        for (int a = 0; a < 3; ++a) dst[3 * i + a] = double(v[4 * i + a]);
-    } else {
-      std::vector<double> v(4 * n);
-      GF_CHECK(c, cudaMemcpy(v.data(), src.p, 32 * n, cudaMemcpyDeviceToHost));
-      for (int64_t i = 0; i < n; ++i)
-        for (int a = 0; a < 3; ++a) dst[3 * i + a] = v[4 * i + a];
-    }
-  }
-  if (family) {
-    std::vector<uint32_t> meta(n);
-    GF_CHECK(c, cudaMemcpy(meta.data(), c->meta.p, 4 * n, cudaMemcpyDeviceToHost));
-    for (int64_t i = 0; i < n; ++i) family[i] = uint8_t(meta_family(meta[i]));
-  }
+  cudaStream_t s = c->s_dt;
+  GF_CHECK(c, cudaDeviceSynchronize());   // the kT stream may still read the state
+  if (!n) return 0;
+  if (ensure(c, c->owner_stage, kStageBytesPerOwner * (n + 1), s)) return -1;
+  const Stage st = stage_of(c->owner_stage, n);
+  k_owners_out<<<unsigned((n + 255) / 256), 256, 0, s>>>(n, c->sub.as<ushort4>(), c->lin_vel.p, c->ang_vel.p,
+                                                       c->meta.as<uint32_t>(), st.sub3, st.lv, st.av, st.fam,
+                                                       c->f32_state ? 1 : 0);
+  if (voxel) GF_CHECK(c, cudaMemcpyAsync(voxel, c->voxel.p, 8 * n, cudaMemcpyDeviceToHost, s));
+  if (quat) GF_CHECK(c, cudaMemcpyAsync(quat, c->quat.p, 16 * n, cudaMemcpyDeviceToHost, s));
+  if (sub) GF_CHECK(c, cudaMemcpyAsync(sub, st.sub3, 6 * n, cudaMemcpyDeviceToHost, s));
+  if (lin_vel) GF_CHECK(c, cudaMemcpyAsync(lin_vel, st.lv, 24 * n, cudaMemcpyDeviceToHost, s));
+  if (ang_vel) GF_CHECK(c, cudaMemcpyAsync(ang_vel, st.av, 24 * n, cudaMemcpyDeviceToHost, s));
+  if (family) GF_CHECK(c, cudaMemcpyAsync(family, st.fam, n, cudaMemcpyDeviceToHost, s));
+  GF_CHECK(c, cudaStreamSynchronize(s));
   return 0;
 }
 
@@ -572,6 +633,8 @@ int gf_upload_geometry(gf_ctx *ctx, int64_t n_s, const int64_t *sph_owner, const
                        const int64_t *ana_owner, const uint8_t *ana_kind, const float *ana_local,
                        const uint8_t *ana_mat) {
   CTX_CHECK(ctx);
+  c->h_tri_owner.assign(tri_owner, tri_owner + n_t);
+  c->h_ana_owner.assign(ana_owner, ana_owner + n_a);
   GF_CHECK(c, cudaDeviceSynchronize());
   if (n_s >= (int64_t(1) << 30) || n_t >= (int64_t(1) << 30)) { c->err = "too many geometries"; return -1; }
   c->n_sph = n_s;
@@ -826,15 +889,16 @@ int gf_set_profiling(gf_ctx *ctx, int on) {
   GF_CHECK(c, cudaDeviceSynchronize());
   c->prof = on != 0;
   c->prof_used = 0;
-  for (int q = 0; q < 4; ++q) c->prof_ms[q] = 0.0;
+  for (int q = 0; q < 5; ++q) c->prof_ms[q] = 0.0;
   c->prof_steps = 0;
   return 0;
 }
 
-int gf_kernel_times(gf_ctx *ctx, double *out5) {
+int gf_kernel_times(gf_ctx *ctx, double *out6) {
   CTX_CHECK(ctx);
-  for (int q = 0; q < 4; ++q) out5[q] = c->prof_ms[q];
-  out5[4] = double(c->prof_steps);
+  for (int q = 0; q < 4; ++q) out6[q] = c->prof_ms[q];
+  out6[4] = double(c->prof_steps);
+  out6[5] = c->prof_ms[4];
   return 0;
 }
 

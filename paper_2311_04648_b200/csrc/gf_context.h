@@ -155,9 +155,10 @@ struct Ctx {
   void *user_fn_f64 = nullptr, *user_fn_f32 = nullptr;
   // per-kernel device timing (enabled by gf_set_profiling)
   bool prof = false;
-  std::vector<cudaEvent_t> prof_ev;   // 4 per profiled step: start, contacts, heavy, integrate
+  std::vector<cudaEvent_t> prof_ev;   // kProfEv per profiled step: start, contacts, heavy, integrate,
+                                      // after the fused sphere-sphere kernel
   size_t prof_used = 0;
-  double prof_ms[4] = {0, 0, 0, 0};   // contacts, heavy, integrate, kT
+  double prof_ms[5] = {0, 0, 0, 0, 0};   // contacts, heavy, integrate, kT, sphere-sphere kernel
   int64_t prof_steps = 0;
   // spatial decomposition (gf_set_decomposition): per-owner class | gid << 2
   DBuf dd, dd_x0;
@@ -165,12 +166,16 @@ struct Ctx {
   int dd_axis = 0;
   double dd_travel = 0.0;
   double lever_override = 0.0;   // global lever arm so fixed-point scales agree across ranks
+  DBuf owner_stage;              // host-layout staging of gf_upload_owners / gf_download_owners
+  std::vector<uint32_t> h_tri_owner, h_ana_owner;   // mesh / analytic owners (world_moving)
+  std::vector<double> h_tpl_moi;
   DBuf halo_scratch;             // uint32 index staging for host-index halo calls
   // split-step run in progress (gf_run_begin ... gf_run_end)
   struct RunState *run = nullptr;
 };
 
 // take 4 timing events for one profiled dT step (nullptr when off)
+constexpr int kProfEv = 5;
 cudaEvent_t *prof_events(Ctx *c);
 // the set the current step's force phase opened (nullptr when off)
 cudaEvent_t *prof_current(Ctx *c);

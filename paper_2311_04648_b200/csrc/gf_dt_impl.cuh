@@ -803,6 +803,7 @@ int dt_forces_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
   GF_CHECK(c, cudaMemsetAsync(&v.st->touching, 0, sizeof(unsigned long long), s));
   cudaEvent_t *ev = prof_events(c);
   if (ev) cudaEventRecord(ev[0], s);
+  bool ss_timed = false;   // ev[4] recorded after the fused sphere-sphere kernel
   if (v.n_acs) {
     unsigned long long *tn = c->tlist_n.as<unsigned long long>();
     // list0: sphere-sphere entries (uint4 records in the fused build), list1: the other kinds
@@ -819,15 +820,17 @@ int dt_forces_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
       k_touch<<<148 * 4, 256, 0, s>>>(v, list0, list1, tn, (unsigned long long)a.step, v.seg + c->n_sph);
       k_forces_f32<<<148 * 8, 256, 0, s>>>(v, a.h, a.sim_time, reinterpret_cast<const uint4 *>(list0), tn);
     } else if (fused) {
-      // the wall kinds' narrow phase (feeds k_forces below), then the
-      // sphere-sphere block in one fused pass
-      k_touch<<<148 * 4, 256, 0, s>>>(v, list0, list1, tn, (unsigned long long)a.step, v.seg + c->n_sph);
+      // the sphere-sphere block in one fused pass, then the wall kinds'
+      // narrow phase (feeds k_forces below)
       if (c->ss_split == 2)
         k_contacts_ss<1, 4><<<148 * 4, 256, 0, s>>>(v, a.h, (unsigned long long)a.step);
       else if (c->ss_split == 3)
         k_contacts_ss<2, 4><<<148 * 4, 256, 0, s>>>(v, a.h, (unsigned long long)a.step);
       else
         k_contacts_ss<2, 3><<<148 * 3, 256, 0, s>>>(v, a.h, (unsigned long long)a.step);
+      if (ev) cudaEventRecord(ev[4], s);
+      ss_timed = true;
+      k_touch<<<148 * 4, 256, 0, s>>>(v, list0, list1, tn, (unsigned long long)a.step, v.seg + c->n_sph);
     } else {
       k_touch<<<unsigned(std::min<int64_t>((v.n_acs + 255) / 256, 148 * 16)), 256, 0, s>>>(
           v, list0, list1, tn, (unsigned long long)a.step, nullptr);
@@ -838,7 +841,10 @@ int dt_forces_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
       k_forces<VelT><<<148 * 8, 128, 0, s>>>(v, a.h, a.sim_time, list0, list1, tn, fused ? 1 : 0);
     }
   }
-  if (ev) cudaEventRecord(ev[1], s);
+  if (ev) {
+    if (!ss_timed) cudaEventRecord(ev[4], s);   // no fused sphere-sphere kernel this step
+    cudaEventRecord(ev[1], s);
+  }
   if (v.n_acs && !c->fixed_reduce) k_heavy<<<64, 256, 0, s>>>(v);
   if (ev) cudaEventRecord(ev[2], s);
   GF_CHECK(c, cudaGetLastError());
