@@ -341,8 +341,12 @@ gf_ctx *gf_create(int device, uint32_t flags) {
   c->flags = flags;
   c->f32_state = (flags & GF_STATE_F32) != 0;
   c->fixed_reduce = c->f32_state;
-  cudaStreamCreateWithFlags(&c->s_dt, cudaStreamNonBlocking);
-  cudaStreamCreateWithFlags(&c->s_kt, cudaStreamNonBlocking);
+  // stream priorities (GF_STREAM_PRIO): 0 equal, 1 dT first, 2 kT first
+  int prio_lo = 0, prio_hi = 0, mode = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  if (const char *sp = std::getenv("GF_STREAM_PRIO")) mode = std::atoi(sp);
+  cudaStreamCreateWithPriority(&c->s_dt, cudaStreamNonBlocking, mode == 1 ? prio_hi : prio_lo);
+  cudaStreamCreateWithPriority(&c->s_kt, cudaStreamNonBlocking, mode == 2 ? prio_hi : prio_lo);
   cudaEventCreateWithFlags(&c->ev_snap, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->ev_ca, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->ev_adopted, cudaEventDisableTiming);

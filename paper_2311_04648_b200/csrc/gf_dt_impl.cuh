@@ -180,17 +180,6 @@ __device__ __forceinline__ void qrotf(const float4 q, float x, float y, float z,
 // after in fp32 (normal, lever arms from the fp32-rotated clump offsets,
 // velocities, the contact law).  The other kinds (walls) take k_forces.
 // Contributions go to the int64 fixed-point owner accumulators as before.
-// Sum of v over this lane's run [lane, run_end] of equal keys, left in the
-// run's head lane (segmented reduction; all 32 lanes take part).
-__device__ __forceinline__ long long run_sum(long long v, int lane, int run_end) {
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const long long o = __shfl_down_sync(0xffffffffu, v, off);
-    if (lane + off <= run_end) v += o;
-  }
-  return v;
-}
-
 constexpr int kSmemMat = 256;   // material pairs staged in shared memory (n_mat <= 16)
 
 // pair table rows E_cnt, G_cnt, mu, C_rr, beta as float (forces.py:443-460),
@@ -319,15 +308,27 @@ __device__ __forceinline__ void ss_force_warp(const DtView &v, bool live, uint32
   const unsigned heads = __ballot_sync(0xffffffffu, head);
   const unsigned later = heads & ~((2u << lane) - 1u);   // heads after this lane
   const int run_end = later ? __ffs(later) - 2 : 31;
-  unsigned long long *fa = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(fixed_a ? oa : 0));
+  // segmented sums over the runs: only as many doubling steps as the longest
+  // run needs (runs are short -- an owner's touching partners of higher slot)
+  const unsigned runlen = (head && fixed_a) ? unsigned(run_end - lane + 1) : 0u;
+  const unsigned maxrun = __reduce_max_sync(0xffffffffu, runlen);
+  long long acc[6];
 #pragma unroll
   for (int q = 0; q < 3; ++q) {
-    const long long f = run_sum(fixed_a ? __double2ll_rn(double(out[q]) * double(sa_f)) : 0ll, lane, run_end);
-    const long long t = run_sum(fixed_a ? __double2ll_rn(double(ta[q]) * double(sa_t)) : 0ll, lane, run_end);
-    if (head && fixed_a) {
-      atomicAdd(fa + q, (unsigned long long)f);
-      atomicAdd(fa + 3 + q, (unsigned long long)t);
+    acc[q] = fixed_a ? __double2ll_rn(double(out[q]) * double(sa_f)) : 0ll;
+    acc[3 + q] = fixed_a ? __double2ll_rn(double(ta[q]) * double(sa_t)) : 0ll;
+  }
+  for (unsigned off = 1; off < maxrun; off <<= 1) {
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      const long long o = __shfl_down_sync(0xffffffffu, acc[q], off);
+      if (lane + int(off) <= run_end) acc[q] += o;
     }
+  }
+  if (head && fixed_a) {
+    unsigned long long *fa = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(oa));
+#pragma unroll
+    for (int q = 0; q < 6; ++q) atomicAdd(fa + q, (unsigned long long)acc[q]);
   }
 }
 
