@@ -31,6 +31,9 @@ import sys
 import threading
 import time
 
+# NCCL's own log lines (NCCL_DEBUG) go to stderr: stdout carries only the JSON line
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -358,11 +361,11 @@ def b200_arm(args):
             "gpu_launches": int(args.steps * launches_per_step + (args.steps // max(1, period)) * kt_launches),
             "cpu_baseline": cpu,
         }
+    if line is not None:
+        print(json.dumps(line), flush=True)
     sim.close()
     if dist is not None:
         dist.destroy_process_group()
-    if line is not None:
-        print(json.dumps(line), flush=True)
 
 
 def measure_e2e(sim, steps):
