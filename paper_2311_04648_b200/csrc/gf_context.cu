@@ -504,9 +504,13 @@ int gf_upload_owners(gf_ctx *ctx, int64_t n, const uint64_t *voxel, const uint16
       ensure(c, c->quat, 16 * n, s) || ensure(c, c->lin_vel, vb * n, s) ||
       ensure(c, c->ang_vel, vb * n, s) || ensure(c, c->meta, 4 * n, s) ||
       ensure(c, c->tpl, 32 * (n_tpl + 1), s) || ensure(c, c->acc, 48 * n, s) ||
-      ensure(c, c->heavy_acc, 48 * n, s) || ensure(c, c->inc_start, 4 * (n + 2), s) ||
       ensure(c, c->facc, 48 * n, s) || ensure(c, c->tpl_scale, 16 * (n_tpl + 1), s) ||
-      ensure(c, c->heavy, 4 * (n + 1), s) || ensure(c, c->owner_stage, kStageBytesPerOwner * (n + 1), s))
+      ensure(c, c->owner_stage, kStageBytesPerOwner * (n + 1), s))
+    return -1;
+  // the parity build's incidence-list reduction (the throughput build sums
+  // into the fixed-point accumulators instead)
+  if (!c->f32_state && (ensure(c, c->heavy_acc, 48 * n, s) || ensure(c, c->inc_start, 4 * (n + 2), s) ||
+                        ensure(c, c->heavy, 4 * (n + 1), s)))
     return -1;
   const Stage st = stage_of(c->owner_stage, n);
   if (n) {

@@ -68,6 +68,7 @@ struct KtScratch {
   int64_t cslot_gen[2] = {-1, -1};
   int64_t cand_gen = 0;
   uint64_t det_serial = 0;
+  int64_t last_ss = 0, ss_need = 0;   // sphere-sphere block size of the last detection / after an overflow
   bool cand_valid = false;
   double cand_skin = -1.0;
   int64_t tmp_cap = 0;
@@ -140,6 +141,7 @@ struct Ctx {
   double kt_margin = 0.0;
   double kt_bin_size = 0.0;  // > 0: explicit bin size (detect_contacts(bin_size=...))
   double skin_factor = 1.0;  // Verlet skin = skin_factor * margin
+  int tlist_words = 5;       // words per contact of the touching lists (1 on the fused path)
   int ss_split = 0;          // throughput build: split narrow/force sphere-sphere kernels (GF_SS_SPLIT=1)
   // schedule state (kept across gf_run calls)
   bool first_adopt = true;     // the first do_dynamics detects and waits (engine.py:679-682)
@@ -176,6 +178,8 @@ struct Ctx {
 
 // take 4 timing events for one profiled dT step (nullptr when off)
 constexpr int kProfEv = 5;
+// throughput build, built-in model: the fused sphere-sphere contact kernel
+inline bool ss_fused(const Ctx *c) { return c->f32_state && c->wild_w == 4 && !c->user_model && c->ss_split != 1; }
 cudaEvent_t *prof_events(Ctx *c);
 // the set the current step's force phase opened (nullptr when off)
 cudaEvent_t *prof_current(Ctx *c);

@@ -807,8 +807,14 @@ int dt_forces_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
   bool ss_timed = false;   // ev[4] recorded after the fused sphere-sphere kernel
   if (v.n_acs) {
     unsigned long long *tn = c->tlist_n.as<unsigned long long>();
+    // the touching lists were sized for the fused path: a user model or the
+    // split path switched on since needs the full layout
+    if (!ss_fused(c) && c->tlist_words != 5) {
+      if (ensure(c, c->tlist, 5 * sizeof(uint32_t) * c->tlist_cap, s)) return -1;
+      c->tlist_words = 5;
+    }
     // list0: sphere-sphere entries (uint4 records in the fused build), list1: the other kinds
-    uint32_t *list0 = c->tlist.as<uint32_t>(), *list1 = list0 + 4 * c->tlist_cap;
+    uint32_t *list0 = c->tlist.as<uint32_t>(), *list1 = list0 + (c->tlist_words == 5 ? 4 * c->tlist_cap : 0);
     GF_CHECK(c, cudaMemsetAsync(tn, 0, 2 * sizeof(unsigned long long), s));
     // throughput build + built-in model: sphere-sphere contacts take the fp32
     // path (k_forces_f32), the wall kinds the generic k_forces

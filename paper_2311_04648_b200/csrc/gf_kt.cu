@@ -901,7 +901,8 @@ __global__ void __launch_bounds__(kFcBlock) k_filter_bits(KtView v, const uint2 
 __global__ void __launch_bounds__(kFcBlock) k_compact(KtView v, const uint2 *cand, int64_t n_cand,
                                                       const uint32_t *bits, const unsigned long long *blk_pre,
                                                       const uint32_t *obits, const unsigned long long *oblk_pre,
-                                                      uint2 *out_ids, unsigned long long *seg, uint32_t *old_pos) {
+                                                      uint2 *out_ids, unsigned long long *seg, uint32_t *old_pos,
+                                                      unsigned long long ss_cap) {
   // the filter block's kFcSpan candidates: kFcSpan / 32 bitmask words
   constexpr int kW = kFcSpan / 32;
   __shared__ uint32_t s_w[kW], s_ow[kW];
@@ -940,7 +941,7 @@ __global__ void __launch_bounds__(kFcBlock) k_compact(KtView v, const uint2 *can
     const long long ap = e > 0 ? (long long)cand[e - 1].x : -1;
     for (long long sp = ap + 1; sp <= a; ++sp) seg[sp] = p;
     const bool hit = (word >> lane) & 1u;
-    if (hit) {
+    if (hit && p < ss_cap) {   // beyond: the fill phase grows the array and recounts
       out_ids[p] = it;
       if (obits) {
         const uint32_t oword = obits[w_base + wl];
@@ -1251,7 +1252,7 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
       ensure(c, k.cell_end, sizeof(uint32_t) * (kMaxCells + 1), s))
     return -1;
   if (k.cand_cap == 0) {
-    int64_t cap = std::max<int64_t>(16 * n, 4096);
+    int64_t cap = std::max<int64_t>(10 * n, 4096);   // grown on overflow below
     if (ensure(c, k.cand_tmp, sizeof(uint2) * cap, s) || ensure(c, k.cand, sizeof(uint2) * cap, s)) return -1;
     k.cand_cap = cap;
   }
@@ -1332,6 +1333,7 @@ int kt_count(Ctx *c, cudaStream_t s, bool force_rebuild) {
   if (force_rebuild || !k.cand_valid || hs->rebuild) {
     hs->cand_total = 0;
     if (rebuild_candidates(c, s)) return -1;
+    hs->rebuild = 0;   // consumed (a recount of this detection must not rebuild again)
   }
   if (ensure(c, k.counts, sizeof(unsigned long long) * (3 * n + 1), s) || ensure(c, k.tmp_n, 16, s))
     return -1;
@@ -1340,10 +1342,13 @@ int kt_count(Ctx *c, cudaStream_t s, bool force_rebuild) {
     if (ensure(c, k.tmp, sizeof(uint2) * cap, s)) return -1;
     k.tmp_cap = cap;
   }
-  // the sphere-sphere block is compacted straight into the next array: size it
-  // for every candidate plus the wall-pair scratch capacity
+  // the sphere-sphere block is compacted straight into the next array: room
+  // for the last block's size + 1/8 (or 3/4 of the candidates) plus the
+  // wall-pair scratch capacity; k_compact drops rows beyond it and the fill
+  // phase grows the array and redoes the count (rare)
   Acs &out = c->acs_next;
-  const int64_t need = k.n_cand + k.tmp_cap + 1;
+  const int64_t ss_guess = k.last_ss > 0 ? k.last_ss + k.last_ss / 8 + 1024 : (3 * k.n_cand) / 4 + 1024;
+  const int64_t need = std::min<int64_t>(k.n_cand, std::max<int64_t>(ss_guess, k.ss_need)) + k.tmp_cap + 1;
   if (need > out.cap) {
     int64_t cap = need + need / 4 + 1024;
     if (ensure(c, out.ids, sizeof(uint2) * cap, s) || ensure(c, out.wild, sizeof(float) * c->wild_w * cap, s) ||
@@ -1381,7 +1386,7 @@ int kt_count(Ctx *c, cudaStream_t s, bool force_rebuild) {
     k_compact<<<unsigned(nblk), kFcBlock, 0, s>>>(
         v, k.cand.as<uint2>(), k.n_cand, k.fbits[cur].as<uint32_t>(), k.fpre[cur].as<unsigned long long>(),
         rows_ok ? k.fbits[prev].as<uint32_t>() : nullptr, rows_ok ? k.fpre[prev].as<unsigned long long>() : nullptr,
-        out.ids.as<uint2>(), oseg, out.old_pos.as<uint32_t>());
+        out.ids.as<uint2>(), oseg, out.old_pos.as<uint32_t>(), (unsigned long long)(out.cap - k.tmp_cap - 1));
   } else {
     GF_CHECK(c, cudaMemsetAsync(oseg, 0, sizeof(unsigned long long) * (n + 1), s));
     GF_CHECK(c, cudaMemsetAsync(k.fpre[cur].p, 0, sizeof(unsigned long long), s));
@@ -1419,21 +1424,27 @@ int kt_detect_fill(Ctx *c, Acs &out, cudaStream_t s) {
   KtScratch &k = c->kt;
   const int64_t n = c->n_sph;
   Status *hs = reinterpret_cast<Status *>(c->h_status);
-  if ((int64_t)hs->other_total > k.tmp_cap) {
-    // the sphere-triangle / sphere-analytic scratch list overflowed: grow, redo
-    {
+  for (int attempt = 0;; ++attempt) {
+    const int64_t ss_total = int64_t(hs->acs_total) - int64_t(hs->other_total);
+    const bool tmp_over = (int64_t)hs->other_total > k.tmp_cap;
+    const bool ss_over = ss_total > out.cap - k.tmp_cap - 1;
+    if (!tmp_over && !ss_over) break;
+    if (attempt > 4) { c->err = "contact array sizing did not converge"; return -1; }
+    // a scratch list or the sphere-sphere block overflowed: grow, redo
+    if (tmp_over) {
       int64_t cap = int64_t(hs->other_total) + int64_t(hs->other_total) / 4 + 4096;
       if (ensure(c, k.tmp, sizeof(uint2) * cap, s)) return -1;
       k.tmp_cap = cap;
     }
+    if (ss_over) k.ss_need = ss_total + ss_total / 8 + 1024;
     k.cslot_cur ^= 1;   // the redo rewrites the same detection's rows
     --k.det_serial;
     if (kt_count(c, s)) return -1;
     GF_CHECK(c, cudaStreamSynchronize(s));
     out.n = int64_t(hs->acs_total);
   }
-  // kt_count sized the array for every candidate plus the scratch capacity
   if (out.n > out.cap) { c->err = "contact array overflow"; return -1; }
+  k.last_ss = int64_t(hs->acs_total) - int64_t(hs->other_total);
   if (n && out.n) {
     const unsigned long long *off = out.seg.as<unsigned long long>();
     GF_CHECK(c, cudaMemsetAsync(k.cursor.p, 0, sizeof(unsigned) * 3 * n, s));
@@ -1526,11 +1537,11 @@ int build_segments(Ctx *c, Acs &a, cudaStream_t s) {
 int build_incidence(Ctx *c, cudaStream_t s) {
   const int64_t n = c->acs.n;
   const int64_t cap = std::max<int64_t>(c->acs.cap, 1);
-  // two compacted lists of touching entries: sphere-sphere (uint4 records)
-  // at [0, 4 cap) words, the other kinds at [4 cap, 5 cap)
-  if (ensure(c, c->tlist, 5 * sizeof(uint32_t) * cap, s) || ensure(c, c->tlist_n, 16, s) ||
-      ensure(c, c->touch, cap, s))
-    return -1;
+  // compacted lists of touching entries: sphere-sphere (uint4 records of the
+  // split path) at [0, 4 cap) words, the other kinds at [4 cap, 5 cap); the
+  // fused throughput path needs only the second (tlist_words says which)
+  c->tlist_words = ss_fused(c) ? 1 : 5;
+  if (ensure(c, c->tlist, c->tlist_words * sizeof(uint32_t) * cap, s) || ensure(c, c->tlist_n, 16, s)) return -1;
   c->tlist_cap = cap;
   if (c->fixed_reduce) return 0;  // throughput build reduces with atomics
   if (ensure(c, c->out_c, sizeof(double) * 9 * cap, s) || ensure(c, c->touch, cap, s) ||

@@ -101,18 +101,24 @@ def lever_max(store) -> float:
 
 
 def morton_order(pos: np.ndarray) -> np.ndarray:
-    """Device order of owners: 30-bit Morton code of the positions (the order
-    Simulator._build_permutation uses), stable."""
+    """Device order of owners: 63-bit Morton code (21 bits per axis) of the
+    positions, stable.  Simulator._build_permutation uses this same function,
+    so a decomposed run orders every rank's owners like a single context."""
     n = pos.shape[0]
     if n <= 1:
         return np.arange(n, dtype=np.int64)
     lo = pos.min(axis=0)
     span = max(float((pos.max(axis=0) - lo).max()), 1e-300)
-    q = np.minimum((pos - lo) / span * 1023.0, 1023.0).astype(np.uint64)
-    code = np.zeros(n, np.uint64)
-    for bit in range(10):
-        for ax in range(3):
-            code |= ((q[:, ax] >> np.uint64(bit)) & np.uint64(1)) << np.uint64(3 * bit + ax)
+    q = np.minimum((pos - lo) / span * 2097151.0, 2097151.0).astype(np.uint64)
+
+    def spread(x):   # bit i of x -> bit 3 i
+        x = x & np.uint64(0x1FFFFF)
+        for sh, m in ((32, 0x1F00000000FFFF), (16, 0x1F0000FF0000FF), (8, 0x100F00F00F00F00F),
+                      (4, 0x10C30C30C30C30C3), (2, 0x1249249249249249)):
+            x = (x | (x << np.uint64(sh))) & np.uint64(m)
+        return x
+
+    code = spread(q[:, 0]) | (spread(q[:, 1]) << np.uint64(1)) | (spread(q[:, 2]) << np.uint64(2))
     return np.argsort(code, kind="stable").astype(np.int64)
 
 

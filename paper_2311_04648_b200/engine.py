@@ -445,15 +445,8 @@ class Simulator:
         s = self.store
         n = s.n_owners
         if self.reorder and n > 1:
-            pos = s.positions()
-            lo = pos.min(axis=0)
-            span = max(float((pos.max(axis=0) - lo).max()), 1e-300)
-            q = np.minimum((pos - lo) / span * 1023.0, 1023.0).astype(np.uint64)
-            code = np.zeros(n, np.uint64)
-            for bit in range(10):
-                for ax in range(3):
-                    code |= ((q[:, ax] >> np.uint64(bit)) & np.uint64(1)) << np.uint64(3 * bit + ax)
-            d2u = np.argsort(code, kind="stable").astype(np.int64)
+            from .decomp import morton_order
+            d2u = morton_order(s.positions())
         else:
             d2u = np.arange(n, dtype=np.int64)
         u2d = np.empty(n, np.int64)

@@ -15,6 +15,9 @@ crater_bed  configs[1]: projectile impact onto an n-sphere polydisperse bed.
             (the reference's 1e-4 s / 30 m/s give a 24 mm detection margin,
             i.e. thousands of candidate pairs per grain).
 settling_box configs[0]: monodisperse r = 5 mm spheres in a walled box.
+tiled_bed   configs[4]'s size sweep: tx x ty copies of a settled crater bed
+            side by side in one box (same grains, same step), so the sphere
+            count grows at fixed grain size.
 """
 
 from __future__ import annotations
@@ -50,8 +53,8 @@ def crater_bed(n_spheres: int = 1_000_000, *, seed: int = 7, h: float = 1e-5, v_
     dom = Domain((-half_x - 0.2 * bed_half, -bed_half * 1.2, -0.02),
                  (half_x + 0.2 * bed_half, bed_half * 1.2, depth * 3.0 + 0.3))
     sim = Simulator(dom, precision=precision, device=device, decomposition=decomposition)
-    grain = sim.load_material({"E": 5e6, "nu": 0.3, "CoR": 0.5, "mu": 0.3, "Crr": 0.01})
-    wall = sim.load_material({"E": 5e6, "nu": 0.3, "CoR": 0.5, "mu": 0.3, "Crr": 0.01})
+    grain = sim.load_material(dict(CRATER_MATERIAL))
+    wall = sim.load_material(dict(CRATER_MATERIAL))
     tpls = [sim.load_clump_template(ClumpTemplate.solid_sphere(
         float(r), 2500.0 * 4.0 / 3.0 * math.pi * float(r) ** 3, grain)) for r in radii]
     # lattice pitch d_max: the largest grains touch, nobody overlaps
@@ -98,6 +101,59 @@ def crater_bed(n_spheres: int = 1_000_000, *, seed: int = 7, h: float = 1e-5, v_
     sim.set_init_time_step(h)
     sim.set_error_out_velocity(v_err)
     sim.set_fixed_lookahead(n_max)
+    return sim
+
+
+CRATER_MATERIAL = {"E": 5e6, "nu": 0.3, "CoR": 0.5, "mu": 0.3, "Crr": 0.01}
+
+
+def tiled_bed(src: Simulator, tx: int, ty: int, *, precision: str = "f32", device: int = 0,
+              n_max: int = 4) -> Simulator:
+    """tx x ty copies of the (settled, released) crater bed `src` in one box:
+    owners keep their state (position, orientation, velocities), copies are
+    laid out at the bed pitch 12 D, the floor and the four outer walls bound
+    the whole array (inner walls removed; every grain is at least its radius
+    from its old wall plane, so copies meet without overlap)."""
+    from .core import OWNER_CLUMP, decode_position
+    s = src.store
+    n = s.n_owners
+    s.voxel  # sync the host mirror
+    d = s.__dict__
+    pos = decode_position(d["_voxel"][:n], d["_subvoxel"][:n], s.domain)
+    clump = d["_owner_kind"][:n] == OWNER_CLUMP
+    tpl = d["_owner_template"][:n]
+    D = 0.0254
+    bed_half = 12.0 * D / 2.0
+    lo, hi = s.domain.lo, s.domain.hi
+    dom = Domain((-tx * bed_half - 0.2 * bed_half, -ty * bed_half - 0.2 * bed_half, float(lo[2])),
+                 (tx * bed_half + 0.2 * bed_half, ty * bed_half + 0.2 * bed_half, float(hi[2])))
+    sim = Simulator(dom, precision=precision, device=device)
+    grain = sim.load_material(dict(CRATER_MATERIAL))
+    wall = sim.load_material(dict(CRATER_MATERIAL))
+    for t in s.templates:
+        sim.load_clump_template(t)
+    offsets = [(-tx * bed_half + (2 * ix + 1) * bed_half, -ty * bed_half + (2 * iy + 1) * bed_half)
+               for iy in range(ty) for ix in range(tx)]
+    dd = sim.store.__dict__
+    for t in range(len(s.templates)):
+        sel = np.nonzero(clump & (tpl == t))[0]
+        if not sel.size:
+            continue
+        for ox, oy in offsets:
+            ids = np.asarray(sim.add_clumps(t, pos[sel] + np.array([ox, oy, 0.0])), dtype=np.int64)
+            for name in ("_lin_vel", "_ang_vel", "_quat", "_owner_family"):
+                dd[name][ids] = d[name][sel]
+    hx, hy = tx * bed_half, ty * bed_half
+    walls = [("plane", (0, 0, 0), (0, 0, 1), wall),
+             ("plane", (-hx, 0, 0), (1, 0, 0), wall), ("plane", (hx, 0, 0), (-1, 0, 0), wall),
+             ("plane", (0, -hy, 0), (0, 1, 0), wall), ("plane", (0, hy, 0), (0, -1, 0), wall)]
+    sim.add_analytic(walls, family=255)
+    sim.set_family_fixed(255)
+    sim.set_gravity(src.gravity)
+    sim.set_init_time_step(src.h)
+    sim.set_error_out_velocity(src.v_err)
+    sim.set_fixed_lookahead(n_max)
+    del grain
     return sim
 
 

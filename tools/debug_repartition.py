@@ -40,10 +40,10 @@ for k in range(0, steps, chunk):
         print("  single x", single._pos[o], "group x", st["pos"][o])
         print("  touching single", single._last_touching, "group", sum(s._last_touching for s in sims))
         ca = single._acs
-        sel = np.nonzero(np.isin(ca.geom_a, single.store.owner_geoms[o]) | np.isin(ca.geom_b, single.store.owner_geoms[o]))[0]
+        sel = np.nonzero(np.isin(ca.geom_a, single.store.geoms_of(o)) | np.isin(ca.geom_b, single.store.geoms_of(o)))[0]
         print("  single acs of owner", [(int(ca.kind[i]), int(ca.geom_a[i]), int(ca.geom_b[i]), [float(ca.wildcards[w][i]) for w in ca.wildcards]) for i in sel])
         ga = st["acs"]
-        sel = np.nonzero(np.isin(ga.geom_a, single.store.owner_geoms[o]) | np.isin(ga.geom_b, single.store.owner_geoms[o]))[0]
+        sel = np.nonzero(np.isin(ga.geom_a, single.store.geoms_of(o)) | np.isin(ga.geom_b, single.store.geoms_of(o)))[0]
         print("  group acs of owner", [(int(ga.kind[i]), int(ga.geom_a[i]), int(ga.geom_b[i]), [float(ga.wildcards[w][i]) for w in ga.wildcards]) for i in sel])
         for s in sims:
             st_ = s._dd
