@@ -28,14 +28,23 @@ namespace gf {
 
 void set_err(Ctx *c, const std::string &msg) { c->err = msg; }
 
+// Grow-only device buffer: exactly `bytes` (callers that grow repeatedly add
+// their own slack); without `keep` the old block is freed first so a large
+// buffer never needs twice its size.
 int ensure(Ctx *c, DBuf &b, size_t bytes, cudaStream_t s, bool keep) {
   if (bytes == 0) bytes = 16;
   if (b.bytes >= bytes) return 0;
-  size_t nb = bytes + bytes / 4 + 256;
+  const size_t nb = bytes + 256;
   void *p = nullptr;
   cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess && !keep && b.p) {
+    cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+  }
   if (e == cudaSuccess) e = cudaMalloc(&p, nb);
   if (e != cudaSuccess) {
+    (void)cudaGetLastError();
     set_err(c, std::string("device allocation of ") + std::to_string(nb) + " bytes failed: " +
                    cudaGetErrorString(e));
     return -1;
@@ -386,7 +395,7 @@ void gf_destroy(gf_ctx *ctx) {
                   &c->kt.tri_start, &c->kt.tri_entries, &c->kt.counts, &c->kt.offsets, &c->kt.cub_tmp,
                   &c->kt.total, &c->kt.cursor, &c->kt.tri_cursor, &c->big_slots, &c->kt.sc,
                   &c->kt.sm, &c->kt.sf, &c->kt.cells, &c->kt.n_cells, &c->kt.cand, &c->kt.cand_tmp, &c->kt.cand_n,
-                  &c->kt.cand_cnt, &c->kt.cand_seg, &c->kt.ref, &c->kt.flag, &c->kt.cflags, &c->kt.sel_n, &c->kt.tmp, &c->kt.tmp_n, &c->acs.seg, &c->acs_next.seg, &c->acs.old_pos, &c->acs_next.old_pos, &c->kt.fbits[0], &c->kt.fbits[1], &c->kt.fpre[0], &c->kt.fpre[1], &c->kt.fcnt, &c->dd, &c->dd_x0, &c->halo_scratch, &c->owner_stage};
+                  &c->kt.cand_cnt, &c->kt.cand_seg, &c->kt.ref, &c->kt.flag, &c->kt.cflags, &c->kt.sel_n, &c->kt.tmp, &c->kt.tmp_n, &c->acs.seg, &c->acs_next.seg, &c->acs.old_pos, &c->acs_next.old_pos, &c->kt.fbits[0], &c->kt.fbits[1], &c->kt.fpre[0], &c->kt.fpre[1], &c->kt.fcnt, &c->dd, &c->dd_x0, &c->halo_scratch, &c->owner_stage, &c->kt.sa_cnt, &c->kt.sa_off, &c->kt.sa_cand};
   for (DBuf *b : bufs) release(*b);
   free_run(c);
   if (c->h_status) cudaFreeHost(c->h_status);
@@ -552,6 +561,9 @@ int gf_upload_owners(gf_ctx *ctx, int64_t n, const uint64_t *voxel, const uint16
     if (refresh_centers(c, s) || refresh_world(c, s)) return -1;
   }
   GF_CHECK(c, cudaStreamSynchronize(s));
+  // the staging buffer is kept for repeated host round trips, except at
+  // scene sizes where device memory is the limit (2^24 owners and up)
+  if (n >= (int64_t(1) << 24)) release(c->owner_stage);
   world_moving_from_host(c, family);
   return 0;
 }
@@ -984,7 +996,7 @@ int gf_step_forces(gf_ctx *ctx, int64_t i) {
   if (c->next_pending && s >= c->adopt_at && run_adopt(c)) return -1;
   // 2. work order: snapshot on the dT stream, detection on the kT stream
   if (!c->next_pending && (c->first_adopt || s - c->last_snap >= R->period)) {
-    if (kt_snapshot(c, c->s_dt)) return -1;
+    if (kt_snapshot(c, c->s_dt, p->margin)) return -1;
     GF_CHECK(c, cudaEventRecord(c->ev_snap, c->s_dt));
     GF_CHECK(c, cudaStreamWaitEvent(c->s_kt, c->ev_snap, 0));
     GF_CHECK(c, cudaStreamWaitEvent(c->s_kt, c->ev_adopted, 0));

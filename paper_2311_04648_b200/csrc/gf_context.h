@@ -68,7 +68,13 @@ struct KtScratch {
   int64_t cslot_gen[2] = {-1, -1};
   int64_t cand_gen = 0;
   uint64_t det_serial = 0;
-  int64_t last_ss = 0, ss_need = 0;   // sphere-sphere block size of the last detection / after an overflow
+  int64_t last_ss = 0, ss_need = 0;
+  bool snap_det = false, snap_checked = false;   // the last snapshot reduced the grid inputs / ran k_disp
+  // sphere-analytic candidates (while no mesh / analytic owner moves):
+  // per-sphere segments of analytic ids within margin + skin at the rebuild
+  DBuf sa_cnt, sa_off, sa_cand;
+  int64_t n_sa_cand = 0;
+  uint64_t sa_world_version = ~0ull;   // sphere-sphere block size of the last detection / after an overflow
   bool cand_valid = false;
   double cand_skin = -1.0;
   int64_t tmp_cap = 0;
@@ -141,6 +147,7 @@ struct Ctx {
   double kt_margin = 0.0;
   double kt_bin_size = 0.0;  // > 0: explicit bin size (detect_contacts(bin_size=...))
   double skin_factor = 1.0;  // Verlet skin = skin_factor * margin
+  uint64_t world_version = 0;   // bumped whenever mesh / analytic world transforms are recomputed
   int tlist_words = 5;       // words per contact of the touching lists (1 on the fused path)
   int ss_split = 0;          // throughput build: split narrow/force sphere-sphere kernels (GF_SS_SPLIT=1)
   // schedule state (kept across gf_run calls)
@@ -208,7 +215,8 @@ Materials materials_view(Ctx *c);
 Families families_view(Ctx *c);
 
 // kT (gf_kt.cu)
-int kt_snapshot(Ctx *c, cudaStream_t s);                 // centers/families -> kT scratch
+int kt_snapshot(Ctx *c, cudaStream_t s, double margin = -1.0);   // centers/families -> kT scratch
+                                                          // (margin >= 0: a detection's, with grid inputs)
 int kt_begin(Ctx *c, double margin, cudaStream_t s);               // grid + displacement check
 int kt_count(Ctx *c, cudaStream_t s, bool force_rebuild = false);   // candidates -> counts
 int kt_detect_fill(Ctx *c, Acs &out, cudaStream_t s);

@@ -18,6 +18,7 @@ int refresh_centers(Ctx *c, cudaStream_t s) {
 int refresh_world(Ctx *c, cudaStream_t s) {
   int64_t n = c->n_tri + c->n_ana;
   if (!n) return 0;
+  c->world_version++;
   k_world<<<unsigned((n + 127) / 128), 128, 0, s>>>(c->dom, owners_view(c), tris_view(c), anas_view(c));
   GF_CHECK(c, cudaGetLastError());
   return 0;

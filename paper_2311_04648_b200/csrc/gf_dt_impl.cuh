@@ -877,6 +877,7 @@ int dt_integrate_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
   if (ev) cudaEventRecord(ev[3], s);
   if ((c->n_tri || c->n_ana) && c->world_moving) {
     int64_t n = c->n_tri + c->n_ana;
+    c->world_version++;
     k_world<<<unsigned((n + 127) / 128), 128, 0, s>>>(c->dom, v.own, v.tri, v.ana);
   }
   GF_CHECK(c, cudaGetLastError());

@@ -17,6 +17,7 @@
 // (i, j > i), sorted by j, at an exclusive-scan offset: the output is already
 // in canonical (kind, a, b) order and no global pair sort is needed.
 #include <cub/cub.cuh>
+#include <cstdlib>
 
 #include "gf_context.h"
 
@@ -73,15 +74,63 @@ struct KtView {
 // snapshot
 // ---------------------------------------------------------------------------
 // frozen copy of the refreshed sphere centres and families (engine.py:577-596)
-__global__ void k_snapshot(Domain dom, Owners own, Spheres sph, double *centers, double4 *c4, uint8_t *sfam) {
-  int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (k >= sph.n) return;
-  const double4 c = sph.center[k];
-  centers[3 * k] = c.x;
-  centers[3 * k + 1] = c.y;
-  centers[3 * k + 2] = c.z;
-  c4[k] = c;
-  sfam[k] = uint8_t(meta_family(own.meta[sph.owner[k]]));
+// detection snapshot: also the exact min / max of the centres and the
+// largest radius (the grid's inputs, broadphase.py:160-186) and -- when
+// candidate lists exist -- whether a sphere moved more than skin / 2 since
+// their rebuild (the k_disp test), in the same pass over the centres
+__global__ void __launch_bounds__(256) k_snapshot(Domain dom, Owners own, Spheres sph, double *centers,
+                                                  double4 *c4, uint8_t *sfam, unsigned long long *mm,
+                                                  const double *ref, double lim2, int *flag) {
+  double lo[3], hi[3], rmax = 0.0;
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    lo[ax] = __longlong_as_double(0x7FF0000000000000ll);
+    hi[ax] = -lo[ax];
+  }
+  bool far = false;
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < sph.n;
+       k += int64_t(gridDim.x) * blockDim.x) {
+    const double4 c = sph.center[k];
+    centers[3 * k] = c.x;
+    centers[3 * k + 1] = c.y;
+    centers[3 * k + 2] = c.z;
+    c4[k] = c;
+    sfam[k] = uint8_t(meta_family(own.meta[sph.owner[k]]));
+    if (mm) {
+      lo[0] = fmin(lo[0], c.x); lo[1] = fmin(lo[1], c.y); lo[2] = fmin(lo[2], c.z);
+      hi[0] = fmax(hi[0], c.x); hi[1] = fmax(hi[1], c.y); hi[2] = fmax(hi[2], c.z);
+      rmax = fmax(rmax, c.w);
+    }
+    if (ref) {
+      const double dx = c.x - ref[3 * k], dy = c.y - ref[3 * k + 1], dz = c.z - ref[3 * k + 2];
+      far = far || dx * dx + dy * dy + dz * dz > lim2;
+    }
+  }
+  if (ref && __any_sync(0xffffffffu, far) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+  if (!mm) return;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      lo[ax] = fmin(lo[ax], __shfl_down_sync(0xffffffff, lo[ax], off));
+      hi[ax] = fmax(hi[ax], __shfl_down_sync(0xffffffff, hi[ax], off));
+    }
+    rmax = fmax(rmax, __shfl_down_sync(0xffffffff, rmax, off));
+  }
+  __shared__ double sh[7][8];
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    for (int ax = 0; ax < 3; ++ax) { sh[ax][warp] = lo[ax]; sh[3 + ax][warp] = hi[ax]; }
+    sh[6][warp] = rmax;
+  }
+  __syncthreads();
+  if (threadIdx.x < 7) {
+    const int q = threadIdx.x;
+    double acc = sh[q][0];
+    for (int w = 1; w < nw; ++w) acc = q < 3 ? fmin(acc, sh[q][w]) : fmax(acc, sh[q][w]);
+    if (q < 3) atomicMin(&mm[q], ord_key(acc));
+    else atomicMax(&mm[q], ord_key(acc));
+  }
 }
 
 __global__ void k_geom_family(int64_t n, const uint32_t *owner, const uint32_t *meta, uint8_t *fam) {
@@ -284,27 +333,6 @@ __device__ __forceinline__ bool bstar_in_ranges(const Grid &g, const double ci[3
   return true;
 }
 
-// collect_sphere_pairs predicate (_kernels.py:305-321) for spheres i, j: the
-// distance test, then the reference's dedup bin (bin of the min corner of the
-// enlarged boxes' intersection) must lie in both registration ranges
-__device__ __forceinline__ bool ss_pair(const KtView &v, const Grid &g, uint32_t i, uint32_t j,
-                                        const double ci[3], float ri_f, const long long lo_i[3],
-                                        const long long hi_i[3], uint32_t oi, uint8_t fi) {
-  uint32_t oj = v.sph.owner[j];
-  if (oi == oj || !dd_keep(v.own.dd, oi, oj)) return false;
-  if (!v.mask[256 * fi + v.sfam[j]]) return false;
-  const double *cj = v.centers + 3 * size_t(j);
-  double dx = sub_(ci[0], cj[0]), dy = sub_(ci[1], cj[1]), dz = sub_(ci[2], cj[2]);
-  float rj_f = v.sph.offr[j].w;
-  double ri = add(double(ri_f), v.margin);
-  double rj = add(double(rj_f), v.margin);
-  double rr = sub_(add(ri, rj), v.margin);
-  if (add(add(mul(dx, dx), mul(dy, dy)), mul(dz, dz)) >= mul(rr, rr)) return false;
-  (void)lo_i; (void)hi_i;
-  double cjv[3] = {cj[0], cj[1], cj[2]};
-  return bstar_in_ranges(g, ci, ri, ri_f, cjv, rj, rj_f, v.margin);
-}
-
 // collect_sphere_tri_pairs predicate (_kernels.py:375-401): distance test,
 // reported once -- in the enumeration cell (fx, fy, fz) holding the min
 // corner -- and only if the reference's dedup bin lies in both reference
@@ -396,41 +424,6 @@ __global__ void k_gather_sorted(int64_t n, const uint32_t *sorted, const double 
   sf[u] = make_float4(float(x - g.glo[0]), float(y - g.glo[1]), float(z - g.glo[2]), offr[i].w);
 }
 
-// exact sphere-sphere predicate (_kernels.py:305-321) on cell-sorted copies;
-// (l, h) are the lower / higher slot, matching the reference's i < j order
-__device__ __forceinline__ bool ss_pair_sorted(const KtView &v, const Grid &g, const double4 &cl,
-                                               const uint4 &ml, const double4 &ch, const uint4 &mh) {
-  if (ml.y == mh.y || !dd_keep(v.own.dd, ml.y, mh.y)) return false;
-  if (!v.mask[256 * ml.z + mh.z]) return false;
-  double dx = sub_(cl.x, ch.x), dy = sub_(cl.y, ch.y), dz = sub_(cl.z, ch.z);
-  double ri = add(cl.w, v.margin);
-  double rj = add(ch.w, v.margin);
-  double rr = sub_(add(ri, rj), v.margin);
-  if (add(add(mul(dx, dx), mul(dy, dy)), mul(dz, dz)) >= mul(rr, rr)) return false;
-  double ci[3] = {cl.x, cl.y, cl.z}, cj[3] = {ch.x, ch.y, ch.z};
-  return bstar_in_ranges(g, ci, ri, float(cl.w), cj, rj, float(ch.w), v.margin);
-}
-
-// exact test of one queued candidate (sorted indices u0, u1) and its output
-__device__ __forceinline__ void ss_resolve(const KtView &v, const Grid &g, const double4 *sc, const uint4 *sm,
-                                           bool valid, uint2 q, unsigned long long *counts, uint2 *tmp,
-                                           unsigned long long *tmp_n, unsigned long long cap) {
-  bool hit = false;
-  uint2 e = make_uint2(0, 0);
-  if (valid) {
-    const double4 c0 = sc[q.x], c1 = sc[q.y];
-    const uint4 m0 = sm[q.x], m1 = sm[q.y];
-    const bool lower = m0.x < m1.x;
-    hit = lower ? ss_pair_sorted(v, g, c0, m0, c1, m1) : ss_pair_sorted(v, g, c1, m1, c0, m0);
-    if (hit) {
-      const uint32_t a = lower ? m0.x : m1.x, b = lower ? m1.x : m0.x;
-      e = make_uint2(a, b);
-      atomicAdd(&counts[a], 1ull);
-    }
-  }
-  append_pair(hit, e, tmp, tmp_n, cap);
-}
-
 // the exact predicate without the owner / family checks (done elsewhere)
 __device__ __forceinline__ bool ss_pair_sorted_nomask(const KtView &v, const Grid &g, const double4 &cl,
                                                       const uint4 &ml, const double4 &ch, const uint4 &mh) {
@@ -444,103 +437,10 @@ __device__ __forceinline__ bool ss_pair_sorted_nomask(const KtView &v, const Gri
   return bstar_in_ranges(g, ci, ri, float(cl.w), cj, rj, float(ch.w), v.margin);
 }
 
-// Sphere-sphere pairs among small spheres, one thread per cell-sorted sphere,
-// half stencil: the later spheres of its own cell plus the 13 forward
-// neighbour cells, so every unordered pair is evaluated exactly once.
-// A cheap conservative fp32 distance test runs per lane; survivors are
-// compacted (ballot) into a per-warp shared-memory queue and the exact fp64
-// reference predicate runs on full 32-lane batches.  Hits are counted into the
-// segment of the lower slot and appended to the scratch list (placed into
-// canonical segments by k_place / k_sort_seg).
-__global__ void __launch_bounds__(128) k_pairs_ss(KtView v, const double4 *sc, const uint4 *sm,
-                                                  const float4 *sf, unsigned long long *counts, uint2 *tmp,
-                                                  unsigned long long *tmp_n, unsigned long long cap) {
-  __shared__ uint2 queue[4][64];
-  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
-  uint2 *Q = queue[wq];
-  int qn = 0;  // warp-uniform queue length
-  int64_t u64 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  const Grid g = *v.grid;
-  bool active = u64 < v.sph.n && g.valid;
-  uint32_t key = active ? v.bin_key[u64] : kNoCell;
-  active = active && key != kNoCell;
-  float4 f0 = make_float4(0.f, 0.f, 0.f, 0.f);
-  long long cx = 0, cy = 0, cz = 0;
-  // conservative fp32 prefilter: coordinates are rounded relative to the grid
-  // origin, so |d_f32 - d| <= ~4 * 2^-24 * extent; the slack below is > 10x that
-  const float ext = float(double(max(g.nc[0], max(g.nc[1], g.nc[2]))) / g.inv_cell);
-  const float slack = 1e-6f * ext + 1e-30f;
-  const float marg = float(v.margin);
-  if (active) {
-    f0 = sf[u64];
-    cx = key % g.nc[0];
-    cy = (key / g.nc[0]) % g.nc[1];
-    cz = key / (g.nc[0] * g.nc[1]);
-  }
-  // spans: own cell after u, then rows (dz, dy) = (0,0) x+1 only, (0,1), (1,-1), (1,0), (1,1)
-  for (int span = 0; span < 6; ++span) {
-    uint32_t s0 = 0, s1 = 0;
-    if (active) {
-      if (span == 0) {
-        s0 = uint32_t(u64) + 1;
-        s1 = v.cell_end[key];
-      } else {
-        long long dz = span >= 3 ? 1 : 0;
-        long long dy = span == 2 ? 1 : (span >= 3 ? span - 4 : 0);
-        long long x0 = span == 1 ? cx + 1 : cx - 1, x1 = cx + 1;
-        long long y = cy + dy, z = cz + dz;
-        if (x0 < 0) x0 = 0;
-        if (x1 >= g.nc[0]) x1 = g.nc[0] - 1;
-        if (y >= 0 && y < g.nc[1] && z < g.nc[2] && x0 <= x1) {
-          long long row = (z * g.nc[1] + y) * g.nc[0];
-          uint32_t a0 = 0xFFFFFFFFu;
-          for (long long x = x0; x <= x1; ++x) {
-            uint32_t st = v.cell_start[row + x];
-            if (st == 0xFFFFFFFFu) continue;
-            if (a0 == 0xFFFFFFFFu) a0 = st;
-            s1 = v.cell_end[row + x];
-          }
-          s0 = a0 == 0xFFFFFFFFu ? 0 : a0;
-          if (a0 == 0xFFFFFFFFu) s1 = 0;
-        }
-      }
-    }
-    const uint32_t len = s1 > s0 ? s1 - s0 : 0;
-    uint32_t maxlen = len;
-    for (int off = 16; off > 0; off >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, off));
-    for (uint32_t t = 0; t < maxlen; ++t) {
-      bool pass = false;
-      const uint32_t w = s0 + t;
-      if (t < len) {
-        const float4 f1 = sf[w];
-        const float dx = f0.x - f1.x, dy = f0.y - f1.y, dz = f0.z - f1.z;
-        const float rr = f0.w + f1.w + marg + slack;
-        pass = dx * dx + dy * dy + dz * dz < rr * rr * 1.0001f;
-      }
-      const unsigned m = __ballot_sync(0xffffffffu, pass);
-      if (pass) Q[qn + __popc(m & ((1u << lane) - 1u))] = make_uint2(uint32_t(u64), w);
-      qn += __popc(m);
-      if (qn >= 32) {
-        __syncwarp();
-        const uint2 q = Q[lane];
-        __syncwarp();
-        if (lane < qn - 32) Q[lane] = Q[32 + lane];
-        qn -= 32;
-        __syncwarp();
-        ss_resolve(v, g, sc, sm, true, q, counts, tmp, tmp_n, cap);
-      }
-    }
-  }
-  __syncwarp();
-  if (qn > 0) {
-    const uint2 q = Q[lane < qn ? lane : 0];
-    ss_resolve(v, g, sc, sm, lane < qn, q, counts, tmp, tmp_n, cap);
-  }
-}
-
 // Sphere-triangle and sphere-analytic pairs, one thread per sphere slot.
 __global__ void __launch_bounds__(128) k_pairs_other(KtView v, unsigned long long *counts, uint2 *tmp,
-                                                     unsigned long long *tmp_n, unsigned long long cap) {
+                                                     unsigned long long *tmp_n, unsigned long long cap,
+                                                     int do_ana) {
   int64_t i64 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   const int64_t n = v.sph.n;
   const Grid g = *v.grid;
@@ -581,70 +481,63 @@ __global__ void __launch_bounds__(128) k_pairs_other(KtView v, unsigned long lon
           }
         }
   }
-  // analytic list: warp-uniform loop
-  for (int64_t k = 0; k < v.n_ana; ++k) {
+  // analytic list: warp-uniform loop (unless k_sa_filter takes the candidates)
+  for (int64_t k = 0; do_ana && k < v.n_ana; ++k) {
     bool hit = active && sa_pair(v, uint32_t(k), ci, ri_f, oi, fi);
     if (hit) ++csa;
     append_pair(hit, make_uint2(i, uint32_t(k) | (2u << kKindShift)), tmp, tmp_n, cap);
   }
   if (active) {
     counts[n + i64] = cst;
-    counts[2 * n + i64] = csa;
+    if (do_ana) counts[2 * n + i64] = csa;
   }
 }
 
-// One CTA per big sphere B (radius > r_cut): pairs with the small spheres of
-// the enumeration cells its reach covers, and with the bigs of higher slot.
-__global__ void __launch_bounds__(128) k_big(KtView v, const uint32_t *bigs, int64_t n_big,
-                                             const double4 *sc, const uint4 *sm,
-                                             unsigned long long *counts, uint2 *tmp,
-                                             unsigned long long *tmp_n, unsigned long long cap) {
-  const Grid g = *v.grid;
-  if (!g.valid) return;
-  for (int64_t bi = blockIdx.x; bi < n_big; bi += gridDim.x) {
-    const uint32_t B = bigs[bi];
-    const double4 cB = make_double4(v.centers[3 * size_t(B)], v.centers[3 * size_t(B) + 1],
-                                    v.centers[3 * size_t(B) + 2], double(v.sph.offr[B].w));
-    const uint4 mB = make_uint4(B, v.sph.owner[B], v.sfam[B], 0u);
-    const double reach = add(add(cB.w, g.r_cut), v.margin);
-    double cbv[3] = {cB.x, cB.y, cB.z};
-    long long flo[3], fhi[3];
-#pragma unroll
-    for (int ax = 0; ax < 3; ++ax) {
-      flo[ax] = axis_bin(sub_(cbv[ax], reach), g.glo[ax], g.inv_cell, g.nc[ax]);
-      fhi[ax] = axis_bin(add(cbv[ax], reach), g.glo[ax], g.inv_cell, g.nc[ax]);
-    }
-    const long long sx = fhi[0] - flo[0] + 1, sy = fhi[1] - flo[1] + 1, sz = fhi[2] - flo[2] + 1;
-    const long long ncell = sx * sy * sz;
-    for (long long q = threadIdx.x; q < ncell; q += blockDim.x) {
-      long long x = flo[0] + q % sx, y = flo[1] + (q / sx) % sy, z = flo[2] + q / (sx * sy);
-      long long b = (z * g.nc[1] + y) * g.nc[0] + x;
-      uint32_t s0 = v.cell_start[b];
-      if (s0 == 0xFFFFFFFFu) continue;
-      uint32_t s1 = v.cell_end[b];
-      for (uint32_t w = s0; w < s1; ++w) {
-        const double4 c1 = sc[w];
-        const uint4 m1 = sm[w];
-        const bool lower = m1.x < B;
-        if (!(lower ? ss_pair_sorted(v, g, c1, m1, cB, mB) : ss_pair_sorted(v, g, cB, mB, c1, m1))) continue;
-        uint32_t a = lower ? m1.x : B, c = lower ? B : m1.x;
-        atomicAdd(&counts[a], 1ull);
-        unsigned long long pos = atomicAdd(tmp_n, 1ull);
-        if (pos < cap) tmp[pos] = make_uint2(a, c);
-      }
-    }
-    for (int64_t q = threadIdx.x; q < n_big; q += blockDim.x) {
-      const uint32_t j = bigs[q];
-      if (j <= B) continue;
-      const double4 cj = make_double4(v.centers[3 * size_t(j)], v.centers[3 * size_t(j) + 1],
-                                      v.centers[3 * size_t(j) + 2], double(v.sph.offr[j].w));
-      const uint4 mj = make_uint4(j, v.sph.owner[j], v.sfam[j], 0u);
-      if (!ss_pair_sorted(v, g, cB, mB, cj, mj)) continue;
-      atomicAdd(&counts[B], 1ull);
-      unsigned long long pos = atomicAdd(tmp_n, 1ull);
-      if (pos < cap) tmp[pos] = make_uint2(B, j);
-    }
+// Sphere-analytic candidates, built with the sphere-sphere lists while no
+// mesh / analytic owner moves: analytic k is a candidate of sphere i if its
+// gap is below r_i + margin + skin at the rebuild.  Gaps to planes and
+// cylinders are 1-Lipschitz in the centre, so a sphere that moved at most
+// skin / 2 since (k_disp) can only pass the exact test with a candidate.
+// Families / masks are not applied (they may change); clump-mates and the
+// decomposition rule are.
+__device__ __forceinline__ bool sa_candidate(const KtView &v, uint32_t i, uint32_t k, double reach) {
+  const uint32_t oi = v.sph.owner[i];
+  if (oi == v.ana_owner[k] || !dd_keep(v.own.dd, oi, v.ana_owner[k])) return false;
+  double gap, bx, by, bz, rb;
+  analytic_gap(v.ana_kind[k], v.ana_world + 8 * size_t(k), v.centers[3 * size_t(i)], v.centers[3 * size_t(i) + 1],
+               v.centers[3 * size_t(i) + 2], gap, bx, by, bz, rb);
+  return gap < double(v.sph.offr[i].w) + reach;
+}
+
+__global__ void k_sa_count(KtView v, double reach, uint32_t *cnt) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= v.sph.n) return;
+  uint32_t c = 0;
+  for (int64_t k = 0; k < v.n_ana; ++k) c += sa_candidate(v, uint32_t(i), uint32_t(k), reach) ? 1u : 0u;
+  cnt[i] = c;
+}
+
+__global__ void k_sa_fill(KtView v, double reach, const unsigned long long *off, uint2 *cand) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= v.sph.n) return;
+  unsigned long long w = off[i];
+  for (int64_t k = 0; k < v.n_ana; ++k)
+    if (sa_candidate(v, uint32_t(i), uint32_t(k), reach)) cand[w++] = make_uint2(uint32_t(i), uint32_t(k));
+}
+
+// exact sphere-analytic predicate (_kernels.py:418-428) on the candidates
+__global__ void k_sa_filter(KtView v, const uint2 *cand, int64_t n_cand, unsigned long long *counts, uint2 *tmp,
+                            unsigned long long *tmp_n, unsigned long long cap) {
+  const int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  bool hit = false;
+  uint2 p = make_uint2(0u, 0u);
+  if (e < n_cand && v.grid->valid) {
+    p = cand[e];
+    const double ci[3] = {v.centers[3 * size_t(p.x)], v.centers[3 * size_t(p.x) + 1], v.centers[3 * size_t(p.x) + 2]};
+    hit = sa_pair(v, p.y, ci, v.sph.offr[p.x].w, v.sph.owner[p.x], v.sfam[p.x]);
+    if (hit) atomicAdd(&counts[2 * v.sph.n + p.x], 1ull);
   }
+  append_pair(hit, make_uint2(p.x, p.y | (2u << kKindShift)), tmp, tmp_n, cap);
 }
 
 // scatter the scratch list into per-(kind, sphere) segments
@@ -1115,7 +1008,7 @@ __global__ void k_inc_start(int64_t n_owner, int64_t n_inc, const uint32_t *sort
 // host entry points
 // ===========================================================================
 
-int kt_snapshot(Ctx *c, cudaStream_t s) {
+int kt_snapshot(Ctx *c, cudaStream_t s, double margin) {
   KtScratch &k = c->kt;
   if (ensure(c, k.centers, sizeof(double) * 3 * (c->n_sph + 1), s) ||
       ensure(c, k.c4, sizeof(double4) * (c->n_sph + 1), s))
@@ -1125,10 +1018,26 @@ int kt_snapshot(Ctx *c, cudaStream_t s) {
   if (ensure(c, k.ana_world, sizeof(double) * 8 * (c->n_ana + 1), s)) return -1;
   if (ensure(c, k.tfam, c->n_tri + 1, s)) return -1;
   if (ensure(c, k.afam, c->n_ana + 1, s)) return -1;
+  if (ensure(c, k.minmax, sizeof(unsigned long long) * 8, s) || ensure(c, k.flag, 16, s)) return -1;
+  // a detection snapshot (margin >= 0) also reduces the grid inputs and runs
+  // the candidate displacement check (kt_begin then skips both)
+  static const bool fuse_off = std::getenv("GF_NO_SNAP_FUSE") != nullptr;
+  const bool det = margin >= 0.0 && !fuse_off;
+  unsigned long long *mm = k.minmax.as<unsigned long long>();
+  bool check = false;
+  if (det) {
+    if (k.cand_valid && c->skin_factor * margin != k.cand_skin) k.cand_valid = false;
+    check = k.cand_valid && c->n_sph;
+    k_minmax_init<<<1, 32, 0, s>>>(mm);
+    if (check) GF_CHECK(c, cudaMemsetAsync(k.flag.p, 0, sizeof(int), s));
+  }
+  const double skin = c->skin_factor * margin;
   if (c->n_sph)
-    k_snapshot<<<grid_for(c->n_sph), kBlock, 0, s>>>(c->dom, owners_view(c), spheres_view(c),
-                                                   k.centers.as<double>(), k.c4.as<double4>(),
-                                                   k.sfam.as<uint8_t>());
+    k_snapshot<<<unsigned(std::min<int64_t>(grid_for(c->n_sph), 148 * 8)), kBlock, 0, s>>>(
+        c->dom, owners_view(c), spheres_view(c), k.centers.as<double>(), k.c4.as<double4>(), k.sfam.as<uint8_t>(),
+        det ? mm : nullptr, check ? k.ref.as<double>() : nullptr, 0.25 * skin * skin, k.flag.as<int>());
+  k.snap_det = det;
+  k.snap_checked = check;
   if (c->n_tri) {
     GF_CHECK(c, cudaMemcpyAsync(k.tri_world.p, c->tri_world.p, sizeof(double) * 9 * c->n_tri,
                                 cudaMemcpyDeviceToDevice, s));
@@ -1192,16 +1101,22 @@ int kt_begin(Ctx *c, double margin, cudaStream_t s) {
       ensure(c, k.flag, 16, s))
     return -1;
   unsigned long long *mm = k.minmax.as<unsigned long long>();
-  k_minmax_init<<<1, 32, 0, s>>>(mm);
-  if (n) k_minmax<<<std::min<int64_t>(grid_for(n), 1184), kBlock, 0, s>>>(n, k.centers.as<double>(), n, c->sph_offr.as<float4>(), mm);
+  const bool snap = k.snap_det;   // the snapshot reduced the sphere centres already
+  k.snap_det = false;
+  if (!snap) {
+    k_minmax_init<<<1, 32, 0, s>>>(mm);
+    if (n) k_minmax<<<std::min<int64_t>(grid_for(n), 1184), kBlock, 0, s>>>(n, k.centers.as<double>(), n, c->sph_offr.as<float4>(), mm);
+  }
   if (nt) k_minmax<<<std::min<int64_t>(grid_for(3 * nt), 1184), kBlock, 0, s>>>(3 * nt, k.tri_world.as<double>(), 0, nullptr, mm);
   k_grid<<<1, 1, 0, s>>>(mm, n_pts, margin, c->kt_bin_size, c->r_cut, (long long)kMaxCells, margin + skin,
                          k.grid.as<Grid>());
   const Grid *gp = k.grid.as<Grid>();
   int *flag = k.flag.as<int>();
   if (k.cand_valid && n) {
-    GF_CHECK(c, cudaMemsetAsync(flag, 0, sizeof(int), s));
-    k_disp<<<grid_for(n), kBlock, 0, s>>>(n, k.centers.as<double>(), k.ref.as<double>(), 0.25 * skin * skin, flag);
+    if (!(snap && k.snap_checked)) {
+      GF_CHECK(c, cudaMemsetAsync(flag, 0, sizeof(int), s));
+      k_disp<<<grid_for(n), kBlock, 0, s>>>(n, k.centers.as<double>(), k.ref.as<double>(), 0.25 * skin * skin, flag);
+    }
   } else {
     k_set_int<<<1, 1, 0, s>>>(flag, 1);
   }
@@ -1252,7 +1167,7 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
       ensure(c, k.cell_end, sizeof(uint32_t) * (kMaxCells + 1), s))
     return -1;
   if (k.cand_cap == 0) {
-    int64_t cap = std::max<int64_t>(10 * n, 4096);   // grown on overflow below
+    int64_t cap = std::max<int64_t>(6 * n, 4096);   // grown to the exact need on overflow below
     if (ensure(c, k.cand_tmp, sizeof(uint2) * cap, s) || ensure(c, k.cand, sizeof(uint2) * cap, s)) return -1;
     k.cand_cap = cap;
   }
@@ -1301,7 +1216,7 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
   GF_CHECK(c, cudaStreamSynchronize(s));
   const int64_t total = int64_t(reinterpret_cast<Status *>(c->h_status)->cand_total);
   if (total > k.cand_cap) {
-    int64_t cap = total + total / 4 + 4096;
+    int64_t cap = total + total / 10 + 4096;
     if (ensure(c, k.cand_tmp, sizeof(uint2) * cap, s) || ensure(c, k.cand, sizeof(uint2) * cap, s)) return -1;
     k.cand_cap = cap;
     return rebuild_candidates(c, s);
@@ -1314,6 +1229,25 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
                                       (unsigned long long)k.cand_cap);
     k_sort_seg<<<grid_for(n), kBlock, 0, s>>>(n, k.cand_seg.as<unsigned long long>(), k.cand.as<uint2>());
     k_copy_ref<<<grid_for(3 * n), kBlock, 0, s>>>(3 * n, k.centers.as<double>(), k.ref.as<double>());
+  }
+  // sphere-analytic candidates for the same skin, while the world is static
+  k.sa_world_version = ~0ull;
+  if (n && c->n_ana && !c->world_moving) {
+    if (ensure(c, k.sa_cnt, 4 * (n + 1), s) || ensure(c, k.sa_off, 8 * (n + 1), s)) return -1;
+    k_sa_count<<<grid_for(n), kBlock, 0, s>>>(v, reach, k.sa_cnt.as<uint32_t>());
+    GF_CHECK(c, cudaMemsetAsync(k.sa_cnt.as<uint32_t>() + n, 0, 4, s));
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, k.sa_cnt.as<uint32_t>(), k.sa_off.as<unsigned long long>(), int(n + 1), s);
+    if (ensure(c, k.cub_tmp, tb + 16, s, false)) return -1;
+    GF_CHECK(c, cub::DeviceScan::ExclusiveSum(k.cub_tmp.p, tb, k.sa_cnt.as<uint32_t>(),
+                                              k.sa_off.as<unsigned long long>(), int(n + 1), s));
+    unsigned long long h_tot = 0;
+    GF_CHECK(c, cudaMemcpyAsync(&h_tot, k.sa_off.as<unsigned long long>() + n, 8, cudaMemcpyDeviceToHost, s));
+    GF_CHECK(c, cudaStreamSynchronize(s));
+    k.n_sa_cand = int64_t(h_tot);
+    if (ensure(c, k.sa_cand, sizeof(uint2) * (k.n_sa_cand + 1), s)) return -1;
+    k_sa_fill<<<grid_for(n), kBlock, 0, s>>>(v, reach, k.sa_off.as<unsigned long long>(), k.sa_cand.as<uint2>());
+    k.sa_world_version = c->world_version;
   }
   k.cand_valid = true;
   k.cand_skin = c->skin_factor * c->kt_margin;
@@ -1337,8 +1271,8 @@ int kt_count(Ctx *c, cudaStream_t s, bool force_rebuild) {
   }
   if (ensure(c, k.counts, sizeof(unsigned long long) * (3 * n + 1), s) || ensure(c, k.tmp_n, 16, s))
     return -1;
-  if (k.tmp_cap == 0) {
-    int64_t cap = std::max<int64_t>(n, 4096);
+  if (k.tmp_cap == 0) {   // wall pairs: a few per boundary sphere; grown on overflow
+    int64_t cap = std::max<int64_t>(n / 16, 4096);
     if (ensure(c, k.tmp, sizeof(uint2) * cap, s)) return -1;
     k.tmp_cap = cap;
   }
@@ -1350,7 +1284,7 @@ int kt_count(Ctx *c, cudaStream_t s, bool force_rebuild) {
   const int64_t ss_guess = k.last_ss > 0 ? k.last_ss + k.last_ss / 8 + 1024 : (3 * k.n_cand) / 4 + 1024;
   const int64_t need = std::min<int64_t>(k.n_cand, std::max<int64_t>(ss_guess, k.ss_need)) + k.tmp_cap + 1;
   if (need > out.cap) {
-    int64_t cap = need + need / 4 + 1024;
+    int64_t cap = need + need / 32 + 1024;
     if (ensure(c, out.ids, sizeof(uint2) * cap, s) || ensure(c, out.wild, sizeof(float) * c->wild_w * cap, s) ||
         ensure(c, out.old_pos, sizeof(uint32_t) * cap, s))
       return -1;
@@ -1398,8 +1332,20 @@ int kt_count(Ctx *c, cudaStream_t s, bool force_rebuild) {
   k.cslot_gen[cur] = k.cand_gen;
   k.cslot_cur ^= 1;
   // sphere-triangle / sphere-analytic pairs: per-sphere counts of kinds 1, 2
-  if (n) {
-    k_pairs_other<<<grid_for(n, 128), 128, 0, s>>>(v, cnt, k.tmp.as<uint2>(), tn, (unsigned long long)k.tmp_cap);
+  static const bool sa_off = std::getenv("GF_NO_SA_CAND") != nullptr;
+  const bool sa_cands = !sa_off && c->n_ana && !c->world_moving && k.sa_world_version == c->world_version;
+  if (n && sa_cands) {
+    // sphere-analytic pairs from the candidates; triangles (if any) as usual
+    GF_CHECK(c, cudaMemsetAsync(cnt + 2 * n, 0, sizeof(unsigned long long) * n, s));
+    if (c->n_tri)
+      k_pairs_other<<<grid_for(n, 128), 128, 0, s>>>(v, cnt, k.tmp.as<uint2>(), tn, (unsigned long long)k.tmp_cap, 0);
+    else
+      GF_CHECK(c, cudaMemsetAsync(cnt + n, 0, sizeof(unsigned long long) * n, s));
+    if (k.n_sa_cand)
+      k_sa_filter<<<grid_for(k.n_sa_cand), kBlock, 0, s>>>(v, k.sa_cand.as<uint2>(), k.n_sa_cand, cnt,
+                                                           k.tmp.as<uint2>(), tn, (unsigned long long)k.tmp_cap);
+  } else if (n) {
+    k_pairs_other<<<grid_for(n, 128), 128, 0, s>>>(v, cnt, k.tmp.as<uint2>(), tn, (unsigned long long)k.tmp_cap, 1);
   }
   // their segment starts follow the sphere-sphere block: exclusive scan of
   // counts[n, 3n] seeded with the block's size
