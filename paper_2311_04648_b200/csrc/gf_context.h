@@ -15,6 +15,11 @@ struct DBuf {
   void *p = nullptr;
   size_t bytes = 0;
   template <class T> T *as() const { return reinterpret_cast<T *>(p); }
+  void release() {   // callers synchronise first
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
 };
 
 // Active contact set in device layout.  ids.x = sphere slot of A;

@@ -1168,9 +1168,10 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
     return -1;
   if (k.cand_cap == 0) {
     int64_t cap = std::max<int64_t>(6 * n, 4096);   // grown to the exact need on overflow below
-    if (ensure(c, k.cand_tmp, sizeof(uint2) * cap, s) || ensure(c, k.cand, sizeof(uint2) * cap, s)) return -1;
+    if (ensure(c, k.cand, sizeof(uint2) * cap, s)) return -1;
     k.cand_cap = cap;
   }
+  if (ensure(c, k.cand_tmp, sizeof(uint2) * k.cand_cap, s)) return -1;   // released after big rebuilds
   const Grid *gp = k.grid.as<Grid>();
   KtView v = kt_view(c, c->kt_margin);
   unsigned long long *cc = k.cand_cnt.as<unsigned long long>();
@@ -1248,6 +1249,15 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
     if (ensure(c, k.sa_cand, sizeof(uint2) * (k.n_sa_cand + 1), s)) return -1;
     k_sa_fill<<<grid_for(n), kBlock, 0, s>>>(v, reach, k.sa_off.as<unsigned long long>(), k.sa_cand.as<uint2>());
     k.sa_world_version = c->world_version;
+  }
+  // at 2^24 spheres and up device memory is the limit: the rebuild-only
+  // scratch (sort keys, cell-sorted copies, candidate counts and staging,
+  // ~170 B / sphere) is released and reallocated at the next rebuild
+  if (n >= (int64_t(1) << 24)) {
+    GF_CHECK(c, cudaStreamSynchronize(s));
+    for (DBuf *b : {&k.bin_key, &k.bin_key_alt, &k.sph_val, &k.sph_val_alt, &k.sc, &k.sm, &k.sf, &k.cand_cnt,
+                    &k.cand_seg, &k.cand_tmp})
+      b->release();
   }
   k.cand_valid = true;
   k.cand_skin = c->skin_factor * c->kt_margin;
