@@ -9,6 +9,15 @@
 
 namespace gf {
 
+// Programmatic dependent launch (sm_90+): a kernel launched with the
+// programmatic-serialization attribute may start while its predecessor in the
+// stream drains.  pdl_wait() blocks until the predecessor grid has completed
+// and its writes are visible; pdl_launch() (called only after pdl_wait(), so
+// every earlier grid is complete too) lets the successor start its prologue.
+// Both are no-ops for a normal launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 template <typename VelT> struct Vel;
 template <> struct Vel<double> {
   static __device__ __forceinline__ void load(const void *p, int64_t i, double v[3]) {

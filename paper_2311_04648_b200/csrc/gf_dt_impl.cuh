@@ -81,6 +81,8 @@ __global__ void __launch_bounds__(256, 4) k_touch(DtView v, uint32_t *tlist, uin
                                                   unsigned long long *tlist_n, unsigned long long step,
                                                   const unsigned long long *k0p) {
   __shared__ int s_live;
+  pdl_wait();
+  pdl_launch();
   if (threadIdx.x == 0) s_live = !v.st->err && v.st->dd_trip >= step;
   __syncthreads();
   if (!s_live) return;
@@ -157,6 +159,8 @@ template <typename VelT>
 __global__ void __launch_bounds__(128) k_forces(DtView v, double ts, double sim_time, const uint32_t *list0,
                                                 const uint32_t *list1, const unsigned long long *counts,
                                                 int skip0) {
+  pdl_wait();
+  pdl_launch();
   if (v.st->err) return;
   const unsigned long long n0 = skip0 ? 0ull : counts[0], n = n0 + counts[1];
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
@@ -377,8 +381,10 @@ static __global__ void __launch_bounds__(256, kMinBlocks) k_contacts_ss(DtView v
   __shared__ uint32_t q_a[kSsWarps][kSsQueue], q_b[kSsWarps][kSsQueue], q_k[kSsWarps][kSsQueue];
   __shared__ float q_g[7][kSsWarps][kSsQueue];
   __shared__ int s_live;
+  const bool smem = stage_materials(v, s_mat);   // static tables: before the predecessor drains
+  pdl_wait();
+  pdl_launch();
   if (threadIdx.x == 0) s_live = !v.st->err && v.st->dd_trip >= step;
-  const bool smem = stage_materials(v, s_mat);
   __syncthreads();
   if (!s_live) return;
   const float ts = float(ts_d);
@@ -576,6 +582,8 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_integrate(DtView v, double 
   double2 sc = make_double2(0.0, 0.0);
   // the fp32-velocity build always reduces into the fixed-point accumulators
   // (Ctx::fixed_reduce == f32_state); the fp64 build always by incidence lists
+  pdl_wait();   // owner state above is the previous step's; the accumulators are this step's
+  pdl_launch();
   if (std::is_same<VelT, float>::value) {
     longlong2 *fp = reinterpret_cast<longlong2 *>(v.own.facc + 6 * size_t(o));
     const longlong2 a0 = fp[0], a1 = fp[1], a2 = fp[2];
@@ -766,6 +774,39 @@ __global__ void k_world(Domain dom, Owners own, Tris tri, Anas ana) {
 
 }  // namespace
 
+namespace {
+// per-step counters (a kernel rather than memsets, so the chain of
+// programmatically-serialised launches is not broken)
+__global__ void k_step_begin(Status *st, unsigned long long *tn) {
+  pdl_wait();
+  pdl_launch();
+  if (threadIdx.x == 0) {
+    st->touching = 0;
+    if (tn) { tn[0] = 0; tn[1] = 0; }
+  }
+}
+
+// launch with programmatic stream serialisation (Ctx::pdl) or plainly
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(const Ctx *c, void (*kern)(KArgs...), dim3 g, dim3 b, cudaStream_t s, Args... args) {
+  if (!c->pdl) {
+    kern<<<g, b, 0, s>>>(args...);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = g;
+  cfg.blockDim = b;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+}  // namespace
+
 template <typename VelT>
 static DtView dt_view(Ctx *c) {
   DtView v;
@@ -801,7 +842,8 @@ template <typename VelT>
 int dt_forces_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
   DtView v = dt_view<VelT>(c);
   v.acc_all = a.write_acc;
-  GF_CHECK(c, cudaMemsetAsync(&v.st->touching, 0, sizeof(unsigned long long), s));
+  GF_CHECK(c, launch_k(c, k_step_begin, dim3(1), dim3(32), s, v.st,
+                       v.n_acs ? c->tlist_n.as<unsigned long long>() : (unsigned long long *)nullptr));
   cudaEvent_t *ev = prof_events(c);
   if (ev) cudaEventRecord(ev[0], s);
   bool ss_timed = false;   // ev[4] recorded after the fused sphere-sphere kernel
@@ -815,7 +857,6 @@ int dt_forces_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
     }
     // list0: sphere-sphere entries (uint4 records in the fused build), list1: the other kinds
     uint32_t *list0 = c->tlist.as<uint32_t>(), *list1 = list0 + (c->tlist_words == 5 ? 4 * c->tlist_cap : 0);
-    GF_CHECK(c, cudaMemsetAsync(tn, 0, 2 * sizeof(unsigned long long), s));
     // throughput build + built-in model: sphere-sphere contacts take the fp32
     // path (k_forces_f32), the wall kinds the generic k_forces
     const bool fused = std::is_same<VelT, float>::value && c->wild_w == 4 && !c->user_model && v.sph.kin;
@@ -829,15 +870,17 @@ int dt_forces_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
     } else if (fused) {
       // the sphere-sphere block in one fused pass, then the wall kinds'
       // narrow phase (feeds k_forces below)
+      const unsigned long long step = (unsigned long long)a.step;
       if (c->ss_split == 2)
-        k_contacts_ss<1, 4><<<148 * 4, 256, 0, s>>>(v, a.h, (unsigned long long)a.step);
+        GF_CHECK(c, launch_k(c, k_contacts_ss<1, 4>, dim3(148 * 4), dim3(256), s, v, a.h, step));
       else if (c->ss_split == 3)
-        k_contacts_ss<2, 4><<<148 * 4, 256, 0, s>>>(v, a.h, (unsigned long long)a.step);
+        GF_CHECK(c, launch_k(c, k_contacts_ss<2, 4>, dim3(148 * 4), dim3(256), s, v, a.h, step));
       else
-        k_contacts_ss<2, 3><<<148 * 3, 256, 0, s>>>(v, a.h, (unsigned long long)a.step);
+        GF_CHECK(c, launch_k(c, k_contacts_ss<2, 3>, dim3(148 * 3), dim3(256), s, v, a.h, step));
       if (ev) cudaEventRecord(ev[4], s);
       ss_timed = true;
-      k_touch<<<148 * 4, 256, 0, s>>>(v, list0, list1, tn, (unsigned long long)a.step, v.seg + c->n_sph);
+      GF_CHECK(c, launch_k(c, k_touch, dim3(148 * 4), dim3(256), s, v, list0, list1, tn, step,
+                           (const unsigned long long *)(v.seg + c->n_sph)));
     } else {
       k_touch<<<unsigned(std::min<int64_t>((v.n_acs + 255) / 256, 148 * 16)), 256, 0, s>>>(
           v, list0, list1, tn, (unsigned long long)a.step, nullptr);
@@ -845,7 +888,9 @@ int dt_forces_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
     if (c->user_model) {
       if (launch_user_forces(c, v, a.h, a.sim_time, s)) return -1;
     } else {
-      k_forces<VelT><<<148 * 8, 128, 0, s>>>(v, a.h, a.sim_time, list0, list1, tn, fused ? 1 : 0);
+      GF_CHECK(c, launch_k(c, k_forces<VelT>, dim3(148 * 8), dim3(128), s, v, a.h, a.sim_time,
+                           (const uint32_t *)list0, (const uint32_t *)list1, (const unsigned long long *)tn,
+                           fused ? 1 : 0));
     }
   }
   if (ev) {
@@ -871,8 +916,8 @@ int dt_integrate_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
   if (c->n_owner) {
     unsigned g = unsigned((c->n_owner + 127) / 128);
     // 8 CTAs / SM (64 registers, a few spills) beats 6 at 91 registers
-    k_integrate<VelT, 8><<<g, 128, 0, s>>>(v, a.h, a.g[0], a.g[1], a.g[2], a.v_err,
-                                          (unsigned long long)a.step, a.write_acc);
+    GF_CHECK(c, launch_k(c, k_integrate<VelT, 8>, dim3(g), dim3(128), s, v, a.h, a.g[0], a.g[1], a.g[2],
+                         a.v_err, (unsigned long long)a.step, a.write_acc));
   }
   if (ev) cudaEventRecord(ev[3], s);
   if ((c->n_tri || c->n_ana) && c->world_moving) {

@@ -15,6 +15,9 @@ crater_bed  configs[1]: projectile impact onto an n-sphere polydisperse bed.
             (the reference's 1e-4 s / 30 m/s give a 24 mm detection margin,
             i.e. thousands of candidate pairs per grain).
 settling_box configs[0]: monodisperse r = 5 mm spheres in a walled box.
+clump_bed   configs[2]'s clump path: 5-sphere cylinder clumps (the reference's
+            WC clump, scenarios.py:386-407: r = 2 mm, L = 8.5 mm, rho = 476)
+            settling in a box, random orientations.
 tiled_bed   configs[4]'s size sweep: tx x ty copies of a settled crater bed
             side by side in one box (same grains, same step), so the sphere
             count grows at fixed grain size.
@@ -35,7 +38,8 @@ G = 9.81
 def crater_bed(n_spheres: int = 1_000_000, *, seed: int = 7, h: float = 1e-5, v_err: float = 5.0,
                n_max: int = 4, precision: str = "f32", device: int = 0, ball: bool = True,
                drop_height: float = 0.20, ball_density: float = 7800.0, decomposition=None,
-               tiles: int = 1, hold_ball: bool = False) -> Simulator:
+               tiles: int = 1, hold_ball: bool = False, force_model: str = "hertz_mindlin",
+               extra_props: dict | None = None) -> Simulator:
     rng = np.random.default_rng(seed)
     D = 0.0254
     bed_half = 12.0 * D / 2.0
@@ -52,9 +56,9 @@ def crater_bed(n_spheres: int = 1_000_000, *, seed: int = 7, h: float = 1e-5, v_
     r_max = float(radii.max())
     dom = Domain((-half_x - 0.2 * bed_half, -bed_half * 1.2, -0.02),
                  (half_x + 0.2 * bed_half, bed_half * 1.2, depth * 3.0 + 0.3))
-    sim = Simulator(dom, precision=precision, device=device, decomposition=decomposition)
-    grain = sim.load_material(dict(CRATER_MATERIAL))
-    wall = sim.load_material(dict(CRATER_MATERIAL))
+    sim = Simulator(dom, force_model, precision=precision, device=device, decomposition=decomposition)
+    grain = sim.load_material({**CRATER_MATERIAL, **(extra_props or {})})
+    wall = sim.load_material({**CRATER_MATERIAL, **(extra_props or {})})
     tpls = [sim.load_clump_template(ClumpTemplate.solid_sphere(
         float(r), 2500.0 * 4.0 / 3.0 * math.pi * float(r) ** 3, grain)) for r in radii]
     # lattice pitch d_max: the largest grains touch, nobody overlaps
@@ -154,6 +158,51 @@ def tiled_bed(src: Simulator, tx: int, ty: int, *, precision: str = "f32", devic
     sim.set_error_out_velocity(src.v_err)
     sim.set_fixed_lookahead(n_max)
     del grain
+    return sim
+
+
+def clump_bed(n_clumps: int = 1_000_000, *, seed: int = 11, h: float = 1e-5, v_err: float = 5.0,
+              n_max: int = 4, precision: str = "f32", device: int = 0) -> Simulator:
+    """configs[2]: n five-sphere cylinder clumps (r = 2 mm, L = 8.5 mm,
+    rho = 476; the reference's WC clump, scenarios.py:386-407) on a cubic
+    lattice with random orientations in a walled box, crater materials."""
+    from .core import ClumpSphere
+    rng = np.random.default_rng(seed)
+    r, L, rho = 0.002, 0.0085, 476.0
+    m = rho * math.pi * r * r * L
+    i_ax = 0.5 * m * r * r
+    i_pe = m * (3 * r * r + L * L) / 12.0
+    pitch = L * 1.02
+    per_side = int(math.ceil((n_clumps * 2.0) ** (1.0 / 3.0)))     # footprint side; ~half as many layers
+    half = per_side * pitch / 2.0
+    layers = int(math.ceil(n_clumps / per_side ** 2)) + 1
+    top = layers * pitch + pitch
+    dom = Domain((-half - 0.05, -half - 0.05, -0.02), (half + 0.05, half + 0.05, top + 0.1))
+    sim = Simulator(dom, precision=precision, device=device)
+    mat = sim.load_material(dict(CRATER_MATERIAL))
+    offs = np.linspace(-(L / 2 - r), L / 2 - r, 5)
+    tpl = sim.load_clump_template(ClumpTemplate(
+        m, np.array([i_ax, i_pe, i_pe]),
+        tuple(ClumpSphere(np.array([x, 0.0, 0.0]), r, mat) for x in offs)))
+    g = (np.arange(per_side) + 0.5) * pitch - half
+    gx, gy = np.meshgrid(g, g, indexing="ij")
+    pts = []
+    for k in range(layers):
+        pts.append(np.stack([gx.ravel(), gy.ravel(), np.full(gx.size, (k + 1) * pitch)], -1))
+    pts = np.concatenate(pts)[:n_clumps]
+    ids = np.asarray(sim.add_clumps(tpl, pts), dtype=np.int64)
+    q = rng.normal(size=(ids.size, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    sim.store.__dict__["_quat"][ids] = q
+    walls = [("plane", (0, 0, 0), (0, 0, 1), mat),
+             ("plane", (-half, 0, 0), (1, 0, 0), mat), ("plane", (half, 0, 0), (-1, 0, 0), mat),
+             ("plane", (0, -half, 0), (0, 1, 0), mat), ("plane", (0, half, 0), (0, -1, 0), mat)]
+    sim.add_analytic(walls, family=255)
+    sim.set_family_fixed(255)
+    sim.set_gravity([0, 0, -G])
+    sim.set_init_time_step(h)
+    sim.set_error_out_velocity(v_err)
+    sim.set_fixed_lookahead(n_max)
     return sim
 
 
