@@ -240,6 +240,8 @@ def b200_arm(args):
     # warm-up (untimed)
     sim.do_dynamics(args.warmup * h)
     ctx = sim._ctx
+    if os.environ.get("GF_BENCH_PROF_IN_TIMED"):   # diagnostics: per-kernel events inside the timed steps
+        ctx.call("gf_set_profiling", C.c_int(1))
 
     def barrier():
         if dist is not None:
@@ -259,6 +261,10 @@ def b200_arm(args):
         if prof_range:
             torch.cuda.profiler.stop()
     rr = sim.last_run
+    # device time of the timed steps: CUDA events on the dT stream around
+    # every gf_run segment (one segment unless a repartition split the call)
+    dt_ms = (sim.scheduler.timing["dyn_force"] - dev0) * 1e3
+    repartitions = getattr(sim.scheduler, "repartitions", 0) - reps0
     # per-kernel CUDA events would sit between the kernels of the chain (and
     # break its programmatic dependent launches): the kernel times come from a
     # separate profiled window right after the timed one
@@ -271,10 +277,6 @@ def b200_arm(args):
     times = np.zeros(6)
     ctx.call("gf_kernel_times", _lib.ptr(times))
     ctx.call("gf_set_profiling", C.c_int(0))
-    # device time of the timed steps: CUDA events on the dT stream around
-    # every gf_run segment (one segment unless a repartition split the call)
-    dt_ms = (sim.scheduler.timing["dyn_force"] - dev0) * 1e3
-    repartitions = getattr(sim.scheduler, "repartitions", 0) - reps0
     if dist is not None:
         t = torch.tensor([dt_ms], device=f"cuda:{device}", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

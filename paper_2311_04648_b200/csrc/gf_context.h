@@ -154,8 +154,10 @@ struct Ctx {
   double skin_factor = 1.0;  // Verlet skin = skin_factor * margin
   uint64_t world_version = 0;   // bumped whenever mesh / analytic world transforms are recomputed
   int tlist_words = 5;       // words per contact of the touching lists (1 on the fused path)
-  int ss_split = 0;
-  int pdl = 1;               // programmatic dependent launch on the dT chain (GF_PDL=0 disables)          // throughput build: split narrow/force sphere-sphere kernels (GF_SS_SPLIT=1)
+  int ss_split = 0;          // throughput build: split narrow/force sphere-sphere kernels (GF_SS_SPLIT=1)
+  // programmatic dependent launch on the dT chain (GF_PDL=1): measured slower
+  // on the bench bed (the chain's kernels already fill the GPU), off by default
+  int pdl = 0;
   // schedule state (kept across gf_run calls)
   bool first_adopt = true;     // the first do_dynamics detects and waits (engine.py:679-682)
   bool fill_done = false;

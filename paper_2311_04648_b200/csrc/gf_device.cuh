@@ -15,8 +15,13 @@ namespace gf {
 // and its writes are visible; pdl_launch() (called only after pdl_wait(), so
 // every earlier grid is complete too) lets the successor start its prologue.
 // Both are no-ops for a normal launch.
+#ifndef GF_NO_PDL_ASM
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#else
+__device__ __forceinline__ void pdl_wait() {}
+__device__ __forceinline__ void pdl_launch() {}
+#endif
 
 template <typename VelT> struct Vel;
 template <> struct Vel<double> {

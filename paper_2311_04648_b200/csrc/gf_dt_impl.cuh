@@ -842,8 +842,13 @@ template <typename VelT>
 int dt_forces_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
   DtView v = dt_view<VelT>(c);
   v.acc_all = a.write_acc;
-  GF_CHECK(c, launch_k(c, k_step_begin, dim3(1), dim3(32), s, v.st,
-                       v.n_acs ? c->tlist_n.as<unsigned long long>() : (unsigned long long *)nullptr));
+  if (c->pdl) {
+    GF_CHECK(c, launch_k(c, k_step_begin, dim3(1), dim3(32), s, v.st,
+                         v.n_acs ? c->tlist_n.as<unsigned long long>() : (unsigned long long *)nullptr));
+  } else {
+    GF_CHECK(c, cudaMemsetAsync(&v.st->touching, 0, sizeof(unsigned long long), s));
+    if (v.n_acs) GF_CHECK(c, cudaMemsetAsync(c->tlist_n.p, 0, 2 * sizeof(unsigned long long), s));
+  }
   cudaEvent_t *ev = prof_events(c);
   if (ev) cudaEventRecord(ev[0], s);
   bool ss_timed = false;   // ev[4] recorded after the fused sphere-sphere kernel
