@@ -253,6 +253,8 @@ def b200_arm(args):
     reps0 = getattr(sim.scheduler, "repartitions", 0)
     dev0 = sim.scheduler.timing["dyn_force"]
     prof_range = bool(os.environ.get("GF_PROFILE_TIMED"))   # ncu --profile-from-start off
+    if os.environ.get("GF_BENCH_KT_FREEZE"):   # diagnostics: the dT chain alone (no detections in the timed steps)
+        os.environ["GF_KT_FREEZE"] = "1"
     with ClockSampler(device) as clocks:
         if prof_range:
             torch.cuda.profiler.start()
@@ -260,6 +262,7 @@ def b200_arm(args):
         barrier()
         if prof_range:
             torch.cuda.profiler.stop()
+    os.environ.pop("GF_KT_FREEZE", None)
     rr = sim.last_run
     # device time of the timed steps: CUDA events on the dT stream around
     # every gf_run segment (one segment unless a repartition split the call)

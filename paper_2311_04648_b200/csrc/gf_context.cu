@@ -1,3 +1,4 @@
+#include <cstdio>
 // gf_context.cu -- C-ABI (include/gf_b200.h): context, scene upload/download,
 // per-kernel entry points and the kT/dT worker protocol (gf_run).
 //
@@ -188,7 +189,22 @@ struct RunState {
   int64_t sum_acs = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kt_ev;   // per-detection kT timing
   std::chrono::steady_clock::time_point w0;
+  // GF_TRACE (diagnostics): timed events on both streams + host waits,
+  // printed to stderr at gf_run_end
+  bool trace = false;
+  struct Mark { const char *what; int64_t step; cudaEvent_t ev; };
+  std::vector<Mark> marks;
+  double host_wait_ms[2] = {0.0, 0.0};   // run_count, run_fill synchronisations
 };
+
+static void trace_mark(Ctx *c, const char *what, int64_t step, cudaStream_t s) {
+  RunState *R = c->run;
+  if (!R || !R->trace) return;
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, s);
+  R->marks.push_back({what, step, e});
+}
 
 static void free_run(Ctx *c) {
   if (!c->run) return;
@@ -215,20 +231,26 @@ static StepArgs step_args(const RunState *R, int64_t i) {
 // kT phases: begun (grid + displacement check queued) -> counted (candidate
 // filter + counts queued) -> filled (canonical array queued)
 static int run_count(Ctx *c) {
+  const auto h0 = std::chrono::steady_clock::now();
   GF_CHECK(c, cudaEventSynchronize(c->ev_disp));
+  if (c->run) c->run->host_wait_ms[0] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
   if (kt_count(c, c->s_kt)) return -1;
   GF_CHECK(c, cudaEventRecord(c->ev_count, c->s_kt));
+  trace_mark(c, "kt_count_end", c->last_snap, c->s_kt);
   c->kt_phase = 2;
   return 0;
 }
 
 static int run_fill(Ctx *c) {
   if (c->kt_phase == 1 && run_count(c)) return -1;
+  const auto h0 = std::chrono::steady_clock::now();
   GF_CHECK(c, cudaEventSynchronize(c->ev_count));
+  if (c->run) c->run->host_wait_ms[1] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
   c->acs_next.n = int64_t(reinterpret_cast<Status *>(c->h_status)->acs_total);
   if (kt_detect_fill(c, c->acs_next, c->s_kt)) return -1;
   if (c->run && !c->run->kt_ev.empty()) GF_CHECK(c, cudaEventRecord(c->run->kt_ev.back().second, c->s_kt));
   GF_CHECK(c, cudaEventRecord(c->ev_ca, c->s_kt));
+  trace_mark(c, "kt_fill_end", c->last_snap, c->s_kt);
   c->fill_done = true;
   return 0;
 }
@@ -389,7 +411,7 @@ void gf_destroy(gf_ctx *ctx) {
                   &c->av_mask, &c->lv_val, &c->av_val, &c->fam_passive, &c->acs.ids, &c->acs.wild, &c->acs_next.ids,
                   &c->acs_next.wild, &c->out_c, &c->touch, &c->inc, &c->inc_alt, &c->inc_key,
                   &c->inc_key_alt, &c->inc_start, &c->heavy, &c->heavy_count, &c->heavy_acc,
-                  &c->cub_tmp_dt, &c->status, &c->dyn_spec, &c->dyn_vals, &c->kt.centers, &c->kt.c4, &c->kt.sfam,
+                  &c->cub_tmp_dt, &c->status, &c->dyn_spec, &c->dyn_vals, &c->kt.c4, &c->kt.sfam,
                   &c->kt.tri_world, &c->kt.ana_world, &c->kt.tfam, &c->kt.afam, &c->kt.grid,
                   &c->kt.minmax, &c->kt.bin_key, &c->kt.bin_key_alt, &c->kt.sph_val, &c->kt.sph_val_alt,
                   &c->kt.cell_start, &c->kt.cell_end, &c->kt.tri_ranges, &c->kt.tri_cnt,
@@ -752,7 +774,10 @@ int gf_download_world(gf_ctx *ctx, double *sph_centers, double *tri_world, doubl
   if (sph_centers && c->n_sph) {
     if (kt_snapshot(c, c->s_dt)) return -1;
     GF_CHECK(c, cudaStreamSynchronize(c->s_dt));
-    GF_CHECK(c, cudaMemcpy(sph_centers, c->kt.centers.p, 24 * c->n_sph, cudaMemcpyDeviceToHost));
+    std::vector<double> c4(4 * c->n_sph);
+    GF_CHECK(c, cudaMemcpy(c4.data(), c->kt.c4.p, 32 * c->n_sph, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < c->n_sph; ++i)
+      for (int ax = 0; ax < 3; ++ax) sph_centers[3 * i + ax] = c4[4 * i + ax];
   }
   if (tri_world && c->n_tri) GF_CHECK(c, cudaMemcpy(tri_world, c->tri_world.p, 72 * c->n_tri, cudaMemcpyDeviceToHost));
   if (ana_world && c->n_ana) GF_CHECK(c, cudaMemcpy(ana_world, c->ana_world.p, 64 * c->n_ana, cudaMemcpyDeviceToHost));
@@ -845,7 +870,7 @@ int gf_detect_snapshot(gf_ctx *ctx, int64_t m, const double *centers, const floa
   for (int64_t i = 0; i < m; ++i) { offr[4 * i] = offr[4 * i + 1] = offr[4 * i + 2] = 0.f; offr[4 * i + 3] = radii[i]; }
   KtScratch &k = c->kt;
   if (upload_u32(c, c->sph_owner, sph_owner, m) || upload_raw(c, c->sph_offr, offr.data(), 16 * m) ||
-      upload_raw(c, k.centers, centers, 24 * m) || upload_raw(c, k.sfam, sph_family, m) ||
+      upload_raw(c, k.sfam, sph_family, m) ||
       upload_u32(c, c->tri_owner, tri_owner, n_t) || upload_raw(c, k.tri_world, tri_world, 72 * n_t) ||
       upload_raw(c, k.tfam, tri_family, n_t) || upload_u32(c, c->ana_owner, ana_owner, n_a) ||
       upload_raw(c, c->ana_kind, ana_kind, n_a) || upload_raw(c, k.ana_world, ana_world, 64 * n_a) ||
@@ -970,6 +995,7 @@ int gf_run_begin(gf_ctx *ctx, const gf_run_params *p) {
   R->p = *p;
   R->period = p->period < 1 ? 1 : p->period;
   R->lag = p->lag < 0 ? 0 : p->lag;
+  R->trace = std::getenv("GF_TRACE") != nullptr;
   c->run = R;
   const int64_t N = p->n_steps;
   c->kt_margin = p->margin;
@@ -993,10 +1019,17 @@ int gf_step_forces(gf_ctx *ctx, int64_t i) {
   if (!R) { c->err = "gf_step_forces outside gf_run_begin / gf_run_end"; return -1; }
   const gf_run_params *p = &R->p;
   const int64_t s = p->step0 + i;
+  trace_mark(c, "dt_step_begin", s, c->s_dt);
   // 1. a detection due at this step boundary is adopted first
-  if (c->next_pending && s >= c->adopt_at && run_adopt(c)) return -1;
+  if (c->next_pending && s >= c->adopt_at) {
+    if (run_adopt(c)) return -1;
+    trace_mark(c, "dt_adopted", s, c->s_dt);
+  }
   // 2. work order: snapshot on the dT stream, detection on the kT stream
-  if (!c->next_pending && (c->first_adopt || s - c->last_snap >= R->period)) {
+  // GF_KT_FREEZE=1 (timing diagnostics only): no work orders after the first
+  // detection, so a run measures the dT chain alone on a frozen contact array
+  const bool kt_freeze = std::getenv("GF_KT_FREEZE") != nullptr;
+  if (!c->next_pending && (c->first_adopt || (!kt_freeze && s - c->last_snap >= R->period))) {
     if (kt_snapshot(c, c->s_dt, p->margin)) return -1;
     GF_CHECK(c, cudaEventRecord(c->ev_snap, c->s_dt));
     GF_CHECK(c, cudaStreamWaitEvent(c->s_kt, c->ev_snap, 0));
@@ -1006,8 +1039,10 @@ int gf_step_forces(gf_ctx *ctx, int64_t i) {
     cudaEventCreate(&e1);
     R->kt_ev.emplace_back(e0, e1);
     GF_CHECK(c, cudaEventRecord(e0, c->s_kt));
+    trace_mark(c, "dt_snapshot_end", s, c->s_dt);
     if (kt_begin(c, p->margin, c->s_kt)) return -1;
     GF_CHECK(c, cudaEventRecord(c->ev_disp, c->s_kt));
+    trace_mark(c, "kt_phaseA_end", s, c->s_kt);
     c->kt_phase = 1;
     c->next_pending = true;
     c->fill_done = false;
@@ -1028,7 +1063,10 @@ int gf_step_forces(gf_ctx *ctx, int64_t i) {
   R->sum_acs += c->acs.n;
   const StepArgs a = step_args(R, i);
   if (update_fixed_scales(c, a.h, a.v_err, a.g)) return -1;
-  return c->f32_state ? dt_forces_f32(c, a, c->s_dt) : dt_forces_f64(c, a, c->s_dt);
+  trace_mark(c, "dt_forces_begin", s, c->s_dt);
+  const int rc = c->f32_state ? dt_forces_f32(c, a, c->s_dt) : dt_forces_f64(c, a, c->s_dt);
+  trace_mark(c, "dt_forces_end", s, c->s_dt);
+  return rc;
 }
 
 int gf_step_integrate(gf_ctx *ctx, int64_t i) {
@@ -1037,6 +1075,7 @@ int gf_step_integrate(gf_ctx *ctx, int64_t i) {
   if (!R) { c->err = "gf_step_integrate outside gf_run_begin / gf_run_end"; return -1; }
   const StepArgs a = step_args(R, i);
   if (c->f32_state ? dt_integrate_f32(c, a, c->s_dt) : dt_integrate_f64(c, a, c->s_dt)) return -1;
+  trace_mark(c, "dt_integrate_end", a.step, c->s_dt);
   // the detection's candidate filter is queued once the dT step is in flight
   if (c->next_pending && c->kt_phase == 1 && run_count(c)) return -1;
   return 0;
@@ -1070,6 +1109,16 @@ int gf_run_end(gf_ctx *ctx, gf_run_result *r) {
   }
   (void)cudaGetLastError();  // an unrecorded timing event is not an error
   r->kt_ms = kt_ms;
+  if (R->trace) {
+    std::fprintf(stderr, "GF_TRACE host_wait_ms count=%.3f fill=%.3f\n", R->host_wait_ms[0], R->host_wait_ms[1]);
+    for (auto &m : R->marks) {
+      float ms = -1.f;
+      cudaEventElapsedTime(&ms, c->t0, m.ev);
+      std::fprintf(stderr, "GF_TRACE %s %lld %.4f\n", m.what, (long long)m.step, ms);
+      cudaEventDestroy(m.ev);
+    }
+    (void)cudaGetLastError();
+  }
   if (c->prof) {
     prof_collect(c);
     c->prof_ms[3] += kt_ms;

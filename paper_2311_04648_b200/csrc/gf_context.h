@@ -43,7 +43,6 @@ struct Acs {
 
 struct KtScratch {
   // snapshot (kT works on a frozen copy; engine.py:577-596)
-  DBuf centers;      // double[n_s*3]
   DBuf c4;           // double4[n_s] (centre, radius)
   DBuf sfam;         // uint8[n_s] sphere family
   DBuf tri_world;    // double[n_t*9]

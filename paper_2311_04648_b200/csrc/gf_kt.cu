@@ -53,7 +53,7 @@ struct KtView {
   const uint32_t *tri_owner;
   const uint32_t *ana_owner;
   const uint8_t *ana_kind;
-  const double *centers;   // snapshot centres [n_s*3]
+  const double *centers;   // snapshot (centre, radius) records viewed as doubles, stride 4
   const uint8_t *sfam;
   const double *tri_world;
   const uint8_t *tfam;
@@ -78,8 +78,7 @@ struct KtView {
 // largest radius (the grid's inputs, broadphase.py:160-186) and -- when
 // candidate lists exist -- whether a sphere moved more than skin / 2 since
 // their rebuild (the k_disp test), in the same pass over the centres
-__global__ void __launch_bounds__(256) k_snapshot(Domain dom, Owners own, Spheres sph, double *centers,
-                                                  double4 *c4, uint8_t *sfam, unsigned long long *mm,
+__global__ void __launch_bounds__(256) k_snapshot(Domain dom, Owners own, Spheres sph, double4 *c4, uint8_t *sfam, unsigned long long *mm,
                                                   const double *ref, double lim2, int *flag) {
   double lo[3], hi[3], rmax = 0.0;
 #pragma unroll
@@ -91,9 +90,6 @@ __global__ void __launch_bounds__(256) k_snapshot(Domain dom, Owners own, Sphere
   for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < sph.n;
        k += int64_t(gridDim.x) * blockDim.x) {
     const double4 c = sph.center[k];
-    centers[3 * k] = c.x;
-    centers[3 * k + 1] = c.y;
-    centers[3 * k + 2] = c.z;
     c4[k] = c;
     sfam[k] = uint8_t(meta_family(own.meta[sph.owner[k]]));
     if (mm) {
@@ -150,7 +146,7 @@ __global__ void k_minmax_init(unsigned long long *mm) {
   if (threadIdx.x == 3) mm[6] = ord_key(0.0);
 }
 
-__global__ void k_minmax(int64_t n_pts, const double *pts, int64_t n_s, const float4 *offr,
+__global__ void k_minmax(int64_t n_pts, const double *pts, int stride, int64_t n_s, const float4 *offr,
                          unsigned long long *mm) {
   double lo[3] = {__longlong_as_double(0x7FF0000000000000ll), 0, 0};
   lo[1] = lo[0]; lo[2] = lo[0];
@@ -160,7 +156,7 @@ __global__ void k_minmax(int64_t n_pts, const double *pts, int64_t n_s, const fl
        i += int64_t(gridDim.x) * blockDim.x) {
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
-      double v = pts[3 * i + ax];
+      double v = pts[stride * i + ax];
       lo[ax] = fmin(lo[ax], v);
       hi[ax] = fmax(hi[ax], v);
     }
@@ -251,9 +247,9 @@ __global__ void k_bin_keys(int64_t n, const double *centers, const float4 *offr,
   Grid g = *gp;
   val[i] = uint32_t(i);
   if (double(offr[i].w) > g.r_cut) { key[i] = kNoCell; return; }
-  long long ix = axis_bin(centers[3 * i], g.glo[0], g.inv_cell, g.nc[0]);
-  long long iy = axis_bin(centers[3 * i + 1], g.glo[1], g.inv_cell, g.nc[1]);
-  long long iz = axis_bin(centers[3 * i + 2], g.glo[2], g.inv_cell, g.nc[2]);
+  long long ix = axis_bin(centers[4 * i], g.glo[0], g.inv_cell, g.nc[0]);
+  long long iy = axis_bin(centers[4 * i + 1], g.glo[1], g.inv_cell, g.nc[1]);
+  long long iz = axis_bin(centers[4 * i + 2], g.glo[2], g.inv_cell, g.nc[2]);
   key[i] = uint32_t((iz * g.nc[1] + iy) * g.nc[0] + ix);
 }
 
@@ -417,7 +413,7 @@ __global__ void k_gather_sorted(int64_t n, const uint32_t *sorted, const double 
   int64_t u = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (u >= n) return;
   uint32_t i = sorted[u];
-  const double x = centers[3 * size_t(i)], y = centers[3 * size_t(i) + 1], z = centers[3 * size_t(i) + 2];
+  const double x = centers[4 * size_t(i)], y = centers[4 * size_t(i) + 1], z = centers[4 * size_t(i) + 2];
   sc[u] = make_double4(x, y, z, double(offr[i].w));
   sm[u] = make_uint4(i, owner[i], sfam[i], 0u);
   const Grid g = *gp;
@@ -452,7 +448,7 @@ __global__ void __launch_bounds__(128) k_pairs_other(KtView v, unsigned long lon
   uint8_t fi = 0;
   long long lo_i[3] = {0, 0, 0}, hi_i[3] = {0, 0, 0};
   if (active) {
-    ci[0] = v.centers[3 * i64]; ci[1] = v.centers[3 * i64 + 1]; ci[2] = v.centers[3 * i64 + 2];
+    ci[0] = v.centers[4 * i64]; ci[1] = v.centers[4 * i64 + 1]; ci[2] = v.centers[4 * i64 + 2];
     ri_f = v.sph.offr[i].w;
     oi = v.sph.owner[i];
     fi = v.sfam[i];
@@ -504,8 +500,8 @@ __device__ __forceinline__ bool sa_candidate(const KtView &v, uint32_t i, uint32
   const uint32_t oi = v.sph.owner[i];
   if (oi == v.ana_owner[k] || !dd_keep(v.own.dd, oi, v.ana_owner[k])) return false;
   double gap, bx, by, bz, rb;
-  analytic_gap(v.ana_kind[k], v.ana_world + 8 * size_t(k), v.centers[3 * size_t(i)], v.centers[3 * size_t(i) + 1],
-               v.centers[3 * size_t(i) + 2], gap, bx, by, bz, rb);
+  analytic_gap(v.ana_kind[k], v.ana_world + 8 * size_t(k), v.centers[4 * size_t(i)], v.centers[4 * size_t(i) + 1],
+               v.centers[4 * size_t(i) + 2], gap, bx, by, bz, rb);
   return gap < double(v.sph.offr[i].w) + reach;
 }
 
@@ -533,7 +529,7 @@ __global__ void k_sa_filter(KtView v, const uint2 *cand, int64_t n_cand, unsigne
   uint2 p = make_uint2(0u, 0u);
   if (e < n_cand && v.grid->valid) {
     p = cand[e];
-    const double ci[3] = {v.centers[3 * size_t(p.x)], v.centers[3 * size_t(p.x) + 1], v.centers[3 * size_t(p.x) + 2]};
+    const double ci[3] = {v.centers[4 * size_t(p.x)], v.centers[4 * size_t(p.x) + 1], v.centers[4 * size_t(p.x) + 2]};
     hit = sa_pair(v, p.y, ci, v.sph.offr[p.x].w, v.sph.owner[p.x], v.sfam[p.x]);
     if (hit) atomicAdd(&counts[2 * v.sph.n + p.x], 1ull);
   }
@@ -572,11 +568,12 @@ __global__ void k_sort_seg(int64_t nseg, const unsigned long long *offsets, uint
 // ---------------------------------------------------------------------------
 
 // any sphere displaced more than skin / 2 since the rebuild -> flag
-__global__ void k_disp(int64_t n, const double *c, const double *ref, double lim2, int *flag) {
+__global__ void k_disp(int64_t n, const double4 *c4, const double *ref, double lim2, int *flag) {
   int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   bool far = false;
   if (i < n) {
-    double dx = c[3 * i] - ref[3 * i], dy = c[3 * i + 1] - ref[3 * i + 1], dz = c[3 * i + 2] - ref[3 * i + 2];
+    const double4 c = c4[i];
+    double dx = c.x - ref[3 * i], dy = c.y - ref[3 * i + 1], dz = c.z - ref[3 * i + 2];
     far = dx * dx + dy * dy + dz * dz > lim2;
   }
   if (__any_sync(0xffffffffu, far) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
@@ -668,7 +665,7 @@ __global__ void __launch_bounds__(128) k_cand_big(KtView v, const uint32_t *bigs
   if (!g.valid) return;
   for (int64_t bi = blockIdx.x; bi < n_big; bi += gridDim.x) {
     const uint32_t B = bigs[bi];
-    const double bx = v.centers[3 * size_t(B)], by = v.centers[3 * size_t(B) + 1], bz = v.centers[3 * size_t(B) + 2];
+    const double bx = v.centers[4 * size_t(B)], by = v.centers[4 * size_t(B) + 1], bz = v.centers[4 * size_t(B) + 2];
     const double rB = double(v.sph.offr[B].w);
     const uint32_t oB = v.sph.owner[B];
     const double reach = rB + g.r_cut + reach_m;
@@ -703,8 +700,8 @@ __global__ void __launch_bounds__(128) k_cand_big(KtView v, const uint32_t *bigs
     for (int64_t q = threadIdx.x; q < n_big; q += blockDim.x) {
       const uint32_t j = bigs[q];
       if (j <= B || v.sph.owner[j] == oB || !dd_keep(v.own.dd, v.sph.owner[j], oB)) continue;
-      const double dx = bx - v.centers[3 * size_t(j)], dy = by - v.centers[3 * size_t(j) + 1],
-                   dz = bz - v.centers[3 * size_t(j) + 2];
+      const double dx = bx - v.centers[4 * size_t(j)], dy = by - v.centers[4 * size_t(j) + 1],
+                   dz = bz - v.centers[4 * size_t(j) + 2];
       const double rr = rB + double(v.sph.offr[j].w) + reach_m;
       if (dx * dx + dy * dy + dz * dz >= rr * rr * (1.0 + 1e-9)) continue;
       atomicAdd(&counts[B], 1ull);
@@ -848,9 +845,13 @@ __global__ void __launch_bounds__(kFcBlock) k_compact(KtView v, const uint2 *can
   }
 }
 
-__global__ void k_copy_ref(int64_t n3, const double *c, double *ref) {
+__global__ void k_copy_ref(int64_t n, const double4 *c4, double *ref) {
   int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (i < n3) ref[i] = c[i];
+  if (i >= n) return;
+  const double4 c = c4[i];
+  ref[3 * i] = c.x;
+  ref[3 * i + 1] = c.y;
+  ref[3 * i + 2] = c.z;
 }
 
 __global__ void k_fill_u32(const Grid *gp, uint32_t *a, uint32_t value, int fine_plus_one) {
@@ -865,7 +866,7 @@ __global__ void k_bin_ranges(int64_t n, const double *centers, const float4 *off
   int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (i >= n) return;
   Grid g = *gp;
-  double c[3] = {centers[3 * i], centers[3 * i + 1], centers[3 * i + 2]};
+  double c[3] = {centers[4 * i], centers[4 * i + 1], centers[4 * i + 2]};
   long long lo[3], hi[3];
   sphere_range(g, c, offr[i].w, margin, lo, hi);
   for (int ax = 0; ax < 3; ++ax) {
@@ -1010,8 +1011,7 @@ __global__ void k_inc_start(int64_t n_owner, int64_t n_inc, const uint32_t *sort
 
 int kt_snapshot(Ctx *c, cudaStream_t s, double margin) {
   KtScratch &k = c->kt;
-  if (ensure(c, k.centers, sizeof(double) * 3 * (c->n_sph + 1), s) ||
-      ensure(c, k.c4, sizeof(double4) * (c->n_sph + 1), s))
+  if (ensure(c, k.c4, sizeof(double4) * (c->n_sph + 1), s))
     return -1;
   if (ensure(c, k.sfam, c->n_sph + 1, s)) return -1;
   if (ensure(c, k.tri_world, sizeof(double) * 9 * (c->n_tri + 1), s)) return -1;
@@ -1034,7 +1034,7 @@ int kt_snapshot(Ctx *c, cudaStream_t s, double margin) {
   const double skin = c->skin_factor * margin;
   if (c->n_sph)
     k_snapshot<<<unsigned(std::min<int64_t>(grid_for(c->n_sph), 148 * 8)), kBlock, 0, s>>>(
-        c->dom, owners_view(c), spheres_view(c), k.centers.as<double>(), k.c4.as<double4>(), k.sfam.as<uint8_t>(),
+        c->dom, owners_view(c), spheres_view(c), k.c4.as<double4>(), k.sfam.as<uint8_t>(),
         det ? mm : nullptr, check ? k.ref.as<double>() : nullptr, 0.25 * skin * skin, k.flag.as<int>());
   k.snap_det = det;
   k.snap_checked = check;
@@ -1065,7 +1065,7 @@ static KtView kt_view(Ctx *c, double margin) {
   v.tri_owner = c->tri_owner.as<uint32_t>();
   v.ana_owner = c->ana_owner.as<uint32_t>();
   v.ana_kind = c->ana_kind.as<uint8_t>();
-  v.centers = k.centers.as<double>();
+  v.centers = k.c4.as<double>();   // the (centre, radius) snapshot records, stride 4
   v.sfam = k.sfam.as<uint8_t>();
   v.tri_world = k.tri_world.as<double>();
   v.tfam = k.tfam.as<uint8_t>();
@@ -1105,9 +1105,9 @@ int kt_begin(Ctx *c, double margin, cudaStream_t s) {
   k.snap_det = false;
   if (!snap) {
     k_minmax_init<<<1, 32, 0, s>>>(mm);
-    if (n) k_minmax<<<std::min<int64_t>(grid_for(n), 1184), kBlock, 0, s>>>(n, k.centers.as<double>(), n, c->sph_offr.as<float4>(), mm);
+    if (n) k_minmax<<<std::min<int64_t>(grid_for(n), 1184), kBlock, 0, s>>>(n, k.c4.as<double>(), 4, n, c->sph_offr.as<float4>(), mm);
   }
-  if (nt) k_minmax<<<std::min<int64_t>(grid_for(3 * nt), 1184), kBlock, 0, s>>>(3 * nt, k.tri_world.as<double>(), 0, nullptr, mm);
+  if (nt) k_minmax<<<std::min<int64_t>(grid_for(3 * nt), 1184), kBlock, 0, s>>>(3 * nt, k.tri_world.as<double>(), 3, 0, nullptr, mm);
   k_grid<<<1, 1, 0, s>>>(mm, n_pts, margin, c->kt_bin_size, c->r_cut, (long long)kMaxCells, margin + skin,
                          k.grid.as<Grid>());
   const Grid *gp = k.grid.as<Grid>();
@@ -1115,7 +1115,7 @@ int kt_begin(Ctx *c, double margin, cudaStream_t s) {
   if (k.cand_valid && n) {
     if (!(snap && k.snap_checked)) {
       GF_CHECK(c, cudaMemsetAsync(flag, 0, sizeof(int), s));
-      k_disp<<<grid_for(n), kBlock, 0, s>>>(n, k.centers.as<double>(), k.ref.as<double>(), 0.25 * skin * skin, flag);
+      k_disp<<<grid_for(n), kBlock, 0, s>>>(n, k.c4.as<double4>(), k.ref.as<double>(), 0.25 * skin * skin, flag);
     }
   } else {
     k_set_int<<<1, 1, 0, s>>>(flag, 1);
@@ -1179,7 +1179,7 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
   GF_CHECK(c, cudaMemsetAsync(cc, 0, 8 * (n + 1), s));
   GF_CHECK(c, cudaMemsetAsync(cn, 0, 8, s));
   if (n) {
-    k_bin_keys<<<grid_for(n), kBlock, 0, s>>>(n, k.centers.as<double>(), c->sph_offr.as<float4>(), gp,
+    k_bin_keys<<<grid_for(n), kBlock, 0, s>>>(n, k.c4.as<double>(), c->sph_offr.as<float4>(), gp,
                                              k.bin_key.as<uint32_t>(), k.sph_val.as<uint32_t>());
     size_t tmp = 0;
     cub::DoubleBuffer<uint32_t> dk(k.bin_key.as<uint32_t>(), k.bin_key_alt.as<uint32_t>());
@@ -1195,7 +1195,7 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
     k_fill_u32<<<592, 256, 0, s>>>(gp, k.cell_start.as<uint32_t>(), 0xFFFFFFFFu, 0);
     k_cell_bounds<<<grid_for(n), kBlock, 0, s>>>(n, k.bin_key.as<uint32_t>(), k.cell_start.as<uint32_t>(),
                                                 k.cell_end.as<uint32_t>());
-    k_gather_sorted<<<grid_for(n), kBlock, 0, s>>>(n, k.sph_val.as<uint32_t>(), k.centers.as<double>(),
+    k_gather_sorted<<<grid_for(n), kBlock, 0, s>>>(n, k.sph_val.as<uint32_t>(), k.c4.as<double>(),
                                                   c->sph_offr.as<float4>(), c->sph_owner.as<uint32_t>(),
                                                   k.sfam.as<uint8_t>(), gp, k.sc.as<double4>(),
                                                   k.sm.as<uint4>(), k.sf.as<float4>());
@@ -1229,7 +1229,7 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
                                       k.cursor.as<unsigned>(), k.cand.as<uint2>(),
                                       (unsigned long long)k.cand_cap);
     k_sort_seg<<<grid_for(n), kBlock, 0, s>>>(n, k.cand_seg.as<unsigned long long>(), k.cand.as<uint2>());
-    k_copy_ref<<<grid_for(3 * n), kBlock, 0, s>>>(3 * n, k.centers.as<double>(), k.ref.as<double>());
+    k_copy_ref<<<grid_for(n), kBlock, 0, s>>>(n, k.c4.as<double4>(), k.ref.as<double>());
   }
   // sphere-analytic candidates for the same skin, while the world is static
   k.sa_world_version = ~0ull;
@@ -1417,7 +1417,7 @@ int kt_bin_ranges(Ctx *c, double margin, int64_t *h_out) {
   const int64_t n = c->n_sph;
   DBuf tmp;
   if (ensure(c, tmp, sizeof(long long) * 6 * (n + 1), s)) return -1;
-  k_bin_ranges<<<grid_for(n), kBlock, 0, s>>>(n, c->kt.centers.as<double>(), c->sph_offr.as<float4>(),
+  k_bin_ranges<<<grid_for(n), kBlock, 0, s>>>(n, c->kt.c4.as<double>(), c->sph_offr.as<float4>(),
                                               c->kt.grid.as<Grid>(), margin, tmp.as<long long>());
   GF_CHECK(c, cudaMemcpyAsync(h_out, tmp.p, sizeof(long long) * 6 * n, cudaMemcpyDeviceToHost, s));
   GF_CHECK(c, cudaStreamSynchronize(s));
