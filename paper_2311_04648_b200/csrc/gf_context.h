@@ -62,7 +62,7 @@ struct KtScratch {
   DBuf cells, n_cells;  // non-empty enumeration cells
   // Verlet candidate lists (rebuilt when a sphere moved > skin / 2)
   DBuf cand, cand_tmp, cand_n, cand_cnt, cand_seg, ref, flag, cflags, sel_n;
-  int64_t cand_cap = 0, n_cand = 0, rebuilds = 0;
+  int64_t cand_cap = 0, n_cand = 0, rebuilds = 0, big_cap = 0;
   // hit bitmask and scanned per-block hit counts of the last two filtered
   // arrays (double-buffered), with the detection serial / candidate
   // generation they belong to
@@ -168,7 +168,7 @@ struct Ctx {
   int64_t last_touching = 0;
   // NVRTC user force model (gf_nvrtc.cu)
   bool user_model = false;
-  void *user_fn_f64 = nullptr, *user_fn_f32 = nullptr;
+  void *user_fn_f64 = nullptr, *user_fn_f32 = nullptr, *user_fn_ss = nullptr, *user_fn_walls = nullptr;
   // per-kernel device timing (enabled by gf_set_profiling)
   bool prof = false;
   std::vector<cudaEvent_t> prof_ev;   // kProfEv per profiled step: start, contacts, heavy, integrate,

@@ -447,6 +447,157 @@ __device__ __forceinline__ void force_entry(const DtView &v, uint32_t k, double 
   }
 }
 
+// A-side contributions of a warp's contacts (entries in A-sorted contact
+// order, so equal A owners sit in consecutive lanes): each run's int64
+// fixed-point words are summed in registers (exact) and added by the run's
+// head lane; boundary owners (scale 0) take fp64 atomics.  Every lane of the
+// warp must call it; `out` = force (3), `ta` = torque on A (3).
+__device__ __forceinline__ void a_side_sums(const DtView &v, bool use_a, uint32_t oa, float sa_f, float sa_t,
+                                            const float *out, const float *ta, int lane) {
+  const bool fixed_a = use_a && sa_f > 0.f;
+  if (use_a && !fixed_a) {   // boundary owner: fp64 atomics, not aggregated
+    unsigned long long *fa = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(oa));
+    for (int q = 0; q < 3; ++q) {
+      atomicAdd(reinterpret_cast<double *>(fa + q), double(out[q]));
+      atomicAdd(reinterpret_cast<double *>(fa + 3 + q), double(ta[q]));
+    }
+  }
+  const uint32_t key = fixed_a ? oa : 0xFFFFFFFFu;
+  const uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
+  const bool head = lane == 0 || prev != key;
+  const unsigned heads = __ballot_sync(0xffffffffu, head);
+  const unsigned later = heads & ~((2u << lane) - 1u);   // heads after this lane
+  const int run_end = later ? __ffs(later) - 2 : 31;
+  // segmented sums over the runs: only as many doubling steps as the longest
+  // run needs (runs are short -- an owner's touching partners of higher slot)
+  const unsigned runlen = (head && fixed_a) ? unsigned(run_end - lane + 1) : 0u;
+  const unsigned maxrun = __reduce_max_sync(0xffffffffu, runlen);
+  long long acc[6];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    acc[q] = fixed_a ? __double2ll_rn(double(out[q]) * double(sa_f)) : 0ll;
+    acc[3 + q] = fixed_a ? __double2ll_rn(double(ta[q]) * double(sa_t)) : 0ll;
+  }
+  for (unsigned off = 1; off < maxrun; off <<= 1) {
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      const long long o = __shfl_down_sync(0xffffffffu, acc[q], off);
+      if (lane + int(off) <= run_end) acc[q] += o;
+    }
+  }
+  if (head && fixed_a) {
+    unsigned long long *fa = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(oa));
+#pragma unroll
+    for (int q = 0; q < 6; ++q) atomicAdd(fa + q, (unsigned long long)acc[q]);
+  }
+}
+
+// Fused sphere-sphere loop of the throughput build for a user model `Core`
+// (NVRTC-compiled, gf_nvrtc.cu): every entry of the sphere-sphere block --
+// a user core may act at any overlap -- in warps of 32 consecutive entries.
+// Geometry in fp64 from the centre records (depth = ra + rb - d, exactly as
+// contact_geometry), kinematics from the fp32 records (one load round), the
+// core in fp64 with the reference's argument list, history in place, B side
+// one atomic per word, A side summed over runs of equal owners.
+template <typename Core>
+__device__ __forceinline__ void user_ss_loop(const DtView &v, double ts, double sim_time) {
+  if (v.st->err) return;
+  const unsigned long long n_ss = v.seg[v.n_sph];
+  const int lane = threadIdx.x & 31;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  unsigned long long touched = 0;
+  for (unsigned long long base = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) & ~31ull; base < n_ss;
+       base += stride) {
+    const unsigned long long k = base + lane;
+    float out[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    float ta[3] = {0.f, 0.f, 0.f};
+    uint32_t oa = 0xFFFFFFFFu;
+    float sa_f = 0.f, sa_t = 0.f;
+    bool use_a = false;
+    if (k < n_ss) {
+      const uint2 id = v.ids[k];
+      const uint32_t a = id.x, b = id.y & kSlotMask;
+      const double4 cA = v.sph.center[a], cB = v.sph.center[b];
+      const SphKin ka = v.sph.kin[a], kb = v.sph.kin[b];
+      const double dx = cA.x - cB.x, dy = cA.y - cB.y, dz = cA.z - cB.z;
+      const double d = sqrt(dx * dx + dy * dy + dz * dz);
+      double depth, bx, by, bz;
+      if (d < 1e-300) {
+        depth = cA.w + cB.w; bx = 0.0; by = 0.0; bz = 1.0;
+      } else {
+        const double inv = 1.0 / d;
+        bx = dx * inv; by = dy * inv; bz = dz * inv;
+        depth = cA.w + cB.w - d;
+      }
+      if (depth > 0.0) ++touched;
+      // contact point p = cA - b (ra - depth / 2); lever arms p - pos_a, p - pos_b
+      const double half = cA.w - 0.5 * depth;
+      const double rax = ka.r.x - bx * half, ray = ka.r.y - by * half, raz = ka.r.z - bz * half;
+      const double rbx = kb.r.x + dx - bx * half, rby = kb.r.y + dy - by * half, rbz = kb.r.z + dz - bz * half;
+      const double rotax = ka.w.y * raz - ka.w.z * ray, rotay = ka.w.z * rax - ka.w.x * raz,
+                   rotaz = ka.w.x * ray - ka.w.y * rax;
+      const double rotbx = kb.w.y * rbz - kb.w.z * rby, rotby = kb.w.z * rbx - kb.w.x * rbz,
+                   rotbz = kb.w.x * rby - kb.w.y * rbx;
+      CoreArgs arg;
+      arg.overlap = depth; arg.ts = ts; arg.sim_time = sim_time;
+      arg.b2ax = bx; arg.b2ay = by; arg.b2az = bz;
+      arg.vx = (ka.v.x + rotax) - (kb.v.x + rotbx);
+      arg.vy = (ka.v.y + rotay) - (kb.v.y + rotby);
+      arg.vz = (ka.v.z + rotaz) - (kb.v.z + rotbz);
+      arg.wrx = rotbx - rotax; arg.wry = rotby - rotay; arg.wrz = rotbz - rotaz;
+      const double ma = ka.v.w, mb = kb.v.w;
+      arg.mass_eff = (ma * mb) / (ma + mb);
+      arg.ra = cA.w; arg.rb = cB.w;
+      arg.mat_a = int(ka.id.y); arg.mat_b = int(kb.id.y);
+      arg.pair = v.mat.pair; arg.n_mat = v.mat.n_mat;
+      arg.wild = v.wild + size_t(v.W) * k;
+      arg.M = &v.mat;
+      double o6[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      Core::eval(arg, o6);
+      if (o6[0] != 0.0 || o6[1] != 0.0 || o6[2] != 0.0 || o6[3] != 0.0 || o6[4] != 0.0 || o6[5] != 0.0) {
+        for (int q = 0; q < 6; ++q) out[q] = float(o6[q]);
+        const double tx = o6[0] + o6[3], ty = o6[1] + o6[4], tz = o6[2] + o6[5];
+        ta[0] = float(ray * tz - raz * ty); ta[1] = float(raz * tx - rax * tz); ta[2] = float(rax * ty - ray * tx);
+        const double tb[3] = {rby * tz - rbz * ty, rbz * tx - rbx * tz, rbx * ty - rby * tx};
+        if (v.acc_all || !(kb.id.z & kKinPassive)) {
+          const double sbf = kb.w.w, sbt = kb.r.w;
+          unsigned long long *fb = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(kb.id.x));
+          for (int q = 0; q < 3; ++q) {
+            if (sbf > 0.0) {
+              atomicAdd(fb + q, (unsigned long long)__double2ll_rn(-o6[q] * sbf));
+              atomicAdd(fb + 3 + q, (unsigned long long)__double2ll_rn(-tb[q] * sbt));
+            } else {
+              atomicAdd(reinterpret_cast<double *>(fb + q), -o6[q]);
+              atomicAdd(reinterpret_cast<double *>(fb + 3 + q), -tb[q]);
+            }
+          }
+        }
+        oa = ka.id.x;
+        use_a = v.acc_all || !(ka.id.z & kKinPassive);
+        sa_f = ka.w.w;
+        sa_t = ka.r.w;
+      }
+    }
+    a_side_sums(v, use_a, oa, sa_f, sa_t, out, ta, lane);
+  }
+  for (int off = 16; off > 0; off >>= 1) touched += __shfl_down_sync(0xffffffffu, touched, off);
+  if (lane == 0 && touched) {
+    atomicAdd(&v.st->touching, 2ull * touched);
+    atomicAdd(&v.st->touch_pairs, touched);
+  }
+}
+
+// a user model's wall kinds: every entry from the start of the (kind 1,
+// sphere 0) segment, generic path
+template <typename VelT, typename Core>
+__device__ __forceinline__ void user_walls_loop(const DtView &v, double ts, double sim_time) {
+  if (v.st->err) return;
+  const unsigned long long n = (unsigned long long)v.n_acs, k0 = v.seg[v.n_sph];
+  for (unsigned long long i = k0 + blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x)
+    force_entry<VelT, Core>(v, uint32_t(i), ts, sim_time);
+}
+
 // The force loop: entries listed in `list` (touching entries of the built-in
 // model) or, for cores that act on every entry (user models may act at
 // negative overlap), all entries.

@@ -296,44 +296,7 @@ __device__ __forceinline__ void ss_force_warp(const DtView &v, bool live, uint32
     sa_f = ka.w.w;
     sa_t = ka.r.w;
   }
-  // A side: sum each run of equal A owners' int64 words in registers (exact)
-  // and let the run's head lane add them
-  const bool fixed_a = use_a && sa_f > 0.f;
-  if (use_a && !fixed_a) {   // boundary owner: fp64 atomics, not aggregated
-    unsigned long long *fa = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(oa));
-    for (int q = 0; q < 3; ++q) {
-      atomicAdd(reinterpret_cast<double *>(fa + q), double(out[q]));
-      atomicAdd(reinterpret_cast<double *>(fa + 3 + q), double(ta[q]));
-    }
-  }
-  const uint32_t key = fixed_a ? oa : 0xFFFFFFFFu;
-  const uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
-  const bool head = lane == 0 || prev != key;
-  const unsigned heads = __ballot_sync(0xffffffffu, head);
-  const unsigned later = heads & ~((2u << lane) - 1u);   // heads after this lane
-  const int run_end = later ? __ffs(later) - 2 : 31;
-  // segmented sums over the runs: only as many doubling steps as the longest
-  // run needs (runs are short -- an owner's touching partners of higher slot)
-  const unsigned runlen = (head && fixed_a) ? unsigned(run_end - lane + 1) : 0u;
-  const unsigned maxrun = __reduce_max_sync(0xffffffffu, runlen);
-  long long acc[6];
-#pragma unroll
-  for (int q = 0; q < 3; ++q) {
-    acc[q] = fixed_a ? __double2ll_rn(double(out[q]) * double(sa_f)) : 0ll;
-    acc[3 + q] = fixed_a ? __double2ll_rn(double(ta[q]) * double(sa_t)) : 0ll;
-  }
-  for (unsigned off = 1; off < maxrun; off <<= 1) {
-#pragma unroll
-    for (int q = 0; q < 6; ++q) {
-      const long long o = __shfl_down_sync(0xffffffffu, acc[q], off);
-      if (lane + int(off) <= run_end) acc[q] += o;
-    }
-  }
-  if (head && fixed_a) {
-    unsigned long long *fa = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(oa));
-#pragma unroll
-    for (int q = 0; q < 6; ++q) atomicAdd(fa + q, (unsigned long long)acc[q]);
-  }
+  a_side_sums(v, use_a, oa, sa_f, sa_t, out, ta, lane);
 }
 
 // Throughput build, built-in Hertz-Mindlin, split form: force phase over the
@@ -886,6 +849,10 @@ int dt_forces_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
       ss_timed = true;
       GF_CHECK(c, launch_k(c, k_touch, dim3(148 * 4), dim3(256), s, v, list0, list1, tn, step,
                            (const unsigned long long *)(v.seg + c->n_sph)));
+    } else if (c->user_model && std::is_same<VelT, float>::value && v.sph.kin && c->user_fn_ss) {
+      // user model, throughput build: the NVRTC sphere-sphere loop counts its
+      // own touching entries; the narrow phase here covers the wall kinds
+      k_touch<<<148 * 4, 256, 0, s>>>(v, list0, list1, tn, (unsigned long long)a.step, v.seg + c->n_sph);
     } else {
       k_touch<<<unsigned(std::min<int64_t>((v.n_acs + 255) / 256, 148 * 16)), 256, 0, s>>>(
           v, list0, list1, tn, (unsigned long long)a.step, nullptr);

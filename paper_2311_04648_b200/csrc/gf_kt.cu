@@ -580,32 +580,32 @@ __global__ void k_disp(int64_t n, const double4 *c4, const double *ref, double l
 }
 
 // candidate pairs among small spheres: half stencil on the enumeration grid
-// (cell = 2 (r_cut + margin + skin)); hits counted per lower slot and
-// appended to a scratch list
+// (cell = 2 (r_cut + margin + skin)), one thread per cell-sorted sphere.
+// Two passes over the same loops, no shared counters: kFill = false counts
+// each thread's hits, kFill = true writes them as (a << 32 | b) keys at the
+// thread's exclusive-scan offset (a = lower slot); a key sort then gives the
+// (a, b)-ordered list.
+template <bool kFill>
 __global__ void __launch_bounds__(128) k_cand_ss(KtView v, const uint4 *sm, const float4 *sf, double reach_m,
-                                                 unsigned long long *counts, uint2 *tmp,
-                                                 unsigned long long *tmp_n, unsigned long long cap) {
+                                                 uint32_t *ucnt, const unsigned long long *uoff,
+                                                 unsigned long long *keys) {
   int64_t u64 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (u64 >= v.sph.n) return;
   const Grid g = *v.grid;
-  bool active = u64 < v.sph.n && g.valid;
+  bool active = g.valid;
   uint32_t key = active ? v.bin_key[u64] : kNoCell;
   active = active && key != kNoCell;
   const float ext = float(double(max(g.nc[0], max(g.nc[1], g.nc[2]))) / g.inv_cell);
   const float slack = 1e-6f * ext + 1e-30f;
   const float marg = float(reach_m);
-  float4 f0 = make_float4(0.f, 0.f, 0.f, 0.f);
-  uint4 m0 = make_uint4(0, 0, 0, 0);
-  long long cx = 0, cy = 0, cz = 0;
+  uint32_t hits = 0;
+  unsigned long long w_out = kFill ? uoff[u64] : 0ull;
   if (active) {
-    f0 = sf[u64];
-    m0 = sm[u64];
-    cx = key % g.nc[0];
-    cy = (key / g.nc[0]) % g.nc[1];
-    cz = key / (g.nc[0] * g.nc[1]);
-  }
-  for (int span = 0; span < 6; ++span) {
-    uint32_t s0 = 0, s1 = 0;
-    if (active) {
+    const float4 f0 = sf[u64];
+    const uint4 m0 = sm[u64];
+    const long long cx = key % g.nc[0], cy = (key / g.nc[0]) % g.nc[1], cz = key / (g.nc[0] * g.nc[1]);
+    for (int span = 0; span < 6; ++span) {
+      uint32_t s0 = 0, s1 = 0;
       if (span == 0) {
         s0 = uint32_t(u64) + 1;
         s1 = v.cell_end[key];
@@ -629,38 +629,31 @@ __global__ void __launch_bounds__(128) k_cand_ss(KtView v, const uint4 *sm, cons
           if (a0 == 0xFFFFFFFFu) s1 = 0;
         }
       }
-    }
-    const uint32_t len = s1 > s0 ? s1 - s0 : 0;
-    uint32_t maxlen = len;
-    for (int off = 16; off > 0; off >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, off));
-    for (uint32_t t = 0; t < maxlen; ++t) {
-      bool hit = false;
-      uint2 e = make_uint2(0, 0);
-      if (t < len) {
-        const uint32_t w = s0 + t;
+      for (uint32_t w = s0; w < s1; ++w) {
         const float4 f1 = sf[w];
         const float dx = f0.x - f1.x, dy = f0.y - f1.y, dz = f0.z - f1.z;
         const float rr = f0.w + f1.w + marg + slack;
         if (dx * dx + dy * dy + dz * dz < rr * rr * 1.0001f) {
           const uint4 m1 = sm[w];
           if (m1.y != m0.y && dd_keep(v.own.dd, m0.y, m1.y)) {
-            hit = true;
-            const uint32_t a = min(m0.x, m1.x), b = max(m0.x, m1.x);
-            e = make_uint2(a, b);
-            atomicAdd(&counts[a], 1ull);
+            if (kFill) {
+              const uint32_t a = min(m0.x, m1.x), b = max(m0.x, m1.x);
+              keys[w_out++] = (static_cast<unsigned long long>(a) << 32) | b;
+            }
+            ++hits;
           }
         }
       }
-      append_pair(hit, e, tmp, tmp_n, cap);
     }
   }
+  if (!kFill) ucnt[u64] = hits;
 }
 
 // candidate pairs involving big spheres (fp64 distance < r_i + r_j + M)
 __global__ void __launch_bounds__(128) k_cand_big(KtView v, const uint32_t *bigs, int64_t n_big,
                                                   const double4 *sc, const uint4 *sm, double reach_m,
-                                                  unsigned long long *counts, uint2 *tmp,
-                                                  unsigned long long *tmp_n, unsigned long long cap) {
+                                                  unsigned long long *keys, unsigned long long *big_n,
+                                                  unsigned long long cap) {
   const Grid g = *v.grid;
   if (!g.valid) return;
   for (int64_t bi = blockIdx.x; bi < n_big; bi += gridDim.x) {
@@ -692,9 +685,8 @@ __global__ void __launch_bounds__(128) k_cand_big(KtView v, const uint32_t *bigs
         const double rr = rB + c1.w + reach_m;
         if (dx * dx + dy * dy + dz * dz >= rr * rr * (1.0 + 1e-9)) continue;
         const uint32_t a = min(m1.x, B), c = max(m1.x, B);
-        atomicAdd(&counts[a], 1ull);
-        unsigned long long pos = atomicAdd(tmp_n, 1ull);
-        if (pos < cap) tmp[pos] = make_uint2(a, c);
+        const unsigned long long pos = atomicAdd(big_n, 1ull);
+        if (pos < cap) keys[pos] = (static_cast<unsigned long long>(a) << 32) | c;
       }
     }
     for (int64_t q = threadIdx.x; q < n_big; q += blockDim.x) {
@@ -704,23 +696,20 @@ __global__ void __launch_bounds__(128) k_cand_big(KtView v, const uint32_t *bigs
                    dz = bz - v.centers[4 * size_t(j) + 2];
       const double rr = rB + double(v.sph.offr[j].w) + reach_m;
       if (dx * dx + dy * dy + dz * dz >= rr * rr * (1.0 + 1e-9)) continue;
-      atomicAdd(&counts[B], 1ull);
-      unsigned long long pos = atomicAdd(tmp_n, 1ull);
-      if (pos < cap) tmp[pos] = make_uint2(B, j);
+      const unsigned long long pos = atomicAdd(big_n, 1ull);
+      if (pos < cap) keys[pos] = (static_cast<unsigned long long>(B) << 32) | j;
     }
   }
 }
 
-// scatter candidates into per-sphere segments (k_sort_seg then orders them)
-__global__ void k_place_cand(const unsigned long long *m_p, const uint2 *tmp, const unsigned long long *seg,
-                             unsigned *cursor, uint2 *cand, unsigned long long cap) {
-  const unsigned long long m = min(*m_p, cap);
-  for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < m;
-       e += (unsigned long long)gridDim.x * blockDim.x) {
-    const uint2 p = tmp[e];
-    cand[seg[p.x] + atomicAdd(&cursor[p.x], 1u)] = p;
+// sorted (a << 32 | b) keys -> the (a, b) candidate list
+__global__ void k_cand_unpack(int64_t total, const unsigned long long *keys, uint2 *cand) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    const unsigned long long k = keys[e];
+    cand[e] = make_uint2(uint32_t(k >> 32), uint32_t(k & 0xFFFFFFFFull));
   }
 }
+
 
 // Sphere-sphere block of a detection in two coalesced passes over the
 // candidate list (sorted by (a, b)):
@@ -1162,7 +1151,7 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
       ensure(c, k.cursor, 4 * (3 * n + 1), s) || ensure(c, k.sc, 32 * (n + 1), s) ||
       ensure(c, k.sm, 16 * (n + 1), s) || ensure(c, k.sf, 16 * (n + 1), s) ||
       ensure(c, k.cand_n, 16, s) || ensure(c, k.cand_cnt, 8 * (n + 1), s) ||
-      ensure(c, k.cand_seg, 8 * (n + 1), s) || ensure(c, k.ref, 24 * (n + 1), s) ||
+      ensure(c, k.ref, 24 * (n + 1), s) ||
       ensure(c, k.cell_start, sizeof(uint32_t) * (kMaxCells + 1), s) ||
       ensure(c, k.cell_end, sizeof(uint32_t) * (kMaxCells + 1), s))
     return -1;
@@ -1174,10 +1163,11 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
   if (ensure(c, k.cand_tmp, sizeof(uint2) * k.cand_cap, s)) return -1;   // released after big rebuilds
   const Grid *gp = k.grid.as<Grid>();
   KtView v = kt_view(c, c->kt_margin);
-  unsigned long long *cc = k.cand_cnt.as<unsigned long long>();
-  unsigned long long *cn = k.cand_n.as<unsigned long long>();
-  GF_CHECK(c, cudaMemsetAsync(cc, 0, 8 * (n + 1), s));
-  GF_CHECK(c, cudaMemsetAsync(cn, 0, 8, s));
+  if (ensure(c, k.counts, sizeof(unsigned long long) * (3 * n + 1), s)) return -1;
+  uint32_t *ucnt = k.cand_cnt.as<uint32_t>();          // per cell-sorted sphere: its hits
+  unsigned long long *uoff = k.counts.as<unsigned long long>();   // their exclusive scan (scratch here)
+  unsigned long long *big_n = k.cand_n.as<unsigned long long>();
+  int64_t small = 0;
   if (n) {
     k_bin_keys<<<grid_for(n), kBlock, 0, s>>>(n, k.c4.as<double>(), c->sph_offr.as<float4>(), gp,
                                              k.bin_key.as<uint32_t>(), k.sph_val.as<uint32_t>());
@@ -1199,38 +1189,67 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
                                                   c->sph_offr.as<float4>(), c->sph_owner.as<uint32_t>(),
                                                   k.sfam.as<uint8_t>(), gp, k.sc.as<double4>(),
                                                   k.sm.as<uint4>(), k.sf.as<float4>());
-    k_cand_ss<<<grid_for(n, 128), 128, 0, s>>>(v, k.sm.as<uint4>(), k.sf.as<float4>(), reach, cc,
-                                               k.cand_tmp.as<uint2>(), cn, (unsigned long long)k.cand_cap);
-    if (c->n_big)
+    // count, scan, fill: every thread writes its own hits at its own offset
+    k_cand_ss<false><<<grid_for(n, 128), 128, 0, s>>>(v, k.sm.as<uint4>(), k.sf.as<float4>(), reach, ucnt,
+                                                      nullptr, nullptr);
+    GF_CHECK(c, cudaMemsetAsync(ucnt + n, 0, sizeof(uint32_t), s));
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp, ucnt, uoff, int(n + 1), s);
+    if (ensure(c, k.cub_tmp, tmp + 16, s, false)) return -1;
+    GF_CHECK(c, cub::DeviceScan::ExclusiveSum(k.cub_tmp.p, tmp, ucnt, uoff, int(n + 1), s));
+    GF_CHECK(c, cudaMemcpyAsync(&reinterpret_cast<Status *>(c->h_status)->cand_total, uoff + n, 8,
+                                cudaMemcpyDeviceToHost, s));
+    GF_CHECK(c, cudaStreamSynchronize(s));
+    small = int64_t(reinterpret_cast<Status *>(c->h_status)->cand_total);
+  }
+  // room for the small-sphere hits plus the big spheres' (grown and redone on
+  // overflow); the key sort needs a second buffer of the same size
+  int64_t big_cap = k.big_cap > 0 ? k.big_cap : (c->n_big ? std::max<int64_t>(4096 * c->n_big, 65536) : 0);
+  for (;;) {
+    const int64_t need = small + big_cap + 1;
+    if (need > k.cand_cap) {
+      const int64_t cap = need + need / 10 + 4096;
+      if (ensure(c, k.cand_tmp, sizeof(uint2) * cap, s) || ensure(c, k.cand, sizeof(uint2) * cap, s)) return -1;
+      k.cand_cap = cap;
+    }
+    unsigned long long *keys = reinterpret_cast<unsigned long long *>(k.cand_tmp.p);
+    if (n)
+      k_cand_ss<true><<<grid_for(n, 128), 128, 0, s>>>(v, k.sm.as<uint4>(), k.sf.as<float4>(), reach, nullptr,
+                                                       uoff, keys);
+    int64_t nbig = 0;
+    if (c->n_big) {
+      GF_CHECK(c, cudaMemsetAsync(big_n, 0, 8, s));
       k_cand_big<<<unsigned(std::min<int64_t>(c->n_big, 4096)), 128, 0, s>>>(
-          v, c->big_slots.as<uint32_t>(), c->n_big, k.sc.as<double4>(), k.sm.as<uint4>(), reach, cc,
-          k.cand_tmp.as<uint2>(), cn, (unsigned long long)k.cand_cap);
+          v, c->big_slots.as<uint32_t>(), c->n_big, k.sc.as<double4>(), k.sm.as<uint4>(), reach, keys + small,
+          big_n, (unsigned long long)big_cap);
+      unsigned long long h = 0;
+      GF_CHECK(c, cudaMemcpyAsync(&h, big_n, 8, cudaMemcpyDeviceToHost, s));
+      GF_CHECK(c, cudaStreamSynchronize(s));
+      nbig = int64_t(h);
+    }
+    if (nbig <= big_cap) {
+      k.n_cand = small + nbig;
+      break;
+    }
+    big_cap = nbig + nbig / 4 + 4096;   // the big spheres' pass overflowed: grow, redo the fill
   }
-  size_t tmp = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tmp, cc, k.cand_seg.as<unsigned long long>(), int(n + 1), s);
-  if (ensure(c, k.cub_tmp, tmp + 16, s, false)) return -1;
-  GF_CHECK(c, cub::DeviceScan::ExclusiveSum(k.cub_tmp.p, tmp, cc, k.cand_seg.as<unsigned long long>(),
-                                            int(n + 1), s));
-  // a rebuild is rare: check the candidate total right away and grow on overflow
-  GF_CHECK(c, cudaMemcpyAsync(&reinterpret_cast<Status *>(c->h_status)->cand_total, cn, 8,
-                              cudaMemcpyDeviceToHost, s));
-  GF_CHECK(c, cudaStreamSynchronize(s));
-  const int64_t total = int64_t(reinterpret_cast<Status *>(c->h_status)->cand_total);
-  if (total > k.cand_cap) {
-    int64_t cap = total + total / 10 + 4096;
-    if (ensure(c, k.cand_tmp, sizeof(uint2) * cap, s) || ensure(c, k.cand, sizeof(uint2) * cap, s)) return -1;
-    k.cand_cap = cap;
-    return rebuild_candidates(c, s);
+  k.big_cap = big_cap;
+  const int64_t total = k.n_cand;
+  if (total) {
+    // (a << 32 | b) keys into (a, b) order, then unpacked into the list
+    size_t tmp = 0;
+    cub::DoubleBuffer<unsigned long long> kb(reinterpret_cast<unsigned long long *>(k.cand_tmp.p),
+                                             reinterpret_cast<unsigned long long *>(k.cand.p));
+    int hi_bit = 33;
+    while ((int64_t(1) << (hi_bit - 32)) < n) ++hi_bit;
+    cub::DeviceRadixSort::SortKeys(nullptr, tmp, kb, int(total), 0, hi_bit, s);
+    if (ensure(c, k.cub_tmp, tmp + 16, s, false)) return -1;
+    GF_CHECK(c, cub::DeviceRadixSort::SortKeys(k.cub_tmp.p, tmp, kb, int(total), 0, hi_bit, s));
+    if (kb.Current() == reinterpret_cast<unsigned long long *>(k.cand.p)) std::swap(k.cand, k.cand_tmp);
+    // sorted keys now in cand_tmp; the (a, b) list goes to cand
+    k_cand_unpack<<<unsigned(std::min<int64_t>((total + 255) / 256, 148 * 16)), 256, 0, s>>>(
+        total, reinterpret_cast<const unsigned long long *>(k.cand_tmp.p), k.cand.as<uint2>());
   }
-  k.n_cand = total;
-  if (n) {
-    GF_CHECK(c, cudaMemsetAsync(k.cursor.p, 0, 4 * n, s));
-    k_place_cand<<<1184, 256, 0, s>>>(cn, k.cand_tmp.as<uint2>(), k.cand_seg.as<unsigned long long>(),
-                                      k.cursor.as<unsigned>(), k.cand.as<uint2>(),
-                                      (unsigned long long)k.cand_cap);
-    k_sort_seg<<<grid_for(n), kBlock, 0, s>>>(n, k.cand_seg.as<unsigned long long>(), k.cand.as<uint2>());
-    k_copy_ref<<<grid_for(n), kBlock, 0, s>>>(n, k.c4.as<double4>(), k.ref.as<double>());
-  }
+  if (n) k_copy_ref<<<grid_for(n), kBlock, 0, s>>>(n, k.c4.as<double4>(), k.ref.as<double>());
   // sphere-analytic candidates for the same skin, while the world is static
   k.sa_world_version = ~0ull;
   if (n && c->n_ana && !c->world_moving) {
@@ -1256,7 +1275,7 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
   if (n >= (int64_t(1) << 24)) {
     GF_CHECK(c, cudaStreamSynchronize(s));
     for (DBuf *b : {&k.bin_key, &k.bin_key_alt, &k.sph_val, &k.sph_val_alt, &k.sc, &k.sm, &k.sf, &k.cand_cnt,
-                    &k.cand_seg, &k.cand_tmp})
+                    &k.cand_tmp})
       b->release();
   }
   k.cand_valid = true;
@@ -1294,7 +1313,10 @@ int kt_count(Ctx *c, cudaStream_t s, bool force_rebuild) {
   const int64_t ss_guess = k.last_ss > 0 ? k.last_ss + k.last_ss / 8 + 1024 : (3 * k.n_cand) / 4 + 1024;
   const int64_t need = std::min<int64_t>(k.n_cand, std::max<int64_t>(ss_guess, k.ss_need)) + k.tmp_cap + 1;
   if (need > out.cap) {
-    int64_t cap = need + need / 32 + 1024;
+    // 25% growth room: the two contact arrays alternate, and a reallocation
+    // synchronises the device, so a slowly growing pair count must not
+    // trigger one per detection
+    int64_t cap = need + need / 4 + 1024;
     if (ensure(c, out.ids, sizeof(uint2) * cap, s) || ensure(c, out.wild, sizeof(float) * c->wild_w * cap, s) ||
         ensure(c, out.old_pos, sizeof(uint32_t) * cap, s))
       return -1;

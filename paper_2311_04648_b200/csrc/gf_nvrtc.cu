@@ -24,7 +24,7 @@ namespace {
 // loaded through the runtime's library API (no libcuda link dependency)
 struct UserModule {
   cudaLibrary_t lib = nullptr;
-  cudaKernel_t f64 = nullptr, f32 = nullptr;
+  cudaKernel_t f64 = nullptr, f32 = nullptr, ss = nullptr, walls = nullptr;
 };
 std::map<std::string, UserModule> g_cache;
 
@@ -48,6 +48,13 @@ extern "C" __global__ void __launch_bounds__(128) gf_user_forces_f64(gf::DtView 
 }
 extern "C" __global__ void __launch_bounds__(128) gf_user_forces_f32(gf::DtView v, double ts, double t) {
   gf::forces_loop<float, GfUserCore>(v, ts, t, nullptr, nullptr);
+}
+// throughput build: the fused sphere-sphere loop + the wall kinds
+extern "C" __global__ void __launch_bounds__(256) gf_user_contacts_ss(gf::DtView v, double ts, double t) {
+  gf::user_ss_loop<GfUserCore>(v, ts, t);
+}
+extern "C" __global__ void __launch_bounds__(128) gf_user_walls_f32(gf::DtView v, double ts, double t) {
+  gf::user_walls_loop<float, GfUserCore>(v, ts, t);
 }
 )";
 }  // namespace
@@ -89,7 +96,9 @@ int set_user_model(Ctx *c, const char *src, const char *include_dir, std::string
     UserModule um;
     if (cudaLibraryLoadData(&um.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) != cudaSuccess ||
         cudaLibraryGetKernel(&um.f64, um.lib, "gf_user_forces_f64") != cudaSuccess ||
-        cudaLibraryGetKernel(&um.f32, um.lib, "gf_user_forces_f32") != cudaSuccess) {
+        cudaLibraryGetKernel(&um.f32, um.lib, "gf_user_forces_f32") != cudaSuccess ||
+        cudaLibraryGetKernel(&um.ss, um.lib, "gf_user_contacts_ss") != cudaSuccess ||
+        cudaLibraryGetKernel(&um.walls, um.lib, "gf_user_walls_f32") != cudaSuccess) {
       set_err(c, std::string("loading the NVRTC user force module failed: ") +
                      cudaGetErrorString(cudaGetLastError()));
       return -1;
@@ -98,6 +107,8 @@ int set_user_model(Ctx *c, const char *src, const char *include_dir, std::string
   }
   c->user_fn_f64 = reinterpret_cast<void *>(it->second.f64);
   c->user_fn_f32 = reinterpret_cast<void *>(it->second.f32);
+  c->user_fn_ss = reinterpret_cast<void *>(it->second.ss);
+  c->user_fn_walls = reinterpret_cast<void *>(it->second.walls);
   c->user_model = true;
   return 0;
 }
@@ -123,9 +134,21 @@ int nvrtc_compile_check(const char *src, const char *include_dir, std::string &l
 }
 
 int launch_user_forces(Ctx *c, const DtView &v, double ts, double sim_time, cudaStream_t s) {
-  cudaKernel_t fn = reinterpret_cast<cudaKernel_t>(c->f32_state ? c->user_fn_f32 : c->user_fn_f64);
   DtView vv = v;
   void *args[] = {&vv, &ts, &sim_time};
+  if (c->f32_state && v.sph.kin && c->user_fn_ss) {
+    // throughput build: the fused sphere-sphere loop, then the wall kinds
+    cudaError_t e = cudaLaunchKernel(reinterpret_cast<const void *>(c->user_fn_ss), dim3(148 * 4), dim3(256), args,
+                                     0, s);
+    if (e == cudaSuccess)
+      e = cudaLaunchKernel(reinterpret_cast<const void *>(c->user_fn_walls), dim3(148 * 4), dim3(128), args, 0, s);
+    if (e != cudaSuccess) {
+      set_err(c, std::string("launching the NVRTC user force kernels failed: ") + cudaGetErrorString(e));
+      return -1;
+    }
+    return 0;
+  }
+  cudaKernel_t fn = reinterpret_cast<cudaKernel_t>(c->f32_state ? c->user_fn_f32 : c->user_fn_f64);
   unsigned grid = unsigned(std::min<int64_t>((v.n_acs + 127) / 128, 148 * 16));
   if (grid == 0) grid = 1;
   cudaError_t e = cudaLaunchKernel(reinterpret_cast<const void *>(fn), dim3(grid), dim3(128), args, 0, s);
