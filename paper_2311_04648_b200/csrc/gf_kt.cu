@@ -556,6 +556,53 @@ __global__ void k_sort_seg(int64_t nseg, const unsigned long long *offsets, uint
   if (cnt > 1) sort_segment_y(out, w, cnt);
 }
 
+// the same, with segments longer than kShortSeg (big spheres' candidates)
+// left to k_sort_long: one CTA each, bitonic sort in shared memory
+constexpr unsigned long long kShortSeg = 64;
+constexpr int kLongSeg = 8192;   // longer: insertion sort fallback (correct, slow)
+__global__ void k_sort_seg_short(int64_t nseg, const unsigned long long *offsets, uint2 *out, uint32_t *longs,
+                                 unsigned long long *n_long) {
+  int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= nseg) return;
+  unsigned long long w = offsets[i], cnt = offsets[i + 1] - w;
+  if (cnt > kShortSeg) longs[atomicAdd(n_long, 1ull)] = uint32_t(i);
+  else if (cnt > 1) sort_segment_y(out, w, cnt);
+}
+
+__global__ void __launch_bounds__(1024) k_sort_long(const unsigned long long *offsets, uint2 *out,
+                                                    const uint32_t *longs, const unsigned long long *n_long) {
+  extern __shared__ uint2 sh[];
+  const unsigned long long nl = *n_long;
+  for (unsigned long long li = blockIdx.x; li < nl; li += gridDim.x) {
+    const uint32_t sg = longs[li];
+    const unsigned long long w = offsets[sg], cnt = offsets[sg + 1] - w;
+    if (cnt > (unsigned long long)kLongSeg) {
+      if (threadIdx.x == 0) sort_segment_y(out, w, cnt);
+      __syncthreads();
+      continue;
+    }
+    int p2 = 1;
+    while (p2 < int(cnt)) p2 <<= 1;
+    for (int t = threadIdx.x; t < p2; t += blockDim.x)
+      sh[t] = t < int(cnt) ? out[w + t] : make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
+    __syncthreads();
+    for (int size = 2; size <= p2; size <<= 1)
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int t = threadIdx.x; t < p2; t += blockDim.x) {
+          const int u = t ^ stride;
+          if (u > t) {
+            const bool up = (t & size) == 0;
+            const uint2 x = sh[t], y = sh[u];
+            if ((x.y > y.y) == up) { sh[t] = y; sh[u] = x; }
+          }
+        }
+        __syncthreads();
+      }
+    for (int t = threadIdx.x; t < int(cnt); t += blockDim.x) out[w + t] = sh[t];
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Verlet candidate lists.  A rebuild enumerates every sphere-sphere pair
 // within margin + skin (fp32 test with conservative slack, different owners;
@@ -582,13 +629,13 @@ __global__ void k_disp(int64_t n, const double4 *c4, const double *ref, double l
 // candidate pairs among small spheres: half stencil on the enumeration grid
 // (cell = 2 (r_cut + margin + skin)), one thread per cell-sorted sphere.
 // Two passes over the same loops, no shared counters: kFill = false counts
-// each thread's hits, kFill = true writes them as (a << 32 | b) keys at the
-// thread's exclusive-scan offset (a = lower slot); a key sort then gives the
-// (a, b)-ordered list.
+// each thread's hits, kFill = true writes them as (a, b) (a = lower slot) at
+// the thread's exclusive-scan offset; a sort by a and a per-segment sort by b
+// then give the (a, b)-ordered list.
 template <bool kFill>
 __global__ void __launch_bounds__(128) k_cand_ss(KtView v, const uint4 *sm, const float4 *sf, double reach_m,
                                                  uint32_t *ucnt, const unsigned long long *uoff,
-                                                 unsigned long long *keys) {
+                                                 uint32_t *ka, uint32_t *kb) {
   int64_t u64 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (u64 >= v.sph.n) return;
   const Grid g = *v.grid;
@@ -637,8 +684,9 @@ __global__ void __launch_bounds__(128) k_cand_ss(KtView v, const uint4 *sm, cons
           const uint4 m1 = sm[w];
           if (m1.y != m0.y && dd_keep(v.own.dd, m0.y, m1.y)) {
             if (kFill) {
-              const uint32_t a = min(m0.x, m1.x), b = max(m0.x, m1.x);
-              keys[w_out++] = (static_cast<unsigned long long>(a) << 32) | b;
+              ka[w_out] = min(m0.x, m1.x);
+              kb[w_out] = max(m0.x, m1.x);
+              ++w_out;
             }
             ++hits;
           }
@@ -652,7 +700,7 @@ __global__ void __launch_bounds__(128) k_cand_ss(KtView v, const uint4 *sm, cons
 // candidate pairs involving big spheres (fp64 distance < r_i + r_j + M)
 __global__ void __launch_bounds__(128) k_cand_big(KtView v, const uint32_t *bigs, int64_t n_big,
                                                   const double4 *sc, const uint4 *sm, double reach_m,
-                                                  unsigned long long *keys, unsigned long long *big_n,
+                                                  uint32_t *ka, uint32_t *kb, unsigned long long *big_n,
                                                   unsigned long long cap) {
   const Grid g = *v.grid;
   if (!g.valid) return;
@@ -686,7 +734,7 @@ __global__ void __launch_bounds__(128) k_cand_big(KtView v, const uint32_t *bigs
         if (dx * dx + dy * dy + dz * dz >= rr * rr * (1.0 + 1e-9)) continue;
         const uint32_t a = min(m1.x, B), c = max(m1.x, B);
         const unsigned long long pos = atomicAdd(big_n, 1ull);
-        if (pos < cap) keys[pos] = (static_cast<unsigned long long>(a) << 32) | c;
+        if (pos < cap) { ka[pos] = a; kb[pos] = c; }
       }
     }
     for (int64_t q = threadIdx.x; q < n_big; q += blockDim.x) {
@@ -697,16 +745,22 @@ __global__ void __launch_bounds__(128) k_cand_big(KtView v, const uint32_t *bigs
       const double rr = rB + double(v.sph.offr[j].w) + reach_m;
       if (dx * dx + dy * dy + dz * dz >= rr * rr * (1.0 + 1e-9)) continue;
       const unsigned long long pos = atomicAdd(big_n, 1ull);
-      if (pos < cap) keys[pos] = (static_cast<unsigned long long>(B) << 32) | j;
+      if (pos < cap) { ka[pos] = B; kb[pos] = j; }
     }
   }
 }
 
-// sorted (a << 32 | b) keys -> the (a, b) candidate list
-__global__ void k_cand_unpack(int64_t total, const unsigned long long *keys, uint2 *cand) {
+// candidates sorted by a -> the (a, b) list and each sphere's segment start
+// (the spheres in (previous entry's a, this entry's a] start here)
+__global__ void k_cand_unpack(int64_t total, int64_t n_sph, const uint32_t *ka, const uint32_t *kb, uint2 *cand,
+                              unsigned long long *seg) {
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
-    const unsigned long long k = keys[e];
-    cand[e] = make_uint2(uint32_t(k >> 32), uint32_t(k & 0xFFFFFFFFull));
+    const int64_t a = ka[e];
+    cand[e] = make_uint2(uint32_t(a), kb[e]);
+    const int64_t ap = e > 0 ? int64_t(ka[e - 1]) : -1;
+    for (int64_t sp = ap + 1; sp <= a; ++sp) seg[sp] = (unsigned long long)e;
+    if (e == total - 1)
+      for (int64_t sp = a + 1; sp <= n_sph; ++sp) seg[sp] = (unsigned long long)total;
   }
 }
 
@@ -1191,7 +1245,7 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
                                                   k.sm.as<uint4>(), k.sf.as<float4>());
     // count, scan, fill: every thread writes its own hits at its own offset
     k_cand_ss<false><<<grid_for(n, 128), 128, 0, s>>>(v, k.sm.as<uint4>(), k.sf.as<float4>(), reach, ucnt,
-                                                      nullptr, nullptr);
+                                                      nullptr, nullptr, nullptr);
     GF_CHECK(c, cudaMemsetAsync(ucnt + n, 0, sizeof(uint32_t), s));
     cub::DeviceScan::ExclusiveSum(nullptr, tmp, ucnt, uoff, int(n + 1), s);
     if (ensure(c, k.cub_tmp, tmp + 16, s, false)) return -1;
@@ -1211,16 +1265,17 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
       if (ensure(c, k.cand_tmp, sizeof(uint2) * cap, s) || ensure(c, k.cand, sizeof(uint2) * cap, s)) return -1;
       k.cand_cap = cap;
     }
-    unsigned long long *keys = reinterpret_cast<unsigned long long *>(k.cand_tmp.p);
+    // (a, b) halves of cand_tmp; cand holds the sort's alternate halves
+    uint32_t *ka = k.cand_tmp.as<uint32_t>(), *kb = ka + k.cand_cap;
     if (n)
       k_cand_ss<true><<<grid_for(n, 128), 128, 0, s>>>(v, k.sm.as<uint4>(), k.sf.as<float4>(), reach, nullptr,
-                                                       uoff, keys);
+                                                       uoff, ka, kb);
     int64_t nbig = 0;
     if (c->n_big) {
       GF_CHECK(c, cudaMemsetAsync(big_n, 0, 8, s));
       k_cand_big<<<unsigned(std::min<int64_t>(c->n_big, 4096)), 128, 0, s>>>(
-          v, c->big_slots.as<uint32_t>(), c->n_big, k.sc.as<double4>(), k.sm.as<uint4>(), reach, keys + small,
-          big_n, (unsigned long long)big_cap);
+          v, c->big_slots.as<uint32_t>(), c->n_big, k.sc.as<double4>(), k.sm.as<uint4>(), reach, ka + small,
+          kb + small, big_n, (unsigned long long)big_cap);
       unsigned long long h = 0;
       GF_CHECK(c, cudaMemcpyAsync(&h, big_n, 8, cudaMemcpyDeviceToHost, s));
       GF_CHECK(c, cudaStreamSynchronize(s));
@@ -1234,20 +1289,36 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
   }
   k.big_cap = big_cap;
   const int64_t total = k.n_cand;
+  if (ensure(c, k.cand_seg, 8 * (n + 1), s)) return -1;
   if (total) {
-    // (a << 32 | b) keys into (a, b) order, then unpacked into the list
+    // sort by a (only as many bits as slots need; b rides along), then each
+    // sphere's segment by b
+    const int64_t cap = k.cand_cap;
+    uint32_t *ka = k.cand_tmp.as<uint32_t>(), *kb = ka + cap;
+    uint32_t *ka2 = k.cand.as<uint32_t>(), *kb2 = ka2 + cap;
+    cub::DoubleBuffer<uint32_t> dk(ka, ka2), dv(kb, kb2);
+    int bits = 1;
+    while ((int64_t(1) << bits) < n) ++bits;
     size_t tmp = 0;
-    cub::DoubleBuffer<unsigned long long> kb(reinterpret_cast<unsigned long long *>(k.cand_tmp.p),
-                                             reinterpret_cast<unsigned long long *>(k.cand.p));
-    int hi_bit = 33;
-    while ((int64_t(1) << (hi_bit - 32)) < n) ++hi_bit;
-    cub::DeviceRadixSort::SortKeys(nullptr, tmp, kb, int(total), 0, hi_bit, s);
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, int(total), 0, bits, s);
     if (ensure(c, k.cub_tmp, tmp + 16, s, false)) return -1;
-    GF_CHECK(c, cub::DeviceRadixSort::SortKeys(k.cub_tmp.p, tmp, kb, int(total), 0, hi_bit, s));
-    if (kb.Current() == reinterpret_cast<unsigned long long *>(k.cand.p)) std::swap(k.cand, k.cand_tmp);
-    // sorted keys now in cand_tmp; the (a, b) list goes to cand
+    GF_CHECK(c, cub::DeviceRadixSort::SortPairs(k.cub_tmp.p, tmp, dk, dv, int(total), 0, bits, s));
+    if (dk.Current() == ka2) std::swap(k.cand, k.cand_tmp);   // sorted halves now in cand_tmp
+    const uint32_t *sa = k.cand_tmp.as<uint32_t>(), *sb = sa + cap;
     k_cand_unpack<<<unsigned(std::min<int64_t>((total + 255) / 256, 148 * 16)), 256, 0, s>>>(
-        total, reinterpret_cast<const unsigned long long *>(k.cand_tmp.p), k.cand.as<uint2>());
+        total, n, sa, sb, k.cand.as<uint2>(), k.cand_seg.as<unsigned long long>());
+    if (ensure(c, k.sa_cnt, 4 * (n + 1), s)) return -1;   // the long-segment list (scratch here)
+    GF_CHECK(c, cudaMemsetAsync(big_n, 0, 8, s));
+    k_sort_seg_short<<<grid_for(n), kBlock, 0, s>>>(n, k.cand_seg.as<unsigned long long>(), k.cand.as<uint2>(),
+                                                   k.sa_cnt.as<uint32_t>(), big_n);
+    static bool smem_set = false;
+    if (!smem_set) {
+      GF_CHECK(c, cudaFuncSetAttribute(k_sort_long, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(sizeof(uint2) * kLongSeg)));
+      smem_set = true;
+    }
+    k_sort_long<<<148, 1024, sizeof(uint2) * kLongSeg, s>>>(k.cand_seg.as<unsigned long long>(), k.cand.as<uint2>(),
+                                                            k.sa_cnt.as<uint32_t>(), big_n);
   }
   if (n) k_copy_ref<<<grid_for(n), kBlock, 0, s>>>(n, k.c4.as<double4>(), k.ref.as<double>());
   // sphere-analytic candidates for the same skin, while the world is static
@@ -1275,7 +1346,7 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
   if (n >= (int64_t(1) << 24)) {
     GF_CHECK(c, cudaStreamSynchronize(s));
     for (DBuf *b : {&k.bin_key, &k.bin_key_alt, &k.sph_val, &k.sph_val_alt, &k.sc, &k.sm, &k.sf, &k.cand_cnt,
-                    &k.cand_tmp})
+                    &k.cand_seg, &k.cand_tmp})
       b->release();
   }
   k.cand_valid = true;
