@@ -384,6 +384,8 @@ gf_ctx *gf_create(int device, uint32_t flags) {
   cudaEventCreateWithFlags(&c->ev_count, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->ev_disp, cudaEventDisableTiming);
   if (const char *sf = std::getenv("GF_SKIN_FACTOR")) c->skin_factor = std::atof(sf);
+  if (const char *sb = std::getenv("GF_SKIN_BIG")) c->skin_big_factor = std::atof(sb);
+  if (c->skin_big_factor < c->skin_factor) c->skin_big_factor = c->skin_factor;
   if (const char *sp = std::getenv("GF_SS_SPLIT")) c->ss_split = std::atoi(sp);
   if (const char *pd = std::getenv("GF_PDL")) c->pdl = std::atoi(pd);
   cudaEventCreate(&c->t0);

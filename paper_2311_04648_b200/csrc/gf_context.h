@@ -151,6 +151,7 @@ struct Ctx {
   double kt_margin = 0.0;
   double kt_bin_size = 0.0;  // > 0: explicit bin size (detect_contacts(bin_size=...))
   double skin_factor = 1.0;  // Verlet skin = skin_factor * margin
+  double skin_big_factor = 8.0;  // skin of big spheres (radius > r_cut), >= skin_factor (GF_SKIN_BIG)
   uint64_t world_version = 0;   // bumped whenever mesh / analytic world transforms are recomputed
   int tlist_words = 5;       // words per contact of the touching lists (1 on the fused path)
   int ss_split = 0;          // throughput build: split narrow/force sphere-sphere kernels (GF_SS_SPLIT=1)

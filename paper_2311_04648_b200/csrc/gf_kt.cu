@@ -78,8 +78,10 @@ struct KtView {
 // largest radius (the grid's inputs, broadphase.py:160-186) and -- when
 // candidate lists exist -- whether a sphere moved more than skin / 2 since
 // their rebuild (the k_disp test), in the same pass over the centres
-__global__ void __launch_bounds__(256) k_snapshot(Domain dom, Owners own, Spheres sph, double4 *c4, uint8_t *sfam, unsigned long long *mm,
-                                                  const double *ref, double lim2, int *flag) {
+__global__ void __launch_bounds__(256) k_snapshot(Domain dom, Owners own, Spheres sph, double4 *c4,
+                                                  uint8_t *sfam, unsigned long long *mm,
+                                                  const double *ref, double lim2, double lim2_big, double r_cut,
+                                                  int *flag) {
   double lo[3], hi[3], rmax = 0.0;
 #pragma unroll
   for (int ax = 0; ax < 3; ++ax) {
@@ -99,7 +101,7 @@ __global__ void __launch_bounds__(256) k_snapshot(Domain dom, Owners own, Sphere
     }
     if (ref) {
       const double dx = c.x - ref[3 * k], dy = c.y - ref[3 * k + 1], dz = c.z - ref[3 * k + 2];
-      far = far || dx * dx + dy * dy + dz * dz > lim2;
+      far = far || dx * dx + dy * dy + dz * dz > ((r_cut > 0.0 && c.w > r_cut) ? lim2_big : lim2);
     }
   }
   if (ref && __any_sync(0xffffffffu, far) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
@@ -505,17 +507,20 @@ __device__ __forceinline__ bool sa_candidate(const KtView &v, uint32_t i, uint32
   return gap < double(v.sph.offr[i].w) + reach;
 }
 
-__global__ void k_sa_count(KtView v, double reach, uint32_t *cnt) {
+__global__ void k_sa_count(KtView v, double reach_s, double reach_b, double r_cut, uint32_t *cnt) {
   const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (i >= v.sph.n) return;
+  const double reach = (r_cut > 0.0 && double(v.sph.offr[i].w) > r_cut) ? reach_b : reach_s;   // big: margin + Sb
   uint32_t c = 0;
   for (int64_t k = 0; k < v.n_ana; ++k) c += sa_candidate(v, uint32_t(i), uint32_t(k), reach) ? 1u : 0u;
   cnt[i] = c;
 }
 
-__global__ void k_sa_fill(KtView v, double reach, const unsigned long long *off, uint2 *cand) {
+__global__ void k_sa_fill(KtView v, double reach_s, double reach_b, double r_cut, const unsigned long long *off,
+                          uint2 *cand) {
   const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (i >= v.sph.n) return;
+  const double reach = (r_cut > 0.0 && double(v.sph.offr[i].w) > r_cut) ? reach_b : reach_s;
   unsigned long long w = off[i];
   for (int64_t k = 0; k < v.n_ana; ++k)
     if (sa_candidate(v, uint32_t(i), uint32_t(k), reach)) cand[w++] = make_uint2(uint32_t(i), uint32_t(k));
@@ -615,13 +620,14 @@ __global__ void __launch_bounds__(1024) k_sort_long(const unsigned long long *of
 // ---------------------------------------------------------------------------
 
 // any sphere displaced more than skin / 2 since the rebuild -> flag
-__global__ void k_disp(int64_t n, const double4 *c4, const double *ref, double lim2, int *flag) {
+__global__ void k_disp(int64_t n, const double4 *c4, const double *ref, double lim2, double lim2_big, double r_cut,
+                       int *flag) {
   int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   bool far = false;
   if (i < n) {
     const double4 c = c4[i];
     double dx = c.x - ref[3 * i], dy = c.y - ref[3 * i + 1], dz = c.z - ref[3 * i + 2];
-    far = dx * dx + dy * dy + dz * dz > lim2;
+    far = dx * dx + dy * dy + dz * dz > ((r_cut > 0.0 && c.w > r_cut) ? lim2_big : lim2);
   }
   if (__any_sync(0xffffffffu, far) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
 }
@@ -698,10 +704,14 @@ __global__ void __launch_bounds__(128) k_cand_ss(KtView v, const uint4 *sm, cons
 }
 
 // candidate pairs involving big spheres (fp64 distance < r_i + r_j + M)
+// Big spheres carry their own, larger skin Sb (Ctx::skin_big_factor): a big
+// sphere may move Sb - S/2 before it forces a rebuild (a small one S/2), so
+// big-small pairs are enumerated within margin + Sb and big-big pairs within
+// margin + 2 Sb - S -- the sum of the two displacement limits in each case.
 __global__ void __launch_bounds__(128) k_cand_big(KtView v, const uint32_t *bigs, int64_t n_big,
                                                   const double4 *sc, const uint4 *sm, double reach_m,
-                                                  uint32_t *ka, uint32_t *kb, unsigned long long *big_n,
-                                                  unsigned long long cap) {
+                                                  double reach_bb, uint32_t *ka, uint32_t *kb,
+                                                  unsigned long long *big_n, unsigned long long cap) {
   const Grid g = *v.grid;
   if (!g.valid) return;
   for (int64_t bi = blockIdx.x; bi < n_big; bi += gridDim.x) {
@@ -742,7 +752,7 @@ __global__ void __launch_bounds__(128) k_cand_big(KtView v, const uint32_t *bigs
       if (j <= B || v.sph.owner[j] == oB || !dd_keep(v.own.dd, v.sph.owner[j], oB)) continue;
       const double dx = bx - v.centers[4 * size_t(j)], dy = by - v.centers[4 * size_t(j) + 1],
                    dz = bz - v.centers[4 * size_t(j) + 2];
-      const double rr = rB + double(v.sph.offr[j].w) + reach_m;
+      const double rr = rB + double(v.sph.offr[j].w) + reach_bb;
       if (dx * dx + dy * dy + dz * dz >= rr * rr * (1.0 + 1e-9)) continue;
       const unsigned long long pos = atomicAdd(big_n, 1ull);
       if (pos < cap) { ka[pos] = B; kb[pos] = j; }
@@ -1074,11 +1084,12 @@ int kt_snapshot(Ctx *c, cudaStream_t s, double margin) {
     k_minmax_init<<<1, 32, 0, s>>>(mm);
     if (check) GF_CHECK(c, cudaMemsetAsync(k.flag.p, 0, sizeof(int), s));
   }
-  const double skin = c->skin_factor * margin;
+  const double skin = c->skin_factor * margin, skin_b = c->skin_big_factor * margin;
   if (c->n_sph)
     k_snapshot<<<unsigned(std::min<int64_t>(grid_for(c->n_sph), 148 * 8)), kBlock, 0, s>>>(
         c->dom, owners_view(c), spheres_view(c), k.c4.as<double4>(), k.sfam.as<uint8_t>(),
-        det ? mm : nullptr, check ? k.ref.as<double>() : nullptr, 0.25 * skin * skin, k.flag.as<int>());
+        det ? mm : nullptr, check ? k.ref.as<double>() : nullptr, 0.25 * skin * skin,
+        (skin_b - 0.5 * skin) * (skin_b - 0.5 * skin), c->n_big ? c->r_cut : 0.0, k.flag.as<int>());
   k.snap_det = det;
   k.snap_checked = check;
   if (c->n_tri) {
@@ -1158,7 +1169,10 @@ int kt_begin(Ctx *c, double margin, cudaStream_t s) {
   if (k.cand_valid && n) {
     if (!(snap && k.snap_checked)) {
       GF_CHECK(c, cudaMemsetAsync(flag, 0, sizeof(int), s));
-      k_disp<<<grid_for(n), kBlock, 0, s>>>(n, k.c4.as<double4>(), k.ref.as<double>(), 0.25 * skin * skin, flag);
+      const double skin_b = c->skin_big_factor * margin;
+      k_disp<<<grid_for(n), kBlock, 0, s>>>(n, k.c4.as<double4>(), k.ref.as<double>(), 0.25 * skin * skin,
+                                            (skin_b - 0.5 * skin) * (skin_b - 0.5 * skin),
+                                            c->n_big ? c->r_cut : 0.0, flag);
     }
   } else {
     k_set_int<<<1, 1, 0, s>>>(flag, 1);
@@ -1199,7 +1213,10 @@ int kt_begin(Ctx *c, double margin, cudaStream_t s) {
 static int rebuild_candidates(Ctx *c, cudaStream_t s) {
   KtScratch &k = c->kt;
   const int64_t n = c->n_sph;
-  const double reach = c->kt_margin + c->skin_factor * c->kt_margin;
+  const double skin = c->skin_factor * c->kt_margin, skin_b = c->skin_big_factor * c->kt_margin;
+  const double reach = c->kt_margin + skin;                         // small-small
+  const double reach_big = c->kt_margin + skin_b;                   // big-small
+  const double reach_bb = c->kt_margin + 2.0 * skin_b - skin;       // big-big
   if (ensure(c, k.bin_key, 4 * (n + 1), s) || ensure(c, k.bin_key_alt, 4 * (n + 1), s) ||
       ensure(c, k.sph_val, 4 * (n + 1), s) || ensure(c, k.sph_val_alt, 4 * (n + 1), s) ||
       ensure(c, k.cursor, 4 * (3 * n + 1), s) || ensure(c, k.sc, 32 * (n + 1), s) ||
@@ -1274,8 +1291,8 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
     if (c->n_big) {
       GF_CHECK(c, cudaMemsetAsync(big_n, 0, 8, s));
       k_cand_big<<<unsigned(std::min<int64_t>(c->n_big, 4096)), 128, 0, s>>>(
-          v, c->big_slots.as<uint32_t>(), c->n_big, k.sc.as<double4>(), k.sm.as<uint4>(), reach, ka + small,
-          kb + small, big_n, (unsigned long long)big_cap);
+          v, c->big_slots.as<uint32_t>(), c->n_big, k.sc.as<double4>(), k.sm.as<uint4>(), reach_big,
+          reach_bb, ka + small, kb + small, big_n, (unsigned long long)big_cap);
       unsigned long long h = 0;
       GF_CHECK(c, cudaMemcpyAsync(&h, big_n, 8, cudaMemcpyDeviceToHost, s));
       GF_CHECK(c, cudaStreamSynchronize(s));
@@ -1325,7 +1342,7 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
   k.sa_world_version = ~0ull;
   if (n && c->n_ana && !c->world_moving) {
     if (ensure(c, k.sa_cnt, 4 * (n + 1), s) || ensure(c, k.sa_off, 8 * (n + 1), s)) return -1;
-    k_sa_count<<<grid_for(n), kBlock, 0, s>>>(v, reach, k.sa_cnt.as<uint32_t>());
+    k_sa_count<<<grid_for(n), kBlock, 0, s>>>(v, reach, reach_big, c->n_big ? c->r_cut : 0.0, k.sa_cnt.as<uint32_t>());
     GF_CHECK(c, cudaMemsetAsync(k.sa_cnt.as<uint32_t>() + n, 0, 4, s));
     size_t tb = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tb, k.sa_cnt.as<uint32_t>(), k.sa_off.as<unsigned long long>(), int(n + 1), s);
@@ -1337,7 +1354,8 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
     GF_CHECK(c, cudaStreamSynchronize(s));
     k.n_sa_cand = int64_t(h_tot);
     if (ensure(c, k.sa_cand, sizeof(uint2) * (k.n_sa_cand + 1), s)) return -1;
-    k_sa_fill<<<grid_for(n), kBlock, 0, s>>>(v, reach, k.sa_off.as<unsigned long long>(), k.sa_cand.as<uint2>());
+    k_sa_fill<<<grid_for(n), kBlock, 0, s>>>(v, reach, reach_big, c->n_big ? c->r_cut : 0.0,
+                                             k.sa_off.as<unsigned long long>(), k.sa_cand.as<uint2>());
     k.sa_world_version = c->world_version;
   }
   // at 2^24 spheres and up device memory is the limit: the rebuild-only
