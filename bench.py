@@ -331,7 +331,7 @@ def b200_arm(args):
         if mode == "decomp":   # halo: pack/add forces, pack/unpack(+centres) state per peer; guard word x2
             launches_per_step += 2 + 5 * len(sim._dd.peers)
         period, lag, _ = schedule(sim)
-        kt_launches = 22
+        kt_launches = 14   # snapshot, grid, filter, compaction, scans, wall pairs, fill, history gather
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
