@@ -93,19 +93,32 @@ __host__ __device__ inline bool dd_keep(const uint32_t *dd, uint32_t oa, uint32_
 // Per-sphere kinematics record of the throughput build, written wherever the
 // sphere centres are (integrator, refresh, halo unpack) so the contact kernel
 // reaches everything it needs one load after the contact list, with no
-// further dependent loads:
-//   v  = owner linear velocity,                  v.w = owner mass (float)
-//   w  = owner angular velocity (global frame),  w.w = fixed-point force scale
-//   r  = centre minus owner position,            r.w = fixed-point torque scale
-//   id = (owner, material, flags, -); flags bit 0 = passive owner.
-// The scales are the owner template's tpl_scale (float-exact by
-// construction, gf_context.cu update_fixed_scales); 0 = boundary owner,
-// summed with fp64 atomics.
+// further dependent loads -- 48 B, three 16-byte loads:
+//   v = owner linear velocity,                  v.w = owner mass (float)
+//   w = owner angular velocity (global frame),  w.w = owner id (bits)
+//   r = centre minus owner position,            r.w = packed (bits): force-scale
+//       exponent (bits 24-31), torque-scale exponent (16-23), material (8-15),
+//       flags (0-7; bit 0 = passive owner)
+// The fixed-point scales are the owner template's tpl_scale, powers of two by
+// construction (gf_context.cu update_fixed_scales), stored as exponents;
+// kKinNoScale = boundary owner (scale 0), summed with fp64 atomics.
 constexpr uint32_t kKinPassive = 1u;
+constexpr int kKinNoScale = -128;
 struct SphKin {
   float4 v, w, r;
-  uint4 id;
 };
+__device__ __forceinline__ uint32_t kin_owner(const SphKin &k) { return __float_as_uint(k.w.w); }
+__device__ __forceinline__ uint32_t kin_mat(const SphKin &k) { return (__float_as_uint(k.r.w) >> 8) & 0xFFu; }
+__device__ __forceinline__ uint32_t kin_flags(const SphKin &k) { return __float_as_uint(k.r.w) & 0xFFu; }
+__device__ __forceinline__ double kin_exp2(int e) {   // 2^e exactly, 0 for kKinNoScale
+  return e == kKinNoScale ? 0.0 : __longlong_as_double((long long)(1023 + e) << 52);
+}
+__device__ __forceinline__ double kin_fscale(const SphKin &k) {
+  return kin_exp2(int((signed char)(__float_as_uint(k.r.w) >> 24)));
+}
+__device__ __forceinline__ double kin_tscale(const SphKin &k) {
+  return kin_exp2(int((signed char)((__float_as_uint(k.r.w) >> 16) & 0xFFu)));
+}
 
 struct Spheres {
   int64_t n;
@@ -235,11 +248,14 @@ __device__ __forceinline__ void write_kin(const Spheres &sph, uint32_t k, uint32
        r[2]);
   qrot(double(q.x), double(q.y), double(q.z), double(q.w), double(av.x), double(av.y), double(av.z), w[0], w[1],
        w[2]);
+  // power-of-two scales -> their exponents (ilogb is exact on powers of two)
+  const int ef = scale.x > 0.0 ? ilogb(scale.x) : kKinNoScale, et = scale.y > 0.0 ? ilogb(scale.y) : kKinNoScale;
+  const uint32_t packed = ((uint32_t(ef) & 0xFFu) << 24) | ((uint32_t(et) & 0xFFu) << 16) |
+                          (uint32_t(sph.mat[k]) << 8) | (flags & 0xFFu);
   SphKin kr;
   kr.v = make_float4(lv.x, lv.y, lv.z, mass);
-  kr.w = make_float4(float(w[0]), float(w[1]), float(w[2]), float(scale.x));
-  kr.r = make_float4(float(r[0]), float(r[1]), float(r[2]), float(scale.y));
-  kr.id = make_uint4(o, sph.mat[k], flags, 0u);
+  kr.w = make_float4(float(w[0]), float(w[1]), float(w[2]), __uint_as_float(o));
+  kr.r = make_float4(float(r[0]), float(r[1]), float(r[2]), __uint_as_float(packed));
   sph.kin[k] = kr;
 }
 

@@ -164,9 +164,11 @@ static int update_fixed_scales(Ctx *c, double h, double v_err, const double *g) 
     // powers of two: float-exact (the contact kernel reads them from the fp32
     // kinematics record) and exactly invertible (the integrator multiplies by
     // the reciprocal)
-    const double sf = std::ldexp(1.0, int(std::floor(std::log2(std::ldexp(1.0, 50) / (64.0 * m * rate)))));
+    // (exponents within [-127, 127]: the kinematics records store them in 8 bits)
+    auto pow2 = [](double x) { return std::ldexp(1.0, std::min(127, std::max(-127, int(std::floor(std::log2(x)))))); };
+    const double sf = pow2(std::ldexp(1.0, 50) / (64.0 * m * rate));
     sc[2 * t] = sf;
-    sc[2 * t + 1] = std::ldexp(1.0, int(std::floor(std::log2(sf / lever))));
+    sc[2 * t + 1] = pow2(sf / lever);
   }
   if (!c->h_tpl_mass.empty())
     GF_CHECK(c, cudaMemcpy(c->tpl_scale.p, sc.data(), 16 * c->h_tpl_mass.size(), cudaMemcpyHostToDevice));

@@ -452,9 +452,9 @@ __device__ __forceinline__ void force_entry(const DtView &v, uint32_t k, double 
 // fixed-point words are summed in registers (exact) and added by the run's
 // head lane; boundary owners (scale 0) take fp64 atomics.  Every lane of the
 // warp must call it; `out` = force (3), `ta` = torque on A (3).
-__device__ __forceinline__ void a_side_sums(const DtView &v, bool use_a, uint32_t oa, float sa_f, float sa_t,
+__device__ __forceinline__ void a_side_sums(const DtView &v, bool use_a, uint32_t oa, double sa_f, double sa_t,
                                             const float *out, const float *ta, int lane) {
-  const bool fixed_a = use_a && sa_f > 0.f;
+  const bool fixed_a = use_a && sa_f > 0.0;
   if (use_a && !fixed_a) {   // boundary owner: fp64 atomics, not aggregated
     unsigned long long *fa = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(oa));
     for (int q = 0; q < 3; ++q) {
@@ -475,8 +475,8 @@ __device__ __forceinline__ void a_side_sums(const DtView &v, bool use_a, uint32_
   long long acc[6];
 #pragma unroll
   for (int q = 0; q < 3; ++q) {
-    acc[q] = fixed_a ? __double2ll_rn(double(out[q]) * double(sa_f)) : 0ll;
-    acc[3 + q] = fixed_a ? __double2ll_rn(double(ta[q]) * double(sa_t)) : 0ll;
+    acc[q] = fixed_a ? __double2ll_rn(double(out[q]) * sa_f) : 0ll;
+    acc[3 + q] = fixed_a ? __double2ll_rn(double(ta[q]) * sa_t) : 0ll;
   }
   for (unsigned off = 1; off < maxrun; off <<= 1) {
 #pragma unroll
@@ -512,7 +512,7 @@ __device__ __forceinline__ void user_ss_loop(const DtView &v, double ts, double 
     float out[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     float ta[3] = {0.f, 0.f, 0.f};
     uint32_t oa = 0xFFFFFFFFu;
-    float sa_f = 0.f, sa_t = 0.f;
+    double sa_f = 0.0, sa_t = 0.0;
     bool use_a = false;
     if (k < n_ss) {
       const uint2 id = v.ids[k];
@@ -548,7 +548,7 @@ __device__ __forceinline__ void user_ss_loop(const DtView &v, double ts, double 
       const double ma = ka.v.w, mb = kb.v.w;
       arg.mass_eff = (ma * mb) / (ma + mb);
       arg.ra = cA.w; arg.rb = cB.w;
-      arg.mat_a = int(ka.id.y); arg.mat_b = int(kb.id.y);
+      arg.mat_a = int(kin_mat(ka)); arg.mat_b = int(kin_mat(kb));
       arg.pair = v.mat.pair; arg.n_mat = v.mat.n_mat;
       arg.wild = v.wild + size_t(v.W) * k;
       arg.M = &v.mat;
@@ -559,9 +559,9 @@ __device__ __forceinline__ void user_ss_loop(const DtView &v, double ts, double 
         const double tx = o6[0] + o6[3], ty = o6[1] + o6[4], tz = o6[2] + o6[5];
         ta[0] = float(ray * tz - raz * ty); ta[1] = float(raz * tx - rax * tz); ta[2] = float(rax * ty - ray * tx);
         const double tb[3] = {rby * tz - rbz * ty, rbz * tx - rbx * tz, rbx * ty - rby * tx};
-        if (v.acc_all || !(kb.id.z & kKinPassive)) {
-          const double sbf = kb.w.w, sbt = kb.r.w;
-          unsigned long long *fb = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(kb.id.x));
+        if (v.acc_all || !(kin_flags(kb) & kKinPassive)) {
+          const double sbf = kin_fscale(kb), sbt = kin_tscale(kb);
+          unsigned long long *fb = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(kin_owner(kb)));
           for (int q = 0; q < 3; ++q) {
             if (sbf > 0.0) {
               atomicAdd(fb + q, (unsigned long long)__double2ll_rn(-o6[q] * sbf));
@@ -572,10 +572,10 @@ __device__ __forceinline__ void user_ss_loop(const DtView &v, double ts, double 
             }
           }
         }
-        oa = ka.id.x;
-        use_a = v.acc_all || !(ka.id.z & kKinPassive);
-        sa_f = ka.w.w;
-        sa_t = ka.r.w;
+        oa = kin_owner(ka);
+        use_a = v.acc_all || !(kin_flags(ka) & kKinPassive);
+        sa_f = kin_fscale(ka);
+        sa_t = kin_tscale(ka);
       }
     }
     a_side_sums(v, use_a, oa, sa_f, sa_t, out, ta, lane);

@@ -232,7 +232,7 @@ __device__ __forceinline__ void ss_force_warp(const DtView &v, bool live, uint32
   float out[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   float ta[3] = {0.f, 0.f, 0.f};
   uint32_t oa = 0xFFFFFFFFu;
-  float sa_f = 0.f, sa_t = 0.f;
+  double sa_f = 0.0, sa_t = 0.0;
   bool use_a = false;
   if (live) {
     // one load round: kinematics records (mass, scales, flags included) and
@@ -247,8 +247,8 @@ __device__ __forceinline__ void ss_force_warp(const DtView &v, bool live, uint32
       const float inv = 1.f / g.d;
       bx = g.dx * inv; by = g.dy * inv; bz = g.dz * inv;
     }
-    oa = ka.id.x;
-    const uint32_t ob = kb.id.x;
+    oa = kin_owner(ka);
+    const uint32_t ob = kin_owner(kb);
     // contact point p = cA - b (ra - depth / 2); lever arms p - pos_a, p - pos_b
     const float ha = g.ra - 0.5f * depth;
     const float rax = ka.r.x - bx * ha, ray = ka.r.y - by * ha, raz = ka.r.z - bz * ha;
@@ -262,7 +262,7 @@ __device__ __forceinline__ void ss_force_warp(const DtView &v, bool live, uint32
     const float vz = (ka.v.z + rotaz) - (kb.v.z + rotbz);
     const double ma = ka.v.w, mb = kb.v.w;
     const float mass_eff = float((ma * mb) / (ma + mb));
-    const int ab = int(ka.id.y) * nm + int(kb.id.y);
+    const int ab = int(kin_mat(ka)) * nm + int(kin_mat(kb));
     float e_cnt, g_cnt, mu, crr, beta;
     if (smem) {
       e_cnt = s_mat[0][ab]; g_cnt = s_mat[1][ab]; mu = s_mat[2][ab]; crr = s_mat[3][ab]; beta = s_mat[4][ab];
@@ -278,8 +278,8 @@ __device__ __forceinline__ void ss_force_warp(const DtView &v, bool live, uint32
     ta[0] = ray * tz - raz * ty; ta[1] = raz * tx - rax * tz; ta[2] = rax * ty - ray * tx;
     const float tb[3] = {rby * tz - rbz * ty, rbz * tx - rbx * tz, rbx * ty - rby * tx};
     // B side: one atomic per word (B owners are scattered)
-    if (v.acc_all || !(kb.id.z & kKinPassive)) {
-      const double sbf = kb.w.w, sbt = kb.r.w;
+    if (v.acc_all || !(kin_flags(kb) & kKinPassive)) {
+      const double sbf = kin_fscale(kb), sbt = kin_tscale(kb);
       unsigned long long *fb = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(ob));
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
@@ -292,9 +292,9 @@ __device__ __forceinline__ void ss_force_warp(const DtView &v, bool live, uint32
         }
       }
     }
-    use_a = v.acc_all || !(ka.id.z & kKinPassive);
-    sa_f = ka.w.w;
-    sa_t = ka.r.w;
+    use_a = v.acc_all || !(kin_flags(ka) & kKinPassive);
+    sa_f = kin_fscale(ka);
+    sa_t = kin_tscale(ka);
   }
   a_side_sums(v, use_a, oa, sa_f, sa_t, out, ta, lane);
 }
