@@ -50,11 +50,20 @@ int ensure(Ctx *c, DBuf &b, size_t bytes, cudaStream_t s, bool keep) {
                    cudaGetErrorString(e));
     return -1;
   }
-  if (keep && b.p && b.bytes) cudaMemcpy(p, b.p, b.bytes, cudaMemcpyDeviceToDevice);
+  if (keep && b.p && b.bytes) {
+    cudaMemcpyAsync(p, b.p, b.bytes, cudaMemcpyDeviceToDevice, s);
+    cudaStreamSynchronize(s);
+  }
   if (b.p) cudaFree(b.p);
   b.p = p;
   b.bytes = nb;
-  (void)s;
+  return 0;
+}
+
+int h2d(Ctx *c, void *dst, const void *src, size_t bytes, cudaStream_t s) {
+  if (!bytes) return 0;
+  GF_CHECK(c, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+  GF_CHECK(c, cudaStreamSynchronize(s));
   return 0;
 }
 
@@ -171,7 +180,7 @@ static int update_fixed_scales(Ctx *c, double h, double v_err, const double *g) 
     sc[2 * t + 1] = pow2(sf / lever);
   }
   if (!c->h_tpl_mass.empty())
-    GF_CHECK(c, cudaMemcpy(c->tpl_scale.p, sc.data(), 16 * c->h_tpl_mass.size(), cudaMemcpyHostToDevice));
+    if (h2d(c, c->tpl_scale.p, sc.data(), 16 * c->h_tpl_mass.size(), c->s_dt)) return -1;
   c->fx_h = h;
   c->fx_verr = v_err;
   // the kinematics records carry the scales
@@ -310,7 +319,7 @@ static int set_split(Ctx *c, const float *radii, int64_t stride, int64_t n) {
   c->r_cut = rc;
   c->n_big = int64_t(big.size());
   if (ensure(c, c->big_slots, 4 * (big.size() + 1), c->s_dt)) return -1;
-  if (!big.empty()) GF_CHECK(c, cudaMemcpy(c->big_slots.p, big.data(), 4 * big.size(), cudaMemcpyHostToDevice));
+  if (!big.empty()) if (h2d(c, c->big_slots.p, big.data(), 4 * big.size(), c->s_dt)) return -1;
   return 0;
 }
 
@@ -624,7 +633,7 @@ int gf_set_owner_families(gf_ctx *ctx, const uint8_t *family) {
   std::vector<uint32_t> meta(n);
   GF_CHECK(c, cudaMemcpy(meta.data(), c->meta.p, 4 * n, cudaMemcpyDeviceToHost));
   for (int64_t i = 0; i < n; ++i) meta[i] = (uint32_t(family[i]) << 24) | (meta[i] & 0xFFFFFFu);
-  GF_CHECK(c, cudaMemcpy(c->meta.p, meta.data(), 4 * n, cudaMemcpyHostToDevice));
+  if (h2d(c, c->meta.p, meta.data(), 4 * n, c->s_dt)) return -1;
   world_moving_update(c);
   return 0;
 }
@@ -641,7 +650,7 @@ int gf_set_external_loads(gf_ctx *ctx, const double *force, const double *torque
       if (force) e[6 * i + a] = force[3 * i + a];
       if (torque) e[6 * i + 3 + a] = torque[3 * i + a];
     }
-  GF_CHECK(c, cudaMemcpy(c->ext.p, e.data(), 48 * n, cudaMemcpyHostToDevice));
+  if (h2d(c, c->ext.p, e.data(), 48 * n, c->s_dt)) return -1;
   c->has_ext = true;
   return 0;
 }
@@ -664,13 +673,13 @@ static int upload_u32(Ctx *c, DBuf &b, const int64_t *src, int64_t n) {
   std::vector<uint32_t> v(n);
   for (int64_t i = 0; i < n; ++i) v[i] = uint32_t(src[i]);
   if (ensure(c, b, 4 * (n + 1), c->s_dt)) return -1;
-  if (n) GF_CHECK(c, cudaMemcpy(b.p, v.data(), 4 * n, cudaMemcpyHostToDevice));
+  if (n && h2d(c, b.p, v.data(), 4 * n, c->s_dt)) return -1;
   return 0;
 }
 
 static int upload_raw(Ctx *c, DBuf &b, const void *src, size_t bytes) {
   if (ensure(c, b, bytes + 16, c->s_dt)) return -1;
-  if (bytes) GF_CHECK(c, cudaMemcpy(b.p, src, bytes, cudaMemcpyHostToDevice));
+  if (bytes && h2d(c, b.p, src, bytes, c->s_dt)) return -1;
   return 0;
 }
 
@@ -805,9 +814,12 @@ int gf_set_acs(gf_ctx *ctx, int64_t n, const uint8_t *kind, const int64_t *slot_
     ids[2 * k + 1] = uint32_t(slot_b[k]) | (uint32_t(kind[k]) << kKindShift);
   }
   if (n) {
-    GF_CHECK(c, cudaMemcpy(c->acs.ids.p, ids.data(), 8 * n, cudaMemcpyHostToDevice));
-    if (wild) GF_CHECK(c, cudaMemcpy(c->acs.wild.p, wild, 4 * W * n, cudaMemcpyHostToDevice));
-    else GF_CHECK(c, cudaMemset(c->acs.wild.p, 0, 4 * W * n));
+    if (h2d(c, c->acs.ids.p, ids.data(), 8 * n, c->s_dt)) return -1;
+    if (wild) {
+      if (h2d(c, c->acs.wild.p, wild, 4 * W * n, c->s_dt)) return -1;
+    } else {
+      GF_CHECK(c, cudaMemsetAsync(c->acs.wild.p, 0, 4 * W * n, c->s_dt));
+    }
   }
   if (build_segments(c, c->acs, c->s_dt) || build_incidence(c, c->s_dt)) return -1;
   GF_CHECK(c, cudaStreamSynchronize(c->s_dt));
@@ -1046,7 +1058,7 @@ int gf_step_forces(gf_ctx *ctx, int64_t i) {
     trace_mark(c, "dt_snapshot_end", s, c->s_dt);
     if (kt_begin(c, p->margin, c->s_kt)) return -1;
     GF_CHECK(c, cudaEventRecord(c->ev_disp, c->s_kt));
-    trace_mark(c, "kt_phaseA_end", s, c->s_kt);
+      trace_mark(c, "kt_phaseA_end", s, c->s_kt);
     c->kt_phase = 1;
     c->next_pending = true;
     c->fill_done = false;
@@ -1172,7 +1184,7 @@ int gf_set_decomposition(gf_ctx *ctx, const uint32_t *dd, double lever_max, int 
     }
     if (ensure(c, c->dd, 4 * (c->n_owner + 1), c->s_dt)) return -1;
     if (axis < 0 || axis > 2) { c->err = "decomposition axis must be 0, 1 or 2"; return -1; }
-    GF_CHECK(c, cudaMemcpy(c->dd.p, dd, 4 * c->n_owner, cudaMemcpyHostToDevice));
+    if (h2d(c, c->dd.p, dd, 4 * c->n_owner, c->s_dt)) return -1;
     // partition-time axis coordinate of every owner (device-side decode)
     if (ensure(c, c->dd_x0, 8 * (c->n_owner + 1), c->s_dt)) return -1;
     if (halo_axis_coords(c, axis, c->dd_x0.as<double>(), c->s_dt)) return -1;

@@ -204,6 +204,10 @@ constexpr int64_t kMaxCells = (int64_t(1) << 24) - 1;  // enumeration-grid cell 
 
 // helpers implemented in gf_context.cu
 int ensure(Ctx *c, DBuf &b, size_t bytes, cudaStream_t s, bool keep = false);
+// host -> device copy ordered on stream s and complete on return: the context's
+// streams are non-blocking, so a legacy-stream cudaMemcpy is not ordered
+// with kernels launched on them afterwards (its DMA may land after they read)
+int h2d(Ctx *c, void *dst, const void *src, size_t bytes, cudaStream_t s);
 void set_err(Ctx *c, const std::string &msg);
 #define GF_CHECK(c, call)                                                      \
   do {                                                                         \

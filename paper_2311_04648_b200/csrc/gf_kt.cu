@@ -1567,11 +1567,11 @@ int merge_host(Ctx *c, int64_t n_old, const uint32_t *old_ids, const float *old_
       ensure(c, wa, 4 * W * (n_old + 1), s) || ensure(c, wb, 4 * W * (n_new + 1), s))
     return -1;
   if (n_old) {
-    GF_CHECK(c, cudaMemcpy(a.p, old_ids, 8 * n_old, cudaMemcpyHostToDevice));
-    GF_CHECK(c, cudaMemcpy(wa.p, old_wild, 4 * W * n_old, cudaMemcpyHostToDevice));
+    if (h2d(c, a.p, old_ids, 8 * n_old, s)) return -1;
+    if (h2d(c, wa.p, old_wild, 4 * W * n_old, s)) return -1;
   }
   if (n_new) {
-    GF_CHECK(c, cudaMemcpy(b.p, new_ids, 8 * n_new, cudaMemcpyHostToDevice));
+    if (h2d(c, b.p, new_ids, 8 * n_new, s)) return -1;
     k_merge<<<grid_for(n_new), kBlock, 0, s>>>(n_new, b.as<uint2>(), wb.as<float>(), n_old, a.as<uint2>(),
                                               wa.as<float>(), W);
     GF_CHECK(c, cudaGetLastError());

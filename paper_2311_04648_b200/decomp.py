@@ -393,6 +393,8 @@ def attach(sim) -> None:
     for q, (send, recv) in st.plan.halo(st.rank).items():
         st.peers[q] = _Peer(q, inv[send], inv[recv], rec, sim.device)
     st.word = torch.full((1,), INT64_MAX, dtype=torch.int64, device=torch.device("cuda", sim.device))
+    # torch fills on its own stream; the context's streams are non-blocking
+    torch.cuda.synchronize(sim.device)
 
 
 # ----------------------------------------------------------------------------
