@@ -41,3 +41,21 @@ def test_no_device_fails_loudly():
     sim.load_material({"E": 1e7, "nu": 0.3, "CoR": 0.5, "mu": 0.3, "Crr": 0.0})
     with pytest.raises(gf.DeviceUnavailableError):
         sim.initialize()
+
+
+def test_host_uploads_are_stream_ordered():
+    """The context's streams are non-blocking: a legacy-stream cudaMemcpy /
+    cudaMemset is not ordered with kernels launched on them afterwards (a
+    fresh context once read its fixed-point scales before their upload
+    landed).  Host -> device copies go through h2d(), memsets are async."""
+    csrc = os.path.join(ROOT, "paper_2311_04648_b200", "csrc")
+    bad = []
+    for name in sorted(os.listdir(csrc)):
+        if not name.endswith((".cu", ".cuh")):
+            continue
+        for no, line in enumerate(open(os.path.join(csrc, name)), 1):
+            code = line.split("//")[0]
+            if re.search(r"\bcudaMemset\s*\(", code) or (
+                    re.search(r"\bcudaMemcpy\s*\(", code) and "DeviceToHost" not in code):
+                bad.append(f"{name}:{no}: {line.strip()}")
+    assert not bad, "\n".join(bad)
