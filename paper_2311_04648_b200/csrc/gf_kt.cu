@@ -846,15 +846,33 @@ __global__ void __launch_bounds__(kFcBlock) k_compact(KtView v, const uint2 *can
                                                       const uint32_t *obits, const unsigned long long *oblk_pre,
                                                       uint2 *out_ids, unsigned long long *seg, uint32_t *old_pos,
                                                       unsigned long long ss_cap) {
-  // the filter block's kFcSpan candidates: kFcSpan / 32 bitmask words
+  // the filter block's kFcSpan candidates: kFcSpan / 32 bitmask words; every
+  // global load is issued up front so its latency overlaps the word scan
   constexpr int kW = kFcSpan / 32;
   __shared__ uint32_t s_w[kW], s_ow[kW];
   const int64_t w_base = blockIdx.x * int64_t(kW);
-  const int64_t n_words = (n_cand + 31) / 32;
-  if (threadIdx.x < kW) {
-    const int64_t w = w_base + threadIdx.x;
-    s_w[threadIdx.x] = w < n_words ? __popc(bits[w]) : 0u;
-    s_ow[threadIdx.x] = (obits && w < n_words) ? __popc(obits[w]) : 0u;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned long long pre = blk_pre[blockIdx.x];
+  const unsigned long long opre = obits ? oblk_pre[blockIdx.x] : 0ull;
+  uint2 it[kFcPer];
+  uint32_t word[kFcPer], oword[kFcPer], ap_g[kFcPer];
+#pragma unroll
+  for (int q = 0; q < kFcPer; ++q) {
+    const int wl = warp + q * (kFcBlock / 32);   // word within the block
+    const int64_t e = (w_base + wl) * 32 + lane;
+    const bool in = e < n_cand;
+    it[q] = in ? cand[e] : make_uint2(0u, 0u);
+    ap_g[q] = (in && lane == 0 && e > 0) ? cand[e - 1].x : 0u;
+    word[q] = in ? bits[w_base + wl] : 0u;
+    oword[q] = (in && obits) ? obits[w_base + wl] : 0u;
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < kFcPer; ++q) {
+      const int wl = warp + q * (kFcBlock / 32);
+      s_w[wl] = __popc(word[q]);
+      s_ow[wl] = __popc(oword[q]);
+    }
   }
   __syncthreads();
   if (threadIdx.x < 32) {   // exclusive scan of the word counts (kW <= 32)
@@ -870,28 +888,23 @@ __global__ void __launch_bounds__(kFcBlock) k_compact(KtView v, const uint2 *can
     if (l < kW) { s_w[l] = x - x0; s_ow[l] = y - y0; }
   }
   __syncthreads();
-  const int lane = threadIdx.x & 31;
   const uint32_t below = (1u << lane) - 1u;
 #pragma unroll
   for (int q = 0; q < kFcPer; ++q) {
-    const int wl = (threadIdx.x >> 5) + q * (kFcBlock / 32);   // word within the block
+    const int wl = warp + q * (kFcBlock / 32);
     const int64_t e = (w_base + wl) * 32 + lane;
+    const uint32_t prev_x = __shfl_up_sync(0xffffffffu, it[q].x, 1);
     if (e >= n_cand) continue;
-    const uint32_t word = bits[w_base + wl];
-    unsigned long long p = blk_pre[blockIdx.x] + s_w[wl] + __popc(word & below);
-    const uint2 it = cand[e];
-    const long long a = (long long)it.x;
-    const long long ap = e > 0 ? (long long)cand[e - 1].x : -1;
+    const unsigned long long p = pre + s_w[wl] + __popc(word[q] & below);
+    const long long a = (long long)it[q].x;
+    const long long ap = e == 0 ? -1 : (long long)(lane ? prev_x : ap_g[q]);
     for (long long sp = ap + 1; sp <= a; ++sp) seg[sp] = p;
-    const bool hit = (word >> lane) & 1u;
+    const bool hit = (word[q] >> lane) & 1u;
     if (hit && p < ss_cap) {   // beyond: the fill phase grows the array and recounts
-      out_ids[p] = it;
-      if (obits) {
-        const uint32_t oword = obits[w_base + wl];
-        old_pos[p] = ((oword >> lane) & 1u)
-                         ? uint32_t(oblk_pre[blockIdx.x] + s_ow[wl] + __popc(oword & below))
-                         : 0xFFFFFFFFu;
-      }
+      out_ids[p] = it[q];
+      if (obits)
+        old_pos[p] = ((oword[q] >> lane) & 1u) ? uint32_t(opre + s_ow[wl] + __popc(oword[q] & below))
+                                              : 0xFFFFFFFFu;
     }
     if (e == n_cand - 1)   // the last candidate closes the block
       for (long long sp = a + 1; sp <= v.sph.n; ++sp) seg[sp] = p + (hit ? 1 : 0);
