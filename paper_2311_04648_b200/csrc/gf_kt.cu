@@ -991,30 +991,58 @@ __global__ void k_merge_seg(int64_t n_new, const uint2 *new_ids, float *new_wild
 // history remap at adoption when both arrays were filtered from the same
 // candidate list: sphere-sphere rows gather their old row directly (old_pos),
 // the wall kinds search their old (kind, a) segment like k_merge_seg
+__device__ __forceinline__ long long adopt_wall_hit(const uint2 *new_ids, const uint2 *old_ids,
+                                                    const unsigned long long *old_seg, int64_t n_sph, int64_t k) {
+  const uint2 id = new_ids[k];
+  const int64_t sg = int64_t(id.y >> kKindShift) * n_sph + id.x;
+  const unsigned long long lo = old_seg[sg], hi = old_seg[sg + 1];
+  for (unsigned long long q = lo; q < hi; ++q) {
+    const uint32_t y = old_ids[q].y;
+    if (y == id.y) return (long long)q;
+    if (y > id.y) break;
+  }
+  return -1;
+}
+
+constexpr int kAdoptPer = 2;   // rows per thread: their gathers are in flight together
+
 __global__ void k_adopt_hist(int64_t n_new, const uint2 *new_ids, const uint32_t *old_pos,
                              const unsigned long long *new_seg, float *new_wild, const uint2 *old_ids,
                              const float *old_wild, const unsigned long long *old_seg, int64_t n_sph, int W) {
-  int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (k >= n_new) return;
-  long long hit = -1;
-  if ((unsigned long long)k < new_seg[n_sph]) {
-    const uint32_t q = old_pos[k];
-    if (q != 0xFFFFFFFFu) hit = (long long)q;
-  } else {
-    const uint2 id = new_ids[k];
-    const int64_t sg = int64_t(id.y >> kKindShift) * n_sph + id.x;
-    const unsigned long long lo = old_seg[sg], hi = old_seg[sg + 1];
-    for (unsigned long long q = lo; q < hi; ++q) {
-      uint32_t y = old_ids[q].y;
-      if (y == id.y) { hit = (long long)q; break; }
-      if (y > id.y) break;
-    }
+  const int64_t k0 = blockIdx.x * int64_t(blockDim.x) * kAdoptPer + threadIdx.x;
+  const unsigned long long n_ss = new_seg[n_sph];
+  uint32_t q[kAdoptPer];
+#pragma unroll
+  for (int j = 0; j < kAdoptPer; ++j) {
+    const int64_t k = k0 + int64_t(j) * blockDim.x;
+    q[j] = k < n_new ? old_pos[k] : 0xFFFFFFFFu;   // wall rows ignore it
+  }
+  long long hit[kAdoptPer];
+#pragma unroll
+  for (int j = 0; j < kAdoptPer; ++j) {
+    const int64_t k = k0 + int64_t(j) * blockDim.x;
+    hit[j] = -1;
+    if (k >= n_new) continue;
+    if ((unsigned long long)k < n_ss) hit[j] = q[j] != 0xFFFFFFFFu ? (long long)q[j] : -1;
+    else hit[j] = adopt_wall_hit(new_ids, old_ids, old_seg, n_sph, k);
   }
   if (W == 4) {
-    reinterpret_cast<float4 *>(new_wild)[k] =
-        hit >= 0 ? reinterpret_cast<const float4 *>(old_wild)[hit] : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 w[kAdoptPer];
+#pragma unroll
+    for (int j = 0; j < kAdoptPer; ++j)
+      w[j] = hit[j] >= 0 ? reinterpret_cast<const float4 *>(old_wild)[hit[j]] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < kAdoptPer; ++j) {
+      const int64_t k = k0 + int64_t(j) * blockDim.x;
+      if (k < n_new) reinterpret_cast<float4 *>(new_wild)[k] = w[j];
+    }
   } else {
-    for (int q = 0; q < W; ++q) new_wild[int64_t(W) * k + q] = hit >= 0 ? old_wild[int64_t(W) * hit + q] : 0.0f;
+#pragma unroll
+    for (int j = 0; j < kAdoptPer; ++j) {
+      const int64_t k = k0 + int64_t(j) * blockDim.x;
+      if (k >= n_new) continue;
+      for (int c = 0; c < W; ++c) new_wild[int64_t(W) * k + c] = hit[j] >= 0 ? old_wild[int64_t(W) * hit[j] + c] : 0.0f;
+    }
   }
 }
 
@@ -1556,7 +1584,7 @@ int adopt_acs(Ctx *c, cudaStream_t s) {
   Acs &nw = c->acs_next;
   Acs &old = c->acs;
   if (nw.n && old.n && old.seg.p && nw.pos_valid && old.det_id != 0 && old.det_id == nw.prev_det)
-    k_adopt_hist<<<grid_for(nw.n), kBlock, 0, s>>>(nw.n, nw.ids.as<uint2>(), nw.old_pos.as<uint32_t>(),
+    k_adopt_hist<<<unsigned((nw.n + kBlock * kAdoptPer - 1) / (kBlock * kAdoptPer)), kBlock, 0, s>>>(nw.n, nw.ids.as<uint2>(), nw.old_pos.as<uint32_t>(),
                                                   nw.seg.as<unsigned long long>(), nw.wild.as<float>(),
                                                   old.ids.as<uint2>(), old.wild.as<float>(),
                                                   old.seg.as<unsigned long long>(), c->n_sph, c->wild_w);
