@@ -89,19 +89,34 @@ __global__ void __launch_bounds__(256) k_snapshot(Domain dom, Owners own, Sphere
     hi[ax] = -lo[ax];
   }
   bool far = false;
-  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < sph.n;
-       k += int64_t(gridDim.x) * blockDim.x) {
-    const double4 c = sph.center[k];
-    c4[k] = c;
-    sfam[k] = uint8_t(meta_family(own.meta[sph.owner[k]]));
-    if (mm) {
-      lo[0] = fmin(lo[0], c.x); lo[1] = fmin(lo[1], c.y); lo[2] = fmin(lo[2], c.z);
-      hi[0] = fmax(hi[0], c.x); hi[1] = fmax(hi[1], c.y); hi[2] = fmax(hi[2], c.z);
-      rmax = fmax(rmax, c.w);
+  // two spheres per iteration, every load issued before the dependent ones
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t k0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k0 < sph.n; k0 += 2 * stride) {
+    const int64_t kk[2] = {k0, k0 + stride};
+    double4 c[2];
+    uint32_t ow[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      if (kk[j] < sph.n) {
+        c[j] = sph.center[kk[j]];
+        ow[j] = sph.owner[kk[j]];
+      }
     }
-    if (ref) {
-      const double dx = c.x - ref[3 * k], dy = c.y - ref[3 * k + 1], dz = c.z - ref[3 * k + 2];
-      far = far || dx * dx + dy * dy + dz * dz > ((r_cut > 0.0 && c.w > r_cut) ? lim2_big : lim2);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int64_t k = kk[j];
+      if (k >= sph.n) continue;
+      c4[k] = c[j];
+      sfam[k] = uint8_t(meta_family(own.meta[ow[j]]));
+      if (mm) {
+        lo[0] = fmin(lo[0], c[j].x); lo[1] = fmin(lo[1], c[j].y); lo[2] = fmin(lo[2], c[j].z);
+        hi[0] = fmax(hi[0], c[j].x); hi[1] = fmax(hi[1], c[j].y); hi[2] = fmax(hi[2], c[j].z);
+        rmax = fmax(rmax, c[j].w);
+      }
+      if (ref) {
+        const double dx = c[j].x - ref[3 * k], dy = c[j].y - ref[3 * k + 1], dz = c[j].z - ref[3 * k + 2];
+        far = far || dx * dx + dy * dy + dz * dz > ((r_cut > 0.0 && c[j].w > r_cut) ? lim2_big : lim2);
+      }
     }
   }
   if (ref && __any_sync(0xffffffffu, far) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
@@ -1126,7 +1141,7 @@ int kt_snapshot(Ctx *c, cudaStream_t s, double margin) {
     if (check) GF_CHECK(c, cudaMemsetAsync(k.flag.p, 0, sizeof(int), s));
   }
   const double skin = c->skin_factor * margin, skin_b = c->skin_big_factor * margin;
-  // one wave (74 registers: 3 CTAs / SM), grid-stride: 2470 vs 2460 M sphere-steps/s at 8 / SM
+  // one wave of 3 CTAs / SM, grid-stride (2470 vs 2460 M sphere-steps/s at 8 / SM)
   constexpr int64_t snap_blocks = 148 * 3;
   if (c->n_sph)
     k_snapshot<<<unsigned(std::min<int64_t>(grid_for(c->n_sph), snap_blocks)), kBlock, 0, s>>>(
