@@ -71,18 +71,52 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks / throttle reasons sampled during the timed region (NVML,
+    else an nvidia-smi child)."""
 
     QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
+    # NVML clocks-event reason bits: sw power cap, hw slowdown, sw / hw thermal
+    _BITS = (0x8, 0x40, 0x20, 0x4)   # order of summary(): hw, hw thermal, sw thermal, power cap
+
     def __init__(self, index):
         self.index = index
         self.rows = []
         self.proc = None
+        self._nvml = None
+
+    def _poll(self):
+        """NVML in-process, every 2 ms: a sub-100 ms timed region still gets
+        samples (an nvidia-smi child often returns none inside it)."""
+        nv, h = self._nvml
+        try:
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        except Exception:
+            mx = 0
+        while True:
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append([str(self.index), str(sm), str(mx), "", ""] +
+                                 ["Active" if rs & b else "Not Active" for b in self._BITS])
+            except Exception:
+                pass
+            if self._stop.wait(0.002):
+                break
 
     def __enter__(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self._nvml = (nv, nv.nvmlDeviceGetHandleByIndex(self.index))
+            self._stop = threading.Event()
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            self._nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}",
@@ -99,6 +133,10 @@ class ClockSampler:
             self.rows.append([x.strip() for x in line.split(",")])
 
     def __exit__(self, *exc):
+        if self._nvml is not None:
+            self._stop.set()
+            self.thread.join(timeout=5)
+            return
         if self.proc is not None:
             self.proc.terminate()
             try:
