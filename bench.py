@@ -1,7 +1,12 @@
-"""Benchmark: M sphere-steps/s of the B200 DEM step (BASELINE.json metric) on
-configs[1], the projectile-impact bed (1M polydisperse spheres).
+"""Benchmark: M sphere-steps/s of the B200 DEM step (BASELINE.json metric).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Workload at N=1 (the largest single-GPU configuration in BASELINE.json's
+configs): configs[4]'s 150M-sphere point -- the settled configs[1] crater
+bed (1M polydisperse spheres + projectile, released after 12 000 untimed
+settling steps) tiled 15 x 10 side by side in one box (scenes.tiled_bed).
+`--tiles 1` times configs[1] itself.
 
 One JSON line on rank 0.  `value` = whole-job sphere-steps/s from CUDA events
 on the dT stream (t0 before the first timed step, t1 after the last step with
@@ -9,7 +14,8 @@ the kT stream joined), max over ranks.  `e2e` = the same metric through the
 C-ABI with host buffers: every step uploads the owner state from pinned host
 memory, runs the step, downloads the state.  `--impl reference` times the
 reference algorithm on the host cores (the C restatement in oracle/, all
-threads) on the same scene.
+threads) on the same settled bed (prepared on the device, untimed), one
+1M-sphere tile per step as the bounded sample.
 
 Multi-GPU (torchrun, one process per GPU): the spatial slab decomposition
 (paper_2311_04648_b200/decomp.py) of N beds laid side by side -- each rank
@@ -49,12 +55,18 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n-spheres", type=int, default=1_000_000)
+    ap.add_argument("--n-spheres", type=int, default=1_000_000, help="spheres per bed (tile)")
+    ap.add_argument("--tiles", type=int, default=150,
+                    help="N=1: copies of the settled bed in one box (configs[4] size sweep; 150 = 150M "
+                         "spheres, the largest single-GPU point); 1 = configs[1] itself")
     ap.add_argument("--n-max", type=int, default=4)
     ap.add_argument("--precision", default="f32", choices=["f32", "f64"])
-    ap.add_argument("--e2e-steps", type=int, default=10)
-    ap.add_argument("--cpu-steps", type=int, default=4)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--amortised-steps", type=int, default=200,
+                    help="extra window over several candidate rebuilds (rebuild-amortised rate)")
+    ap.add_argument("--prof-steps", type=int, default=20, help="per-kernel event window")
     ap.add_argument("--mode", default="auto", choices=["auto", "single", "replicas", "decomp"],
                     help="auto: single on 1 GPU, decomp (slab decomposition) on N > 1")
     ap.add_argument("--settle-steps", type=int, default=12000,
@@ -201,32 +213,86 @@ def schedule(sim):
     return period, lag, sim._current_margin()
 
 
+DTYPE = ("fp32 contact law (fp64 centre difference and overlap numerator R^2 - d^2), fp32 velocities, "
+         "int64 fixed-point owner force/torque sums, fixed-point positions (u64 voxel + 3 x u16)")
+DTYPE_F64 = "fp64 contact law and velocities (parity build), fixed-point positions"
+
+
+def factor(t):
+    """tx x ty = t, as square as possible"""
+    ty = int(math.isqrt(t))
+    while t % ty:
+        ty -= 1
+    return t // ty, ty
+
+
+def workload_config(args, world, mode):
+    """The `config` object of both arms (identical by construction)."""
+    tiles = max(1, args.tiles) if world == 1 else 1
+    tx, ty = factor(tiles)
+    if world == 1 and tiles > 1:
+        wl = (f"configs[4] size-sweep point: the settled configs[1] crater bed ({args.n_spheres} polydisperse "
+              f"spheres + projectile) tiled {tx}x{ty} in one box = {tiles * (args.n_spheres + 1)} spheres "
+              f"on one B200")
+    else:
+        wl = (f"configs[1] crater impact bed, {args.n_spheres} polydisperse spheres + projectile"
+              + (f" per GPU, {world} beds side by side" if world > 1 else ""))
+    return {"workload": wl, "n_spheres_per_bed": args.n_spheres, "tiles": f"{tx}x{ty}",
+            "n_max": args.n_max, "h": 1e-5, "v_err": 5.0, "precision": args.precision,
+            "settle_steps": args.settle_steps,
+            "parallelism": ({"decomp": f"slab decomposition x{world} (NCCL halo + force return)",
+                             "replicas": f"replicas x{world}"}.get(mode, "single GPU")),
+            "inputs_vs_l2": "state + contact arrays larger than L2 (no flush)",
+            "bed": ("settled: the untimed settling steps from the HCP lattice with the projectile parked, "
+                    "then the projectile released 2 mm above the surface at the 20 cm-drop speed")
+            if args.settle_steps > 0 else "raw HCP lattice"}
+
+
+def settled_source(args, device, tiles=1, decomposition=None):
+    """The settled configs[1] bed (device; untimed setup shared by both arms)."""
+    from paper_2311_04648_b200 import scenes
+    src = build_scene(args, device, tiles=tiles, decomposition=decomposition, hold_ball=args.settle_steps > 0)
+    src.initialize()
+    t_s = time.perf_counter()
+    if args.settle_steps > 0:
+        # the reference settles the bed before the drop (scenarios.py:255-307)
+        src.do_dynamics(args.settle_steps * src.h)
+        scenes.release_balls(src)
+    return src, time.perf_counter() - t_s
+
+
 def reference_arm(args):
-    rank, world, _ = dist_env()
+    """The reference's algorithm on the host cores (oracle/gf_oracle.c, the C
+    restatement of grainforge's numba kernels, OpenMP on every core) on the
+    same settled bed the b200 arm times.  The bed is settled on the device
+    (untimed input preparation: 12 000 steps are out of reach on the host);
+    each timed step advances one 1M-sphere tile -- the bounded sample; the
+    per-sphere cost does not depend on how many tiles sit side by side."""
+    rank, world, local = dist_env()
     if rank != 0:
         return
     from paper_2311_04648_b200 import scenes
-    sim = build_scene(args, 0)
-    scene = scenes.oracle_scene(sim)
-    period, lag, margin = schedule(sim)
+    src, _ = settled_source(args, local)
+    scene = scenes.oracle_scene(src)
+    period, lag, margin = schedule(src)
+    src.close()
     n_s = int(np.sum(scene["geom_kind"] == 0))
     threads = os.cpu_count() or 1
-    steps = max(1, min(args.steps, args.cpu_steps))
-    wall = cpu_run(scene, steps, max(1, min(args.warmup, 2)), period, lag, threads, margin)
+    steps = max(1, args.steps)
+    warm = max(1, min(args.warmup, 2))
+    wall = cpu_run(scene, steps, warm, period, lag, threads, margin)
     value = n_s * steps / wall / 1e6
+    mode = "decomp" if world > 1 else "single"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": steps, "warmup": max(1, min(args.warmup, 2)), "ms_per_step": wall / steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": f"crater impact bed, {n_s} polydisperse spheres (configs[1])",
-                   "n_max": args.n_max, "h": scene["h"], "inputs_vs_l2": "larger than L2",
-                   "bed": "raw HCP lattice (settling it takes ~12k steps, out of reach on the host; "
-                          "the lattice has almost no touching contacts, so this is an upper bound "
-                          "for the CPU on the settled bed the b200 arm times)"},
+        "steps": steps, "warmup": warm, "ms_per_step": wall / steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp64 (numba fastmath=False "
+        "semantics, -ffp-contract=off)", "data": "synthetic",
+        "config": workload_config(args, world, mode),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{steps} steps of the lattice bed (oracle/gf_oracle.c, OpenMP "
-                                   f"contact + integrate loops, serial detection)"},
+                         "sample": f"each step: one step of one {n_s}-sphere tile of the settled bed "
+                                   f"(oracle/gf_oracle.c, OpenMP contact/reduce/integrate loops, serial "
+                                   f"detection; period {period}, lag {lag}, margin {margin:.3g} m)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -248,18 +314,19 @@ def b200_arm(args):
     device = local
     from paper_2311_04648_b200 import _lib, decomp, scenes
     dec = decomp.SlabDecomposition(travel=args.travel) if mode == "decomp" else None
-    sim = build_scene(args, device, tiles=world if mode == "decomp" else 1, decomposition=dec,
-                      hold_ball=args.settle_steps > 0)
-    sim.initialize()
-    settle_s = 0.0
-    if args.settle_steps > 0:
-        # the reference settles the bed before the drop (scenarios.py:255-307);
-        # untimed setup on the device, then the projectile is released
-        t_s = time.perf_counter()
-        sim.do_dynamics(args.settle_steps * sim.h)
-        scenes.release_balls(sim)
-        settle_s = time.perf_counter() - t_s
+    t_setup = time.perf_counter()
+    sim, settle_s = settled_source(args, device, tiles=world if mode == "decomp" else 1, decomposition=dec)
+    # the CPU baseline's sample: one settled tile
     scene0 = scenes.oracle_scene(sim) if (rank == 0 and world == 1 and not args.no_cpu) else None
+    tiles = max(1, args.tiles) if (world == 1 and mode == "single") else 1
+    if tiles > 1:
+        tx, ty = factor(tiles)
+        src = sim
+        sim = scenes.tiled_bed(src, tx, ty, precision=args.precision, device=device, n_max=args.n_max)
+        src.close()
+        del src
+        sim.initialize()
+    setup_s = time.perf_counter() - t_setup
     if mode == "decomp":
         cls = sim._dd.dd & 3
         n_s = int(np.sum(cls[sim._sph_owner] == decomp.DD_LOCAL))   # spheres this rank integrates
@@ -274,6 +341,8 @@ def b200_arm(args):
         n_ghost_owners = 0
         n_sph_total = n_s * world
     n_o = int(sim.store.n_owners)
+    # non-fixed owners, from the host arrays (no device sync)
+    n_free0 = int(np.sum(~sim._fixed_flag[sim.store.__dict__["_owner_family"][:n_o]]))
     h = sim.h
     # warm-up (untimed)
     sim.do_dynamics(args.warmup * h)
@@ -306,12 +375,26 @@ def b200_arm(args):
     # every gf_run segment (one segment unless a repartition split the call)
     dt_ms = (sim.scheduler.timing["dyn_force"] - dev0) * 1e3
     repartitions = getattr(sim.scheduler, "repartitions", 0) - reps0
+    # rebuild-amortised rate: a longer window (CUDA events on the dT stream,
+    # kT joined) spanning several Verlet candidate rebuilds -- a short timed
+    # window may contain none (one rebuild every ~40 steps on this bed)
+    amort = None
+    if args.amortised_steps > 0 and mode == "single":
+        rb0 = int(sim.last_run.kt_rebuilds)
+        d0 = sim.scheduler.timing["dyn_force"]
+        barrier()
+        sim.do_dynamics(args.amortised_steps * h)
+        barrier()
+        a_ms = (sim.scheduler.timing["dyn_force"] - d0) * 1e3
+        amort = {"value": n_sph_total * args.amortised_steps / (a_ms * 1e-3) / 1e6, "unit": UNIT,
+                 "steps": args.amortised_steps, "ms_per_step": a_ms / args.amortised_steps,
+                 "kt_candidate_rebuilds": int(sim.last_run.kt_rebuilds) - rb0}
     # per-kernel CUDA events would sit between the kernels of the chain (and
     # break its programmatic dependent launches): the kernel times come from a
     # separate profiled window right after the timed one
     ctx = sim._ctx   # a repartition rebuilds the context
     ctx.call("gf_set_profiling", C.c_int(1))
-    prof_steps = max(2 * 2, min(args.steps, 50))
+    prof_steps = max(2 * 2, min(args.steps, args.prof_steps))
     sim.do_dynamics(prof_steps * h)
     barrier()
     ctx = sim._ctx
@@ -326,7 +409,7 @@ def b200_arm(args):
     value = n_sph_total * args.steps / (dt_ms * 1e-3) / 1e6
     n_acs_avg = float(rr.sum_acs) / max(1, args.steps)
     n_touch_avg = float(rr.sum_touch_pairs) / max(1, args.steps)
-    n_free = int(np.sum(~sim._fixed_flag[sim.store.owner_family[:n_o]]))
+    n_free = n_free0
 
     # --- roofline: dominant kernel (k_contacts_ss) and the whole dT chain ---
     hbm, hbm_kind = peaks()
@@ -362,9 +445,10 @@ def b200_arm(args):
             period, lag, margin = schedule(sim)
             csteps = max(1, args.cpu_steps)
             wall = cpu_run(scene0, csteps, 1, period, lag, 1, margin)
-            cpu = {"value": n_s * csteps / wall / 1e6, "unit": UNIT, "cores": 1, "kind": "port",
-                   "sample": f"{csteps} steps (+1 warm-up) of the same bed from the same initial "
-                             f"state, serial C restatement (oracle/gf_oracle.c)"}
+            n_s0 = int(np.sum(scene0["geom_kind"] == 0))
+            cpu = {"value": n_s0 * csteps / wall / 1e6, "unit": UNIT, "cores": 1, "kind": "port",
+                   "sample": f"{csteps} steps (+1 warm-up) of one {n_s0}-sphere tile of the same settled bed "
+                             f"(1/{tiles} of the workload), serial C restatement (oracle/gf_oracle.c)"}
         launches_per_step = 3 + (1 if sim._tri_geom.size or sim._ana_geom.size else 0)
         if mode == "decomp":   # halo: pack/add forces, pack/unpack(+centres) state per peer; guard word x2
             launches_per_step += 2 + 5 * len(sim._dd.peers)
@@ -374,24 +458,17 @@ def b200_arm(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64 contact math, " + ("f32" if args.precision == "f32" else "f64") + " velocities",
+            "dtype": DTYPE if args.precision == "f32" else DTYPE_F64,
             "data": "synthetic",
-            "config": {"workload": f"crater impact bed, {n_s} polydisperse spheres + projectile "
-                                   f"(configs[1])" + (f" per GPU, {world} beds side by side" if world > 1 else ""),
-                       "n_spheres": n_s, "n_owners": n_o,
-                       "n_max": args.n_max, "period": period, "lag": lag, "h": h,
-                       "parallelism": ({"decomp": f"slab decomposition x{world} (NCCL halo + force return)",
-                                        "replicas": f"replicas x{world}"}.get(mode, "single GPU")),
-                       "n_spheres_total": n_sph_total,
-                       "inputs_vs_l2": "state + contact arrays larger than L2 (no flush)",
-                       "avg_acs": n_acs_avg, "avg_touching_pairs": n_touch_avg,
-                       "kt_candidate_rebuilds_in_timed_steps": int(rr.kt_rebuilds) - rebuilds0,
-                       "precision": args.precision,
-                       "bed": (f"settled: {args.settle_steps} untimed steps from the HCP lattice, then the "
-                               f"projectile released 2 mm above the surface at the 20 cm-drop speed "
-                               f"({settle_s:.1f} s setup)") if args.settle_steps > 0 else "raw HCP lattice",
-                       **({"ghost_owners_rank0": n_ghost_owners, "travel_m": args.travel,
-                           "repartitions_in_timed_steps": repartitions} if mode == "decomp" else {})},
+            "config": workload_config(args, world, mode),
+            "workload_stats": {"n_spheres": n_s, "n_owners": n_o, "n_spheres_total": n_sph_total,
+                               "period": period, "lag": lag, "avg_acs": n_acs_avg,
+                               "avg_touching_pairs": n_touch_avg,
+                               "kt_candidate_rebuilds_in_timed_steps": int(rr.kt_rebuilds) - rebuilds0,
+                               "setup_s": setup_s, "settle_s": settle_s,
+                               **({"ghost_owners_rank0": n_ghost_owners, "travel_m": args.travel,
+                                   "repartitions_in_timed_steps": repartitions} if mode == "decomp" else {})},
+            "rebuild_amortised": amort,
             "roofline": {"bound": "hbm", "kernel": "k_contacts_ss", "achieved": ach_c, "peak": hbm,
                          "unit": "GB/s", "frac": ach_c / hbm, "peak_kind": hbm_kind,
                          "traffic": profiled_traffic("k_contacts_ss"),

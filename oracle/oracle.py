@@ -389,7 +389,10 @@ class OracleStepper:
                 s["pair_stack"], self.wild, s["h"], self.sim_time, self.nthreads, self.model)
         else:
             self.last_touching = 0
-            out_ft = np.zeros((0, 6)); cp = np.zeros((0, 3))
+            out_ft = np.zeros((0, 6)); cp = np.zeros((0, 3)); depth = np.zeros(0)
+        # the step's per-contact forces (tests normalise tolerances by them)
+        self.last_force_median = (float(np.median(np.linalg.norm(out_ft[depth > 0, :3], axis=1)))
+                                  if np.any(depth > 0) else 0.0)
         self.acc_f, self.acc_t = reduce_to_owners(go[ga], go[gb], out_ft, cp, self.pos)
         for fam, tab, ax, fn in self.dyn_prescriptions:
             s[tab][fam, ax] = fn(self.sim_time)

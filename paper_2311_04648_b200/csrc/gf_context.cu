@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cmath>
 #include <chrono>
+#include <deque>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -44,6 +45,15 @@ int ensure(Ctx *c, DBuf &b, size_t bytes, cudaStream_t s, bool keep) {
     b.bytes = 0;
   }
   if (e == cudaSuccess) e = cudaMalloc(&p, nb);
+  if (e == cudaErrorMemoryAllocation) {
+    // blocks parked in the stream-ordered pool (big kT scratch) hold device
+    // memory: return them and retry once
+    (void)cudaGetLastError();
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, c->device) == cudaSuccess && cudaDeviceSynchronize() == cudaSuccess &&
+        cudaMemPoolTrimTo(pool, 0) == cudaSuccess)
+      e = cudaMalloc(&p, nb);
+  }
   if (e != cudaSuccess) {
     (void)cudaGetLastError();
     set_err(c, std::string("device allocation of ") + std::to_string(nb) + " bytes failed: " +
@@ -57,6 +67,37 @@ int ensure(Ctx *c, DBuf &b, size_t bytes, cudaStream_t s, bool keep) {
   if (b.p) cudaFree(b.p);
   b.p = p;
   b.bytes = nb;
+  return 0;
+}
+
+int ensure_scratch(Ctx *c, DBuf &b, size_t bytes, cudaStream_t s) {
+  if (!big_scratch(c)) return ensure(c, b, bytes, s);
+  return ensure_pooled(c, b, bytes, s);
+}
+
+int ensure_pooled(Ctx *c, DBuf &b, size_t bytes, cudaStream_t s) {
+  if (bytes == 0) bytes = 16;
+  if (b.bytes >= bytes) return 0;
+  if (b.p) GF_CHECK(c, cudaFreeAsync(b.p, s));
+  b.p = nullptr;
+  b.bytes = 0;
+  const size_t nb = bytes + 256;
+  cudaError_t e = cudaMallocAsync(&b.p, nb, s);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    b.p = nullptr;
+    set_err(c, std::string("stream-ordered allocation of ") + std::to_string(nb) + " bytes failed: " +
+                   cudaGetErrorString(e));
+    return -1;
+  }
+  b.bytes = nb;
+  return 0;
+}
+
+int release_scratch(Ctx *c, DBuf &b, cudaStream_t s) {
+  if (b.p) GF_CHECK(c, cudaFreeAsync(b.p, s));
+  b.p = nullptr;
+  b.bytes = 0;
   return 0;
 }
 
@@ -198,7 +239,13 @@ struct RunState {
   gf_run_params p{};
   int period = 1, lag = 0;
   int64_t sum_acs = 0;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kt_ev;   // per-detection kT timing
+  // per-detection kT timing: (start, end) event pairs of the detections in
+  // flight; a pair whose end has completed is folded into kt_ms and recycled,
+  // so a long run holds a handful of events, not one pair per detection
+  std::deque<std::pair<cudaEvent_t, cudaEvent_t>> kt_ev;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kt_ev_free;
+  double kt_ms = 0.0;
+  bool kt_freeze = false;   // GF_KT_FREEZE, read once per run
   std::chrono::steady_clock::time_point w0;
   // GF_TRACE (diagnostics): timed events on both streams + host waits,
   // printed to stderr at gf_run_end
@@ -220,6 +267,10 @@ static void trace_mark(Ctx *c, const char *what, int64_t step, cudaStream_t s) {
 static void free_run(Ctx *c) {
   if (!c->run) return;
   for (auto &e : c->run->kt_ev) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  for (auto &e : c->run->kt_ev_free) {
     cudaEventDestroy(e.first);
     cudaEventDestroy(e.second);
   }
@@ -402,6 +453,18 @@ gf_ctx *gf_create(int device, uint32_t flags) {
   cudaEventCreate(&c->t0);
   cudaEventCreate(&c->t1);
   cudaEventRecord(c->ev_adopted, c->s_dt);
+  // the rebuild-only kT scratch of big scenes cycles through the device's
+  // stream-ordered pool (ensure_scratch): keep freed blocks mapped in the
+  // pool so the next rebuild reuses them instead of remapping tens of GB;
+  // ensure() trims the pool if a plain allocation ever runs short
+  {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    (void)cudaGetLastError();
+  }
   if (cudaMallocHost(&c->h_status, sizeof(Status)) != cudaSuccess) { delete ctx; return nullptr; }
   if (ensure(c, c->status, sizeof(Status), c->s_dt) || ensure(c, c->heavy_count, 16, c->s_dt)) {
     delete ctx;
@@ -534,6 +597,13 @@ static void world_moving_from_host(Ctx *c, const uint8_t *family) {
       }
 }
 
+// host-layout staging of the owner round trips: kept below 2^24 owners,
+// from the stream-ordered pool above (see gf_upload_owners)
+static int ensure_stage(Ctx *c, int64_t n, cudaStream_t s) {
+  const size_t bytes = kStageBytesPerOwner * (n + 1);
+  return n >= (int64_t(1) << 24) ? ensure_pooled(c, c->owner_stage, bytes, s) : ensure(c, c->owner_stage, bytes, s);
+}
+
 int gf_upload_owners(gf_ctx *ctx, int64_t n, const uint64_t *voxel, const uint16_t *sub,
                      const float *quat, const double *lin_vel, const double *ang_vel,
                      const uint8_t *family, const uint32_t *tpl, int64_t n_tpl,
@@ -549,9 +619,9 @@ int gf_upload_owners(gf_ctx *ctx, int64_t n, const uint64_t *voxel, const uint16
       ensure(c, c->quat, 16 * n, s) || ensure(c, c->lin_vel, vb * n, s) ||
       ensure(c, c->ang_vel, vb * n, s) || ensure(c, c->meta, 4 * n, s) ||
       ensure(c, c->tpl, 32 * (n_tpl + 1), s) || ensure(c, c->acc, 48 * n, s) ||
-      ensure(c, c->facc, 48 * n, s) || ensure(c, c->tpl_scale, 16 * (n_tpl + 1), s) ||
-      ensure(c, c->owner_stage, kStageBytesPerOwner * (n + 1), s))
+      ensure(c, c->facc, 48 * n, s) || ensure(c, c->tpl_scale, 16 * (n_tpl + 1), s))
     return -1;
+  if (ensure_stage(c, n, s)) return -1;
   // the parity build's incidence-list reduction (the throughput build sums
   // into the fixed-point accumulators instead)
   if (!c->f32_state && (ensure(c, c->heavy_acc, 48 * n, s) || ensure(c, c->inc_start, 4 * (n + 2), s) ||
@@ -596,10 +666,11 @@ int gf_upload_owners(gf_ctx *ctx, int64_t n, const uint64_t *voxel, const uint16
   if (c->n_sph && c->sph_first.p && c->sph_center.bytes >= size_t(32 * c->n_sph)) {
     if (refresh_centers(c, s) || refresh_world(c, s)) return -1;
   }
-  GF_CHECK(c, cudaStreamSynchronize(s));
   // the staging buffer is kept for repeated host round trips, except at
-  // scene sizes where device memory is the limit (2^24 owners and up)
-  if (n >= (int64_t(1) << 24)) release(c->owner_stage);
+  // scene sizes where device memory is the limit (2^24 owners and up): there
+  // it goes back to the stream-ordered pool
+  if (n >= (int64_t(1) << 24) && release_scratch(c, c->owner_stage, s)) return -1;
+  GF_CHECK(c, cudaStreamSynchronize(s));
   world_moving_from_host(c, family);
   return 0;
 }
@@ -611,7 +682,7 @@ int gf_download_owners(gf_ctx *ctx, uint64_t *voxel, uint16_t *sub, float *quat,
   cudaStream_t s = c->s_dt;
   GF_CHECK(c, cudaDeviceSynchronize());   // the kT stream may still read the state
   if (!n) return 0;
-  if (ensure(c, c->owner_stage, kStageBytesPerOwner * (n + 1), s)) return -1;
+  if (ensure_stage(c, n, s)) return -1;
   const Stage st = stage_of(c->owner_stage, n);
   k_owners_out<<<unsigned((n + 255) / 256), 256, 0, s>>>(n, c->sub.as<ushort4>(), c->lin_vel.p, c->ang_vel.p,
                                                        c->meta.as<uint32_t>(), st.sub3, st.lv, st.av, st.fam,
@@ -622,6 +693,7 @@ int gf_download_owners(gf_ctx *ctx, uint64_t *voxel, uint16_t *sub, float *quat,
   if (lin_vel) GF_CHECK(c, cudaMemcpyAsync(lin_vel, st.lv, 24 * n, cudaMemcpyDeviceToHost, s));
   if (ang_vel) GF_CHECK(c, cudaMemcpyAsync(ang_vel, st.av, 24 * n, cudaMemcpyDeviceToHost, s));
   if (family) GF_CHECK(c, cudaMemcpyAsync(family, st.fam, n, cudaMemcpyDeviceToHost, s));
+  if (n >= (int64_t(1) << 24) && release_scratch(c, c->owner_stage, s)) return -1;
   GF_CHECK(c, cudaStreamSynchronize(s));
   return 0;
 }
@@ -803,7 +875,11 @@ int gf_set_acs(gf_ctx *ctx, int64_t n, const uint8_t *kind, const int64_t *slot_
   GF_CHECK(c, cudaDeviceSynchronize());
   if (W != c->wild_w) { c->err = "wildcard count differs from the active force model's"; return -1; }
   int64_t cap = n + n / 2 + 1024;
-  if (ensure(c, c->acs.ids, 8 * cap, c->s_dt) || ensure(c, c->acs.wild, 4 * W * cap, c->s_dt)) return -1;
+  // every array of the capacity carries its candidate-row column: the two
+  // arrays alternate, and the compaction writes old_pos into whichever is next
+  if (ensure(c, c->acs.ids, 8 * cap, c->s_dt) || ensure(c, c->acs.wild, 4 * W * cap, c->s_dt) ||
+      ensure(c, c->acs.old_pos, 4 * cap, c->s_dt))
+    return -1;
   c->acs.cap = cap;
   c->acs.n = n;
   c->acs.det_id = 0;   // installed: no candidate rows refer to it
@@ -1012,6 +1088,7 @@ int gf_run_begin(gf_ctx *ctx, const gf_run_params *p) {
   R->period = p->period < 1 ? 1 : p->period;
   R->lag = p->lag < 0 ? 0 : p->lag;
   R->trace = std::getenv("GF_TRACE") != nullptr;
+  R->kt_freeze = std::getenv("GF_KT_FREEZE") != nullptr;
   c->run = R;
   const int64_t N = p->n_steps;
   c->kt_margin = p->margin;
@@ -1044,17 +1121,32 @@ int gf_step_forces(gf_ctx *ctx, int64_t i) {
   // 2. work order: snapshot on the dT stream, detection on the kT stream
   // GF_KT_FREEZE=1 (timing diagnostics only): no work orders after the first
   // detection, so a run measures the dT chain alone on a frozen contact array
-  const bool kt_freeze = std::getenv("GF_KT_FREEZE") != nullptr;
-  if (!c->next_pending && (c->first_adopt || (!kt_freeze && s - c->last_snap >= R->period))) {
+  if (!c->next_pending && (c->first_adopt || (!R->kt_freeze && s - c->last_snap >= R->period))) {
     if (kt_snapshot(c, c->s_dt, p->margin)) return -1;
     GF_CHECK(c, cudaEventRecord(c->ev_snap, c->s_dt));
     GF_CHECK(c, cudaStreamWaitEvent(c->s_kt, c->ev_snap, 0));
     GF_CHECK(c, cudaStreamWaitEvent(c->s_kt, c->ev_adopted, 0));
-    cudaEvent_t e0, e1;
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    R->kt_ev.emplace_back(e0, e1);
-    GF_CHECK(c, cudaEventRecord(e0, c->s_kt));
+    // retire completed detections' timing events (every one but the newest
+    // has been adopted, so its end event is recorded), then reuse a pair
+    while (R->kt_ev.size() > 1 || (!R->kt_ev.empty() && cudaEventQuery(R->kt_ev.front().second) == cudaSuccess)) {
+      auto e = R->kt_ev.front();
+      if (cudaEventQuery(e.second) != cudaSuccess) break;
+      float m = 0.f;
+      if (cudaEventElapsedTime(&m, e.first, e.second) == cudaSuccess) R->kt_ms += m;
+      R->kt_ev.pop_front();
+      R->kt_ev_free.push_back(e);
+    }
+    (void)cudaGetLastError();   // a not-ready query is not an error
+    std::pair<cudaEvent_t, cudaEvent_t> e;
+    if (!R->kt_ev_free.empty()) {
+      e = R->kt_ev_free.back();
+      R->kt_ev_free.pop_back();
+    } else {
+      GF_CHECK(c, cudaEventCreate(&e.first));
+      GF_CHECK(c, cudaEventCreate(&e.second));
+    }
+    R->kt_ev.push_back(e);
+    GF_CHECK(c, cudaEventRecord(e.first, c->s_kt));
     trace_mark(c, "dt_snapshot_end", s, c->s_dt);
     if (kt_begin(c, p->margin, c->s_kt)) return -1;
     GF_CHECK(c, cudaEventRecord(c->ev_disp, c->s_kt));
@@ -1118,7 +1210,7 @@ int gf_run_end(gf_ctx *ctx, gf_run_result *r) {
   float ms = 0.f;
   cudaEventElapsedTime(&ms, c->t0, c->t1);
   r->dt_ms = ms;
-  double kt_ms = 0.0;
+  double kt_ms = R->kt_ms;
   for (auto &e : R->kt_ev) {
     float m = 0.f;
     if (cudaEventElapsedTime(&m, e.first, e.second) == cudaSuccess) kt_ms += m;

@@ -88,6 +88,7 @@ struct KtScratch {
   DBuf cub_tmp;
   DBuf total;        // device copy of totals
   int64_t nbins_cap = 0;
+  bool sort_long_smem = false;   // k_sort_long's 64 KB dynamic shared memory opted in on this context's device
 };
 
 struct Ctx {
@@ -204,6 +205,13 @@ constexpr int64_t kMaxCells = (int64_t(1) << 24) - 1;  // enumeration-grid cell 
 
 // helpers implemented in gf_context.cu
 int ensure(Ctx *c, DBuf &b, size_t bytes, cudaStream_t s, bool keep = false);
+// rebuild-only kT scratch: from 2^24 spheres up (big_scratch) it is taken
+// from and returned to the stream-ordered pool on the kT stream
+// (cudaMallocAsync / cudaFreeAsync: no device-wide sync); below, ensure()
+inline bool big_scratch(const Ctx *c) { return c->n_sph >= (int64_t(1) << 24); }
+int ensure_scratch(Ctx *c, DBuf &b, size_t bytes, cudaStream_t s);
+int ensure_pooled(Ctx *c, DBuf &b, size_t bytes, cudaStream_t s);   // always from the pool
+int release_scratch(Ctx *c, DBuf &b, cudaStream_t s);
 // host -> device copy ordered on stream s and complete on return: the context's
 // streams are non-blocking, so a legacy-stream cudaMemcpy is not ordered
 // with kernels launched on them afterwards (its DMA may land after they read)

@@ -1275,11 +1275,11 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
   const double reach = c->kt_margin + skin;                         // small-small
   const double reach_big = c->kt_margin + skin_b;                   // big-small
   const double reach_bb = c->kt_margin + 2.0 * skin_b - skin;       // big-big
-  if (ensure(c, k.bin_key, 4 * (n + 1), s) || ensure(c, k.bin_key_alt, 4 * (n + 1), s) ||
-      ensure(c, k.sph_val, 4 * (n + 1), s) || ensure(c, k.sph_val_alt, 4 * (n + 1), s) ||
-      ensure(c, k.cursor, 4 * (3 * n + 1), s) || ensure(c, k.sc, 32 * (n + 1), s) ||
-      ensure(c, k.sm, 16 * (n + 1), s) || ensure(c, k.sf, 16 * (n + 1), s) ||
-      ensure(c, k.cand_n, 16, s) || ensure(c, k.cand_cnt, 8 * (n + 1), s) ||
+  if (ensure_scratch(c, k.bin_key, 4 * (n + 1), s) || ensure_scratch(c, k.bin_key_alt, 4 * (n + 1), s) ||
+      ensure_scratch(c, k.sph_val, 4 * (n + 1), s) || ensure_scratch(c, k.sph_val_alt, 4 * (n + 1), s) ||
+      ensure(c, k.cursor, 4 * (3 * n + 1), s) || ensure_scratch(c, k.sc, 32 * (n + 1), s) ||
+      ensure_scratch(c, k.sm, 16 * (n + 1), s) || ensure_scratch(c, k.sf, 16 * (n + 1), s) ||
+      ensure(c, k.cand_n, 16, s) || ensure_scratch(c, k.cand_cnt, 8 * (n + 1), s) ||
       ensure(c, k.ref, 24 * (n + 1), s) ||
       ensure(c, k.cell_start, sizeof(uint32_t) * (kMaxCells + 1), s) ||
       ensure(c, k.cell_end, sizeof(uint32_t) * (kMaxCells + 1), s))
@@ -1289,7 +1289,7 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
     if (ensure(c, k.cand, sizeof(uint2) * cap, s)) return -1;
     k.cand_cap = cap;
   }
-  if (ensure(c, k.cand_tmp, sizeof(uint2) * k.cand_cap, s)) return -1;   // released after big rebuilds
+  if (ensure_scratch(c, k.cand_tmp, sizeof(uint2) * k.cand_cap, s)) return -1;   // released after big rebuilds
   const Grid *gp = k.grid.as<Grid>();
   KtView v = kt_view(c, c->kt_margin);
   if (ensure(c, k.counts, sizeof(unsigned long long) * (3 * n + 1), s)) return -1;
@@ -1337,7 +1337,7 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
     const int64_t need = small + big_cap + 1;
     if (need > k.cand_cap) {
       const int64_t cap = need + need / 10 + 4096;
-      if (ensure(c, k.cand_tmp, sizeof(uint2) * cap, s) || ensure(c, k.cand, sizeof(uint2) * cap, s)) return -1;
+      if (ensure_scratch(c, k.cand_tmp, sizeof(uint2) * cap, s) || ensure(c, k.cand, sizeof(uint2) * cap, s)) return -1;
       k.cand_cap = cap;
     }
     // (a, b) halves of cand_tmp; cand holds the sort's alternate halves
@@ -1364,7 +1364,7 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
   }
   k.big_cap = big_cap;
   const int64_t total = k.n_cand;
-  if (ensure(c, k.cand_seg, 8 * (n + 1), s)) return -1;
+  if (ensure_scratch(c, k.cand_seg, 8 * (n + 1), s)) return -1;
   if (total) {
     // sort by a (only as many bits as slots need; b rides along), then each
     // sphere's segment by b
@@ -1386,11 +1386,12 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
     GF_CHECK(c, cudaMemsetAsync(big_n, 0, 8, s));
     k_sort_seg_short<<<grid_for(n), kBlock, 0, s>>>(n, k.cand_seg.as<unsigned long long>(), k.cand.as<uint2>(),
                                                    k.sa_cnt.as<uint32_t>(), big_n);
-    static bool smem_set = false;
-    if (!smem_set) {
+    // the opt-in is per device: tracked per context (a process may hold
+    // contexts on several devices, and kT and dT may sit on different ones)
+    if (!k.sort_long_smem) {
       GF_CHECK(c, cudaFuncSetAttribute(k_sort_long, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(sizeof(uint2) * kLongSeg)));
-      smem_set = true;
+      k.sort_long_smem = true;
     }
     k_sort_long<<<148, 1024, sizeof(uint2) * kLongSeg, s>>>(k.cand_seg.as<unsigned long long>(), k.cand.as<uint2>(),
                                                             k.sa_cnt.as<uint32_t>(), big_n);
@@ -1418,12 +1419,13 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
   }
   // at 2^24 spheres and up device memory is the limit: the rebuild-only
   // scratch (sort keys, cell-sorted copies, candidate counts and staging,
-  // ~170 B / sphere) is released and reallocated at the next rebuild
-  if (n >= (int64_t(1) << 24)) {
-    GF_CHECK(c, cudaStreamSynchronize(s));
+  // ~170 B / sphere) comes from the stream-ordered pool (ensure_scratch) and
+  // goes back to it here, ordered on the kT stream -- no device-wide
+  // synchronisation, so the dT stream never stalls on a rebuild
+  if (big_scratch(c)) {
     for (DBuf *b : {&k.bin_key, &k.bin_key_alt, &k.sph_val, &k.sph_val_alt, &k.sc, &k.sm, &k.sf, &k.cand_cnt,
                     &k.cand_seg, &k.cand_tmp})
-      b->release();
+      if (release_scratch(c, *b, s)) return -1;
   }
   k.cand_valid = true;
   k.cand_skin = c->skin_factor * c->kt_margin;

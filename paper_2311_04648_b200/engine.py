@@ -383,10 +383,7 @@ class Simulator:
         n = s.n_owners
         self._build_permutation()
         # mass-property templates: unique (mass, moi) rows
-        mm = np.concatenate([s.mass[:n, None], s.moi[:n]], axis=1) if n else np.zeros((0, 4))
-        tpl_rows, tpl_id = np.unique(mm, axis=0, return_inverse=True) if n else (np.zeros((0, 4)), np.zeros(0, int))
-        self._tpl_rows = np.ascontiguousarray(tpl_rows, dtype=np.float64)
-        self._tpl_id = np.ascontiguousarray(np.asarray(tpl_id).reshape(-1), dtype=np.uint32)
+        self._tpl_rows, self._tpl_id = self._mass_templates()
 
         self._ctx = _lib.Context(self.device, f32_state=(self.precision == "f32"))
         ctx, P = self._ctx, _lib.ptr
@@ -441,6 +438,36 @@ class Simulator:
         return False
 
     # -- host <-> device ----------------------------------------------------------
+    def _mass_templates(self):
+        """Unique (mass, moi) rows and each owner's row (what the device's
+        template table holds).  Clump owners normally carry their clump
+        template's mass properties: those are matched in one vectorised pass,
+        and only the rest (boundary owners, edited masses) go through a row
+        sort -- np.unique over every owner's row costs minutes at 1e8
+        owners."""
+        s = self.store
+        n = s.n_owners
+        if n == 0:
+            return np.zeros((0, 4)), np.zeros(0, np.uint32)
+        mass, moi = s.mass[:n], s.moi[:n]
+        tpl = np.asarray(s.owner_template[:n], dtype=np.int64)
+        nt = len(s.templates)
+        ref = np.full((nt + 1, 4), np.nan)
+        for t, ct in enumerate(s.templates):
+            ref[t, 0] = ct.mass
+            ref[t, 1:] = np.asarray(ct.moi, dtype=np.float64)
+        k = np.where(tpl >= 0, tpl, nt)
+        ok = (mass == ref[k, 0]) & np.all(moi == ref[k, 1:], axis=1)
+        rest = np.nonzero(~ok)[0]
+        rest_rows = np.concatenate([mass[rest, None], moi[rest]], axis=1)
+        cand = np.concatenate([ref[:nt], rest_rows], axis=0)
+        rows, inv = np.unique(cand, axis=0, return_inverse=True)
+        inv = np.asarray(inv).reshape(-1)
+        tid = np.empty(n, np.int64)
+        tid[ok] = inv[k[ok]]
+        tid[rest] = inv[nt + np.arange(rest.size)]
+        return np.ascontiguousarray(rows, dtype=np.float64), np.ascontiguousarray(tid, dtype=np.uint32)
+
     def _build_permutation(self):
         s = self.store
         n = s.n_owners
@@ -449,14 +476,21 @@ class Simulator:
             d2u = morton_order(s.positions())
         else:
             d2u = np.arange(n, dtype=np.int64)
-        u2d = np.empty(n, np.int64)
-        u2d[d2u] = np.arange(n, dtype=np.int64)
+        identity = not (self.reorder and n > 1)
+        u2d = d2u if identity else np.empty(n, np.int64)
+        if not identity:
+            u2d[d2u] = np.arange(n, dtype=np.int64)
         self._own_d2u, self._own_u2d = d2u, u2d
+        self._own_identity = identity
         # device sphere slots: grouped by device owner, geometry order within
         sph_owner_dev = u2d[s.geom_owner[self._sph_geom]] if self._sph_geom.size else np.zeros(0, np.int64)
-        sd2u = np.lexsort((np.arange(self._sph_geom.size), sph_owner_dev)).astype(np.int64)
-        su2d = np.empty(sd2u.size, np.int64)
-        su2d[sd2u] = np.arange(sd2u.size, dtype=np.int64)
+        if sph_owner_dev.size == 0 or np.all(sph_owner_dev[1:] >= sph_owner_dev[:-1]):
+            sd2u = np.arange(sph_owner_dev.size, dtype=np.int64)   # already grouped (no sort)
+            su2d = sd2u
+        else:
+            sd2u = np.argsort(sph_owner_dev, kind="stable").astype(np.int64)
+            su2d = np.empty(sd2u.size, np.int64)
+            su2d[sd2u] = np.arange(sd2u.size, dtype=np.int64)
         self._sph_d2u, self._sph_u2d = sd2u, su2d
 
     def _upload_tables(self):
@@ -478,7 +512,7 @@ class Simulator:
         s, ctx, P = self.store, self._ctx, _lib.ptr
         n = s.n_owners
         d = s.__dict__
-        p = self._own_d2u
+        p = slice(0, n) if self._own_identity else self._own_d2u
         keep = [_lib.carr(d["_voxel"][:n][p], np.uint64), _lib.carr(d["_subvoxel"][:n][p], np.uint16),
                 _lib.carr(d["_quat"][:n][p], np.float32), _lib.carr(d["_lin_vel"][:n][p], np.float64),
                 _lib.carr(d["_ang_vel"][:n][p], np.float64), _lib.carr(d["_owner_family"][:n][p], np.uint8),
@@ -511,7 +545,7 @@ class Simulator:
         af = np.zeros((n, 3))
         at = np.zeros((n, 3))
         self._ctx.call("gf_download_accumulators", P(af), P(at))
-        p = self._own_d2u
+        p = slice(0, n) if self._own_identity else self._own_d2u
         d["_voxel"][:n][p] = vox
         d["_subvoxel"][:n][p] = sub
         d["_quat"][:n][p] = quat

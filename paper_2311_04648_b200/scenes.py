@@ -118,7 +118,7 @@ def tiled_bed(src: Simulator, tx: int, ty: int, *, precision: str = "f32", devic
     laid out at the bed pitch 12 D, the floor and the four outer walls bound
     the whole array (inner walls removed; every grain is at least its radius
     from its old wall plane, so copies meet without overlap)."""
-    from .core import OWNER_CLUMP, decode_position
+    from .core import OWNER_CLUMP, decode_position, encode_position
     s = src.store
     n = s.n_owners
     s.voxel  # sync the host mirror
@@ -131,22 +131,51 @@ def tiled_bed(src: Simulator, tx: int, ty: int, *, precision: str = "f32", devic
     lo, hi = s.domain.lo, s.domain.hi
     dom = Domain((-tx * bed_half - 0.2 * bed_half, -ty * bed_half - 0.2 * bed_half, float(lo[2])),
                  (tx * bed_half + 0.2 * bed_half, ty * bed_half + 0.2 * bed_half, float(hi[2])))
-    sim = Simulator(dom, precision=precision, device=device)
+    sim = Simulator(dom, precision=precision, device=device, reorder=False)
     grain = sim.load_material(dict(CRATER_MATERIAL))
     wall = sim.load_material(dict(CRATER_MATERIAL))
     for t in s.templates:
         sim.load_clump_template(t)
     offsets = [(-tx * bed_half + (2 * ix + 1) * bed_half, -ty * bed_half + (2 * iy + 1) * bed_half)
                for iy in range(ty) for ix in range(tx)]
-    dd = sim.store.__dict__
-    for t in range(len(s.templates)):
-        sel = np.nonzero(clump & (tpl == t))[0]
-        if not sel.size:
-            continue
-        for ox, oy in offsets:
-            ids = np.asarray(sim.add_clumps(t, pos[sel] + np.array([ox, oy, 0.0])), dtype=np.int64)
-            for name in ("_lin_vel", "_ang_vel", "_quat", "_owner_family"):
-                dd[name][ids] = d[name][sel]
+    # owners tile by tile, each tile in the source's device (Morton) order:
+    # the copy needs no reordering of its own (reorder=False above), and
+    # every tile is a block copy of the source rows (only the positions are
+    # re-encoded), so the 150M-sphere setup does no sort, permutation or
+    # per-owner Python work
+    order = np.asarray(getattr(src, "_own_d2u", np.arange(n)), dtype=np.int64)
+    order = order[clump[order]]
+    n_c = order.size
+    T = len(offsets)
+    ng_all = s.n_geoms
+    go = d["_geom_owner"][:ng_all]
+    gsort = np.argsort(go, kind="stable")
+    gcnt = np.bincount(go, minlength=n)
+    gstart = np.concatenate([[0], np.cumsum(gcnt)])
+    kk = gcnt[order]
+    gidx = gsort[np.repeat(gstart[order], kk) + (np.arange(int(kk.sum())) - np.repeat(np.cumsum(kk) - kk, kk))]
+    n_g = gidx.size
+    st = sim.store
+    st.reserve(n_c * T + 8, n_g * T + 8)
+    dd = st.__dict__
+    own_rows = {name: d[name][order] for name in ("_owner_kind", "_owner_template", "_owner_family", "_quat",
+                                                  "_lin_vel", "_ang_vel", "_mass", "_moi")}
+    geo_rows = {name: d[name][gidx] for name in ("_geom_kind", "_geom_material", "_geom_params")}
+    local_owner = np.repeat(np.arange(n_c, dtype=np.int64), kk)
+    p0 = pos[order]
+    for ti, (ox, oy) in enumerate(offsets):
+        o0, g0 = st.n_owners, st.n_geoms
+        vox, sub = encode_position(p0 + np.array([ox, oy, 0.0]), st.domain)
+        osl, gsl = slice(o0, o0 + n_c), slice(g0, g0 + n_g)
+        dd["_voxel"][osl] = vox
+        dd["_subvoxel"][osl] = sub
+        for name, rows in own_rows.items():
+            dd[name][osl] = rows
+        dd["_geom_owner"][gsl] = local_owner + o0
+        for name, rows in geo_rows.items():
+            dd[name][gsl] = rows
+        st.n_owners += n_c
+        st.n_geoms += n_g
     hx, hy = tx * bed_half, ty * bed_half
     walls = [("plane", (0, 0, 0), (0, 0, 1), wall),
              ("plane", (-hx, 0, 0), (1, 0, 0), wall), ("plane", (hx, 0, 0), (-1, 0, 0), wall),
