@@ -244,6 +244,57 @@ int gf_trip_word(gf_ctx *ctx, void *word, int mode);
 /* block until the context's dT stream is idle */
 int gf_sync(gf_ctx *ctx);
 
+/* ---- reference-shaped entry points (host buffers in the reference's own
+ * layouts; one call = upload, one kernel pass on the context's device, download;
+ * fp64 arithmetic statement by statement like numba fastmath=False) ---------- */
+/* make_contact_kernel's sweep (forces.py:547-593) with the context's force
+ * model (built-in Hertz-Mindlin, W = 4, or the NVRTC model of
+ * gf_set_force_model): per entry k of (kind, slot_a, slot_b) the contact
+ * geometry (_kernels.py:441-486), pair kinematics (forces.py:55-79) and the
+ * core; wild (n, W) float32 updated in place; out_ft (n, 6) = force on A +
+ * torque-only force, depth (n), cp (n, 3); *touching = 2 per touching
+ * sphere-sphere entry, 1 per touching wall entry.  sph_centers (m, 3)
+ * float64, sph_radii (m) float32, tri_world (n_t, 9), ana_world (n_a, 8),
+ * owner_pos / lin_vel / ang_vel_global (n_o, 3) float64, mass (n_o). */
+int gf_contact_forces(gf_ctx *ctx, int64_t n, const uint8_t *kind, const int64_t *slot_a,
+                      const int64_t *slot_b, const int64_t *owner_a, const int64_t *owner_b,
+                      const uint8_t *mat_a, const uint8_t *mat_b, int64_t n_sph,
+                      const double *sph_centers, const float *sph_radii, int64_t n_tri,
+                      const double *tri_world, int64_t n_ana, const double *ana_world,
+                      const uint8_t *ana_kind, int64_t n_owner, const double *owner_pos,
+                      const double *lin_vel, const double *ang_vel_global, const double *mass,
+                      int n_mat, int n_rows, const double *pair_stack, float *wild, int W, double ts,
+                      double sim_time, double *out_ft, double *depth, double *cp, int64_t *touching);
+/* the model core over n contexts (forces.py:82-87 scalar contract; the
+ * ForceModel.core / jit_core / evaluate surface, forces.py:360-405):
+ * args (n, 15) = overlap, ts, sim_time, b2a xyz, v xyz, wr xyz, mass_eff, ra,
+ * rb; mats (n, 2) int32; wild (n, W) in place; out (n, 6). */
+int gf_eval_core(gf_ctx *ctx, int64_t n, const double *args, const int32_t *mats, int n_mat, int n_rows,
+                 const double *pair_stack, float *wild, int W, double *out);
+/* reduce_to_owners (_kernels.py:515-545): per owner, the contributions in the
+ * reference loop's order (+F / r_a x (F + tof) on A, the negation at r_b on
+ * B); mass != NULL adds mass * gravity3 afterwards (forces.py:600-614).
+ * forces / tofs / cps (n, 3); owner_pos (n_o, 3); out (n_o, 3) each. */
+int gf_reduce(gf_ctx *ctx, int64_t n, const int64_t *owner_a, const int64_t *owner_b, const double *forces,
+              const double *tofs, const double *cps, int64_t n_owner, const double *owner_pos,
+              const double *mass, const double *gravity3, double *acc_force, double *acc_torque);
+/* integrate_and_refresh (_kernels.py:548-670): semi-implicit Euler step,
+ * re-encode (voxel (n) uint64, sub (n, 3) uint16) and decode, sphere centres
+ * (n_s, 3) of sph_geom through geom_params (n_geom, 9) float32 /
+ * geom_owner; *bad / *oob = first speeding / out-of-domain owner or -1.
+ * fixed_flag / prescribed_flag (256), lv_mask / av_mask (256, 3) uint8,
+ * lv_val / av_val (256, 3) float64; ext_force / ext_torque may be NULL. */
+int gf_integrate_and_refresh(gf_ctx *ctx, double h, const double *g3, int64_t n, double *owner_pos,
+                             float *quat, double *lin_vel, double *ang_vel, const double *mass,
+                             const double *moi, const double *acc_force, const double *acc_torque,
+                             const double *ext_force, const double *ext_torque, const uint8_t *family,
+                             const uint8_t *fixed_flag, const uint8_t *lv_mask, const double *lv_val,
+                             const uint8_t *av_mask, const double *av_val, const uint8_t *prescribed_flag,
+                             double v_err, const double *lo3, const double *hi3, double edge,
+                             uint64_t *voxel, uint16_t *sub, int64_t n_s, const int64_t *sph_geom,
+                             int64_t n_geom, const float *geom_params, const int64_t *geom_owner,
+                             double *sph_centers, int64_t *bad, int64_t *oob);
+
 /* per-kernel device timing of subsequent gf_run calls (CUDA events on the dT
  * stream); out6 = cumulative ms of {contact phase, k_heavy, k_integrate, kT},
  * the number of profiled steps, then the ms of the fused sphere-sphere kernel

@@ -60,6 +60,7 @@ EXPORTS = (
     "gf_nvrtc_compile", "gf_run_begin", "gf_step_forces", "gf_step_integrate", "gf_run_end",
     "gf_set_decomposition", "gf_halo_record_bytes", "gf_stream", "gf_pack_state", "gf_unpack_state",
     "gf_pack_forces", "gf_add_forces", "gf_trip_word", "gf_sync",
+    "gf_contact_forces", "gf_eval_core", "gf_reduce", "gf_integrate_and_refresh",
 )
 
 _lib = None

@@ -199,3 +199,84 @@ def merge_history(old: ContactArray, new_pairs: ContactArray) -> ContactArray:
     for i, name in enumerate(names):
         out.wildcards[name] = res[:, i].copy()
     return out
+
+
+def build_bins(centers, radii, bin_size, margin: float = 0.0):
+    """Uniform-grid CSR of the margin-enlarged sphere boxes (broadphase.py:
+    303-323; exposed for tests -- detection itself enumerates centre cells,
+    csrc/gf_kt.cu).  The per-sphere bin ranges come from the device
+    (gf_bin_ranges on the reference grid); the CSR keeps the reference's
+    stable sphere order within a bin.  Returns (grid_lo, inv_bin_size,
+    bins_per_axis, starts, entries)."""
+    centers = np.asarray(centers, dtype=np.float64).reshape(-1, 3)
+    radii = np.asarray(radii, dtype=REAL).reshape(-1)
+    r_max = float(radii.max()) if radii.size else 0.0
+    min_bin = 2.0 * (r_max + margin)
+    if bin_size < min_bin:
+        raise ValidationError(f"bin_size {bin_size} below max enlarged sphere diameter {min_bin}")
+    m = centers.shape[0]
+    snap = DetectionSnapshot(
+        sph_center=centers, sph_radius=radii, sph_geom=np.arange(m, dtype=np.int64),
+        sph_owner=np.arange(m, dtype=np.int64), sph_family=np.zeros(m, np.uint8),
+        tri_world=np.zeros((0, 9)), tri_geom=np.zeros(0, np.int64), tri_owner=np.zeros(0, np.int64),
+        tri_family=np.zeros(0, np.uint8), ana_world=np.zeros((0, 8)), ana_kind=np.zeros(0, np.uint8),
+        ana_geom=np.zeros(0, np.int64), ana_owner=np.zeros(0, np.int64), ana_family=np.zeros(0, np.uint8),
+        mask=np.ones((256, 256), dtype=bool))
+    _, _, _, glo, inv, nb = detect_contacts_raw(snap, margin, bin_size)
+    ranges = np.zeros((m, 6), np.int64)
+    if m:
+        _util_ctx(0).call("gf_bin_ranges", C.c_double(margin), _lib.ptr(ranges))
+    # (bin, sphere) registrations, stable in sphere order within a bin (_kernels.py:270-283)
+    bins, owners = [], []
+    for i in range(m):
+        xs = np.arange(ranges[i, 0], ranges[i, 1] + 1)
+        ys = np.arange(ranges[i, 2], ranges[i, 3] + 1)
+        zs = np.arange(ranges[i, 4], ranges[i, 5] + 1)
+        b = ((zs[:, None, None] * nb[1] + ys[None, :, None]) * nb[0] + xs[None, None, :]).reshape(-1)
+        bins.append(b)
+        owners.append(np.full(b.size, i, np.int64))
+    nbins = int(nb[0] * nb[1] * nb[2])
+    b = np.concatenate(bins) if bins else np.zeros(0, np.int64)
+    o = np.concatenate(owners) if owners else np.zeros(0, np.int64)
+    order = np.argsort(b, kind="stable")
+    starts = np.zeros(nbins + 1, np.int64)
+    np.cumsum(np.bincount(b, minlength=nbins), out=starts[1:])
+    return glo, inv, nb, starts, o[order]
+
+
+def closest_point_on_triangle(p, tri):
+    """Closest point on the closed triangle and its distance to p
+    (broadphase.py:291-300; Ericson RTCD 5.1.5, the branch order of
+    _kernels.py:159-194 and of the device closest_on_tri)."""
+    tri = np.asarray(tri, dtype=np.float64).reshape(3, 3)
+    area = 0.5 * np.linalg.norm(np.cross(tri[1] - tri[0], tri[2] - tri[0]))
+    if area <= 0.0:
+        raise ValidationError("degenerate triangle")
+    p = np.asarray(p, dtype=np.float64).reshape(3)
+    a, b, c = tri
+    ab, ac, ap = b - a, c - a, p - a
+    d1, d2 = float(ab @ ap), float(ac @ ap)
+    if d1 <= 0.0 and d2 <= 0.0:
+        q = a
+    else:
+        bp = p - b
+        d3, d4 = float(ab @ bp), float(ac @ bp)
+        vc = d1 * d4 - d3 * d2
+        cp = p - c
+        d5, d6 = float(ab @ cp), float(ac @ cp)
+        vb = d5 * d2 - d1 * d6
+        va = d3 * d6 - d5 * d4
+        if d3 >= 0.0 and d4 <= d3:
+            q = b
+        elif vc <= 0.0 and d1 >= 0.0 and d3 <= 0.0:
+            q = a + (d1 / (d1 - d3)) * ab
+        elif d6 >= 0.0 and d5 <= d6:
+            q = c
+        elif vb <= 0.0 and d2 >= 0.0 and d6 <= 0.0:
+            q = a + (d2 / (d2 - d6)) * ac
+        elif va <= 0.0 and (d4 - d3) >= 0.0 and (d5 - d6) >= 0.0:
+            q = b + ((d4 - d3) / ((d4 - d3) + (d5 - d6))) * (c - b)
+        else:
+            denom = 1.0 / (va + vb + vc)
+            q = a + ab * (vb * denom) + ac * (vc * denom)
+    return np.array(q, dtype=np.float64), float(np.linalg.norm(p - q))

@@ -449,6 +449,9 @@ gf_ctx *gf_create(int device, uint32_t flags) {
   if (const char *sb = std::getenv("GF_SKIN_BIG")) c->skin_big_factor = std::atof(sb);
   if (c->skin_big_factor < c->skin_factor) c->skin_big_factor = c->skin_factor;
   if (const char *sp = std::getenv("GF_SS_SPLIT")) c->ss_split = std::atoi(sp);
+  if (const char *sr = std::getenv("GF_SS_RED")) c->ss_red = std::atoi(sr);
+  cudaDeviceGetAttribute(&c->n_sm, cudaDevAttrMultiProcessorCount, device);
+  if (c->n_sm <= 0) c->n_sm = 148;
   if (const char *pd = std::getenv("GF_PDL")) c->pdl = std::atoi(pd);
   cudaEventCreate(&c->t0);
   cudaEventCreate(&c->t1);

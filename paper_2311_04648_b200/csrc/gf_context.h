@@ -155,6 +155,8 @@ struct Ctx {
   double skin_big_factor = 8.0;  // skin of big spheres (radius > r_cut), >= skin_factor (GF_SKIN_BIG)
   uint64_t world_version = 0;   // bumped whenever mesh / analytic world transforms are recomputed
   int tlist_words = 5;       // words per contact of the touching lists (1 on the fused path)
+  int n_sm = 148;             // multiprocessors of the device (grid sizing)
+  int ss_red = 1;            // fused sphere-sphere kernel: staged fixed-point rows (GF_SS_RED=0: per-word REDs)
   int ss_split = 0;          // throughput build: split narrow/force sphere-sphere kernels (GF_SS_SPLIT=1)
   // programmatic dependent launch on the dT chain (GF_PDL=1): measured slower
   // on the bench bed (the chain's kernels already fill the GPU), off by default
@@ -171,6 +173,7 @@ struct Ctx {
   // NVRTC user force model (gf_nvrtc.cu)
   bool user_model = false;
   void *user_fn_f64 = nullptr, *user_fn_f32 = nullptr, *user_fn_ss = nullptr, *user_fn_walls = nullptr;
+  void *user_fn_ref = nullptr, *user_fn_batch = nullptr;   // gf_contact_forces / gf_eval_core of a user model
   // per-kernel device timing (enabled by gf_set_profiling)
   bool prof = false;
   std::vector<cudaEvent_t> prof_ev;   // kProfEv per profiled step: start, contacts, heavy, integrate,

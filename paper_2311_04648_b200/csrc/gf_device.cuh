@@ -447,13 +447,28 @@ __device__ __forceinline__ void force_entry(const DtView &v, uint32_t k, double 
   }
 }
 
+// Issue the staged fixed-point rows red[6 * i + q] of owners own[i], i < n / 6:
+// consecutive lanes take consecutive words, so each RED instruction touches
+// the rows of ~5 owners (contiguous 48 B each).  Warp-collective; leaves the
+// buffers free for reuse.
+__device__ __forceinline__ void red_rows(const DtView &v, const long long *red, const uint32_t *own, int n,
+                                         int lane) {
+  for (int j = lane; j < n; j += 32) {
+    const int i = j / 6, q = j - 6 * i;
+    atomicAdd(reinterpret_cast<unsigned long long *>(v.own.facc) + 6 * size_t(own[i]) + q,
+              (unsigned long long)red[j]);
+  }
+  __syncwarp();
+}
+
 // A-side contributions of a warp's contacts (entries in A-sorted contact
 // order, so equal A owners sit in consecutive lanes): each run's int64
 // fixed-point words are summed in registers (exact) and added by the run's
 // head lane; boundary owners (scale 0) take fp64 atomics.  Every lane of the
 // warp must call it; `out` = force (3), `ta` = torque on A (3).
 __device__ __forceinline__ void a_side_sums(const DtView &v, bool use_a, uint32_t oa, double sa_f, double sa_t,
-                                            const float *out, const float *ta, int lane) {
+                                            const float *out, const float *ta, int lane,
+                                            long long *red = nullptr, uint32_t *own = nullptr) {
   const bool fixed_a = use_a && sa_f > 0.0;
   if (use_a && !fixed_a) {   // boundary owner: fp64 atomics, not aggregated
     unsigned long long *fa = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(oa));
@@ -485,12 +500,28 @@ __device__ __forceinline__ void a_side_sums(const DtView &v, bool use_a, uint32_
       if (lane + int(off) <= run_end) acc[q] += o;
     }
   }
-  if (head && fixed_a) {
-    unsigned long long *fa = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(oa));
+  if (red == nullptr) {
+    if (head && fixed_a) {
+      unsigned long long *fa = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(oa));
 #pragma unroll
-    for (int q = 0; q < 6; ++q) atomicAdd(fa + q, (unsigned long long)acc[q]);
+      for (int q = 0; q < 6; ++q) atomicAdd(fa + q, (unsigned long long)acc[q]);
+    }
+    return;
   }
+  // staged: the run heads' six words go through the warp's shared buffer so
+  // that one RED instruction covers ~5 owners' contiguous 48-byte rows (two
+  // sectors each) instead of one word of 32 scattered owners
+  const unsigned hf = __ballot_sync(0xffffffffu, head && fixed_a);
+  if (head && fixed_a) {
+    const int h = __popc(hf & ((1u << lane) - 1u));
+    own[h] = oa;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) red[6 * h + q] = acc[q];
+  }
+  __syncwarp();
+  red_rows(v, red, own, 6 * __popc(hf), lane);
 }
+
 
 // Fused sphere-sphere loop of the throughput build for a user model `Core`
 // (NVRTC-compiled, gf_nvrtc.cu): every entry of the sphere-sphere block --
@@ -609,6 +640,153 @@ __device__ __forceinline__ void forces_loop(const DtView &v, double ts, double s
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
        i += (unsigned long long)gridDim.x * blockDim.x)
     force_entry<VelT, Core>(v, Core::kAllEntries ? uint32_t(i) : list[i], ts, sim_time);
+}
+
+// ---------------------------------------------------------------------------
+// Reference-shaped entry points (include/gf_b200.h gf_contact_forces /
+// gf_eval_core): the reference's own array layouts, one thread per contact,
+// the model core `Core` (built-in Hertz-Mindlin or an NVRTC user model).
+// ---------------------------------------------------------------------------
+struct RefContacts {
+  int64_t n;
+  const uint8_t *kind;
+  const int64_t *slot_a, *slot_b, *owner_a, *owner_b;
+  const uint8_t *mat_a, *mat_b;
+  const double *sph_centers;   // (m, 3)
+  const float *sph_radii;      // (m,)
+  const double *tri_world;     // (n_t, 9)
+  const double *ana_world;     // (n_a, 8)
+  const uint8_t *ana_kind;
+  const double *owner_pos, *lin_vel, *ang_vel_global, *mass;   // (n_o, 3) / (n_o,)
+  Materials mat;
+  float *wild;                 // (n, W)
+  int W;
+  double ts, sim_time;
+  double *out_ft, *depth, *cp; // (n, 6), (n,), (n, 3)
+  unsigned long long *touching;
+};
+
+// contact_geom_one (_kernels.py:441-486) on the reference arrays
+__device__ __forceinline__ void ref_geom_one(const RefContacts &r, int kd, int64_t i, int64_t j, double &depth,
+                                             double &bx, double &by, double &bz, double &px, double &py,
+                                             double &pz, double &rb) {
+  const double cx = r.sph_centers[3 * i], cy = r.sph_centers[3 * i + 1], cz = r.sph_centers[3 * i + 2];
+  const double ra = double(r.sph_radii[i]);
+  if (kd == 0) {
+    const double dx = cx - r.sph_centers[3 * j], dy = cy - r.sph_centers[3 * j + 1],
+                 dz = cz - r.sph_centers[3 * j + 2];
+    const double d = sqrt(dx * dx + dy * dy + dz * dz);
+    rb = double(r.sph_radii[j]);
+    if (d < 1e-300) {
+      depth = ra + rb; bx = 0.0; by = 0.0; bz = 1.0;
+      px = cx; py = cy; pz = cz;
+      return;
+    }
+    const double inv = 1.0 / d;
+    bx = dx * inv; by = dy * inv; bz = dz * inv;
+    depth = ra + rb - d;
+  } else if (kd == 1) {
+    const double *T = r.tri_world + 9 * j;
+    double qx, qy, qz;
+    closest_on_tri(cx, cy, cz, T, qx, qy, qz);
+    const double dx = cx - qx, dy = cy - qy, dz = cz - qz;
+    const double d = sqrt(dx * dx + dy * dy + dz * dz);
+    if (d < 1e-300) {
+      const double e1x = T[3] - T[0], e1y = T[4] - T[1], e1z = T[5] - T[2];
+      const double e2x = T[6] - T[0], e2y = T[7] - T[1], e2z = T[8] - T[2];
+      bx = e1y * e2z - e1z * e2y; by = e1z * e2x - e1x * e2z; bz = e1x * e2y - e1y * e2x;
+      const double nn = sqrt(bx * bx + by * by + bz * bz);
+      bx /= nn; by /= nn; bz /= nn;
+    } else {
+      const double inv = 1.0 / d;
+      bx = dx * inv; by = dy * inv; bz = dz * inv;
+    }
+    depth = ra - d;
+    rb = kFlatRadius;
+  } else {
+    double gap;
+    analytic_gap(r.ana_kind[j], r.ana_world + 8 * j, cx, cy, cz, gap, bx, by, bz, rb);
+    depth = ra - gap;
+  }
+  const double half = ra - 0.5 * depth;
+  px = cx - bx * half; py = cy - by * half; pz = cz - bz * half;
+}
+
+// one entry of make_contact_kernel's sweep (forces.py:553-591)
+template <typename Core>
+__device__ __forceinline__ void ref_contact_entry(const RefContacts &r, int64_t k) {
+  const int kd = r.kind[k];
+  const int64_t sa = r.slot_a[k];
+  double dep, bx, by, bz, px, py, pz, rb;
+  ref_geom_one(r, kd, sa, r.slot_b[k], dep, bx, by, bz, px, py, pz, rb);
+  r.depth[k] = dep;
+  r.cp[3 * k] = px; r.cp[3 * k + 1] = py; r.cp[3 * k + 2] = pz;
+  const int64_t oa = r.owner_a[k], ob = r.owner_b[k];
+  const double *pa = r.owner_pos + 3 * oa, *pb = r.owner_pos + 3 * ob;
+  const double *va = r.lin_vel + 3 * oa, *vb = r.lin_vel + 3 * ob;
+  const double *wa = r.ang_vel_global + 3 * oa, *wb = r.ang_vel_global + 3 * ob;
+  const double rax = px - pa[0], ray = py - pa[1], raz = pz - pa[2];
+  const double rbx = px - pb[0], rby = py - pb[1], rbz = pz - pb[2];
+  const double rotax = wa[1] * raz - wa[2] * ray, rotay = wa[2] * rax - wa[0] * raz,
+               rotaz = wa[0] * ray - wa[1] * rax;
+  const double rotbx = wb[1] * rbz - wb[2] * rby, rotby = wb[2] * rbx - wb[0] * rbz,
+               rotbz = wb[0] * rby - wb[1] * rbx;
+  CoreArgs arg;
+  arg.overlap = dep; arg.ts = r.ts; arg.sim_time = r.sim_time;
+  arg.b2ax = bx; arg.b2ay = by; arg.b2az = bz;
+  arg.vx = (va[0] + rotax) - (vb[0] + rotbx);
+  arg.vy = (va[1] + rotay) - (vb[1] + rotby);
+  arg.vz = (va[2] + rotaz) - (vb[2] + rotbz);
+  arg.wrx = rotbx - rotax; arg.wry = rotby - rotay; arg.wrz = rotbz - rotaz;
+  const double ma = r.mass[oa], mb = r.mass[ob];
+  arg.mass_eff = (ma * mb) / (ma + mb);
+  arg.ra = double(r.sph_radii[sa]); arg.rb = rb;
+  arg.mat_a = r.mat_a[k]; arg.mat_b = r.mat_b[k];
+  arg.pair = r.mat.pair; arg.n_mat = r.mat.n_mat;
+  arg.wild = r.wild + size_t(r.W) * k;
+  arg.M = &r.mat;
+  double out[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  Core::eval(arg, out);
+  for (int q = 0; q < 6; ++q) r.out_ft[6 * k + q] = out[q];
+  if (dep > 0.0) atomicAdd(r.touching, kd == 0 ? 2ull : 1ull);
+}
+
+template <typename Core>
+__device__ __forceinline__ void ref_contacts_loop(const RefContacts &r) {
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < r.n; k += int64_t(gridDim.x) * blockDim.x)
+    ref_contact_entry<Core>(r, k);
+}
+
+// Batched model core (the reference core's scalar signature, forces.py:82-87):
+// args row = overlap, ts, sim_time, b2a xyz, v xyz, wr xyz, mass_eff, ra, rb
+struct CoreBatch {
+  int64_t n;
+  const double *args;    // (n, 15)
+  const int *mats;       // (n, 2) int32
+  Materials mat;
+  float *wild;           // (n, W)
+  int W;
+  double *out;           // (n, 6)
+};
+
+template <typename Core>
+__device__ __forceinline__ void core_batch_loop(const CoreBatch &b) {
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < b.n; k += int64_t(gridDim.x) * blockDim.x) {
+    const double *x = b.args + 15 * k;
+    CoreArgs arg;
+    arg.overlap = x[0]; arg.ts = x[1]; arg.sim_time = x[2];
+    arg.b2ax = x[3]; arg.b2ay = x[4]; arg.b2az = x[5];
+    arg.vx = x[6]; arg.vy = x[7]; arg.vz = x[8];
+    arg.wrx = x[9]; arg.wry = x[10]; arg.wrz = x[11];
+    arg.mass_eff = x[12]; arg.ra = x[13]; arg.rb = x[14];
+    arg.mat_a = b.mats[2 * k]; arg.mat_b = b.mats[2 * k + 1];
+    arg.pair = b.mat.pair; arg.n_mat = b.mat.n_mat;
+    arg.wild = b.wild + size_t(b.W) * k;
+    arg.M = &b.mat;
+    double out[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    Core::eval(arg, out);
+    for (int q = 0; q < 6; ++q) b.out[6 * k + q] = out[q];
+  }
 }
 
 }  // namespace gf

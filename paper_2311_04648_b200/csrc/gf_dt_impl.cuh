@@ -228,12 +228,15 @@ __device__ __forceinline__ bool ss_geom(const DtView &v, uint32_t a, uint32_t b,
 // Every lane of the warp must call it.
 __device__ __forceinline__ void ss_force_warp(const DtView &v, bool live, uint32_t a, uint32_t b, uint32_t k,
                                               const SsGeom &g, float ts, const float (*s_mat)[kSmemMat],
-                                              bool smem, int lane) {
+                                              bool smem, int lane, long long *red = nullptr,
+                                              uint32_t *own = nullptr) {
   float out[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   float ta[3] = {0.f, 0.f, 0.f};
   uint32_t oa = 0xFFFFFFFFu;
   double sa_f = 0.0, sa_t = 0.0;
-  bool use_a = false;
+  bool use_a = false, b_row = false;
+  long long rb6[6];
+  uint32_t ob_ = 0;
   if (live) {
     // one load round: kinematics records (mass, scales, flags included) and
     // the history row
@@ -249,6 +252,7 @@ __device__ __forceinline__ void ss_force_warp(const DtView &v, bool live, uint32
     }
     oa = kin_owner(ka);
     const uint32_t ob = kin_owner(kb);
+    ob_ = ob;
     // contact point p = cA - b (ra - depth / 2); lever arms p - pos_a, p - pos_b
     const float ha = g.ra - 0.5f * depth;
     const float rax = ka.r.x - bx * ha, ray = ka.r.y - by * ha, raz = ka.r.z - bz * ha;
@@ -277,9 +281,18 @@ __device__ __forceinline__ void ss_force_warp(const DtView &v, bool live, uint32
     const float tx = out[0] + out[3], ty = out[1] + out[4], tz = out[2] + out[5];
     ta[0] = ray * tz - raz * ty; ta[1] = raz * tx - rax * tz; ta[2] = rax * ty - ray * tx;
     const float tb[3] = {rby * tz - rbz * ty, rbz * tx - rbx * tz, rbx * ty - rby * tx};
-    // B side: one atomic per word (B owners are scattered)
+    // B side: one atomic per word (B owners are scattered); staged (red !=
+    // nullptr): fixed-point rows through the warp's shared buffer below
     if (v.acc_all || !(kin_flags(kb) & kKinPassive)) {
       const double sbf = kin_fscale(kb), sbt = kin_tscale(kb);
+      if (red != nullptr && sbf > 0.0) {
+        b_row = true;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          rb6[q] = __double2ll_rn(-double(out[q]) * sbf);
+          rb6[3 + q] = __double2ll_rn(-double(tb[q]) * sbt);
+        }
+      } else {
       unsigned long long *fb = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(ob));
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
@@ -291,12 +304,25 @@ __device__ __forceinline__ void ss_force_warp(const DtView &v, bool live, uint32
           atomicAdd(reinterpret_cast<double *>(fb + 3 + q), -double(tb[q]));
         }
       }
+      }
     }
     use_a = v.acc_all || !(kin_flags(ka) & kKinPassive);
     sa_f = kin_fscale(ka);
     sa_t = kin_tscale(ka);
   }
-  a_side_sums(v, use_a, oa, sa_f, sa_t, out, ta, lane);
+  if (red != nullptr) {
+    // B rows, compacted: one RED instruction covers ~5 owners' rows
+    const unsigned bm = __ballot_sync(0xffffffffu, b_row);
+    if (b_row) {
+      const int h = __popc(bm & ((1u << lane) - 1u));
+      own[h] = ob_;
+#pragma unroll
+      for (int q = 0; q < 6; ++q) red[6 * h + q] = rb6[q];
+    }
+    __syncwarp();
+    red_rows(v, red, own, 6 * __popc(bm), lane);
+  }
+  a_side_sums(v, use_a, oa, sa_f, sa_t, out, ta, lane, red, own);
 }
 
 // Throughput build, built-in Hertz-Mindlin, split form: force phase over the
@@ -337,19 +363,23 @@ static __global__ void __launch_bounds__(256, 4) k_forces_f32(DtView v, double t
 // touching list never goes through HBM.
 constexpr int kSsWarps = 8;
 
-template <int kSsPerLane, int kMinBlocks>
+template <int kSsPerLane, int kMinBlocks, bool kStaged = true>
 static __global__ void __launch_bounds__(256, kMinBlocks) k_contacts_ss(DtView v, double ts_d, unsigned long long step) {
   constexpr int kSsQueue = 32 * (kSsPerLane + 1);
   __shared__ float s_mat[5][kSmemMat];
+  // staged fixed-point rows of the warp's force batch (B side, then A side)
+  __shared__ long long s_red[kStaged ? kSsWarps : 1][kStaged ? 192 : 1];
+  __shared__ uint32_t s_own[kSsWarps][32];   // [0][0] doubles as the block's live flag at entry
   __shared__ uint32_t q_a[kSsWarps][kSsQueue], q_b[kSsWarps][kSsQueue], q_k[kSsWarps][kSsQueue];
   __shared__ float q_g[7][kSsWarps][kSsQueue];
-  __shared__ int s_live;
   const bool smem = stage_materials(v, s_mat);   // static tables: before the predecessor drains
   pdl_wait();
   pdl_launch();
-  if (threadIdx.x == 0) s_live = !v.st->err && v.st->dd_trip >= step;
+  if (threadIdx.x == 0) s_own[0][0] = !v.st->err && v.st->dd_trip >= step;
   __syncthreads();
-  if (!s_live) return;
+  const bool block_live = s_own[0][0] != 0;
+  __syncthreads();
+  if (!block_live) return;
   const float ts = float(ts_d);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned long long n_ss = v.seg[v.n_sph];
@@ -367,7 +397,8 @@ static __global__ void __launch_bounds__(256, kMinBlocks) k_contacts_ss(DtView v
       g.dx = q_g[0][warp][lane]; g.dy = q_g[1][warp][lane]; g.dz = q_g[2][warp][lane];
       g.d = q_g[3][warp][lane]; g.num = q_g[4][warp][lane]; g.ra = q_g[5][warp][lane]; g.rb = q_g[6][warp][lane];
     }
-    ss_force_warp(v, live, a, b, k, g, ts, s_mat, smem, lane);
+    ss_force_warp(v, live, a, b, k, g, ts, s_mat, smem, lane, kStaged ? s_red[warp] : nullptr,
+                  kStaged ? s_own[warp] : nullptr);
     __syncwarp();
     // shift the rest of the queue down
     const int rest = qn - take;
@@ -833,34 +864,37 @@ int dt_forces_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
       k_touch_ss<<<unsigned((v.n_acs + per_block - 1) / per_block), 256, 0, s>>>(
           v, reinterpret_cast<uint4 *>(list0), tn, (unsigned long long)a.step);
       // the wall kinds: from the start of the (kind 1, sphere 0) segment
-      k_touch<<<148 * 4, 256, 0, s>>>(v, list0, list1, tn, (unsigned long long)a.step, v.seg + c->n_sph);
-      k_forces_f32<<<148 * 8, 256, 0, s>>>(v, a.h, a.sim_time, reinterpret_cast<const uint4 *>(list0), tn);
+      k_touch<<<unsigned(c->n_sm) * 4, 256, 0, s>>>(v, list0, list1, tn, (unsigned long long)a.step, v.seg + c->n_sph);
+      k_forces_f32<<<unsigned(c->n_sm) * 8, 256, 0, s>>>(v, a.h, a.sim_time, reinterpret_cast<const uint4 *>(list0), tn);
     } else if (fused) {
       // the sphere-sphere block in one fused pass, then the wall kinds'
       // narrow phase (feeds k_forces below)
       const unsigned long long step = (unsigned long long)a.step;
+      const unsigned nsm = unsigned(c->n_sm);
       if (c->ss_split == 2)
-        GF_CHECK(c, launch_k(c, k_contacts_ss<1, 4>, dim3(148 * 4), dim3(256), s, v, a.h, step));
+        GF_CHECK(c, launch_k(c, k_contacts_ss<1, 4, false>, dim3(nsm * 4), dim3(256), s, v, a.h, step));
       else if (c->ss_split == 3)
-        GF_CHECK(c, launch_k(c, k_contacts_ss<2, 4>, dim3(148 * 4), dim3(256), s, v, a.h, step));
+        GF_CHECK(c, launch_k(c, k_contacts_ss<2, 4, false>, dim3(nsm * 4), dim3(256), s, v, a.h, step));
+      else if (!c->ss_red)   // per-word REDs (the round-1 kernel; A/B switch GF_SS_RED=0)
+        GF_CHECK(c, launch_k(c, k_contacts_ss<2, 3, false>, dim3(nsm * 3), dim3(256), s, v, a.h, step));
       else
-        GF_CHECK(c, launch_k(c, k_contacts_ss<2, 3>, dim3(148 * 3), dim3(256), s, v, a.h, step));
+        GF_CHECK(c, launch_k(c, k_contacts_ss<2, 3, true>, dim3(nsm * 3), dim3(256), s, v, a.h, step));
       if (ev) cudaEventRecord(ev[4], s);
       ss_timed = true;
-      GF_CHECK(c, launch_k(c, k_touch, dim3(148 * 4), dim3(256), s, v, list0, list1, tn, step,
+      GF_CHECK(c, launch_k(c, k_touch, dim3(unsigned(c->n_sm) * 4), dim3(256), s, v, list0, list1, tn, step,
                            (const unsigned long long *)(v.seg + c->n_sph)));
     } else if (c->user_model && std::is_same<VelT, float>::value && v.sph.kin && c->user_fn_ss) {
       // user model, throughput build: the NVRTC sphere-sphere loop counts its
       // own touching entries; the narrow phase here covers the wall kinds
-      k_touch<<<148 * 4, 256, 0, s>>>(v, list0, list1, tn, (unsigned long long)a.step, v.seg + c->n_sph);
+      k_touch<<<unsigned(c->n_sm) * 4, 256, 0, s>>>(v, list0, list1, tn, (unsigned long long)a.step, v.seg + c->n_sph);
     } else {
-      k_touch<<<unsigned(std::min<int64_t>((v.n_acs + 255) / 256, 148 * 16)), 256, 0, s>>>(
+      k_touch<<<unsigned(std::min<int64_t>((v.n_acs + 255) / 256, int64_t(c->n_sm) * 16)), 256, 0, s>>>(
           v, list0, list1, tn, (unsigned long long)a.step, nullptr);
     }
     if (c->user_model) {
       if (launch_user_forces(c, v, a.h, a.sim_time, s)) return -1;
     } else {
-      GF_CHECK(c, launch_k(c, k_forces<VelT>, dim3(148 * 8), dim3(128), s, v, a.h, a.sim_time,
+      GF_CHECK(c, launch_k(c, k_forces<VelT>, dim3(unsigned(c->n_sm) * 8), dim3(128), s, v, a.h, a.sim_time,
                            (const uint32_t *)list0, (const uint32_t *)list1, (const unsigned long long *)tn,
                            fused ? 1 : 0));
     }

@@ -1142,7 +1142,7 @@ int kt_snapshot(Ctx *c, cudaStream_t s, double margin) {
   }
   const double skin = c->skin_factor * margin, skin_b = c->skin_big_factor * margin;
   // one wave of 3 CTAs / SM, grid-stride (2470 vs 2460 M sphere-steps/s at 8 / SM)
-  constexpr int64_t snap_blocks = 148 * 3;
+  const int64_t snap_blocks = int64_t(c->n_sm) * 3;
   if (c->n_sph)
     k_snapshot<<<unsigned(std::min<int64_t>(grid_for(c->n_sph), snap_blocks)), kBlock, 0, s>>>(
         c->dom, owners_view(c), spheres_view(c), k.c4.as<double4>(), k.sfam.as<uint8_t>(),
@@ -1380,7 +1380,7 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
     GF_CHECK(c, cub::DeviceRadixSort::SortPairs(k.cub_tmp.p, tmp, dk, dv, int(total), 0, bits, s));
     if (dk.Current() == ka2) std::swap(k.cand, k.cand_tmp);   // sorted halves now in cand_tmp
     const uint32_t *sa = k.cand_tmp.as<uint32_t>(), *sb = sa + cap;
-    k_cand_unpack<<<unsigned(std::min<int64_t>((total + 255) / 256, 148 * 16)), 256, 0, s>>>(
+    k_cand_unpack<<<unsigned(std::min<int64_t>((total + 255) / 256, int64_t(c->n_sm) * 16)), 256, 0, s>>>(
         total, n, sa, sb, k.cand.as<uint2>(), k.cand_seg.as<unsigned long long>());
     if (ensure(c, k.sa_cnt, 4 * (n + 1), s)) return -1;   // the long-segment list (scratch here)
     GF_CHECK(c, cudaMemsetAsync(big_n, 0, 8, s));
@@ -1393,7 +1393,7 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
                                        int(sizeof(uint2) * kLongSeg)));
       k.sort_long_smem = true;
     }
-    k_sort_long<<<148, 1024, sizeof(uint2) * kLongSeg, s>>>(k.cand_seg.as<unsigned long long>(), k.cand.as<uint2>(),
+    k_sort_long<<<c->n_sm, 1024, sizeof(uint2) * kLongSeg, s>>>(k.cand_seg.as<unsigned long long>(), k.cand.as<uint2>(),
                                                             k.sa_cnt.as<uint32_t>(), big_n);
   }
   if (n) k_copy_ref<<<grid_for(n), kBlock, 0, s>>>(n, k.c4.as<double4>(), k.ref.as<double>());

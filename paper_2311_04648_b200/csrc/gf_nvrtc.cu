@@ -24,7 +24,7 @@ namespace {
 // loaded through the runtime's library API (no libcuda link dependency)
 struct UserModule {
   cudaLibrary_t lib = nullptr;
-  cudaKernel_t f64 = nullptr, f32 = nullptr, ss = nullptr, walls = nullptr;
+  cudaKernel_t f64 = nullptr, f32 = nullptr, ss = nullptr, walls = nullptr, ref = nullptr, batch = nullptr;
 };
 std::map<std::string, UserModule> g_cache;
 
@@ -55,6 +55,13 @@ extern "C" __global__ void __launch_bounds__(256) gf_user_contacts_ss(gf::DtView
 }
 extern "C" __global__ void __launch_bounds__(128) gf_user_walls_f32(gf::DtView v, double ts, double t) {
   gf::user_walls_loop<float, GfUserCore>(v, ts, t);
+}
+// the reference-shaped entry points (gf_contact_forces, gf_eval_core)
+extern "C" __global__ void __launch_bounds__(128) gf_user_ref_contacts(gf::RefContacts r) {
+  gf::ref_contacts_loop<GfUserCore>(r);
+}
+extern "C" __global__ void __launch_bounds__(128) gf_user_core_batch(gf::CoreBatch b) {
+  gf::core_batch_loop<GfUserCore>(b);
 }
 )";
 }  // namespace
@@ -98,7 +105,9 @@ int set_user_model(Ctx *c, const char *src, const char *include_dir, std::string
         cudaLibraryGetKernel(&um.f64, um.lib, "gf_user_forces_f64") != cudaSuccess ||
         cudaLibraryGetKernel(&um.f32, um.lib, "gf_user_forces_f32") != cudaSuccess ||
         cudaLibraryGetKernel(&um.ss, um.lib, "gf_user_contacts_ss") != cudaSuccess ||
-        cudaLibraryGetKernel(&um.walls, um.lib, "gf_user_walls_f32") != cudaSuccess) {
+        cudaLibraryGetKernel(&um.walls, um.lib, "gf_user_walls_f32") != cudaSuccess ||
+        cudaLibraryGetKernel(&um.ref, um.lib, "gf_user_ref_contacts") != cudaSuccess ||
+        cudaLibraryGetKernel(&um.batch, um.lib, "gf_user_core_batch") != cudaSuccess) {
       set_err(c, std::string("loading the NVRTC user force module failed: ") +
                      cudaGetErrorString(cudaGetLastError()));
       return -1;
@@ -109,6 +118,8 @@ int set_user_model(Ctx *c, const char *src, const char *include_dir, std::string
   c->user_fn_f32 = reinterpret_cast<void *>(it->second.f32);
   c->user_fn_ss = reinterpret_cast<void *>(it->second.ss);
   c->user_fn_walls = reinterpret_cast<void *>(it->second.walls);
+  c->user_fn_ref = reinterpret_cast<void *>(it->second.ref);
+  c->user_fn_batch = reinterpret_cast<void *>(it->second.batch);
   c->user_model = true;
   return 0;
 }
@@ -138,10 +149,10 @@ int launch_user_forces(Ctx *c, const DtView &v, double ts, double sim_time, cuda
   void *args[] = {&vv, &ts, &sim_time};
   if (c->f32_state && v.sph.kin && c->user_fn_ss) {
     // throughput build: the fused sphere-sphere loop, then the wall kinds
-    cudaError_t e = cudaLaunchKernel(reinterpret_cast<const void *>(c->user_fn_ss), dim3(148 * 4), dim3(256), args,
+    cudaError_t e = cudaLaunchKernel(reinterpret_cast<const void *>(c->user_fn_ss), dim3(unsigned(c->n_sm) * 4), dim3(256), args,
                                      0, s);
     if (e == cudaSuccess)
-      e = cudaLaunchKernel(reinterpret_cast<const void *>(c->user_fn_walls), dim3(148 * 4), dim3(128), args, 0, s);
+      e = cudaLaunchKernel(reinterpret_cast<const void *>(c->user_fn_walls), dim3(unsigned(c->n_sm) * 4), dim3(128), args, 0, s);
     if (e != cudaSuccess) {
       set_err(c, std::string("launching the NVRTC user force kernels failed: ") + cudaGetErrorString(e));
       return -1;
@@ -149,7 +160,7 @@ int launch_user_forces(Ctx *c, const DtView &v, double ts, double sim_time, cuda
     return 0;
   }
   cudaKernel_t fn = reinterpret_cast<cudaKernel_t>(c->f32_state ? c->user_fn_f32 : c->user_fn_f64);
-  unsigned grid = unsigned(std::min<int64_t>((v.n_acs + 127) / 128, 148 * 16));
+  unsigned grid = unsigned(std::min<int64_t>((v.n_acs + 127) / 128, int64_t(c->n_sm) * 16));
   if (grid == 0) grid = 1;
   cudaError_t e = cudaLaunchKernel(reinterpret_cast<const void *>(fn), dim3(grid), dim3(128), args, 0, s);
   if (e != cudaSuccess) {
