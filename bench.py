@@ -67,8 +67,9 @@ def parse():
     ap.add_argument("--amortised-steps", type=int, default=200,
                     help="extra window over several candidate rebuilds (rebuild-amortised rate)")
     ap.add_argument("--prof-steps", type=int, default=20, help="per-kernel event window")
-    ap.add_argument("--mode", default="auto", choices=["auto", "single", "replicas", "decomp"],
-                    help="auto: single on 1 GPU, decomp (slab decomposition) on N > 1")
+    ap.add_argument("--mode", default="auto", choices=["auto", "single", "replicas", "decomp", "ktdt"],
+                    help="auto: single on 1 GPU, decomp (slab decomposition) on N > 1; ktdt: the paper's "
+                         "2-GPU split of one scene (rank 0: dT on GPU 0, kT on GPU 1; other ranks idle)")
     ap.add_argument("--settle-steps", type=int, default=12000,
                     help="untimed steps that settle the lattice bed (projectile parked) before the "
                          "projectile is released at the settled surface; 0 = time the raw lattice")
@@ -205,7 +206,8 @@ def cpu_run(scene, steps, warmup, period, lag, nthreads, margin):
 def build_scene(args, device, tiles=1, decomposition=None, hold_ball=False):
     from paper_2311_04648_b200 import scenes
     return scenes.crater_bed(args.n_spheres, n_max=args.n_max, precision=args.precision, device=device,
-                             tiles=tiles, decomposition=decomposition, hold_ball=hold_ball)
+                             tiles=tiles, decomposition=decomposition, hold_ball=hold_ball,
+                             kt_device=getattr(args, "kt_device", None))
 
 
 def schedule(sim):
@@ -241,7 +243,9 @@ def workload_config(args, world, mode):
             "n_max": args.n_max, "h": 1e-5, "v_err": 5.0, "precision": args.precision,
             "settle_steps": args.settle_steps,
             "parallelism": ({"decomp": f"slab decomposition x{world} (NCCL halo + force return)",
-                             "replicas": f"replicas x{world}"}.get(mode, "single GPU")),
+                             "replicas": f"replicas x{world}",
+                             "ktdt": "2-GPU kT/dT split: dT on GPU 0, kT on GPU 1 (NVLink peer access)"}
+                            .get(mode, "single GPU")),
             "inputs_vs_l2": "state + contact arrays larger than L2 (no flush)",
             "bed": ("settled: the untimed settling steps from the HCP lattice with the projectile parked, "
                     "then the projectile released 2 mm above the surface at the 20 cm-drop speed")
@@ -301,9 +305,15 @@ def reference_arm(args):
 def b200_arm(args):
     rank, world, local = dist_env()
     import torch
+    if args.mode == "ktdt":
+        # one scene on two GPUs: rank 0 drives both devices
+        if rank != 0:
+            return
+        world, args.kt_device = 1, (1 if torch.cuda.device_count() > 1 else 0)
     mode = args.mode if args.mode != "auto" else ("decomp" if world > 1 else "single")
     if mode == "single" and world > 1:
         mode = "replicas"
+    kt_dev = getattr(args, "kt_device", None)
     dist = None
     if world > 1 or mode == "decomp":
         import torch.distributed as dist
@@ -318,11 +328,12 @@ def b200_arm(args):
     sim, settle_s = settled_source(args, device, tiles=world if mode == "decomp" else 1, decomposition=dec)
     # the CPU baseline's sample: one settled tile
     scene0 = scenes.oracle_scene(sim) if (rank == 0 and world == 1 and not args.no_cpu) else None
-    tiles = max(1, args.tiles) if (world == 1 and mode == "single") else 1
+    tiles = max(1, args.tiles) if (world == 1 and mode in ("single", "ktdt")) else 1
     if tiles > 1:
         tx, ty = factor(tiles)
         src = sim
-        sim = scenes.tiled_bed(src, tx, ty, precision=args.precision, device=device, n_max=args.n_max)
+        sim = scenes.tiled_bed(src, tx, ty, precision=args.precision, device=device, n_max=args.n_max,
+                               kt_device=kt_dev)
         src.close()
         del src
         sim.initialize()
@@ -379,7 +390,7 @@ def b200_arm(args):
     # kT joined) spanning several Verlet candidate rebuilds -- a short timed
     # window may contain none (one rebuild every ~40 steps on this bed)
     amort = None
-    if args.amortised_steps > 0 and mode == "single":
+    if args.amortised_steps > 0 and mode in ("single", "ktdt"):
         rb0 = int(sim.last_run.kt_rebuilds)
         d0 = sim.scheduler.timing["dyn_force"]
         barrier()
@@ -455,7 +466,8 @@ def b200_arm(args):
         period, lag, _ = schedule(sim)
         kt_launches = 14   # snapshot, grid, filter, compaction, scans, wall pairs, fill, history gather
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": (args.gpus if mode == "ktdt" else world),
+            "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None,
             "dtype": DTYPE if args.precision == "f32" else DTYPE_F64,

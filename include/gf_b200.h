@@ -47,7 +47,14 @@ typedef struct gf_ctx gf_ctx;
 /* flags for gf_create */
 #define GF_STATE_F32 1u /* store owner velocities as float32 (throughput build) */
 
-gf_ctx *gf_create(int device, uint32_t flags);
+/* device = the dT device (state, contact arrays, force/integrate kernels).
+ * kt_device < 0: kT on the same device as a second stream (one GPU);
+ * kt_device >= 0: the paper's 2-GPU split
+ * -- the kT stream, its scratch and events on kt_device, the detection
+ * snapshot written there and the contact arrays written back over NVLink
+ * peer access (enabled here; NULL if the devices cannot reach each other).
+ * kt_device == device runs the split bookkeeping on one device. */
+gf_ctx *gf_create(int device, int kt_device, uint32_t flags);
 void gf_destroy(gf_ctx *ctx);
 /* copies the last error message into buf (always NUL-terminated) */
 int gf_last_error(gf_ctx *ctx, char *buf, size_t n);
@@ -69,8 +76,24 @@ int gf_upload_owners(gf_ctx *ctx, int64_t n, const uint64_t *voxel, const uint16
 int gf_download_owners(gf_ctx *ctx, uint64_t *voxel, uint16_t *sub, float *quat,
                        double *lin_vel, double *ang_vel, uint8_t *family);
 int gf_set_owner_families(gf_ctx *ctx, const uint8_t *family);
+/* active boxes (engine.py:857-879, ActiveBoxPolicy): every clump owner of
+ * active_family or frozen_family is re-tagged by whether its position lies
+ * in any box -- boxes (n_box, 6) = centre xyz (used when anchors[b] < 0) and
+ * half extents xyz; anchors[b] = owner whose position is the box centre --
+ * owners frozen now lose their velocities; on the device, no state round
+ * trip.  *n_changed = owners re-tagged. */
+int gf_apply_active_boxes(gf_ctx *ctx, int n_box, const double *boxes, const int64_t *anchors,
+                          int active_family, int frozen_family, int64_t *n_changed);
 /* external loads (n,3) float64 each; both NULL clears them */
 int gf_set_external_loads(gf_ctx *ctx, const double *force, const double *torque);
+/* selected owners' state without a full download (trackers, engine.py:132-189):
+ * idx (n) device owner indices; out (n, 23) float64 per owner = voxel (the
+ * uint64 bits), sub-voxel xyz, quaternion wxyz, lin vel, ang vel (local),
+ * family, contact force, contact torque (of the last reported step), 2 pad */
+int gf_read_owners(gf_ctx *ctx, int64_t n, const int64_t *idx, double *out);
+/* max |v| over the clump owners of non-fixed families (Inspector
+ * "clump_max_absv", engine.py:198-214), a device reduction */
+int gf_clump_max_absv(gf_ctx *ctx, double *out);
 /* per-owner contact force/torque of the last stepped step (n,3) each */
 int gf_download_accumulators(gf_ctx *ctx, double *acc_force, double *acc_torque);
 
@@ -158,6 +181,11 @@ int gf_dt_step(gf_ctx *ctx, const gf_step_params *p, int64_t *touching, int64_t 
  * gf_device.cuh.  The compiler log is copied to log. */
 int gf_set_force_model(gf_ctx *ctx, const char *cuda_src, const char *include_dir, int W, char *log,
                        size_t log_n);
+/* bonded models (engine.py:639-662): at every adoption, a contact of the
+ * active array whose wildcard `col` is > 0 (an intact bond) and that the new
+ * detection no longer holds is re-appended with its history; col < 0 turns
+ * it off.  Call after gf_set_force_model (col < W). */
+int gf_set_persistent_wildcard(gf_ctx *ctx, int col);
 /* NVRTC compile of a user model without a device (validation only) */
 int gf_nvrtc_compile(const char *cuda_src, const char *include_dir, char *log, size_t log_n);
 

@@ -60,7 +60,8 @@ EXPORTS = (
     "gf_nvrtc_compile", "gf_run_begin", "gf_step_forces", "gf_step_integrate", "gf_run_end",
     "gf_set_decomposition", "gf_halo_record_bytes", "gf_stream", "gf_pack_state", "gf_unpack_state",
     "gf_pack_forces", "gf_add_forces", "gf_trip_word", "gf_sync",
-    "gf_contact_forces", "gf_eval_core", "gf_reduce", "gf_integrate_and_refresh",
+    "gf_contact_forces", "gf_eval_core", "gf_reduce", "gf_integrate_and_refresh", "gf_apply_active_boxes",
+    "gf_set_persistent_wildcard", "gf_read_owners", "gf_clump_max_absv",
 )
 
 _lib = None
@@ -83,7 +84,7 @@ def load_library():
             f"{LIB_PATH} is missing; build it with `make -C {PKG_DIR}` (there is no CPU fallback)")
     L = C.CDLL(LIB_PATH)
     L.gf_create.restype = _P
-    L.gf_create.argtypes = [C.c_int, C.c_uint32]
+    L.gf_create.argtypes = [C.c_int, C.c_int, C.c_uint32]
     L.gf_destroy.argtypes = [_P]
     L.gf_acs_size.restype = _I64
     L.gf_acs_size.argtypes = [_P, C.c_int]
@@ -126,15 +127,19 @@ def carr(a, dtype, shape=None):
 class Context:
     """Owns one gf_ctx (device buffers, streams, events)."""
 
-    def __init__(self, device: int = 0, f32_state: bool = False):
+    def __init__(self, device: int = 0, f32_state: bool = False, kt_device=None):
+        """kt_device: None = kT as a second stream on `device`; an index =
+        the paper's 2-GPU split, kT on that device (include/gf_b200.h)."""
         L = load_library()
         if L.gf_device_count() <= 0:
             raise DeviceUnavailableError("no CUDA device visible; the B200 path has no CPU fallback")
         self.L = L
-        self.h = L.gf_create(int(device), GF_STATE_F32 if f32_state else 0)
+        kt = -1 if kt_device is None else int(kt_device)
+        self.h = L.gf_create(int(device), kt, GF_STATE_F32 if f32_state else 0)
         if not self.h:
-            raise DeviceUnavailableError(f"gf_create failed on device {device}")
+            raise DeviceUnavailableError(f"gf_create failed on device {device} (kT device {kt})")
         self.f32_state = f32_state
+        self.kt_device = kt_device
 
     def close(self):
         if getattr(self, "h", None):

@@ -120,6 +120,27 @@ __device__ __forceinline__ double kin_tscale(const SphKin &k) {
   return kin_exp2(int((signed char)((__float_as_uint(k.r.w) >> 16) & 0xFFu)));
 }
 
+// one 256-bit read-only load of a 32-byte record (LDG.E.256 on sm_100).  An
+// NVRTC older than 12.9 (torch ships 12.8; a process that imported torch has
+// it loaded) rejects 256-bit vectors: code compiled there takes two 128-bit
+// loads.
+#if defined(__CUDACC_RTC__) && (__CUDACC_VER_MAJOR__ * 100 + __CUDACC_VER_MINOR__ < 1209)
+#define GF_LD256 0
+#else
+#define GF_LD256 1
+#endif
+__device__ __forceinline__ double4 ld256(const double4 *p) {
+  double4 r;
+#if GF_LD256
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
+#else
+  const double2 *q = reinterpret_cast<const double2 *>(p);
+  const double2 a = __ldg(q), b = __ldg(q + 1);
+  r = make_double4(a.x, a.y, b.x, b.y);
+#endif
+  return r;
+}
+
 struct Spheres {
   int64_t n;
   uint32_t *owner;

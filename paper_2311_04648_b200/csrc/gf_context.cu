@@ -50,7 +50,9 @@ int ensure(Ctx *c, DBuf &b, size_t bytes, cudaStream_t s, bool keep) {
     // memory: return them and retry once
     (void)cudaGetLastError();
     cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, c->device) == cudaSuccess && cudaDeviceSynchronize() == cudaSuccess &&
+    int cur = c->device;
+    cudaGetDevice(&cur);
+    if (cudaDeviceGetDefaultMemPool(&pool, cur) == cudaSuccess && cudaDeviceSynchronize() == cudaSuccess &&
         cudaMemPoolTrimTo(pool, 0) == cudaSuccess)
       e = cudaMalloc(&p, nb);
   }
@@ -258,6 +260,7 @@ struct RunState {
 static void trace_mark(Ctx *c, const char *what, int64_t step, cudaStream_t s) {
   RunState *R = c->run;
   if (!R || !R->trace) return;
+  DevGuard g(stream_device(s));
   cudaEvent_t e;
   cudaEventCreate(&e);
   cudaEventRecord(e, s);
@@ -426,30 +429,64 @@ int gf_device_count(void) {
   return n;
 }
 
-gf_ctx *gf_create(int device, uint32_t flags) {
+gf_ctx *gf_create(int device, int kt_device, uint32_t flags) {
   if (cudaSetDevice(device) != cudaSuccess) return nullptr;
   gf_ctx *ctx = new gf_ctx();
   Ctx *c = &ctx->c;
   c->device = device;
+  c->split = kt_device >= 0;
+  c->kt_device = c->split ? kt_device : device;
   c->flags = flags;
   c->f32_state = (flags & GF_STATE_F32) != 0;
   c->fixed_reduce = c->f32_state;
+  if (c->split && kt_device != device) {
+    // kT kernels write the dT device's contact arrays and read its tables;
+    // the dT device's snapshot kernel writes the kT device's snapshot
+    int ab = 0, ba = 0;
+    cudaDeviceCanAccessPeer(&ab, device, kt_device);
+    cudaDeviceCanAccessPeer(&ba, kt_device, device);
+    if (!ab || !ba) {
+      delete ctx;
+      return nullptr;
+    }
+    cudaError_t e = cudaDeviceEnablePeerAccess(kt_device, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) { delete ctx; return nullptr; }
+    cudaSetDevice(kt_device);
+    e = cudaDeviceEnablePeerAccess(device, 0);
+    cudaSetDevice(device);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) { delete ctx; return nullptr; }
+    (void)cudaGetLastError();
+  }
   // stream priorities (GF_STREAM_PRIO): 0 equal, 1 dT first, 2 kT first
   int prio_lo = 0, prio_hi = 0, mode = 0;
   cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
   if (const char *sp = std::getenv("GF_STREAM_PRIO")) mode = std::atoi(sp);
   cudaStreamCreateWithPriority(&c->s_dt, cudaStreamNonBlocking, mode == 1 ? prio_hi : prio_lo);
-  cudaStreamCreateWithPriority(&c->s_kt, cudaStreamNonBlocking, mode == 2 ? prio_hi : prio_lo);
   cudaEventCreateWithFlags(&c->ev_snap, cudaEventDisableTiming);
-  cudaEventCreateWithFlags(&c->ev_ca, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->ev_adopted, cudaEventDisableTiming);
-  cudaEventCreateWithFlags(&c->ev_count, cudaEventDisableTiming);
-  cudaEventCreateWithFlags(&c->ev_disp, cudaEventDisableTiming);
+  {
+    // the kT stream and the events recorded on it belong to the kT device
+    DevGuard g(c->kt_device);
+    cudaStreamCreateWithPriority(&c->s_kt, cudaStreamNonBlocking, mode == 2 ? prio_hi : prio_lo);
+    cudaEventCreateWithFlags(&c->ev_ca, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->ev_count, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->ev_disp, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->ev_kt_join, cudaEventDisableTiming);
+    if (c->kt_device != device) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, c->kt_device) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+      (void)cudaGetLastError();
+    }
+  }
   if (const char *sf = std::getenv("GF_SKIN_FACTOR")) c->skin_factor = std::atof(sf);
   if (const char *sb = std::getenv("GF_SKIN_BIG")) c->skin_big_factor = std::atof(sb);
   if (c->skin_big_factor < c->skin_factor) c->skin_big_factor = c->skin_factor;
   if (const char *sp = std::getenv("GF_SS_SPLIT")) c->ss_split = std::atoi(sp);
   if (const char *sr = std::getenv("GF_SS_RED")) c->ss_red = std::atoi(sr);
+  if (const char *sp = std::getenv("GF_SS_PF")) c->ss_pf = std::atoi(sp);
   cudaDeviceGetAttribute(&c->n_sm, cudaDevAttrMultiProcessorCount, device);
   if (c->n_sm <= 0) c->n_sm = 148;
   if (const char *pd = std::getenv("GF_PDL")) c->pdl = std::atoi(pd);
@@ -468,7 +505,8 @@ gf_ctx *gf_create(int device, uint32_t flags) {
     }
     (void)cudaGetLastError();
   }
-  if (cudaMallocHost(&c->h_status, sizeof(Status)) != cudaSuccess) { delete ctx; return nullptr; }
+  // pinned status mirror, written by both streams' devices
+  if (cudaHostAlloc(&c->h_status, sizeof(Status), cudaHostAllocPortable) != cudaSuccess) { delete ctx; return nullptr; }
   if (ensure(c, c->status, sizeof(Status), c->s_dt) || ensure(c, c->heavy_count, 16, c->s_dt)) {
     delete ctx;
     return nullptr;
@@ -481,6 +519,10 @@ gf_ctx *gf_create(int device, uint32_t flags) {
 void gf_destroy(gf_ctx *ctx) {
   if (!ctx) return;
   Ctx *c = &ctx->c;
+  if (c->split) {
+    cudaSetDevice(c->kt_device);
+    cudaDeviceSynchronize();
+  }
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   DBuf *bufs[] = {&c->sph_kin, &c->tlist, &c->tlist_n, &c->facc, &c->tpl_scale, &c->sph_center, &c->sph_first, &c->voxel, &c->sub, &c->quat, &c->lin_vel, &c->ang_vel, &c->meta, &c->tpl, &c->acc,
@@ -501,7 +543,7 @@ void gf_destroy(gf_ctx *ctx) {
   for (DBuf *b : bufs) release(*b);
   free_run(c);
   if (c->h_status) cudaFreeHost(c->h_status);
-  cudaEvent_t evs[] = {c->ev_snap, c->ev_ca, c->ev_adopted, c->ev_count, c->ev_disp, c->t0, c->t1};
+  cudaEvent_t evs[] = {c->ev_snap, c->ev_ca, c->ev_adopted, c->ev_count, c->ev_disp, c->ev_kt_join, c->t0, c->t1};
   for (auto e : evs) cudaEventDestroy(e);
   cudaStreamDestroy(c->s_dt);
   cudaStreamDestroy(c->s_kt);
@@ -624,6 +666,10 @@ int gf_upload_owners(gf_ctx *ctx, int64_t n, const uint64_t *voxel, const uint16
       ensure(c, c->tpl, 32 * (n_tpl + 1), s) || ensure(c, c->acc, 48 * n, s) ||
       ensure(c, c->facc, 48 * n, s) || ensure(c, c->tpl_scale, 16 * (n_tpl + 1), s))
     return -1;
+  // fixed-point scales are set at the first run (update_fixed_scales); until
+  // then the kinematics records carry zeros, not uninitialised words
+  // (compute-sanitizer initcheck)
+  if (c->fx_h < 0.0) GF_CHECK(c, cudaMemsetAsync(c->tpl_scale.p, 0, 16 * (n_tpl + 1), s));
   if (ensure_stage(c, n, s)) return -1;
   // the parity build's incidence-list reduction (the throughput build sums
   // into the fixed-point accumulators instead)
@@ -678,6 +724,52 @@ int gf_upload_owners(gf_ctx *ctx, int64_t n, const uint64_t *voxel, const uint16
   return 0;
 }
 
+// selected owners' state (trackers: no full-state download);
+// row r of the 23-double output = voxel (bits), sub xyz, quat wxyz, v, w,
+// family, acc force, acc torque
+__global__ void k_read_owners(int64_t n, const long long *idx, const uint64_t *voxel, const ushort4 *sub,
+                              const float4 *quat, const void *lin_vel, const void *ang_vel, const uint32_t *meta,
+                              const double *acc, int f32, double *out) {
+  const int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (r >= n) return;
+  const int64_t o = idx[r];
+  double *w = out + 23 * r;
+  w[0] = __longlong_as_double((long long)voxel[o]);
+  const ushort4 sb = sub[o];
+  w[1] = sb.x; w[2] = sb.y; w[3] = sb.z;
+  const float4 q = quat[o];
+  w[4] = q.x; w[5] = q.y; w[6] = q.z; w[7] = q.w;
+  for (int a = 0; a < 3; ++a) {
+    w[8 + a] = f32 ? double(reinterpret_cast<const float *>(lin_vel)[4 * o + a])
+                   : reinterpret_cast<const double *>(lin_vel)[4 * o + a];
+    w[11 + a] = f32 ? double(reinterpret_cast<const float *>(ang_vel)[4 * o + a])
+                    : reinterpret_cast<const double *>(ang_vel)[4 * o + a];
+  }
+  w[14] = double(meta_family(meta[o]));
+  for (int a = 0; a < 6; ++a) w[15 + a] = acc ? acc[6 * o + a] : 0.0;
+  w[21] = 0.0; w[22] = 0.0;
+}
+
+// max |v| over the clump owners (owners with spheres) of non-fixed families
+// (Inspector "clump_max_absv", engine.py:198-214)
+__global__ void k_clump_max_absv(int64_t n, const uint32_t *first, const uint32_t *meta, const uint8_t *fam_flags,
+                                 const void *lin_vel, int f32, unsigned long long *out) {
+  double best = 0.0;
+  for (int64_t o = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; o < n; o += int64_t(gridDim.x) * blockDim.x) {
+    if (first[o + 1] == first[o] || (fam_flags[meta_family(meta[o])] & kFamFixed)) continue;
+    double v2 = 0.0;
+    for (int a = 0; a < 3; ++a) {
+      const double x = f32 ? double(reinterpret_cast<const float *>(lin_vel)[4 * o + a])
+                           : reinterpret_cast<const double *>(lin_vel)[4 * o + a];
+      v2 += x * x;
+    }
+    best = fmax(best, sqrt(v2));
+  }
+  for (int off = 16; off > 0; off >>= 1) best = fmax(best, __shfl_down_sync(0xffffffffu, best, off));
+  // non-negative doubles order like their bit patterns
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(best));
+}
+
 int gf_download_owners(gf_ctx *ctx, uint64_t *voxel, uint16_t *sub, float *quat, double *lin_vel,
                        double *ang_vel, uint8_t *family) {
   CTX_CHECK(ctx);
@@ -701,6 +793,46 @@ int gf_download_owners(gf_ctx *ctx, uint64_t *voxel, uint16_t *sub, float *quat,
   return 0;
 }
 
+int gf_read_owners(gf_ctx *ctx, int64_t n, const int64_t *idx, double *out) {
+  CTX_CHECK(ctx);
+  if (n <= 0) return 0;
+  for (int64_t r = 0; r < n; ++r)
+    if (idx[r] < 0 || idx[r] >= c->n_owner) { c->err = "gf_read_owners: owner out of range"; return -1; }
+  cudaStream_t s = c->s_dt;
+  long long *d_idx = nullptr;
+  double *d_out = nullptr;
+  GF_CHECK(c, cudaMallocAsync(&d_idx, 8 * n, s));
+  GF_CHECK(c, cudaMallocAsync(&d_out, 8 * 23 * n, s));
+  GF_CHECK(c, cudaMemcpyAsync(d_idx, idx, 8 * n, cudaMemcpyHostToDevice, s));
+  k_read_owners<<<unsigned((n + 127) / 128), 128, 0, s>>>(n, d_idx, c->voxel.as<uint64_t>(), c->sub.as<ushort4>(),
+                                                          c->quat.as<float4>(), c->lin_vel.p, c->ang_vel.p,
+                                                          c->meta.as<uint32_t>(), c->acc.as<double>(),
+                                                          c->f32_state ? 1 : 0, d_out);
+  GF_CHECK(c, cudaMemcpyAsync(out, d_out, 8 * 23 * n, cudaMemcpyDeviceToHost, s));
+  cudaFreeAsync(d_idx, s);
+  cudaFreeAsync(d_out, s);
+  GF_CHECK(c, cudaStreamSynchronize(s));
+  return 0;
+}
+
+int gf_clump_max_absv(gf_ctx *ctx, double *out) {
+  CTX_CHECK(ctx);
+  *out = 0.0;
+  if (!c->n_owner || !c->sph_first.p) return 0;
+  cudaStream_t s = c->s_dt;
+  unsigned long long *d = nullptr, h = 0;
+  GF_CHECK(c, cudaMallocAsync(&d, 8, s));
+  GF_CHECK(c, cudaMemsetAsync(d, 0, 8, s));
+  k_clump_max_absv<<<unsigned(std::min<int64_t>((c->n_owner + 255) / 256, int64_t(c->n_sm) * 8)), 256, 0, s>>>(
+      c->n_owner, c->sph_first.as<uint32_t>(), c->meta.as<uint32_t>(), c->fam_flags.as<uint8_t>(), c->lin_vel.p,
+      c->f32_state ? 1 : 0, d);
+  GF_CHECK(c, cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, s));
+  cudaFreeAsync(d, s);
+  GF_CHECK(c, cudaStreamSynchronize(s));
+  std::memcpy(out, &h, 8);
+  return 0;
+}
+
 int gf_set_owner_families(gf_ctx *ctx, const uint8_t *family) {
   CTX_CHECK(ctx);
   const int64_t n = c->n_owner;
@@ -710,6 +842,46 @@ int gf_set_owner_families(gf_ctx *ctx, const uint8_t *family) {
   for (int64_t i = 0; i < n; ++i) meta[i] = (uint32_t(family[i]) << 24) | (meta[i] & 0xFFFFFFu);
   if (h2d(c, c->meta.p, meta.data(), 4 * n, c->s_dt)) return -1;
   world_moving_update(c);
+  return 0;
+}
+
+int gf_apply_active_boxes(gf_ctx *ctx, int n_box, const double *boxes, const int64_t *anchors, int active_family,
+                          int frozen_family, int64_t *n_changed) {
+  CTX_CHECK(ctx);
+  if (n_box < 0 || active_family < 0 || active_family > 255 || frozen_family < 0 || frozen_family > 255) {
+    c->err = "gf_apply_active_boxes: bad arguments";
+    return -1;
+  }
+  for (int b = 0; b < n_box; ++b)
+    if (anchors[b] >= c->n_owner) { c->err = "gf_apply_active_boxes: anchor owner out of range"; return -1; }
+  if (n_changed) *n_changed = 0;
+  if (!c->n_owner || !n_box) return 0;
+  cudaStream_t s = c->s_dt;
+  double *d_box = nullptr;
+  long long *d_anchor = nullptr;
+  unsigned long long *d_cnt = nullptr;
+  GF_CHECK(c, cudaMallocAsync(&d_box, sizeof(double) * 6 * n_box, s));
+  GF_CHECK(c, cudaMallocAsync(&d_anchor, sizeof(long long) * n_box, s));
+  GF_CHECK(c, cudaMallocAsync(&d_cnt, sizeof(unsigned long long), s));
+  GF_CHECK(c, cudaMemcpyAsync(d_box, boxes, sizeof(double) * 6 * n_box, cudaMemcpyHostToDevice, s));
+  GF_CHECK(c, cudaMemcpyAsync(d_anchor, anchors, sizeof(long long) * n_box, cudaMemcpyHostToDevice, s));
+  GF_CHECK(c, cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), s));
+  if (active_boxes(c, n_box, d_box, d_anchor, uint32_t(active_family), uint32_t(frozen_family), d_cnt, s))
+    return -1;
+  unsigned long long h_cnt = 0;
+  GF_CHECK(c, cudaMemcpyAsync(&h_cnt, d_cnt, sizeof(h_cnt), cudaMemcpyDeviceToHost, s));
+  cudaFreeAsync(d_box, s);
+  cudaFreeAsync(d_anchor, s);
+  cudaFreeAsync(d_cnt, s);
+  GF_CHECK(c, cudaStreamSynchronize(s));
+  if (n_changed) *n_changed = int64_t(h_cnt);
+  return 0;
+}
+
+int gf_set_persistent_wildcard(gf_ctx *ctx, int col) {
+  CTX_CHECK(ctx);
+  if (col >= c->wild_w) { c->err = "persistent wildcard column out of range"; return -1; }
+  c->persist_col = col < 0 ? -1 : col;
   return 0;
 }
 
@@ -1145,6 +1317,7 @@ int gf_step_forces(gf_ctx *ctx, int64_t i) {
       e = R->kt_ev_free.back();
       R->kt_ev_free.pop_back();
     } else {
+      DevGuard g(c->kt_device);
       GF_CHECK(c, cudaEventCreate(&e.first));
       GF_CHECK(c, cudaEventCreate(&e.second));
     }
@@ -1202,8 +1375,8 @@ int gf_run_end(gf_ctx *ctx, gf_run_result *r) {
   // finish enqueuing an in-flight detection (its fill) inside this call
   if (c->next_pending && !c->fill_done && run_fill(c)) return fail_run(c);
   // join the kT stream so in-flight detection work counts in the timed window
-  if (cudaEventRecord(c->ev_snap, c->s_kt) != cudaSuccess ||
-      cudaStreamWaitEvent(c->s_dt, c->ev_snap, 0) != cudaSuccess ||
+  if (cudaEventRecord(c->ev_kt_join, c->s_kt) != cudaSuccess ||
+      cudaStreamWaitEvent(c->s_dt, c->ev_kt_join, 0) != cudaSuccess ||
       cudaEventRecord(c->t1, c->s_dt) != cudaSuccess || cudaStreamSynchronize(c->s_kt) != cudaSuccess) {
     c->err = cudaGetErrorString(cudaGetLastError());
     return fail_run(c);
@@ -1275,6 +1448,10 @@ int gf_set_decomposition(gf_ctx *ctx, const uint32_t *dd, double lever_max, int 
   } else {
     if (!c->fixed_reduce) {
       c->err = "spatial decomposition needs the fixed-point owner reduction (GF_STATE_F32)";
+      return -1;
+    }
+    if (c->split) {
+      c->err = "spatial decomposition and the 2-GPU kT/dT split are separate modes";
       return -1;
     }
     if (ensure(c, c->dd, 4 * (c->n_owner + 1), c->s_dt)) return -1;

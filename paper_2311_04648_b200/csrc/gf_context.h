@@ -91,8 +91,38 @@ struct KtScratch {
   bool sort_long_smem = false;   // k_sort_long's 64 KB dynamic shared memory opted in on this context's device
 };
 
+// Sets the current device for a scope (the 2-GPU kT/dT split launches kT work
+// on the kT device and allocates contact arrays on the dT device).
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (dev >= 0 && dev != prev) cudaSetDevice(dev);
+    else prev = -1;
+  }
+  ~DevGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+// the device a stream belongs to
+inline int stream_device(cudaStream_t s) {
+  int d = -1;
+  if (cudaStreamGetDevice(s, &d) != cudaSuccess) {
+    (void)cudaGetLastError();
+    cudaGetDevice(&d);
+  }
+  return d;
+}
+
 struct Ctx {
   int device = 0;
+  // the paper's 2-GPU split: the kT stream, its scratch and
+  // events live on kt_device; contact arrays, state and the dT stream on
+  // `device`; kT kernels read the dT device's tables and write the contact
+  // arrays through NVLink peer access.  split = false: one device.
+  int kt_device = 0;
+  bool split = false;
+  cudaEvent_t ev_kt_join = nullptr;   // recorded on s_kt (kT device) at the end of a run
   uint32_t flags = 0;
   bool f32_state = false;
   std::string err;
@@ -155,7 +185,10 @@ struct Ctx {
   double skin_big_factor = 8.0;  // skin of big spheres (radius > r_cut), >= skin_factor (GF_SKIN_BIG)
   uint64_t world_version = 0;   // bumped whenever mesh / analytic world transforms are recomputed
   int tlist_words = 5;       // words per contact of the touching lists (1 on the fused path)
+  int persist_col = -1;      // wildcard column whose > 0 rows persist across detections (bonds), or -1
+  int64_t persisted = 0;     // rows re-appended by that rule so far
   int n_sm = 148;             // multiprocessors of the device (grid sizing)
+  int ss_pf = 1;             // fused kernel read-ahead / prefetch (GF_SS_PF=0: off)
   int ss_red = 1;            // fused sphere-sphere kernel: staged fixed-point rows (GF_SS_RED=0: per-word REDs)
   int ss_split = 0;          // throughput build: split narrow/force sphere-sphere kernels (GF_SS_SPLIT=1)
   // programmatic dependent launch on the dT chain (GF_PDL=1): measured slower
@@ -274,6 +307,8 @@ int halo_pack_state(Ctx *c, const uint32_t *idx, int64_t n, void *out, cudaStrea
 int halo_unpack_state(Ctx *c, const uint32_t *idx, int64_t n, const void *in, cudaStream_t s);
 int halo_pack_forces(Ctx *c, const uint32_t *idx, int64_t n, void *out, cudaStream_t s);
 int halo_add_forces(Ctx *c, const uint32_t *idx, int64_t n, const void *in, cudaStream_t s);
+int active_boxes(Ctx *c, int n_box, const double *box, const long long *anchor, uint32_t active, uint32_t frozen,
+                 unsigned long long *n_changed, cudaStream_t s);
 int dt_forces_f32(Ctx *c, const StepArgs &a, cudaStream_t s);
 int dt_integrate_f32(Ctx *c, const StepArgs &a, cudaStream_t s);
 int dt_forces_f64(Ctx *c, const StepArgs &a, cudaStream_t s);

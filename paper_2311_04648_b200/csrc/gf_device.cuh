@@ -69,6 +69,7 @@ struct DtView {
   double *heavy_acc;    // [n_owner*6] (only heavy owners written)
   Status *st;
   int acc_all;          // throughput build: also accumulate onto passive owners (write_acc step)
+  int pf;               // fused sphere-sphere kernel: list read-ahead + L2 prefetch of the force records
 };
 
 // An owner whose accumulated force never feeds its motion: fixed, or every

@@ -209,7 +209,7 @@ struct SsGeom {
 };
 
 __device__ __forceinline__ bool ss_geom(const DtView &v, uint32_t a, uint32_t b, SsGeom &g) {
-  const double4 cA = v.sph.center[a], cB = v.sph.center[b];
+  const double4 cA = ld256(v.sph.center + a), cB = ld256(v.sph.center + b);
   const double dx = cA.x - cB.x, dy = cA.y - cB.y, dz = cA.z - cB.z;
   const double d2 = dx * dx + dy * dy + dz * dz;
   const double R = cA.w + cB.w;
@@ -416,12 +416,30 @@ static __global__ void __launch_bounds__(256, kMinBlocks) k_contacts_ss(DtView v
     __syncwarp();
     qn = rest;
   };
+  // the contact list is streamed one iteration ahead (its load is off the
+  // critical path of the centre gathers); v.pf also prefetches each touching
+  // contact's kinematics records and history row into L2 when it is queued,
+  // so the force batch's loads find them there
+  uint2 id_next[kSsPerLane];
+#pragma unroll
+  for (int j = 0; j < kSsPerLane; ++j) {
+    const unsigned long long e = w0 + 32 * j + lane;
+    id_next[j] = e < n_ss ? __ldcs(v.ids + e) : make_uint2(0u, 0u);
+  }
   for (unsigned long long base = w0; base < n_ss; base += wstride) {
     uint2 id[kSsPerLane];
 #pragma unroll
     for (int j = 0; j < kSsPerLane; ++j) {
-      const unsigned long long e = base + 32 * j + lane;
-      id[j] = e < n_ss ? v.ids[e] : make_uint2(0u, 0u);
+      id[j] = id_next[j];
+      const unsigned long long e = base + wstride + 32 * j + lane;
+      if (v.pf) id_next[j] = e < n_ss ? __ldcs(v.ids + e) : make_uint2(0u, 0u);
+    }
+    if (!v.pf) {   // A/B switch (GF_SS_PF=0): the round-1 order, list loaded in the iteration
+#pragma unroll
+      for (int j = 0; j < kSsPerLane; ++j) {
+        const unsigned long long e = base + 32 * j + lane;
+        id[j] = e < n_ss ? v.ids[e] : make_uint2(0u, 0u);
+      }
     }
     SsGeom g[kSsPerLane];
     bool t[kSsPerLane];
@@ -429,6 +447,20 @@ static __global__ void __launch_bounds__(256, kMinBlocks) k_contacts_ss(DtView v
     for (int j = 0; j < kSsPerLane; ++j) {
       const unsigned long long e = base + 32 * j + lane;
       t[j] = e < n_ss && ss_geom(v, id[j].x, id[j].y & kSlotMask, g[j]);
+    }
+    if (v.pf) {
+#pragma unroll
+      for (int j = 0; j < kSsPerLane; ++j) {
+        if (t[j]) {
+          const char *ka = reinterpret_cast<const char *>(v.sph.kin + id[j].x);
+          const char *kb = reinterpret_cast<const char *>(v.sph.kin + (id[j].y & kSlotMask));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(kb));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(kb + 47));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(ka + 47));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const float4 *>(v.wild) +
+                                                        (base + 32 * j + lane)));
+        }
+      }
     }
 #pragma unroll
     for (int j = 0; j < kSsPerLane; ++j) {
@@ -826,6 +858,7 @@ static DtView dt_view(Ctx *c) {
   v.heavy_acc = c->heavy_acc.as<double>();
   v.st = c->status.as<Status>();
   v.acc_all = 1;
+  v.pf = c->ss_pf;
   return v;
 }
 

@@ -187,4 +187,60 @@ int halo_add_forces(Ctx *c, const uint32_t *idx, int64_t n, const void *in, cuda
   return 0;
 }
 
+// ---------------------------------------------------------------------------
+// active boxes on the device (engine.py:857-879): every
+// clump owner of the active or frozen family is re-tagged by whether its
+// position lies inside any box (|p - c| <= half per axis, c = the anchor
+// owner's position or a static centre); owners frozen now lose their
+// velocities; the re-tagged owners' kinematics records pick up the new
+// family's passive flag.  No host round trip of the owner state.
+// ---------------------------------------------------------------------------
+__global__ void k_active_boxes(Domain dom, Owners own, Spheres sph, int nbox, const double *box,
+                               const long long *anchor, uint32_t active, uint32_t frozen, int vel_f32,
+                               unsigned long long *n_changed) {
+  const int64_t o = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (o >= own.n) return;
+  const uint32_t s0 = sph.first[o], s1 = sph.first[o + 1];
+  if (s1 == s0) return;   // not a clump (meshes / analytic boundaries own no spheres)
+  const uint32_t meta = own.meta[o], fam = meta_family(meta);
+  if (fam != active && fam != frozen) return;
+  double p[3];
+  decode_pos(dom, own.voxel[o], own.sub[o], p[0], p[1], p[2]);
+  bool inside = false;
+  for (int b = 0; b < nbox && !inside; ++b) {
+    double cx = box[6 * b], cy = box[6 * b + 1], cz = box[6 * b + 2];
+    if (anchor[b] >= 0) {
+      const uint32_t a = uint32_t(anchor[b]);
+      decode_pos(dom, own.voxel[a], own.sub[a], cx, cy, cz);
+    }
+    inside = fabs(p[0] - cx) <= box[6 * b + 3] && fabs(p[1] - cy) <= box[6 * b + 4] &&
+             fabs(p[2] - cz) <= box[6 * b + 5];
+  }
+  const uint32_t nf = inside ? active : frozen;
+  if (nf == fam) return;
+  own.meta[o] = (nf << 24) | meta_tpl(meta);
+  if (nf == frozen) {
+    if (vel_f32) {
+      reinterpret_cast<float4 *>(own.lin_vel)[o] = make_float4(0.f, 0.f, 0.f, 0.f);
+      reinterpret_cast<float4 *>(own.ang_vel)[o] = make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+      double2 *lv = reinterpret_cast<double2 *>(own.lin_vel) + 2 * o, *av = reinterpret_cast<double2 *>(own.ang_vel) + 2 * o;
+      lv[0] = make_double2(0.0, 0.0); lv[1] = make_double2(0.0, 0.0);
+      av[0] = make_double2(0.0, 0.0); av[1] = make_double2(0.0, 0.0);
+    }
+  }
+  if (sph.kin)
+    for (uint32_t k = s0; k < s1; ++k) write_kin_from_state(own, sph, k, uint32_t(o));
+  atomicAdd(n_changed, 1ull);
+}
+
+int active_boxes(Ctx *c, int n_box, const double *box, const long long *anchor, uint32_t active, uint32_t frozen,
+                 unsigned long long *n_changed, cudaStream_t s) {
+  if (!c->n_owner) return 0;
+  k_active_boxes<<<blocks(c->n_owner, 256), 256, 0, s>>>(c->dom, owners_view(c), spheres_view(c), n_box, box, anchor,
+                                                         active, frozen, c->f32_state ? 1 : 0, n_changed);
+  GF_CHECK(c, cudaGetLastError());
+  return 0;
+}
+
 }  // namespace gf

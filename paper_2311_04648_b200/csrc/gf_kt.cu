@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(256) k_snapshot(Domain dom, Owners own, Sphere
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       if (kk[j] < sph.n) {
-        c[j] = sph.center[kk[j]];
+        c[j] = ld256(sph.center + kk[j]);
         ow[j] = sph.owner[kk[j]];
       }
     }
@@ -824,8 +824,8 @@ __global__ void __launch_bounds__(kFcBlock) k_filter_bits(KtView v, const uint2 
 #pragma unroll
   for (int q = 0; q < kFcPer; ++q) {
     if (e0 + 32 * q < n_cand) {
-      ci4[q] = v.c4[p[q].x];
-      cj4[q] = v.c4[p[q].y];
+      ci4[q] = ld256(v.c4 + p[q].x);
+      cj4[q] = ld256(v.c4 + p[q].y);
     }
   }
   uint32_t cnt = 0;
@@ -1118,16 +1118,30 @@ __global__ void k_inc_start(int64_t n_owner, int64_t n_inc, const uint32_t *sort
 // host entry points
 // ===========================================================================
 
+__global__ void k_set_int(int *p, int v) { *p = v; }
+
+// memset of possibly-peer memory from a stream of another device
+__global__ void k_zero_u64(unsigned long long *p, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    p[i] = 0ull;
+}
+
 int kt_snapshot(Ctx *c, cudaStream_t s, double margin) {
   KtScratch &k = c->kt;
-  if (ensure(c, k.c4, sizeof(double4) * (c->n_sph + 1), s))
-    return -1;
-  if (ensure(c, k.sfam, c->n_sph + 1, s)) return -1;
-  if (ensure(c, k.tri_world, sizeof(double) * 9 * (c->n_tri + 1), s)) return -1;
-  if (ensure(c, k.ana_world, sizeof(double) * 8 * (c->n_ana + 1), s)) return -1;
-  if (ensure(c, k.tfam, c->n_tri + 1, s)) return -1;
-  if (ensure(c, k.afam, c->n_ana + 1, s)) return -1;
-  if (ensure(c, k.minmax, sizeof(unsigned long long) * 8, s) || ensure(c, k.flag, 16, s)) return -1;
+  DevGuard gs(stream_device(s));   // launched on the stream's device (the dT one in a run)
+  {
+    // the snapshot lives with the rest of the kT scratch (the kT device of a
+    // 2-GPU split: the snapshot kernel stores it over NVLink)
+    DevGuard ga(c->kt_device);
+    if (ensure(c, k.c4, sizeof(double4) * (c->n_sph + 1), s))
+      return -1;
+    if (ensure(c, k.sfam, c->n_sph + 1, s)) return -1;
+    if (ensure(c, k.tri_world, sizeof(double) * 9 * (c->n_tri + 1), s)) return -1;
+    if (ensure(c, k.ana_world, sizeof(double) * 8 * (c->n_ana + 1), s)) return -1;
+    if (ensure(c, k.tfam, c->n_tri + 1, s)) return -1;
+    if (ensure(c, k.afam, c->n_ana + 1, s)) return -1;
+    if (ensure(c, k.minmax, sizeof(unsigned long long) * 8, s) || ensure(c, k.flag, 16, s)) return -1;
+  }
   // a detection snapshot (margin >= 0) also reduces the grid inputs and runs
   // the candidate displacement check (kt_begin then skips both)
   static const bool fuse_off = std::getenv("GF_NO_SNAP_FUSE") != nullptr;
@@ -1138,7 +1152,7 @@ int kt_snapshot(Ctx *c, cudaStream_t s, double margin) {
     if (k.cand_valid && c->skin_factor * margin != k.cand_skin) k.cand_valid = false;
     check = k.cand_valid && c->n_sph;
     k_minmax_init<<<1, 32, 0, s>>>(mm);
-    if (check) GF_CHECK(c, cudaMemsetAsync(k.flag.p, 0, sizeof(int), s));
+    if (check) k_set_int<<<1, 1, 0, s>>>(k.flag.as<int>(), 0);   // a kernel: the flag may be peer memory
   }
   const double skin = c->skin_factor * margin, skin_b = c->skin_big_factor * margin;
   // one wave of 3 CTAs / SM, grid-stride (2470 vs 2460 M sphere-steps/s at 8 / SM)
@@ -1197,12 +1211,11 @@ static KtView kt_view(Ctx *c, double margin) {
   return v;
 }
 
-__global__ void k_set_int(int *p, int v) { *p = v; }
-
 // phase A of a detection: grid, triangle registration, and the displacement
 // check that decides whether the candidate lists must be rebuilt (flag copied
 // to the pinned status mirror; the host reads it before kt_count)
 int kt_begin(Ctx *c, double margin, cudaStream_t s) {
+  DevGuard g_kt(stream_device(s));   // the kT device of a 2-GPU split
   KtScratch &k = c->kt;
   const int64_t n = c->n_sph, nt = c->n_tri;
   const int64_t n_pts = n + 3 * nt;
@@ -1269,6 +1282,7 @@ int kt_begin(Ctx *c, double margin, cudaStream_t s) {
 // rebuild the candidate lists from the current snapshot (enumeration grid
 // with reach margin + skin)
 static int rebuild_candidates(Ctx *c, cudaStream_t s) {
+  DevGuard g_kt(stream_device(s));   // the kT device of a 2-GPU split
   KtScratch &k = c->kt;
   const int64_t n = c->n_sph;
   const double skin = c->skin_factor * c->kt_margin, skin_b = c->skin_big_factor * c->kt_margin;
@@ -1439,6 +1453,7 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
 // filter of the candidates, sphere-triangle / sphere-analytic pairs, counts,
 // scan; the pair total goes to the pinned status mirror
 int kt_count(Ctx *c, cudaStream_t s, bool force_rebuild) {
+  DevGuard g_kt(stream_device(s));   // the kT device of a 2-GPU split
   KtScratch &k = c->kt;
   const int64_t n = c->n_sph;
   Status *hs = reinterpret_cast<Status *>(c->h_status);
@@ -1466,12 +1481,16 @@ int kt_count(Ctx *c, cudaStream_t s, bool force_rebuild) {
     // synchronises the device, so a slowly growing pair count must not
     // trigger one per detection
     int64_t cap = need + need / 4 + 1024;
+    DevGuard g_dt(c->device);   // contact arrays live on the dT device
     if (ensure(c, out.ids, sizeof(uint2) * cap, s) || ensure(c, out.wild, sizeof(float) * c->wild_w * cap, s) ||
         ensure(c, out.old_pos, sizeof(uint32_t) * cap, s))
       return -1;
     out.cap = cap;
   }
-  if (ensure(c, out.seg, sizeof(unsigned long long) * (3 * n + 1), s)) return -1;
+  {
+    DevGuard g_dt(c->device);
+    if (ensure(c, out.seg, sizeof(unsigned long long) * (3 * n + 1), s)) return -1;
+  }
   KtView v = kt_view(c, c->kt_margin);
   unsigned long long *cnt = k.counts.as<unsigned long long>();
   unsigned long long *tn = k.tmp_n.as<unsigned long long>();
@@ -1503,7 +1522,7 @@ int kt_count(Ctx *c, cudaStream_t s, bool force_rebuild) {
         rows_ok ? k.fbits[prev].as<uint32_t>() : nullptr, rows_ok ? k.fpre[prev].as<unsigned long long>() : nullptr,
         out.ids.as<uint2>(), oseg, out.old_pos.as<uint32_t>(), (unsigned long long)(out.cap - k.tmp_cap - 1));
   } else {
-    GF_CHECK(c, cudaMemsetAsync(oseg, 0, sizeof(unsigned long long) * (n + 1), s));
+    k_zero_u64<<<grid_for(n + 1), kBlock, 0, s>>>(oseg, n + 1);   // oseg: the dT device's array
     GF_CHECK(c, cudaMemsetAsync(k.fpre[cur].p, 0, sizeof(unsigned long long), s));
   }
   out.det_id = det;
@@ -1548,6 +1567,7 @@ int kt_count(Ctx *c, cudaStream_t s, bool force_rebuild) {
 // canonical (kind, a, b) array; keeps the segment offsets with the array for
 // the next history remap.  Host has synced on the count phase.
 int kt_detect_fill(Ctx *c, Acs &out, cudaStream_t s) {
+  DevGuard g_kt(stream_device(s));   // the kT device of a 2-GPU split
   KtScratch &k = c->kt;
   const int64_t n = c->n_sph;
   Status *hs = reinterpret_cast<Status *>(c->h_status);
@@ -1585,6 +1605,7 @@ int kt_detect_fill(Ctx *c, Acs &out, cudaStream_t s) {
 
 int kt_bin_ranges(Ctx *c, double margin, int64_t *h_out) {
   cudaStream_t s = c->s_kt;
+  DevGuard g_kt(c->kt_device);
   const int64_t n = c->n_sph;
   DBuf tmp;
   if (ensure(c, tmp, sizeof(long long) * 6 * (n + 1), s)) return -1;
@@ -1593,6 +1614,142 @@ int kt_bin_ranges(Ctx *c, double margin, int64_t *h_out) {
   GF_CHECK(c, cudaMemcpyAsync(h_out, tmp.p, sizeof(long long) * 6 * n, cudaMemcpyDeviceToHost, s));
   GF_CHECK(c, cudaStreamSynchronize(s));
   cudaFree(tmp.p);
+  return 0;
+}
+
+
+// Persistent contacts (bonded models, engine.py:639-662): an old row whose
+// wildcard `col` is > 0 (an intact bond) that the new detection no longer
+// holds is re-appended.  k_persist_mark flags them, k_persist_keys /
+// k_persist_gather rebuild the array in canonical order.
+__global__ void k_persist_mark(int64_t n_old, const uint2 *old_ids, const float *old_wild, int W, int col,
+                               const uint2 *new_ids, const unsigned long long *new_seg, int64_t n_sph,
+                               uint8_t *lost, unsigned long long *n_lost) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= n_old) return;
+  uint8_t l = 0;
+  if (old_wild[int64_t(W) * i + col] > 0.0f) {
+    const uint2 id = old_ids[i];
+    const int64_t sg = int64_t(id.y >> kKindShift) * n_sph + id.x;
+    bool found = false;
+    for (unsigned long long q = new_seg[sg]; q < new_seg[sg + 1]; ++q) {
+      const uint32_t y = new_ids[q].y;
+      if (y == id.y) { found = true; break; }
+      if (y > id.y) break;
+    }
+    l = found ? 0 : 1;
+    if (l) atomicAdd(n_lost, 1ull);
+  }
+  lost[i] = l;
+}
+
+__device__ __forceinline__ unsigned long long persist_key(uint2 id) {
+  return (static_cast<unsigned long long>(id.y >> kKindShift) << 60) |
+         (static_cast<unsigned long long>(id.x) << 30) | static_cast<unsigned long long>(id.y & kSlotMask);
+}
+
+// keys of the new rows (source r) and of the lost old rows (source ~i),
+// appended at the positions `pos` (exclusive scan of `lost`)
+__global__ void k_persist_keys(int64_t n_new, const uint2 *new_ids, int64_t n_old, const uint2 *old_ids,
+                               const uint8_t *lost, const unsigned long long *pos, unsigned long long *keys,
+                               long long *src) {
+  const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (t < n_new) {
+    keys[t] = persist_key(new_ids[t]);
+    src[t] = t;
+  } else if (t < n_new + n_old) {
+    const int64_t i = t - n_new;
+    if (lost[i]) {
+      keys[n_new + pos[i]] = persist_key(old_ids[i]);
+      src[n_new + pos[i]] = ~static_cast<long long>(i);
+    }
+  }
+}
+
+__global__ void k_persist_gather(int64_t n, const long long *src, const uint2 *new_ids, const float *new_wild,
+                                 const uint2 *old_ids, const float *old_wild, int W, uint2 *out_ids,
+                                 float *out_wild) {
+  const int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (k >= n) return;
+  const long long s_ = src[k];
+  const bool from_old = s_ < 0;
+  const int64_t r = from_old ? ~s_ : s_;
+  out_ids[k] = from_old ? old_ids[r] : new_ids[r];
+  const float *w = (from_old ? old_wild : new_wild) + int64_t(W) * r;
+  for (int q = 0; q < W; ++q) out_wild[int64_t(W) * k + q] = w[q];
+}
+
+
+// re-append the intact bonds the new detection dropped (rare; synchronises
+// once per adoption while a persistent column is set)
+static int persist_lost(Ctx *c, cudaStream_t s) {
+  Acs &nw = c->acs_next;
+  Acs &old = c->acs;
+  const int W = c->wild_w;
+  uint8_t *lost = nullptr;
+  unsigned long long *cnt = nullptr, *pos = nullptr;
+  GF_CHECK(c, cudaMallocAsync(&lost, size_t(old.n) + 1, s));
+  GF_CHECK(c, cudaMallocAsync(&cnt, sizeof(unsigned long long), s));
+  GF_CHECK(c, cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), s));
+  if (!nw.seg.p && build_segments(c, nw, s)) return -1;
+  k_persist_mark<<<grid_for(old.n), kBlock, 0, s>>>(old.n, old.ids.as<uint2>(), old.wild.as<float>(), W,
+                                                    c->persist_col, nw.ids.as<uint2>(),
+                                                    nw.seg.as<unsigned long long>(), c->n_sph, lost, cnt);
+  unsigned long long h_lost = 0;
+  GF_CHECK(c, cudaMemcpyAsync(&h_lost, cnt, sizeof(h_lost), cudaMemcpyDeviceToHost, s));
+  GF_CHECK(c, cudaStreamSynchronize(s));
+  if (h_lost) {
+    const int64_t n_tot = nw.n + int64_t(h_lost);
+    unsigned long long *keys = nullptr, *keys2 = nullptr;
+    long long *src = nullptr, *src2 = nullptr;
+    uint2 *ids = nullptr;
+    float *wild = nullptr;
+    GF_CHECK(c, cudaMallocAsync(&pos, sizeof(unsigned long long) * (old.n + 1), s));
+    GF_CHECK(c, cudaMallocAsync(&keys, sizeof(unsigned long long) * n_tot, s));
+    GF_CHECK(c, cudaMallocAsync(&keys2, sizeof(unsigned long long) * n_tot, s));
+    GF_CHECK(c, cudaMallocAsync(&src, sizeof(long long) * n_tot, s));
+    GF_CHECK(c, cudaMallocAsync(&src2, sizeof(long long) * n_tot, s));
+    GF_CHECK(c, cudaMallocAsync(&ids, sizeof(uint2) * n_tot, s));
+    GF_CHECK(c, cudaMallocAsync(&wild, sizeof(float) * W * n_tot, s));
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, lost, pos, int(old.n), s);
+    void *tmp = nullptr;
+    GF_CHECK(c, cudaMallocAsync(&tmp, tb + 16, s));
+    GF_CHECK(c, cub::DeviceScan::ExclusiveSum(tmp, tb, lost, pos, int(old.n), s));
+    cudaFreeAsync(tmp, s);
+    k_persist_keys<<<grid_for(nw.n + old.n), kBlock, 0, s>>>(nw.n, nw.ids.as<uint2>(), old.n, old.ids.as<uint2>(),
+                                                             lost, pos, keys, src);
+    tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, src, src2, int(n_tot), 0, 62, s);
+    GF_CHECK(c, cudaMallocAsync(&tmp, tb + 16, s));
+    GF_CHECK(c, cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, src, src2, int(n_tot), 0, 62, s));
+    cudaFreeAsync(tmp, s);
+    k_persist_gather<<<grid_for(n_tot), kBlock, 0, s>>>(n_tot, src2, nw.ids.as<uint2>(), nw.wild.as<float>(),
+                                                        old.ids.as<uint2>(), old.wild.as<float>(), W, ids, wild);
+    if (n_tot > nw.cap) {
+      const int64_t cap = n_tot + n_tot / 4 + 1024;
+      if (ensure(c, nw.ids, sizeof(uint2) * cap, s) || ensure(c, nw.wild, sizeof(float) * W * cap, s) ||
+          ensure(c, nw.old_pos, sizeof(uint32_t) * cap, s))
+        return -1;
+      nw.cap = cap;
+    }
+    GF_CHECK(c, cudaMemcpyAsync(nw.ids.p, ids, sizeof(uint2) * n_tot, cudaMemcpyDeviceToDevice, s));
+    GF_CHECK(c, cudaMemcpyAsync(nw.wild.p, wild, sizeof(float) * W * n_tot, cudaMemcpyDeviceToDevice, s));
+    for (void *p : {static_cast<void *>(pos), static_cast<void *>(keys), static_cast<void *>(keys2),
+                    static_cast<void *>(src), static_cast<void *>(src2), static_cast<void *>(ids),
+                    static_cast<void *>(wild)})
+      cudaFreeAsync(p, s);
+    nw.n = n_tot;
+    // the rows no longer mirror the candidate filter: the next adoption
+    // searches segments instead of gathering by candidate rank
+    nw.det_id = 0;
+    nw.pos_valid = false;
+    if (build_segments(c, nw, s)) return -1;
+    c->persisted += int64_t(h_lost);
+  }
+  cudaFreeAsync(lost, s);
+  cudaFreeAsync(cnt, s);
+  GF_CHECK(c, cudaGetLastError());
   return 0;
 }
 
@@ -1611,6 +1768,7 @@ int adopt_acs(Ctx *c, cudaStream_t s) {
                                                  old.seg.as<unsigned long long>(), c->n_sph, c->wild_w);
   else if (nw.n)
     GF_CHECK(c, cudaMemsetAsync(nw.wild.p, 0, sizeof(float) * c->wild_w * nw.n, s));
+  if (c->persist_col >= 0 && old.n && old.seg.p && persist_lost(c, s)) return -1;
   std::swap(c->acs, c->acs_next);
   c->ca_updates++;
   GF_CHECK(c, cudaGetLastError());

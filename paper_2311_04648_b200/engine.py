@@ -86,22 +86,46 @@ class ActiveBoxPolicy:
 
 
 class Tracker:
-    """Owner handle (engine.py:132-189); reads reflect the last completed step."""
+    """Owner handle (engine.py:132-189); reads reflect the last completed step.
+
+    While the host mirrors are stale (after a run), reads gather just this
+    owner's record on the device (gf_read_owners) instead of syncing the
+    whole state -- the rover co-simulation's per-wheel force readback
+     costs one small copy, not an n-owner download."""
 
     def __init__(self, sim: "Simulator", owner: int):
         self._sim = sim
         self.owner = owner
 
+    def _dev(self):
+        """This owner's device record, or None when the host mirror is current."""
+        sim = self._sim
+        if sim._ctx is None or not sim._host_stale or sim.decomposition is not None:
+            return None
+        return sim._read_owner(self.owner)
+
     def pos(self) -> np.ndarray:
+        r = self._dev()
+        if r is not None:
+            return r["pos"]
         return self._sim._pos[self.owner].copy()
 
     def vel(self) -> np.ndarray:
+        r = self._dev()
+        if r is not None:
+            return r["lin_vel"]
         return self._sim.store.lin_vel[self.owner].astype(np.float64)
 
     def ang_vel_local(self) -> np.ndarray:
+        r = self._dev()
+        if r is not None:
+            return r["ang_vel"]
         return self._sim.store.ang_vel[self.owner].astype(np.float64)
 
     def quat(self) -> np.ndarray:
+        r = self._dev()
+        if r is not None:
+            return r["quat"]
         return self._sim.store.quat[self.owner].astype(np.float64)
 
     def moi(self) -> np.ndarray:
@@ -111,17 +135,23 @@ class Tracker:
         return float(self._sim.store.mass[self.owner])
 
     def contact_force(self) -> np.ndarray:
+        r = self._dev()
+        if r is not None:
+            return r["acc_force"]
         return self._sim.store.acc_force[self.owner].copy()
 
     def contact_torque(self) -> np.ndarray:
+        r = self._dev()
+        if r is not None:
+            return r["acc_torque"]
         return self._sim.store.acc_torque[self.owner].copy()
 
     def contact_acc(self) -> np.ndarray:
         return self.contact_force() / self.mass()
 
     def contact_ang_acc_local(self) -> np.ndarray:
-        q = self._sim.store.quat[self.owner].astype(np.float64)
-        tl = quat_rotate(np.array([q[0], -q[1], -q[2], -q[3]]), self._sim.store.acc_torque[self.owner])
+        q = self.quat()
+        tl = quat_rotate(np.array([q[0], -q[1], -q[2], -q[3]]), self.contact_torque())
         return tl / self.moi()
 
     def set_pos(self, xyz) -> None:
@@ -153,6 +183,10 @@ class Inspector:
     def get_value(self) -> float:
         sim = self._sim
         if self.quantity == "clump_max_absv":
+            if sim._ctx is not None and sim._host_stale and sim.decomposition is None:
+                out = C.c_double(0.0)   # a device reduction, no state download
+                sim._ctx.call("gf_clump_max_absv", C.byref(out))
+                return float(out.value)
             s = sim.store
             n = s.n_owners
             if n == 0:
@@ -178,7 +212,8 @@ class Simulator:
     default_sync = False
 
     def __init__(self, domain: Domain, force_model: str = "hertz_mindlin", *,
-                 device: int = 0, precision: str = "f64", reorder=None, decomposition=None):
+                 device: int = 0, precision: str = "f64", reorder=None, decomposition=None,
+                 kt_device=None):
         if precision not in ("f64", "f32"):
             raise ValidationError(f"precision must be 'f64' or 'f32', got {precision!r}")
         self.materials = MaterialTable()
@@ -193,6 +228,12 @@ class Simulator:
         self.sim_time = 0.0
         self.active_box_policy = None
         self.device = int(device)
+        # the paper's 2-GPU split: contact detection (kT) on
+        # kt_device, forces and integration (dT) on `device`; None = both on
+        # `device` as concurrent streams
+        self.kt_device = None if kt_device is None else int(kt_device)
+        if self.kt_device is not None and decomposition is not None:
+            raise ConfigurationError("the 2-GPU kT/dT split and the slab decomposition are separate modes")
         self.precision = precision
         # device memory order: Morton order of the initial positions so contact
         # gathers hit nearby owners; the fp64 parity build keeps the reference's
@@ -347,8 +388,27 @@ class Simulator:
             self.set_family_mask(policy.frozen_family, fam, False)
 
     def init_bonds(self, gamma_int: float):
-        raise ConfigurationError("init_bonds requires the breakage force model, which this "
-                                 "build does not provide on the device")
+        """Install bonds between nearby sphere pairs (engine.py:409-427); call
+        after the scene is built and before initialize().  Requires the
+        breakage force model (models.BREAKAGE_SRC, NVRTC).  Bond candidates
+        come from the device detection (forces.build_bonds)."""
+        if self.model.name != "breakage":
+            raise ConfigurationError("init_bonds requires the breakage force model")
+        if self._initialized:
+            raise ConfigurationError("init_bonds must run before initialize()")
+        from .core import quat_rotate_many
+        s = self.store
+        geom_ids = np.nonzero(s.geom_kind[:s.n_geoms] == GEOM_SPHERE)[0].astype(np.int64)
+        owners = s.geom_owner[geom_ids]
+        pos = s.positions()
+        offsets = s.geom_params[geom_ids, :3].astype(np.float64)
+        centers = pos[owners] + quat_rotate_many(s.quat[owners], offsets)
+        radii = s.geom_params[geom_ids, 3].astype(REAL)
+        bonds, stats = F.build_bonds(centers, radii, geom_ids, owners, gamma_int)
+        r_max = float(radii.max()) if radii.size else 0.0
+        self.set_added_margin(max(0.0, (gamma_int - 1.0) * 2.0 * r_max) + 0.05 * r_max)
+        self._acs = bonds
+        return stats
 
     # -- lifecycle ----------------------------------------------------------------
     def initialize(self) -> None:
@@ -385,7 +445,7 @@ class Simulator:
         # mass-property templates: unique (mass, moi) rows
         self._tpl_rows, self._tpl_id = self._mass_templates()
 
-        self._ctx = _lib.Context(self.device, f32_state=(self.precision == "f32"))
+        self._ctx = _lib.Context(self.device, f32_state=(self.precision == "f32"), kt_device=self.kt_device)
         ctx, P = self._ctx, _lib.ptr
         dom = s.domain
         ctx.call("gf_set_domain", P(_lib.carr(dom.lo, np.float64)), P(_lib.carr(dom.hi, np.float64)),
@@ -394,6 +454,8 @@ class Simulator:
             log = C.create_string_buffer(1 << 16)
             ctx.call("gf_set_force_model", self.model.cuda_src.encode(), _lib.CSRC_DIR.encode(),
                      C.c_int(len(self.model.wildcards)), log, C.c_size_t(1 << 16))
+            if "unbroken" in self.model.wildcards:   # bonds persist (engine.py:639-662)
+                ctx.call("gf_set_persistent_wildcard", C.c_int(self.model.wildcards.index("unbroken")))
         self._upload_tables()
         self._upload_owners()
         gp = s.geom_params[:n_g]
@@ -527,6 +589,20 @@ class Simulator:
             ctx.call("gf_set_external_loads", P(ef), P(et))
         else:
             ctx.call("gf_set_external_loads", None, None)
+
+    def _read_owner(self, owner: int) -> dict:
+        """One owner's state straight from the device (gf_read_owners)."""
+        from .core import decode_position
+        d = int(self._own_u2d[int(owner)])
+        out = np.zeros((1, 23), np.float64)
+        with self._lock:
+            self._ctx.call("gf_read_owners", C.c_int64(1), _lib.ptr(np.array([d], np.int64)), _lib.ptr(out))
+        r = out[0]
+        vox = np.array([r[0]], np.float64).view(np.uint64)
+        sub = r[1:4].astype(np.uint16).reshape(1, 3)
+        return {"pos": decode_position(vox, sub, self.store.domain)[0], "quat": r[4:8].copy(),
+                "lin_vel": r[8:11].copy(), "ang_vel": r[11:14].copy(), "family": int(r[14]),
+                "acc_force": r[15:18].copy(), "acc_torque": r[18:21].copy()}
 
     def _sync_all(self):
         """Device -> host mirror of every owner field."""
@@ -755,28 +831,30 @@ class Simulator:
         return getattr(self, "_box_next", 0.0)
 
     def _apply_active_boxes(self) -> None:
-        """Family re-tagging at box refresh (engine.py:857-879), host-side at a
-        step boundary."""
+        """Family re-tagging at box refresh (engine.py:857-879), on the device
+        (gf_apply_active_boxes): positions, families and velocities never
+        leave HBM; the host mirrors are marked stale."""
         policy = self.active_box_policy
-        s = self.store
-        n = s.n_owners
-        fam = s.owner_family[:n]
-        managed = ((fam == policy.active_family) | (fam == policy.frozen_family)) & \
-            (s.owner_kind[:n] == OWNER_CLUMP)
-        if not managed.any():
+        nb = len(policy.half_extents)
+        if nb == 0:
             return
-        pos = self._pos[:n]
-        inside = np.zeros(n, dtype=bool)
-        for half, anchor, center in zip(policy.half_extents, policy.anchors, policy.centers):
-            c = pos[anchor] if anchor is not None else np.asarray(center)
-            inside |= np.all(np.abs(pos - c) <= np.asarray(half, dtype=np.float64), axis=1)
-        new_fam = np.where(inside, policy.active_family, policy.frozen_family)
-        changed = managed & (fam != new_fam)
-        if changed.any():
-            s.owner_family[:n][changed] = new_fam[changed]
-            frozen_now = changed & (new_fam == policy.frozen_family)
-            s.lin_vel[:n][frozen_now] = 0.0
-            s.ang_vel[:n][frozen_now] = 0.0
+        boxes = np.zeros((nb, 6), np.float64)
+        anchors = np.full(nb, -1, np.int64)
+        for b, (half, anchor, center) in enumerate(zip(policy.half_extents, policy.anchors, policy.centers)):
+            boxes[b, 3:] = np.asarray(half, dtype=np.float64)
+            if anchor is not None:
+                anchors[b] = int(self._own_u2d[int(anchor)])
+            else:
+                boxes[b, :3] = np.asarray(center, dtype=np.float64)
+        with self._lock:
+            self._push_host()
+            changed = C.c_int64(0)
+            self._ctx.call("gf_apply_active_boxes", C.c_int(nb), _lib.ptr(boxes), _lib.ptr(anchors),
+                           C.c_int(int(policy.active_family)), C.c_int(int(policy.frozen_family)),
+                           C.byref(changed))
+            if changed.value:
+                self._host_stale = True
+        self.box_retags = getattr(self, "box_retags", 0) + int(changed.value)
 
     def _run(self, steps: int) -> None:
         if self.decomposition is not None:

@@ -280,6 +280,12 @@ DEFAULT_MODEL = register_force_model(ForceModel(
 ))
 
 
+def _registered_models():
+    """BREAKAGE_MODEL and the other shipped NVRTC models (models.py)."""
+    from . import models
+    return models.breakage_model()
+
+
 def evaluate_default_model(ctx: ContactContext, materials: MaterialTable) -> ContactResult:
     """forces.py:468-469: the built-in model on one context."""
     return DEFAULT_MODEL.evaluate(ctx, material_pair_stack(materials, DEFAULT_MODEL))
@@ -401,3 +407,49 @@ def reduce_to_owners(owner_a, owner_b, forces, tofs, contact_points, owner_pos, 
         P(carr(contact_points, np.float64).reshape(-1, 3)), C.c_int64(n_o), P(op),
         P(carr(mass, np.float64).reshape(-1)), P(carr(gravity, np.float64).reshape(3)), P(acc_f), P(acc_t))
     return acc_f, acc_t
+
+
+BREAKAGE_MODEL = _registered_models()
+
+
+def build_bonds(centers, radii, geom_ids, owner_ids, gamma_int: float):
+    """Bond every sphere pair whose centre distance is below gamma_int (R_i +
+    R_j) (forces.py:617-675): candidate pairs from the device detection
+    (detect_contacts with margin (gamma_int - 1) 2 r_max), the exact distance
+    cut, initialLength = the overlap at creation.  Returns (ContactArray with
+    the breakage wildcards, stats)."""
+    from . import broadphase as B
+    if gamma_int <= 0.0:
+        raise ValidationError(f"gamma_int must be positive, got {gamma_int}")
+    centers = np.asarray(centers, dtype=np.float64).reshape(-1, 3)
+    radii = np.asarray(radii, dtype=REAL).reshape(-1)
+    m = centers.shape[0]
+    r_max = float(radii.max()) if m else 0.0
+    margin = max(0.0, (gamma_int - 1.0) * 2.0 * r_max) + 1e-12
+    snap = B.DetectionSnapshot(
+        sph_center=centers, sph_radius=radii, sph_geom=np.arange(m, dtype=np.int64),
+        sph_owner=np.asarray(owner_ids, dtype=np.int64), sph_family=np.zeros(m, np.uint8),
+        tri_world=np.zeros((0, 9)), tri_geom=np.zeros(0, np.int64), tri_owner=np.zeros(0, np.int64),
+        tri_family=np.zeros(0, np.uint8), ana_world=np.zeros((0, 8)), ana_kind=np.zeros(0, np.uint8),
+        ana_geom=np.zeros(0, np.int64), ana_owner=np.zeros(0, np.int64), ana_family=np.zeros(0, np.uint8),
+        mask=np.ones((256, 256), dtype=bool))
+    cand = B.detect_contacts(snap, margin)
+    a, b = cand.geom_a, cand.geom_b
+    d = np.linalg.norm(centers[a] - centers[b], axis=1)
+    rsum = radii[a].astype(np.float64) + radii[b].astype(np.float64)
+    keep = d < gamma_int * rsum
+    a, b = a[keep], b[keep]
+    overlap = rsum[keep] - d[keep]
+    gid = np.asarray(geom_ids, dtype=np.int64)
+    bonds = B.ContactArray(np.full(a.shape[0], B.CONTACT_SS, dtype=np.uint8), gid[a], gid[b])
+    for name in BREAKAGE_MODEL.wildcards:
+        bonds.wildcards[name] = np.zeros(bonds.size, dtype=REAL)
+    bonds.wildcards["unbroken"][:] = 1.0
+    bonds.wildcards["initialLength"][:] = overlap.astype(REAL)
+    bonds = bonds.canonicalize()
+    degree = np.bincount(a, minlength=m) + np.bincount(b, minlength=m)
+    assigned = np.bincount(a, minlength=m)
+    stats = {"count": int(a.shape[0]), "mean_degree": float(degree.mean()) if m else 0.0,
+             "modal_degree": int(np.bincount(degree).argmax()) if m else 0,
+             "modal_assigned": int(np.bincount(assigned).argmax()) if m else 0}
+    return bonds, stats

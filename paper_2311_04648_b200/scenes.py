@@ -39,7 +39,7 @@ def crater_bed(n_spheres: int = 1_000_000, *, seed: int = 7, h: float = 1e-5, v_
                n_max: int = 4, precision: str = "f32", device: int = 0, ball: bool = True,
                drop_height: float = 0.20, ball_density: float = 7800.0, decomposition=None,
                tiles: int = 1, hold_ball: bool = False, force_model: str = "hertz_mindlin",
-               extra_props: dict | None = None) -> Simulator:
+               extra_props: dict | None = None, kt_device=None) -> Simulator:
     rng = np.random.default_rng(seed)
     D = 0.0254
     bed_half = 12.0 * D / 2.0
@@ -56,7 +56,8 @@ def crater_bed(n_spheres: int = 1_000_000, *, seed: int = 7, h: float = 1e-5, v_
     r_max = float(radii.max())
     dom = Domain((-half_x - 0.2 * bed_half, -bed_half * 1.2, -0.02),
                  (half_x + 0.2 * bed_half, bed_half * 1.2, depth * 3.0 + 0.3))
-    sim = Simulator(dom, force_model, precision=precision, device=device, decomposition=decomposition)
+    sim = Simulator(dom, force_model, precision=precision, device=device, decomposition=decomposition,
+                    kt_device=kt_device)
     grain = sim.load_material({**CRATER_MATERIAL, **(extra_props or {})})
     wall = sim.load_material({**CRATER_MATERIAL, **(extra_props or {})})
     tpls = [sim.load_clump_template(ClumpTemplate.solid_sphere(
@@ -112,7 +113,7 @@ CRATER_MATERIAL = {"E": 5e6, "nu": 0.3, "CoR": 0.5, "mu": 0.3, "Crr": 0.01}
 
 
 def tiled_bed(src: Simulator, tx: int, ty: int, *, precision: str = "f32", device: int = 0,
-              n_max: int = 4) -> Simulator:
+              n_max: int = 4, kt_device=None) -> Simulator:
     """tx x ty copies of the (settled, released) crater bed `src` in one box:
     owners keep their state (position, orientation, velocities), copies are
     laid out at the bed pitch 12 D, the floor and the four outer walls bound
@@ -131,7 +132,7 @@ def tiled_bed(src: Simulator, tx: int, ty: int, *, precision: str = "f32", devic
     lo, hi = s.domain.lo, s.domain.hi
     dom = Domain((-tx * bed_half - 0.2 * bed_half, -ty * bed_half - 0.2 * bed_half, float(lo[2])),
                  (tx * bed_half + 0.2 * bed_half, ty * bed_half + 0.2 * bed_half, float(hi[2])))
-    sim = Simulator(dom, precision=precision, device=device, reorder=False)
+    sim = Simulator(dom, precision=precision, device=device, reorder=False, kt_device=kt_device)
     grain = sim.load_material(dict(CRATER_MATERIAL))
     wall = sim.load_material(dict(CRATER_MATERIAL))
     for t in s.templates:
@@ -331,3 +332,139 @@ def oracle_scene(sim: Simulator) -> dict:
         lv_mask=sim._lv_mask.astype(np.uint8), lv_val=sim._lv_val.copy(),
         av_mask=sim._av_mask.astype(np.uint8), av_val=sim._av_val.copy(),
         gravity=sim.gravity.copy(), h=float(sim.h), v_err=float(sim.v_err))
+
+
+# ---------------------------------------------------------------------------
+# configs[4] rover wheel: a grousered wheel mesh with a
+# prescribed spin of 0.8 rad/s rolling through a GRC-1-like terrain of
+# multi-sphere clumps (table GRCDS: component radius,
+# clump size, weight share; E = 1e8, nu = 0.3, mu = 0.4, CoR = 0.5), DEM step
+# 2e-6 s.
+# ---------------------------------------------------------------------------
+
+# type: (clump size, component radius, weight share) -- PAPER.md:1196-1202
+GRC1_TYPES = ((21.0e-3, 3.6e-3, 0.17), (11.4e-3, 1.95e-3, 0.21), (6.6e-3, 1.81e-3, 0.14),
+              (4.5e-3, 1.24e-3, 0.19), (3.0e-3, 0.82e-3, 0.16), (2.75e-3, 0.75e-3, 0.05),
+              (2.5e-3, 0.70e-3, 0.08))
+GRC1_MATERIAL = {"E": 1e8, "nu": 0.3, "CoR": 0.5, "mu": 0.4, "Crr": 0.0}
+WHEEL_FAMILY = 2
+
+
+def grousered_wheel(radius: float = 0.25, width: float = 0.2, n_around: int = 96, n_grousers: int = 24,
+                    grouser_h: float = 0.02) -> np.ndarray:
+    """Triangles (n, 3, 3) of a wheel centred at the origin, axle along y:
+    the rim (n_around quads), two side disks (fans) and n_grousers radial
+    fins of height grouser_h spanning the width."""
+    th = np.linspace(0.0, 2.0 * math.pi, n_around + 1)
+    hw = width / 2.0
+    tris = []
+    for a, b in zip(th[:-1], th[1:]):
+        p = lambda t, y, r=radius: (r * math.cos(t), y, r * math.sin(t))  # noqa: E731
+        tris.append((p(a, -hw), p(b, -hw), p(b, hw)))
+        tris.append((p(a, -hw), p(b, hw), p(a, hw)))
+        for y in (-hw, hw):
+            tris.append(((0.0, y, 0.0), p(a, y), p(b, y)))
+    for t in np.linspace(0.0, 2.0 * math.pi, n_grousers, endpoint=False):
+        c, s = math.cos(t), math.sin(t)
+        r0, r1 = radius, radius + grouser_h
+        q00, q10 = (r0 * c, -hw, r0 * s), (r1 * c, -hw, r1 * s)
+        q01, q11 = (r0 * c, hw, r0 * s), (r1 * c, hw, r1 * s)
+        tris.append((q00, q10, q11))
+        tris.append((q00, q11, q01))
+    return np.asarray(tris, dtype=np.float64)
+
+
+def grc1_templates(sim: Simulator, material: int, density: float = 2500.0, scale: float = 1.0):
+    """One clump template per GRC-1 type: ceil(size / (2 r_c)) component
+    spheres of radius r_c on a line spanning the clump size; mass and
+    principal MOI of the spheres (overlaps ignored)."""
+    from .core import ClumpSphere
+    out = []
+    for size, rc, share in GRC1_TYPES:
+        size, rc = size * scale, rc * scale
+        k = max(2, int(math.ceil(size / (2.0 * rc))))
+        span = size - 2.0 * rc
+        xs = np.linspace(-span / 2.0, span / 2.0, k)
+        ms = density * 4.0 / 3.0 * math.pi * rc ** 3
+        m = k * ms
+        i_ax = k * 0.4 * ms * rc * rc
+        i_pe = i_ax + ms * float(np.sum(xs * xs))
+        tpl = ClumpTemplate(m, np.array([i_ax, i_pe, i_pe]),
+                            tuple(ClumpSphere(np.array([x, 0.0, 0.0]), rc, material) for x in xs))
+        out.append((sim.load_clump_template(tpl), tpl, share, size, k))
+    return out
+
+
+def rover_wheel(n_spheres: int = 11_000_000, *, seed: int = 3, h: float = 2e-6, v_err: float = 3.0,
+                n_max: int = 8, precision: str = "f32", device: int = 0, omega: float = 0.8,
+                slip: float = 0.2, wheel_radius: float = 0.25, sinkage: float = 0.02,
+                aspect: float = 4.0, kt_device=None) -> Simulator:
+    """A GRC-1-like terrain of about n_spheres component spheres in a walled
+    trough (length = aspect x width) with the grousered wheel resting
+    `sinkage` into its surface at one end, spinning at `omega` about its axle
+    and moving forward at omega R (1 - slip) (family WHEEL_FAMILY, fully
+    prescribed: a boundary owner whose contact force is read back).  Clumps
+    sit on an HCP lattice of pitch = the type-2 clump size (11.4 mm), random
+    types by number share (the 21 mm type-1 clumps take two lattice sites),
+    random orientations."""
+    rng = np.random.default_rng(seed)
+    pitch = GRC1_TYPES[1][0] * 1.02
+    # number shares from the weight shares (w / m, m ~ k rc^3)
+    w = np.array([t[2] for t in GRC1_TYPES])
+    per = np.array([max(2, math.ceil(t[0] / (2 * t[1]))) * t[1] ** 3 for t in GRC1_TYPES])
+    num = w / per
+    num /= num.sum()
+    k_of = np.array([max(2, math.ceil(t[0] / (2 * t[1]))) for t in GRC1_TYPES])
+    spheres_per_site = float(np.sum(num * k_of))
+    n_sites = int(n_spheres / spheres_per_site)
+    site_vol = pitch ** 3 / math.sqrt(2.0)
+    depth = 0.12 if n_sites > 200_000 else 0.06
+    width = math.sqrt(n_sites * site_vol / (aspect * depth))
+    length = aspect * width
+    dom = Domain((-length / 2 - 0.3, -width / 2 - 0.05, -0.02),
+                 (length / 2 + 0.3, width / 2 + 0.05, depth + 2.5 * wheel_radius + 0.3))
+    sim = Simulator(dom, precision=precision, device=device, kt_device=kt_device)
+    mat = sim.load_material(dict(GRC1_MATERIAL))
+    tpls = grc1_templates(sim, mat)
+    pts = hcp_sample_box((0.0, 0.0, depth / 2 + pitch / 2), (length / 2 - pitch, width / 2 - pitch, depth / 2),
+                         pitch)
+    pts = pts[:n_sites]
+    kinds = rng.choice(len(GRC1_TYPES), size=pts.shape[0], p=num)
+    # a 21 mm type-1 clump clears its first lattice shell (12 sites at one pitch)
+    big = np.nonzero(kinds == 0)[0]
+    if big.size:
+        from scipy.spatial import cKDTree
+        keep = np.ones(pts.shape[0], dtype=bool)
+        tree = cKDTree(pts)
+        for i in big:
+            if keep[i]:
+                for j in tree.query_ball_point(pts[i], pitch * 1.05):
+                    if j != i:
+                        keep[j] = False
+        pts, kinds = pts[keep], kinds[keep]
+    for t, (tid, tpl, _, size, k) in enumerate(tpls):
+        sel = pts[kinds == t]
+        if sel.shape[0] == 0:
+            continue
+        ids = np.asarray(sim.add_clumps(tid, sel), dtype=np.int64)
+        q = rng.normal(size=(ids.size, 4))
+        q /= np.linalg.norm(q, axis=1, keepdims=True)
+        sim.store.__dict__["_quat"][ids] = q
+    surface = float(pts[:, 2].max()) + pitch / 2
+    walls = [("plane", (0, 0, 0), (0, 0, 1), mat),
+             ("plane", (-length / 2, 0, 0), (1, 0, 0), mat), ("plane", (length / 2, 0, 0), (-1, 0, 0), mat),
+             ("plane", (0, -width / 2, 0), (0, 1, 0), mat), ("plane", (0, width / 2, 0), (0, -1, 0), mat)]
+    sim.add_analytic(walls, family=255)
+    sim.set_family_fixed(255)
+    wheel_w = min(0.2, 0.6 * width)
+    tris = grousered_wheel(radius=wheel_radius, width=wheel_w)
+    x0 = -length / 2 + wheel_radius + 0.05
+    z0 = surface + wheel_radius - sinkage
+    sim.add_mesh(tris, mat, family=WHEEL_FAMILY, position=(x0, 0.0, z0))
+    sim.set_family_prescribed_lin_vel(WHEEL_FAMILY, omega * wheel_radius * (1.0 - slip), 0.0, 0.0)
+    sim.set_family_prescribed_ang_vel(WHEEL_FAMILY, 0.0, omega, 0.0)
+    sim.set_gravity([0, 0, -G])
+    sim.set_init_time_step(h)
+    sim.set_error_out_velocity(v_err)
+    sim.set_fixed_lookahead(n_max)
+    return sim

@@ -256,3 +256,157 @@ def crater_fixed_point(mu, rho_b, rho_g, D_cm, h_cm, C=0.14):
     for _ in range(200):
         d = k * (h_cm + d) ** (1.0 / 3.0)
     return d
+
+
+# ---------------------------------------------------------------------------
+# configs[2] hopper discharge: run_hopper test 2 (scenarios.py:486-575) --
+# five-sphere WC cylinder clumps (_cylinder_clump :386-398, DRUM_SETUPS WC)
+# in a flat-bottom hopper discharging through a slot.  `scale` multiplies
+# the hopper (width, depth, layer height, orifice) at fixed particle size
+# (x3.68 for ~1 M clumps); `fill` is the reference's
+# fill_scale.  v_err / lookahead reduced as for the crater fixtures.
+# ---------------------------------------------------------------------------
+
+HOPPER_H = 4e-5
+HOPPER_V_ERR = 5.0
+HOPPER_N_MAX = 2
+WC = dict(radius=2.0e-3, length=8.5e-3, density=476.0, E=1e7, nu=0.35, CoR=0.55)
+
+
+def cylinder_clump(gf, radius, length, density, material, n_spheres=5):
+    """Five spheres on the axis; mass / MOI of the ideal cylinder."""
+    vol = math.pi * radius ** 2 * length
+    mass = density * vol
+    ixx = mass * (3 * radius ** 2 + length ** 2) / 12.0
+    izz = 0.5 * mass * radius ** 2
+    span = length - 2 * radius
+    zs = np.linspace(-span / 2.0, span / 2.0, n_spheres)
+    spheres = tuple(gf.ClumpSphere(np.array([0.0, 0.0, z]), radius, material) for z in zs)
+    return gf.ClumpTemplate(mass=mass, moi=np.array([ixx, ixx, izz]), spheres=spheres)
+
+
+def quad(x0, x1, y0, y1, z):
+    """Two facets covering [x0, x1] x [y0, y1] at height z."""
+    p00, p10, p01, p11 = (x0, y0, z), (x1, y0, z), (x0, y1, z), (x1, y1, z)
+    return np.array([(p00, p10, p11), (p00, p11, p01)], dtype=np.float64)
+
+
+def hopper_sim(gf, scale: float = 1.0, fill: float = 1.0, orifice: float = 0.04, mu_i: float = 0.70,
+               cr: float = 0.07, h: float = HOPPER_H, v_err: float = HOPPER_V_ERR, n_max: int = HOPPER_N_MAX,
+               **sim_kw):
+    """Returns (sim, n_clumps, clump_mass, gate_family)."""
+    width, depth_y, height = 0.20 * scale, 0.04 * scale, 0.40 * scale
+    lo = (-0.13 * scale, -0.05 * scale, -0.32 * scale)
+    hi = (0.13 * scale, 0.05 * scale, 0.10 * scale + 0.40 * scale * fill + 0.05)
+    sim = gf.Simulator(gf.Domain(lo, hi), **sim_kw)
+    gate_fam, wall_fam = 20, 255
+    wall = sim.load_material({"E": WC["E"], "nu": 0.3, "CoR": 0.5, "mu": 0.45, "Crr": 0.0})
+    mat = sim.load_material({"E": WC["E"], "nu": WC["nu"], "CoR": WC["CoR"], "mu": mu_i, "Crr": cr})
+    tpl = cylinder_clump(gf, WC["radius"], WC["length"], WC["density"], mat)
+    tid = sim.load_clump_template(tpl)
+    hw, hd, so = width / 2, depth_y / 2, (orifice * scale) / 2
+    floor = np.concatenate([quad(-hw, -so, -hd, hd, 0.0), quad(so, hw, -hd, hd, 0.0)])
+    sim.add_mesh(floor, wall, family=wall_fam)
+    sim.add_mesh(quad(-so, so, -hd, hd, -1e-4), wall, family=gate_fam)
+    for x, nx in ((-hw, 1.0), (hw, -1.0)):
+        sim.add_analytic([("plane", (x, 0, -0.3 * scale), (nx, 0, 0), wall)], family=wall_fam)
+    for y, ny in ((-hd, 1.0), (hd, -1.0)):
+        sim.add_analytic([("plane", (0, y, 0), (0, ny, 0), wall)], family=wall_fam)
+    sim.add_analytic([("plane", (0, 0, -0.30 * scale), (0, 0, 1), wall)], family=wall_fam)
+    sim.set_family_fixed(wall_fam)
+    sim.set_family_fixed(gate_fam)
+    layer_h = 0.36 * scale * fill
+    spacing = WC["length"] * 1.06
+    # the reference offsets the lattice by 1.2 r above the floor
+    # (scenarios.py:540); its upright 8.5 mm rods then start inside the floor
+    # plate, so here the lowest rod end clears it by 1 mm
+    pts = gf.hcp_sample_box((0, 0, layer_h / 2 + WC["length"] / 2 + 1e-3),
+                            (hw - 1.6 * WC["radius"], hd - 1.6 * WC["radius"], layer_h / 2), spacing)
+    sim.add_clumps(tid, pts)
+    sim.set_gravity([0, 0, -G])
+    sim.set_init_time_step(h)
+    sim.set_error_out_velocity(v_err)
+    sim.set_fixed_lookahead(n_max)
+    return sim, int(pts.shape[0]), float(tpl.mass), gate_fam
+
+
+def settle(sim, max_time, calm=0.1, threshold=0.12):
+    """scenarios.py:24-35"""
+    probe = sim.create_inspector("clump_max_absv")
+    t = 0.0
+    while t < max_time:
+        sim.do_dynamics(calm)
+        t += calm
+        if probe.get_value() < threshold:
+            break
+    return t
+
+
+def run_hopper(gf, scale=1.0, fill=0.25, settle_time=0.6, discharge_time=1.0, sample_dt=0.1, **kw) -> dict:
+    """Settle, open the gate (mask it against the grains), sample the
+    discharged mass fraction (clumps below z = -0.05 scale) every sample_dt
+    (scenarios.py:552-575)."""
+    sim, n_clumps, cmass, gate_fam = hopper_sim(gf, scale=scale, fill=fill, **kw)
+    sim.initialize()
+    try:
+        t_settle = settle(sim, settle_time)
+        sim.set_family_mask(gate_fam, 0, False)
+        t, ts, frac = 0.0, [0.0], [0.0]
+        while t < discharge_time - 1e-9:
+            sim.do_dynamics(sample_dt)
+            t += sample_dt
+            z = np.asarray(sim._pos)[:n_clumps, 2]
+            ts.append(t)
+            frac.append(float(np.mean(z < -0.05 * scale)))
+    finally:
+        sim.close()
+    return {"t": np.asarray(ts), "frac": np.asarray(frac), "n_clumps": n_clumps, "settle_t": t_settle}
+
+
+# ---------------------------------------------------------------------------
+# bonded granite block (the breakage model, forces.py:185-291; init_bonds,
+# engine.py:409-427): a 6 x 6 x 4 cubic block of touching 12 mm spheres,
+# bonded (gamma_int 1.01), dropped from 2 cm onto a fixed plane.
+# ---------------------------------------------------------------------------
+
+GRANITE = {"E": 60e9, "nu": 0.25, "CoR": 0.5, "mu": 0.3, "Crr": 0.0, "tension": -9.3e6, "cohesion": 200e6}
+BLOCK_R = 12e-3
+
+
+def bonded_block(gf, drop=0.02, h=1e-6, **sim_kw):
+    sim = gf.Simulator(gf.Domain((-0.2, -0.2, -0.05), (0.2, 0.2, 0.35)), "breakage", **sim_kw)
+    mat = sim.load_material(dict(GRANITE))
+    m = 2650.0 * 4.0 / 3.0 * math.pi * BLOCK_R ** 3
+    tpl = sim.load_clump_template(gf.ClumpTemplate.solid_sphere(BLOCK_R, m, mat))
+    g = (np.arange(6) - 2.5) * 2 * BLOCK_R
+    gz = np.arange(4) * 2 * BLOCK_R + BLOCK_R + drop
+    pts = np.array([(x, y, z) for z in gz for y in g for x in g])
+    sim.add_clumps(tpl, pts)
+    sim.add_analytic([("plane", (0, 0, 0), (0, 0, 1), mat)], family=255)
+    sim.set_family_fixed(255)
+    sim.set_gravity([0, 0, -G])
+    sim.set_init_time_step(h)
+    sim.set_error_out_velocity(5.0)
+    sim.set_fixed_lookahead(4)
+    stats = sim.init_bonds(1.01)
+    return sim, int(pts.shape[0]), stats
+
+
+def run_bonded_block(gf, t_end=0.08, every=0.002, **kw) -> dict:
+    sim, n, stats = bonded_block(gf, **kw)
+    sim.initialize()
+    out = {"t": [0.0], "intact": [int(stats["count"])], "com_z": []}
+    try:
+        out["com_z"].append(float(np.mean(np.asarray(sim._pos)[:n, 2])))
+        t = 0.0
+        while t < t_end - 1e-12:
+            sim.do_dynamics(every)
+            t += every
+            wild = np.asarray(sim._wild)
+            intact = int(np.sum(wild[:, 4] > 0.0)) if wild.size else 0
+            out["t"].append(t)
+            out["intact"].append(intact)
+            out["com_z"].append(float(np.mean(np.asarray(sim._pos)[:n, 2])))
+    finally:
+        sim.close()
+    return {k: np.asarray(v) for k, v in out.items()}

@@ -5,6 +5,8 @@ running the REFERENCE `grainforge` itself, in this build container:
     NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_bulk.py crater_bed
     NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_bulk.py crater_drop 2200
     NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_bulk.py crater_drop 7800
+    NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_bulk.py crater_drop 15000
+    NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_bulk.py hopper
 
 Outputs (tests/golden/):
 * bulk_c1.npz           C1 10k settling box (tests/_bulk.py c1_box), pile
@@ -92,12 +94,23 @@ def crater_drop(rho: float, n_max: int = BK.CRATER_N_MAX):
          n_max=np.int64(n_max), eq7_depth_cm=np.float64(fit), seconds=np.float64(time.time() - t0))
 
 
+def hopper():
+    t0 = time.time()
+    r = BK.run_hopper(gf)
+    print(f"hopper: {time.time() - t0:.0f} s; {r['n_clumps']} clumps, settled {r['settle_t']:.1f} s, "
+          f"discharged {r['frac'][-1]:.3f}", flush=True)
+    save("bulk_hopper", t=r["t"], frac=r["frac"], n_clumps=np.int64(r["n_clumps"]),
+         settle_t=np.float64(r["settle_t"]), seconds=np.float64(time.time() - t0))
+
+
 if __name__ == "__main__":
     what = sys.argv[1]
     if what == "c1":
         c1()
     elif what == "crater_bed":
         crater_bed()
+    elif what == "hopper":
+        hopper()
     elif what == "crater_drop":
         crater_drop(float(sys.argv[2]), *(int(x) for x in sys.argv[3:4]))
     else:

@@ -5,10 +5,19 @@ joined.  One JSON line per config on stdout.
 
   cohesive  configs[3]: the crater bed at 4M spheres with the NVRTC-compiled
             cohesive Hertz-Mindlin user model (models.py)
-  clumps    configs[2]: 1M five-sphere cylinder clumps (5M spheres) settling
-            in a box (the clump owner-reduction path)
+  hopper    configs[2]: the reference's hopper test 2 (five-sphere WC
+            cylinder clumps, scenarios.py:486-575) scaled at fixed particle
+            size to ~1M clumps (5M spheres), settled, gate opened, timed
+            while discharging (tests/_bulk.py hopper_sim)
+  clumps    1M five-sphere cylinder clumps settling in a box
+  rover     configs[4]: the grousered wheel (prescribed 0.8 rad/s) rolling
+            through an 11M-sphere GRC-1-like clump terrain at h = 2e-6
+            (scenes.rover_wheel); the terrain settles first at h = 1e-5
 
-usage: python tools/bench_configs.py [--configs cohesive,clumps] [--steps 100]
+The timed window has no per-kernel events in it; kernel times come from a
+separate profiled window after it.
+
+usage: python tools/bench_configs.py [--configs cohesive,hopper,rover] [--steps 100]
 """
 
 import argparse
@@ -24,19 +33,23 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def timed(sim, steps, warmup):
+def timed(sim, steps, warmup, prof_steps=10):
     import torch
     from paper_2311_04648_b200 import _lib
     sim.do_dynamics(warmup * sim.h)
-    sim._ctx.call("gf_set_profiling", C.c_int(1))
     torch.cuda.synchronize()
     dev0 = sim.scheduler.timing["dyn_force"]
     sim.do_dynamics(steps * sim.h)
     torch.cuda.synchronize()
     dt_ms = (sim.scheduler.timing["dyn_force"] - dev0) * 1e3
+    rr = sim.last_run
+    # per-kernel events only in a separate window after the timed one
+    sim._ctx.call("gf_set_profiling", C.c_int(1))
+    sim.do_dynamics(prof_steps * sim.h)
+    torch.cuda.synchronize()
     times = np.zeros(6)
     sim._ctx.call("gf_kernel_times", _lib.ptr(times))
-    rr = sim.last_run
+    sim._ctx.call("gf_set_profiling", C.c_int(0))
     n_s = int(sim._sph_geom.size)
     steps_prof = max(1.0, times[4])
     return {"n_spheres": n_s, "n_owners": int(sim.store.n_owners), "steps": steps,
@@ -50,10 +63,13 @@ def timed(sim, steps, warmup):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--configs", default="cohesive,clumps")
+    ap.add_argument("--configs", default="cohesive,hopper,rover")
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--settle-steps", type=int, default=6000)
+    ap.add_argument("--hopper-scale", type=float, default=5.85, help="~1M clumps at fill 1")
+    ap.add_argument("--hopper-settle", type=float, default=0.6)
+    ap.add_argument("--rover-spheres", type=int, default=11_000_000)
     args = ap.parse_args()
     from paper_2311_04648_b200 import models, scenes
     for name in args.configs.split(","):
@@ -66,6 +82,24 @@ def main():
             sim.do_dynamics(args.settle_steps * sim.h)
             scenes.release_balls(sim)
             rec = {"config": "configs[3]: crater bed, 4M spheres, cohesive Hertz-Mindlin via NVRTC (coh 1e4 Pa)"}
+        elif name == "hopper":
+            sys.path.insert(0, os.path.join(ROOT, "tests"))
+            import _bulk as BK
+            import paper_2311_04648_b200 as gf
+            sim, n_clumps, _, gate = BK.hopper_sim(gf, scale=args.hopper_scale, fill=1.0, precision="f32")
+            sim.initialize()
+            BK.settle(sim, args.hopper_settle)
+            sim.set_family_mask(gate, 0, False)
+            sim.do_dynamics(0.05)   # the discharge under way
+            rec = {"config": f"configs[2]: hopper test 2 scaled x{args.hopper_scale} at fixed particle size, "
+                             f"{n_clumps} five-sphere WC cylinder clumps, discharging through the orifice"}
+        elif name == "rover":
+            sim = scenes.rover_wheel(args.rover_spheres, h=1e-5)
+            sim.initialize()
+            sim.do_dynamics(args.settle_steps * sim.h)   # terrain settles (untimed input preparation)
+            sim.set_init_time_step(2e-6)
+            rec = {"config": f"configs[4]: grousered wheel (0.8 rad/s, 20% slip) on a {args.rover_spheres}-sphere "
+                             "GRC-1-like clump terrain, h = 2e-6"}
         elif name == "clumps":
             sim = scenes.clump_bed(1_000_000)
             sim.initialize()
