@@ -323,6 +323,11 @@ int gf_integrate_and_refresh(gf_ctx *ctx, double h, const double *g3, int64_t n,
                              int64_t n_geom, const float *geom_params, const int64_t *geom_owner,
                              double *sph_centers, int64_t *bad, int64_t *oob);
 
+/* an output frame's per-sphere columns in one pass on the device
+ * (io.write_sphere_csv, io.py:132-166): out (n_s, 8) float64 per device
+ * sphere slot = centre xyz, |v| of its owner, owner family, owner v xyz */
+int gf_sphere_frame(gf_ctx *ctx, double *out);
+
 /* per-kernel device timing of subsequent gf_run calls (CUDA events on the dT
  * stream); out6 = cumulative ms of {contact phase, k_heavy, k_integrate, kT},
  * the number of profiled steps, then the ms of the fused sphere-sphere kernel

@@ -61,7 +61,7 @@ EXPORTS = (
     "gf_set_decomposition", "gf_halo_record_bytes", "gf_stream", "gf_pack_state", "gf_unpack_state",
     "gf_pack_forces", "gf_add_forces", "gf_trip_word", "gf_sync",
     "gf_contact_forces", "gf_eval_core", "gf_reduce", "gf_integrate_and_refresh", "gf_apply_active_boxes",
-    "gf_set_persistent_wildcard", "gf_read_owners", "gf_clump_max_absv",
+    "gf_set_persistent_wildcard", "gf_read_owners", "gf_clump_max_absv", "gf_sphere_frame",
 )
 
 _lib = None

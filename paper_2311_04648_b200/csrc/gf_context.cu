@@ -511,6 +511,7 @@ gf_ctx *gf_create(int device, int kt_device, uint32_t flags) {
     delete ctx;
     return nullptr;
   }
+  cudaMemsetAsync(c->status.p, 0, sizeof(Status), c->s_dt);   // pad words read by read_status (initcheck)
   reset_status(c, c->s_dt);
   cudaStreamSynchronize(c->s_dt);
   return ctx;

@@ -276,6 +276,25 @@ __global__ void k_ref_centres(int64_t n_s, const int64_t *sph_geom, const float 
   }
 }
 
+
+// one output frame's per-sphere columns (io.write_sphere_csv, io.py:132-166):
+// centre xyz, |v| of the owner (fp64, the reference's summation order),
+// family, owner v xyz; device sphere slot order
+__global__ void k_sphere_frame(Spheres sph, Owners own, int f32, double *out) {
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < sph.n; k += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t o = sph.owner[k];
+    const double4 c = sph.center[k];
+    double v[3];
+    for (int a = 0; a < 3; ++a)
+      v[a] = f32 ? double(reinterpret_cast<const float *>(own.lin_vel)[4 * size_t(o) + a])
+                 : reinterpret_cast<const double *>(own.lin_vel)[4 * size_t(o) + a];
+    double *w = out + 8 * k;
+    w[0] = c.x; w[1] = c.y; w[2] = c.z;
+    w[3] = sqrt((v[0] * v[0] + v[1] * v[1]) + v[2] * v[2]);
+    w[4] = double(meta_family(own.meta[o]));
+    w[5] = v[0]; w[6] = v[1]; w[7] = v[2];
+  }
+}
 }  // namespace
 }  // namespace gf
 
@@ -511,6 +530,19 @@ int gf_integrate_and_refresh(gf_ctx *ctx, double h, const double *g3, int64_t n,
   if (bad) *bad = hf[0] == ~0ull ? -1 : int64_t(hf[0]);
   if (oob) *oob = hf[1] == ~0ull ? -1 : int64_t(hf[1]);
   return rc;
+}
+
+int gf_sphere_frame(gf_ctx *ctx, double *out) {
+  if (!ctx) return -1;
+  Ctx *c = &ctx->c;
+  if (cudaSetDevice(c->device) != cudaSuccess) return -1;
+  if (!c->n_sph) return 0;
+  Stage S(c);
+  double *d = S.alloc<double>(8 * size_t(c->n_sph));
+  if (S.failed) return S.finish();
+  k_sphere_frame<<<grid_of(c->n_sph, 256), 256, 0, S.s>>>(spheres_view(c), owners_view(c), c->f32_state ? 1 : 0, d);
+  S.out(out, d, 8 * size_t(c->n_sph));
+  return S.finish();
 }
 
 }  // extern "C"

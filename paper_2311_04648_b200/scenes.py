@@ -397,8 +397,8 @@ def grc1_templates(sim: Simulator, material: int, density: float = 2500.0, scale
 
 def rover_wheel(n_spheres: int = 11_000_000, *, seed: int = 3, h: float = 2e-6, v_err: float = 3.0,
                 n_max: int = 8, precision: str = "f32", device: int = 0, omega: float = 0.8,
-                slip: float = 0.2, wheel_radius: float = 0.25, sinkage: float = 0.02,
-                aspect: float = 4.0, kt_device=None) -> Simulator:
+                slip: float = 0.2, wheel_radius: float = 0.25, sinkage: float = 0.005,
+                aspect: float = 4.0, plunge: float = 0.0, kt_device=None) -> Simulator:
     """A GRC-1-like terrain of about n_spheres component spheres in a walled
     trough (length = aspect x width) with the grousered wheel resting
     `sinkage` into its surface at one end, spinning at `omega` about its axle
@@ -426,20 +426,27 @@ def rover_wheel(n_spheres: int = 11_000_000, *, seed: int = 3, h: float = 2e-6, 
     sim = Simulator(dom, precision=precision, device=device, kt_device=kt_device)
     mat = sim.load_material(dict(GRC1_MATERIAL))
     tpls = grc1_templates(sim, mat)
-    pts = hcp_sample_box((0.0, 0.0, depth / 2 + pitch / 2), (length / 2 - pitch, width / 2 - pitch, depth / 2),
-                         pitch)
+    lift = GRC1_TYPES[0][0] / 2 + 1e-3     # the lowest (and outermost) sites clear the walls for any type
+    pts = hcp_sample_box((0.0, 0.0, depth / 2 + lift), (length / 2 - lift, width / 2 - lift, depth / 2), pitch)
     pts = pts[:n_sites]
     kinds = rng.choice(len(GRC1_TYPES), size=pts.shape[0], p=num)
-    # a 21 mm type-1 clump clears its first lattice shell (12 sites at one pitch)
+    # reach of each type from its centre (any orientation)
+    reach = np.array([(k - 1) * 0.5 * (t[0] - 2 * t[1]) / max(k - 1, 1) + t[1]
+                      for t, k in zip(GRC1_TYPES, k_of)])
+    # a 21 mm type-1 clump clears every site it could touch: the others
+    # within its reach + the largest other reach, other type-1 within twice
+    # its reach
     big = np.nonzero(kinds == 0)[0]
     if big.size:
         from scipy.spatial import cKDTree
         keep = np.ones(pts.shape[0], dtype=bool)
         tree = cKDTree(pts)
+        r_other = reach[0] + reach[1:].max() + 1e-4
+        r_big = 2.0 * reach[0] + 1e-4
         for i in big:
             if keep[i]:
-                for j in tree.query_ball_point(pts[i], pitch * 1.05):
-                    if j != i:
+                for j in tree.query_ball_point(pts[i], max(r_other, r_big)):
+                    if j != i and (kinds[j] == 0 or np.linalg.norm(pts[j] - pts[i]) < r_other):
                         keep[j] = False
         pts, kinds = pts[keep], kinds[keep]
     for t, (tid, tpl, _, size, k) in enumerate(tpls):
@@ -450,21 +457,96 @@ def rover_wheel(n_spheres: int = 11_000_000, *, seed: int = 3, h: float = 2e-6, 
         q = rng.normal(size=(ids.size, 4))
         q /= np.linalg.norm(q, axis=1, keepdims=True)
         sim.store.__dict__["_quat"][ids] = q
-    surface = float(pts[:, 2].max()) + pitch / 2
+    surface = float(np.max(pts[:, 2] + reach[kinds]))   # the highest grain's top
     walls = [("plane", (0, 0, 0), (0, 0, 1), mat),
              ("plane", (-length / 2, 0, 0), (1, 0, 0), mat), ("plane", (length / 2, 0, 0), (-1, 0, 0), mat),
              ("plane", (0, -width / 2, 0), (0, 1, 0), mat), ("plane", (0, width / 2, 0), (0, -1, 0), mat)]
     sim.add_analytic(walls, family=255)
     sim.set_family_fixed(255)
     wheel_w = min(0.2, 0.6 * width)
-    tris = grousered_wheel(radius=wheel_radius, width=wheel_w)
-    x0 = -length / 2 + wheel_radius + 0.05
-    z0 = surface + wheel_radius - sinkage
+    grouser = 0.08 * wheel_radius
+    tris = grousered_wheel(radius=wheel_radius, width=wheel_w, grouser_h=grouser)
+    x0 = -length / 2 + wheel_radius + grouser + 0.01
+    # the terrain top under the wheel's lowest grouser (the grain reaching
+    # highest within a grain size of the axle's vertical plane)
+    foot = (np.abs(pts[:, 0] - x0) < 0.012) & (np.abs(pts[:, 1]) < wheel_w / 2)
+    top_under = float(np.max(pts[foot, 2] + reach[kinds[foot]])) if foot.any() else surface
+    z0 = top_under + wheel_radius + grouser - sinkage   # the lowest grouser tip `sinkage` into it
     sim.add_mesh(tris, mat, family=WHEEL_FAMILY, position=(x0, 0.0, z0))
-    sim.set_family_prescribed_lin_vel(WHEEL_FAMILY, omega * wheel_radius * (1.0 - slip), 0.0, 0.0)
+    sim.set_family_prescribed_lin_vel(WHEEL_FAMILY, omega * wheel_radius * (1.0 - slip), 0.0, -plunge)
     sim.set_family_prescribed_ang_vel(WHEEL_FAMILY, 0.0, omega, 0.0)
     sim.set_gravity([0, 0, -G])
     sim.set_init_time_step(h)
     sim.set_error_out_velocity(v_err)
     sim.set_fixed_lookahead(n_max)
     return sim
+
+
+# ---------------------------------------------------------------------------
+# the paper's mixer timing scene (scenarios.py:752-838, `grainforge bench
+# mixer`, cli.py:183-209): a cylindrical chamber, a rotating two-paddle blade
+# mesh, granular fill of 1-, 3- or 6-sphere clumps above the blades.
+# ---------------------------------------------------------------------------
+
+def paddle_blades(nu: int = 6, nv: int = 1) -> np.ndarray:
+    """Two crossed vertical paddles spanning x / y in [-0.9, 0.9], z in
+    [-0.5, 0.5] (unit box), each an nu x nv quad grid (2 nu nv facets)."""
+    tris = []
+    for blade in (0, 1):
+        for i in range(nu):
+            for j in range(nv):
+                u0, u1 = -0.9 + 1.8 * i / nu, -0.9 + 1.8 * (i + 1) / nu
+                z0, z1 = -0.5 + j / nv, -0.5 + (j + 1) / nv
+                pt = (lambda u, z: (u, 0.0, z)) if blade == 0 else (lambda u, z: (0.0, u, z))
+                p00, p10, p01, p11 = pt(u0, z0), pt(u1, z0), pt(u0, z1), pt(u1, z1)
+                tris.append((p00, p10, p11))
+                tris.append((p00, p11, p01))
+    return np.asarray(tris, dtype=np.float64)
+
+
+def mixer(target_spheres: int, *, clump: str = "3sph", young: float = 1e7, omega: float = 2.0 * math.pi,
+          precision: str = "f32", device: int = 0, h: float | None = None) -> tuple:
+    """build_mixer_sim at the grain size that puts ~target_spheres in the
+    fill (run_mixer_timing's sizing rule).  Returns (sim, meta)."""
+    from .core import ClumpSphere
+    from .engine import hcp_sample_cylinder
+    per = {"spheres": 1, "3sph": 3, "6sph": 6}[clump]
+    chamber_vol = math.pi * 0.25 * (1.0 / 3.0)
+    n_clumps = target_spheres / per
+    r = (chamber_vol * 0.42 / (n_clumps * per * 4.19)) ** (1 / 3)
+    world = 1.0
+    chamber_h = world / 3.0
+    sim = Simulator(Domain.cube(world * 1.02), precision=precision, device=device)
+    mat_mixer = sim.load_material({"E": young, "nu": 0.3, "CoR": 0.6, "mu": 0.5, "Crr": 0.0})
+    mat_gran = sim.load_material({"E": young, "nu": 0.3, "CoR": 0.6, "mu": 0.2, "Crr": 0.0})
+    sim.set_material_pair("mu", mat_mixer, mat_gran, 0.5)
+    wall_fam, mixer_fam = 255, 10
+    sim.add_analytic([("cylinder", (0, 0, 0), (0, 0, 1), world / 2, -1.0, mat_mixer),
+                      ("plane", (0, 0, -world / 2), (0, 0, 1), mat_mixer),
+                      ("plane", (0, 0, world / 2), (0, 0, -1), mat_mixer)], family=wall_fam)
+    sim.set_family_fixed(wall_fam)
+    m_id = sim.add_mesh(paddle_blades(), mat_mixer, family=mixer_fam, position=(0, 0, -world / 2 + chamber_h / 2))
+    sim.store.scale_mesh(m_id, (world / 2 * 0.92, world / 2 * 0.92, chamber_h * 0.96))
+    sim.set_family_prescribed_ang_vel(mixer_fam, "0", "0", f"{omega!r}")
+    if clump == "spheres":
+        spheres = (ClumpSphere(np.zeros(3), r, mat_gran),)
+    elif clump == "3sph":
+        spheres = tuple(ClumpSphere(np.array([dx, 0.0, 0.0]), r, mat_gran) for dx in (-r, 0.0, r))
+    else:
+        spheres = tuple(ClumpSphere(np.array(off) * r, r, mat_gran)
+                        for off in ((-1, 0, 0), (1, 0, 0), (0, -1, 0), (0, 1, 0), (0, 0, -1), (0, 0, 1)))
+    density = 2.6e3
+    mass = density * sum(4 / 3 * math.pi * s.radius ** 3 for s in spheres)
+    span = max(np.linalg.norm(s.offset) + s.radius for s in spheres)
+    tpl = ClumpTemplate(mass=mass, moi=np.array([0.4 * mass * span ** 2] * 3), spheres=spheres)
+    tid = sim.load_clump_template(tpl)
+    fill_bottom = -world / 2 + chamber_h
+    pts = hcp_sample_cylinder((0, 0, fill_bottom + chamber_h / 2), world / 2 - 2.2 * span, chamber_h / 2 - span,
+                              2.0 * span * 1.05)
+    sim.add_clumps(tid, pts)
+    if h is None:
+        h = 0.3 / math.sqrt(2.0 * young * r * 0.02 / mass)
+    sim.set_gravity([0, 0, -G])
+    sim.set_init_time_step(h)
+    sim.set_error_out_velocity(25.0)
+    return sim, {"n_clumps": int(pts.shape[0]), "n_spheres": int(pts.shape[0]) * len(spheres), "h": h, "r": r}

@@ -24,8 +24,10 @@ pytestmark = pytest.mark.gpu
 
 
 def small_rover(precision="f64"):
-    sim = scenes.rover_wheel(6_000, precision=precision, h=2e-6, v_err=3.0, n_max=4, sinkage=0.004,
-                             wheel_radius=0.05, aspect=2.0)
+    # the wheel plunges at 1 m/s while it spins, so its grousers and rim
+    # reach the grains under it within the window
+    sim = scenes.rover_wheel(6_000, precision=precision, h=1e-5, v_err=3.0, n_max=4, sinkage=0.0,
+                             wheel_radius=0.05, aspect=2.0, plunge=1.0)
     return sim
 
 
@@ -33,7 +35,7 @@ def test_rover_wheel_sync_trajectory_matches_oracle():
     sim = small_rover()
     scene = scenes.oracle_scene(sim)
     margin = O.margin_for(float(scene["v_err"]), float(scene["h"]), 1)
-    steps = 40
+    steps = 400
     ref = O.OracleStepper(scene, margin, period=1, lag=0)
     for _ in range(steps):
         ref.step_once()
@@ -55,7 +57,7 @@ def test_rover_wheel_f32_within_tolerance():
     scene["lin_vel"] = scene["lin_vel"].astype(np.float32).astype(np.float64)
     scene["ang_vel"] = scene["ang_vel"].astype(np.float32).astype(np.float64)
     margin = O.margin_for(float(scene["v_err"]), float(scene["h"]), 1)
-    steps = 20
+    steps = 400
     ref = O.OracleStepper(scene, margin, period=1, lag=0)
     for _ in range(steps):
         ref.step_once()
@@ -73,11 +75,11 @@ def test_wheel_contact_force_readback():
     """Through the Simulator: after a do_dynamics call the wheel owner's
     accumulated force (acc_force, read back for passive owners on the
     reported step) balances the grains' wall-contact forces."""
-    sim = scenes.rover_wheel(20_000, precision="f64", h=2e-6, v_err=3.0, n_max=4, sinkage=0.006,
-                             wheel_radius=0.06, aspect=2.0)
+    sim = scenes.rover_wheel(20_000, precision="f64", h=1e-5, v_err=3.0, n_max=4, sinkage=0.0,
+                             wheel_radius=0.06, aspect=2.0, plunge=1.0)
     sim.initialize()
     with sim:
-        sim.do_dynamics(50 * sim.h)
+        sim.do_dynamics(400 * sim.h)
         s = sim.store
         n = s.n_owners
         wheel = [o for o in range(n) if s.owner_family[o] == scenes.WHEEL_FAMILY][0]
