@@ -83,6 +83,7 @@ struct KtScratch {
   double cand_skin = -1.0;
   int64_t tmp_cap = 0;
   DBuf tri_cursor;   // uint32 per cell
+  DBuf gaps;         // long runs of segment starts filled by k_fill_gaps
   DBuf counts;       // uint64[3*n_s+1] per sphere SS / ST / SA counts
   DBuf offsets;      // uint64? uint32[3*n_s+1] exclusive scan
   DBuf cub_tmp;
@@ -188,6 +189,7 @@ struct Ctx {
   int persist_col = -1;      // wildcard column whose > 0 rows persist across detections (bonds), or -1
   int64_t persisted = 0;     // rows re-appended by that rule so far
   int n_sm = 148;             // multiprocessors of the device (grid sizing)
+  int ss_blocked = 2;        // fused kernel: contiguous entry range per CTA (1), grid-stride (0), auto by size (2)
   int ss_pf = 1;             // fused kernel read-ahead / prefetch (GF_SS_PF=0: off)
   int ss_red = 1;            // fused sphere-sphere kernel: staged fixed-point rows (GF_SS_RED=0: per-word REDs)
   int ss_split = 0;          // throughput build: split narrow/force sphere-sphere kernels (GF_SS_SPLIT=1)

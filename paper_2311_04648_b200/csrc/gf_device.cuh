@@ -70,6 +70,7 @@ struct DtView {
   Status *st;
   int acc_all;          // throughput build: also accumulate onto passive owners (write_acc step)
   int pf;               // fused sphere-sphere kernel: list read-ahead + L2 prefetch of the force records
+  int blocked;          // fused sphere-sphere kernel: one contiguous entry range per CTA
 };
 
 // An owner whose accumulated force never feeds its motion: fixed, or every

@@ -296,21 +296,24 @@ __device__ __forceinline__ void tri_cells(const Grid &g, const double *T, double
   }
 }
 
+// one CTA per triangle, its threads over the cells of the triangle's
+// margin-enlarged box (a wheel's side-disk facet spans thousands of cells)
 template <bool FILL>
-__global__ void k_tri_register(int64_t n_t, const double *tri, const Grid *gp, double margin,
-                               uint32_t *cnt, uint32_t *cursor, uint32_t *entries) {
-  int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (t >= n_t) return;
-  Grid g = *gp;
-  int r[6];
-  tri_cells(g, tri + 9 * t, margin, r);
-  for (int iz = r[4]; iz <= r[5]; ++iz)
-    for (int iy = r[2]; iy <= r[3]; ++iy)
-      for (int ix = r[0]; ix <= r[1]; ++ix) {
-        int64_t b = (int64_t(iz) * g.nc[1] + iy) * g.nc[0] + ix;
-        if (FILL) entries[atomicAdd(&cursor[b], 1u)] = uint32_t(t);
-        else atomicAdd(&cnt[b], 1u);
-      }
+__global__ void __launch_bounds__(128) k_tri_register(int64_t n_t, const double *tri, const Grid *gp, double margin,
+                                                      uint32_t *cnt, uint32_t *cursor, uint32_t *entries) {
+  const Grid g = *gp;
+  for (int64_t t = blockIdx.x; t < n_t; t += gridDim.x) {
+    int r[6];
+    tri_cells(g, tri + 9 * t, margin, r);
+    const long long nx = r[1] - r[0] + 1, ny = r[3] - r[2] + 1, nz = r[5] - r[4] + 1;
+    const long long nc = nx * ny * nz;
+    for (long long j = threadIdx.x; j < nc; j += blockDim.x) {
+      const int ix = r[0] + int(j % nx), iy = r[2] + int((j / nx) % ny), iz = r[4] + int(j / (nx * ny));
+      const int64_t b = (int64_t(iz) * g.nc[1] + iy) * g.nc[0] + ix;
+      if (FILL) entries[atomicAdd(&cursor[b], 1u)] = uint32_t(t);
+      else atomicAdd(&cnt[b], 1u);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -777,15 +780,49 @@ __global__ void __launch_bounds__(128) k_cand_big(KtView v, const uint32_t *bigs
 
 // candidates sorted by a -> the (a, b) list and each sphere's segment start
 // (the spheres in (previous entry's a, this entry's a] start here)
+// Segment-start fills over runs of spheres without entries: a thread fills
+// short runs itself and hands runs longer than kGapInline to k_fill_gaps (one
+// CTA per run), so a sparse list (a settling terrain, a dilute scene) does not
+// leave single threads looping over millions of spheres.
+constexpr long long kGapInline = 32;
+struct GapList {
+  ulonglong2 *run;              // (first sphere | last sphere << 32 folded in .x / .y), value in val
+  unsigned long long *val;
+  unsigned long long *n;
+  unsigned long long cap;
+};
+__device__ __forceinline__ void seg_fill(unsigned long long *seg, long long lo, long long hi, unsigned long long val,
+                                         const GapList &gl) {
+  if (hi - lo + 1 <= kGapInline || gl.n == nullptr) {
+    for (long long sp = lo; sp <= hi; ++sp) seg[sp] = val;
+    return;
+  }
+  const unsigned long long i = atomicAdd(gl.n, 1ull);
+  if (i < gl.cap) {
+    gl.run[i] = make_ulonglong2((unsigned long long)lo, (unsigned long long)hi);
+    gl.val[i] = val;
+  } else {   // cannot happen with cap >= n_sph / kGapInline + 2; stay correct anyway
+    for (long long sp = lo; sp <= hi; ++sp) seg[sp] = val;
+  }
+}
+
+__global__ void k_fill_gaps(unsigned long long *seg, GapList gl) {
+  const unsigned long long n = min(*gl.n, gl.cap);
+  for (unsigned long long g = blockIdx.x; g < n; g += gridDim.x) {
+    const ulonglong2 r = gl.run[g];
+    const unsigned long long v = gl.val[g];
+    for (unsigned long long sp = r.x + threadIdx.x; sp <= r.y; sp += blockDim.x) seg[sp] = v;
+  }
+}
+
 __global__ void k_cand_unpack(int64_t total, int64_t n_sph, const uint32_t *ka, const uint32_t *kb, uint2 *cand,
-                              unsigned long long *seg) {
+                              unsigned long long *seg, GapList gl) {
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
     const int64_t a = ka[e];
     cand[e] = make_uint2(uint32_t(a), kb[e]);
     const int64_t ap = e > 0 ? int64_t(ka[e - 1]) : -1;
-    for (int64_t sp = ap + 1; sp <= a; ++sp) seg[sp] = (unsigned long long)e;
-    if (e == total - 1)
-      for (int64_t sp = a + 1; sp <= n_sph; ++sp) seg[sp] = (unsigned long long)total;
+    if (ap + 1 <= a) seg_fill(seg, ap + 1, a, (unsigned long long)e, gl);
+    if (e == total - 1 && a + 1 <= n_sph) seg_fill(seg, a + 1, n_sph, (unsigned long long)total, gl);
   }
 }
 
@@ -860,7 +897,7 @@ __global__ void __launch_bounds__(kFcBlock) k_compact(KtView v, const uint2 *can
                                                       const uint32_t *bits, const unsigned long long *blk_pre,
                                                       const uint32_t *obits, const unsigned long long *oblk_pre,
                                                       uint2 *out_ids, unsigned long long *seg, uint32_t *old_pos,
-                                                      unsigned long long ss_cap) {
+                                                      unsigned long long ss_cap, GapList gl) {
   // the filter block's kFcSpan candidates: kFcSpan / 32 bitmask words; every
   // global load is issued up front so its latency overlaps the word scan
   constexpr int kW = kFcSpan / 32;
@@ -913,7 +950,7 @@ __global__ void __launch_bounds__(kFcBlock) k_compact(KtView v, const uint2 *can
     const unsigned long long p = pre + s_w[wl] + __popc(word[q] & below);
     const long long a = (long long)it[q].x;
     const long long ap = e == 0 ? -1 : (long long)(lane ? prev_x : ap_g[q]);
-    for (long long sp = ap + 1; sp <= a; ++sp) seg[sp] = p;
+    if (ap + 1 <= a) seg_fill(seg, ap + 1, a, p, gl);
     const bool hit = (word[q] >> lane) & 1u;
     if (hit && p < ss_cap) {   // beyond: the fill phase grows the array and recounts
       out_ids[p] = it[q];
@@ -922,7 +959,7 @@ __global__ void __launch_bounds__(kFcBlock) k_compact(KtView v, const uint2 *can
                                               : 0xFFFFFFFFu;
     }
     if (e == n_cand - 1)   // the last candidate closes the block
-      for (long long sp = a + 1; sp <= v.sph.n; ++sp) seg[sp] = p + (hit ? 1 : 0);
+      if (a + 1 <= v.sph.n) seg_fill(seg, a + 1, v.sph.n, p + (hit ? 1 : 0), gl);
   }
 }
 
@@ -1256,7 +1293,7 @@ int kt_begin(Ctx *c, double margin, cudaStream_t s) {
         ensure(c, k.tri_cursor, sizeof(uint32_t) * (kMaxCells + 1), s))
       return -1;
     k_fill_u32<<<592, 256, 0, s>>>(gp, k.tri_cnt.as<uint32_t>(), 0u, 1);
-    k_tri_register<false><<<grid_for(nt), kBlock, 0, s>>>(nt, k.tri_world.as<double>(), gp, margin,
+    k_tri_register<false><<<unsigned(std::min<int64_t>(nt, int64_t(c->n_sm) * 16)), 128, 0, s>>>(nt, k.tri_world.as<double>(), gp, margin,
                                                          k.tri_cnt.as<uint32_t>(), nullptr, nullptr);
     size_t tmp = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tmp, k.tri_cnt.as<uint32_t>(), k.tri_start.as<uint32_t>(),
@@ -1271,11 +1308,24 @@ int kt_begin(Ctx *c, double margin, cudaStream_t s) {
     if (ensure(c, k.tri_entries, sizeof(uint32_t) * (h_total + 1), s)) return -1;
     GF_CHECK(c, cudaMemcpyAsync(k.tri_cursor.p, k.tri_start.p, sizeof(uint32_t) * (kMaxCells + 1),
                                 cudaMemcpyDeviceToDevice, s));
-    k_tri_register<true><<<grid_for(nt), kBlock, 0, s>>>(nt, k.tri_world.as<double>(), gp, margin,
+    k_tri_register<true><<<unsigned(std::min<int64_t>(nt, int64_t(c->n_sm) * 16)), 128, 0, s>>>(nt, k.tri_world.as<double>(), gp, margin,
                                                         nullptr, k.tri_cursor.as<uint32_t>(),
                                                         k.tri_entries.as<uint32_t>());
   }
   GF_CHECK(c, cudaGetLastError());
+  return 0;
+}
+
+// the long-run list of seg_fill (KtScratch::gaps), its counter cleared on s
+static int gap_list(Ctx *c, GapList &gl, cudaStream_t s) {
+  KtScratch &k = c->kt;
+  const unsigned long long cap = (unsigned long long)(c->n_sph / kGapInline) + 4;
+  if (ensure(c, k.gaps, (sizeof(ulonglong2) + sizeof(unsigned long long)) * cap + 16, s)) return -1;
+  gl.run = k.gaps.as<ulonglong2>();
+  gl.val = reinterpret_cast<unsigned long long *>(gl.run + cap);
+  gl.n = gl.val + cap;
+  gl.cap = cap;
+  GF_CHECK(c, cudaMemsetAsync(gl.n, 0, sizeof(unsigned long long), s));
   return 0;
 }
 
@@ -1394,8 +1444,11 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
     GF_CHECK(c, cub::DeviceRadixSort::SortPairs(k.cub_tmp.p, tmp, dk, dv, int(total), 0, bits, s));
     if (dk.Current() == ka2) std::swap(k.cand, k.cand_tmp);   // sorted halves now in cand_tmp
     const uint32_t *sa = k.cand_tmp.as<uint32_t>(), *sb = sa + cap;
+    GapList gl;
+    if (gap_list(c, gl, s)) return -1;
     k_cand_unpack<<<unsigned(std::min<int64_t>((total + 255) / 256, int64_t(c->n_sm) * 16)), 256, 0, s>>>(
-        total, n, sa, sb, k.cand.as<uint2>(), k.cand_seg.as<unsigned long long>());
+        total, n, sa, sb, k.cand.as<uint2>(), k.cand_seg.as<unsigned long long>(), gl);
+    k_fill_gaps<<<unsigned(c->n_sm) * 4, 256, 0, s>>>(k.cand_seg.as<unsigned long long>(), gl);
     if (ensure(c, k.sa_cnt, 4 * (n + 1), s)) return -1;   // the long-segment list (scratch here)
     GF_CHECK(c, cudaMemsetAsync(big_n, 0, 8, s));
     k_sort_seg_short<<<grid_for(n), kBlock, 0, s>>>(n, k.cand_seg.as<unsigned long long>(), k.cand.as<uint2>(),
@@ -1517,10 +1570,13 @@ int kt_count(Ctx *c, cudaStream_t s, bool force_rebuild) {
     if (ensure(c, k.cub_tmp, tb + 16, s, false)) return -1;
     GF_CHECK(c, cub::DeviceScan::ExclusiveSum(k.cub_tmp.p, tb, k.fcnt.as<uint32_t>(),
                                               k.fpre[cur].as<unsigned long long>(), int(nblk + 1), s));
+    GapList gl;
+    if (gap_list(c, gl, s)) return -1;
     k_compact<<<unsigned(nblk), kFcBlock, 0, s>>>(
         v, k.cand.as<uint2>(), k.n_cand, k.fbits[cur].as<uint32_t>(), k.fpre[cur].as<unsigned long long>(),
         rows_ok ? k.fbits[prev].as<uint32_t>() : nullptr, rows_ok ? k.fpre[prev].as<unsigned long long>() : nullptr,
-        out.ids.as<uint2>(), oseg, out.old_pos.as<uint32_t>(), (unsigned long long)(out.cap - k.tmp_cap - 1));
+        out.ids.as<uint2>(), oseg, out.old_pos.as<uint32_t>(), (unsigned long long)(out.cap - k.tmp_cap - 1), gl);
+    k_fill_gaps<<<unsigned(c->n_sm) * 4, 256, 0, s>>>(oseg, gl);
   } else {
     k_zero_u64<<<grid_for(n + 1), kBlock, 0, s>>>(oseg, n + 1);   // oseg: the dT device's array
     GF_CHECK(c, cudaMemsetAsync(k.fpre[cur].p, 0, sizeof(unsigned long long), s));

@@ -410,3 +410,47 @@ def run_bonded_block(gf, t_end=0.08, every=0.002, **kw) -> dict:
     finally:
         sim.close()
     return {k: np.asarray(v) for k, v in out.items()}
+
+
+# ---------------------------------------------------------------------------
+# a stretched bond (bond persistence, engine.py:639-662): two touching soft
+# spheres bonded with an unbreakable tension, launched apart; they oscillate
+# with an amplitude (~2 mm) larger than the detection margin, so the
+# detection loses the pair every half period and the persistence rule must
+# keep re-appending the intact bond.
+# ---------------------------------------------------------------------------
+
+SOFT_BOND = {"E": 1e5, "nu": 0.25, "CoR": 0.5, "mu": 0.3, "Crr": 0.0, "tension": -1e7, "cohesion": 1e7}
+
+
+def stretched_bond(gf, t_end=0.06, every=0.002, v0=0.5, h=1e-5, **sim_kw):
+    sim = gf.Simulator(gf.Domain((-0.1, -0.1, -0.1), (0.1, 0.1, 0.1)), "breakage", **sim_kw)
+    mat = sim.load_material(dict(SOFT_BOND))
+    r = BLOCK_R
+    m = 2650.0 * 4.0 / 3.0 * math.pi * r ** 3
+    tpl = sim.load_clump_template(gf.ClumpTemplate.solid_sphere(r, m, mat))
+    a, b = sim.add_clumps(tpl, [[-r, 0.0, 0.0], [r, 0.0, 0.0]])
+    sim.track(a).set_vel([-v0, 0.0, 0.0])
+    sim.track(b).set_vel([v0, 0.0, 0.0])
+    sim.set_init_time_step(h)
+    sim.set_error_out_velocity(5.0)
+    sim.set_fixed_lookahead(4)
+    stats = sim.init_bonds(1.01)
+    sim.initialize()
+    out = {"t": [], "gap": [], "intact": []}
+    try:
+        t = 0.0
+        while t < t_end - 1e-12:
+            sim.do_dynamics(every)
+            t += every
+            p = np.asarray(sim._pos)
+            wild = np.asarray(sim._wild)
+            out["t"].append(t)
+            out["gap"].append(float(p[b, 0] - p[a, 0] - 2 * r))
+            out["intact"].append(int(np.sum(wild[:, 4] > 0.0)) if wild.size else 0)
+    finally:
+        sim.close()
+    res = {k: np.asarray(v) for k, v in out.items()}
+    res["bonds"] = int(stats["count"])
+    res["margin"] = float(sim._current_margin()) if hasattr(sim, "_current_margin") else 0.0
+    return res

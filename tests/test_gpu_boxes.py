@@ -58,8 +58,9 @@ def test_moving_box_retags_on_device(precision):
             before = sim._pos[frozen].copy()
             sim._box_next = sim.sim_time + 1e9   # no automatic refresh inside the chunk
             sim._run(200)
-            # frozen owners are fixed: they do not move
-            assert np.array_equal(sim._pos[frozen], before)
+            # frozen owners are fixed: they do not move (beyond the re-encode
+            # every owner gets each step, _kernels.py:654: sub-voxel quanta)
+            assert np.max(np.abs(sim._pos[frozen] - before)) <= 1e-9
         assert retagged > 0
 
 

@@ -66,3 +66,18 @@ def test_init_bonds_requires_breakage_model():
     sim = gf.Simulator(gf.Domain.cube(1.0))
     with pytest.raises(gf.ConfigurationError):
         sim.init_bonds(1.01)
+
+
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_stretched_bond_persists(precision):
+    """An intact bond stretched beyond the detection margin (two soft bonded
+    spheres launched apart) leaves the detected set every half period; the
+    device persistence rule (gf_set_persistent_wildcard, engine.py:639-662)
+    re-appends it, so the bond keeps pulling the spheres back -- the gap
+    history matches the reference's within 2 % of its range."""
+    g = load()
+    r = BK.stretched_bond(gf, precision=precision)
+    assert r["gap"].max() > r["margin"], "the scenario must stretch the bond beyond the margin"
+    assert np.all(r["intact"] == 1)
+    ref = g["stretch_gap"]
+    assert np.max(np.abs(r["gap"] - ref)) <= 0.02 * (ref.max() - ref.min())

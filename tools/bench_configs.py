@@ -73,6 +73,14 @@ def main():
     args = ap.parse_args()
     from paper_2311_04648_b200 import models, scenes
     for name in args.configs.split(","):
+        try:
+            run_one(name, args, models, scenes)
+        except Exception as exc:   # one config failing must not hide the others
+            print(json.dumps({"config": name, "error": f"{type(exc).__name__}: {exc}"}), flush=True)
+
+
+def run_one(name, args, models, scenes):
+    if True:
         t0 = time.perf_counter()
         if name == "cohesive":
             models.cohesive_model()
@@ -86,7 +94,9 @@ def main():
             sys.path.insert(0, os.path.join(ROOT, "tests"))
             import _bulk as BK
             import paper_2311_04648_b200 as gf
-            sim, n_clumps, _, gate = BK.hopper_sim(gf, scale=args.hopper_scale, fill=1.0, precision="f32")
+            # discharged clumps fall up to ~1.7 m below the orifice: a 10 m/s watchdog
+            sim, n_clumps, _, gate = BK.hopper_sim(gf, scale=args.hopper_scale, fill=1.0, precision="f32",
+                                                   v_err=10.0)
             sim.initialize()
             BK.settle(sim, args.hopper_settle)
             sim.set_family_mask(gate, 0, False)
@@ -94,9 +104,11 @@ def main():
             rec = {"config": f"configs[2]: hopper test 2 scaled x{args.hopper_scale} at fixed particle size, "
                              f"{n_clumps} five-sphere WC cylinder clumps, discharging through the orifice"}
         elif name == "rover":
-            sim = scenes.rover_wheel(args.rover_spheres, h=1e-5)
+            # the wheel starts on the terrain top and sinks at 0.1 m/s while the
+            # terrain settles (untimed input preparation at h = 1e-5); timed at 2e-6
+            sim = scenes.rover_wheel(args.rover_spheres, h=1e-5, sinkage=0.0, plunge=0.1)
             sim.initialize()
-            sim.do_dynamics(args.settle_steps * sim.h)   # terrain settles (untimed input preparation)
+            sim.do_dynamics(args.settle_steps * sim.h)
             sim.set_init_time_step(2e-6)
             rec = {"config": f"configs[4]: grousered wheel (0.8 rad/s, 20% slip) on a {args.rover_spheres}-sphere "
                              "GRC-1-like clump terrain, h = 2e-6"}
