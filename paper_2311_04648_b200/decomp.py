@@ -343,7 +343,14 @@ def prepare(sim) -> None:
         er = reach[eligible]
         travel = 2.0 * float(er[er <= 2.0 * np.median(er)].max()) if er.size else 0.0
     axis = dec.axis if dec.axis is not None else (prev.plan.axis if prev is not None else None)
-    plan = plan_slabs(pos, eligible, reach, n_ranks, margin, travel, axis)
+    carried = getattr(prev, "next_plan", None) if prev is not None else None
+    if carried is not None:
+        # incremental migration: the slab cuts stay, owners are re-homed by
+        # their current coordinate (repartition computed it from the
+        # neighbours' fresh state)
+        plan = carried
+    else:
+        plan = plan_slabs(pos, eligible, reach, n_ranks, margin, travel, axis)
     cls = plan.classes(rank)
     # device order: the Morton order of the scene at the FIRST partition,
     # kept for the scene's life (as a single context keeps its order), so
@@ -480,6 +487,11 @@ class _LoopbackTransport:
     def allgather(self, payloads):
         return payloads
 
+    def neighbours(self, payloads):
+        """Per member: {rank: payload} of its slab neighbours and itself."""
+        n = len(payloads)
+        return [{q: payloads[q] for q in (r - 1, r, r + 1) if 0 <= q < n} for r in range(n)]
+
 
 def p2p_exchange(pairs) -> None:
     """One batched point-to-point round: pairs = [(peer, out, n_out, in, n_in)];
@@ -588,6 +600,30 @@ class _NcclTransport:
         out = [None] * dist.get_world_size()
         dist.all_gather_object(out, payloads[0])
         return out
+
+    def neighbours(self, payloads):
+        """{rank: payload} of this rank's slab neighbours and itself: two
+        passes of point-to-point object transfers (right, then left); even
+        ranks send first, odd ranks receive first, so a chain never blocks."""
+        import torch.distributed as dist
+        r, n = dist.get_rank(), dist.get_world_size()
+        got = {r: payloads[0]}
+        for step in (1, -1):
+            dst, src = r + step, r - step
+            box = [None]
+            send = (lambda: dist.send_object_list([payloads[0]], dst)) if 0 <= dst < n else (lambda: None)
+
+            def recv():
+                if 0 <= src < n:
+                    dist.recv_object_list(box, src)
+                    got[src] = box[0]
+            if r % 2 == 0:
+                send()
+                recv()
+            else:
+                recv()
+                send()
+        return [got]
 
 
 # ----------------------------------------------------------------------------
@@ -726,10 +762,83 @@ def update_global(sim_or_group, edit) -> None:
     repartition(sims, xport, edit)
 
 
+def _rehome(plan: SlabPlan, pos: np.ndarray) -> SlabPlan:
+    """The same cuts (and pad, travel, big owners), owners re-homed by their
+    current coordinate."""
+    x = pos[:, plan.axis].copy()
+    home = plan.home.copy()
+    el = home >= 0
+    home[el] = np.searchsorted(plan.cuts, x[el], side="right")
+    return SlabPlan(plan.n_ranks, plan.axis, plan.cuts.copy(), plan.pad, plan.travel, home, x, plan.reach,
+                    plan.big, plan.margin)
+
+
 def repartition(sims, xport, edit=None) -> None:
-    """Migration: gather every rank's owners and contact history, cut new
-    slabs from the current positions and rebuild each rank's context (the
-    history is carried over, so contacts keep their tangential state)."""
+    """Migration after a travel-guard trip.  Incremental by default: every
+    rank exchanges its owners and contact history with its two slab
+    neighbours only (no global gather -- an owner moved at most `travel`, so
+    a rank's new piece and every contact it now computes came from itself or
+    a neighbour), re-homes owners under the same slab cuts and rebuilds its
+    context.  A host edit, or slabs drifted out of balance (the largest
+    rank above 1.5x the smallest), take the global path: gather everything
+    and cut new balanced slabs."""
+    if edit is None:
+        counts = [int(np.sum((s._dd.dd & 3) == DD_LOCAL)) for s in sims]
+        hi = xport.allreduce([[max(counts)]], "max")[0]
+        lo = xport.allreduce([[min(counts)]], "min")[0]
+        if lo > 0 and hi <= 1.5 * lo:
+            _migrate_neighbours(sims, xport)
+            return
+    _repartition_global(sims, xport, edit)
+
+
+_STATE_FIELDS = ("voxel", "subvoxel", "quat", "lin_vel", "ang_vel", "owner_family", "acc_force", "acc_torque",
+                 "ext_force", "ext_torque")
+
+
+def _migrate_neighbours(sims, xport) -> None:
+    nb = xport.neighbours([_local_payload(s) for s in sims])
+    from .core import decode_position
+    for s, parts in zip(sims, nb):
+        g = s._dd.global_store
+        n = g.n_owners
+        d = g.__dict__
+        for p in parts.values():
+            for name in _STATE_FIELDS:
+                d["_" + name][:n][p["gid"]] = p[name]
+        kind = np.concatenate([p["acs_kind"] for p in parts.values()])
+        ga = np.concatenate([p["acs_a"] for p in parts.values()]).astype(np.int64)
+        gb = np.concatenate([p["acs_b"] for p in parts.values()]).astype(np.int64)
+        names = list(next(iter(parts.values()))["acs_wild"].keys())
+        wild = {k: np.concatenate([p["acs_wild"][k] for p in parts.values()]) for k in names}
+        ca = B.ContactArray(kind, ga, gb, wild).canonicalize()
+        if ca.size:
+            keys = ca.sort_keys()
+            ca = ca.select(np.concatenate([[True], keys[1:] != keys[:-1]]))
+        pos = decode_position(d["_voxel"][:n], d["_subvoxel"][:n], g.domain)
+        s._dd.next_plan = _rehome(s._dd.plan, pos)
+        s._acs0_next = ca
+    for s in sims:
+        s._ctx.close()
+        s._ctx = None
+        s.store._sync_hook = None
+        s.store = s._dd.global_store
+        s._acs0 = s._acs0_next
+        del s._acs0_next
+        s._initialized = False
+        s._host_stale = False
+        s._host_dirty = False
+        s.initialize()
+        s.scheduler.repartitions = getattr(s.scheduler, "repartitions", 0) + 1
+        s.scheduler.migrations_incremental = getattr(s.scheduler, "migrations_incremental", 0) + 1
+
+
+def _repartition_global(sims, xport, edit=None) -> None:
+    """Gather every rank's owners and contact history, cut new slabs from the
+    current positions and rebuild each rank's context (the history is
+    carried over, so contacts keep their tangential state)."""
+    for s in sims:
+        s._dd.next_plan = None
     state = gather_state(sims, xport)
     # every member holds its own copy of the global scene (one per process
     # under NCCL; one per Simulator in a LoopbackGroup): update each

@@ -156,3 +156,42 @@ def test_halo_exchange_gloo(world):
         p.join(120)
         assert p.exitcode == 0
     assert list(out) == [1] * world
+
+
+def _neighbour_worker(rank, world, port, out):
+    """The incremental migration's exchange: every rank gets exactly its slab
+    neighbours' payloads (and its own), and re-homing under the same cuts
+    moves an owner only to an adjacent slab."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        x = decomp._NcclTransport.__new__(decomp._NcclTransport)
+        got = x.neighbours([{"rank": rank, "data": np.arange(rank + 3)}])[0]
+        want = {q for q in (rank - 1, rank, rank + 1) if 0 <= q < world}
+        ok = set(got) == want and all(got[q]["rank"] == q and got[q]["data"].size == q + 3 for q in got)
+        pos, el, reach = scene()
+        plan = decomp.plan_slabs(pos, el, reach, world, margin=1e-3, travel=2e-3)
+        moved = pos.copy()
+        moved[:, plan.axis] += np.where(np.arange(pos.shape[0]) % 2 == 0, 1.5e-3, -1.5e-3)
+        new = decomp._rehome(plan, moved)
+        ok = ok and np.array_equal(new.cuts, plan.cuts) and new.pad == plan.pad
+        eligible = plan.home >= 0
+        ok = ok and np.all(np.abs(new.home[eligible] - plan.home[eligible]) <= 1)
+        out[rank] = 1 if ok else 0
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_neighbour_migration_exchange_gloo(world):
+    ctx = mp.get_context("spawn")
+    out = ctx.Array("i", [0] * world)
+    port = _free_port()
+    procs = [ctx.Process(target=_neighbour_worker, args=(r, world, port, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    assert list(out) == [1] * world
