@@ -367,6 +367,18 @@ static int set_split(Ctx *c, const float *radii, int64_t stride, int64_t n) {
   double rc = 0.0;
   for (float x : r)
     if (double(x) <= 2.0 * med && double(x) > rc) rc = double(x);
+  // the big-sphere path (k_big / k_cand_big: atomic appends, long segments)
+  // is for a few large bodies such as the crater projectile; a size
+  // distribution with a heavy tail (GRC-1 terrain: 5 % of spheres above twice
+  // the median) instead raises r_cut so that at most 0.1 % stay big
+  const int64_t limit = std::max<int64_t>(64, n / 1000);
+  int64_t n_above = 0;
+  for (float x : r) n_above += double(x) > rc ? 1 : 0;
+  if (n_above > limit) {
+    std::vector<float> s2(r);
+    std::nth_element(s2.begin(), s2.begin() + (n - limit - 1), s2.end());
+    rc = std::max(rc, double(s2[n - limit - 1]));
+  }
   std::vector<uint32_t> big;
   for (int64_t i = 0; i < n; ++i)
     if (double(r[i]) > rc) big.push_back(uint32_t(i));
@@ -844,6 +856,12 @@ int gf_set_owner_families(gf_ctx *ctx, const uint8_t *family) {
   for (int64_t i = 0; i < n; ++i) meta[i] = (uint32_t(family[i]) << 24) | (meta[i] & 0xFFFFFFu);
   if (h2d(c, c->meta.p, meta.data(), 4 * n, c->s_dt)) return -1;
   world_moving_update(c);
+  // the kinematics records carry the family's passive flag (the integrator
+  // refreshes only their velocity halves)
+  if (c->f32_state && c->n_sph && c->sph_first.p && c->sph_center.bytes >= size_t(32 * c->n_sph)) {
+    if (refresh_centers(c, c->s_dt)) return -1;
+    GF_CHECK(c, cudaStreamSynchronize(c->s_dt));
+  }
   return 0;
 }
 

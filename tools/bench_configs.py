@@ -95,8 +95,10 @@ def run_one(name, args, models, scenes):
             import _bulk as BK
             import paper_2311_04648_b200 as gf
             # discharged clumps fall up to ~1.7 m below the orifice: a 10 m/s watchdog
+            # (h = 2e-5: at the scaled column height 4e-5 -- the reference's
+            # step for its 0.4 m hopper -- let a clump reach 15-30 m/s)
             sim, n_clumps, _, gate = BK.hopper_sim(gf, scale=args.hopper_scale, fill=1.0, precision="f32",
-                                                   v_err=10.0)
+                                                   v_err=10.0, h=2e-5)
             sim.initialize()
             BK.settle(sim, args.hopper_settle)
             sim.set_family_mask(gate, 0, False)

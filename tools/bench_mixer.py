@@ -27,18 +27,23 @@ def main():
     ap.add_argument("--settle-time", type=float, default=0.02)
     ap.add_argument("--out", default="gpurun_out/mixer")
     ap.add_argument("--v-err", type=float, default=10.0)
-    ap.add_argument("--h", type=float, default=1e-4)
+    ap.add_argument("--h-scale", type=float, default=0.1)
     args = ap.parse_args()
     import torch
     from paper_2311_04648_b200 import scenes
     rows = []
     for n in args.n:
-        sim, meta = scenes.mixer(int(n), clump=args.clump, h=args.h)
-        # the reference's step (0.3 / sqrt(k / m), ~5e-4 s) and 25 m/s
-        # watchdog give a detection margin of ~17 grain radii (thousands of
-        # candidate pairs per grain); here h = 1e-4 and 10 m/s (blade tips
-        # move at 2.9 m/s) with a fixed lookahead of 2: a ~1.3-radius margin
-        # (documented deviation; time per step vs N is the measured quantity)
+        sim, meta = scenes.mixer(int(n), clump=args.clump)
+        # the reference's step, 0.3 / sqrt(k / m) (proportional to the grain
+        # size), with its 25 m/s watchdog gives a detection margin of ~17 grain
+        # radii (thousands of candidate pairs per grain); here the step is
+        # h_scale x the reference's (still proportional to the grain size, so
+        # the margin / radius ratio -- and the work per sphere -- is the same
+        # at every N) and 10 m/s (blade tips move at 2.9 m/s) with a fixed
+        # lookahead of 2: a ~0.7-radius margin (documented deviation; time per
+        # step vs N is the measured quantity)
+        sim.set_init_time_step(meta["h"] * args.h_scale)
+        meta["h"] = sim.h
         sim.set_error_out_velocity(args.v_err)
         sim.set_fixed_lookahead(2)
         sim.initialize()

@@ -30,7 +30,7 @@ def main():
         import _bulk as BK
         import paper_2311_04648_b200 as gf
         sim, _, _, gate = BK.hopper_sim(gf, scale=float(sys.argv[3]) if len(sys.argv) > 3 else 3.68, fill=1.0,
-                                        precision="f32", v_err=10.0)
+                                        precision="f32", v_err=10.0, h=float(sys.argv[4]) if len(sys.argv) > 4 else 4e-5)
         sim.initialize()
         BK.settle(sim, 0.3)
         sim.set_family_mask(gate, 0, False)
