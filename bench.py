@@ -64,6 +64,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-f64", action="store_true", help="skip the fp64 parity-build rate")
     ap.add_argument("--amortised-steps", type=int, default=200,
                     help="extra window over several candidate rebuilds (rebuild-amortised rate)")
     ap.add_argument("--prof-steps", type=int, default=20, help="per-kernel event window")
@@ -501,11 +502,38 @@ def b200_arm(args):
             "gpu_launches": int(args.steps * launches_per_step + (args.steps // max(1, period)) * kt_launches),
             "cpu_baseline": cpu,
         }
+    sim.close()
+    if line is not None and mode in ("single", "ktdt") and not args.no_f64 and args.precision == "f32":
+        # the reference's own arithmetic (fp64 state and contact law, the
+        # bit-exact parity build) on configs[1]'s bed, for comparison
+        line["f64_build"] = f64_build_rate(args, device)
     if line is not None:
         print(json.dumps(line), flush=True)
-    sim.close()
     if dist is not None:
         dist.destroy_process_group()
+
+
+def f64_build_rate(args, device, steps=100):
+    """M sphere-steps/s of the fp64 parity build on the settled configs[1]
+    bed (1M spheres + projectile), CUDA events on the dT stream."""
+    import torch
+    a = argparse.Namespace(**vars(args))
+    a.precision = "f64"
+    sim, _ = settled_source(a, device)
+    try:
+        sim.do_dynamics(5 * sim.h)
+        torch.cuda.synchronize(device)
+        d0 = sim.scheduler.timing["dyn_force"]
+        sim.do_dynamics(steps * sim.h)
+        torch.cuda.synchronize(device)
+        ms = (sim.scheduler.timing["dyn_force"] - d0) * 1e3
+        n_s = int(sim._sph_geom.size)
+        return {"value": n_s * steps / (ms * 1e-3) / 1e6, "unit": UNIT, "ms_per_step": ms / steps,
+                "steps": steps, "dtype": DTYPE_F64,
+                "workload": f"configs[1] settled crater bed, {n_s} spheres (one tile), fp64 parity build "
+                            "(bit-exact per step against the reference's arithmetic)"}
+    finally:
+        sim.close()
 
 
 def measure_e2e(sim, steps):

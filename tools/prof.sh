@@ -6,7 +6,7 @@
 set -u
 tag=$1; tiles=$2; kre=${3:-"k_contacts_ss|k_integrate"}; shift 3 || true
 mkdir -p gpurun_out
-B="python bench.py --tiles $tiles --steps 8 --warmup 4 --no-cpu --e2e-steps 0 --amortised-steps 0 --prof-steps 4 $*"
+B="python bench.py --tiles $tiles --steps 8 --warmup 4 --no-cpu --no-f64 --e2e-steps 0 --amortised-steps 0 --prof-steps 4 $*"
 GF_PROFILE_TIMED=1 timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none \
   --csv --log-file gpurun_out/launches_$tag.csv $B > gpurun_out/launches_$tag.log 2>&1
 python profiles/launch_summary.py gpurun_out/launches_$tag.csv > gpurun_out/launch_summary_$tag.txt 2>&1
