@@ -90,45 +90,35 @@ __host__ __device__ inline bool dd_keep(const uint32_t *dd, uint32_t oa, uint32_
   return ca == kDdPrimary && cb == kDdPrimary;
 }
 
-// Per-sphere records of the contact kernels -- two 32-byte records, each read
-// with ONE 256-bit load (ld256 / ld_kin, sm_100's LDG.E.256):
-//   centre (double4): world centre x, y, z (fp64); the w slot carries the
-//       sphere radius (float32 -- the reference's geometry parameter, low
-//       word) and the packed word (high word): force-scale exponent (bits
-//       24-31), torque-scale exponent (16-23), material (8-15), flags (0-7;
-//       bit 0 passive owner, bit 1 lever);
-//   SphKin (throughput build): v = owner linear velocity + owner mass,
-//       w = owner angular velocity (global frame) + owner id (bits).
-// A sphere off its owner's centre (kKinLever) has its lever arm (centre minus
-// owner position, rotated) in Spheres::lever; a single-sphere owner's lever
-// is zero and is never stored or loaded.  The narrow phase has the packed
-// words of both spheres in registers once the centres are in, so the force
-// phase gathers only the 32-byte velocity records.
+// Per-sphere kinematics record of the throughput build, written wherever the
+// sphere centres are (integrator, refresh, halo unpack) so the contact kernel
+// reaches everything it needs one load after the contact list, with no
+// further dependent loads -- 48 B, three 16-byte loads:
+//   v = owner linear velocity,                  v.w = owner mass (float)
+//   w = owner angular velocity (global frame),  w.w = owner id (bits)
+//   r = centre minus owner position,            r.w = packed (bits): force-scale
+//       exponent (bits 24-31), torque-scale exponent (16-23), material (8-15),
+//       flags (0-7; bit 0 = passive owner)
 // The fixed-point scales are the owner template's tpl_scale, powers of two by
 // construction (gf_context.cu update_fixed_scales), stored as exponents;
 // kKinNoScale = boundary owner (scale 0), summed with fp64 atomics.
 constexpr uint32_t kKinPassive = 1u;
-constexpr uint32_t kKinLever = 2u;
 constexpr int kKinNoScale = -128;
-struct __align__(32) SphKin {
-  float4 v, w;
+struct SphKin {
+  float4 v, w, r;
 };
 __device__ __forceinline__ uint32_t kin_owner(const SphKin &k) { return __float_as_uint(k.w.w); }
-__device__ __forceinline__ uint32_t kin_mat(uint32_t packed) { return (packed >> 8) & 0xFFu; }
-__device__ __forceinline__ uint32_t kin_flags(uint32_t packed) { return packed & 0xFFu; }
+__device__ __forceinline__ uint32_t kin_mat(const SphKin &k) { return (__float_as_uint(k.r.w) >> 8) & 0xFFu; }
+__device__ __forceinline__ uint32_t kin_flags(const SphKin &k) { return __float_as_uint(k.r.w) & 0xFFu; }
 __device__ __forceinline__ double kin_exp2(int e) {   // 2^e exactly, 0 for kKinNoScale
   return e == kKinNoScale ? 0.0 : __longlong_as_double((long long)(1023 + e) << 52);
 }
-__device__ __forceinline__ double kin_fscale(uint32_t packed) { return kin_exp2(int((signed char)(packed >> 24))); }
-__device__ __forceinline__ double kin_tscale(uint32_t packed) {
-  return kin_exp2(int((signed char)((packed >> 16) & 0xFFu)));
+__device__ __forceinline__ double kin_fscale(const SphKin &k) {
+  return kin_exp2(int((signed char)(__float_as_uint(k.r.w) >> 24)));
 }
-
-__device__ __forceinline__ double4 make_centre(double x, double y, double z, float r, uint32_t packed) {
-  return make_double4(x, y, z, __hiloint2double(int(packed), __float_as_int(r)));
+__device__ __forceinline__ double kin_tscale(const SphKin &k) {
+  return kin_exp2(int((signed char)((__float_as_uint(k.r.w) >> 16) & 0xFFu)));
 }
-__device__ __forceinline__ float centre_r(const double4 &c) { return __int_as_float(__double2loint(c.w)); }
-__device__ __forceinline__ uint32_t centre_packed(const double4 &c) { return uint32_t(__double2hiint(c.w)); }
 
 // one 256-bit read-only load of a 32-byte record (LDG.E.256 on sm_100).  An
 // NVRTC older than 12.9 (torch ships 12.8; a process that imported torch has
@@ -151,28 +141,14 @@ __device__ __forceinline__ double4 ld256(const double4 *p) {
   return r;
 }
 
-__device__ __forceinline__ SphKin ld_kin(const SphKin *p) {
-  SphKin k;
-#if GF_LD256
-  asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-      : "=f"(k.v.x), "=f"(k.v.y), "=f"(k.v.z), "=f"(k.v.w), "=f"(k.w.x), "=f"(k.w.y), "=f"(k.w.z), "=f"(k.w.w)
-      : "l"(p));
-#else
-  k.v = __ldg(&p->v);
-  k.w = __ldg(&p->w);
-#endif
-  return k;
-}
-
 struct Spheres {
   int64_t n;
   uint32_t *owner;
   float4 *offr;        // local offset xyz + radius (float32 geom params)
   uint8_t *mat;
-  double4 *center;     // world centre + (float radius, packed word), refreshed by the integrator
+  double4 *center;     // world centre + radius, refreshed by the integrator
   uint32_t *first;     // [n_owner + 1] CSR: spheres of owner o are [first[o], first[o+1])
   SphKin *kin;         // throughput build only (fp32 velocities), else nullptr
-  float4 *lever;       // throughput build: lever arms of kKinLever spheres (else unused / nullptr)
 };
 
 struct Tris {
@@ -282,45 +258,47 @@ __device__ __forceinline__ void qrot(double qw, double qx, double qy, double qz,
   rz = add(vz, mul(2.0, sub_(mul(qx, ty), mul(qy, tx))));
 }
 
-// the packed word of sphere k (power-of-two scales -> exponents: ilogb is
-// exact on powers of two)
-__device__ __forceinline__ uint32_t kin_packed_of(const Spheres &sph, uint32_t k, double2 scale, uint32_t flags,
-                                                  bool lever) {
-  const int ef = scale.x > 0.0 ? ilogb(scale.x) : kKinNoScale, et = scale.y > 0.0 ? ilogb(scale.y) : kKinNoScale;
-  return ((uint32_t(ef) & 0xFFu) << 24) | ((uint32_t(et) & 0xFFu) << 16) | (uint32_t(sph.mat[k]) << 8) |
-         ((flags | (lever ? kKinLever : 0u)) & 0xFFu);
-}
-
-// kinematics record (and lever) from the STORED owner state (quaternion,
-// float32 velocities), identical wherever it is computed
+// kinematics record from the STORED owner state (quaternion, float32
+// velocities), identical wherever it is computed
 __device__ __forceinline__ void write_kin(const Spheres &sph, uint32_t k, uint32_t o, const float4 q,
-                                          const float4 lv, const float4 av, float mass, const float4 orr) {
-  double w[3];
+                                          const float4 lv, const float4 av, float mass, double2 scale,
+                                          uint32_t flags) {
+  const float4 orr = sph.offr[k];
+  double r[3], w[3];
+  qrot(double(q.x), double(q.y), double(q.z), double(q.w), double(orr.x), double(orr.y), double(orr.z), r[0], r[1],
+       r[2]);
   qrot(double(q.x), double(q.y), double(q.z), double(q.w), double(av.x), double(av.y), double(av.z), w[0], w[1],
        w[2]);
-  if (orr.x != 0.f || orr.y != 0.f || orr.z != 0.f) {
-    double r[3];
-    qrot(double(q.x), double(q.y), double(q.z), double(q.w), double(orr.x), double(orr.y), double(orr.z), r[0],
-         r[1], r[2]);
-    sph.lever[k] = make_float4(float(r[0]), float(r[1]), float(r[2]), 0.f);
-  }
+  // power-of-two scales -> their exponents (ilogb is exact on powers of two)
+  const int ef = scale.x > 0.0 ? ilogb(scale.x) : kKinNoScale, et = scale.y > 0.0 ? ilogb(scale.y) : kKinNoScale;
+  const uint32_t packed = ((uint32_t(ef) & 0xFFu) << 24) | ((uint32_t(et) & 0xFFu) << 16) |
+                          (uint32_t(sph.mat[k]) << 8) | (flags & 0xFFu);
   SphKin kr;
   kr.v = make_float4(lv.x, lv.y, lv.z, mass);
   kr.w = make_float4(float(w[0]), float(w[1]), float(w[2]), __uint_as_float(o));
+  kr.r = make_float4(float(r[0]), float(r[1]), float(r[2]), __uint_as_float(packed));
   sph.kin[k] = kr;
 }
 
-__device__ __forceinline__ uint32_t packed_from_state(const Owners &own, const Spheres &sph, uint32_t k, uint32_t o) {
-  const uint32_t meta = own.meta[o], t = meta_tpl(meta);
-  const uint32_t flags = (own.passive && own.passive[meta_family(meta)]) ? kKinPassive : 0u;
-  const float4 orr = sph.offr[k];
-  return kin_packed_of(sph, k, own.tpl_scale[t], flags, orr.x != 0.f || orr.y != 0.f || orr.z != 0.f);
+// the integrator's per-step refresh of a record whose sphere sits at its
+// owner's centre: the lever is zero and the packed word (scales, material,
+// flags) only changes with the tables, which rewrite whole records
+// (refresh_centers) -- so only the velocity halves are stored (32 of 48 B)
+__device__ __forceinline__ void write_kin_vel(const Spheres &sph, uint32_t k, uint32_t o, const float4 q,
+                                              const float4 lv, const float4 av, float mass) {
+  double w[3];
+  qrot(double(q.x), double(q.y), double(q.z), double(q.w), double(av.x), double(av.y), double(av.z), w[0], w[1],
+       w[2]);
+  float4 *rec = reinterpret_cast<float4 *>(sph.kin + k);
+  rec[0] = make_float4(lv.x, lv.y, lv.z, mass);
+  rec[1] = make_float4(float(w[0]), float(w[1]), float(w[2]), __uint_as_float(o));
 }
 
 __device__ __forceinline__ void write_kin_from_state(const Owners &own, const Spheres &sph, uint32_t k, uint32_t o) {
-  const uint32_t t = meta_tpl(own.meta[o]);
+  const uint32_t meta = own.meta[o], t = meta_tpl(meta);
+  const uint32_t flags = (own.passive && own.passive[meta_family(meta)]) ? kKinPassive : 0u;
   write_kin(sph, k, o, own.quat[o], reinterpret_cast<const float4 *>(own.lin_vel)[o],
-            reinterpret_cast<const float4 *>(own.ang_vel)[o], float(own.tpl[t].x), sph.offr[k]);
+            reinterpret_cast<const float4 *>(own.ang_vel)[o], float(own.tpl[t].x), own.tpl_scale[t], flags);
 }
 
 // sphere world centre: owner pos + q * offset (_kernels.py:91-106)

@@ -140,8 +140,7 @@ Owners owners_view(Ctx *c) {
 Spheres spheres_view(Ctx *c) {
   return Spheres{c->n_sph, c->sph_owner.as<uint32_t>(), c->sph_offr.as<float4>(), c->sph_mat.as<uint8_t>(),
                  c->sph_center.as<double4>(), c->sph_first.as<uint32_t>(),
-                 c->f32_state ? c->sph_kin.as<SphKin>() : nullptr,
-                 c->f32_state ? c->sph_lever.as<float4>() : nullptr};
+                 c->f32_state ? c->sph_kin.as<SphKin>() : nullptr};
 }
 Tris tris_view(Ctx *c) {
   return Tris{c->n_tri, c->tri_owner.as<uint32_t>(), c->tri_local.as<float>(), c->tri_mat.as<uint8_t>(),
@@ -540,7 +539,7 @@ void gf_destroy(gf_ctx *ctx) {
   }
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
-  DBuf *bufs[] = {&c->sph_kin, &c->sph_lever, &c->tlist, &c->tlist_n, &c->facc, &c->tpl_scale, &c->sph_center, &c->sph_first, &c->voxel, &c->sub, &c->quat, &c->lin_vel, &c->ang_vel, &c->meta, &c->tpl, &c->acc,
+  DBuf *bufs[] = {&c->sph_kin, &c->tlist, &c->tlist_n, &c->facc, &c->tpl_scale, &c->sph_center, &c->sph_first, &c->voxel, &c->sub, &c->quat, &c->lin_vel, &c->ang_vel, &c->meta, &c->tpl, &c->acc,
                   &c->ext, &c->sph_owner, &c->sph_offr, &c->sph_mat, &c->tri_owner, &c->tri_local,
                   &c->tri_mat, &c->tri_world, &c->ana_owner, &c->ana_kind, &c->ana_local, &c->ana_mat,
                   &c->ana_world, &c->pair, &c->beta, &c->fam_mask, &c->fam_flags, &c->lv_mask,
@@ -998,14 +997,9 @@ int gf_upload_geometry(gf_ctx *ctx, int64_t n_s, const int64_t *sph_owner, const
       first[sph_owner[k] + 1]++;
     }
     for (int64_t o = 0; o < c->n_owner; ++o) first[o + 1] += first[o];
-    // lever arms are stored only for spheres off their owner's centre (clumps)
-    bool levers = false;
-    for (int64_t k = 0; k < n_s && !levers; ++k)
-      levers = sph_params[4 * k] != 0.f || sph_params[4 * k + 1] != 0.f || sph_params[4 * k + 2] != 0.f;
     if (upload_raw(c, c->sph_first, first.data(), 4 * (c->n_owner + 1)) ||
         ensure(c, c->sph_center, 32 * (n_s + 1), c->s_dt) ||
-        (c->f32_state && ensure(c, c->sph_kin, sizeof(SphKin) * (n_s + 1), c->s_dt)) ||
-        (c->f32_state && levers && ensure(c, c->sph_lever, sizeof(float4) * (n_s + 1), c->s_dt)))
+        (c->f32_state && ensure(c, c->sph_kin, sizeof(SphKin) * (n_s + 1), c->s_dt)))
       return -1;
   }
   if (refresh_centers(c, c->s_dt)) return -1;

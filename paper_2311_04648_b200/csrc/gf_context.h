@@ -144,7 +144,6 @@ struct Ctx {
   int64_t n_sph = 0, n_tri = 0, n_ana = 0;
   DBuf sph_owner, sph_offr, sph_mat, sph_center, sph_first;
   DBuf sph_kin;  // SphKin per sphere (fp32-velocity build)
-  DBuf sph_lever;  // float4 lever arm per sphere, allocated when any sphere is off its owner's centre
   DBuf tri_owner, tri_local, tri_mat, tri_world;
   DBuf ana_owner, ana_kind, ana_local, ana_mat, ana_world;
   bool world_moving = true;  // any tri/ana owner not fixed
@@ -190,7 +189,6 @@ struct Ctx {
   int persist_col = -1;      // wildcard column whose > 0 rows persist across detections (bonds), or -1
   int64_t persisted = 0;     // rows re-appended by that rule so far
   int n_sm = 148;             // multiprocessors of the device (grid sizing)
-  bool ss_smem_set = false;  // k_contacts_ss dynamic shared memory opted in (attributes are per device)
   int ss_blocked = 2;        // fused kernel: contiguous entry range per CTA (1), grid-stride (0), auto by size (2)
   int ss_pf = 1;             // fused kernel read-ahead / prefetch (GF_SS_PF=0: off)
   int ss_red = 1;            // fused sphere-sphere kernel: staged fixed-point rows (GF_SS_RED=0: per-word REDs)

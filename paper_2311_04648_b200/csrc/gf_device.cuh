@@ -102,12 +102,12 @@ __device__ __forceinline__ void contact_geometry(const DtView &v, uint2 id, doub
   const uint32_t kind = id.y >> kKindShift, sb = id.y & kSlotMask;
   const double4 cA = v.sph.center[id.x];
   ca[0] = cA.x; ca[1] = cA.y; ca[2] = cA.z;
-  ra = double(centre_r(cA));
+  ra = cA.w;
   if (kind == 0) {
     const double4 cB = v.sph.center[sb];
     double dx = ca[0] - cB.x, dy = ca[1] - cB.y, dz = ca[2] - cB.z;
     double d = sqrt(dx * dx + dy * dy + dz * dz);
-    rb = double(centre_r(cB));
+    rb = cB.w;
     if (d < 1e-300) {
       depth = ra + rb; bx = 0.0; by = 0.0; bz = 1.0;
     } else {
@@ -550,27 +550,23 @@ __device__ __forceinline__ void user_ss_loop(const DtView &v, double ts, double 
     if (k < n_ss) {
       const uint2 id = v.ids[k];
       const uint32_t a = id.x, b = id.y & kSlotMask;
-      const double4 cA = ld256(v.sph.center + a), cB = ld256(v.sph.center + b);
-      const SphKin ka = ld_kin(v.sph.kin + a), kb = ld_kin(v.sph.kin + b);
-      const uint32_t pa = centre_packed(cA), pb = centre_packed(cB);
-      const float4 la = (kin_flags(pa) & kKinLever) ? v.sph.lever[a] : make_float4(0.f, 0.f, 0.f, 0.f);
-      const float4 lb = (kin_flags(pb) & kKinLever) ? v.sph.lever[b] : make_float4(0.f, 0.f, 0.f, 0.f);
-      const double ra_ = double(centre_r(cA)), rb_ = double(centre_r(cB));
+      const double4 cA = v.sph.center[a], cB = v.sph.center[b];
+      const SphKin ka = v.sph.kin[a], kb = v.sph.kin[b];
       const double dx = cA.x - cB.x, dy = cA.y - cB.y, dz = cA.z - cB.z;
       const double d = sqrt(dx * dx + dy * dy + dz * dz);
       double depth, bx, by, bz;
       if (d < 1e-300) {
-        depth = ra_ + rb_; bx = 0.0; by = 0.0; bz = 1.0;
+        depth = cA.w + cB.w; bx = 0.0; by = 0.0; bz = 1.0;
       } else {
         const double inv = 1.0 / d;
         bx = dx * inv; by = dy * inv; bz = dz * inv;
-        depth = ra_ + rb_ - d;
+        depth = cA.w + cB.w - d;
       }
       if (depth > 0.0) ++touched;
       // contact point p = cA - b (ra - depth / 2); lever arms p - pos_a, p - pos_b
-      const double half = ra_ - 0.5 * depth;
-      const double rax = la.x - bx * half, ray = la.y - by * half, raz = la.z - bz * half;
-      const double rbx = lb.x + dx - bx * half, rby = lb.y + dy - by * half, rbz = lb.z + dz - bz * half;
+      const double half = cA.w - 0.5 * depth;
+      const double rax = ka.r.x - bx * half, ray = ka.r.y - by * half, raz = ka.r.z - bz * half;
+      const double rbx = kb.r.x + dx - bx * half, rby = kb.r.y + dy - by * half, rbz = kb.r.z + dz - bz * half;
       const double rotax = ka.w.y * raz - ka.w.z * ray, rotay = ka.w.z * rax - ka.w.x * raz,
                    rotaz = ka.w.x * ray - ka.w.y * rax;
       const double rotbx = kb.w.y * rbz - kb.w.z * rby, rotby = kb.w.z * rbx - kb.w.x * rbz,
@@ -584,8 +580,8 @@ __device__ __forceinline__ void user_ss_loop(const DtView &v, double ts, double 
       arg.wrx = rotbx - rotax; arg.wry = rotby - rotay; arg.wrz = rotbz - rotaz;
       const double ma = ka.v.w, mb = kb.v.w;
       arg.mass_eff = (ma * mb) / (ma + mb);
-      arg.ra = ra_; arg.rb = rb_;
-      arg.mat_a = int(kin_mat(pa)); arg.mat_b = int(kin_mat(pb));
+      arg.ra = cA.w; arg.rb = cB.w;
+      arg.mat_a = int(kin_mat(ka)); arg.mat_b = int(kin_mat(kb));
       arg.pair = v.mat.pair; arg.n_mat = v.mat.n_mat;
       arg.wild = v.wild + size_t(v.W) * k;
       arg.M = &v.mat;
@@ -596,8 +592,8 @@ __device__ __forceinline__ void user_ss_loop(const DtView &v, double ts, double 
         const double tx = o6[0] + o6[3], ty = o6[1] + o6[4], tz = o6[2] + o6[5];
         ta[0] = float(ray * tz - raz * ty); ta[1] = float(raz * tx - rax * tz); ta[2] = float(rax * ty - ray * tx);
         const double tb[3] = {rby * tz - rbz * ty, rbz * tx - rbx * tz, rbx * ty - rby * tx};
-        if (v.acc_all || !(kin_flags(pb) & kKinPassive)) {
-          const double sbf = kin_fscale(pb), sbt = kin_tscale(pb);
+        if (v.acc_all || !(kin_flags(kb) & kKinPassive)) {
+          const double sbf = kin_fscale(kb), sbt = kin_tscale(kb);
           unsigned long long *fb = reinterpret_cast<unsigned long long *>(v.own.facc + 6 * size_t(kin_owner(kb)));
           for (int q = 0; q < 3; ++q) {
             if (sbf > 0.0) {
@@ -610,9 +606,9 @@ __device__ __forceinline__ void user_ss_loop(const DtView &v, double ts, double 
           }
         }
         oa = kin_owner(ka);
-        use_a = v.acc_all || !(kin_flags(pa) & kKinPassive);
-        sa_f = kin_fscale(pa);
-        sa_t = kin_tscale(pa);
+        use_a = v.acc_all || !(kin_flags(ka) & kKinPassive);
+        sa_f = kin_fscale(ka);
+        sa_t = kin_tscale(ka);
       }
     }
     a_side_sums(v, use_a, oa, sa_f, sa_t, out, ta, lane);

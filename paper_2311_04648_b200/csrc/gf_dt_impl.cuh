@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(256, 4) k_touch_ss(DtView v, uint4 *rec, unsig
     for (int j = 0; j < E; ++j) {
       if (s_live && k0 + j < n_ss) {
         const double dx = ca[j].x - cb[j].x, dy = ca[j].y - cb[j].y, dz = ca[j].z - cb[j].z;
-        const double R = double(centre_r(ca[j])) + double(centre_r(cb[j]));
+        const double R = ca[j].w + cb[j].w;
         if (float(R * R - (dx * dx + dy * dy + dz * dz)) > 0.f) m |= 1u << j;
       }
     }
@@ -206,19 +206,17 @@ __device__ __forceinline__ bool stage_materials(const DtView &v, float (*s_mat)[
 // numerator R^2 - d^2 (fp64, rounded) and the radii.
 struct SsGeom {
   float dx, dy, dz, d, num, ra, rb;
-  uint32_t pa, pb;   // the spheres' packed words (scales, material, flags)
 };
 
 __device__ __forceinline__ bool ss_geom(const DtView &v, uint32_t a, uint32_t b, SsGeom &g) {
   const double4 cA = ld256(v.sph.center + a), cB = ld256(v.sph.center + b);
   const double dx = cA.x - cB.x, dy = cA.y - cB.y, dz = cA.z - cB.z;
   const double d2 = dx * dx + dy * dy + dz * dz;
-  g.ra = centre_r(cA); g.rb = centre_r(cB);
-  const double R = double(g.ra) + double(g.rb);
+  const double R = cA.w + cB.w;
   g.num = float(R * R - d2);
   g.dx = float(dx); g.dy = float(dy); g.dz = float(dz);
   g.d = sqrtf(float(d2));
-  g.pa = centre_packed(cA); g.pb = centre_packed(cB);
+  g.ra = float(cA.w); g.rb = float(cB.w);
   return g.num > 0.f;
 }
 
@@ -242,7 +240,7 @@ __device__ __forceinline__ void ss_force_warp(const DtView &v, bool live, uint32
   if (live) {
     // one load round: kinematics records (mass, scales, flags included) and
     // the history row
-    const SphKin ka = ld_kin(v.sph.kin + a), kb = ld_kin(v.sph.kin + b);
+    const SphKin ka = v.sph.kin[a], kb = v.sph.kin[b];
     float4 *wp = reinterpret_cast<float4 *>(v.wild) + k;
     const float4 w4 = *wp;
     const int nm = v.mat.n_mat, mm = nm * nm;
@@ -257,11 +255,8 @@ __device__ __forceinline__ void ss_force_warp(const DtView &v, bool live, uint32
     ob_ = ob;
     // contact point p = cA - b (ra - depth / 2); lever arms p - pos_a, p - pos_b
     const float ha = g.ra - 0.5f * depth;
-    float4 la = make_float4(0.f, 0.f, 0.f, 0.f), lb = la;
-    if (kin_flags(g.pa) & kKinLever) la = v.sph.lever[a];
-    if (kin_flags(g.pb) & kKinLever) lb = v.sph.lever[b];
-    const float rax = la.x - bx * ha, ray = la.y - by * ha, raz = la.z - bz * ha;
-    const float rbx = lb.x + g.dx - bx * ha, rby = lb.y + g.dy - by * ha, rbz = lb.z + g.dz - bz * ha;
+    const float rax = ka.r.x - bx * ha, ray = ka.r.y - by * ha, raz = ka.r.z - bz * ha;
+    const float rbx = kb.r.x + g.dx - bx * ha, rby = kb.r.y + g.dy - by * ha, rbz = kb.r.z + g.dz - bz * ha;
     const float rotax = ka.w.y * raz - ka.w.z * ray, rotay = ka.w.z * rax - ka.w.x * raz,
                 rotaz = ka.w.x * ray - ka.w.y * rax;
     const float rotbx = kb.w.y * rbz - kb.w.z * rby, rotby = kb.w.z * rbx - kb.w.x * rbz,
@@ -271,7 +266,7 @@ __device__ __forceinline__ void ss_force_warp(const DtView &v, bool live, uint32
     const float vz = (ka.v.z + rotaz) - (kb.v.z + rotbz);
     const double ma = ka.v.w, mb = kb.v.w;
     const float mass_eff = float((ma * mb) / (ma + mb));
-    const int ab = int(kin_mat(g.pa)) * nm + int(kin_mat(g.pb));
+    const int ab = int(kin_mat(ka)) * nm + int(kin_mat(kb));
     float e_cnt, g_cnt, mu, crr, beta;
     if (smem) {
       e_cnt = s_mat[0][ab]; g_cnt = s_mat[1][ab]; mu = s_mat[2][ab]; crr = s_mat[3][ab]; beta = s_mat[4][ab];
@@ -288,8 +283,8 @@ __device__ __forceinline__ void ss_force_warp(const DtView &v, bool live, uint32
     const float tb[3] = {rby * tz - rbz * ty, rbz * tx - rbx * tz, rbx * ty - rby * tx};
     // B side: one atomic per word (B owners are scattered); staged (red !=
     // nullptr): fixed-point rows through the warp's shared buffer below
-    if (v.acc_all || !(kin_flags(g.pb) & kKinPassive)) {
-      const double sbf = kin_fscale(g.pb), sbt = kin_tscale(g.pb);
+    if (v.acc_all || !(kin_flags(kb) & kKinPassive)) {
+      const double sbf = kin_fscale(kb), sbt = kin_tscale(kb);
       if (red != nullptr && sbf > 0.0) {
         b_row = true;
 #pragma unroll
@@ -311,9 +306,9 @@ __device__ __forceinline__ void ss_force_warp(const DtView &v, bool live, uint32
       }
       }
     }
-    use_a = v.acc_all || !(kin_flags(g.pa) & kKinPassive);
-    sa_f = kin_fscale(g.pa);
-    sa_t = kin_tscale(g.pa);
+    use_a = v.acc_all || !(kin_flags(ka) & kKinPassive);
+    sa_f = kin_fscale(ka);
+    sa_t = kin_tscale(ka);
   }
   if (red != nullptr) {
     // B rows, compacted: one RED instruction covers ~5 owners' rows
@@ -367,9 +362,6 @@ static __global__ void __launch_bounds__(256, 4) k_forces_f32(DtView v, double t
 // queued contacts, so force lanes are never idle on false positives and the
 // touching list never goes through HBM.
 constexpr int kSsWarps = 8;
-// dynamic shared memory of k_contacts_ss<kSsPerLane>: the per-warp queue
-template <int kSsPerLane>
-constexpr size_t ss_queue_bytes() { return sizeof(uint32_t) * 12 * kSsWarps * 32 * (kSsPerLane + 1); }
 
 template <int kSsPerLane, int kMinBlocks, bool kStaged = true>
 static __global__ void __launch_bounds__(256, kMinBlocks) k_contacts_ss(DtView v, double ts_d, unsigned long long step) {
@@ -378,13 +370,8 @@ static __global__ void __launch_bounds__(256, kMinBlocks) k_contacts_ss(DtView v
   // staged fixed-point rows of the warp's force batch (B side, then A side)
   __shared__ long long s_red[kStaged ? kSsWarps : 1][kStaged ? 192 : 1];
   __shared__ uint32_t s_own[kSsWarps][32];   // [0][0] doubles as the block's live flag at entry
-  extern __shared__ __align__(16) uint32_t ss_queue[];   // dynamic: a, b, k, packed A / B, 7 geometry floats
-  uint32_t (*q_a)[kSsQueue] = reinterpret_cast<uint32_t (*)[kSsQueue]>(ss_queue);
-  uint32_t (*q_b)[kSsQueue] = q_a + kSsWarps;
-  uint32_t (*q_k)[kSsQueue] = q_b + kSsWarps;
-  uint32_t (*q_pa)[kSsQueue] = q_k + kSsWarps;
-  uint32_t (*q_pb)[kSsQueue] = q_pa + kSsWarps;
-  float (*q_g)[kSsWarps][kSsQueue] = reinterpret_cast<float (*)[kSsWarps][kSsQueue]>(q_pb + kSsWarps);
+  __shared__ uint32_t q_a[kSsWarps][kSsQueue], q_b[kSsWarps][kSsQueue], q_k[kSsWarps][kSsQueue];
+  __shared__ float q_g[7][kSsWarps][kSsQueue];
   const bool smem = stage_materials(v, s_mat);   // static tables: before the predecessor drains
   pdl_wait();
   pdl_launch();
@@ -422,7 +409,6 @@ static __global__ void __launch_bounds__(256, kMinBlocks) k_contacts_ss(DtView v
       a = qa[lane]; b = qb[lane]; k = qk[lane];
       g.dx = q_g[0][warp][lane]; g.dy = q_g[1][warp][lane]; g.dz = q_g[2][warp][lane];
       g.d = q_g[3][warp][lane]; g.num = q_g[4][warp][lane]; g.ra = q_g[5][warp][lane]; g.rb = q_g[6][warp][lane];
-      g.pa = q_pa[warp][lane]; g.pb = q_pb[warp][lane];
     }
     ss_force_warp(v, live, a, b, k, g, ts, s_mat, smem, lane, kStaged ? s_red[warp] : nullptr,
                   kStaged ? s_own[warp] : nullptr);
@@ -431,12 +417,12 @@ static __global__ void __launch_bounds__(256, kMinBlocks) k_contacts_ss(DtView v
     const int rest = qn - take;
     for (int j = lane; j < rest; j += 32) {
       const int src = take + j;
-      const uint32_t xa = qa[src], xb = qb[src], xk = qk[src], xpa = q_pa[warp][src], xpb = q_pb[warp][src];
+      const uint32_t xa = qa[src], xb = qb[src], xk = qk[src];
       float xg[7];
 #pragma unroll
       for (int f = 0; f < 7; ++f) xg[f] = q_g[f][warp][src];
       __syncwarp(__activemask());
-      qa[j] = xa; qb[j] = xb; qk[j] = xk; q_pa[warp][j] = xpa; q_pb[warp][j] = xpb;
+      qa[j] = xa; qb[j] = xb; qk[j] = xk;
 #pragma unroll
       for (int f = 0; f < 7; ++f) q_g[f][warp][j] = xg[f];
     }
@@ -495,7 +481,6 @@ static __global__ void __launch_bounds__(256, kMinBlocks) k_contacts_ss(DtView v
       if (t[j]) {
         const int pos = qn + __popc(m & ((1u << lane) - 1u));
         qa[pos] = id[j].x; qb[pos] = id[j].y & kSlotMask; qk[pos] = uint32_t(base + 32 * j + lane);
-        q_pa[warp][pos] = g[j].pa; q_pb[warp][pos] = g[j].pb;
         q_g[0][warp][pos] = g[j].dx; q_g[1][warp][pos] = g[j].dy; q_g[2][warp][pos] = g[j].dz;
         q_g[3][warp][pos] = g[j].d; q_g[4][warp][pos] = g[j].num; q_g[5][warp][pos] = g[j].ra;
         q_g[6][warp][pos] = g[j].rb;
@@ -765,10 +750,13 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_integrate(DtView v, double 
       double r[3];
       qrot(double(q.x), double(q.y), double(q.z), double(q.w), double(orr.x), double(orr.y), double(orr.z),
            r[0], r[1], r[2]);
-      const uint32_t packed =
-          v.sph.kin ? kin_packed_of(v.sph, k, sc, kflags, orr.x != 0.f || orr.y != 0.f || orr.z != 0.f) : 0u;
-      v.sph.center[k] = make_centre(add(pd[0], r[0]), add(pd[1], r[1]), add(pd[2], r[2]), orr.w, packed);
-      if (v.sph.kin) write_kin(v.sph, k, o, q, lv4, av4, float(tp.x), orr);
+      v.sph.center[k] = make_double4(add(pd[0], r[0]), add(pd[1], r[1]), add(pd[2], r[2]), double(orr.w));
+      if (v.sph.kin) {
+        if (orr.x == 0.f && orr.y == 0.f && orr.z == 0.f)
+          write_kin_vel(v.sph, k, o, q, lv4, av4, float(tp.x));
+        else
+          write_kin(v.sph, k, o, q, lv4, av4, float(tp.x), sc, kflags);
+      }
     }
   }
 }
@@ -790,7 +778,7 @@ __global__ void k_centers(Domain dom, Owners own, Spheres sph) {
   float r;
   uint32_t o;
   sphere_center(dom, own, sph, uint32_t(k), c, r, o);
-  sph.center[k] = make_centre(c[0], c[1], c[2], r, sph.kin ? packed_from_state(own, sph, uint32_t(k), o) : 0u);
+  sph.center[k] = make_double4(c[0], c[1], c[2], double(r));
   if (sph.kin) write_kin_from_state(own, sph, uint32_t(k), o);
 }
 
@@ -844,16 +832,15 @@ __global__ void k_step_begin(Status *st, unsigned long long *tn) {
 
 // launch with programmatic stream serialisation (Ctx::pdl) or plainly
 template <typename... KArgs, typename... Args>
-cudaError_t launch_k(const Ctx *c, void (*kern)(KArgs...), dim3 g, dim3 b, cudaStream_t s, size_t smem,
-                     Args... args) {
+cudaError_t launch_k(const Ctx *c, void (*kern)(KArgs...), dim3 g, dim3 b, cudaStream_t s, Args... args) {
   if (!c->pdl) {
-    kern<<<g, b, smem, s>>>(args...);
+    kern<<<g, b, 0, s>>>(args...);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = g;
   cfg.blockDim = b;
-  cfg.dynamicSmemBytes = smem;
+  cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -905,7 +892,7 @@ int dt_forces_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
   DtView v = dt_view<VelT>(c);
   v.acc_all = a.write_acc;
   if (c->pdl) {
-    GF_CHECK(c, launch_k(c, k_step_begin, dim3(1), dim3(32), s, size_t(0), v.st,
+    GF_CHECK(c, launch_k(c, k_step_begin, dim3(1), dim3(32), s, v.st,
                          v.n_acs ? c->tlist_n.as<unsigned long long>() : (unsigned long long *)nullptr));
   } else {
     GF_CHECK(c, cudaMemsetAsync(&v.st->touching, 0, sizeof(unsigned long long), s));
@@ -939,28 +926,17 @@ int dt_forces_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
       // narrow phase (feeds k_forces below)
       const unsigned long long step = (unsigned long long)a.step;
       const unsigned nsm = unsigned(c->n_sm);
-      if (!c->ss_smem_set) {   // > 48 KB of shared memory per block: opt in (per device)
-        GF_CHECK(c, cudaFuncSetAttribute(k_contacts_ss<1, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(ss_queue_bytes<1>())));
-        GF_CHECK(c, cudaFuncSetAttribute(k_contacts_ss<2, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(ss_queue_bytes<2>())));
-        GF_CHECK(c, cudaFuncSetAttribute(k_contacts_ss<2, 3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(ss_queue_bytes<2>())));
-        GF_CHECK(c, cudaFuncSetAttribute(k_contacts_ss<2, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(ss_queue_bytes<2>())));
-        c->ss_smem_set = true;
-      }
       if (c->ss_split == 2)
-        GF_CHECK(c, launch_k(c, k_contacts_ss<1, 4, false>, dim3(nsm * 4), dim3(256), s, ss_queue_bytes<1>(), v, a.h, step));
+        GF_CHECK(c, launch_k(c, k_contacts_ss<1, 4, false>, dim3(nsm * 4), dim3(256), s, v, a.h, step));
       else if (c->ss_split == 3)
-        GF_CHECK(c, launch_k(c, k_contacts_ss<2, 4, false>, dim3(nsm * 4), dim3(256), s, ss_queue_bytes<2>(), v, a.h, step));
+        GF_CHECK(c, launch_k(c, k_contacts_ss<2, 4, false>, dim3(nsm * 4), dim3(256), s, v, a.h, step));
       else if (!c->ss_red)   // per-word REDs (the round-1 kernel; A/B switch GF_SS_RED=0)
-        GF_CHECK(c, launch_k(c, k_contacts_ss<2, 3, false>, dim3(nsm * 3), dim3(256), s, ss_queue_bytes<2>(), v, a.h, step));
+        GF_CHECK(c, launch_k(c, k_contacts_ss<2, 3, false>, dim3(nsm * 3), dim3(256), s, v, a.h, step));
       else
-        GF_CHECK(c, launch_k(c, k_contacts_ss<2, 3, true>, dim3(nsm * 3), dim3(256), s, ss_queue_bytes<2>(), v, a.h, step));
+        GF_CHECK(c, launch_k(c, k_contacts_ss<2, 3, true>, dim3(nsm * 3), dim3(256), s, v, a.h, step));
       if (ev) cudaEventRecord(ev[4], s);
       ss_timed = true;
-      GF_CHECK(c, launch_k(c, k_touch, dim3(unsigned(c->n_sm) * 4), dim3(256), s, size_t(0), v, list0, list1, tn, step,
+      GF_CHECK(c, launch_k(c, k_touch, dim3(unsigned(c->n_sm) * 4), dim3(256), s, v, list0, list1, tn, step,
                            (const unsigned long long *)(v.seg + c->n_sph)));
     } else if (c->user_model && std::is_same<VelT, float>::value && v.sph.kin && c->user_fn_ss) {
       // user model, throughput build: the NVRTC sphere-sphere loop counts its
@@ -973,7 +949,7 @@ int dt_forces_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
     if (c->user_model) {
       if (launch_user_forces(c, v, a.h, a.sim_time, s)) return -1;
     } else {
-      GF_CHECK(c, launch_k(c, k_forces<VelT>, dim3(unsigned(c->n_sm) * 8), dim3(128), s, size_t(0), v, a.h, a.sim_time,
+      GF_CHECK(c, launch_k(c, k_forces<VelT>, dim3(unsigned(c->n_sm) * 8), dim3(128), s, v, a.h, a.sim_time,
                            (const uint32_t *)list0, (const uint32_t *)list1, (const unsigned long long *)tn,
                            fused ? 1 : 0));
     }
@@ -1001,7 +977,7 @@ int dt_integrate_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
   if (c->n_owner) {
     unsigned g = unsigned((c->n_owner + 127) / 128);
     // 8 CTAs / SM (64 registers, a few spills) beats 6 at 91 registers
-    GF_CHECK(c, launch_k(c, k_integrate<VelT, 8>, dim3(g), dim3(128), s, size_t(0), v, a.h, a.g[0], a.g[1], a.g[2],
+    GF_CHECK(c, launch_k(c, k_integrate<VelT, 8>, dim3(g), dim3(128), s, v, a.h, a.g[0], a.g[1], a.g[2],
                          a.v_err, (unsigned long long)a.step, a.write_acc));
   }
   if (ev) cudaEventRecord(ev[3], s);

@@ -77,7 +77,7 @@ __global__ void k_owner_centers(Domain dom, Owners own, Spheres sph, const uint3
     float rad;
     uint32_t ow;
     sphere_center(dom, own, sph, k, c, rad, ow);
-    sph.center[k] = make_centre(c[0], c[1], c[2], rad, sph.kin ? packed_from_state(own, sph, k, o) : 0u);
+    sph.center[k] = make_double4(c[0], c[1], c[2], double(rad));
     if (sph.kin) write_kin_from_state(own, sph, k, o);
   }
 }

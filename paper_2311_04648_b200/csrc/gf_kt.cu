@@ -106,7 +106,6 @@ __global__ void __launch_bounds__(256) k_snapshot(Domain dom, Owners own, Sphere
     for (int j = 0; j < 2; ++j) {
       const int64_t k = kk[j];
       if (k >= sph.n) continue;
-      c[j].w = double(centre_r(c[j]));   // the snapshot record: (centre, radius) in fp64
       c4[k] = c[j];
       sfam[k] = uint8_t(meta_family(own.meta[ow[j]]));
       if (mm) {
