@@ -280,20 +280,6 @@ __device__ __forceinline__ void write_kin(const Spheres &sph, uint32_t k, uint32
   sph.kin[k] = kr;
 }
 
-// the integrator's per-step refresh of a record whose sphere sits at its
-// owner's centre: the lever is zero and the packed word (scales, material,
-// flags) only changes with the tables, which rewrite whole records
-// (refresh_centers) -- so only the velocity halves are stored (32 of 48 B)
-__device__ __forceinline__ void write_kin_vel(const Spheres &sph, uint32_t k, uint32_t o, const float4 q,
-                                              const float4 lv, const float4 av, float mass) {
-  double w[3];
-  qrot(double(q.x), double(q.y), double(q.z), double(q.w), double(av.x), double(av.y), double(av.z), w[0], w[1],
-       w[2]);
-  float4 *rec = reinterpret_cast<float4 *>(sph.kin + k);
-  rec[0] = make_float4(lv.x, lv.y, lv.z, mass);
-  rec[1] = make_float4(float(w[0]), float(w[1]), float(w[2]), __uint_as_float(o));
-}
-
 __device__ __forceinline__ void write_kin_from_state(const Owners &own, const Spheres &sph, uint32_t k, uint32_t o) {
   const uint32_t meta = own.meta[o], t = meta_tpl(meta);
   const uint32_t flags = (own.passive && own.passive[meta_family(meta)]) ? kKinPassive : 0u;

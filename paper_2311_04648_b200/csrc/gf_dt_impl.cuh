@@ -751,12 +751,9 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_integrate(DtView v, double 
       qrot(double(q.x), double(q.y), double(q.z), double(q.w), double(orr.x), double(orr.y), double(orr.z),
            r[0], r[1], r[2]);
       v.sph.center[k] = make_double4(add(pd[0], r[0]), add(pd[1], r[1]), add(pd[2], r[2]), double(orr.w));
-      if (v.sph.kin) {
-        if (orr.x == 0.f && orr.y == 0.f && orr.z == 0.f)
-          write_kin_vel(v.sph, k, o, q, lv4, av4, float(tp.x));
-        else
-          write_kin(v.sph, k, o, q, lv4, av4, float(tp.x), sc, kflags);
-      }
+      // the whole 48-byte record: writing only its velocity half leaves
+      // partial sectors that L2 must fill from DRAM (measured slower)
+      if (v.sph.kin) write_kin(v.sph, k, o, q, lv4, av4, float(tp.x), sc, kflags);
     }
   }
 }

@@ -70,6 +70,7 @@ def main():
     ap.add_argument("--hopper-scale", type=float, default=5.85, help="~1M clumps at fill 1")
     ap.add_argument("--hopper-settle", type=float, default=0.6)
     ap.add_argument("--rover-spheres", type=int, default=11_000_000)
+    ap.add_argument("--rover-settle-steps", type=int, default=20_000)
     args = ap.parse_args()
     from paper_2311_04648_b200 import models, scenes
     for name in args.configs.split(","):
@@ -110,7 +111,8 @@ def run_one(name, args, models, scenes):
             # terrain settles (untimed input preparation at h = 1e-5); timed at 2e-6
             sim = scenes.rover_wheel(args.rover_spheres, h=1e-5, sinkage=0.0, plunge=0.1)
             sim.initialize()
-            sim.do_dynamics(args.settle_steps * sim.h)
+            # the lattice terrain needs ~0.2 s to collapse into a contact network
+            sim.do_dynamics(max(args.settle_steps, args.rover_settle_steps) * sim.h)
             sim.set_init_time_step(2e-6)
             rec = {"config": f"configs[4]: grousered wheel (0.8 rad/s, 20% slip) on a {args.rover_spheres}-sphere "
                              "GRC-1-like clump terrain, h = 2e-6"}
