@@ -179,14 +179,27 @@ def peaks():
     return 6650.0, "fallback"
 
 
-def profiled_traffic(kernel):
-    """DRAM bytes per launch of `kernel` from the committed ncu summary, if any."""
+def profiled_traffic(kernel, alg_bytes=None):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture
+    (profiles/ncu_traffic.json).  The capture is of the 16M-sphere point of
+    the same sweep (ncu cannot replay the 150M state); with `alg_bytes` the
+    captured traffic / algorithmic-byte ratio is applied to this run's
+    algorithmic bytes per launch.  Returns (bytes, note)."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            return json.load(f).get(kernel)
+            d = json.load(f)
     except (OSError, ValueError):
-        return None
+        return None, "no capture"
+    t = d.get(kernel)
+    ref = d.get("_alg_bytes_" + kernel)
+    if t is None:
+        return None, "no capture"
+    if alg_bytes is None or not ref:
+        return t, "ncu dram bytes per launch of the captured run"
+    ratio = t / ref
+    return ratio * alg_bytes, (f"ncu dram bytes (read + write) of the 16M capture = {ratio:.3f} x its algorithmic "
+                               "bytes, applied to this launch's algorithmic bytes (profiles/ncu_traffic.json)")
 
 
 # ---------------------------------------------------------------------------
@@ -436,6 +449,7 @@ def b200_arm(args):
     bytes_contacts = 24.0 * n_acs_avg + 16.0 * n_touch_avg
     bytes_chain = per_owner * n_free + 4.0 * n_s + bytes_contacts
     ach_c = bytes_contacts / t_ss / 1e9 if t_ss > 0 else 0.0
+    traffic_c, traffic_note = profiled_traffic("k_contacts_ss", bytes_contacts)
     ach_chain = bytes_chain / t_chain / 1e9 if t_chain > 0 else 0.0
 
     # --- e2e: host-buffer round trip per step through the C-ABI ---
@@ -484,8 +498,8 @@ def b200_arm(args):
             "rebuild_amortised": amort,
             "roofline": {"bound": "hbm", "kernel": "k_contacts_ss", "achieved": ach_c, "peak": hbm,
                          "unit": "GB/s", "frac": ach_c / hbm, "peak_kind": hbm_kind,
-                         "traffic": profiled_traffic("k_contacts_ss"),
-                         "traffic_note": "ncu dram bytes per launch, cold cache (profiles/ncu_traffic.json)",
+                         "traffic": traffic_c,
+                         "traffic_note": traffic_note,
                          "algorithmic_bytes_per_launch": bytes_contacts,
                          "launch_ms": t_ss * 1e3},
             "roofline_dt_chain": {"bound": "hbm", "achieved": ach_chain, "peak": hbm, "unit": "GB/s",

@@ -484,6 +484,7 @@ gf_ctx *gf_create(int device, int kt_device, uint32_t flags) {
     cudaEventCreateWithFlags(&c->ev_count, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&c->ev_disp, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&c->ev_kt_join, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->ev_snap_done, cudaEventDisableTiming);
     if (c->kt_device != device) {
       cudaMemPool_t pool;
       if (cudaDeviceGetDefaultMemPool(&pool, c->kt_device) == cudaSuccess) {
@@ -500,6 +501,7 @@ gf_ctx *gf_create(int device, int kt_device, uint32_t flags) {
   if (const char *sr = std::getenv("GF_SS_RED")) c->ss_red = std::atoi(sr);
   if (const char *sp = std::getenv("GF_SS_PF")) c->ss_pf = std::atoi(sp);
   if (const char *sb = std::getenv("GF_SS_BLOCKED")) c->ss_blocked = std::atoi(sb);
+  if (const char *sa = std::getenv("GF_SNAP_ASYNC")) c->snap_async = std::atoi(sa) != 0;
   cudaDeviceGetAttribute(&c->n_sm, cudaDevAttrMultiProcessorCount, device);
   if (c->n_sm <= 0) c->n_sm = 148;
   if (const char *pd = std::getenv("GF_PDL")) c->pdl = std::atoi(pd);
@@ -557,7 +559,8 @@ void gf_destroy(gf_ctx *ctx) {
   for (DBuf *b : bufs) release(*b);
   free_run(c);
   if (c->h_status) cudaFreeHost(c->h_status);
-  cudaEvent_t evs[] = {c->ev_snap, c->ev_ca, c->ev_adopted, c->ev_count, c->ev_disp, c->ev_kt_join, c->t0, c->t1};
+  cudaEvent_t evs[] = {c->ev_snap, c->ev_ca, c->ev_adopted, c->ev_count, c->ev_disp, c->ev_kt_join, c->ev_snap_done,
+                       c->t0, c->t1};
   for (auto e : evs) cudaEventDestroy(e);
   cudaStreamDestroy(c->s_dt);
   cudaStreamDestroy(c->s_kt);
@@ -1317,10 +1320,22 @@ int gf_step_forces(gf_ctx *ctx, int64_t i) {
   // GF_KT_FREEZE=1 (timing diagnostics only): no work orders after the first
   // detection, so a run measures the dT chain alone on a frozen contact array
   if (!c->next_pending && (c->first_adopt || (!R->kt_freeze && s - c->last_snap >= R->period))) {
-    if (kt_snapshot(c, c->s_dt, p->margin)) return -1;
-    GF_CHECK(c, cudaEventRecord(c->ev_snap, c->s_dt));
-    GF_CHECK(c, cudaStreamWaitEvent(c->s_kt, c->ev_snap, 0));
-    GF_CHECK(c, cudaStreamWaitEvent(c->s_kt, c->ev_adopted, 0));
+    if (c->snap_async) {
+      // the snapshot runs on the kT stream, overlapped with this step's force
+      // phase (both only read the state the last integration left); this
+      // step's integration waits for it before overwriting the centres
+      GF_CHECK(c, cudaEventRecord(c->ev_snap, c->s_dt));
+      GF_CHECK(c, cudaStreamWaitEvent(c->s_kt, c->ev_snap, 0));
+      GF_CHECK(c, cudaStreamWaitEvent(c->s_kt, c->ev_adopted, 0));
+      if (kt_snapshot(c, c->s_kt, p->margin)) return -1;
+      GF_CHECK(c, cudaEventRecord(c->ev_snap_done, c->s_kt));
+      c->snap_wait = true;
+    } else {
+      if (kt_snapshot(c, c->s_dt, p->margin)) return -1;
+      GF_CHECK(c, cudaEventRecord(c->ev_snap, c->s_dt));
+      GF_CHECK(c, cudaStreamWaitEvent(c->s_kt, c->ev_snap, 0));
+      GF_CHECK(c, cudaStreamWaitEvent(c->s_kt, c->ev_adopted, 0));
+    }
     // retire completed detections' timing events (every one but the newest
     // has been adopted, so its end event is recorded), then reuse a pair
     while (R->kt_ev.size() > 1 || (!R->kt_ev.empty() && cudaEventQuery(R->kt_ev.front().second) == cudaSuccess)) {
@@ -1378,6 +1393,10 @@ int gf_step_integrate(gf_ctx *ctx, int64_t i) {
   RunState *R = c->run;
   if (!R) { c->err = "gf_step_integrate outside gf_run_begin / gf_run_end"; return -1; }
   const StepArgs a = step_args(R, i);
+  if (c->snap_wait) {   // the kT stream's snapshot of this step's start state
+    GF_CHECK(c, cudaStreamWaitEvent(c->s_dt, c->ev_snap_done, 0));
+    c->snap_wait = false;
+  }
   if (c->f32_state ? dt_integrate_f32(c, a, c->s_dt) : dt_integrate_f64(c, a, c->s_dt)) return -1;
   trace_mark(c, "dt_integrate_end", a.step, c->s_dt);
   // the detection's candidate filter is queued once the dT step is in flight
