@@ -125,7 +125,7 @@ struct Ctx {
   bool split = false;
   cudaEvent_t ev_kt_join = nullptr;   // recorded on s_kt (kT device) at the end of a run
   cudaEvent_t ev_snap_done = nullptr; // the kT-stream snapshot of a step's start state is complete
-  bool snap_async = true;   // snapshot on the kT stream, overlapped with the force phase (GF_SNAP_ASYNC=0: dT)
+  bool snap_async = false;  // snapshot on the kT stream (GF_SNAP_ASYNC=1); measured neutral: the force kernels fill every SM
   bool snap_wait = false;   // the next integration waits for ev_snap_done
   uint32_t flags = 0;
   bool f32_state = false;

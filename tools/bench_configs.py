@@ -108,8 +108,8 @@ def run_one(name, args, models, scenes):
                              f"{n_clumps} five-sphere WC cylinder clumps, discharging through the orifice"}
         elif name == "rover":
             # the wheel starts on the terrain top and sinks at 0.1 m/s while the
-            # terrain settles (untimed input preparation at h = 1e-5); timed at 2e-6
-            sim = scenes.rover_wheel(args.rover_spheres, h=1e-5, sinkage=0.0, plunge=0.1)
+            # terrain settles (untimed input preparation at h = 4e-6); timed at 2e-6
+            sim = scenes.rover_wheel(args.rover_spheres, h=4e-6, sinkage=0.0, plunge=0.1, v_err=8.0)
             sim.initialize()
             # the lattice terrain needs ~0.2 s to collapse into a contact network
             sim.do_dynamics(max(args.settle_steps, args.rover_settle_steps) * sim.h)
