@@ -299,15 +299,37 @@ static int run_count(Ctx *c) {
   const auto h0 = std::chrono::steady_clock::now();
   GF_CHECK(c, cudaEventSynchronize(c->ev_disp));
   if (c->run) c->run->host_wait_ms[0] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
-  if (kt_count(c, c->s_kt)) return -1;
+  const int rc = kt_count_async(c, c->s_kt);
+  if (rc < 0) return -1;
   GF_CHECK(c, cudaEventRecord(c->ev_count, c->s_kt));
+  if (rc == 1) {   // a staged candidate rebuild: resumed by advance_kt
+    c->kt_phase = 3;
+    return 0;
+  }
   trace_mark(c, "kt_count_end", c->last_snap, c->s_kt);
   c->kt_phase = 2;
   return 0;
 }
 
+// resume a staged rebuild (phase 3) as far as its device counts allow;
+// block = wait for each (the fill needs the result now)
+static int advance_kt(Ctx *c, bool block) {
+  const auto h0 = std::chrono::steady_clock::now();
+  const int rc = kt_advance(c, c->s_kt, c->ev_count, block);
+  if (block && c->run)
+    c->run->host_wait_ms[0] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+  if (rc < 0) return -1;
+  if (rc == 0) {
+    GF_CHECK(c, cudaEventRecord(c->ev_count, c->s_kt));
+    trace_mark(c, "kt_count_end", c->last_snap, c->s_kt);
+    c->kt_phase = 2;
+  }
+  return 0;
+}
+
 static int run_fill(Ctx *c) {
   if (c->kt_phase == 1 && run_count(c)) return -1;
+  if (c->kt_phase == 3 && advance_kt(c, true)) return -1;
   const auto h0 = std::chrono::steady_clock::now();
   GF_CHECK(c, cudaEventSynchronize(c->ev_count));
   if (c->run) c->run->host_wait_ms[1] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
@@ -502,6 +524,7 @@ gf_ctx *gf_create(int device, int kt_device, uint32_t flags) {
   if (const char *sp = std::getenv("GF_SS_PF")) c->ss_pf = std::atoi(sp);
   if (const char *sb = std::getenv("GF_SS_BLOCKED")) c->ss_blocked = std::atoi(sb);
   if (const char *sa = std::getenv("GF_SNAP_ASYNC")) c->snap_async = std::atoi(sa) != 0;
+  if (const char *ra = std::getenv("GF_RB_ASYNC")) c->rb_async = std::atoi(ra) != 0;
   cudaDeviceGetAttribute(&c->n_sm, cudaDevAttrMultiProcessorCount, device);
   if (c->n_sm <= 0) c->n_sm = 148;
   if (const char *pd = std::getenv("GF_PDL")) c->pdl = std::atoi(pd);
@@ -1370,7 +1393,9 @@ int gf_step_forces(gf_ctx *ctx, int64_t i) {
     c->adopt_at = c->first_adopt ? s : s + R->lag;
     if (c->adopt_at <= s && run_adopt(c)) return -1;
   }
-  // 3. launch the fill as soon as the count is known (no dT stall)
+  // 3. advance a staged rebuild; launch the fill as soon as the count is
+  // known (no dT stall)
+  if (c->next_pending && c->kt_phase == 3 && advance_kt(c, false)) return -1;
   if (c->next_pending && !c->fill_done && c->kt_phase == 2) {
     cudaError_t q = cudaEventQuery(c->ev_count);
     if (q == cudaErrorNotReady) {
@@ -1401,6 +1426,7 @@ int gf_step_integrate(gf_ctx *ctx, int64_t i) {
   trace_mark(c, "dt_integrate_end", a.step, c->s_dt);
   // the detection's candidate filter is queued once the dT step is in flight
   if (c->next_pending && c->kt_phase == 1 && run_count(c)) return -1;
+  if (c->next_pending && c->kt_phase == 3 && advance_kt(c, false)) return -1;
   return 0;
 }
 

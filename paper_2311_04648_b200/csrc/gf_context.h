@@ -84,6 +84,11 @@ struct KtScratch {
   int64_t tmp_cap = 0;
   DBuf tri_cursor;   // uint32 per cell
   DBuf gaps;         // long runs of segment starts filled by k_fill_gaps
+  // a staged candidate rebuild in flight (gf_kt.cu rb_stage_*): next stage
+  // 1..3, 0 = none; its small-pair count and big-pair capacity
+  int rb_stage = 0;
+  int64_t rb_small = 0, rb_big_cap = 0;
+  bool rb_sa = false;
   DBuf counts;       // uint64[3*n_s+1] per sphere SS / ST / SA counts
   DBuf offsets;      // uint64? uint32[3*n_s+1] exclusive scan
   DBuf cub_tmp;
@@ -125,6 +130,7 @@ struct Ctx {
   bool split = false;
   cudaEvent_t ev_kt_join = nullptr;   // recorded on s_kt (kT device) at the end of a run
   cudaEvent_t ev_snap_done = nullptr; // the kT-stream snapshot of a step's start state is complete
+  bool rb_async = true;     // staged non-blocking candidate rebuild inside runs (GF_RB_ASYNC=0: blocking)
   bool snap_async = false;  // snapshot on the kT stream (GF_SNAP_ASYNC=1); measured neutral: the force kernels fill every SM
   bool snap_wait = false;   // the next integration waits for ev_snap_done
   uint32_t flags = 0;
@@ -132,7 +138,7 @@ struct Ctx {
   std::string err;
   cudaStream_t s_dt = nullptr, s_kt = nullptr;
   cudaEvent_t ev_snap = nullptr, ev_ca = nullptr, ev_adopted = nullptr, ev_count = nullptr, ev_disp = nullptr;
-  int kt_phase = 0;  // in-flight detection: 1 begun, 2 counted
+  int kt_phase = 0;  // in-flight detection: 1 begun, 2 counted, 3 staged rebuild in flight
   cudaEvent_t t0 = nullptr, t1 = nullptr;
 
   Domain dom{};
@@ -280,6 +286,8 @@ int kt_snapshot(Ctx *c, cudaStream_t s, double margin = -1.0);   // centers/fami
                                                           // (margin >= 0: a detection's, with grid inputs)
 int kt_begin(Ctx *c, double margin, cudaStream_t s);               // grid + displacement check
 int kt_count(Ctx *c, cudaStream_t s, bool force_rebuild = false);   // candidates -> counts
+int kt_count_async(Ctx *c, cudaStream_t s);   // 1 = a staged rebuild started (resume with kt_advance)
+int kt_advance(Ctx *c, cudaStream_t s, cudaEvent_t ev, bool block);   // 1 = stages remain
 int kt_detect_fill(Ctx *c, Acs &out, cudaStream_t s);
 int kt_bin_ranges(Ctx *c, double margin, int64_t *h_out);
 int adopt_acs(Ctx *c, cudaStream_t s);                   // merge history + incidence lists

@@ -1331,14 +1331,23 @@ static int gap_list(Ctx *c, GapList &gl, cudaStream_t s) {
 
 // rebuild the candidate lists from the current snapshot (enumeration grid
 // with reach margin + skin)
-static int rebuild_candidates(Ctx *c, cudaStream_t s) {
-  DevGuard g_kt(stream_device(s));   // the kT device of a 2-GPU split
+// The candidate rebuild in four resumable stages.  Each stage ends where the
+// host needs a device count (to size the next stage's buffers): the count is
+// copied to the pinned status block and an event recorded, and the stage
+// returns.  kt_count_async / kt_advance (gf_context.cu run_count /
+// advance_kt) resume the next stage once the event has completed, between
+// the host's dT step enqueues -- so the dT stream stays fed while a rebuild
+// runs on the kT stream, instead of the host blocking on each count.
+//   A  keys, cell sort, cell bounds, cell-sorted copies, small-pair count + scan
+//   B  small-pair fill, big-sphere pairs (count -> host)
+//   C  sort by a, unpack, segment sorts, reference centres; sphere-analytic
+//      candidate count (-> host)
+//   D  sphere-analytic fill, scratch release, bookkeeping
+static int rb_stage_a(Ctx *c, cudaStream_t s) {
   KtScratch &k = c->kt;
   const int64_t n = c->n_sph;
-  const double skin = c->skin_factor * c->kt_margin, skin_b = c->skin_big_factor * c->kt_margin;
+  const double skin = c->skin_factor * c->kt_margin;
   const double reach = c->kt_margin + skin;                         // small-small
-  const double reach_big = c->kt_margin + skin_b;                   // big-small
-  const double reach_bb = c->kt_margin + 2.0 * skin_b - skin;       // big-big
   if (ensure_scratch(c, k.bin_key, 4 * (n + 1), s) || ensure_scratch(c, k.bin_key_alt, 4 * (n + 1), s) ||
       ensure_scratch(c, k.sph_val, 4 * (n + 1), s) || ensure_scratch(c, k.sph_val_alt, 4 * (n + 1), s) ||
       ensure(c, k.cursor, 4 * (3 * n + 1), s) || ensure_scratch(c, k.sc, 32 * (n + 1), s) ||
@@ -1355,12 +1364,11 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
   }
   if (ensure_scratch(c, k.cand_tmp, sizeof(uint2) * k.cand_cap, s)) return -1;   // released after big rebuilds
   const Grid *gp = k.grid.as<Grid>();
-  KtView v = kt_view(c, c->kt_margin);
   if (ensure(c, k.counts, sizeof(unsigned long long) * (3 * n + 1), s)) return -1;
   uint32_t *ucnt = k.cand_cnt.as<uint32_t>();          // per cell-sorted sphere: its hits
   unsigned long long *uoff = k.counts.as<unsigned long long>();   // their exclusive scan (scratch here)
-  unsigned long long *big_n = k.cand_n.as<unsigned long long>();
-  int64_t small = 0;
+  Status *hs = reinterpret_cast<Status *>(c->h_status);
+  hs->cand_total = 0;
   if (n) {
     k_bin_keys<<<grid_for(n), kBlock, 0, s>>>(n, k.c4.as<double>(), c->sph_offr.as<float4>(), gp,
                                              k.bin_key.as<uint32_t>(), k.sph_val.as<uint32_t>());
@@ -1374,7 +1382,7 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
       std::swap(k.bin_key, k.bin_key_alt);
       std::swap(k.sph_val, k.sph_val_alt);
     }
-    v = kt_view(c, c->kt_margin);
+    KtView v = kt_view(c, c->kt_margin);
     k_fill_u32<<<592, 256, 0, s>>>(gp, k.cell_start.as<uint32_t>(), 0xFFFFFFFFu, 0);
     k_cell_bounds<<<grid_for(n), kBlock, 0, s>>>(n, k.bin_key.as<uint32_t>(), k.cell_start.as<uint32_t>(),
                                                 k.cell_end.as<uint32_t>());
@@ -1389,45 +1397,59 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
     cub::DeviceScan::ExclusiveSum(nullptr, tmp, ucnt, uoff, int(n + 1), s);
     if (ensure(c, k.cub_tmp, tmp + 16, s, false)) return -1;
     GF_CHECK(c, cub::DeviceScan::ExclusiveSum(k.cub_tmp.p, tmp, ucnt, uoff, int(n + 1), s));
-    GF_CHECK(c, cudaMemcpyAsync(&reinterpret_cast<Status *>(c->h_status)->cand_total, uoff + n, 8,
-                                cudaMemcpyDeviceToHost, s));
-    GF_CHECK(c, cudaStreamSynchronize(s));
-    small = int64_t(reinterpret_cast<Status *>(c->h_status)->cand_total);
+    GF_CHECK(c, cudaMemcpyAsync(&hs->cand_total, uoff + n, 8, cudaMemcpyDeviceToHost, s));
   }
-  // room for the small-sphere hits plus the big spheres' (grown and redone on
-  // overflow); the key sort needs a second buffer of the same size
-  int64_t big_cap = k.big_cap > 0 ? k.big_cap : (c->n_big ? std::max<int64_t>(4096 * c->n_big, 65536) : 0);
-  for (;;) {
-    const int64_t need = small + big_cap + 1;
-    if (need > k.cand_cap) {
-      const int64_t cap = need + need / 10 + 4096;
-      if (ensure_scratch(c, k.cand_tmp, sizeof(uint2) * cap, s) || ensure(c, k.cand, sizeof(uint2) * cap, s)) return -1;
-      k.cand_cap = cap;
-    }
-    // (a, b) halves of cand_tmp; cand holds the sort's alternate halves
-    uint32_t *ka = k.cand_tmp.as<uint32_t>(), *kb = ka + k.cand_cap;
-    if (n)
-      k_cand_ss<true><<<grid_for(n, 128), 128, 0, s>>>(v, k.sm.as<uint4>(), k.sf.as<float4>(), reach, nullptr,
-                                                       uoff, ka, kb);
-    int64_t nbig = 0;
-    if (c->n_big) {
-      GF_CHECK(c, cudaMemsetAsync(big_n, 0, 8, s));
-      k_cand_big<<<unsigned(std::min<int64_t>(c->n_big, 4096)), 128, 0, s>>>(
-          v, c->big_slots.as<uint32_t>(), c->n_big, k.sc.as<double4>(), k.sm.as<uint4>(), reach_big,
-          reach_bb, ka + small, kb + small, big_n, (unsigned long long)big_cap);
-      unsigned long long h = 0;
-      GF_CHECK(c, cudaMemcpyAsync(&h, big_n, 8, cudaMemcpyDeviceToHost, s));
-      GF_CHECK(c, cudaStreamSynchronize(s));
-      nbig = int64_t(h);
-    }
-    if (nbig <= big_cap) {
-      k.n_cand = small + nbig;
-      break;
-    }
-    big_cap = nbig + nbig / 4 + 4096;   // the big spheres' pass overflowed: grow, redo the fill
+  k.rb_big_cap = k.big_cap > 0 ? k.big_cap : (c->n_big ? std::max<int64_t>(4096 * c->n_big, 65536) : 0);
+  return 0;
+}
+
+static int rb_stage_b(Ctx *c, cudaStream_t s) {
+  KtScratch &k = c->kt;
+  const int64_t n = c->n_sph;
+  const double skin = c->skin_factor * c->kt_margin, skin_b = c->skin_big_factor * c->kt_margin;
+  const double reach = c->kt_margin + skin, reach_big = c->kt_margin + skin_b;
+  const double reach_bb = c->kt_margin + 2.0 * skin_b - skin;       // big-big
+  const int64_t small = int64_t(reinterpret_cast<Status *>(c->h_status)->cand_total);
+  k.rb_small = small;
+  const int64_t need = small + k.rb_big_cap + 1;
+  if (need > k.cand_cap) {
+    const int64_t cap = need + need / 10 + 4096;
+    if (ensure_scratch(c, k.cand_tmp, sizeof(uint2) * cap, s) || ensure(c, k.cand, sizeof(uint2) * cap, s)) return -1;
+    k.cand_cap = cap;
   }
-  k.big_cap = big_cap;
+  // (a, b) halves of cand_tmp; cand holds the sort's alternate halves
+  uint32_t *ka = k.cand_tmp.as<uint32_t>(), *kb = ka + k.cand_cap;
+  KtView v = kt_view(c, c->kt_margin);
+  if (n)
+    k_cand_ss<true><<<grid_for(n, 128), 128, 0, s>>>(v, k.sm.as<uint4>(), k.sf.as<float4>(), reach, nullptr,
+                                                     k.counts.as<unsigned long long>(), ka, kb);
+  unsigned long long *big_n = k.cand_n.as<unsigned long long>();
+  GF_CHECK(c, cudaMemsetAsync(big_n, 0, 8, s));
+  if (c->n_big)
+    k_cand_big<<<unsigned(std::min<int64_t>(c->n_big, 4096)), 128, 0, s>>>(
+        v, c->big_slots.as<uint32_t>(), c->n_big, k.sc.as<double4>(), k.sm.as<uint4>(), reach_big, reach_bb,
+        ka + small, kb + small, big_n, (unsigned long long)k.rb_big_cap);
+  GF_CHECK(c, cudaMemcpyAsync(&reinterpret_cast<Status *>(c->h_status)->other_total, big_n, 8,
+                              cudaMemcpyDeviceToHost, s));
+  return 0;
+}
+
+// returns 1 when the big-sphere pass overflowed (stage B must be redone with
+// the grown capacity)
+static int rb_stage_c(Ctx *c, cudaStream_t s) {
+  KtScratch &k = c->kt;
+  const int64_t n = c->n_sph;
+  const double skin = c->skin_factor * c->kt_margin, skin_b = c->skin_big_factor * c->kt_margin;
+  const double reach = c->kt_margin + skin, reach_big = c->kt_margin + skin_b;
+  const int64_t nbig = int64_t(reinterpret_cast<Status *>(c->h_status)->other_total);
+  if (nbig > k.rb_big_cap) {
+    k.rb_big_cap = nbig + nbig / 4 + 4096;
+    return 1;
+  }
+  k.big_cap = k.rb_big_cap;
+  k.n_cand = k.rb_small + nbig;
   const int64_t total = k.n_cand;
+  unsigned long long *big_n = k.cand_n.as<unsigned long long>();
   if (ensure_scratch(c, k.cand_seg, 8 * (n + 1), s)) return -1;
   if (total) {
     // sort by a (only as many bits as slots need; b rides along), then each
@@ -1466,7 +1488,9 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
   if (n) k_copy_ref<<<grid_for(n), kBlock, 0, s>>>(n, k.c4.as<double4>(), k.ref.as<double>());
   // sphere-analytic candidates for the same skin, while the world is static
   k.sa_world_version = ~0ull;
-  if (n && c->n_ana && !c->world_moving) {
+  k.rb_sa = n && c->n_ana && !c->world_moving;
+  if (k.rb_sa) {
+    KtView v = kt_view(c, c->kt_margin);
     if (ensure(c, k.sa_cnt, 4 * (n + 1), s) || ensure(c, k.sa_off, 8 * (n + 1), s)) return -1;
     k_sa_count<<<grid_for(n), kBlock, 0, s>>>(v, reach, reach_big, c->n_big ? c->r_cut : 0.0, k.sa_cnt.as<uint32_t>());
     GF_CHECK(c, cudaMemsetAsync(k.sa_cnt.as<uint32_t>() + n, 0, 4, s));
@@ -1475,11 +1499,21 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
     if (ensure(c, k.cub_tmp, tb + 16, s, false)) return -1;
     GF_CHECK(c, cub::DeviceScan::ExclusiveSum(k.cub_tmp.p, tb, k.sa_cnt.as<uint32_t>(),
                                               k.sa_off.as<unsigned long long>(), int(n + 1), s));
-    unsigned long long h_tot = 0;
-    GF_CHECK(c, cudaMemcpyAsync(&h_tot, k.sa_off.as<unsigned long long>() + n, 8, cudaMemcpyDeviceToHost, s));
-    GF_CHECK(c, cudaStreamSynchronize(s));
-    k.n_sa_cand = int64_t(h_tot);
+    GF_CHECK(c, cudaMemcpyAsync(&reinterpret_cast<Status *>(c->h_status)->other_total,
+                                k.sa_off.as<unsigned long long>() + n, 8, cudaMemcpyDeviceToHost, s));
+  }
+  return 0;
+}
+
+static int rb_stage_d(Ctx *c, cudaStream_t s) {
+  KtScratch &k = c->kt;
+  const int64_t n = c->n_sph;
+  const double skin = c->skin_factor * c->kt_margin, skin_b = c->skin_big_factor * c->kt_margin;
+  const double reach = c->kt_margin + skin, reach_big = c->kt_margin + skin_b;
+  if (k.rb_sa) {
+    k.n_sa_cand = int64_t(reinterpret_cast<Status *>(c->h_status)->other_total);
     if (ensure(c, k.sa_cand, sizeof(uint2) * (k.n_sa_cand + 1), s)) return -1;
+    KtView v = kt_view(c, c->kt_margin);
     k_sa_fill<<<grid_for(n), kBlock, 0, s>>>(v, reach, reach_big, c->n_big ? c->r_cut : 0.0,
                                              k.sa_off.as<unsigned long long>(), k.sa_cand.as<uint2>());
     k.sa_world_version = c->world_version;
@@ -1499,6 +1533,78 @@ static int rebuild_candidates(Ctx *c, cudaStream_t s) {
   k.rebuilds++;
   k.cand_gen++;   // candidate rows of earlier arrays no longer apply
   GF_CHECK(c, cudaGetLastError());
+  return 0;
+}
+
+// the whole rebuild, blocking on each count (gf_detect, recounts)
+static int rebuild_candidates(Ctx *c, cudaStream_t s) {
+  DevGuard g_kt(stream_device(s));   // the kT device of a 2-GPU split
+  if (rb_stage_a(c, s)) return -1;
+  for (;;) {
+    GF_CHECK(c, cudaStreamSynchronize(s));
+    if (rb_stage_b(c, s)) return -1;
+    GF_CHECK(c, cudaStreamSynchronize(s));
+    const int rc = rb_stage_c(c, s);
+    if (rc < 0) return -1;
+    if (rc == 0) break;
+  }
+  GF_CHECK(c, cudaStreamSynchronize(s));
+  return rb_stage_d(c, s);
+}
+
+// Non-blocking entry of the count phase: a detection that needs a rebuild
+// starts stage A and returns 1 (the caller resumes with kt_advance); else
+// the filter / compaction is queued and 0 returned.
+int kt_count_async(Ctx *c, cudaStream_t s) {
+  DevGuard g_kt(stream_device(s));
+  KtScratch &k = c->kt;
+  Status *hs = reinterpret_cast<Status *>(c->h_status);
+  if (c->rb_async && (!k.cand_valid || hs->rebuild)) {
+    hs->cand_total = 0;
+    hs->rebuild = 0;   // consumed
+    if (rb_stage_a(c, s)) return -1;
+    k.rb_stage = 1;
+    return 1;
+  }
+  return kt_count(c, s, false);
+}
+
+// Resume a staged rebuild once its pending count is on the host (block =
+// wait for it): returns 1 while stages remain, 0 when the rebuild finished
+// and the detection's filter / compaction is queued.
+int kt_advance(Ctx *c, cudaStream_t s, cudaEvent_t ev, bool block) {
+  DevGuard g_kt(stream_device(s));
+  KtScratch &k = c->kt;
+  while (k.rb_stage > 0) {
+    if (block) {
+      GF_CHECK(c, cudaEventSynchronize(ev));
+    } else {
+      const cudaError_t q = cudaEventQuery(ev);
+      if (q == cudaErrorNotReady) {
+        (void)cudaGetLastError();
+        return 1;
+      }
+      GF_CHECK(c, q);
+    }
+    if (k.rb_stage == 1) {
+      if (rb_stage_b(c, s)) return -1;
+      k.rb_stage = 2;
+    } else if (k.rb_stage == 2) {
+      const int rc = rb_stage_c(c, s);
+      if (rc < 0) return -1;
+      if (rc == 1) {   // big pass overflowed: redo stage B with the grown capacity
+        if (rb_stage_b(c, s)) return -1;
+        k.rb_stage = 2;
+      } else {
+        k.rb_stage = 3;
+      }
+    } else {
+      if (rb_stage_d(c, s)) return -1;
+      k.rb_stage = 0;
+      return kt_count(c, s, false) ? -1 : 0;
+    }
+    GF_CHECK(c, cudaEventRecord(ev, s));
+  }
   return 0;
 }
 
