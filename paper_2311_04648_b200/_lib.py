@@ -15,7 +15,8 @@ import subprocess
 import numpy as np
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libgf_b200.so")
+# GF_LIB: an alternative build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("GF_LIB") or os.path.join(PKG_DIR, "libgf_b200.so")
 CSRC_DIR = os.path.join(PKG_DIR, "csrc")  # gf_device.cuh for NVRTC user models
 
 GF_STATE_F32 = 1

@@ -845,7 +845,10 @@ constexpr int kFcBlock = 256;
 // kFcPer candidates per thread (item q of lane l in warp w is candidate
 // block_base + w * 32 * kFcPer + q * 32 + l: one bitmask word per (warp, q))
 // so their record gathers are in flight together
-constexpr int kFcPer = 2;
+#ifndef GF_FC_PER
+#define GF_FC_PER 2
+#endif
+constexpr int kFcPer = GF_FC_PER;
 constexpr int kFcSpan = kFcBlock * kFcPer;   // candidates per filter block
 
 __global__ void __launch_bounds__(kFcBlock) k_filter_bits(KtView v, const uint2 *cand, int64_t n_cand,
@@ -962,6 +965,7 @@ __global__ void __launch_bounds__(kFcBlock) k_compact(KtView v, const uint2 *can
       if (a + 1 <= v.sph.n) seg_fill(seg, a + 1, v.sph.n, p + (hit ? 1 : 0), gl);
   }
 }
+
 
 __global__ void k_copy_ref(int64_t n, const double4 *c4, double *ref) {
   int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
