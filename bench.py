@@ -479,7 +479,13 @@ def b200_arm(args):
         if mode == "decomp":   # halo: pack/add forces, pack/unpack(+centres) state per peer; guard word x2
             launches_per_step += 2 + 5 * len(sim._dd.peers)
         period, lag, _ = schedule(sim)
-        kt_launches = 14   # snapshot, grid, filter, compaction, scans, wall pairs, fill, history gather
+        # per detection: snapshot, min/max init, grid, family geometry, filter, 2 scans + inits,
+        # compaction, gap fill, wall pairs, place, segment sort, flag reset, history gather (16);
+        # per candidate rebuild ~45 (cell sort, candidate count/fill, pair sort passes, segment
+        # sorts, sphere-analytic candidates) -- the ncu launch list of the timed steps
+        # (profiles/r2/launches_150m_with_rebuilds.csv: 1290 launches in 100 steps, 2 rebuilds)
+        kt_launches = 16
+        rb_launches = 45 * (int(rr.kt_rebuilds) - rebuilds0)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": (args.gpus if mode == "ktdt" else world),
             "steps": args.steps,
@@ -513,7 +519,8 @@ def b200_arm(args):
                                    "kT_per_cycle": times[3] / max(1, int(steps_prof) // max(1, period))},
             "clocks": clocks.summary(),
             "e2e": e2e,
-            "gpu_launches": int(args.steps * launches_per_step + (args.steps // max(1, period)) * kt_launches),
+            "gpu_launches": int(args.steps * launches_per_step + (args.steps // max(1, period)) * kt_launches
+                                + rb_launches),
             "cpu_baseline": cpu,
         }
     sim.close()

@@ -525,6 +525,7 @@ gf_ctx *gf_create(int device, int kt_device, uint32_t flags) {
   if (const char *sb = std::getenv("GF_SS_BLOCKED")) c->ss_blocked = std::atoi(sb);
   if (const char *sa = std::getenv("GF_SNAP_ASYNC")) c->snap_async = std::atoi(sa) != 0;
   if (const char *ra = std::getenv("GF_RB_ASYNC")) c->rb_async = std::atoi(ra) != 0;
+  if (const char *rs = std::getenv("GF_RB_SLOT")) c->rb_slot = std::atoi(rs) != 0;
   cudaDeviceGetAttribute(&c->n_sm, cudaDevAttrMultiProcessorCount, device);
   if (c->n_sm <= 0) c->n_sm = 148;
   if (const char *pd = std::getenv("GF_PDL")) c->pdl = std::atoi(pd);
@@ -578,7 +579,7 @@ void gf_destroy(gf_ctx *ctx) {
                   &c->kt.tri_start, &c->kt.tri_entries, &c->kt.counts, &c->kt.offsets, &c->kt.cub_tmp,
                   &c->kt.total, &c->kt.cursor, &c->kt.tri_cursor, &c->big_slots, &c->kt.sc,
                   &c->kt.sm, &c->kt.sf, &c->kt.cells, &c->kt.n_cells, &c->kt.cand, &c->kt.cand_tmp, &c->kt.cand_n,
-                  &c->kt.cand_cnt, &c->kt.cand_seg, &c->kt.ref, &c->kt.flag, &c->kt.cflags, &c->kt.sel_n, &c->kt.tmp, &c->kt.tmp_n, &c->acs.seg, &c->acs_next.seg, &c->acs.old_pos, &c->acs_next.old_pos, &c->kt.fbits[0], &c->kt.fbits[1], &c->kt.fpre[0], &c->kt.fpre[1], &c->kt.fcnt, &c->dd, &c->dd_x0, &c->halo_scratch, &c->owner_stage, &c->kt.sa_cnt, &c->kt.sa_off, &c->kt.sa_cand, &c->kt.gaps};
+                  &c->kt.cand_cnt, &c->kt.cand_own, &c->kt.cand_seg, &c->kt.ref, &c->kt.flag, &c->kt.cflags, &c->kt.sel_n, &c->kt.tmp, &c->kt.tmp_n, &c->acs.seg, &c->acs_next.seg, &c->acs.old_pos, &c->acs_next.old_pos, &c->kt.fbits[0], &c->kt.fbits[1], &c->kt.fpre[0], &c->kt.fpre[1], &c->kt.fcnt, &c->dd, &c->dd_x0, &c->halo_scratch, &c->owner_stage, &c->kt.sa_cnt, &c->kt.sa_off, &c->kt.sa_cand, &c->kt.gaps};
   for (DBuf *b : bufs) release(*b);
   free_run(c);
   if (c->h_status) cudaFreeHost(c->h_status);

@@ -62,6 +62,7 @@ struct KtScratch {
   DBuf cells, n_cells;  // non-empty enumeration cells
   // Verlet candidate lists (rebuilt when a sphere moved > skin / 2)
   DBuf cand, cand_tmp, cand_n, cand_cnt, cand_seg, ref, flag, cflags, sel_n;
+  DBuf cand_own;     // slot-grouped rebuild: each cell-sorted sphere's own-slot pair count
   int64_t cand_cap = 0, n_cand = 0, rebuilds = 0, big_cap = 0;
   // hit bitmask and scanned per-block hit counts of the last two filtered
   // arrays (double-buffered), with the detection serial / candidate
@@ -130,6 +131,7 @@ struct Ctx {
   bool split = false;
   cudaEvent_t ev_kt_join = nullptr;   // recorded on s_kt (kT device) at the end of a run
   cudaEvent_t ev_snap_done = nullptr; // the kT-stream snapshot of a step's start state is complete
+  bool rb_slot = true;      // candidate rebuild grouped by slot with atomic cursors (GF_RB_SLOT=0: pair radix sort)
   bool rb_async = true;     // staged non-blocking candidate rebuild inside runs (GF_RB_ASYNC=0: blocking)
   bool snap_async = false;  // snapshot on the kT stream (GF_SNAP_ASYNC=1); measured neutral: the force kernels fill every SM
   bool snap_wait = false;   // the next integration waits for ev_snap_done

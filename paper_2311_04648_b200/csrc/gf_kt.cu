@@ -778,6 +778,141 @@ __global__ void __launch_bounds__(128) k_cand_big(KtView v, const uint32_t *bigs
   }
 }
 
+// The same pairs grouped by their lower slot without a pair sort (the
+// default rebuild, Ctx::rb_slot).  kFill = false counts every slot's pairs:
+// hits whose lower slot is the thread's own sphere are summed in a register
+// (kept per thread in `own`), the others add one to the partner's counter.
+// After an exclusive scan over slots (the segment starts), kFill = true
+// reserves the thread's own run with one atomic on its slot's cursor and
+// places every other hit at its partner's segment start + that slot's
+// cursor.  The order inside a segment is the per-segment sort by b's.
+template <bool kFill>
+__global__ void __launch_bounds__(128) k_cand_slot(KtView v, const uint4 *sm, const float4 *sf, double reach_m,
+                                                   uint32_t *scnt, uint32_t *own, const unsigned long long *seg,
+                                                   uint32_t *cursor, uint2 *cand) {
+  int64_t u64 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (u64 >= v.sph.n) return;
+  const Grid g = *v.grid;
+  bool active = g.valid;
+  uint32_t key = active ? v.bin_key[u64] : kNoCell;
+  active = active && key != kNoCell;
+  const float ext = float(double(max(g.nc[0], max(g.nc[1], g.nc[2]))) / g.inv_cell);
+  const float slack = 1e-6f * ext + 1e-30f;
+  const float marg = float(reach_m);
+  uint32_t mine = 0;
+  unsigned long long w_own = 0;
+  if (active) {
+    const float4 f0 = sf[u64];
+    const uint4 m0 = sm[u64];
+    if (kFill) {
+      const uint32_t n_own = own[u64];
+      if (n_own) w_own = seg[m0.x] + atomicAdd(cursor + m0.x, n_own);
+    }
+    const long long cx = key % g.nc[0], cy = (key / g.nc[0]) % g.nc[1], cz = key / (g.nc[0] * g.nc[1]);
+    for (int span = 0; span < 6; ++span) {
+      uint32_t s0 = 0, s1 = 0;
+      if (span == 0) {
+        s0 = uint32_t(u64) + 1;
+        s1 = v.cell_end[key];
+      } else {
+        long long dz = span >= 3 ? 1 : 0;
+        long long dy = span == 2 ? 1 : (span >= 3 ? span - 4 : 0);
+        long long x0 = span == 1 ? cx + 1 : cx - 1, x1 = cx + 1;
+        long long y = cy + dy, z = cz + dz;
+        if (x0 < 0) x0 = 0;
+        if (x1 >= g.nc[0]) x1 = g.nc[0] - 1;
+        if (y >= 0 && y < g.nc[1] && z < g.nc[2] && x0 <= x1) {
+          long long row = (z * g.nc[1] + y) * g.nc[0];
+          uint32_t a0 = 0xFFFFFFFFu;
+          for (long long x = x0; x <= x1; ++x) {
+            uint32_t st = v.cell_start[row + x];
+            if (st == 0xFFFFFFFFu) continue;
+            if (a0 == 0xFFFFFFFFu) a0 = st;
+            s1 = v.cell_end[row + x];
+          }
+          s0 = a0 == 0xFFFFFFFFu ? 0 : a0;
+          if (a0 == 0xFFFFFFFFu) s1 = 0;
+        }
+      }
+      for (uint32_t w = s0; w < s1; ++w) {
+        const float4 f1 = sf[w];
+        const float dx = f0.x - f1.x, dy = f0.y - f1.y, dz = f0.z - f1.z;
+        const float rr = f0.w + f1.w + marg + slack;
+        if (dx * dx + dy * dy + dz * dz < rr * rr * 1.0001f) {
+          const uint4 m1 = sm[w];
+          if (m1.y != m0.y && dd_keep(v.own.dd, m0.y, m1.y)) {
+            if (m0.x < m1.x) {
+              if (kFill) cand[w_own + mine] = make_uint2(m0.x, m1.x);
+              ++mine;
+            } else if (kFill) {
+              cand[seg[m1.x] + atomicAdd(cursor + m1.x, 1u)] = make_uint2(m1.x, m0.x);
+            } else {
+              atomicAdd(scnt + m1.x, 1u);
+            }
+          }
+        }
+      }
+    }
+    if (!kFill && mine) atomicAdd(scnt + m0.x, mine);
+  }
+  if (!kFill) own[u64] = mine;
+}
+
+// big-sphere pairs into the slot-grouped list (k_cand_big's enumeration)
+template <bool kFill>
+__global__ void __launch_bounds__(128) k_cand_big_slot(KtView v, const uint32_t *bigs, int64_t n_big,
+                                                       const double4 *sc, const uint4 *sm, double reach_m,
+                                                       double reach_bb, uint32_t *scnt,
+                                                       const unsigned long long *seg, uint32_t *cursor,
+                                                       uint2 *cand) {
+  const Grid g = *v.grid;
+  if (!g.valid) return;
+  for (int64_t bi = blockIdx.x; bi < n_big; bi += gridDim.x) {
+    const uint32_t B = bigs[bi];
+    const double bx = v.centers[4 * size_t(B)], by = v.centers[4 * size_t(B) + 1], bz = v.centers[4 * size_t(B) + 2];
+    const double rB = double(v.sph.offr[B].w);
+    const uint32_t oB = v.sph.owner[B];
+    const double reach = rB + g.r_cut + reach_m;
+    const double cbv[3] = {bx, by, bz};
+    long long flo[3], fhi[3];
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      flo[ax] = axis_bin(cbv[ax] - reach, g.glo[ax], g.inv_cell, g.nc[ax]);
+      fhi[ax] = axis_bin(cbv[ax] + reach, g.glo[ax], g.inv_cell, g.nc[ax]);
+    }
+    const long long sx = fhi[0] - flo[0] + 1, sy = fhi[1] - flo[1] + 1, sz = fhi[2] - flo[2] + 1;
+    const long long ncell = sx * sy * sz;
+    for (long long q = threadIdx.x; q < ncell; q += blockDim.x) {
+      long long x = flo[0] + q % sx, y = flo[1] + (q / sx) % sy, z = flo[2] + q / (sx * sy);
+      long long b = (z * g.nc[1] + y) * g.nc[0] + x;
+      uint32_t s0 = v.cell_start[b];
+      if (s0 == 0xFFFFFFFFu) continue;
+      uint32_t s1 = v.cell_end[b];
+      for (uint32_t w = s0; w < s1; ++w) {
+        const double4 c1 = sc[w];
+        const uint4 m1 = sm[w];
+        if (m1.y == oB || !dd_keep(v.own.dd, m1.y, oB)) continue;
+        const double dx = bx - c1.x, dy = by - c1.y, dz = bz - c1.z;
+        const double rr = rB + c1.w + reach_m;
+        if (dx * dx + dy * dy + dz * dz >= rr * rr * (1.0 + 1e-9)) continue;
+        const uint32_t a = min(m1.x, B), c = max(m1.x, B);
+        if (kFill) cand[seg[a] + atomicAdd(cursor + a, 1u)] = make_uint2(a, c);
+        else atomicAdd(scnt + a, 1u);
+      }
+    }
+    for (int64_t q = threadIdx.x; q < n_big; q += blockDim.x) {
+      const uint32_t j = bigs[q];
+      if (j <= B || v.sph.owner[j] == oB || !dd_keep(v.own.dd, v.sph.owner[j], oB)) continue;
+      const double dx = bx - v.centers[4 * size_t(j)], dy = by - v.centers[4 * size_t(j) + 1],
+                   dz = bz - v.centers[4 * size_t(j) + 2];
+      const double rr = rB + double(v.sph.offr[j].w) + reach_bb;
+      if (dx * dx + dy * dy + dz * dz >= rr * rr * (1.0 + 1e-9)) continue;
+      if (kFill) cand[seg[B] + atomicAdd(cursor + B, 1u)] = make_uint2(B, j);
+      else atomicAdd(scnt + B, 1u);
+    }
+  }
+}
+
 // candidates sorted by a -> the (a, b) list and each sphere's segment start
 // (the spheres in (previous entry's a, this entry's a] start here)
 // Segment-start fills over runs of spheres without entries: a thread fills
@@ -1366,7 +1501,8 @@ static int rb_stage_a(Ctx *c, cudaStream_t s) {
     if (ensure(c, k.cand, sizeof(uint2) * cap, s)) return -1;
     k.cand_cap = cap;
   }
-  if (ensure_scratch(c, k.cand_tmp, sizeof(uint2) * k.cand_cap, s)) return -1;   // released after big rebuilds
+  if (!c->rb_slot && ensure_scratch(c, k.cand_tmp, sizeof(uint2) * k.cand_cap, s))   // released after big rebuilds
+    return -1;
   const Grid *gp = k.grid.as<Grid>();
   if (ensure(c, k.counts, sizeof(unsigned long long) * (3 * n + 1), s)) return -1;
   uint32_t *ucnt = k.cand_cnt.as<uint32_t>();          // per cell-sorted sphere: its hits
@@ -1394,6 +1530,23 @@ static int rb_stage_a(Ctx *c, cudaStream_t s) {
                                                   c->sph_offr.as<float4>(), c->sph_owner.as<uint32_t>(),
                                                   k.sfam.as<uint8_t>(), gp, k.sc.as<double4>(),
                                                   k.sm.as<uint4>(), k.sf.as<float4>());
+    if (c->rb_slot) {   // per-slot pair counts -> segment starts (cand_seg)
+      const double skin_b = c->skin_big_factor * c->kt_margin;
+      if (ensure_scratch(c, k.cand_own, 4 * (n + 1), s) || ensure_scratch(c, k.cand_seg, 8 * (n + 1), s)) return -1;
+      GF_CHECK(c, cudaMemsetAsync(ucnt, 0, 4 * (n + 1), s));
+      k_cand_slot<false><<<grid_for(n, 128), 128, 0, s>>>(v, k.sm.as<uint4>(), k.sf.as<float4>(), reach, ucnt,
+                                                          k.cand_own.as<uint32_t>(), nullptr, nullptr, nullptr);
+      if (c->n_big)
+        k_cand_big_slot<false><<<unsigned(std::min<int64_t>(c->n_big, 4096)), 128, 0, s>>>(
+            v, c->big_slots.as<uint32_t>(), c->n_big, k.sc.as<double4>(), k.sm.as<uint4>(), c->kt_margin + skin_b,
+            c->kt_margin + 2.0 * skin_b - skin, ucnt, nullptr, nullptr, nullptr);
+      unsigned long long *seg = k.cand_seg.as<unsigned long long>();
+      cub::DeviceScan::ExclusiveSum(nullptr, tmp, ucnt, seg, int(n + 1), s);
+      if (ensure(c, k.cub_tmp, tmp + 16, s, false)) return -1;
+      GF_CHECK(c, cub::DeviceScan::ExclusiveSum(k.cub_tmp.p, tmp, ucnt, seg, int(n + 1), s));
+      GF_CHECK(c, cudaMemcpyAsync(&hs->cand_total, seg + n, 8, cudaMemcpyDeviceToHost, s));
+      return 0;
+    }
     // count, scan, fill: every thread writes its own hits at its own offset
     k_cand_ss<false><<<grid_for(n, 128), 128, 0, s>>>(v, k.sm.as<uint4>(), k.sf.as<float4>(), reach, ucnt,
                                                       nullptr, nullptr, nullptr);
@@ -1438,13 +1591,13 @@ static int rb_stage_b(Ctx *c, cudaStream_t s) {
   return 0;
 }
 
+static int rb_lists_tail(Ctx *c, cudaStream_t s);
+
 // returns 1 when the big-sphere pass overflowed (stage B must be redone with
 // the grown capacity)
 static int rb_stage_c(Ctx *c, cudaStream_t s) {
   KtScratch &k = c->kt;
   const int64_t n = c->n_sph;
-  const double skin = c->skin_factor * c->kt_margin, skin_b = c->skin_big_factor * c->kt_margin;
-  const double reach = c->kt_margin + skin, reach_big = c->kt_margin + skin_b;
   const int64_t nbig = int64_t(reinterpret_cast<Status *>(c->h_status)->other_total);
   if (nbig > k.rb_big_cap) {
     k.rb_big_cap = nbig + nbig / 4 + 4096;
@@ -1453,7 +1606,6 @@ static int rb_stage_c(Ctx *c, cudaStream_t s) {
   k.big_cap = k.rb_big_cap;
   k.n_cand = k.rb_small + nbig;
   const int64_t total = k.n_cand;
-  unsigned long long *big_n = k.cand_n.as<unsigned long long>();
   if (ensure_scratch(c, k.cand_seg, 8 * (n + 1), s)) return -1;
   if (total) {
     // sort by a (only as many bits as slots need; b rides along), then each
@@ -1475,6 +1627,20 @@ static int rb_stage_c(Ctx *c, cudaStream_t s) {
     k_cand_unpack<<<unsigned(std::min<int64_t>((total + 255) / 256, int64_t(c->n_sm) * 16)), 256, 0, s>>>(
         total, n, sa, sb, k.cand.as<uint2>(), k.cand_seg.as<unsigned long long>(), gl);
     k_fill_gaps<<<unsigned(c->n_sm) * 4, 256, 0, s>>>(k.cand_seg.as<unsigned long long>(), gl);
+  }
+  return rb_lists_tail(c, s);
+}
+
+// both rebuild variants, once the (a, b) list and its per-sphere segment
+// starts are in place: each segment sorted by b, the reference centres, the
+// sphere-analytic candidate count (-> host)
+static int rb_lists_tail(Ctx *c, cudaStream_t s) {
+  KtScratch &k = c->kt;
+  const int64_t n = c->n_sph;
+  const double skin = c->skin_factor * c->kt_margin, skin_b = c->skin_big_factor * c->kt_margin;
+  const double reach = c->kt_margin + skin, reach_big = c->kt_margin + skin_b;
+  unsigned long long *big_n = k.cand_n.as<unsigned long long>();
+  if (k.n_cand) {
     if (ensure(c, k.sa_cnt, 4 * (n + 1), s)) return -1;   // the long-segment list (scratch here)
     GF_CHECK(c, cudaMemsetAsync(big_n, 0, 8, s));
     k_sort_seg_short<<<grid_for(n), kBlock, 0, s>>>(n, k.cand_seg.as<unsigned long long>(), k.cand.as<uint2>(),
@@ -1509,6 +1675,35 @@ static int rb_stage_c(Ctx *c, cudaStream_t s) {
   return 0;
 }
 
+// slot-grouped rebuild, stage B: the list sized from the total, every pair
+// placed in its lower slot's segment, then the common tail
+static int rb_slot_b(Ctx *c, cudaStream_t s) {
+  KtScratch &k = c->kt;
+  const int64_t n = c->n_sph;
+  const double skin = c->skin_factor * c->kt_margin, skin_b = c->skin_big_factor * c->kt_margin;
+  const int64_t total = int64_t(reinterpret_cast<Status *>(c->h_status)->cand_total);
+  k.n_cand = total;
+  if (total + 1 > k.cand_cap) {
+    const int64_t cap = total + total / 10 + 4096;
+    if (ensure(c, k.cand, sizeof(uint2) * cap, s)) return -1;
+    k.cand_cap = cap;
+  }
+  if (n && total) {
+    KtView v = kt_view(c, c->kt_margin);
+    uint32_t *cur = k.cursor.as<uint32_t>();
+    const unsigned long long *seg = k.cand_seg.as<unsigned long long>();
+    GF_CHECK(c, cudaMemsetAsync(cur, 0, 4 * (n + 1), s));
+    k_cand_slot<true><<<grid_for(n, 128), 128, 0, s>>>(v, k.sm.as<uint4>(), k.sf.as<float4>(), c->kt_margin + skin,
+                                                       nullptr, k.cand_own.as<uint32_t>(), seg, cur,
+                                                       k.cand.as<uint2>());
+    if (c->n_big)
+      k_cand_big_slot<true><<<unsigned(std::min<int64_t>(c->n_big, 4096)), 128, 0, s>>>(
+          v, c->big_slots.as<uint32_t>(), c->n_big, k.sc.as<double4>(), k.sm.as<uint4>(), c->kt_margin + skin_b,
+          c->kt_margin + 2.0 * skin_b - skin, nullptr, seg, cur, k.cand.as<uint2>());
+  }
+  return rb_lists_tail(c, s);
+}
+
 static int rb_stage_d(Ctx *c, cudaStream_t s) {
   KtScratch &k = c->kt;
   const int64_t n = c->n_sph;
@@ -1529,7 +1724,7 @@ static int rb_stage_d(Ctx *c, cudaStream_t s) {
   // synchronisation, so the dT stream never stalls on a rebuild
   if (big_scratch(c)) {
     for (DBuf *b : {&k.bin_key, &k.bin_key_alt, &k.sph_val, &k.sph_val_alt, &k.sc, &k.sm, &k.sf, &k.cand_cnt,
-                    &k.cand_seg, &k.cand_tmp})
+                    &k.cand_seg, &k.cand_tmp, &k.cand_own})
       if (release_scratch(c, *b, s)) return -1;
   }
   k.cand_valid = true;
@@ -1544,6 +1739,12 @@ static int rb_stage_d(Ctx *c, cudaStream_t s) {
 static int rebuild_candidates(Ctx *c, cudaStream_t s) {
   DevGuard g_kt(stream_device(s));   // the kT device of a 2-GPU split
   if (rb_stage_a(c, s)) return -1;
+  if (c->rb_slot) {
+    GF_CHECK(c, cudaStreamSynchronize(s));
+    if (rb_slot_b(c, s)) return -1;
+    GF_CHECK(c, cudaStreamSynchronize(s));
+    return rb_stage_d(c, s);
+  }
   for (;;) {
     GF_CHECK(c, cudaStreamSynchronize(s));
     if (rb_stage_b(c, s)) return -1;
@@ -1590,7 +1791,10 @@ int kt_advance(Ctx *c, cudaStream_t s, cudaEvent_t ev, bool block) {
       }
       GF_CHECK(c, q);
     }
-    if (k.rb_stage == 1) {
+    if (k.rb_stage == 1 && c->rb_slot) {
+      if (rb_slot_b(c, s)) return -1;
+      k.rb_stage = 3;
+    } else if (k.rb_stage == 1) {
       if (rb_stage_b(c, s)) return -1;
       k.rb_stage = 2;
     } else if (k.rb_stage == 2) {

@@ -70,7 +70,7 @@ def main():
     ap.add_argument("--hopper-scale", type=float, default=5.85, help="~1M clumps at fill 1")
     ap.add_argument("--hopper-settle", type=float, default=0.6)
     ap.add_argument("--rover-spheres", type=int, default=11_000_000)
-    ap.add_argument("--rover-settle-steps", type=int, default=20_000)
+    ap.add_argument("--rover-settle-steps", type=int, default=60_000)
     args = ap.parse_args()
     from paper_2311_04648_b200 import models, scenes
     for name in args.configs.split(","):
@@ -107,15 +107,50 @@ def run_one(name, args, models, scenes):
             rec = {"config": f"configs[2]: hopper test 2 scaled x{args.hopper_scale} at fixed particle size, "
                              f"{n_clumps} five-sphere WC cylinder clumps, discharging through the orifice"}
         elif name == "rover":
-            # the wheel starts on the terrain top and sinks at 0.1 m/s while the
-            # terrain settles (untimed input preparation at h = 4e-6); timed at 2e-6
-            sim = scenes.rover_wheel(args.rover_spheres, h=4e-6, sinkage=0.0, plunge=0.1, v_err=8.0)
+            # the terrain settles with the wheel held still just above it
+            # (untimed input preparation at h = 4e-6), the wheel is pushed
+            # down into the settled surface, then rolls: timed at h = 2e-6
+            # (the lattice falls into place: grains with no support below drop up
+            # to ~5 cm and the pile-up throws a few at 2-3 m/s for a moment, so
+            # the settle runs with a loose watchdog; 8 m/s once timed)
+            sim = scenes.rover_wheel(args.rover_spheres, h=4e-6, sinkage=0.0, plunge=0.0, v_err=50.0)
+            fam = scenes.WHEEL_FAMILY
+            sim.set_family_prescribed_lin_vel(fam, 0.0, 0.0, 0.0)
+            sim.set_family_prescribed_ang_vel(fam, 0.0, 0.0, 0.0)
             sim.initialize()
             # the lattice terrain needs ~0.2 s to collapse into a contact network
+            # (60k steps at 4e-6 = 0.24 s)
             sim.do_dynamics(max(args.settle_steps, args.rover_settle_steps) * sim.h)
+            fam_of = sim.store.__dict__["_owner_family"][:sim.store.n_owners]
+            wheel = sim.track(int(np.nonzero(fam_of == fam)[0][0]))
+            # the settled surface sits centimetres below the lattice top the
+            # wheel was placed on: move the wheel down onto it, its lowest
+            # grouser tips 0.2 mm above the highest grain under its footprint
+            cen, rad = sim._sph_centers, np.asarray(sim._sph_radius, np.float64)
+            wp = wheel.pos()
+            foot = (np.abs(cen[:, 0] - wp[0]) < 0.012) & (np.abs(cen[:, 1] - wp[1]) < 0.1)
+            top = float(np.max(cen[foot, 2] + rad[foot]))
+            t_down = float(wp[2] - (top + 0.25 + 0.08 * 0.25 + 2e-4))
+            wheel.set_pos([wp[0], wp[1], wp[2] - t_down])
             sim.set_init_time_step(2e-6)
+            sim.set_error_out_velocity(8.0)
+            # down at 0.2 m/s until the grousers meet the grains (the wheel's
+            # contact force read back on the device, 0.4 mm per check), then
+            # 0.5 mm further while rolling
+            sim.set_family_prescribed_lin_vel(fam, 0.0, 0.0, -0.2)
+            n_down = 0
+            while np.linalg.norm(wheel.contact_force()) == 0.0 and n_down < 50:
+                sim.do_dynamics(0.002)
+                n_down += 1
+            sim.set_family_prescribed_lin_vel(fam, 0.8 * 0.25 * 0.8, 0.0, -0.05)
+            sim.set_family_prescribed_ang_vel(fam, 0.0, 0.8, 0.0)
+            sim.do_dynamics(0.01)
+            sim.set_family_prescribed_lin_vel(fam, 0.8 * 0.25 * 0.8, 0.0, -0.01)
             rec = {"config": f"configs[4]: grousered wheel (0.8 rad/s, 20% slip) on a {args.rover_spheres}-sphere "
                              "GRC-1-like clump terrain, h = 2e-6"}
+            rec["wheel_lowered_m"] = t_down
+            rec["wheel_plunge_checks"] = n_down
+            rec["wheel_force_N_before_timed"] = [float(x) for x in wheel.contact_force()]
         elif name == "clumps":
             sim = scenes.clump_bed(1_000_000)
             sim.initialize()
