@@ -1206,7 +1206,7 @@ __global__ void k_adopt_hist(int64_t n_new, const uint2 *new_ids, const uint32_t
 #pragma unroll
   for (int j = 0; j < kAdoptPer; ++j) {
     const int64_t k = k0 + int64_t(j) * blockDim.x;
-    q[j] = k < n_new ? old_pos[k] : 0xFFFFFFFFu;   // wall rows ignore it
+    q[j] = (k < n_new && (unsigned long long)k < n_ss) ? old_pos[k] : 0xFFFFFFFFu;   // sphere-sphere rows only
   }
   long long hit[kAdoptPer];
 #pragma unroll

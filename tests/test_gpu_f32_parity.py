@@ -313,3 +313,28 @@ def test_crater_window_vs_oracle(n, crr):
     assert rr.touching > n
     check_state(out, ref.s, sc, sc["lin_vel"], sc["ang_vel"], steps=steps, label=f"crater {n} crr {crr}",
                 fmed=ref.last_force_median, crr=crr)
+
+
+# ---------------------------------------------------------------------------
+# the fused kernel's TMA gather4 variant (GF_SS_TMA=1) reads the same centre
+# records through the TMA unit: bitwise the same trajectory
+# ---------------------------------------------------------------------------
+
+def test_tma_gather_variant_bit_identical(c1_scene, monkeypatch):
+    scene, margin = c1_scene
+    sc = f32_rounded(scene)
+    steps = 12
+    runs = []
+    for tma in ("0", "1"):
+        monkeypatch.setenv("GF_SS_TMA", tma)   # read when the context is created
+        ctx = S.upload_scene(sc, f32_state=True)
+        rr = S.run(ctx, sc, steps, margin, period=2, lag=2)
+        out = S.download_state(ctx, sc["voxel"].shape[0])
+        kind, sa, sb, wild = S.get_acs(ctx)
+        ctx.close()
+        assert rr.bad_owner == -1 and rr.touching > 1000
+        runs.append((rr.touching, out, wild))
+    assert runs[0][0] == runs[1][0]
+    for key in ("voxel", "subvoxel", "quat", "lin_vel", "ang_vel"):
+        assert np.array_equal(runs[0][1][key], runs[1][1][key]), key
+    assert np.array_equal(runs[0][2], runs[1][2])
