@@ -96,6 +96,43 @@ int ensure_pooled(Ctx *c, DBuf &b, size_t bytes, cudaStream_t s) {
   return 0;
 }
 
+// The centre records (double4 per sphere) as a 2-D tensor [n_sph rows x 4
+// doubles] for TMA tile::gather4 (box = one row); re-encoded when the buffer
+// moves.  cuTensorMapEncodeTiled comes from the driver through the runtime's
+// entry-point query (no link-time libcuda dependency).
+int center_tmap(Ctx *c) {
+  void *p = c->sph_center.p;
+  if (!p || c->n_sph <= 0) return -1;
+  if (p == c->tm_center_ptr && c->n_sph == c->tm_center_n) return 0;
+  using Encode = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                              const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Encode encode = nullptr;
+  if (!encode) {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn) {
+      c->err = "cuTensorMapEncodeTiled unavailable";
+      return -1;
+    }
+    encode = reinterpret_cast<Encode>(fn);
+  }
+  const cuuint64_t dims[2] = {4, cuuint64_t(c->n_sph)};
+  const cuuint64_t strides[1] = {32};
+  const cuuint32_t box[2] = {4, 1};
+  const cuuint32_t es[2] = {1, 1};
+  if (encode(&c->tm_center, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, p, dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+    c->err = "cuTensorMapEncodeTiled failed for the centre records";
+    return -1;
+  }
+  c->tm_center_ptr = p;
+  c->tm_center_n = c->n_sph;
+  return 0;
+}
+
 int release_scratch(Ctx *c, DBuf &b, cudaStream_t s) {
   if (b.p) GF_CHECK(c, cudaFreeAsync(b.p, s));
   b.p = nullptr;
@@ -526,6 +563,7 @@ gf_ctx *gf_create(int device, int kt_device, uint32_t flags) {
   if (const char *sa = std::getenv("GF_SNAP_ASYNC")) c->snap_async = std::atoi(sa) != 0;
   if (const char *ra = std::getenv("GF_RB_ASYNC")) c->rb_async = std::atoi(ra) != 0;
   if (const char *rs = std::getenv("GF_RB_SLOT")) c->rb_slot = std::atoi(rs) != 0;
+  if (const char *st = std::getenv("GF_SS_TMA")) c->ss_tma = std::atoi(st) != 0;
   cudaDeviceGetAttribute(&c->n_sm, cudaDevAttrMultiProcessorCount, device);
   if (c->n_sm <= 0) c->n_sm = 148;
   if (const char *pd = std::getenv("GF_PDL")) c->pdl = std::atoi(pd);

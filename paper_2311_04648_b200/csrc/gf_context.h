@@ -1,5 +1,6 @@
 // gf_context.h -- host-side device context behind the C-ABI (include/gf_b200.h).
 #pragma once
+#include <cuda.h>   // CUtensorMap
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -131,6 +132,11 @@ struct Ctx {
   bool split = false;
   cudaEvent_t ev_kt_join = nullptr;   // recorded on s_kt (kT device) at the end of a run
   cudaEvent_t ev_snap_done = nullptr; // the kT-stream snapshot of a step's start state is complete
+  bool ss_tma = false;      // B-side centre gathers by TMA gather4 in the fused kernel (GF_SS_TMA=1)
+  bool ss_tma_smem = false; // its dynamic shared-memory opt-in is set (per context: per device)
+  alignas(64) CUtensorMap tm_center;   // the sphere-centre records as a 2-D tensor (rows of 4 doubles)
+  void *tm_center_ptr = nullptr;
+  int64_t tm_center_n = -1;
   bool rb_slot = true;      // candidate rebuild grouped by slot with atomic cursors (GF_RB_SLOT=0: pair radix sort)
   bool rb_async = true;     // staged non-blocking candidate rebuild inside runs (GF_RB_ASYNC=0: blocking)
   bool snap_async = false;  // snapshot on the kT stream (GF_SNAP_ASYNC=1); measured neutral: the force kernels fill every SM
@@ -288,6 +294,7 @@ int kt_snapshot(Ctx *c, cudaStream_t s, double margin = -1.0);   // centers/fami
                                                           // (margin >= 0: a detection's, with grid inputs)
 int kt_begin(Ctx *c, double margin, cudaStream_t s);               // grid + displacement check
 int kt_count(Ctx *c, cudaStream_t s, bool force_rebuild = false);   // candidates -> counts
+int center_tmap(Ctx *c);   // (re)encode tm_center for the current centre buffer
 int kt_count_async(Ctx *c, cudaStream_t s);   // 1 = a staged rebuild started (resume with kt_advance)
 int kt_advance(Ctx *c, cudaStream_t s, cudaEvent_t ev, bool block);   // 1 = stages remain
 int kt_detect_fill(Ctx *c, Acs &out, cudaStream_t s);

@@ -498,6 +498,176 @@ static __global__ void __launch_bounds__(256, kMinBlocks) k_contacts_ss(DtView v
   }
 }
 
+// ---------------------------------------------------------------------------
+// The fused kernel with the B-side centre gathers moved off the L1 data pipe:
+// each warp's 32 B rows (32-byte double4 records) are fetched by the TMA unit
+// with tile::gather4 (four rows per instruction, eight instructions per 32
+// entries) into a per-warp shared-memory stage, one iteration ahead, and
+// completed on an mbarrier; the lanes then read their partner's centre from
+// shared memory.  The A side stays an LDG (entries are A-sorted, so a warp's
+// A loads coalesce).  Everything after the geometry is k_contacts_ss's.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return uint32_t(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "GF_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra GF_WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_gather4(void *dst, const CUtensorMap *tm, uint64_t *bar, int r0, int r1, int r2,
+                                            int r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ bool ss_geom_cb(const DtView &v, uint32_t a, const double4 &cB, SsGeom &g) {
+  const double4 cA = ld256(v.sph.center + a);
+  const double dx = cA.x - cB.x, dy = cA.y - cB.y, dz = cA.z - cB.z;
+  const double d2 = dx * dx + dy * dy + dz * dz;
+  const double R = cA.w + cB.w;
+  g.num = float(R * R - d2);
+  g.dx = float(dx); g.dy = float(dy); g.dz = float(dz);
+  g.d = sqrtf(float(d2));
+  g.ra = float(cA.w); g.rb = float(cB.w);
+  return g.num > 0.f;
+}
+
+constexpr int kTmaStageBytes = 2 * kSsWarps * 32 * 32 + 128;   // two stages of 32 rows x 32 B per warp + alignment slack
+
+template <int kMinBlocks>
+static __global__ void __launch_bounds__(256, kMinBlocks)
+    k_contacts_ss_tma(DtView v, double ts_d, unsigned long long step, const __grid_constant__ CUtensorMap tm_c) {
+  constexpr int kSsQueue = 64;
+  extern __shared__ __align__(128) unsigned char dsm[];
+  __shared__ float s_mat[5][kSmemMat];
+  __shared__ long long s_red[kSsWarps][192];
+  __shared__ uint32_t s_own[kSsWarps][32];
+  __shared__ uint32_t q_a[kSsWarps][kSsQueue], q_b[kSsWarps][kSsQueue], q_k[kSsWarps][kSsQueue];
+  __shared__ float q_g[7][kSsWarps][kSsQueue];
+  __shared__ __align__(8) uint64_t s_bar[kSsWarps][2];
+  const bool smem = stage_materials(v, s_mat);
+  pdl_wait();
+  pdl_launch();
+  if (threadIdx.x == 0) s_own[0][0] = !v.st->err && v.st->dd_trip >= step;
+  __syncthreads();
+  const bool block_live = s_own[0][0] != 0;
+  __syncthreads();
+  if (!block_live) return;
+  const float ts = float(ts_d);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned long long n_ss = v.seg[v.n_sph];
+  constexpr unsigned long long kCta = (unsigned long long)kSsWarps * 32;
+  unsigned long long wstride = (unsigned long long)gridDim.x * kCta;
+  unsigned long long w0 = (blockIdx.x * (unsigned long long)kSsWarps + warp) * 32;
+  unsigned long long hi = n_ss;
+  if (v.blocked) {
+    const unsigned long long span = ((n_ss + gridDim.x * kCta - 1) / (gridDim.x * kCta)) * kCta;
+    const unsigned long long lo = blockIdx.x * span;
+    hi = min(n_ss, lo + span);
+    wstride = kCta;
+    w0 = lo + (unsigned long long)warp * 32;
+  }
+  uint32_t *qa = q_a[warp], *qb = q_b[warp], *qk = q_k[warp];
+  // TMA destinations 128-byte aligned whatever the dynamic base
+  unsigned char *dsm_a = dsm + ((128u - (smem_u32(dsm) & 127u)) & 127u);
+  double4 *cb = reinterpret_cast<double4 *>(dsm_a) + warp * 32;   // stage st at + st * kSsWarps * 32
+  uint64_t *bar = s_bar[warp];
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  int qn = 0;
+  unsigned long long touched = 0;
+  auto run_batch = [&](int take) {
+    const bool live = lane < take;
+    SsGeom g;
+    uint32_t a = 0, b = 0, k = 0;
+    if (live) {
+      a = qa[lane]; b = qb[lane]; k = qk[lane];
+      g.dx = q_g[0][warp][lane]; g.dy = q_g[1][warp][lane]; g.dz = q_g[2][warp][lane];
+      g.d = q_g[3][warp][lane]; g.num = q_g[4][warp][lane]; g.ra = q_g[5][warp][lane]; g.rb = q_g[6][warp][lane];
+    }
+    ss_force_warp(v, live, a, b, k, g, ts, s_mat, smem, lane, s_red[warp], s_own[warp]);
+    __syncwarp();
+    const int rest = qn - take;
+    for (int j = lane; j < rest; j += 32) {
+      const int src = take + j;
+      const uint32_t xa = qa[src], xb = qb[src], xk = qk[src];
+      float xg[7];
+#pragma unroll
+      for (int f = 0; f < 7; ++f) xg[f] = q_g[f][warp][src];
+      __syncwarp(__activemask());
+      qa[j] = xa; qb[j] = xb; qk[j] = xk;
+#pragma unroll
+      for (int f = 0; f < 7; ++f) q_g[f][warp][j] = xg[f];
+    }
+    __syncwarp();
+    qn = rest;
+  };
+  // 32 partner rows of the entries at `base` into stage st (rows past the
+  // block's end read row 0: the byte count stays 1 KB)
+  auto issue = [&](int st, uint32_t brow) {
+    if (lane == 0) mbar_expect_tx(bar + st, 32 * 32);
+    __syncwarp();
+    int r[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) r[q] = __shfl_sync(0xffffffffu, int(brow), (lane & 7) * 4 + q);
+    if (lane < 8) tma_gather4(cb + st * (kSsWarps * 32) + 4 * lane, &tm_c, bar + st, r[0], r[1], r[2], r[3]);
+  };
+  unsigned long long base = w0;
+  uint2 id_cur = base + lane < hi ? __ldcs(v.ids + base + lane) : make_uint2(0u, 0u);
+  if (base < hi) issue(0, base + lane < hi ? (id_cur.y & kSlotMask) : 0u);
+  uint2 id_n1 = base + wstride + lane < hi ? __ldcs(v.ids + base + wstride + lane) : make_uint2(0u, 0u);
+  for (int it = 0; base < hi; base += wstride, ++it) {
+    const unsigned long long nb = base + wstride;
+    if (nb < hi) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // the stage's last reads precede the refill
+      issue((it + 1) & 1, nb + lane < hi ? (id_n1.y & kSlotMask) : 0u);
+    }
+    const uint2 id_n2 = nb + wstride + lane < hi ? __ldcs(v.ids + nb + wstride + lane) : make_uint2(0u, 0u);
+    mbar_wait(bar + (it & 1), uint32_t(it >> 1) & 1u);
+    const double4 cB = cb[(it & 1) * (kSsWarps * 32) + lane];
+    const unsigned long long e = base + lane;
+    SsGeom g;
+    const bool t = e < hi && ss_geom_cb(v, id_cur.x, cB, g);
+    __syncwarp();
+    const unsigned m = __ballot_sync(0xffffffffu, t);
+    if (t) {
+      const int pos = qn + __popc(m & ((1u << lane) - 1u));
+      qa[pos] = id_cur.x; qb[pos] = id_cur.y & kSlotMask; qk[pos] = uint32_t(e);
+      q_g[0][warp][pos] = g.dx; q_g[1][warp][pos] = g.dy; q_g[2][warp][pos] = g.dz;
+      q_g[3][warp][pos] = g.d; q_g[4][warp][pos] = g.num; q_g[5][warp][pos] = g.ra; q_g[6][warp][pos] = g.rb;
+    }
+    qn += __popc(m);
+    touched += __popc(m);
+    __syncwarp();
+    while (qn >= 32) run_batch(32);
+    id_cur = id_n1;
+    id_n1 = id_n2;
+  }
+  if (qn > 0) run_batch(qn);
+  if (lane == 0 && touched) {
+    atomicAdd(&v.st->touching, 2ull * touched);
+    atomicAdd(&v.st->touch_pairs, touched);
+  }
+}
+
 // one contact's contribution to owner position p (A side +, B side -)
 __device__ __forceinline__ void contribute(const DtView &v, uint32_t k, bool side_b, const double p[3],
                                            double af[3], double at[3]) {
@@ -829,15 +999,16 @@ __global__ void k_step_begin(Status *st, unsigned long long *tn) {
 
 // launch with programmatic stream serialisation (Ctx::pdl) or plainly
 template <typename... KArgs, typename... Args>
-cudaError_t launch_k(const Ctx *c, void (*kern)(KArgs...), dim3 g, dim3 b, cudaStream_t s, Args... args) {
+cudaError_t launch_ks(const Ctx *c, void (*kern)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t s,
+                      Args... args) {
   if (!c->pdl) {
-    kern<<<g, b, 0, s>>>(args...);
+    kern<<<g, b, smem, s>>>(args...);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = g;
   cfg.blockDim = b;
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -845,6 +1016,10 @@ cudaError_t launch_k(const Ctx *c, void (*kern)(KArgs...), dim3 g, dim3 b, cudaS
   cfg.attrs = at;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(const Ctx *c, void (*kern)(KArgs...), dim3 g, dim3 b, cudaStream_t s, Args... args) {
+  return launch_ks(c, kern, g, b, 0, s, args...);
 }
 }  // namespace
 
@@ -927,7 +1102,15 @@ int dt_forces_impl(Ctx *c, const StepArgs &a, cudaStream_t s) {
         GF_CHECK(c, launch_k(c, k_contacts_ss<1, 4, false>, dim3(nsm * 4), dim3(256), s, v, a.h, step));
       else if (c->ss_split == 3)
         GF_CHECK(c, launch_k(c, k_contacts_ss<2, 4, false>, dim3(nsm * 4), dim3(256), s, v, a.h, step));
-      else if (!c->ss_red)   // per-word REDs (the round-1 kernel; A/B switch GF_SS_RED=0)
+      else if (c->ss_tma && center_tmap(c) == 0) {
+        if (!c->ss_tma_smem) {
+          GF_CHECK(c, cudaFuncSetAttribute(k_contacts_ss_tma<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           kTmaStageBytes));
+          c->ss_tma_smem = true;
+        }
+        GF_CHECK(c, launch_ks(c, k_contacts_ss_tma<3>, dim3(nsm * 3), dim3(256), size_t(kTmaStageBytes), s, v, a.h,
+                              step, c->tm_center));
+      } else if (!c->ss_red)   // per-word REDs (the round-1 kernel; A/B switch GF_SS_RED=0)
         GF_CHECK(c, launch_k(c, k_contacts_ss<2, 3, false>, dim3(nsm * 3), dim3(256), s, v, a.h, step));
       else
         GF_CHECK(c, launch_k(c, k_contacts_ss<2, 3, true>, dim3(nsm * 3), dim3(256), s, v, a.h, step));

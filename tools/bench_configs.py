@@ -80,6 +80,19 @@ def main():
             print(json.dumps({"config": name, "error": f"{type(exc).__name__}: {exc}"}), flush=True)
 
 
+def rover_clearance(sim, wp, cen, rad):
+    """Smallest vertical gap between the wheel's lower envelope (a circle of
+    the grouser-tip radius about the axle, over the wheel's width) and the
+    grains under it."""
+    tw = sim._tri_world.reshape(-1, 3, 3)
+    ylo, yhi = float(tw[:, :, 1].min()), float(tw[:, :, 1].max())
+    rg = float(wp[2] - tw[:, :, 2].min())
+    sel = (cen[:, 1] > ylo) & (cen[:, 1] < yhi) & (np.abs(cen[:, 0] - wp[0]) < rg)
+    dx = cen[sel, 0] - wp[0]
+    bottom = wp[2] - np.sqrt(np.maximum(rg * rg - dx * dx, 0.0))
+    return float(np.min(bottom - (cen[sel, 2] + rad[sel])))
+
+
 def run_one(name, args, models, scenes):
     if True:
         t0 = time.perf_counter()
@@ -124,33 +137,35 @@ def run_one(name, args, models, scenes):
             fam_of = sim.store.__dict__["_owner_family"][:sim.store.n_owners]
             wheel = sim.track(int(np.nonzero(fam_of == fam)[0][0]))
             # the settled surface sits centimetres below the lattice top the
-            # wheel was placed on: move the wheel down onto it, its lowest
-            # grouser tips 0.2 mm above the highest grain under its footprint
+            # wheel was placed on: move the wheel down onto it, 0.2 mm above
+            # the first grain its grouser-tip envelope would meet
             cen, rad = sim._sph_centers, np.asarray(sim._sph_radius, np.float64)
             wp = wheel.pos()
-            foot = (np.abs(cen[:, 0] - wp[0]) < 0.012) & (np.abs(cen[:, 1] - wp[1]) < 0.1)
-            top = float(np.max(cen[foot, 2] + rad[foot]))
-            t_down = float(wp[2] - (top + 0.25 + 0.08 * 0.25 + 2e-4))
+            wp[0] = -0.5   # away from the trough's end wall, where the lattice packs unevenly
+            t_down = rover_clearance(sim, wp, cen, rad) - 2e-4
             wheel.set_pos([wp[0], wp[1], wp[2] - t_down])
-            sim.set_init_time_step(2e-6)
-            sim.set_error_out_velocity(8.0)
-            # down at 0.2 m/s until the grousers meet the grains (the wheel's
-            # contact force read back on the device, 0.4 mm per check), then
-            # 0.5 mm further while rolling
+            # down at 0.2 m/s (still at the settling step) until the grousers
+            # meet the grains -- sphere-triangle entries in the contact array,
+            # 0.4 mm per check -- then roll at the timed step
+            def wheel_entries():
+                kind = sim._acs_arrays()[0]
+                return int(np.sum(kind == 1))
             sim.set_family_prescribed_lin_vel(fam, 0.0, 0.0, -0.2)
             n_down = 0
-            while np.linalg.norm(wheel.contact_force()) == 0.0 and n_down < 50:
+            while wheel_entries() < 20 and n_down < 100:
                 sim.do_dynamics(0.002)
                 n_down += 1
-            sim.set_family_prescribed_lin_vel(fam, 0.8 * 0.25 * 0.8, 0.0, -0.05)
-            sim.set_family_prescribed_ang_vel(fam, 0.0, 0.8, 0.0)
-            sim.do_dynamics(0.01)
+            sim.set_init_time_step(2e-6)
+            sim.set_error_out_velocity(8.0)
             sim.set_family_prescribed_lin_vel(fam, 0.8 * 0.25 * 0.8, 0.0, -0.01)
+            sim.set_family_prescribed_ang_vel(fam, 0.0, 0.8, 0.0)
+            sim.do_dynamics(0.004)
             rec = {"config": f"configs[4]: grousered wheel (0.8 rad/s, 20% slip) on a {args.rover_spheres}-sphere "
                              "GRC-1-like clump terrain, h = 2e-6"}
             rec["wheel_lowered_m"] = t_down
             rec["wheel_plunge_checks"] = n_down
             rec["wheel_force_N_before_timed"] = [float(x) for x in wheel.contact_force()]
+            rec["wheel_contact_entries_before_timed"] = wheel_entries()
         elif name == "clumps":
             sim = scenes.clump_bed(1_000_000)
             sim.initialize()
