@@ -151,8 +151,11 @@ def run_one(name, args, models, scenes):
                 kind = sim._acs_arrays()[0]
                 return int(np.sum(kind == 1))
             sim.set_family_prescribed_lin_vel(fam, 0.0, 0.0, -0.2)
-            n_down = 0
-            while wheel_entries() < 20 and n_down < 100:
+            n_down, trace = 0, []
+            while n_down < 100:
+                trace.append(wheel_entries())
+                if trace[-1] >= 20:
+                    break
                 sim.do_dynamics(0.002)
                 n_down += 1
             sim.set_init_time_step(2e-6)
@@ -164,6 +167,7 @@ def run_one(name, args, models, scenes):
                              "GRC-1-like clump terrain, h = 2e-6"}
             rec["wheel_lowered_m"] = t_down
             rec["wheel_plunge_checks"] = n_down
+            rec["wheel_entries_per_check"] = trace
             rec["wheel_force_N_before_timed"] = [float(x) for x in wheel.contact_force()]
             rec["wheel_contact_entries_before_timed"] = wheel_entries()
         elif name == "clumps":
