@@ -399,35 +399,26 @@ static __global__ void __launch_bounds__(256, kMinBlocks) k_contacts_ss(DtView v
     w0 = lo + (unsigned long long)warp * 32 * kSsPerLane;
   }
   uint32_t *qa = q_a[warp], *qb = q_b[warp], *qk = q_k[warp];
-  int qn = 0;
+  // the queue is a ring of kSsQueue slots: qh = its head, qn = its length
+  // (a batch advances the head; nothing is moved)
+  int qn = 0, qh = 0;
+  auto ring = [](int x) { return x >= kSsQueue ? x - kSsQueue : x; };   // x < 2 kSsQueue
   unsigned long long touched = 0;
   auto run_batch = [&](int take) {
     const bool live = lane < take;
     SsGeom g;
     uint32_t a = 0, b = 0, k = 0;
     if (live) {
-      a = qa[lane]; b = qb[lane]; k = qk[lane];
-      g.dx = q_g[0][warp][lane]; g.dy = q_g[1][warp][lane]; g.dz = q_g[2][warp][lane];
-      g.d = q_g[3][warp][lane]; g.num = q_g[4][warp][lane]; g.ra = q_g[5][warp][lane]; g.rb = q_g[6][warp][lane];
+      const int q = ring(qh + lane);
+      a = qa[q]; b = qb[q]; k = qk[q];
+      g.dx = q_g[0][warp][q]; g.dy = q_g[1][warp][q]; g.dz = q_g[2][warp][q];
+      g.d = q_g[3][warp][q]; g.num = q_g[4][warp][q]; g.ra = q_g[5][warp][q]; g.rb = q_g[6][warp][q];
     }
     ss_force_warp(v, live, a, b, k, g, ts, s_mat, smem, lane, kStaged ? s_red[warp] : nullptr,
                   kStaged ? s_own[warp] : nullptr);
     __syncwarp();
-    // shift the rest of the queue down
-    const int rest = qn - take;
-    for (int j = lane; j < rest; j += 32) {
-      const int src = take + j;
-      const uint32_t xa = qa[src], xb = qb[src], xk = qk[src];
-      float xg[7];
-#pragma unroll
-      for (int f = 0; f < 7; ++f) xg[f] = q_g[f][warp][src];
-      __syncwarp(__activemask());
-      qa[j] = xa; qb[j] = xb; qk[j] = xk;
-#pragma unroll
-      for (int f = 0; f < 7; ++f) q_g[f][warp][j] = xg[f];
-    }
-    __syncwarp();
-    qn = rest;
+    qh = ring(qh + take);
+    qn -= take;
   };
   // the contact list is streamed one iteration ahead (its load is off the
   // critical path of the centre gathers); v.pf also prefetches each touching
@@ -479,7 +470,7 @@ static __global__ void __launch_bounds__(256, kMinBlocks) k_contacts_ss(DtView v
     for (int j = 0; j < kSsPerLane; ++j) {
       const unsigned m = __ballot_sync(0xffffffffu, t[j]);
       if (t[j]) {
-        const int pos = qn + __popc(m & ((1u << lane) - 1u));
+        const int pos = ring(qh + qn + __popc(m & ((1u << lane) - 1u)));
         qa[pos] = id[j].x; qb[pos] = id[j].y & kSlotMask; qk[pos] = uint32_t(base + 32 * j + lane);
         q_g[0][warp][pos] = g[j].dx; q_g[1][warp][pos] = g[j].dy; q_g[2][warp][pos] = g[j].dz;
         q_g[3][warp][pos] = g[j].d; q_g[4][warp][pos] = g[j].num; q_g[5][warp][pos] = g[j].ra;
