@@ -159,13 +159,22 @@ template <typename VelT>
 __global__ void __launch_bounds__(128) k_forces(DtView v, double ts, double sim_time, const uint32_t *list0,
                                                 const uint32_t *list1, const unsigned long long *counts,
                                                 int skip0) {
+  __shared__ BCache bc;
+  __shared__ int s_err;
   pdl_wait();
   pdl_launch();
-  if (v.st->err) return;
+  bcache_init(bc);
+  if (threadIdx.x == 0) s_err = v.st->err;
+  __syncthreads();
+  if (s_err) return;
+  BCache *bcp = v.own.facc ? &bc : nullptr;
   const unsigned long long n0 = skip0 ? 0ull : counts[0], n = n0 + counts[1];
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
        i += (unsigned long long)gridDim.x * blockDim.x)
-    force_entry<VelT, HmCore>(v, i < n0 ? list0[i] : list1[i - n0], ts, sim_time);
+    force_entry<VelT, HmCore>(v, i < n0 ? list0[i] : list1[i - n0], ts, sim_time, bcp);
+  if (bcp == nullptr) return;
+  __syncthreads();
+  bcache_flush(v, bc);
 }
 
 // fp32 rotation by q = (w, x, y, z) (lever arms and angular velocities of
