@@ -590,18 +590,26 @@ def measure_e2e(sim, steps):
     step0 = sim.scheduler.step_counter
     torch.cuda.synchronize()
     t0 = time.perf_counter()
+    ph = [0.0, 0.0, 0.0]   # host wall per call (each call returns synchronised)
     for i in range(steps):
+        ta = time.perf_counter()
         ctx.call("gf_upload_owners", C.c_int64(n), P(vox), P(sub), P(quat), P(lv), P(av), P(fam),
                  P(tpl), C.c_int64(rows.shape[0]), P(mass), P(moi))
+        tb = time.perf_counter()
         rp.step0 = step0 + i
         ctx.call("gf_run", C.byref(rp), C.byref(rr))
+        tc = time.perf_counter()
         ctx.call("gf_download_owners", P(vox), P(sub), P(quat), P(lv), P(av), P(fam))
+        td = time.perf_counter()
+        ph[0] += tb - ta; ph[1] += tc - tb; ph[2] += td - tc
     wall = time.perf_counter() - t0
     sim.scheduler.step_counter = step0 + steps
     n_s = int(sim._sph_geom.size)
     per = n * (8 + 6 + 16 + 24 + 24 + 1)
     return {"value": n_s * steps / wall / 1e6, "unit": UNIT, "h2d_bytes_per_step": per,
             "d2h_bytes_per_step": per + 64, "steps": steps, "wall": wall,
+            "ms_per_call": {"upload": 1e3 * ph[0] / steps, "run_1_step": 1e3 * ph[1] / steps,
+                            "download": 1e3 * ph[2] / steps},
             "path": "gf_upload_owners -> gf_run(1 step) -> gf_download_owners, pinned host buffers"}
 
 
