@@ -395,18 +395,138 @@ def grc1_templates(sim: Simulator, material: int, density: float = 2500.0, scale
     return out
 
 
+def _grc1_layers(n_spheres: int, lo, hi, rng, gap: float = 0.05, tilt: float = 0.02):
+    """Dense GRC-1 layers inside the box lo..hi (x, y; z from lo[2] up) until
+    n_spheres component spheres: per layer one type t (probability ~ weight
+    share / layer thickness, so volumes follow the weight shares), clumps
+    aligned with the layer's yaw (0 or 90 degrees, alternating), spaced
+    (1 + gap) x (clump size, sphere diameter), rows offset by half a pitch,
+    each tilted by a random angle <= `tilt` about its horizontal normal
+    (small enough for the gap).  Returns (type, centres (n, 3), quats (n, 4)
+    as (w, x, y, z)) per layer."""
+    size = np.array([t[0] for t in GRC1_TYPES])
+    rc = np.array([t[1] for t in GRC1_TYPES])
+    k_of = np.array([max(2, math.ceil(t[0] / (2 * t[1]))) for t in GRC1_TYPES])
+    thick = 2.0 * rc * (1.0 + gap)
+    p = np.array([t[2] for t in GRC1_TYPES]) / thick
+    p /= p.sum()
+    layers, total, z_top, yaw, prev_rc = [], 0, float(lo[2]), 0, 0.0
+    while total < n_spheres:
+        t = int(rng.choice(len(GRC1_TYPES), p=p))
+        a, b = size[t] * (1.0 + gap), 2.0 * rc[t] * (1.0 + gap)
+        half = 0.5 * (size[t] - 2.0 * rc[t])
+        # the layer's centre plane: the previous layer's top + this one's
+        # radius, with room for both tilts
+        z = (z_top + rc[t] * (1.0 + gap) + half * math.sin(tilt)) if layers else float(lo[2]) + rc[t] + half * math.sin(tilt) + 1e-4
+        ax_len = (hi[0] - lo[0], hi[1] - lo[1]) if yaw == 0 else (hi[1] - lo[1], hi[0] - lo[0])
+        n_along = int((ax_len[0] - size[t]) // a) + 1
+        n_across = int((ax_len[1] - 2.0 * rc[t]) // b) + 1
+        if n_along < 1 or n_across < 1:
+            raise ValueError("trough too small for the GRC-1 clumps")
+        i, j = np.meshgrid(np.arange(n_along - 1), np.arange(n_across), indexing="ij")
+        u = (i + 0.5 * (j % 2)) * a + 0.5 * size[t] + 0.5 * (ax_len[0] - size[t] - (n_along - 1) * a)
+        v = j * b + rc[t] + 0.5 * (ax_len[1] - 2.0 * rc[t] - (n_across - 1) * b)
+        u, v = u.ravel(), v.ravel()
+        if yaw == 0:
+            cen = np.stack([lo[0] + u, lo[1] + v, np.full(u.size, z)], axis=1)
+        else:
+            cen = np.stack([lo[0] + v, lo[1] + u, np.full(u.size, z)], axis=1)
+        need = -(-(n_spheres - total) // int(k_of[t]))
+        if cen.shape[0] > need:
+            cen = cen[rng.permutation(cen.shape[0])[:need]]
+        n = cen.shape[0]
+        al = rng.uniform(-tilt, tilt, n)
+        psi = 0.0 if yaw == 0 else 0.5 * math.pi
+        cy, sy = math.cos(psi / 2), math.sin(psi / 2)
+        ct, st = np.cos(al / 2), np.sin(al / 2)
+        q = np.stack([cy * ct, -sy * st, cy * st, sy * ct], axis=1)   # yaw (z) * tilt (body y)
+        layers.append((t, cen, q))
+        total += n * int(k_of[t])
+        z_top = z + rc[t] + half * math.sin(tilt)
+        yaw ^= 1
+    return layers, z_top
+
+
+def _rover_dense(n_spheres, *, seed, h, v_err, n_max, precision, device, omega, slip, wheel_radius,
+                 sinkage, aspect, plunge, kt_device, bed_depth):
+    rng = np.random.default_rng(seed)
+    gap = 0.05
+    size = np.array([t[0] for t in GRC1_TYPES])
+    rc = np.array([t[1] for t in GRC1_TYPES])
+    k_of = np.array([max(2, math.ceil(t[0] / (2 * t[1]))) for t in GRC1_TYPES])
+    w = np.array([t[2] for t in GRC1_TYPES])
+    # solid fraction of each type's layer, volume-weighted mean
+    phi_t = k_of * 4.0 / 3.0 * math.pi * rc ** 3 / (size * (2 * rc) ** 2 * (1 + gap) ** 3)
+    phi = float(np.sum(w * phi_t) / np.sum(w))
+    # mean component-sphere volume: spheres per unit volume of each type
+    sph_vol = 4.0 / 3.0 * math.pi * rc ** 3
+    share_sph = w / (k_of * sph_vol) * k_of   # spheres per unit solid volume of each type
+    v_mean = float(np.sum(w) / np.sum(share_sph))
+    depth = bed_depth if bed_depth is not None else (0.06 if n_spheres >= 2_000_000 else 0.03)
+    area = n_spheres * v_mean / (phi * depth)
+    width = max(math.sqrt(area / aspect), 1.4 * min(0.2, 2.0 * wheel_radius))
+    length = max(area / width, 4.0 * wheel_radius + 0.2)
+    wall_gap = 2e-3
+    lo = (-length / 2 + wall_gap, -width / 2 + wall_gap, 1e-4)
+    hi = (length / 2 - wall_gap, width / 2 - wall_gap, None)
+    layers, top = _grc1_layers(n_spheres, lo, hi, rng, gap=gap)
+    dom = Domain((-length / 2 - 0.3, -width / 2 - 0.05, -0.02),
+                 (length / 2 + 0.3, width / 2 + 0.05, top + 2.5 * wheel_radius + 0.3))
+    sim = Simulator(dom, precision=precision, device=device, kt_device=kt_device)
+    mat = sim.load_material(dict(GRC1_MATERIAL))
+    tpls = grc1_templates(sim, mat)
+    for t, cen, q in layers:
+        ids = np.asarray(sim.store.add_clumps_array(tpls[t][0], cen), dtype=np.int64)
+        sim.store.__dict__["_quat"][ids] = q
+    walls = [("plane", (0, 0, 0), (0, 0, 1), mat),
+             ("plane", (-length / 2, 0, 0), (1, 0, 0), mat), ("plane", (length / 2, 0, 0), (-1, 0, 0), mat),
+             ("plane", (0, -width / 2, 0), (0, 1, 0), mat), ("plane", (0, width / 2, 0), (0, -1, 0), mat)]
+    sim.add_analytic(walls, family=255)
+    sim.set_family_fixed(255)
+    wheel_w = min(0.2, 0.6 * width)
+    grouser = 0.08 * wheel_radius
+    tris = grousered_wheel(radius=wheel_radius, width=wheel_w, grouser_h=grouser)
+    x0 = -length / 2 + wheel_radius + grouser + 0.05
+    z0 = top + wheel_radius + grouser - sinkage   # the lowest grouser tip `sinkage` into the bed top
+    sim.add_mesh(tris, mat, family=WHEEL_FAMILY, position=(x0, 0.0, z0))
+    sim.set_family_prescribed_lin_vel(WHEEL_FAMILY, omega * wheel_radius * (1.0 - slip), 0.0, -plunge)
+    sim.set_family_prescribed_ang_vel(WHEEL_FAMILY, 0.0, omega, 0.0)
+    sim.set_gravity([0, 0, -G])
+    sim.set_init_time_step(h)
+    sim.set_error_out_velocity(v_err)
+    sim.set_fixed_lookahead(n_max)
+    sim.rover_bed = {"length": length, "width": width, "bed_top": top, "solid_fraction": phi,
+                     "layers": len(layers)}
+    return sim
+
+
 def rover_wheel(n_spheres: int = 11_000_000, *, seed: int = 3, h: float = 2e-6, v_err: float = 3.0,
                 n_max: int = 8, precision: str = "f32", device: int = 0, omega: float = 0.8,
                 slip: float = 0.2, wheel_radius: float = 0.25, sinkage: float = 0.005,
-                aspect: float = 4.0, plunge: float = 0.0, kt_device=None) -> Simulator:
+                aspect: float = 4.0, plunge: float = 0.0, kt_device=None,
+                packing: str = "dense", bed_depth: float = None) -> Simulator:
     """A GRC-1-like terrain of about n_spheres component spheres in a walled
     trough (length = aspect x width) with the grousered wheel resting
     `sinkage` into its surface at one end, spinning at `omega` about its axle
     and moving forward at omega R (1 - slip) (family WHEEL_FAMILY, fully
-    prescribed: a boundary owner whose contact force is read back).  Clumps
-    sit on an HCP lattice of pitch = the type-2 clump size (11.4 mm), random
-    types by number share (the 21 mm type-1 clumps take two lattice sites),
-    random orientations."""
+    prescribed: a boundary owner whose contact force is read back).
+
+    packing "dense" (default): horizontal layers of one GRC-1 type each
+    (layer types drawn so the volume shares follow the weight shares), rows
+    of clumps 5 % apart, yaw alternating 0 / 90 degrees between layers, a
+    small random tilt -- a bed `bed_depth` deep (0.06 m from 2M spheres up,
+    else 0.03 m) that settles by a few per cent.  packing "lattice": the
+    round-2 HCP lattice of pitch = the type-2 clump size (11.4 mm, random
+    types by number share, random orientations); its solid fraction is ~1 %,
+    so it collapses to a grain monolayer -- kept for the small parity scenes
+    in tests/."""
+    if packing == "dense":
+        return _rover_dense(n_spheres, seed=seed, h=h, v_err=v_err, n_max=n_max, precision=precision,
+                            device=device, omega=omega, slip=slip, wheel_radius=wheel_radius,
+                            sinkage=sinkage, aspect=aspect, plunge=plunge, kt_device=kt_device,
+                            bed_depth=bed_depth)
+    if packing != "lattice":
+        raise ValueError(f"unknown packing {packing!r}")
     rng = np.random.default_rng(seed)
     pitch = GRC1_TYPES[1][0] * 1.02
     # number shares from the weight shares (w / m, m ~ k rc^3)

@@ -44,7 +44,7 @@ def test_sphere_csv_byte_identical(tmp_path, precision):
 
 
 def test_mesh_vtk_frame(tmp_path):
-    sim = scenes.rover_wheel(6_000, precision="f64", h=2e-6, v_err=3.0, n_max=4, sinkage=0.0005,
+    sim = scenes.rover_wheel(6_000, packing="lattice", precision="f64", h=2e-6, v_err=3.0, n_max=4, sinkage=0.0005,
                              wheel_radius=0.05, aspect=2.0)
     sim.initialize()
     with sim:

@@ -26,7 +26,7 @@ pytestmark = pytest.mark.gpu
 def small_rover(precision="f64"):
     # the wheel plunges at 1 m/s while it spins, so its grousers and rim
     # reach the grains under it within the window
-    sim = scenes.rover_wheel(6_000, precision=precision, h=1e-5, v_err=3.0, n_max=4, sinkage=0.0,
+    sim = scenes.rover_wheel(6_000, packing="lattice", precision=precision, h=1e-5, v_err=3.0, n_max=4, sinkage=0.0,
                              wheel_radius=0.05, aspect=2.0, plunge=1.0)
     return sim
 
@@ -75,7 +75,7 @@ def test_wheel_contact_force_readback():
     """Through the Simulator: after a do_dynamics call the wheel owner's
     accumulated force (acc_force, read back for passive owners on the
     reported step) balances the grains' wall-contact forces."""
-    sim = scenes.rover_wheel(20_000, precision="f64", h=1e-5, v_err=3.0, n_max=4, sinkage=0.0,
+    sim = scenes.rover_wheel(20_000, packing="lattice", precision="f64", h=1e-5, v_err=3.0, n_max=4, sinkage=0.0,
                              wheel_radius=0.06, aspect=2.0, plunge=1.0)
     sim.initialize()
     with sim:

@@ -41,3 +41,39 @@ def test_tiled_bed_replicates_state_without_overlap():
     pos = t.positions()[t.owner_kind[: t.n_owners] == OWNER_CLUMP]
     assert pos[:, 0].max() <= 3 * 6 * 0.0254 and pos[:, 0].min() >= -3 * 6 * 0.0254
     assert pos[:, 1].max() <= 2 * 6 * 0.0254 and pos[:, 1].min() >= -2 * 6 * 0.0254
+
+
+def test_rover_dense_terrain_packed_without_overlap():
+    """configs[4]'s dense GRC-1 bed (scenes.rover_wheel packing "dense"):
+    the requested sphere count, every GRC-1 type present at 1M spheres is
+    a real component radius, no two clumps overlap, and the bed is a packed
+    layer stack (solid fraction ~0.49, a few centimetres deep) -- the
+    lattice packing collapses to a monolayer (solid fraction ~1 %)."""
+    from scipy.spatial import cKDTree
+    from paper_2311_04648_b200 import scenes
+    n = 200_000
+    sim = scenes.rover_wheel(n, sinkage=0.0, bed_depth=0.02)
+    bed = sim.rover_bed
+    assert 0.45 < bed["solid_fraction"] < 0.55
+    assert bed["layers"] >= 3 and 0.005 < bed["bed_top"] < 0.04
+    sc = scenes.oracle_scene(sim)
+    pos = np.asarray(sim.store.positions())
+    sel = sc["geom_kind"] == 0
+    assert int(sel.sum()) in (n, n + 1)
+    o = sc["geom_owner"][sel]
+    off = sc["geom_params"][sel][:, :3].astype(np.float64)
+    r = sc["geom_params"][sel][:, 3].astype(np.float64)
+    assert set(np.unique(r.astype(np.float32))) <= {np.float32(t[1]) for t in scenes.GRC1_TYPES}
+    w, x, y, z = (sc["quat"][o, i].astype(np.float64) for i in range(4))
+    vx, vy, vz = off[:, 0], off[:, 1], off[:, 2]
+    tx, ty, tz = 2 * (y * vz - z * vy), 2 * (z * vx - x * vz), 2 * (x * vy - y * vx)
+    c = pos[o] + np.stack([vx + w * tx + (y * tz - z * ty), vy + w * ty + (z * tx - x * tz),
+                           vz + w * tz + (x * ty - y * tx)], axis=1)
+    pairs = cKDTree(c).query_pairs(2 * r.max(), output_type="ndarray")
+    inter = o[pairs[:, 0]] != o[pairs[:, 1]]
+    gap = np.linalg.norm(c[pairs[:, 0]] - c[pairs[:, 1]], axis=1) - (r[pairs[:, 0]] + r[pairs[:, 1]])
+    assert float(gap[inter].min()) > 0.0
+    # inside the trough, above the floor
+    assert float((c[:, 2] - r).min()) > 0.0
+    assert float(np.abs(c[:, 0]).max() + r.max()) < bed["length"] / 2
+    assert float(np.abs(c[:, 1]).max() + r.max()) < bed["width"] / 2

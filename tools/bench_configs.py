@@ -70,7 +70,8 @@ def main():
     ap.add_argument("--hopper-scale", type=float, default=5.85, help="~1M clumps at fill 1")
     ap.add_argument("--hopper-settle", type=float, default=0.6)
     ap.add_argument("--rover-spheres", type=int, default=11_000_000)
-    ap.add_argument("--rover-settle-steps", type=int, default=60_000)
+    ap.add_argument("--rover-settle-steps", type=int, default=25_000)
+    ap.add_argument("--rover-sinkage", type=float, default=0.01, help="grouser-tip sinkage before timing (m)")
     args = ap.parse_args()
     from paper_2311_04648_b200 import models, scenes
     for name in args.configs.split(","):
@@ -123,41 +124,39 @@ def run_one(name, args, models, scenes):
             # the terrain settles with the wheel held still just above it
             # (untimed input preparation at h = 4e-6), the wheel is pushed
             # down into the settled surface, then rolls: timed at h = 2e-6
-            # (the lattice falls into place: grains with no support below drop up
-            # to ~5 cm and the pile-up throws a few at 2-3 m/s for a moment, so
-            # the settle runs with a loose watchdog; 8 m/s once timed)
+            # (the dense layered bed -- scenes.rover_wheel packing "dense" --
+            # closes its 5 % gaps within ~0.05 s; the settle runs with a loose
+            # watchdog, 8 m/s once timed)
             sim = scenes.rover_wheel(args.rover_spheres, h=4e-6, sinkage=0.0, plunge=0.0, v_err=50.0)
             fam = scenes.WHEEL_FAMILY
             sim.set_family_prescribed_lin_vel(fam, 0.0, 0.0, 0.0)
             sim.set_family_prescribed_ang_vel(fam, 0.0, 0.0, 0.0)
             sim.initialize()
-            # the lattice terrain needs ~0.2 s to collapse into a contact network
-            # (60k steps at 4e-6 = 0.24 s)
+            # 25k steps at 4e-6 = 0.1 s
             sim.do_dynamics(max(args.settle_steps, args.rover_settle_steps) * sim.h)
             fam_of = sim.store.__dict__["_owner_family"][:sim.store.n_owners]
             wheel = sim.track(int(np.nonzero(fam_of == fam)[0][0]))
-            # the settled surface sits centimetres below the lattice top the
-            # wheel was placed on: move the wheel down onto it, 0.2 mm above
-            # the first grain its grouser-tip envelope would meet
+            # the dense layered bed settles by a few per cent: move the wheel
+            # down onto the settled surface, 0.2 mm above the first grain its
+            # grouser-tip envelope would meet
             cen, rad = sim._sph_centers, np.asarray(sim._sph_radius, np.float64)
             wp = wheel.pos()
-            wp[0] = -0.5   # away from the trough's end wall, where the lattice packs unevenly
             t_down = rover_clearance(sim, wp, cen, rad) - 2e-4
             wheel.set_pos([wp[0], wp[1], wp[2] - t_down])
-            # down at 0.2 m/s (still at the settling step) until the grousers
-            # meet the grains -- sphere-triangle entries in the contact array,
-            # 0.4 mm per check -- then roll at the timed step
+            # then down at 0.2 m/s (still at the settling step), 0.4 mm per
+            # check, until the grouser tips sit `rover_sinkage` into the bed;
+            # then roll at the timed step
             def wheel_entries():
                 kind = sim._acs_arrays()[0]
                 return int(np.sum(kind == 1))
             sim.set_family_prescribed_lin_vel(fam, 0.0, 0.0, -0.2)
             n_down, trace = 0, []
-            while n_down < 100:
+            n_checks = int(round(args.rover_sinkage / 4e-4))
+            while n_down < n_checks:
                 trace.append(wheel_entries())
-                if trace[-1] >= 20:
-                    break
                 sim.do_dynamics(0.002)
                 n_down += 1
+            trace.append(wheel_entries())
             sim.set_init_time_step(2e-6)
             sim.set_error_out_velocity(8.0)
             sim.set_family_prescribed_lin_vel(fam, 0.8 * 0.25 * 0.8, 0.0, -0.01)
@@ -165,6 +164,7 @@ def run_one(name, args, models, scenes):
             sim.do_dynamics(0.004)
             rec = {"config": f"configs[4]: grousered wheel (0.8 rad/s, 20% slip) on a {args.rover_spheres}-sphere "
                              "GRC-1-like clump terrain, h = 2e-6"}
+            rec["terrain"] = {k: float(v) for k, v in sim.rover_bed.items()}
             rec["wheel_lowered_m"] = t_down
             rec["wheel_plunge_checks"] = n_down
             rec["wheel_entries_per_check"] = trace
