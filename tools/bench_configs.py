@@ -71,6 +71,7 @@ def main():
     ap.add_argument("--hopper-settle", type=float, default=0.6)
     ap.add_argument("--rover-spheres", type=int, default=11_000_000)
     ap.add_argument("--rover-settle-steps", type=int, default=25_000)
+    ap.add_argument("--rover-settle-verr", type=float, default=50.0, help="watchdog speed while the terrain settles")
     ap.add_argument("--rover-sinkage", type=float, default=0.01, help="grouser-tip sinkage before timing (m)")
     args = ap.parse_args()
     from paper_2311_04648_b200 import models, scenes
@@ -78,6 +79,8 @@ def main():
         try:
             run_one(name, args, models, scenes)
         except Exception as exc:   # one config failing must not hide the others
+            import traceback
+            traceback.print_exc()
             print(json.dumps({"config": name, "error": f"{type(exc).__name__}: {exc}"}), flush=True)
 
 
@@ -127,7 +130,7 @@ def run_one(name, args, models, scenes):
             # (the dense layered bed -- scenes.rover_wheel packing "dense" --
             # closes its 5 % gaps within ~0.05 s; the settle runs with a loose
             # watchdog, 8 m/s once timed)
-            sim = scenes.rover_wheel(args.rover_spheres, h=4e-6, sinkage=0.0, plunge=0.0, v_err=50.0)
+            sim = scenes.rover_wheel(args.rover_spheres, h=4e-6, sinkage=0.0, plunge=0.0, v_err=args.rover_settle_verr)
             fam = scenes.WHEEL_FAMILY
             sim.set_family_prescribed_lin_vel(fam, 0.0, 0.0, 0.0)
             sim.set_family_prescribed_ang_vel(fam, 0.0, 0.0, 0.0)
@@ -152,8 +155,10 @@ def run_one(name, args, models, scenes):
             sim.set_family_prescribed_lin_vel(fam, 0.0, 0.0, -0.2)
             n_down, trace = 0, []
             n_checks = int(round(args.rover_sinkage / 4e-4))
+            ztrace = []
             while n_down < n_checks:
                 trace.append(wheel_entries())
+                ztrace.append(round(float(wheel.pos()[2]), 5))
                 sim.do_dynamics(0.002)
                 n_down += 1
             trace.append(wheel_entries())
@@ -168,6 +173,7 @@ def run_one(name, args, models, scenes):
             rec["wheel_lowered_m"] = t_down
             rec["wheel_plunge_checks"] = n_down
             rec["wheel_entries_per_check"] = trace
+            rec["wheel_z_per_check"] = ztrace
             rec["wheel_force_N_before_timed"] = [float(x) for x in wheel.contact_force()]
             rec["wheel_contact_entries_before_timed"] = wheel_entries()
         elif name == "clumps":
