@@ -199,7 +199,8 @@ struct Status {
   unsigned long long acs_total;   // last detection's pair count
   unsigned long long cand_total;   // candidate pairs of the last rebuild
   unsigned long long other_total;  // sphere-triangle / sphere-analytic pairs of the last detection
-  unsigned long long pad1[13];
+  unsigned long long cand_overflow;  // candidate fill: pairs beyond the counted capacity (must stay 0)
+  unsigned long long pad1[12];
   // line 2: dT counters (one atomic per k_touch block)
   unsigned long long touching;
   unsigned long long touch_pairs;  // touching ACS entries summed over the run's steps

@@ -659,7 +659,8 @@ __global__ void k_disp(int64_t n, const double4 *c4, const double *ref, double l
 template <bool kFill>
 __global__ void __launch_bounds__(128) k_cand_ss(KtView v, const uint4 *sm, const float4 *sf, double reach_m,
                                                  uint32_t *ucnt, const unsigned long long *uoff,
-                                                 uint32_t *ka, uint32_t *kb) {
+                                                 uint32_t *ka, uint32_t *kb, unsigned long long cap = 0,
+                                                 unsigned long long *ovf = nullptr) {
   int64_t u64 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (u64 >= v.sph.n) return;
   const Grid g = *v.grid;
@@ -708,8 +709,12 @@ __global__ void __launch_bounds__(128) k_cand_ss(KtView v, const uint4 *sm, cons
           const uint4 m1 = sm[w];
           if (m1.y != m0.y && dd_keep(v.own.dd, m0.y, m1.y)) {
             if (kFill) {
-              ka[w_out] = min(m0.x, m1.x);
-              kb[w_out] = max(m0.x, m1.x);
+              if (w_out < cap) {
+                ka[w_out] = min(m0.x, m1.x);
+                kb[w_out] = max(m0.x, m1.x);
+              } else {
+                atomicAdd(ovf, 1ull);   // the count pass disagreed: reported, never written
+              }
               ++w_out;
             }
             ++hits;
@@ -786,10 +791,20 @@ __global__ void __launch_bounds__(128) k_cand_big(KtView v, const uint32_t *bigs
 // reserves the thread's own run with one atomic on its slot's cursor and
 // places every other hit at its partner's segment start + that slot's
 // cursor.  The order inside a segment is the per-segment sort by b's.
+// a fill-pass store guarded by the capacity the count pass sized: a pair the
+// count did not see is counted in *ovf (the host fails the rebuild loudly)
+// instead of being written past the list
+__device__ __forceinline__ void cand_put(uint2 *cand, unsigned long long i, uint2 p, unsigned long long cap,
+                                         unsigned long long *ovf) {
+  if (i < cap) cand[i] = p;
+  else atomicAdd(ovf, 1ull);
+}
+
 template <bool kFill>
 __global__ void __launch_bounds__(128) k_cand_slot(KtView v, const uint4 *sm, const float4 *sf, double reach_m,
                                                    uint32_t *scnt, uint32_t *own, const unsigned long long *seg,
-                                                   uint32_t *cursor, uint2 *cand) {
+                                                   uint32_t *cursor, uint2 *cand, unsigned long long cap = 0,
+                                                   unsigned long long *ovf = nullptr) {
   int64_t u64 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (u64 >= v.sph.n) return;
   const Grid g = *v.grid;
@@ -842,10 +857,10 @@ __global__ void __launch_bounds__(128) k_cand_slot(KtView v, const uint4 *sm, co
           const uint4 m1 = sm[w];
           if (m1.y != m0.y && dd_keep(v.own.dd, m0.y, m1.y)) {
             if (m0.x < m1.x) {
-              if (kFill) cand[w_own + mine] = make_uint2(m0.x, m1.x);
+              if (kFill) cand_put(cand, w_own + mine, make_uint2(m0.x, m1.x), cap, ovf);
               ++mine;
             } else if (kFill) {
-              cand[seg[m1.x] + atomicAdd(cursor + m1.x, 1u)] = make_uint2(m1.x, m0.x);
+              cand_put(cand, seg[m1.x] + atomicAdd(cursor + m1.x, 1u), make_uint2(m1.x, m0.x), cap, ovf);
             } else {
               atomicAdd(scnt + m1.x, 1u);
             }
@@ -864,7 +879,8 @@ __global__ void __launch_bounds__(128) k_cand_big_slot(KtView v, const uint32_t 
                                                        const double4 *sc, const uint4 *sm, double reach_m,
                                                        double reach_bb, uint32_t *scnt,
                                                        const unsigned long long *seg, uint32_t *cursor,
-                                                       uint2 *cand) {
+                                                       uint2 *cand, unsigned long long cap = 0,
+                                                       unsigned long long *ovf = nullptr) {
   const Grid g = *v.grid;
   if (!g.valid) return;
   for (int64_t bi = blockIdx.x; bi < n_big; bi += gridDim.x) {
@@ -896,7 +912,7 @@ __global__ void __launch_bounds__(128) k_cand_big_slot(KtView v, const uint32_t 
         const double rr = rB + c1.w + reach_m;
         if (dx * dx + dy * dy + dz * dz >= rr * rr * (1.0 + 1e-9)) continue;
         const uint32_t a = min(m1.x, B), c = max(m1.x, B);
-        if (kFill) cand[seg[a] + atomicAdd(cursor + a, 1u)] = make_uint2(a, c);
+        if (kFill) cand_put(cand, seg[a] + atomicAdd(cursor + a, 1u), make_uint2(a, c), cap, ovf);
         else atomicAdd(scnt + a, 1u);
       }
     }
@@ -907,7 +923,7 @@ __global__ void __launch_bounds__(128) k_cand_big_slot(KtView v, const uint32_t 
                    dz = bz - v.centers[4 * size_t(j) + 2];
       const double rr = rB + double(v.sph.offr[j].w) + reach_bb;
       if (dx * dx + dy * dy + dz * dz >= rr * rr * (1.0 + 1e-9)) continue;
-      if (kFill) cand[seg[B] + atomicAdd(cursor + B, 1u)] = make_uint2(B, j);
+      if (kFill) cand_put(cand, seg[B] + atomicAdd(cursor + B, 1u), make_uint2(B, j), cap, ovf);
       else atomicAdd(scnt + B, 1u);
     }
   }
@@ -1482,6 +1498,17 @@ static int gap_list(Ctx *c, GapList &gl, cudaStream_t s) {
 //   C  sort by a, unpack, segment sorts, reference centres; sphere-analytic
 //      candidate count (-> host)
 //   D  sphere-analytic fill, scratch release, bookkeeping
+// the fill pass met more pairs than the count pass sized (the pinned mirror
+// of Status::cand_overflow, copied after the fill; read once the fill's
+// event has completed): fail the rebuild loudly
+static int cand_overflowed(Ctx *c) {
+  const unsigned long long o = reinterpret_cast<Status *>(c->h_status)->cand_overflow;
+  if (!o) return 0;
+  set_err(c, "candidate rebuild: the fill pass found " + std::to_string(o) +
+                 " pairs beyond the counted capacity (count / fill mismatch)");
+  return 1;
+}
+
 static int rb_stage_a(Ctx *c, cudaStream_t s) {
   KtScratch &k = c->kt;
   const int64_t n = c->n_sph;
@@ -1577,9 +1604,14 @@ static int rb_stage_b(Ctx *c, cudaStream_t s) {
   // (a, b) halves of cand_tmp; cand holds the sort's alternate halves
   uint32_t *ka = k.cand_tmp.as<uint32_t>(), *kb = ka + k.cand_cap;
   KtView v = kt_view(c, c->kt_margin);
+  unsigned long long *ovf = &c->status.as<Status>()->cand_overflow;
+  GF_CHECK(c, cudaMemsetAsync(ovf, 0, 8, s));
   if (n)
     k_cand_ss<true><<<grid_for(n, 128), 128, 0, s>>>(v, k.sm.as<uint4>(), k.sf.as<float4>(), reach, nullptr,
-                                                     k.counts.as<unsigned long long>(), ka, kb);
+                                                     k.counts.as<unsigned long long>(), ka, kb,
+                                                     (unsigned long long)small, ovf);
+  GF_CHECK(c, cudaMemcpyAsync(&reinterpret_cast<Status *>(c->h_status)->cand_overflow, ovf, 8,
+                              cudaMemcpyDeviceToHost, s));
   unsigned long long *big_n = k.cand_n.as<unsigned long long>();
   GF_CHECK(c, cudaMemsetAsync(big_n, 0, 8, s));
   if (c->n_big)
@@ -1598,6 +1630,7 @@ static int rb_lists_tail(Ctx *c, cudaStream_t s);
 static int rb_stage_c(Ctx *c, cudaStream_t s) {
   KtScratch &k = c->kt;
   const int64_t n = c->n_sph;
+  if (cand_overflowed(c)) return -1;
   const int64_t nbig = int64_t(reinterpret_cast<Status *>(c->h_status)->other_total);
   if (nbig > k.rb_big_cap) {
     k.rb_big_cap = nbig + nbig / 4 + 4096;
@@ -1693,19 +1726,25 @@ static int rb_slot_b(Ctx *c, cudaStream_t s) {
     uint32_t *cur = k.cursor.as<uint32_t>();
     const unsigned long long *seg = k.cand_seg.as<unsigned long long>();
     GF_CHECK(c, cudaMemsetAsync(cur, 0, 4 * (n + 1), s));
+    unsigned long long *ovf = &c->status.as<Status>()->cand_overflow;
+    GF_CHECK(c, cudaMemsetAsync(ovf, 0, 8, s));
+    const unsigned long long cap = (unsigned long long)total;
     k_cand_slot<true><<<grid_for(n, 128), 128, 0, s>>>(v, k.sm.as<uint4>(), k.sf.as<float4>(), c->kt_margin + skin,
                                                        nullptr, k.cand_own.as<uint32_t>(), seg, cur,
-                                                       k.cand.as<uint2>());
+                                                       k.cand.as<uint2>(), cap, ovf);
     if (c->n_big)
       k_cand_big_slot<true><<<unsigned(std::min<int64_t>(c->n_big, 4096)), 128, 0, s>>>(
           v, c->big_slots.as<uint32_t>(), c->n_big, k.sc.as<double4>(), k.sm.as<uint4>(), c->kt_margin + skin_b,
-          c->kt_margin + 2.0 * skin_b - skin, nullptr, seg, cur, k.cand.as<uint2>());
+          c->kt_margin + 2.0 * skin_b - skin, nullptr, seg, cur, k.cand.as<uint2>(), cap, ovf);
+    GF_CHECK(c, cudaMemcpyAsync(&reinterpret_cast<Status *>(c->h_status)->cand_overflow, ovf, 8,
+                                cudaMemcpyDeviceToHost, s));
   }
   return rb_lists_tail(c, s);
 }
 
 static int rb_stage_d(Ctx *c, cudaStream_t s) {
   KtScratch &k = c->kt;
+  if (c->rb_slot && cand_overflowed(c)) return -1;
   const int64_t n = c->n_sph;
   const double skin = c->skin_factor * c->kt_margin, skin_b = c->skin_big_factor * c->kt_margin;
   const double reach = c->kt_margin + skin, reach_big = c->kt_margin + skin_b;
