@@ -1339,6 +1339,21 @@ int gf_dt_step(gf_ctx *ctx, const gf_step_params *p, int64_t *touching, int64_t 
 // begin / per-step forces / per-step integrate / end so a decomposed run can
 // exchange ghost forces and ghost state between the halves (gf_run is the
 // plain loop over them).
+// GF_SYNC_DEBUG=1 (diagnostics only): synchronise the device after every
+// phase of the step and name the phase a kernel fault surfaced in
+static bool sync_debug() {
+  static const bool on = std::getenv("GF_SYNC_DEBUG") != nullptr;
+  return on;
+}
+static int dbg_sync(Ctx *c, const char *what, int64_t step) {
+  if (!sync_debug()) return 0;
+  const cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) return 0;
+  set_err(c, std::string("GF_SYNC_DEBUG: ") + cudaGetErrorString(e) + " after " + what + " (step " +
+                 std::to_string(step) + ")");
+  return -1;
+}
+
 int gf_run_begin(gf_ctx *ctx, const gf_run_params *p) {
   CTX_CHECK(ctx);
   if (c->run) { c->err = "a run is already in progress (gf_run_end missing)"; return -1; }
@@ -1375,7 +1390,7 @@ int gf_step_forces(gf_ctx *ctx, int64_t i) {
   trace_mark(c, "dt_step_begin", s, c->s_dt);
   // 1. a detection due at this step boundary is adopted first
   if (c->next_pending && s >= c->adopt_at) {
-    if (run_adopt(c)) return -1;
+    if (run_adopt(c) || dbg_sync(c, "run_adopt", s)) return -1;
     trace_mark(c, "dt_adopted", s, c->s_dt);
   }
   // 2. work order: snapshot on the dT stream, detection on the kT stream
@@ -1393,7 +1408,7 @@ int gf_step_forces(gf_ctx *ctx, int64_t i) {
       GF_CHECK(c, cudaEventRecord(c->ev_snap_done, c->s_kt));
       c->snap_wait = true;
     } else {
-      if (kt_snapshot(c, c->s_dt, p->margin)) return -1;
+      if (kt_snapshot(c, c->s_dt, p->margin) || dbg_sync(c, "kt_snapshot", s)) return -1;
       GF_CHECK(c, cudaEventRecord(c->ev_snap, c->s_dt));
       GF_CHECK(c, cudaStreamWaitEvent(c->s_kt, c->ev_snap, 0));
       GF_CHECK(c, cudaStreamWaitEvent(c->s_kt, c->ev_adopted, 0));
@@ -1421,7 +1436,7 @@ int gf_step_forces(gf_ctx *ctx, int64_t i) {
     R->kt_ev.push_back(e);
     GF_CHECK(c, cudaEventRecord(e.first, c->s_kt));
     trace_mark(c, "dt_snapshot_end", s, c->s_dt);
-    if (kt_begin(c, p->margin, c->s_kt)) return -1;
+    if (kt_begin(c, p->margin, c->s_kt) || dbg_sync(c, "kt_begin", s)) return -1;
     GF_CHECK(c, cudaEventRecord(c->ev_disp, c->s_kt));
       trace_mark(c, "kt_phaseA_end", s, c->s_kt);
     c->kt_phase = 1;
@@ -1434,12 +1449,12 @@ int gf_step_forces(gf_ctx *ctx, int64_t i) {
   }
   // 3. advance a staged rebuild; launch the fill as soon as the count is
   // known (no dT stall)
-  if (c->next_pending && c->kt_phase == 3 && advance_kt(c, false)) return -1;
+  if (c->next_pending && c->kt_phase == 3 && (advance_kt(c, false) || dbg_sync(c, "advance_kt", s))) return -1;
   if (c->next_pending && !c->fill_done && c->kt_phase == 2) {
     cudaError_t q = cudaEventQuery(c->ev_count);
     if (q == cudaErrorNotReady) {
       if (cudaPeekAtLastError() == cudaErrorNotReady) (void)cudaGetLastError();
-    } else if (run_fill(c)) {
+    } else if (run_fill(c) || dbg_sync(c, "run_fill", s)) {
       return -1;
     }
   }
@@ -1449,6 +1464,7 @@ int gf_step_forces(gf_ctx *ctx, int64_t i) {
   trace_mark(c, "dt_forces_begin", s, c->s_dt);
   const int rc = c->f32_state ? dt_forces_f32(c, a, c->s_dt) : dt_forces_f64(c, a, c->s_dt);
   trace_mark(c, "dt_forces_end", s, c->s_dt);
+  if (rc == 0 && dbg_sync(c, "dt_forces", s)) return -1;
   return rc;
 }
 
@@ -1462,10 +1478,11 @@ int gf_step_integrate(gf_ctx *ctx, int64_t i) {
     c->snap_wait = false;
   }
   if (c->f32_state ? dt_integrate_f32(c, a, c->s_dt) : dt_integrate_f64(c, a, c->s_dt)) return -1;
+  if (dbg_sync(c, "dt_integrate", a.step)) return -1;
   trace_mark(c, "dt_integrate_end", a.step, c->s_dt);
   // the detection's candidate filter is queued once the dT step is in flight
-  if (c->next_pending && c->kt_phase == 1 && run_count(c)) return -1;
-  if (c->next_pending && c->kt_phase == 3 && advance_kt(c, false)) return -1;
+  if (c->next_pending && c->kt_phase == 1 && (run_count(c) || dbg_sync(c, "run_count", a.step))) return -1;
+  if (c->next_pending && c->kt_phase == 3 && (advance_kt(c, false) || dbg_sync(c, "advance_kt", a.step))) return -1;
   return 0;
 }
 
