@@ -72,6 +72,21 @@ int ensure(Ctx *c, DBuf &b, size_t bytes, cudaStream_t s, bool keep) {
   return 0;
 }
 
+// GF_SYNC_DEBUG=1 (diagnostics only): synchronise the device after every
+// phase of the step and name the phase a kernel fault surfaced in
+bool sync_debug() {
+  static const bool on = std::getenv("GF_SYNC_DEBUG") != nullptr;
+  return on;
+}
+int dbg_sync(Ctx *c, const char *what, int64_t step) {
+  if (!sync_debug()) return 0;
+  const cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) return 0;
+  set_err(c, std::string("GF_SYNC_DEBUG: ") + cudaGetErrorString(e) + " after " + what + " (step " +
+                 std::to_string(step) + ")");
+  return -1;
+}
+
 int ensure_scratch(Ctx *c, DBuf &b, size_t bytes, cudaStream_t s) {
   if (!big_scratch(c)) return ensure(c, b, bytes, s);
   return ensure_pooled(c, b, bytes, s);
@@ -1339,21 +1354,6 @@ int gf_dt_step(gf_ctx *ctx, const gf_step_params *p, int64_t *touching, int64_t 
 // begin / per-step forces / per-step integrate / end so a decomposed run can
 // exchange ghost forces and ghost state between the halves (gf_run is the
 // plain loop over them).
-// GF_SYNC_DEBUG=1 (diagnostics only): synchronise the device after every
-// phase of the step and name the phase a kernel fault surfaced in
-static bool sync_debug() {
-  static const bool on = std::getenv("GF_SYNC_DEBUG") != nullptr;
-  return on;
-}
-static int dbg_sync(Ctx *c, const char *what, int64_t step) {
-  if (!sync_debug()) return 0;
-  const cudaError_t e = cudaDeviceSynchronize();
-  if (e == cudaSuccess) return 0;
-  set_err(c, std::string("GF_SYNC_DEBUG: ") + cudaGetErrorString(e) + " after " + what + " (step " +
-                 std::to_string(step) + ")");
-  return -1;
-}
-
 int gf_run_begin(gf_ctx *ctx, const gf_run_params *p) {
   CTX_CHECK(ctx);
   if (c->run) { c->err = "a run is already in progress (gf_run_end missing)"; return -1; }

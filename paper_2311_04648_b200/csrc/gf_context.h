@@ -337,4 +337,8 @@ int dt_forces_f64(Ctx *c, const StepArgs &a, cudaStream_t s);
 int dt_integrate_f64(Ctx *c, const StepArgs &a, cudaStream_t s);
 int dt_step_f32(Ctx *c, const StepArgs &a, cudaStream_t s);
 
+// GF_SYNC_DEBUG=1: device sync + fault attribution (gf_context.cu)
+int dbg_sync(Ctx *c, const char *what, int64_t step);
+bool sync_debug();
+
 }  // namespace gf

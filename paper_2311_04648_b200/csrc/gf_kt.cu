@@ -1673,11 +1673,28 @@ static int rb_lists_tail(Ctx *c, cudaStream_t s) {
   const double skin = c->skin_factor * c->kt_margin, skin_b = c->skin_big_factor * c->kt_margin;
   const double reach = c->kt_margin + skin, reach_big = c->kt_margin + skin_b;
   unsigned long long *big_n = k.cand_n.as<unsigned long long>();
+  if (k.n_cand && sync_debug()) {   // GF_SYNC_DEBUG: the segment table against the list it indexes
+    std::vector<unsigned long long> hseg(n + 1);
+    GF_CHECK(c, cudaMemcpy(hseg.data(), k.cand_seg.p, 8 * (n + 1), cudaMemcpyDeviceToHost));
+    unsigned long long mx = 0, bad = 0;
+    for (int64_t i = 0; i < n; ++i) {
+      if (hseg[i + 1] < hseg[i]) ++bad;
+      else mx = std::max(mx, hseg[i + 1] - hseg[i]);
+    }
+    if (bad || hseg[n] != (unsigned long long)k.n_cand || 8 * hseg[n] > k.cand.bytes) {
+      set_err(c, "GF_SYNC_DEBUG: candidate segments: " + std::to_string(bad) + " decreasing, seg[n] " +
+                     std::to_string(hseg[n]) + " vs n_cand " + std::to_string(k.n_cand) + ", list bytes " +
+                     std::to_string(k.cand.bytes) + ", longest " + std::to_string(mx) + ", seg[0] " +
+                     std::to_string(hseg[0]));
+      return -1;
+    }
+  }
   if (k.n_cand) {
     if (ensure(c, k.sa_cnt, 4 * (n + 1), s)) return -1;   // the long-segment list (scratch here)
     GF_CHECK(c, cudaMemsetAsync(big_n, 0, 8, s));
     k_sort_seg_short<<<grid_for(n), kBlock, 0, s>>>(n, k.cand_seg.as<unsigned long long>(), k.cand.as<uint2>(),
                                                    k.sa_cnt.as<uint32_t>(), big_n);
+    if (dbg_sync(c, "k_sort_seg_short", -1)) return -1;
     // the opt-in is per device: tracked per context (a process may hold
     // contexts on several devices, and kT and dT may sit on different ones)
     if (!k.sort_long_smem) {
@@ -1687,6 +1704,7 @@ static int rb_lists_tail(Ctx *c, cudaStream_t s) {
     }
     k_sort_long<<<c->n_sm, 1024, sizeof(uint2) * kLongSeg, s>>>(k.cand_seg.as<unsigned long long>(), k.cand.as<uint2>(),
                                                             k.sa_cnt.as<uint32_t>(), big_n);
+    if (dbg_sync(c, "k_sort_long", -1)) return -1;
   }
   if (n) k_copy_ref<<<grid_for(n), kBlock, 0, s>>>(n, k.c4.as<double4>(), k.ref.as<double>());
   // sphere-analytic candidates for the same skin, while the world is static
@@ -1736,6 +1754,7 @@ static int rb_slot_b(Ctx *c, cudaStream_t s) {
       k_cand_big_slot<true><<<unsigned(std::min<int64_t>(c->n_big, 4096)), 128, 0, s>>>(
           v, c->big_slots.as<uint32_t>(), c->n_big, k.sc.as<double4>(), k.sm.as<uint4>(), c->kt_margin + skin_b,
           c->kt_margin + 2.0 * skin_b - skin, nullptr, seg, cur, k.cand.as<uint2>(), cap, ovf);
+    if (dbg_sync(c, "rb_slot_b fill", -1)) return -1;
     GF_CHECK(c, cudaMemcpyAsync(&reinterpret_cast<Status *>(c->h_status)->cand_overflow, ovf, 8,
                                 cudaMemcpyDeviceToHost, s));
   }
