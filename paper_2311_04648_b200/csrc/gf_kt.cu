@@ -21,6 +21,14 @@
 
 #include "gf_context.h"
 
+// per-slot candidate counts are u32 (memory); their prefix sums can pass
+// 2^32 (a 10.6M-sphere GRC-1 bed at a 1.6 mm margin has ~5e9 candidates), so
+// every scan over them accumulates in u64
+struct U32ToU64 {
+  __host__ __device__ __forceinline__ unsigned long long operator()(const uint32_t x) const { return x; }
+};
+using CountsU64 = cub::TransformInputIterator<unsigned long long, U32ToU64, const uint32_t *>;
+
 namespace gf {
 
 namespace {
@@ -1568,9 +1576,10 @@ static int rb_stage_a(Ctx *c, cudaStream_t s) {
             v, c->big_slots.as<uint32_t>(), c->n_big, k.sc.as<double4>(), k.sm.as<uint4>(), c->kt_margin + skin_b,
             c->kt_margin + 2.0 * skin_b - skin, ucnt, nullptr, nullptr, nullptr);
       unsigned long long *seg = k.cand_seg.as<unsigned long long>();
-      cub::DeviceScan::ExclusiveSum(nullptr, tmp, ucnt, seg, int(n + 1), s);
+      const CountsU64 ucnt64(ucnt, U32ToU64());
+      cub::DeviceScan::ExclusiveSum(nullptr, tmp, ucnt64, seg, int(n + 1), s);
       if (ensure(c, k.cub_tmp, tmp + 16, s, false)) return -1;
-      GF_CHECK(c, cub::DeviceScan::ExclusiveSum(k.cub_tmp.p, tmp, ucnt, seg, int(n + 1), s));
+      GF_CHECK(c, cub::DeviceScan::ExclusiveSum(k.cub_tmp.p, tmp, ucnt64, seg, int(n + 1), s));
       GF_CHECK(c, cudaMemcpyAsync(&hs->cand_total, seg + n, 8, cudaMemcpyDeviceToHost, s));
       return 0;
     }
@@ -1578,9 +1587,10 @@ static int rb_stage_a(Ctx *c, cudaStream_t s) {
     k_cand_ss<false><<<grid_for(n, 128), 128, 0, s>>>(v, k.sm.as<uint4>(), k.sf.as<float4>(), reach, ucnt,
                                                       nullptr, nullptr, nullptr);
     GF_CHECK(c, cudaMemsetAsync(ucnt + n, 0, sizeof(uint32_t), s));
-    cub::DeviceScan::ExclusiveSum(nullptr, tmp, ucnt, uoff, int(n + 1), s);
+    const CountsU64 ucnt64(ucnt, U32ToU64());
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp, ucnt64, uoff, int(n + 1), s);
     if (ensure(c, k.cub_tmp, tmp + 16, s, false)) return -1;
-    GF_CHECK(c, cub::DeviceScan::ExclusiveSum(k.cub_tmp.p, tmp, ucnt, uoff, int(n + 1), s));
+    GF_CHECK(c, cub::DeviceScan::ExclusiveSum(k.cub_tmp.p, tmp, ucnt64, uoff, int(n + 1), s));
     GF_CHECK(c, cudaMemcpyAsync(&hs->cand_total, uoff + n, 8, cudaMemcpyDeviceToHost, s));
   }
   k.rb_big_cap = k.big_cap > 0 ? k.big_cap : (c->n_big ? std::max<int64_t>(4096 * c->n_big, 65536) : 0);
@@ -1640,6 +1650,11 @@ static int rb_stage_c(Ctx *c, cudaStream_t s) {
   k.n_cand = k.rb_small + nbig;
   const int64_t total = k.n_cand;
   if (ensure_scratch(c, k.cand_seg, 8 * (n + 1), s)) return -1;
+  if (total > int64_t(INT32_MAX)) {
+    set_err(c, "candidate rebuild: " + std::to_string(total) +
+                   " candidates exceed the sort-based rebuild's 2^31 items (use the slot-grouped rebuild, GF_RB_SLOT=1)");
+    return -1;
+  }
   if (total) {
     // sort by a (only as many bits as slots need; b rides along), then each
     // sphere's segment by b
