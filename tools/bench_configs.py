@@ -71,7 +71,7 @@ def main():
     ap.add_argument("--hopper-settle", type=float, default=0.6)
     ap.add_argument("--rover-spheres", type=int, default=11_000_000)
     ap.add_argument("--rover-settle-steps", type=int, default=25_000)
-    ap.add_argument("--rover-settle-verr", type=float, default=50.0, help="watchdog speed while the terrain settles")
+    ap.add_argument("--rover-settle-verr", type=float, default=20.0, help="watchdog speed while the terrain settles")
     ap.add_argument("--rover-sinkage", type=float, default=0.01, help="grouser-tip sinkage before timing (m)")
     args = ap.parse_args()
     from paper_2311_04648_b200 import models, scenes
